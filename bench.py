@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""Benchmark: half-stored symmetric SpMM  Y = H·X + Hᵀ·X  on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "C2"): synthetic half-stored H with
+n = 2²² = 4,194,304, 64×64 tiles, all 65,536 diagonal tiles plus Bernoulli
+upper tiles (p = 422,745 / #upper-pairs) → ~488k tiles ≈ 2.0·10⁹ stored
+values (8 GB f32), values h(i XOR j; 0) generated on the device, X ~ N(0,1)
+fp32 with k = 8.  For N > 1 the matrix keeps n and grows to N·488,281 tiles
+(N=8 is BASELINE config 3, 16·10⁹ stored values), row-block sharded with
+NCCL all-gather(X) / reduce-scatter(Y): weak scaling.
+
+One step = one full apply (zero Y + the sm_100a kernel [+ collectives]).
+`value` = algorithmic GFLOP/s of the whole job, 2·k·(2·nnz_off + nnz_diag)
+per apply, device-timed with CUDA events (max over ranks).  `e2e` = the same
+metric through the public API with X in pinned host memory and Y read back
+to the host each step.  The CPU oracle/baseline (oracle/, test
+infrastructure) is only executed by the cpu_baseline leg and --impl reference.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_BASE = 1 << 22
+TILES_PER_GPU = 488_281  # ≈ 2.0e9 stored values per GPU
+K_DEFAULT = 8
+METRIC = "H·X+Hᵀ·X SpMM GFLOP/s & HBM GB/s (fp32,k=8) at 1/2/4/8 B200 vs CPU ref"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--k", type=int, default=K_DEFAULT)
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--n", type=int, default=N_BASE)
+    ap.add_argument("--tiles-per-gpu", type=int, default=TILES_PER_GPU)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget for the cpu_baseline leg")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def workload(args, world):
+    n = args.n
+    nb = (n + 63) // 64
+    n_tiles = world * args.tiles_per_gpu
+    n_off = max(0, n_tiles - nb)
+    n_pairs = nb * (nb - 1) // 2
+    p = n_off / n_pairs if n_pairs else 0.0
+    return n, nb, n_off, p
+
+
+def measured_peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[1]) for s in self.samples if len(s) > 8 and s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if len(s) > 8 and s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            if len(s) > 8:
+                for nm, v in zip(names, s[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# -----------------------------------------------------------------------------
+# CPU baseline (oracle port; test infrastructure, never the product path)
+# -----------------------------------------------------------------------------
+
+def cpu_sample(n, nb, p, k, sample_tiles):
+    """The first `sample_tiles` tiles (block-row order) of the same synthetic
+    workload: identical pattern generator, values and vector count."""
+    import paper_2110_10765_b200 as pkg
+    from oracle import cpu
+
+    rc = pkg.synthetic_pattern(nb, p, seed=0)
+    rows_end = np.searchsorted(rc[:, 0], rc[min(sample_tiles, rc.shape[0]) - 1, 0], side="right")
+    rc = rc[:rows_end]
+    tiles = cpu.fill_h(rc, n, 0)
+    X = np.random.default_rng(0).standard_normal((nb * 64, k)).astype(np.float32)
+    return cpu.F32Problem(rc, tiles, X), rc.shape[0]
+
+
+def run_cpu(n, nb, p, k, budget_s, sample_tiles=24576, min_reps=3):
+    from oracle import cpu
+
+    prob, ntiles = cpu_sample(n, nb, p, k, sample_tiles)
+    threads = cpu.max_threads()
+    prob.run(threads)  # warmup (reference protocol: one warmup, bench.py:170-178)
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < min_reps or (time.perf_counter() - t_start) < budget_s:
+        t0 = time.perf_counter()
+        prob.run(threads)
+        times.append(time.perf_counter() - t0)
+        if len(times) >= 200:
+            break
+    med = float(np.median(times))
+    return {
+        "value": prob.flops() / med / 1e9,
+        "unit": "GFLOP/s",
+        "cores": threads,
+        "kind": "port",
+        "sample": (f"{ntiles} tiles (first block rows of the same C2 pattern, {ntiles * 4096 / 1e6:.0f}M stored "
+                   f"values, k={k} f32), median of {len(times)} reps after 1 warmup, OpenMP private-Y "
+                   f"(array_clause discipline) on {threads} threads; os.cpu_count()={os.cpu_count()}"),
+        "ms_per_apply": med * 1e3,
+    }
+
+
+def impl_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    n, nb, n_off, p = workload(args, world)
+    from oracle import cpu
+
+    prob, ntiles = cpu_sample(n, nb, p, args.k, 24576)
+    threads = cpu.max_threads()
+    for _ in range(args.warmup):
+        prob.run(threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        prob.run(threads)
+    dt = (time.perf_counter() - t0) / args.steps
+    val = prob.flops() / dt / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"C2 sample: first {ntiles} tiles of the n={n} synthetic half-stored H, k={args.k}",
+                   "n": n, "k": args.k, "sample_tiles": int(ntiles)},
+        "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+                         "sample": f"{ntiles} tiles of C2 per step (oracle/sym_spmm_ref.c, OpenMP, "
+                                   f"{threads} threads; reference has no SpMM — SPEC.md:388)"},
+        "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# -----------------------------------------------------------------------------
+# GPU arm
+# -----------------------------------------------------------------------------
+
+def impl_ours(args):
+    import paper_2110_10765_b200 as pkg
+    from paper_2110_10765_b200._lib import CIM_ACCUMULATE, check, lib
+    from paper_2110_10765_b200.sharded import ShardedSymSpmm
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        print(f"warning: WORLD_SIZE={world} but --gpus={args.gpus}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    dtype = torch.float32 if args.dtype == "f32" else torch.float64
+    k = args.k
+    n, nb, n_off, p = workload(args, world)
+
+    t_build = time.perf_counter()
+    S = ShardedSymSpmm.synthetic(n, k=k, p=p, seed=0, dtype=dtype, device=dev)
+    H = S.H
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t_build
+    es = H.vals.element_size()
+    # global accounting (every rank knows the global pattern counts)
+    g_tiles = H.meta["global_tiles"]
+    g_off = H.meta["global_off_tiles"]
+    g_diag = g_tiles - g_off
+    flops_global = 2 * k * (2 * g_off + g_diag) * 4096
+    flops_local = H.flops(k)
+    bytes_local = es * H.nnz_stored + 8 * H.n_tiles + 2 * n * k * es
+
+    stream = torch.cuda.current_stream(dev)
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    X_local = torch.randn((S.rows_per_rank, k), device=dev, dtype=dtype, generator=gen)
+    lo, hi = S.local_rows()
+    X_local[max(0, hi - lo):] = 0
+
+    kern_ms = []
+
+    def step(timed):
+        if world == 1:
+            # the whole apply: zero Y, then the kernel (ACCUMULATE) — events bracket the kernel
+            S.Y_part.zero_()
+            if timed:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            with torch.cuda.device(dev):
+                check(lib().cim_sym_spmm(H.descriptor(), X_full.data_ptr(), S.Y_part.data_ptr(), S.k, S.k, S.k,
+                                         CIM_ACCUMULATE, stream.cuda_stream), "cim_sym_spmm")
+            if timed:
+                e1.record(stream)
+                kern_ms.append((e0, e1))
+        else:
+            if timed:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+            dist.all_gather_into_tensor(S.X_full, X_local)
+            S.Y_part.zero_()
+            if timed:
+                e0.record(stream)
+            with torch.cuda.device(dev):
+                check(lib().cim_sym_spmm(H.descriptor(), S.X_full.data_ptr(), S.Y_part.data_ptr(), S.k, S.k, S.k,
+                                         CIM_ACCUMULATE, stream.cuda_stream), "cim_sym_spmm")
+            if timed:
+                e1.record(stream)
+                kern_ms.append((e0, e1))
+            dist.reduce_scatter_tensor(S.Y_local, S.Y_part, op=dist.ReduceOp.SUM)
+
+    X_full = S.X_full
+    if world == 1:
+        X_full.copy_(X_local[: X_full.shape[0]])
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    with clocks:
+        ev_a = torch.cuda.Event(enable_timing=True)
+        ev_b = torch.cuda.Event(enable_timing=True)
+        ev_a.record(stream)
+        for _ in range(args.steps):
+            step(True)
+        ev_b.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms_total = ev_a.elapsed_time(ev_b)
+    kern = float(np.mean([a.elapsed_time(b) for a, b in kern_ms]))
+    t = torch.tensor([ms_total, kern], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total, kern_max = float(t[0]), float(t[1])
+    ms_step = ms_total / args.steps
+    value = flops_global / (ms_step / 1e3) / 1e9
+
+    # ---- e2e through the public API, host (pinned) buffers, copies timed ----
+    Xh = torch.empty((S.rows_per_rank, k), dtype=dtype, pin_memory=True)
+    Xh.copy_(X_local.cpu())
+    Yh = torch.empty((S.rows_per_rank, k), dtype=dtype, pin_memory=True)
+    e2e_steps = max(1, args.e2e_steps)
+    if world == 1:
+        Xh1 = Xh[:n]
+        Yh1 = Yh[:n]
+
+        def e2e_step():
+            pkg.sym_spmm(H, Xh1, out=Yh1)
+    else:
+        def e2e_step():
+            Yh.copy_(S.apply(Xh.to(dev, non_blocking=True)), non_blocking=False)
+    e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_val = flops_global / float(e2e_s) / 1e9
+    h2d = (n if world == 1 else S.rows_per_rank) * k * es
+    d2h = h2d
+
+    if rank == 0:
+        peaks = measured_peaks()
+        hbm = peaks.get("hbm_gbs", 6650.0)
+        achieved = bytes_local / (kern_max / 1e3) / 1e9
+        traffic = None
+        tf = ROOT / "profiles" / "roofline_traffic.json"
+        if tf.exists():
+            try:
+                traffic = json.loads(tf.read_text()).get(f"k{k}_{args.dtype}")
+            except Exception:
+                traffic = None
+        cpu_b = None
+        if not args.no_cpu_baseline and world == 1:
+            try:
+                cpu_b = run_cpu(n, nb, p, k, args.cpu_seconds)
+            except Exception as ex:  # never let the baseline kill the GPU line
+                cpu_b = {"value": None, "unit": "GFLOP/s", "cores": None, "kind": "port", "sample": f"failed: {ex}"}
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "GFLOP/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32" if dtype == torch.float32 else "f64",
+            "data": "synthetic",
+            "config": {
+                "workload": ("C2" if world == 1 else f"C3-family weak scaling ({world}x C2 tiles, same n)")
+                + f": synthetic half-stored symmetric H, n={n}, block 64, {g_tiles} stored tiles "
+                  f"({g_diag} diagonal + {g_off} upper), {g_tiles * 4096 / 1e9:.3f}e9 stored values, "
+                  f"k={k}, values h(i XOR j; 0) on device, X ~ N(0,1)",
+                "n": n, "k": k, "stored_tiles": g_tiles, "stored_nnz": g_tiles * 4096,
+                "parallelism": f"row-block shard x{world}" if world > 1 else "single GPU",
+                "l2": "inputs (8.3 GB per GPU) far larger than L2 (126 MB): no flush",
+                "gflop_per_apply": flops_global / 1e9,
+                "hbm_gbs_kernel": achieved,
+                "build_s": t_build,
+            },
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic,
+                         "kernel": "sym_spmm_kernel", "kernel_ms": kern_max,
+                         "algorithmic_bytes_per_launch": bytes_local,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6650",
+                         "frac_of_8TBs_spec": achieved / 8000.0},
+            "cpu_baseline": cpu_b,
+            "e2e": {"value": e2e_val, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": args.steps * (1 if k <= 8 else max(1, k // 16)),
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return impl_reference(args)
+    return impl_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

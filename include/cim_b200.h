@@ -1,0 +1,177 @@
+/*
+ * cim_b200.h — C-ABI of the B200-native half-stored symmetric SpMM
+ *
+ *     Y = U·X + U_offᵀ·X  (= A·X for the full symmetric A)
+ *
+ * where U is the set of stored 64×64 tiles (R ≤ C, diagonal tiles held in
+ * full) and U_off the stored tiles with R < C.  This is the hot path of the
+ * eigensolver in arXiv 2110.10765 (Fig. 1 line 15) that the
+ * reference package `cimotifs` approaches only through its pair-walk operator
+ * `contract_observables` (pkg/src/cimotifs/pipeline.py:534-570).
+ *
+ * The reference has no C ABI; its operator boundary is Python over numpy
+ * arrays.  Each entry point below states which reference
+ * interface it replaces.  No torch types appear here: every buffer is a plain
+ * device (or host, where stated) pointer plus sizes, owned by the caller.
+ *
+ * Storage ("HalfTiles", fragment layout v1)
+ * -----------------------------------------
+ *   tile_rc  int32 [n_tiles][2]  (R, C) with R ≤ C, sorted by R then C,
+ *                                unique.  Replaces SparseSkeleton.tiles +
+ *                                colind (pipeline.py:96-116): the reference
+ *                                stores both triangles at entry granularity.
+ *   units    int32 [n_units][4]  (R, t0, t1, 0): work units, a contiguous
+ *                                tile range inside block row R.  Built by
+ *                                cim_plan_units.
+ *   vals     f32|f64 [n_tiles][4096] in fragment order: for tile t,
+ *                                micro-row i∈[0,8), micro-block mb∈[0,128),
+ *                                column slot j∈[0,4):
+ *                                  vals[t][i][mb][j] = T[rg + 8i][cg + 16j]
+ *                                with rg = (mb & 31) >> 2,
+ *                                     cg = 4·(mb >> 5) + (mb & 3).
+ *                                (f64: vals[t][i][h][mb][jj] with j = 2h+jj.)
+ *                                Rows/cols ≥ n inside the last block are 0.
+ *
+ * Vectors: X and Y are row-major (n_pad, k) with n_pad = 64·ceil(n/64).
+ * X rows ≥ n must be finite (they meet zero matrix entries).  Y rows ≥ n
+ * receive zeros.  X must be dense (ldx == k); Y may be strided (ldy ≥ k,
+ * ldy % 4 == 0 for f32, ldy % 2 == 0 for f64, 16-byte aligned base).
+ *
+ * Threading: every device entry point is asynchronous and stream-ordered;
+ * calls are re-entrant for distinct Y.  The only global state is a per-device
+ * cache (SM count, occupancy, a ring of scheduler counters).
+ */
+#ifndef CIM_B200_H
+#define CIM_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CIM_API __attribute__((visibility("default")))
+#else
+#define CIM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* return codes */
+#define CIM_OK            0
+#define CIM_EINVAL        1   /* bad argument (shape, alignment, order)     */
+#define CIM_ECUDA         2   /* a CUDA runtime call failed                 */
+#define CIM_EUNSUPPORTED  3   /* k / dtype combination not compiled         */
+
+/* dtypes */
+#define CIM_F32 0
+#define CIM_F64 1
+
+/* cim_sym_spmm flags */
+#define CIM_ACCUMULATE    1u  /* Y += A·X instead of Y = A·X                */
+
+/* value kinds for cim_fill_synthetic_values */
+#define CIM_VALUES_H_XOR      0  /* h(i XOR j; seed)      pipeline.py:216-222 */
+#define CIM_VALUES_OP_HASH    1  /* O_ij(k=op_k; seed)    pipeline.py:224-232 */
+#define CIM_VALUES_IDENTITY   2  /* δ_ij                  pipeline.py:226-227 */
+
+#define CIM_BLOCK 64
+
+typedef struct cim_half_tiles {
+  int64_t        n;        /* matrix order                                   */
+  int32_t        block;    /* must be 64                                     */
+  int32_t        dtype;    /* CIM_F32 | CIM_F64                              */
+  int64_t        n_tiles;
+  int64_t        n_units;
+  const int32_t *tile_rc;  /* device, [n_tiles][2]                           */
+  const int32_t *units;    /* device, [n_units][4]                           */
+  const void    *vals;     /* device, [n_tiles][4096] fragment order         */
+} cim_half_tiles;
+
+/* Library version / build string (host). */
+CIM_API const char *cim_version(void);
+
+/* Last error message of the calling thread (host). */
+CIM_API const char *cim_last_error(void);
+
+/*
+ * Y = A·X (or Y += A·X with CIM_ACCUMULATE) on `stream` (a cudaStream_t, may
+ * be NULL for the legacy stream).  X, Y are device pointers to (n_pad, k)
+ * row-major arrays of the tile dtype.
+ *
+ * Replaces: contract_observables(...) (pipeline.py:534-570) as the operator
+ * that walks every stored pair once per call; its validation contract
+ * (ValueError before compute, pipeline.py:550-555) maps to CIM_EINVAL.
+ * Supported k: f32 {1,2,4} ∪ 8ℕ (≤ 64); f64 {1,2} ∪ 4ℕ (≤ 64).
+ */
+CIM_API int cim_sym_spmm(const cim_half_tiles *H, const void *X, void *Y, int32_t k,
+                 int64_t ldx, int64_t ldy, uint32_t flags, void *stream);
+
+/* 1 if (dtype, k) has a compiled kernel, else 0. */
+CIM_API int cim_sym_spmm_supported(int32_t dtype, int32_t k);
+
+/*
+ * Host: build work units from a sorted tile list (R, C pairs, host memory).
+ * Every block row's tiles are split into runs of at most `max_unit` tiles.
+ * units_out must hold n_tiles*4 int32 (upper bound); *n_units_out receives
+ * the count.  Also validates order (R ≤ C, sorted, unique, in range nb).
+ *
+ * Replaces: the per-(tile,row) segment layout CountsAndOffsets built by
+ * counts_to_offsets (pipeline.py:319-330, fill.py:79-91).
+ */
+CIM_API int cim_plan_units(const int32_t *tile_rc_host, int64_t n_tiles, int64_t nb,
+                   int32_t max_unit, int32_t *units_out, int64_t *n_units_out);
+
+/*
+ * Host: split units into `parts` contiguous ranges with balanced tile counts
+ * (row-block sharding over GPUs).  bounds_out[parts+1].
+ */
+CIM_API int cim_partition_units(const int32_t *units_host, int64_t n_units,
+                        int32_t parts, int64_t *bounds_out);
+
+/*
+ * Device: fill `vals` (fragment order, dtype) with synthetic symmetric
+ * values for the tiles in tile_rc: kind CIM_VALUES_H_XOR gives the reference
+ * matrix values h(i XOR j; seed) (pipeline.py:216-222, _h_values_np :247-249),
+ * bit-exact after rounding to f32 (f64 tiles hold the same f32 values).
+ * Entries with i ≥ n or j ≥ n are 0.
+ */
+CIM_API int cim_fill_synthetic_values(const int32_t *tile_rc, int64_t n_tiles, int64_t n,
+                              int32_t dtype, int32_t kind, uint64_t seed,
+                              int32_t op_k, void *vals, void *stream);
+
+/*
+ * Device: operator values on a stored pattern — vals[e] = value(i,j) where
+ * mask[e] != 0, else 0 (both in fragment order).  Gives the reference's
+ * observable operators O_ij(k) (pipeline.py:224-232) restricted to the
+ * interacting pairs, for the GPU contract_observables.
+ */
+CIM_API int cim_fill_masked_values(const int32_t *tile_rc, int64_t n_tiles, int64_t n,
+                                   int32_t dtype, int32_t kind, uint64_t seed,
+                                   int32_t op_k, const void *mask, void *vals,
+                                   void *stream);
+
+/*
+ * Device: repack row-major dense tiles src[n_tiles][64][64] into fragment
+ * order dst (same dtype).  The repacking layer's device half
+ * (SURVEY.md §7 step 4).
+ */
+CIM_API int cim_pack_tiles(const void *src_rowmajor, int64_t n_tiles, int32_t dtype,
+                   void *dst_fragment, void *stream);
+
+/* Device: inverse of cim_pack_tiles (debug / export). */
+CIM_API int cim_unpack_tiles(const void *src_fragment, int64_t n_tiles, int32_t dtype,
+                     void *dst_rowmajor, void *stream);
+
+/*
+ * Device: the reference's value hashes on explicit index arrays, for parity
+ * checks of the device hash against _h_values_np / _op_values_np
+ * (pipeline.py:247-263).  out is f32[count].
+ */
+CIM_API int cim_hash_values(const int64_t *i, const int64_t *j, int64_t count,
+                    int32_t kind, uint64_t seed, int32_t op_k, float *out,
+                    void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CIM_B200_H */

@@ -1,0 +1,104 @@
+"""ctypes binding of the C-ABI library ``libcim_b200.so`` (include/cim_b200.h).
+
+The library is built in-tree (``__graft_entry__.build()`` / ``make -C
+paper_2110_10765_b200/csrc``).  There is no fallback: if the shared object is
+missing, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libcim_b200.so"
+
+CIM_OK, CIM_EINVAL, CIM_ECUDA, CIM_EUNSUPPORTED = 0, 1, 2, 3
+CIM_F32, CIM_F64 = 0, 1
+CIM_ACCUMULATE = 1
+CIM_VALUES_H_XOR, CIM_VALUES_OP_HASH, CIM_VALUES_IDENTITY = 0, 1, 2
+BLOCK = 64
+
+EXPORTS = (
+    "cim_version",
+    "cim_last_error",
+    "cim_sym_spmm",
+    "cim_sym_spmm_supported",
+    "cim_plan_units",
+    "cim_partition_units",
+    "cim_fill_synthetic_values",
+    "cim_fill_masked_values",
+    "cim_pack_tiles",
+    "cim_unpack_tiles",
+    "cim_hash_values",
+)
+
+
+class CimHalfTiles(ctypes.Structure):
+    """Mirror of ``struct cim_half_tiles``."""
+
+    _fields_ = [
+        ("n", ctypes.c_int64),
+        ("block", ctypes.c_int32),
+        ("dtype", ctypes.c_int32),
+        ("n_tiles", ctypes.c_int64),
+        ("n_units", ctypes.c_int64),
+        ("tile_rc", ctypes.c_void_p),
+        ("units", ctypes.c_void_p),
+        ("vals", ctypes.c_void_p),
+    ]
+
+
+class CimError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load (once) and return the C-ABI library; raise if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = Path(os.environ.get("CIM_B200_LIB", LIB_PATH))
+    if not path.exists():
+        raise ImportError(
+            f"libcim_b200.so not found at {path}; build it with "
+            "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)"
+        )
+    L = ctypes.CDLL(str(path))
+    c = ctypes
+    L.cim_version.restype = c.c_char_p
+    L.cim_last_error.restype = c.c_char_p
+    L.cim_sym_spmm.argtypes = [c.POINTER(CimHalfTiles), c.c_void_p, c.c_void_p, c.c_int32, c.c_int64,
+                               c.c_int64, c.c_uint32, c.c_void_p]
+    L.cim_sym_spmm_supported.argtypes = [c.c_int32, c.c_int32]
+    L.cim_plan_units.argtypes = [c.c_void_p, c.c_int64, c.c_int64, c.c_int32, c.c_void_p, c.POINTER(c.c_int64)]
+    L.cim_partition_units.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_void_p]
+    L.cim_fill_synthetic_values.argtypes = [c.c_void_p, c.c_int64, c.c_int64, c.c_int32, c.c_int32, c.c_uint64,
+                                            c.c_int32, c.c_void_p, c.c_void_p]
+    L.cim_fill_masked_values.argtypes = [c.c_void_p, c.c_int64, c.c_int64, c.c_int32, c.c_int32, c.c_uint64,
+                                         c.c_int32, c.c_void_p, c.c_void_p, c.c_void_p]
+    L.cim_pack_tiles.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_void_p, c.c_void_p]
+    L.cim_unpack_tiles.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_void_p, c.c_void_p]
+    L.cim_hash_values.argtypes = [c.c_void_p, c.c_void_p, c.c_int64, c.c_int32, c.c_uint64, c.c_int32,
+                                  c.c_void_p, c.c_void_p]
+    for name in EXPORTS:
+        if name not in ("cim_version", "cim_last_error"):
+            getattr(L, name).restype = c.c_int
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str) -> None:
+    """Map a C-ABI return code to the reference's exception conventions:
+    CIM_EINVAL → ValueError (pipeline.py:550-555 style), others → RuntimeError."""
+    if rc == CIM_OK:
+        return
+    msg = lib().cim_last_error().decode(errors="replace")
+    if rc == CIM_EINVAL:
+        raise ValueError(f"{what}: {msg}")
+    if rc == CIM_EUNSUPPORTED:
+        raise NotImplementedError(f"{what}: {msg}")
+    raise CimError(f"{what}: {msg} (code {rc})")

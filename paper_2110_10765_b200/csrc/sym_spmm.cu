@@ -1,0 +1,626 @@
+// One-pass half-stored symmetric SpMM for sm_100a:  Y = U·X + U_offᵀ·X.
+//
+// Each stored 64×64 tile is streamed from HBM exactly once per pass by a
+// single-thread producer (cp.async.bulk into a multi-stage shared-memory
+// ring, mbarrier-synchronised) and used by 128 consumer threads per vector
+// group for BOTH products:
+//
+//   direct      acc_r[row][v] += T[row][col] · X_C[col][v]   (Y_R, block row)
+//   transposed  acc_c[col][v] += T[row][col] · X_R[row][v]   (Y_C, block col)
+//
+// Thread ↔ data map (fragment layout v1, include/cim_b200.h): consumer mb owns
+// rows rg+8i (i<8) and columns cg+16j (j<4) of every tile, so one LDS.128 per
+// micro-row feeds 4·2·KV FMAs with all operands in registers.
+//
+//  * acc_r lives in registers across a whole work unit (a run of tiles of one
+//    block row) and is reduced once per unit: a 2-step butterfly over the 4
+//    lanes that share rows, then a 4-warp sum through shared memory, then one
+//    vector red.global.add per output chunk.
+//  * acc_c is reduced per tile inside the warp (the 8 lanes sharing columns)
+//    through a bank-swizzled per-warp scratch, then red.global.add.v4 into Y_C.
+//
+// Diagonal tiles (R == C) are stored in full and only feed the direct product.
+// The reference reaches this arithmetic only as a pair walk
+// (_contract_array_clause / _contract_atomic, pipeline.py:461-488) over the
+// full COO from _collect_pairs (pipeline.py:428-458).
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "cim_b200.h"
+#include "common.cuh"
+#include "host_util.h"
+
+namespace cim {
+
+enum : int { HDR_FIRST = 1, HDR_LAST = 2, HDR_DIAG = 4, HDR_TERM = 8 };
+
+struct __align__(16) StageHdr {
+  int R, C, flags, pad;
+};
+
+struct SpmmParams {
+  const int4 *units;    // (R, t0, t1, 0)
+  const int2 *tile_rc;  // (R, C)
+  const unsigned char *vals;
+  const unsigned char *X;
+  unsigned char *Y;
+  unsigned int *counter;
+  long long n_units;
+  long long ldy;  // elements
+  int k;          // row length of X (all vectors)
+  int v_base;     // first vector handled by this pass
+  int stages;
+  unsigned int stage_bytes;
+  unsigned int tile_bytes;
+  unsigned int xblk_bytes;  // 64·k·sizeof(T)
+};
+
+template <typename T>
+struct Chunk;  // 16-byte vector of T
+template <>
+struct Chunk<float> {
+  using V = float4;
+  static constexpr int N = 4;
+};
+template <>
+struct Chunk<double> {
+  using V = double2;
+  static constexpr int N = 2;
+};
+
+// Load KV consecutive elements (16-byte aligned when KV·sizeof(T) ≥ 16).
+template <typename T, int KV>
+__device__ __forceinline__ void load_vec(T (&d)[KV], const T *s) {
+  if constexpr (KV * sizeof(T) >= 16) {
+    using V = typename Chunk<T>::V;
+    constexpr int C = Chunk<T>::N;
+#pragma unroll
+    for (int q = 0; q < KV / C; ++q) {
+      const V v = reinterpret_cast<const V *>(s)[q];
+      if constexpr (C == 4) {
+        d[4 * q + 0] = v.x;
+        d[4 * q + 1] = v.y;
+        d[4 * q + 2] = v.z;
+        d[4 * q + 3] = v.w;
+      } else {
+        d[2 * q + 0] = v.x;
+        d[2 * q + 1] = v.y;
+      }
+    }
+  } else if constexpr (KV == 2 && sizeof(T) == 4) {
+    const float2 v = *reinterpret_cast<const float2 *>(s);
+    d[0] = v.x;
+    d[1] = v.y;
+  } else {
+#pragma unroll
+    for (int q = 0; q < KV; ++q) d[q] = s[q];
+  }
+}
+
+// One micro-row of the tile for this thread: 4 values, columns cg+16j.
+template <typename T>
+__device__ __forceinline__ void load_trow(T (&t)[4], const T *Ts, int i, int mb) {
+  if constexpr (sizeof(T) == 4) {
+    const float4 v = reinterpret_cast<const float4 *>(Ts)[i * 128 + mb];
+    t[0] = v.x;
+    t[1] = v.y;
+    t[2] = v.z;
+    t[3] = v.w;
+  } else {
+    const double2 a = reinterpret_cast<const double2 *>(Ts)[(2 * i + 0) * 128 + mb];
+    const double2 b = reinterpret_cast<const double2 *>(Ts)[(2 * i + 1) * 128 + mb];
+    t[0] = a.x;
+    t[1] = a.y;
+    t[2] = b.x;
+    t[3] = b.y;
+  }
+}
+
+template <typename T, int KV, bool DIAG>
+__device__ __forceinline__ void tile_fma(const T *__restrict__ Ts, const T *__restrict__ XC,
+                                         const T *__restrict__ XR, int mb, int rg, int cg, int k, int v0,
+                                         T (&acc_r)[8][KV], T (&acc_c)[4][KV]) {
+  T xc[4][KV];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) load_vec<T, KV>(xc[j], XC + (cg + 16 * j) * k + v0);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    T t[4];
+    load_trow<T>(t, Ts, i, mb);
+    T xr[KV];
+    if constexpr (!DIAG) load_vec<T, KV>(xr, XR + (rg + 8 * i) * k + v0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int v = 0; v < KV; ++v) {
+        acc_r[i][v] = fma(t[j], xc[j][v], acc_r[i][v]);
+        if constexpr (!DIAG) acc_c[j][v] = fma(t[j], xr[v], acc_c[j][v]);
+      }
+    }
+  }
+}
+
+// Store a chunk-sized run of outputs with one vector reduction when possible.
+template <typename T, int KV>
+__device__ __forceinline__ void red_chunk(T *ybase, long long ldy, int e0, const T (&s)[Chunk<T>::N]) {
+  constexpr int C = Chunk<T>::N;
+  if constexpr (KV >= C) {
+    // chunk = one row (or column) index, C consecutive vectors
+    const int r = e0 / KV, v = e0 % KV;
+    T *p = ybase + (long long)r * ldy + v;
+    if constexpr (sizeof(T) == 4) {
+      red_add_v4(reinterpret_cast<float *>(p), s[0], s[1], s[2], s[3]);
+    } else {
+      red_add(p, s[0]);
+      red_add(p + 1, s[1]);
+    }
+  } else {
+#pragma unroll
+    for (int x = 0; x < C; ++x) {
+      const int e = e0 + x, r = e / KV, v = e % KV;
+      red_add(ybase + (long long)r * ldy + v, s[x]);
+    }
+  }
+}
+
+// Per-tile reduction of acc_c over the 8 lanes (rg) that share columns.
+// scr: this warp's scratch, 32 lanes × 4·KV elements.
+template <typename T, int KV>
+__device__ __forceinline__ void reduce_cols(T (&acc)[4][KV], T *scr, int lane, int w, T *yblk, long long ldy) {
+  using V = typename Chunk<T>::V;
+  constexpr int C = Chunk<T>::N;
+  constexpr int NCH = (4 * KV) / C;  // chunks per lane
+  static_assert((4 * KV) % C == 0, "KV too small for chunking");
+  const T *flat = &acc[0][0];
+  V *sv = reinterpret_cast<V *>(scr);
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < NCH; ++q) {
+    V v;
+    if constexpr (C == 4) {
+      v = make_float4(flat[4 * q], flat[4 * q + 1], flat[4 * q + 2], flat[4 * q + 3]);
+    } else {
+      v = make_double2(flat[2 * q], flat[2 * q + 1]);
+    }
+    sv[q * 32 + (lane ^ ((q & 1) << 2))] = v;
+  }
+  __syncwarp();
+  if (lane < 4 * NCH) {
+    const int cg_lo = lane & 3, q = lane >> 2;
+    T s[C];
+#pragma unroll
+    for (int x = 0; x < C; ++x) s[x] = T(0);
+#pragma unroll
+    for (int rg = 0; rg < 8; ++rg) {
+      const V v = sv[q * 32 + ((rg * 4 + cg_lo) ^ ((q & 1) << 2))];
+      if constexpr (C == 4) {
+        s[0] += v.x;
+        s[1] += v.y;
+        s[2] += v.z;
+        s[3] += v.w;
+      } else {
+        s[0] += v.x;
+        s[1] += v.y;
+      }
+    }
+    // flat element e = j·KV + v ; column = cg + 16·j
+    const int cg = w * 4 + cg_lo;
+    const int e0 = q * C;
+    if constexpr (KV >= C) {
+      const int j = e0 / KV, v = e0 % KV;
+      T *p = yblk + (long long)(cg + 16 * j) * ldy + v;
+      if constexpr (sizeof(T) == 4) {
+        red_add_v4(reinterpret_cast<float *>(p), s[0], s[1], s[2], s[3]);
+      } else {
+        red_add(p, s[0]);
+        red_add(p + 1, s[1]);
+      }
+    } else {
+#pragma unroll
+      for (int x = 0; x < C; ++x) {
+        const int e = e0 + x, j = e / KV, v = e % KV;
+        red_add(yblk + (long long)(cg + 16 * j) * ldy + v, s[x]);
+      }
+    }
+  }
+}
+
+// Per-unit reduction of acc_r over the 16 threads (4 lanes × 4 warps) that
+// share rows.  scr: group scratch, 4 warps × 64·KV elements.
+template <typename T, int KV>
+__device__ __forceinline__ void reduce_rows(T (&acc)[8][KV], T *scr, int lane, int w, int rg, int gt, int bar_id,
+                                            T *yblk, long long ldy) {
+  using V = typename Chunk<T>::V;
+  constexpr int C = Chunk<T>::N;
+  // butterfly over lane bit 0: keep rows i + 4·b0
+  const bool b0 = lane & 1;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int v = 0; v < KV; ++v) {
+      const T send = b0 ? acc[i][v] : acc[i + 4][v];
+      const T keep = b0 ? acc[i + 4][v] : acc[i][v];
+      acc[i][v] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+    }
+  }
+  // butterfly over lane bit 1: keep rows i + 2·b1 (+4·b0)
+  const bool b1 = lane & 2;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+#pragma unroll
+    for (int v = 0; v < KV; ++v) {
+      const T send = b1 ? acc[i][v] : acc[i + 2][v];
+      const T keep = b1 ? acc[i + 2][v] : acc[i][v];
+      acc[i][v] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+  }
+  const int i0 = (b0 ? 4 : 0) + (b1 ? 2 : 0);
+  named_bar_sync(bar_id, kGroupThreads);  // previous unit's readers are done
+  T *mine = scr + w * 64 * KV;
+  // every lane now holds distinct rows: rg + 8·(i0 + ri)
+#pragma unroll
+  for (int ri = 0; ri < 2; ++ri) {
+    const int row = rg + 8 * (i0 + ri);
+#pragma unroll
+    for (int v = 0; v < KV; ++v) mine[row * KV + v] = acc[ri][v];
+  }
+  named_bar_sync(bar_id, kGroupThreads);
+  constexpr int NOUT = 64 * KV / C;  // output chunks
+  for (int c = gt; c < NOUT; c += kGroupThreads) {
+    T s[C];
+    const V a = reinterpret_cast<const V *>(scr)[c];
+    const V b = reinterpret_cast<const V *>(scr + 64 * KV)[c];
+    const V d = reinterpret_cast<const V *>(scr + 128 * KV)[c];
+    const V e = reinterpret_cast<const V *>(scr + 192 * KV)[c];
+    if constexpr (C == 4) {
+      s[0] = (a.x + b.x) + (d.x + e.x);
+      s[1] = (a.y + b.y) + (d.y + e.y);
+      s[2] = (a.z + b.z) + (d.z + e.z);
+      s[3] = (a.w + b.w) + (d.w + e.w);
+    } else {
+      s[0] = (a.x + b.x) + (d.x + e.x);
+      s[1] = (a.y + b.y) + (d.y + e.y);
+    }
+    red_chunk<T, KV>(yblk, ldy, c * C, s);
+  }
+}
+
+template <typename T, int KV, int NG>
+__global__ void __launch_bounds__(NG * kGroupThreads + 32, (NG == 1 ? 2 : 1))
+    sym_spmm_kernel(const SpmmParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int tid = threadIdx.x;
+  constexpr int NCONS = NG * kGroupThreads;
+  const int S = p.stages;
+  unsigned char *stage_base = smem;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)S * p.stage_bytes);
+  uint64_t *empty = full + S;
+  T *scr_c = reinterpret_cast<T *>(smem + (size_t)S * p.stage_bytes + 128);  // barriers fit in 128 B (S ≤ 8)
+  T *scr_r = scr_c + NG * 4 * 32 * 4 * KV;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NG * 4);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const unsigned int tile_bytes = p.tile_bytes, xblk = p.xblk_bytes;
+
+  if (tid >= NCONS) {
+    // ======================= producer warp =======================
+    const int lane = tid & 31;
+    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_keep = policy_evict_last();
+    int stage = 0;
+    uint32_t phase = 0;
+    unsigned int u = 0;
+    if (lane == 0) u = atomicAdd(p.counter, 1u);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    while ((long long)u < p.n_units) {
+      const int4 unit = p.units[u];
+      unsigned int u_next = 0;
+      if (lane == 0) u_next = atomicAdd(p.counter, 1u);  // prefetch the next ticket
+      const int R = unit.x, t0 = unit.y, t1 = unit.z;
+      const unsigned char *xr_src = p.X + (size_t)R * xblk;
+      for (int tb = t0; tb < t1; tb += 32) {
+        const int t = tb + lane;
+        const int myC = (t < t1) ? p.tile_rc[t].y : 0;
+        const int cnt = min(32, t1 - tb);
+        for (int q = 0; q < cnt; ++q) {
+          const int C = __shfl_sync(0xffffffffu, myC, q);
+          if (lane == 0) {
+            mbar_wait(&empty[stage], phase ^ 1u);
+            unsigned char *st = stage_base + (size_t)stage * p.stage_bytes;
+            const int tt = tb + q;
+            const bool diag = (C == R);
+            const int flags = (tt == t0 ? HDR_FIRST : 0) | (tt == t1 - 1 ? HDR_LAST : 0) | (diag ? HDR_DIAG : 0);
+            StageHdr *h = reinterpret_cast<StageHdr *>(st + tile_bytes + 2 * xblk);
+            *h = StageHdr{R, C, flags, 0};
+            mbar_arrive_expect_tx(&full[stage], tile_bytes + (diag ? xblk : 2 * xblk));
+            bulk_g2s(st, p.vals + (size_t)tt * tile_bytes, tile_bytes, &full[stage], pol_stream);
+            bulk_g2s(st + tile_bytes, p.X + (size_t)C * xblk, xblk, &full[stage], pol_keep);
+            if (!diag) bulk_g2s(st + tile_bytes + xblk, xr_src, xblk, &full[stage], pol_keep);
+          }
+          __syncwarp();
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+      u = __shfl_sync(0xffffffffu, u_next, 0);
+    }
+    if (lane == 0) {
+      mbar_wait(&empty[stage], phase ^ 1u);
+      StageHdr *h = reinterpret_cast<StageHdr *>(stage_base + (size_t)stage * p.stage_bytes + tile_bytes + 2 * xblk);
+      *h = StageHdr{0, 0, HDR_TERM, 0};
+      mbar_arrive(&full[stage]);
+    }
+    return;
+  }
+
+  // ======================= consumer groups =======================
+  const int g = tid / kGroupThreads;
+  const int gt = tid % kGroupThreads;  // micro-block id
+  const int w = gt >> 5, lane = tid & 31;
+  const int rg = frag_rg(gt), cg = frag_cg(gt);
+  const int k = p.k;
+  const int v0 = p.v_base + g * KV;
+  T *my_scr_c = scr_c + (g * 4 + w) * 32 * 4 * KV;
+  T *my_scr_r = scr_r + g * 4 * 64 * KV;
+  T *Y = reinterpret_cast<T *>(p.Y);
+
+  T acc_r[8][KV];
+  T acc_c[4][KV];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int v = 0; v < KV; ++v) acc_r[i][v] = T(0);
+
+  int stage = 0;
+  uint32_t phase = 0;
+  while (true) {
+    mbar_wait(&full[stage], phase);
+    const unsigned char *st = stage_base + (size_t)stage * p.stage_bytes;
+    const StageHdr h = *reinterpret_cast<const StageHdr *>(st + tile_bytes + 2 * xblk);
+    if (h.flags & HDR_TERM) break;
+    if (h.flags & HDR_FIRST) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int v = 0; v < KV; ++v) acc_r[i][v] = T(0);
+    }
+    const T *Ts = reinterpret_cast<const T *>(st);
+    const T *XC = reinterpret_cast<const T *>(st + tile_bytes);
+    const T *XR = reinterpret_cast<const T *>(st + tile_bytes + xblk);
+    const bool diag = h.flags & HDR_DIAG;
+    if (diag) {
+      tile_fma<T, KV, true>(Ts, XC, XR, gt, rg, cg, k, v0, acc_r, acc_c);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int v = 0; v < KV; ++v) acc_c[j][v] = T(0);
+      tile_fma<T, KV, false>(Ts, XC, XR, gt, rg, cg, k, v0, acc_r, acc_c);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == S) {
+      stage = 0;
+      phase ^= 1u;
+    }
+    if (!diag) reduce_cols<T, KV>(acc_c, my_scr_c, lane, w, Y + (long long)h.C * kBlock * p.ldy + v0, p.ldy);
+    if (h.flags & HDR_LAST)
+      reduce_rows<T, KV>(acc_r, my_scr_r, lane, w, rg, gt, 1 + g, Y + (long long)h.R * kBlock * p.ldy + v0, p.ldy);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+namespace {
+
+struct DeviceState {
+  int sms = 0;
+  unsigned int *counters = nullptr;  // ring of scheduler counters
+  int ring_pos = 0;
+};
+constexpr int kCounterRing = 4096;
+std::mutex g_mu;
+std::vector<DeviceState> g_dev;
+
+int device_state(DeviceState **out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return set_error(CIM_ECUDA, "cudaGetDevice failed");
+  std::lock_guard<std::mutex> lk(g_mu);
+  if ((int)g_dev.size() <= dev) g_dev.resize(dev + 1);
+  DeviceState &d = g_dev[dev];
+  if (d.sms == 0) {
+    int sms = 0;
+    cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("cudaDeviceGetAttribute: ") + cudaGetErrorString(e));
+    e = cudaMalloc(&d.counters, kCounterRing * sizeof(unsigned int));
+    if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("cudaMalloc counters: ") + cudaGetErrorString(e));
+    d.sms = sms;
+  }
+  *out = &d;
+  return CIM_OK;
+}
+
+// take `n` consecutive counter slots (host-side ring; slots are memset on the
+// caller's stream before use, so concurrent streams never share a slot)
+unsigned int *take_counters(DeviceState *d, int n) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (d->ring_pos + n > kCounterRing) d->ring_pos = 0;
+  unsigned int *p = d->counters + d->ring_pos;
+  d->ring_pos += n;
+  return p;
+}
+
+struct LaunchCfg {
+  int KV, NG, passes;
+};
+
+bool pick_cfg(int dtype, int k, LaunchCfg &c) {
+  if (k < 1 || k > 64) return false;
+  if (dtype == CIM_F32) {
+    if (k == 1 || k == 2 || k == 4) {
+      c = {k, 1, 1};
+      return true;
+    }
+    if (k % 8 == 0) {
+      const int m = k / 8;
+      c = {8, (m % 2 == 0) ? 2 : 1, 0};
+      c.passes = m / c.NG;
+      return true;
+    }
+    return false;
+  }
+  if (dtype == CIM_F64) {
+    if (k == 1 || k == 2) {
+      c = {k, 1, 1};
+      return true;
+    }
+    if (k % 4 == 0) {
+      const int m = k / 4;
+      c = {4, (m % 2 == 0) ? 2 : 1, 0};
+      c.passes = m / c.NG;
+      return true;
+    }
+    return false;
+  }
+  return false;
+}
+
+template <typename T, int KV, int NG>
+int launch_kernel(const cim_half_tiles *H, const void *X, void *Y, int k, long long ldy, int passes,
+                  cudaStream_t stream, DeviceState *ds) {
+  static std::mutex mu;
+  static int attr_set_dev_mask = 0;
+  const unsigned int tile_bytes = kTileElems * sizeof(T);
+  const unsigned int xblk = (unsigned int)(kBlock * k * sizeof(T));
+  const unsigned int stage_bytes = (tile_bytes + 2 * xblk + sizeof(StageHdr) + 127u) & ~127u;
+  const size_t scratch = (size_t)NG * 4 * 32 * 4 * KV * sizeof(T) + (size_t)NG * 4 * 64 * KV * sizeof(T);
+  const int ctas_per_sm = (NG == 1) ? 2 : 1;
+  const size_t budget = (size_t)(227 * 1024) / ctas_per_sm - (ctas_per_sm > 1 ? 1024 : 0);
+  if (budget < scratch + 128 + 2 * (size_t)stage_bytes) return set_error(CIM_EUNSUPPORTED, "k too large for smem");
+  int S = (int)((budget - scratch - 128) / stage_bytes);
+  S = std::min(S, 8);
+  const size_t smem = (size_t)S * stage_bytes + 128 + scratch;
+
+  auto kern = sym_spmm_kernel<T, KV, NG>;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    // attribute must cover the largest smem we ever request; set to the max once per device
+    if (!(attr_set_dev_mask & (1 << dev))) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      if (e != cudaSuccess)
+        return set_error(CIM_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+      attr_set_dev_mask |= (1 << dev);
+    }
+  }
+  int occ = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NG * kGroupThreads + 32, smem);
+  if (e != cudaSuccess || occ < 1) occ = 1;
+  long long grid = (long long)ds->sms * occ;
+  grid = std::min<long long>(grid, H->n_units);
+  if (grid < 1) return CIM_OK;
+
+  unsigned int *ctr = take_counters(ds, passes);
+  e = cudaMemsetAsync(ctr, 0, passes * sizeof(unsigned int), stream);
+  if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("cudaMemsetAsync counter: ") + cudaGetErrorString(e));
+
+  for (int ps = 0; ps < passes; ++ps) {
+    SpmmParams p;
+    p.units = reinterpret_cast<const int4 *>(H->units);
+    p.tile_rc = reinterpret_cast<const int2 *>(H->tile_rc);
+    p.vals = reinterpret_cast<const unsigned char *>(H->vals);
+    p.X = reinterpret_cast<const unsigned char *>(X);
+    p.Y = reinterpret_cast<unsigned char *>(Y);
+    p.counter = ctr + ps;
+    p.n_units = H->n_units;
+    p.ldy = ldy;
+    p.k = k;
+    p.v_base = ps * KV * NG;
+    p.stages = S;
+    p.stage_bytes = stage_bytes;
+    p.tile_bytes = tile_bytes;
+    p.xblk_bytes = xblk;
+    kern<<<(unsigned int)grid, NG * kGroupThreads + 32, smem, stream>>>(p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("sym_spmm launch: ") + cudaGetErrorString(e));
+  }
+  return CIM_OK;
+}
+
+}  // namespace
+}  // namespace cim
+
+using namespace cim;
+
+extern "C" int cim_sym_spmm_supported(int32_t dtype, int32_t k) {
+  LaunchCfg c;
+  return pick_cfg(dtype, k, c) ? 1 : 0;
+}
+
+extern "C" int cim_sym_spmm(const cim_half_tiles *H, const void *X, void *Y, int32_t k, int64_t ldx, int64_t ldy,
+                            uint32_t flags, void *stream_) {
+  clear_error();
+  if (!H) return set_error(CIM_EINVAL, "H is NULL");
+  if (H->block != kBlock) return set_error(CIM_EINVAL, "block must be 64");
+  if (H->n < 1) return set_error(CIM_EINVAL, "n must be >= 1");
+  if (H->dtype != CIM_F32 && H->dtype != CIM_F64) return set_error(CIM_EINVAL, "dtype must be CIM_F32 or CIM_F64");
+  if (!X || !Y) return set_error(CIM_EINVAL, "X and Y must be non-NULL");
+  if (k < 1) return set_error(CIM_EINVAL, "k must be >= 1");
+  if (ldx != k) return set_error(CIM_EINVAL, "X must be dense row-major (ldx == k)");
+  if (ldy < k) return set_error(CIM_EINVAL, "ldy must be >= k");
+  if (H->n_tiles < 0 || H->n_units < 0) return set_error(CIM_EINVAL, "negative tile/unit count");
+  if (H->n_tiles > 0 && (!H->tile_rc || !H->units || !H->vals)) return set_error(CIM_EINVAL, "tile arrays are NULL");
+  const size_t es = H->dtype == CIM_F32 ? 4 : 8;
+  if ((reinterpret_cast<uintptr_t>(X) & 15) || (reinterpret_cast<uintptr_t>(Y) & 15) ||
+      (reinterpret_cast<uintptr_t>(H->vals) & 15))
+    return set_error(CIM_EINVAL, "X, Y and vals must be 16-byte aligned");
+  if ((ldy * (int64_t)es) % 16 != 0 && k * es >= 16) return set_error(CIM_EINVAL, "ldy*sizeof(T) must be a multiple of 16");
+  LaunchCfg cfg;
+  if (!pick_cfg(H->dtype, k, cfg)) return set_error(CIM_EUNSUPPORTED, "unsupported (dtype, k)");
+
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  DeviceState *ds = nullptr;
+  int rc = device_state(&ds);
+  if (rc) return rc;
+  const int64_t nb = (H->n + kBlock - 1) / kBlock;
+  const int64_t n_pad = nb * kBlock;
+  if (!(flags & CIM_ACCUMULATE)) {
+    cudaError_t e = (ldy == k) ? cudaMemsetAsync(Y, 0, (size_t)n_pad * k * es, stream)
+                               : cudaMemset2DAsync(Y, (size_t)ldy * es, 0, (size_t)k * es, (size_t)n_pad, stream);
+    if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("zeroing Y: ") + cudaGetErrorString(e));
+  }
+  if (H->n_tiles == 0 || H->n_units == 0) return CIM_OK;
+
+  if (H->dtype == CIM_F32) {
+    switch (cfg.KV * 10 + cfg.NG) {
+      case 11: return launch_kernel<float, 1, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+      case 21: return launch_kernel<float, 2, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+      case 41: return launch_kernel<float, 4, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+      case 81: return launch_kernel<float, 8, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+      case 82: return launch_kernel<float, 8, 2>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+    }
+  } else {
+    switch (cfg.KV * 10 + cfg.NG) {
+      case 11: return launch_kernel<double, 1, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+      case 21: return launch_kernel<double, 2, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+      case 41: return launch_kernel<double, 4, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+      case 42: return launch_kernel<double, 4, 2>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+    }
+  }
+  return set_error(CIM_EUNSUPPORTED, "no kernel for (dtype, k)");
+}

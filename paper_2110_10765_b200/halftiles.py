@@ -1,0 +1,359 @@
+"""Block-half tile storage of a symmetric matrix, laid out for B200 streaming.
+
+``HalfTiles`` is the B200 replacement of the reference's ``SparseSkeleton``
+(pkg/src/cimotifs/pipeline.py:96-116).  The reference stores BOTH triangles
+entry by entry (int64 column + f32 value per entry, segmented per
+(tile,row)).  Here only the upper block triangle is stored, as dense 64×64
+tiles in the fragment order the sm_100a kernel consumes (include/cim_b200.h):
+
+* ``tile_rc``  int32 (T, 2): (R, C) with R ≤ C, sorted — diagonal tiles first
+  in each block row and stored in full;
+* ``units``    int32 (U, 4): the kernel's work units (≤ ``max_unit`` tiles of
+  one block row), from the native planner ``cim_plan_units``;
+* ``vals``     (T, 4096) f32/f64 in HBM, 16 KB (f32) per tile, one
+  ``cp.async.bulk`` each.
+
+Constructors mirror how the reference gets a matrix:
+``from_skeleton`` (a reference ``SparseSkeleton`` + orbitals),
+``from_coo`` (any exactly-symmetric COO), and ``synthetic`` (the BASELINE
+configs: seeded Bernoulli tile pattern, values ``h(i XOR j; seed)`` generated
+bit-exactly on the device, pipeline.py:216-222).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import BLOCK, CIM_F32, CIM_F64, CimHalfTiles, check, lib
+
+DEFAULT_MAX_UNIT = 32
+VALUE_KINDS = {"h_xor": _lib.CIM_VALUES_H_XOR, "op_hash": _lib.CIM_VALUES_OP_HASH, "identity": _lib.CIM_VALUES_IDENTITY}
+
+
+def _dtype_code(dtype: torch.dtype) -> int:
+    if dtype == torch.float32:
+        return CIM_F32
+    if dtype == torch.float64:
+        return CIM_F64
+    raise ValueError(f"dtype must be torch.float32 or torch.float64, got {dtype}")
+
+
+def _as_torch_dtype(dtype) -> torch.dtype:
+    if isinstance(dtype, torch.dtype):
+        return dtype
+    d = np.dtype(dtype)
+    if d == np.float32:
+        return torch.float32
+    if d == np.float64:
+        return torch.float64
+    raise ValueError(f"dtype must be float32 or float64, got {dtype}")
+
+
+def plan_units(tile_rc: np.ndarray, nb: int, max_unit: int = DEFAULT_MAX_UNIT) -> np.ndarray:
+    """Work units (R, t0, t1, 0) via the native planner (validates tile order)."""
+    rc = np.ascontiguousarray(tile_rc, dtype=np.int32)
+    T = rc.shape[0]
+    out = np.zeros((max(T, 1), 4), dtype=np.int32)
+    nu = ctypes.c_int64(0)
+    check(lib().cim_plan_units(rc.ctypes.data if T else None, T, nb, max_unit, out.ctypes.data, ctypes.byref(nu)),
+          "cim_plan_units")
+    return out[: nu.value].copy()
+
+
+def partition_units(units: np.ndarray, parts: int) -> np.ndarray:
+    """Balanced contiguous unit ranges for `parts` GPUs (bounds, len parts+1)."""
+    u = np.ascontiguousarray(units, dtype=np.int32)
+    b = np.zeros(parts + 1, dtype=np.int64)
+    check(lib().cim_partition_units(u.ctypes.data if u.size else None, u.shape[0], parts, b.ctypes.data),
+          "cim_partition_units")
+    return b
+
+
+def synthetic_pattern(nb: int, p: float, seed: int = 0) -> np.ndarray:
+    """Tile pattern of the BASELINE configs: every diagonal tile, plus each
+    upper pair (R<C) kept with probability p.
+
+    Small grids (≤ 2²⁶ upper pairs) draw one Bernoulli per pair from
+    ``np.random.default_rng(seed)`` in ``triu_indices`` order (SURVEY.md §8(d)
+    C1: 5,244 off-diagonal tiles at nb=1024, p=0.01, seed 0).  Large grids
+    draw geometric gaps over the same linear order (C2/C3).
+    """
+    rng = np.random.default_rng(seed)
+    n_pairs = nb * (nb - 1) // 2
+    if n_pairs == 0 or p <= 0:
+        lin = np.zeros(0, dtype=np.int64)
+    elif n_pairs <= (1 << 26):
+        lin = np.flatnonzero(rng.random(n_pairs) < p).astype(np.int64)
+    else:
+        parts = []
+        pos = -1
+        expect = int(n_pairs * p * 1.05) + 1024
+        while True:
+            gaps = rng.geometric(p, size=expect)
+            cs = pos + np.cumsum(gaps, dtype=np.int64)
+            parts.append(cs[cs < n_pairs])
+            if cs[-1] >= n_pairs:
+                break
+            pos = int(cs[-1])
+        lin = np.concatenate(parts)
+    # linear upper-triangle index → (R, C): row R starts at R·(nb-1) − R(R-1)/2
+    R_all = np.arange(nb, dtype=np.int64)
+    starts = R_all * (nb - 1) - R_all * (R_all - 1) // 2
+    R = np.searchsorted(starts, lin, side="right") - 1
+    C = lin - starts[R] + R + 1
+    diag = np.stack([R_all, R_all], axis=1)
+    off = np.stack([R, C], axis=1)
+    rc = np.concatenate([diag, off]).astype(np.int32)
+    order = np.lexsort((rc[:, 1], rc[:, 0]))
+    return np.ascontiguousarray(rc[order])
+
+
+def fragment_pack_host(tiles: np.ndarray) -> np.ndarray:
+    """Row-major (T,64,64) → fragment order (T,4096) on the host (numpy).
+    Same map as the device ``cim_pack_tiles``; used for host-built fixtures."""
+    T = tiles.shape[0]
+    is64 = tiles.dtype == np.float64
+    idx = np.arange(4096)
+    if not is64:
+        j = idx & 3
+        mb = (idx >> 2) & 127
+        i = idx >> 9
+    else:
+        jj = idx & 1
+        mb = (idx >> 1) & 127
+        h = (idx >> 8) & 1
+        i = idx >> 9
+        j = 2 * h + jj
+    rg = (mb & 31) >> 2
+    cg = ((mb >> 5) << 2) | (mb & 3)
+    row = rg + 8 * i
+    col = cg + 16 * j
+    return np.ascontiguousarray(tiles.reshape(T, 4096)[:, row * BLOCK + col])
+
+
+@dataclass
+class HalfTiles:
+    """Half-stored symmetric block-sparse matrix resident in HBM."""
+
+    n: int
+    tile_rc: torch.Tensor  # int32 (T,2) on device
+    units: torch.Tensor  # int32 (U,4) on device
+    vals: torch.Tensor  # (T,4096) on device, fragment order
+    tile_rc_host: np.ndarray
+    units_host: np.ndarray
+    meta: dict = field(default_factory=dict)
+    _desc: CimHalfTiles | None = field(default=None, repr=False)
+
+    # ------------------------------------------------------------------ props
+    @property
+    def dtype(self) -> torch.dtype:
+        return self.vals.dtype
+
+    @property
+    def device(self) -> torch.device:
+        return self.vals.device
+
+    @property
+    def nb(self) -> int:
+        return (self.n + BLOCK - 1) // BLOCK
+
+    @property
+    def n_pad(self) -> int:
+        return self.nb * BLOCK
+
+    @property
+    def n_tiles(self) -> int:
+        return int(self.tile_rc_host.shape[0])
+
+    @property
+    def n_diag_tiles(self) -> int:
+        rc = self.tile_rc_host
+        return int(np.count_nonzero(rc[:, 0] == rc[:, 1]))
+
+    @property
+    def n_off_tiles(self) -> int:
+        return self.n_tiles - self.n_diag_tiles
+
+    @property
+    def nnz_stored(self) -> int:
+        """Stored entries (dense tiles: 4096 per tile)."""
+        return self.n_tiles * BLOCK * BLOCK
+
+    def flops(self, k: int) -> int:
+        """Algorithmic FLOPs of one apply: 2·k·(2·nnz_off + nnz_diag)."""
+        return 2 * k * (2 * self.n_off_tiles + self.n_diag_tiles) * BLOCK * BLOCK
+
+    def algorithmic_bytes(self, k: int) -> int:
+        """s·nnz_stored + 8·n_tiles + 2·n·k·s (dense tiles)."""
+        s = self.vals.element_size()
+        return s * self.nnz_stored + 8 * self.n_tiles + 2 * self.n * k * s
+
+    def descriptor(self) -> CimHalfTiles:
+        if self._desc is None:
+            self._desc = CimHalfTiles(
+                n=self.n,
+                block=BLOCK,
+                dtype=_dtype_code(self.dtype),
+                n_tiles=self.n_tiles,
+                n_units=int(self.units_host.shape[0]),
+                tile_rc=self.tile_rc.data_ptr() if self.n_tiles else None,
+                units=self.units.data_ptr() if self.units.numel() else None,
+                vals=self.vals.data_ptr() if self.n_tiles else None,
+            )
+        return self._desc
+
+    # ----------------------------------------------------------- constructors
+    @classmethod
+    def _from_pattern(cls, n: int, tile_rc: np.ndarray, dtype, device, max_unit: int) -> "HalfTiles":
+        dtype = _as_torch_dtype(dtype)
+        _dtype_code(dtype)
+        device = torch.device(device)
+        if device.type != "cuda":
+            raise ValueError("HalfTiles live in GPU memory: device must be a CUDA device")
+        nb = (n + BLOCK - 1) // BLOCK
+        rc = np.ascontiguousarray(tile_rc, dtype=np.int32).reshape(-1, 2)
+        units = plan_units(rc, nb, max_unit)  # validates order / range
+        t_rc = torch.from_numpy(rc).to(device)
+        t_units = torch.from_numpy(units).to(device)
+        vals = torch.empty((rc.shape[0], BLOCK * BLOCK), dtype=dtype, device=device)
+        return cls(n=int(n), tile_rc=t_rc, units=t_units, vals=vals, tile_rc_host=rc, units_host=units)
+
+    @classmethod
+    def synthetic(cls, n: int, p: float | None = None, *, n_off: int | None = None, seed: int = 0,
+                  value_seed: int = 0, values: str = "h_xor", op_k: int = 0, dtype=torch.float32,
+                  device="cuda", max_unit: int = DEFAULT_MAX_UNIT, tile_rc: np.ndarray | None = None) -> "HalfTiles":
+        """Synthetic half-stored matrix (BASELINE.json configs).
+
+        Pattern: all diagonal tiles plus upper tiles kept with probability p
+        (or p = n_off / #upper-pairs).  Values: ``h_xor`` = h(i XOR j;
+        value_seed) (reference matrix values), ``op_hash`` = O_ij(op_k;
+        value_seed) (no XOR structure — proves the kernel treats values as
+        opaque), ``identity`` = δ_ij.  Generated on the device.
+        """
+        if values not in VALUE_KINDS:
+            raise ValueError(f"unknown values {values!r}, expected one of {tuple(VALUE_KINDS)}")
+        nb = (n + BLOCK - 1) // BLOCK
+        if tile_rc is None:
+            n_pairs = nb * (nb - 1) // 2
+            if p is None:
+                p = 0.0 if n_pairs == 0 else float(n_off or 0) / n_pairs
+            if not 0.0 <= p <= 1.0:
+                raise ValueError(f"p must be in [0, 1], got {p}")
+            tile_rc = synthetic_pattern(nb, p, seed)
+        H = cls._from_pattern(n, tile_rc, dtype, device, max_unit)
+        stream = torch.cuda.current_stream(H.device).cuda_stream
+        with torch.cuda.device(H.device):
+            check(lib().cim_fill_synthetic_values(H.tile_rc.data_ptr() if H.n_tiles else None, H.n_tiles, n,
+                                                  _dtype_code(H.dtype), VALUE_KINDS[values], value_seed, op_k,
+                                                  H.vals.data_ptr() if H.n_tiles else None, stream),
+                  "cim_fill_synthetic_values")
+        H.meta.update(kind="synthetic", p=p, seed=seed, value_seed=value_seed, values=values, op_k=op_k)
+        return H
+
+    @classmethod
+    def from_dense_tiles(cls, n: int, tile_rc: np.ndarray, tiles, *, dtype=None, device="cuda",
+                         max_unit: int = DEFAULT_MAX_UNIT) -> "HalfTiles":
+        """From row-major dense tiles (T,64,64); repacked on the device."""
+        tiles_t = torch.as_tensor(tiles)
+        dtype = _as_torch_dtype(dtype if dtype is not None else tiles_t.dtype)
+        H = cls._from_pattern(n, tile_rc, dtype, device, max_unit)
+        if H.n_tiles:
+            src = tiles_t.to(device=H.device, dtype=dtype).reshape(H.n_tiles, BLOCK * BLOCK).contiguous()
+            stream = torch.cuda.current_stream(H.device).cuda_stream
+            with torch.cuda.device(H.device):
+                check(lib().cim_pack_tiles(src.data_ptr(), H.n_tiles, _dtype_code(dtype), H.vals.data_ptr(), stream),
+                      "cim_pack_tiles")
+            torch.cuda.current_stream(H.device).synchronize()
+        return H
+
+    @classmethod
+    def from_coo(cls, n: int, i, j, v, *, dtype=torch.float32, device="cuda", check_symmetric: bool = True,
+                 max_unit: int = DEFAULT_MAX_UNIT) -> "HalfTiles":
+        """From a full (both-triangle) symmetric COO, e.g. a reference skeleton.
+
+        Keeps entries with ⌊i/64⌋ ≤ ⌊j/64⌋ — lossless for an exactly symmetric
+        matrix.  Raises ValueError if (i,j,v) is not exactly
+        symmetric (when check_symmetric) or indices fall outside [0, n).
+        """
+        i = np.asarray(i, dtype=np.int64)
+        j = np.asarray(j, dtype=np.int64)
+        v = np.asarray(v)
+        if not (i.shape == j.shape == v.shape) or i.ndim != 1:
+            raise ValueError("i, j, v must be equal-length 1-D arrays")
+        if i.size and (i.min() < 0 or j.min() < 0 or i.max() >= n or j.max() >= n):
+            raise ValueError(f"COO indices must lie in [0, {n})")
+        if check_symmetric and i.size:
+            a = np.lexsort((j, i))
+            b = np.lexsort((i, j))
+            if not (np.array_equal(i[a], j[b]) and np.array_equal(j[a], i[b]) and np.array_equal(v[a], v[b])):
+                raise ValueError("COO is not exactly symmetric; the half-stored format needs A == Aᵀ")
+        nb = (n + BLOCK - 1) // BLOCK
+        R = i // BLOCK
+        C = j // BLOCK
+        keep = R <= C
+        i, j, v, R, C = i[keep], j[keep], v[keep], R[keep], C[keep]
+        key = R * nb + C
+        uniq, inv = np.unique(key, return_inverse=True)
+        np_dtype = np.float64 if _as_torch_dtype(dtype) == torch.float64 else np.float32
+        tiles = np.zeros((uniq.size, BLOCK, BLOCK), dtype=np.float64)
+        np.add.at(tiles, (inv, i % BLOCK, j % BLOCK), v.astype(np.float64))
+        rc = np.stack([uniq // nb, uniq % nb], axis=1).astype(np.int32)
+        H = cls.from_dense_tiles(n, rc, tiles.astype(np_dtype), dtype=dtype, device=device, max_unit=max_unit)
+        H.meta.update(kind="coo", nnz_full=int(keep.size), nnz_half=int(i.size))
+        return H
+
+    @classmethod
+    def from_skeleton(cls, skeleton, orbitals, n: int | None = None, **kw) -> "HalfTiles":
+        """From a reference ``SparseSkeleton`` (pipeline.py:96-116) and its
+        orbitals: rows are recovered from the per-(tile,row) segments
+        (pipeline.py:319-330), then ``from_coo``."""
+        start = {o.id: o.start for o in orbitals}
+        size = {o.id: o.stop - o.start for o in orbitals}
+        seg_row = np.concatenate(
+            [start[t.row_orbital] + np.arange(size[t.row_orbital], dtype=np.int64) for t in skeleton.tiles])
+        i = np.repeat(seg_row, np.asarray(skeleton.segments.counts, dtype=np.int64))
+        if n is None:
+            n = max(o.stop for o in orbitals)
+        return cls.from_coo(n, i, skeleton.colind, skeleton.values, **kw)
+
+    # ----------------------------------------------------------------- export
+    def dense_tiles(self) -> torch.Tensor:
+        """Row-major (T,64,64) copy of the stored tiles (device)."""
+        out = torch.empty((self.n_tiles, BLOCK, BLOCK), dtype=self.dtype, device=self.device)
+        if self.n_tiles:
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+            with torch.cuda.device(self.device):
+                check(lib().cim_unpack_tiles(self.vals.data_ptr(), self.n_tiles, _dtype_code(self.dtype),
+                                             out.data_ptr(), stream), "cim_unpack_tiles")
+        return out
+
+    def save(self, path) -> None:
+        """npz interchange: n, tile_rc, row-major tiles (host)."""
+        np.savez_compressed(path, n=self.n, tile_rc=self.tile_rc_host, tiles=self.dense_tiles().cpu().numpy(),
+                            format="cim_half_tiles_v1")
+
+    @classmethod
+    def load(cls, path, device="cuda", **kw) -> "HalfTiles":
+        z = np.load(path)
+        if str(z["format"]) != "cim_half_tiles_v1":
+            raise ValueError(f"{path}: not a cim_half_tiles_v1 file")
+        return cls.from_dense_tiles(int(z["n"]), z["tile_rc"], z["tiles"], device=device, **kw)
+
+    def shard(self, unit_lo: int, unit_hi: int) -> "HalfTiles":
+        """View of the tiles of units [unit_lo, unit_hi) (same n; GPU panel)."""
+        u = self.units_host[unit_lo:unit_hi]
+        if u.shape[0] == 0:
+            t0 = t1 = 0
+        else:
+            t0, t1 = int(u[0, 1]), int(u[-1, 2])
+        units = u.copy()
+        units[:, 1:3] -= t0
+        sub = HalfTiles(n=self.n, tile_rc=self.tile_rc[t0:t1], units=torch.from_numpy(units).to(self.device),
+                        vals=self.vals[t0:t1], tile_rc_host=self.tile_rc_host[t0:t1], units_host=units,
+                        meta=dict(self.meta, shard=(unit_lo, unit_hi)))
+        return sub

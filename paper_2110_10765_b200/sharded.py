@@ -1,0 +1,133 @@
+"""Row-block sharding of the half-stored SpMM over the GPUs of one box.
+
+SURVEY.md §8(e): GPU g owns a contiguous run of block rows chosen so the
+stored-tile counts are balanced (upper-triangular storage puts ~p·(nb−R)
+tiles in block row R, so equal row counts would be badly unbalanced).  The
+vectors are distributed separately, in equal 64-aligned row chunks, so the
+two exchange steps are plain fixed-size NCCL collectives over NVLink:
+
+    X_full  = all_gather(X_local)                  (every rank needs any X_C)
+    Y_part  = U_g·X_full + U_g,offᵀ·X_full          (local sm_100a kernel)
+    Y_local = reduce_scatter(Y_part, SUM)           (Hᵀ·X lands on other ranks)
+
+One process per GPU, ``torch.distributed`` with the NCCL backend.  The
+reference has no distribution at all; its only parallelism is
+numba's thread pool (_util.py:37-62).
+"""
+
+from __future__ import annotations
+
+from typing import Callable
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from ._lib import BLOCK
+from .halftiles import HalfTiles, partition_units, plan_units, synthetic_pattern
+from .spmm import _launch, padded_k
+
+
+def row_chunks(n: int, world: int) -> tuple[int, int]:
+    """(rows per rank, total padded rows) for the equal X/Y row distribution."""
+    nb = (n + BLOCK - 1) // BLOCK
+    per = ((nb + world - 1) // world) * BLOCK
+    return per, per * world
+
+
+def shard_tile_range(units: np.ndarray, world: int, rank: int) -> tuple[int, int, int, int]:
+    """(unit_lo, unit_hi, tile_lo, tile_hi) of `rank` under balanced partition."""
+    b = partition_units(units, world)
+    lo, hi = int(b[rank]), int(b[rank + 1])
+    if hi > lo:
+        return lo, hi, int(units[lo, 1]), int(units[hi - 1, 2])
+    return lo, hi, 0, 0
+
+
+class ShardedSymSpmm:
+    """Distributed ``Y = A·X`` with A's tiles row-block sharded over ranks.
+
+    ``local_apply(X_full, Y_part)`` computes this rank's panel product into
+    the zero-initialised-by-callee ``Y_part``; the default is the sm_100a
+    kernel on ``H_local``.  (Tests on CPU/gloo inject the oracle here; the
+    product path never does.)
+    """
+
+    def __init__(self, n: int, k: int, dtype: torch.dtype, device, H_local: HalfTiles | None = None,
+                 group=None, local_apply: Callable | None = None):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.n = int(n)
+        self.dtype = dtype
+        self.device = torch.device(device)
+        self.H = H_local
+        if local_apply is None:
+            if H_local is None:
+                raise ValueError("need H_local (CUDA kernel) or local_apply")
+            self.k = padded_k(dtype, k)
+            local_apply = self._cuda_apply
+        else:
+            self.k = int(k)
+        self.k_user = int(k)
+        self.local_apply = local_apply
+        self.rows_per_rank, self.rows_total = row_chunks(self.n, self.world)
+        self.X_full = torch.zeros((self.rows_total, self.k), dtype=dtype, device=self.device)
+        self.Y_part = torch.zeros((self.rows_total, self.k), dtype=dtype, device=self.device)
+        self.Y_local = torch.zeros((self.rows_per_rank, self.k), dtype=dtype, device=self.device)
+        self.n_pad = ((self.n + BLOCK - 1) // BLOCK) * BLOCK
+
+    # ------------------------------------------------------------------ build
+    @classmethod
+    def synthetic(cls, n: int, *, k: int, p: float | None = None, n_off: int | None = None, seed: int = 0,
+                  value_seed: int = 0, dtype=torch.float32, device=None, group=None, max_unit: int = 32,
+                  values: str = "h_xor") -> "ShardedSymSpmm":
+        """Every rank draws the same global tile pattern (seeded), keeps its
+        balanced panel, and generates only its own tile values on its GPU."""
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        nb = (n + BLOCK - 1) // BLOCK
+        if p is None:
+            n_pairs = nb * (nb - 1) // 2
+            p = 0.0 if n_pairs == 0 else float(n_off or 0) / n_pairs
+        rc = synthetic_pattern(nb, p, seed)
+        units = plan_units(rc, nb, max_unit)
+        _, _, t0, t1 = shard_tile_range(units, world, rank)
+        device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        H = HalfTiles.synthetic(n, tile_rc=rc[t0:t1], value_seed=value_seed, values=values, dtype=dtype,
+                                device=device, max_unit=max_unit)
+        H.meta.update(global_tiles=int(rc.shape[0]), global_off_tiles=int(np.count_nonzero(rc[:, 0] != rc[:, 1])),
+                      p=p, seed=seed)
+        return cls(n, k, dtype, device, H_local=H, group=group)
+
+    # ------------------------------------------------------------------ apply
+    def _cuda_apply(self, X_full: torch.Tensor, Y_part: torch.Tensor) -> None:
+        _launch(self.H, X_full[: self.n_pad], Y_part[: self.n_pad], False, None)
+
+    def local_rows(self) -> tuple[int, int]:
+        """Global row range [lo, hi) of this rank's X/Y chunk (clipped to n)."""
+        lo = self.rank * self.rows_per_rank
+        return min(lo, self.n), min(lo + self.rows_per_rank, self.n)
+
+    def apply(self, X_local: torch.Tensor) -> torch.Tensor:
+        """Y_local = (A·X)[local rows] given X_local = X[local rows]
+        (shape (rows_per_rank, k_user); rows ≥ n must be 0)."""
+        if X_local.shape[0] != self.rows_per_rank:
+            raise ValueError(f"X_local must have {self.rows_per_rank} rows, got {X_local.shape[0]}")
+        if X_local.shape[1] != self.k_user:
+            raise ValueError(f"X_local must have {self.k_user} columns, got {X_local.shape[1]}")
+        if self.k != self.k_user:
+            xl = torch.zeros((self.rows_per_rank, self.k), dtype=self.dtype, device=self.device)
+            xl[:, : self.k_user] = X_local
+        else:
+            xl = X_local.contiguous()
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.X_full, xl, group=self.group)
+        else:
+            self.X_full.copy_(xl)
+        self.local_apply(self.X_full, self.Y_part)
+        if self.world > 1:
+            dist.reduce_scatter_tensor(self.Y_local, self.Y_part, op=dist.ReduceOp.SUM, group=self.group)
+        else:
+            self.Y_local.copy_(self.Y_part)
+        return self.Y_local[:, : self.k_user]

@@ -1,0 +1,137 @@
+"""The operator:  Y = H·X + Hᵀ·X  over a half-stored symmetric ``HalfTiles``.
+
+``sym_spmm`` is the B200 drop-in for the reference's pair-walk operator
+boundary (``contract_observables``, pkg/src/cimotifs/pipeline.py:534-570):
+validate first and raise ``ValueError`` before any compute (:550-555), coerce
+inputs to C-contiguous float arrays (:395), write into a caller-owned buffer
+or return a fresh array (:569).  Compute happens only in the sm_100a kernel
+behind the C-ABI (``cim_sym_spmm``); there is no CPU path.
+
+Layouts: X may be ``(n, k)`` (row-major, what the kernel streams) or
+``(k, n)`` — the reference's ``ObservablesInput.c`` layout (n_vec, n),
+pipeline.py:387 — selected with ``layout=`` (``"auto"`` prefers (n, k) when
+ambiguous).  numpy inputs are copied to the device and the result is returned
+as numpy (host buffers in, host buffers out).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from ._lib import BLOCK, CIM_ACCUMULATE, check, lib
+from .halftiles import HalfTiles
+
+LAYOUTS = ("auto", "nk", "kn")
+
+
+def supported_k(dtype: torch.dtype, k: int) -> bool:
+    code = 0 if dtype == torch.float32 else 1
+    return bool(lib().cim_sym_spmm_supported(code, int(k)))
+
+
+def padded_k(dtype: torch.dtype, k: int) -> int:
+    """Smallest compiled vector count ≥ k (extra columns are zero)."""
+    kk = int(k)
+    while kk <= 64 and not supported_k(dtype, kk):
+        kk += 1
+    if kk > 64:
+        raise ValueError(f"k={k} exceeds the largest compiled vector count (64); split X into column blocks")
+    return kk
+
+
+def _launch(H: HalfTiles, Xd: torch.Tensor, Yd: torch.Tensor, accumulate: bool, stream) -> None:
+    """Raw C-ABI call on device tensors of shape (n_pad, k) (k compiled)."""
+    k = Xd.shape[1]
+    s = stream if stream is not None else torch.cuda.current_stream(H.device)
+    handle = s.cuda_stream if isinstance(s, torch.cuda.Stream) else int(s)
+    with torch.cuda.device(H.device):
+        rc = lib().cim_sym_spmm(H.descriptor(), Xd.data_ptr(), Yd.data_ptr(), k, Xd.stride(0), Yd.stride(0),
+                                CIM_ACCUMULATE if accumulate else 0, handle)
+    check(rc, "cim_sym_spmm")
+
+
+def sym_spmm(H: HalfTiles, X, out=None, *, layout: str = "auto", accumulate: bool = False, stream=None):
+    """Y = H·X + Hᵀ·X = A·X for the symmetric A stored as block-half tiles.
+
+    Parameters
+    ----------
+    H : HalfTiles
+    X : torch.Tensor (CUDA or CPU) or numpy array, (n, k) or (k, n), dtype of H
+    out : optional tensor/array of X's shape to write into (``accumulate``
+        adds to it instead of overwriting)
+    layout : "auto" | "nk" | "kn"
+    stream : torch.cuda.Stream or raw cudaStream_t handle (default: current)
+    """
+    if not isinstance(H, HalfTiles):
+        raise ValueError(f"H must be a HalfTiles, got {type(H).__name__}")
+    if layout not in LAYOUTS:
+        raise ValueError(f"unknown layout {layout!r}, expected one of {LAYOUTS}")
+    is_numpy = isinstance(X, np.ndarray)
+    Xt = torch.from_numpy(np.ascontiguousarray(X)) if is_numpy else X
+    if not isinstance(Xt, torch.Tensor):
+        raise ValueError(f"X must be a torch.Tensor or numpy.ndarray, got {type(X).__name__}")
+    if Xt.ndim != 2:
+        raise ValueError(f"X must be 2-D (n, k) or (k, n), got shape {tuple(Xt.shape)}")
+    if Xt.dtype != H.dtype:
+        raise ValueError(f"X dtype {Xt.dtype} does not match the matrix dtype {H.dtype}")
+    n = H.n
+    if layout == "auto":
+        if Xt.shape[0] == n:
+            layout = "nk"
+        elif Xt.shape[1] == n:
+            layout = "kn"
+        else:
+            raise ValueError(f"X of shape {tuple(Xt.shape)} does not cover the n={n} matrix rows")
+    if layout == "nk" and Xt.shape[0] != n:
+        raise ValueError(f"X has {Xt.shape[0]} rows, matrix has n={n}")
+    if layout == "kn" and Xt.shape[1] != n:
+        raise ValueError(f"X covers {Xt.shape[1]} states, matrix has n={n}")
+    k = Xt.shape[1] if layout == "nk" else Xt.shape[0]
+    if k < 1:
+        raise ValueError("X must hold at least one vector")
+    if out is not None:
+        if tuple(out.shape) != tuple(Xt.shape):
+            raise ValueError(f"out has shape {tuple(out.shape)}, expected {tuple(Xt.shape)}")
+        if (isinstance(out, np.ndarray) and out.dtype != np.dtype(str(H.dtype).split(".")[-1])) or (
+                isinstance(out, torch.Tensor) and out.dtype != H.dtype):
+            raise ValueError("out dtype must match the matrix dtype")
+
+    dev = H.device
+    kk = padded_k(H.dtype, k)
+    Xd = Xt.to(dev, non_blocking=True)
+    if layout == "kn":
+        Xd = Xd.t()
+    direct = (Xd.is_contiguous() and kk == k and H.n_pad == n and Xd.data_ptr() % 16 == 0)
+    if not direct:
+        Xp = torch.zeros((H.n_pad, kk), dtype=H.dtype, device=dev)
+        Xp[:n, :k] = Xd
+        Xd = Xp
+    # output buffer on device, (n_pad, kk) row-major
+    out_is_dev_nk = (isinstance(out, torch.Tensor) and out.device == dev and layout == "nk" and direct
+                     and out.is_contiguous())
+    if out_is_dev_nk:
+        Yd = out
+    else:
+        Yd = torch.empty((H.n_pad, kk), dtype=H.dtype, device=dev)
+        if accumulate and out is not None:
+            o = torch.as_tensor(out).to(dev)
+            Yd.zero_()
+            Yd[:n, :k] = o if layout == "nk" else o.t()
+        elif accumulate:
+            raise ValueError("accumulate=True needs an `out` buffer to add into")
+    _launch(H, Xd, Yd, accumulate, stream)
+    Y = Yd[:n, :k]
+    if layout == "kn":
+        Y = Y.t()
+    if out_is_dev_nk:
+        return out
+    if out is not None:
+        if isinstance(out, np.ndarray):
+            out[...] = Y.cpu().numpy()
+        else:
+            out.copy_(Y)
+        return out
+    if is_numpy:
+        return Y.cpu().numpy()
+    return Y.contiguous() if layout == "kn" else (Y if direct else Y.contiguous())

@@ -1,0 +1,336 @@
+"""GPU parity: the sm_100a path through the C-ABI vs the CPU oracle.
+
+Gate (BASELINE.json north star): ‖ΔY‖_F / (‖A‖_F·‖X‖_F) ≤ 1e-5 (f32),
+≤ 1e-12 (f64); plus the componentwise bound |ΔY| ≤ (c+2)·u·(|A||X|) with
+c = max row nnz, u = 2⁻²⁴ (f32) / 2⁻⁵³ (f64), which a TF32 shortcut fails.
+Structure and values are bit-exact (integer/bitwise comparisons).
+"""
+
+import json
+
+import numpy as np
+import pytest
+import torch
+
+from golden_util import GOLDEN, load_fixture
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+F32_GATE, F64_GATE = 1e-5, 1e-12
+U32, U64 = 2.0 ** -24, 2.0 ** -53
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2110_10765_b200 as p
+
+    return p
+
+
+def check_result(n, rc, tiles, X, Y, dtype):
+    """Normwise + componentwise gates against the f64 oracle."""
+    X = np.asarray(X, np.float64)
+    Y_ref = oracle.sym_spmm(n, rc, tiles, X)
+    A_f = oracle.frobenius_full(rc, tiles)
+    err = oracle.normwise_error(Y, Y_ref, A_f, X)
+    gate = F32_GATE if dtype == torch.float32 else F64_GATE
+    assert err <= gate, f"normwise error {err:.3e} > {gate}"
+    u = U32 if dtype == torch.float32 else U64
+    nnz_row = 64 * max(1, int(np.bincount(np.concatenate([rc[:, 0], rc[rc[:, 0] != rc[:, 1], 1]])).max()))
+    absAX = oracle.abs_product(n, rc, tiles, X)
+    assert oracle.componentwise_ok(Y, Y_ref, absAX, nnz_row, u), "componentwise bound violated"
+    return err
+
+
+def f32bits(a):
+    return np.asarray(a, dtype=np.float32).view(np.uint32)
+
+
+# ----------------------------------------------------------------------------
+# device hash / value generation / repacking: bit-exact
+# ----------------------------------------------------------------------------
+
+def test_device_hash_matches_reference_kats(pkg):
+    kat = json.loads((GOLDEN / "hash_kat.json").read_text())
+    for key, kind in (("h", 0), ("op", None)):
+        cases = kat[key]
+        I = torch.tensor([c["i"] for c in cases], dtype=torch.int64, device="cuda")
+        J = torch.tensor([c["j"] for c in cases], dtype=torch.int64, device="cuda")
+        for idx, c in enumerate(cases):
+            kd = kind if kind is not None else (1 if c["op_code"] == 1 else 2)
+            out = torch.empty(1, dtype=torch.float32, device="cuda")
+            pkg._lib.check(pkg.lib().cim_hash_values(I[idx:].data_ptr(), J[idx:].data_ptr(), 1, kd, c["seed"],
+                                                     c.get("k", 0), out.data_ptr(), None), "hash")
+            torch.cuda.synchronize()
+            assert int(f32bits(out.cpu().numpy())[0]) == c["bits"], c
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("values,kind", [("h_xor", 0), ("op_hash", 1), ("identity", 2)])
+def test_synthetic_values_bit_exact(pkg, dtype, values, kind):
+    n = 1000  # ragged: last block half empty
+    rc = pkg.synthetic_pattern((n + 63) // 64, 0.3, seed=1)
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, values=values, value_seed=7, op_k=2, dtype=dtype)
+    got = H.dense_tiles().cpu().numpy()
+    want = oracle.synthetic_dense_tiles(n, rc, seed=7, kind=kind, op_k=2).astype(got.dtype)
+    assert np.array_equal(got.view(np.uint8), want.view(np.uint8))
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_pack_matches_host_layout_and_roundtrips(pkg, dtype):
+    from paper_2110_10765_b200.halftiles import fragment_pack_host
+
+    rng = np.random.default_rng(3)
+    npd = np.float32 if dtype == torch.float32 else np.float64
+    tiles = rng.standard_normal((5, 64, 64)).astype(npd)
+    rc = np.array([[0, 0], [0, 2], [1, 1], [1, 3], [2, 2]], np.int32)
+    H = pkg.HalfTiles.from_dense_tiles(4 * 64, rc, tiles, dtype=dtype)
+    assert np.array_equal(H.vals.cpu().numpy(), fragment_pack_host(tiles))
+    assert np.array_equal(H.dense_tiles().cpu().numpy(), tiles)
+
+
+# ----------------------------------------------------------------------------
+# SpMM parity on reference skeletons
+# ----------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["skel_small.npz", "skel_n1024.npz", "skel_identity.npz"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_reference_skeleton_spmm(pkg, name, dtype):
+    f = load_fixture(name)
+    n = int(f["n"])
+    H = pkg.HalfTiles.from_coo(n, f["i"], f["j"], f["v"], dtype=dtype)
+    # structure: the stored half-tile set reproduces the reference pair set exactly
+    tiles = H.dense_tiles().cpu().numpy()
+    i, j, v = oracle.half_tiles_to_coo(n, H.tile_rc_host, tiles)
+    assert oracle.pair_set_digest(i, j) == str(f["pair_digest"])
+    X = torch.from_numpy(f["X"]).to(dtype)
+    Y = pkg.sym_spmm(H, X.cuda()).cpu().numpy()
+    check_result(n, H.tile_rc_host, tiles.astype(np.float64), f["X"], Y, dtype)
+    # against the reference's matrix product computed by scipy from its COO
+    rel = np.linalg.norm(Y - f["Y_ref"]) / np.linalg.norm(f["Y_ref"])
+    assert rel <= (1e-5 if dtype == torch.float32 else 1e-12)
+
+
+@pytest.mark.parametrize("name", ["skel_small.npz", "skel_n1024.npz", "skel_identity.npz"])
+def test_contract_observables_matches_reference(pkg, name):
+    f = load_fixture(name)
+    n = int(f["n"])
+    pattern = pkg.HalfTiles.from_coo(n, f["i"], f["j"], np.ones_like(f["v"]))
+    c = f["X"].T.copy()
+    inp = pkg.ObservablesInput(c=c, m_ops=int(f["m_ops"]), op_kind=str(f["op_kind"]), seed=int(f["op_seed"]))
+    got = pkg.contract_observables(pattern, inp).astype(np.float64)
+    tol = oracle.contraction_tolerance(c, int(f["nnz"]))
+    assert np.abs(got - f["accum_oracle"]).max() <= tol
+    assert np.abs(got - f["accum"]).max() <= tol
+    got_t = pkg.contract_observables(pattern, pkg.ObservablesInput(c=c, m_ops=int(f["m_ops"]),
+                                                                  op_kind=str(f["op_kind"]), seed=int(f["op_seed"])),
+                                     transpose=True)
+    assert np.abs(got_t - got).max() <= tol
+    if str(f["op_kind"]) == "identity":
+        assert np.all(np.abs(got - 1.0) <= 2.0 ** -20)
+
+
+def test_single_state_diagonal(pkg):
+    # test_pipeline.py:131-138: one state → nnz 1, value h(0,0,0)
+    H = pkg.HalfTiles.from_coo(1, [0], [0], np.array([oracle.h_values(0, 0, 0)], np.float32).reshape(1))
+    assert H.n_tiles == 1 and H.n == 1
+    Y = pkg.sym_spmm(H, torch.tensor([[2.0]], device="cuda"))
+    assert float(Y[0, 0]) == 2.0 * float(oracle.h_values(0, 0, 0))
+
+
+# ----------------------------------------------------------------------------
+# synthetic configs, vector-count sweep, edge cases
+# ----------------------------------------------------------------------------
+
+@pytest.fixture(scope="module")
+def c1_small(pkg):
+    """A C1-family matrix (block 64, Bernoulli tiles) small enough for the f64
+    numpy oracle: n = 8192 - 37 (ragged), p = 0.05."""
+    n = 8192 - 37
+    rc = pkg.synthetic_pattern((n + 63) // 64, 0.05, seed=11)
+    tiles = oracle.synthetic_dense_tiles(n, rc, seed=0)
+    return n, rc, tiles
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 8, 16, 24, 32])
+def test_k_sweep_f32(pkg, c1_small, k):
+    n, rc, tiles = c1_small
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=torch.float32)
+    X = torch.randn((n, k), generator=torch.Generator().manual_seed(k))
+    Y = pkg.sym_spmm(H, X.cuda()).cpu().numpy()
+    check_result(n, rc, tiles, X.numpy(), Y, torch.float32)
+
+
+@pytest.mark.parametrize("k", [1, 2, 4, 8, 12, 16, 32])
+def test_k_sweep_f64(pkg, c1_small, k):
+    n, rc, tiles = c1_small
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=torch.float64)
+    X = torch.randn((n, k), generator=torch.Generator().manual_seed(k), dtype=torch.float64)
+    Y = pkg.sym_spmm(H, X.cuda()).cpu().numpy()
+    check_result(n, rc, tiles.astype(np.float64), X.numpy(), Y, torch.float64)
+
+
+def test_opaque_random_symmetric_values(pkg, c1_small):
+    """Values with no XOR structure (op hash of (min,max)) — the kernel must
+    treat tile values as opaque streamed data (SURVEY.md §7 hard parts)."""
+    n, rc, _ = c1_small
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, values="op_hash", value_seed=99, op_k=3)
+    tiles = oracle.synthetic_dense_tiles(n, rc, seed=99, kind=1, op_k=3)
+    X = torch.randn((n, 8), generator=torch.Generator().manual_seed(1))
+    check_result(n, rc, tiles, X.numpy(), pkg.sym_spmm(H, X.cuda()).cpu().numpy(), torch.float32)
+
+
+def test_c1_config_vs_c_oracle(pkg):
+    """BASELINE config 1: n=65,536, p=0.01 (5,244 off-diagonal tiles), k=8 f32."""
+    from oracle import cpu
+
+    n, k = 65536, 8
+    H = pkg.HalfTiles.synthetic(n, p=0.01, seed=0)
+    assert H.n_off_tiles == 5244 and H.n_diag_tiles == 1024
+    rc = H.tile_rc_host
+    tiles = cpu.fill_h(rc, n, 0)
+    X = np.random.default_rng(0).standard_normal((n, k)).astype(np.float32)
+    Y = pkg.sym_spmm(H, torch.from_numpy(X).cuda()).cpu().numpy()
+    Y_ref = cpu.sym_spmm_f64(n, rc, tiles, X)
+    err = oracle.normwise_error(Y, Y_ref, oracle.frobenius_full(rc, tiles), X)
+    assert err <= F32_GATE
+    # componentwise bound with |A||X|
+    absAX = cpu.sym_spmm_f64(n, rc, np.abs(tiles), np.abs(X))
+    nnz_row = 64 * int(np.bincount(np.concatenate([rc[:, 0], rc[rc[:, 0] != rc[:, 1], 1]])).max())
+    assert oracle.componentwise_ok(Y, Y_ref, absAX, nnz_row, U32)
+
+
+@pytest.mark.parametrize("n", [1, 63, 64, 65, 200])
+def test_ragged_and_tiny(pkg, n):
+    nb = (n + 63) // 64
+    rc = pkg.synthetic_pattern(nb, 1.0, seed=0)  # every upper tile
+    tiles = oracle.synthetic_dense_tiles(n, rc, seed=5)
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, value_seed=5)
+    X = torch.randn((n, 4), generator=torch.Generator().manual_seed(n))
+    check_result(n, rc, tiles, X.numpy(), pkg.sym_spmm(H, X.cuda()).cpu().numpy(), torch.float32)
+
+
+def test_diagonal_only_and_long_rows(pkg):
+    # no off-diagonal tiles at all; then a dense upper triangle (long block rows → many units)
+    for p in (0.0, 1.0):
+        n = 40 * 64
+        rc = pkg.synthetic_pattern(40, p, seed=0)
+        H = pkg.HalfTiles.synthetic(n, tile_rc=rc, max_unit=7)
+        tiles = oracle.synthetic_dense_tiles(n, rc, seed=0)
+        X = torch.randn((n, 8), generator=torch.Generator().manual_seed(2))
+        check_result(n, rc, tiles, X.numpy(), pkg.sym_spmm(H, X.cuda()).cpu().numpy(), torch.float32)
+
+
+def test_layouts_numpy_out_accumulate(pkg, c1_small):
+    n, rc, tiles = c1_small
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc)
+    Xn = np.random.default_rng(4).standard_normal((n, 8)).astype(np.float32)
+    Y_nk = pkg.sym_spmm(H, Xn)  # numpy in → numpy out
+    assert isinstance(Y_nk, np.ndarray) and Y_nk.shape == (n, 8)
+    Y_kn = pkg.sym_spmm(H, Xn.T.copy())  # reference (n_vec, n) layout
+    assert Y_kn.shape == (8, n)
+    assert np.abs(Y_kn.T - Y_nk).max() <= 1e-5 * np.abs(Y_nk).max()
+    out = torch.ones((n, 8), device="cuda")
+    pkg.sym_spmm(H, torch.from_numpy(Xn).cuda(), out=out, accumulate=True)
+    assert np.abs(out.cpu().numpy() - (Y_nk + 1.0)).max() <= 1e-4 * np.abs(Y_nk).max()
+    out2 = np.zeros((n, 8), np.float32)
+    pkg.sym_spmm(H, Xn, out=out2)
+    assert np.abs(out2 - Y_nk).max() <= 1e-5 * np.abs(Y_nk).max()
+
+
+def test_validation_raises_before_compute(pkg, c1_small):
+    n, rc, _ = c1_small
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc)
+    with pytest.raises(ValueError):
+        pkg.sym_spmm(H, torch.zeros((n, 4), dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError):
+        pkg.sym_spmm(H, torch.zeros((n + 1, 4), device="cuda"))
+    with pytest.raises(ValueError):
+        pkg.sym_spmm(H, torch.zeros((n,), device="cuda"))
+    with pytest.raises(ValueError):
+        pkg.sym_spmm(H, torch.zeros((n, 4), device="cuda"), layout="xy")
+    with pytest.raises(ValueError):
+        pkg.HalfTiles.from_coo(4, [0, 1], [1, 0], np.array([1.0, 2.0], np.float32))  # not symmetric
+    # the C-ABI itself rejects a strided X (ldx != k)
+    X = torch.zeros((H.n_pad, 16), device="cuda")[:, :8]
+    Y = torch.zeros((H.n_pad, 8), device="cuda")
+    rc_ = pkg.lib().cim_sym_spmm(H.descriptor(), X.data_ptr(), Y.data_ptr(), 8, 16, 8, 0, None)
+    assert rc_ == 1
+
+
+def test_deterministic_structure_and_repeatable_values(pkg, c1_small):
+    n, rc, _ = c1_small
+    H1 = pkg.HalfTiles.synthetic(n, tile_rc=rc)
+    H2 = pkg.HalfTiles.synthetic(n, tile_rc=rc)
+    assert torch.equal(H1.vals, H2.vals)
+    X = torch.randn((n, 8), generator=torch.Generator().manual_seed(0)).cuda()
+    Ya, Yb = pkg.sym_spmm(H1, X), pkg.sym_spmm(H1, X)
+    # float atomics: order-dependent only at the ulp level
+    assert (Ya - Yb).abs().max().item() <= 1e-5 * Ya.abs().max().item()
+
+
+def test_save_load_roundtrip(pkg, c1_small, tmp_path):
+    n, rc, _ = c1_small
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc)
+    H.save(tmp_path / "h.npz")
+    H2 = pkg.HalfTiles.load(tmp_path / "h.npz")
+    assert torch.equal(H.vals, H2.vals) and np.array_equal(H.tile_rc_host, H2.tile_rc_host)
+
+
+def test_sharded_world1_equals_direct(pkg):
+    n = 4096
+    S = pkg.ShardedSymSpmm.synthetic(n, k=8, p=0.1, seed=3)
+    rc = pkg.synthetic_pattern(64, 0.1, seed=3)
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc)
+    X = torch.randn((n, 8), generator=torch.Generator().manual_seed(0)).cuda()
+    Y = S.apply(X)
+    assert torch.allclose(Y, pkg.sym_spmm(H, X), rtol=0, atol=1e-5 * pkg.sym_spmm(H, X).abs().max().item())
+
+
+# ----------------------------------------------------------------------------
+# BASELINE config 2 at full size: size-independent properties
+# ----------------------------------------------------------------------------
+
+@pytest.mark.slow
+def test_c2_full_size_properties(pkg):
+    """n = 2²², ~2·10⁹ stored values, k = 8 f32 (8 GB in HBM).
+
+    * symmetry:  ⟨X₁, A X₂⟩ = ⟨A X₁, X₂⟩   (every tile used both ways)
+    * linearity: A(X₁ + 2X₂) = A X₁ + 2 A X₂
+    * exact block rows: block row 0 and the last block row recomputed on the
+      host from the oracle hash (row 0 has only direct tiles; the last row
+      only its diagonal tile plus transposed contributions).
+    """
+    n, k = 1 << 22, 8
+    nb = n // 64
+    n_off = 488281 - 65536
+    H = pkg.HalfTiles.synthetic(n, n_off=n_off, seed=0)
+    assert abs(H.nnz_stored - 2_000_000_000) < 2_000_000 * 2
+    g = torch.Generator(device="cuda").manual_seed(0)
+    X1 = torch.randn((n, k), device="cuda", generator=g)
+    X2 = torch.randn((n, k), device="cuda", generator=g)
+    Y1 = pkg.sym_spmm(H, X1)
+    Y2 = pkg.sym_spmm(H, X2)
+    a = (X1.double() * Y2.double()).sum(0)
+    b = (Y1.double() * X2.double()).sum(0)
+    assert torch.all((a - b).abs() <= 1e-5 * (X1.double().abs() * Y2.double().abs()).sum(0))
+    Y3 = pkg.sym_spmm(H, X1 + 2 * X2)
+    lin = (Y3 - (Y1 + 2 * Y2)).norm() / (Y3.norm())
+    assert lin.item() <= 1e-5
+    rc = H.tile_rc_host
+    X1h = X1.cpu().numpy()
+    for R in (0, nb - 1):
+        sel = np.flatnonzero((rc[:, 0] == R) | (rc[:, 1] == R))
+        sub = rc[sel]
+        tiles = oracle.synthetic_dense_tiles(n, sub, seed=0).astype(np.float64)
+        yr = np.zeros((64, k))
+        for t, (r, c) in enumerate(sub):
+            if r == R:
+                yr += tiles[t] @ X1h[c * 64:(c + 1) * 64]
+            if c == R and r != R:
+                yr += tiles[t].T @ X1h[r * 64:(r + 1) * 64]
+        got = Y1[R * 64:(R + 1) * 64].cpu().numpy()
+        assert np.abs(got - yr).max() <= 1e-5 * max(1.0, np.abs(yr).max())

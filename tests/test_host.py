@@ -1,0 +1,130 @@
+"""CPU-side checks: the C-ABI library loads and exports every symbol the
+header declares; the native planner/partitioner; the synthetic pattern; the
+host fragment map agrees with the header's formula.  No GPU compute here."""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2110_10765_b200 as pkg
+from paper_2110_10765_b200 import _lib
+from paper_2110_10765_b200.halftiles import fragment_pack_host
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def header_symbols():
+    text = (ROOT / "include" / "cim_b200.h").read_text()
+    return sorted(set(re.findall(r"CIM_API\s+[\w\s\*]*?\b(cim_\w+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = pkg.lib()
+    syms = header_symbols()
+    assert len(syms) >= 10
+    for s in syms:
+        assert hasattr(L, s), s
+    assert set(syms) == set(_lib.EXPORTS)
+    assert b"sm_100a" in L.cim_version()
+
+
+def test_library_is_built_for_sm100a():
+    import subprocess
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", str(_lib.LIB_PATH)],
+                         capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_struct_layout_matches_header():
+    assert pkg._lib.CimHalfTiles.n_tiles.offset == 16
+    assert pkg._lib.CimHalfTiles.vals.offset == 48
+    assert pkg._lib.CimHalfTiles.__sizeof__(pkg._lib.CimHalfTiles()) >= 56
+
+
+def test_supported_k_table():
+    for k in (1, 2, 4, 8, 16, 24, 32, 64):
+        assert pkg.supported_k(__import__("torch").float32, k)
+    import torch
+
+    assert not pkg.supported_k(torch.float32, 3)
+    assert pkg.padded_k(torch.float32, 3) == 4
+    assert pkg.padded_k(torch.float32, 5) == 8
+    assert pkg.padded_k(torch.float64, 6) == 8
+    assert pkg.padded_k(torch.float64, 12) == 12
+
+
+class TestPlanUnits:
+    def test_units_cover_rows_and_respect_max(self):
+        rc = pkg.synthetic_pattern(300, 0.2, seed=1)
+        u = pkg.plan_units(rc, 300, max_unit=5)
+        assert u[0, 1] == 0 and u[-1, 2] == rc.shape[0]
+        assert np.all(u[1:, 1] == u[:-1, 2])
+        assert np.all(u[:, 2] - u[:, 1] <= 5) and np.all(u[:, 2] > u[:, 1])
+        for R, t0, t1, _ in u:
+            assert np.all(rc[t0:t1, 0] == R)
+
+    @pytest.mark.parametrize("bad", [
+        [[0, 0], [1, 0]],          # below the diagonal
+        [[1, 1], [0, 0]],          # rows unsorted
+        [[0, 1], [0, 1]],          # duplicate
+        [[0, 0], [0, 9]],          # column out of range
+    ])
+    def test_rejects_bad_tile_lists(self, bad):
+        with pytest.raises(ValueError):
+            pkg.plan_units(np.array(bad, np.int32), 4)
+
+    def test_partition_is_balanced_and_row_aligned(self):
+        nb = 4096
+        rc = pkg.synthetic_pattern(nb, 0.01, seed=0)
+        u = pkg.plan_units(rc, nb, max_unit=4)
+        for parts in (2, 4, 8):
+            b = pkg.partition_units(u, parts)
+            assert b[0] == 0 and b[-1] == u.shape[0] and np.all(np.diff(b) >= 0)
+            tiles = [int(u[b[q + 1] - 1, 2] - u[b[q], 1]) for q in range(parts)]
+            assert max(tiles) - min(tiles) <= 0.05 * sum(tiles) / parts + 64
+            for q in range(1, parts):
+                if 0 < b[q] < u.shape[0]:
+                    assert u[b[q], 0] != u[b[q] - 1, 0]  # rows never straddle ranks
+
+
+class TestSyntheticPattern:
+    def test_c1_tile_count(self):
+        # nb=1024, p=0.01, seed 0 → 5,244 off-diagonal tiles
+        rc = pkg.synthetic_pattern(1024, 0.01, seed=0)
+        assert rc.shape[0] == 1024 + 5244
+        assert np.all(rc[:, 0] <= rc[:, 1])
+
+    def test_large_grid_geometric_sampling(self):
+        nb = 65536
+        p = 422745 / (nb * (nb - 1) // 2)
+        rc = pkg.synthetic_pattern(nb, p, seed=0)
+        off = rc[rc[:, 0] != rc[:, 1]]
+        assert abs(off.shape[0] - 422745) < 5 * np.sqrt(422745)
+        assert np.all(off[:, 0] < off[:, 1]) and off[:, 1].max() < nb
+        key = rc[:, 0].astype(np.int64) * nb + rc[:, 1]
+        assert np.all(np.diff(key) > 0)  # sorted, unique
+        assert np.array_equal(rc, pkg.synthetic_pattern(nb, p, seed=0))
+
+
+def test_fragment_map_matches_header_formula():
+    t = np.arange(4096, dtype=np.float32).reshape(1, 64, 64)
+    f = fragment_pack_host(t)[0]
+    # vals[t][i][mb][j] = T[rg + 8i][cg + 16j], rg=(mb&31)>>2, cg=4(mb>>5)+(mb&3)
+    for i in (0, 3, 7):
+        for mb in (0, 5, 37, 127):
+            for j in range(4):
+                rg = (mb & 31) >> 2
+                cg = 4 * (mb >> 5) + (mb & 3)
+                assert f[(i * 128 + mb) * 4 + j] == t[0, rg + 8 * i, cg + 16 * j]
+    assert np.array_equal(np.sort(f), np.arange(4096, dtype=np.float32))  # a permutation
+    t64 = t.astype(np.float64)
+    f64 = fragment_pack_host(t64)[0]
+    assert np.array_equal(np.sort(f64), np.arange(4096, dtype=np.float64))
+
+
+def test_halftiles_requires_cuda_device():
+    with pytest.raises(ValueError):
+        pkg.HalfTiles.synthetic(128, p=0.5, device="cpu")
