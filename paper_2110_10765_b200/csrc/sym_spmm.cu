@@ -24,6 +24,8 @@
 // (_contract_array_clause / _contract_atomic, pipeline.py:461-488) over the
 // full COO from _collect_pairs (pipeline.py:428-458).
 #include <algorithm>
+#include <type_traits>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -139,6 +141,64 @@ __device__ __forceinline__ void tile_fma(const T *__restrict__ Ts, const T *__re
       for (int v = 0; v < KV; ++v) {
         acc_r[i][v] = fma(t[j], xc[j][v], acc_r[i][v]);
         if constexpr (!DIAG) acc_c[j][v] = fma(t[j], xr[v], acc_c[j][v]);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Packed FP32 path (sm_100 FFMA2): accumulators are register pairs holding two
+// consecutive vectors, and every FMA is  acc[v:v+2] += t · x[v:v+2]  with t a
+// broadcast scalar — one FFMA2 instruction for two FMAs, halving the issue
+// cost of the inner loop.
+// ---------------------------------------------------------------------------
+typedef unsigned long long u64;
+
+__device__ __forceinline__ u64 fma2(float t, u64 x, u64 acc) {
+  u64 tt, r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(tt) : "f"(t));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(tt), "l"(x), "l"(acc));
+  return r;
+}
+
+__device__ __forceinline__ void unpack2(u64 x, float &a, float &b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x));
+}
+
+template <int P>  // P = KV/2 pairs, 8-byte aligned source
+__device__ __forceinline__ void load_pairs(u64 (&d)[P], const float *s) {
+  if constexpr (P >= 2) {
+#pragma unroll
+    for (int q = 0; q < P / 2; ++q) {
+      const ulonglong2 v = reinterpret_cast<const ulonglong2 *>(s)[q];
+      d[2 * q] = v.x;
+      d[2 * q + 1] = v.y;
+    }
+  } else {
+    d[0] = *reinterpret_cast<const u64 *>(s);
+  }
+}
+
+template <int KV, bool DIAG>
+__device__ __forceinline__ void tile_fma2(const float *__restrict__ Ts, const float *__restrict__ XC,
+                                          const float *__restrict__ XR, int mb, int rg, int cg, int k, int v0,
+                                          u64 (&ar)[8][KV / 2], u64 (&ac)[4][KV / 2]) {
+  constexpr int P = KV / 2;
+  u64 xc[4][P];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) load_pairs<P>(xc[j], XC + (cg + 16 * j) * k + v0);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float4 t4 = reinterpret_cast<const float4 *>(Ts)[i * 128 + mb];
+    const float t[4] = {t4.x, t4.y, t4.z, t4.w};
+    u64 xr[P];
+    if constexpr (!DIAG) load_pairs<P>(xr, XR + (rg + 8 * i) * k + v0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        ar[i][q] = fma2(t[j], xc[j][q], ar[i][q]);
+        if constexpr (!DIAG) ac[j][q] = fma2(t[j], xr[q], ac[j][q]);
       }
     }
   }
@@ -289,8 +349,15 @@ __device__ __forceinline__ void reduce_rows(T (&acc)[8][KV], T *scr, int lane, i
   }
 }
 
+// CTAs per SM the register budget is tuned for: two when a thread carries at
+// most 8 vectors' worth of accumulators in total, else one.
 template <typename T, int KV, int NG>
-__global__ void __launch_bounds__(NG * kGroupThreads + 32, (NG == 1 ? 2 : 1))
+constexpr int min_ctas() {
+  return (KV * NG * (int)sizeof(T) <= 32) ? 2 : 1;
+}
+
+template <typename T, int KV, int NG>
+__global__ void __launch_bounds__(NG * kGroupThreads + 32, min_ctas<T, KV, NG>())
     sym_spmm_kernel(const SpmmParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
@@ -336,7 +403,7 @@ __global__ void __launch_bounds__(NG * kGroupThreads + 32, (NG == 1 ? 2 : 1))
         for (int q = 0; q < cnt; ++q) {
           const int C = __shfl_sync(0xffffffffu, myC, q);
           if (lane == 0) {
-            mbar_wait(&empty[stage], phase ^ 1u);
+            mbar_wait_backoff(&empty[stage], phase ^ 1u);
             unsigned char *st = stage_base + (size_t)stage * p.stage_bytes;
             const int tt = tb + q;
             const bool diag = (C == R);
@@ -358,7 +425,7 @@ __global__ void __launch_bounds__(NG * kGroupThreads + 32, (NG == 1 ? 2 : 1))
       u = __shfl_sync(0xffffffffu, u_next, 0);
     }
     if (lane == 0) {
-      mbar_wait(&empty[stage], phase ^ 1u);
+      mbar_wait_backoff(&empty[stage], phase ^ 1u);
       StageHdr *h = reinterpret_cast<StageHdr *>(stage_base + (size_t)stage * p.stage_bytes + tile_bytes + 2 * xblk);
       *h = StageHdr{0, 0, HDR_TERM, 0};
       mbar_arrive(&full[stage]);
@@ -377,12 +444,15 @@ __global__ void __launch_bounds__(NG * kGroupThreads + 32, (NG == 1 ? 2 : 1))
   T *my_scr_r = scr_r + g * 4 * 64 * KV;
   T *Y = reinterpret_cast<T *>(p.Y);
 
-  T acc_r[8][KV];
-  T acc_c[4][KV];
+  constexpr bool PACKED = (sizeof(T) == 4) && (KV % 2 == 0);
+  using AccE = typename std::conditional<PACKED, u64, T>::type;
+  constexpr int NA = PACKED ? KV / 2 : KV;  // accumulator elements per row / column
+  AccE acc_r[8][NA];
+  AccE acc_c[4][NA];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int v = 0; v < KV; ++v) acc_r[i][v] = T(0);
+    for (int v = 0; v < NA; ++v) acc_r[i][v] = AccE(0);
 
   int stage = 0;
   uint32_t phase = 0;
@@ -395,20 +465,28 @@ __global__ void __launch_bounds__(NG * kGroupThreads + 32, (NG == 1 ? 2 : 1))
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int v = 0; v < KV; ++v) acc_r[i][v] = T(0);
+        for (int v = 0; v < NA; ++v) acc_r[i][v] = AccE(0);
     }
     const T *Ts = reinterpret_cast<const T *>(st);
     const T *XC = reinterpret_cast<const T *>(st + tile_bytes);
     const T *XR = reinterpret_cast<const T *>(st + tile_bytes + xblk);
     const bool diag = h.flags & HDR_DIAG;
-    if (diag) {
-      tile_fma<T, KV, true>(Ts, XC, XR, gt, rg, cg, k, v0, acc_r, acc_c);
-    } else {
+    if (!diag) {
 #pragma unroll
       for (int j = 0; j < 4; ++j)
 #pragma unroll
-        for (int v = 0; v < KV; ++v) acc_c[j][v] = T(0);
-      tile_fma<T, KV, false>(Ts, XC, XR, gt, rg, cg, k, v0, acc_r, acc_c);
+        for (int v = 0; v < NA; ++v) acc_c[j][v] = AccE(0);
+    }
+    if constexpr (PACKED) {
+      if (diag)
+        tile_fma2<KV, true>(Ts, XC, XR, gt, rg, cg, k, v0, acc_r, acc_c);
+      else
+        tile_fma2<KV, false>(Ts, XC, XR, gt, rg, cg, k, v0, acc_r, acc_c);
+    } else {
+      if (diag)
+        tile_fma<T, KV, true>(Ts, XC, XR, gt, rg, cg, k, v0, acc_r, acc_c);
+      else
+        tile_fma<T, KV, false>(Ts, XC, XR, gt, rg, cg, k, v0, acc_r, acc_c);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
@@ -416,9 +494,34 @@ __global__ void __launch_bounds__(NG * kGroupThreads + 32, (NG == 1 ? 2 : 1))
       stage = 0;
       phase ^= 1u;
     }
-    if (!diag) reduce_cols<T, KV>(acc_c, my_scr_c, lane, w, Y + (long long)h.C * kBlock * p.ldy + v0, p.ldy);
-    if (h.flags & HDR_LAST)
-      reduce_rows<T, KV>(acc_r, my_scr_r, lane, w, rg, gt, 1 + g, Y + (long long)h.R * kBlock * p.ldy + v0, p.ldy);
+    if (!diag) {
+      T fc[4][KV];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int v = 0; v < NA; ++v) {
+          if constexpr (PACKED) {
+            unpack2(acc_c[j][v], fc[j][2 * v], fc[j][2 * v + 1]);
+          } else {
+            fc[j][v] = acc_c[j][v];
+          }
+        }
+      reduce_cols<T, KV>(fc, my_scr_c, lane, w, Y + (long long)h.C * kBlock * p.ldy + v0, p.ldy);
+    }
+    if (h.flags & HDR_LAST) {
+      T fr[8][KV];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int v = 0; v < NA; ++v) {
+          if constexpr (PACKED) {
+            unpack2(acc_r[i][v], fr[i][2 * v], fr[i][2 * v + 1]);
+          } else {
+            fr[i][v] = acc_r[i][v];
+          }
+        }
+      reduce_rows<T, KV>(fr, my_scr_r, lane, w, rg, gt, 1 + g, Y + (long long)h.R * kBlock * p.ldy + v0, p.ldy);
+    }
   }
 }
 
@@ -468,7 +571,24 @@ struct LaunchCfg {
   int KV, NG, passes;
 };
 
+bool pick_cfg_default(int dtype, int k, LaunchCfg &c);
+
+// CIM_SPLIT=<KV>x<NG> forces a vector split when that variant is compiled
+// (tuning experiments only; the default table below is what ships).
 bool pick_cfg(int dtype, int k, LaunchCfg &c) {
+  if (!pick_cfg_default(dtype, k, c)) return false;
+  if (const char *e = getenv("CIM_SPLIT")) {
+    int kv = 0, ng = 0;
+    if (sscanf(e, "%dx%d", &kv, &ng) == 2 && kv > 0 && ng > 0 && k % (kv * ng) == 0) {
+      c.KV = kv;
+      c.NG = ng;
+      c.passes = k / (kv * ng);
+    }
+  }
+  return true;
+}
+
+bool pick_cfg_default(int dtype, int k, LaunchCfg &c) {
   if (k < 1 || k > 64) return false;
   if (dtype == CIM_F32) {
     if (k == 1 || k == 2 || k == 4) {
@@ -508,7 +628,7 @@ int launch_kernel(const cim_half_tiles *H, const void *X, void *Y, int k, long l
   const unsigned int xblk = (unsigned int)(kBlock * k * sizeof(T));
   const unsigned int stage_bytes = (tile_bytes + 2 * xblk + sizeof(StageHdr) + 127u) & ~127u;
   const size_t scratch = (size_t)NG * 4 * 32 * 4 * KV * sizeof(T) + (size_t)NG * 4 * 64 * KV * sizeof(T);
-  const int ctas_per_sm = (NG == 1) ? 2 : 1;
+  const int ctas_per_sm = min_ctas<T, KV, NG>();
   const size_t budget = (size_t)(227 * 1024) / ctas_per_sm - (ctas_per_sm > 1 ? 1024 : 0);
   if (budget < scratch + 128 + 2 * (size_t)stage_bytes) return set_error(CIM_EUNSUPPORTED, "k too large for smem");
   int S = (int)((budget - scratch - 128) / stage_bytes);
@@ -611,6 +731,8 @@ extern "C" int cim_sym_spmm(const cim_half_tiles *H, const void *X, void *Y, int
       case 11: return launch_kernel<float, 1, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
       case 21: return launch_kernel<float, 2, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
       case 41: return launch_kernel<float, 4, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+      case 42: return launch_kernel<float, 4, 2>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+      case 24: return launch_kernel<float, 2, 4>(H, X, Y, k, ldy, cfg.passes, stream, ds);
       case 81: return launch_kernel<float, 8, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
       case 82: return launch_kernel<float, 8, 2>(H, X, Y, k, ldy, cfg.passes, stream, ds);
     }
