@@ -161,6 +161,18 @@ __device__ __forceinline__ u64 fma2(float t, u64 x, u64 acc) {
   return r;
 }
 
+__device__ __forceinline__ u64 pack2(float a, float b) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+  u64 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
 __device__ __forceinline__ void unpack2(u64 x, float &a, float &b) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x));
 }
@@ -252,20 +264,42 @@ __device__ __forceinline__ void reduce_cols(T (&acc)[4][KV], T *scr, int lane, i
   if (lane < 4 * NCH) {
     const int cg_lo = lane & 3, q = lane >> 2;
     T s[C];
+    V part[8];
 #pragma unroll
-    for (int x = 0; x < C; ++x) s[x] = T(0);
+    for (int rg = 0; rg < 8; ++rg) part[rg] = sv[q * 32 + ((rg * 4 + cg_lo) ^ ((q & 1) << 2))];
+    if constexpr (C == 4) {
+      // pairwise tree of packed adds: 3 levels × 2 FADD2 instead of 28 FADD
+      u64 lo[8], hi[8];
 #pragma unroll
-    for (int rg = 0; rg < 8; ++rg) {
-      const V v = sv[q * 32 + ((rg * 4 + cg_lo) ^ ((q & 1) << 2))];
-      if constexpr (C == 4) {
-        s[0] += v.x;
-        s[1] += v.y;
-        s[2] += v.z;
-        s[3] += v.w;
-      } else {
-        s[0] += v.x;
-        s[1] += v.y;
+      for (int r = 0; r < 8; ++r) {
+        lo[r] = pack2(part[r].x, part[r].y);
+        hi[r] = pack2(part[r].z, part[r].w);
       }
+#pragma unroll
+      for (int w2 = 4; w2 >= 1; w2 >>= 1)
+#pragma unroll
+        for (int r = 0; r < w2; ++r) {
+          lo[r] = add2(lo[r], lo[r + w2]);
+          hi[r] = add2(hi[r], hi[r + w2]);
+        }
+      unpack2(lo[0], s[0], s[1]);
+      unpack2(hi[0], s[2], s[3]);
+    } else {
+      T a[8], b[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        a[r] = part[r].x;
+        b[r] = part[r].y;
+      }
+#pragma unroll
+      for (int w2 = 4; w2 >= 1; w2 >>= 1)
+#pragma unroll
+        for (int r = 0; r < w2; ++r) {
+          a[r] += a[r + w2];
+          b[r] += b[r + w2];
+        }
+      s[0] = a[0];
+      s[1] = b[0];
     }
     // flat element e = j·KV + v ; column = cg + 16·j
     const int cg = w * 4 + cg_lo;
