@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--k", type=int, default=K_DEFAULT)
     ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--layout", default=None, choices=["tc", "frag"],
+                    help="tile layout/kernel: frag = CUDA-core FFMA2 (default), tc = tcgen05 3xTF32 split")
     ap.add_argument("--n", type=int, default=N_BASE)
     ap.add_argument("--tiles-per-gpu", type=int, default=TILES_PER_GPU)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -235,7 +237,7 @@ def impl_ours(args):
     n, nb, n_off, p = workload(args, world)
 
     t_build = time.perf_counter()
-    S = ShardedSymSpmm.synthetic(n, k=k, p=p, seed=0, dtype=dtype, device=dev)
+    S = ShardedSymSpmm.synthetic(n, k=k, p=p, seed=0, dtype=dtype, device=dev, layout=args.layout)
     H = S.H
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t_build
@@ -383,6 +385,7 @@ def impl_ours(args):
                   f"k={k}, values h(i XOR j; 0) on device, X ~ N(0,1)",
                 "n": n, "k": k, "stored_tiles": g_tiles, "stored_nnz": g_tiles * 4096,
                 "parallelism": f"row-block shard x{world}" if world > 1 else "single GPU",
+                "layout": H.layout,
                 "l2": "inputs (8.3 GB per GPU) far larger than L2 (126 MB): no flush",
                 "gflop_per_apply": flops_global / 1e9,
                 "hbm_gbs_kernel": achieved,
@@ -390,13 +393,14 @@ def impl_ours(args):
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
-                         "kernel": "sym_spmm_kernel", "kernel_ms": kern_max,
+                         "kernel": "sym_spmm_tc_kernel (tcgen05 kind::tf32, 3xTF32 split)" if H.layout == "tc"
+                         else "sym_spmm_kernel (FFMA2)", "kernel_ms": kern_max,
                          "algorithmic_bytes_per_launch": bytes_local,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6650",
                          "frac_of_8TBs_spec": achieved / 8000.0},
             "cpu_baseline": cpu_b,
             "e2e": {"value": e2e_val, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-            "gpu_launches": args.steps * (1 if k <= 8 else max(1, k // 16)),
+            "gpu_launches": args.steps * (max(1, -(-S.k // 16)) if H.layout == "tc" else (1 if k <= 8 else max(1, k // 16))),
             "clocks": clocks.summary(),
         }
         print(json.dumps(line))

@@ -76,6 +76,12 @@ extern "C" {
 
 #define CIM_BLOCK 64
 
+/* tile value layouts (cim_half_tiles.layout) */
+#define CIM_LAYOUT_FRAG 0   /* fragment order v1: CUDA-core FFMA/FFMA2 kernel (f32, f64)   */
+#define CIM_LAYOUT_TC   1   /* tcgen05 TF32 operand layout (f32 only): per tile,
+                               byte(r,c) = (c/32)·8192 + (r/4)·512 + s((r%4)·128 + (c%32)·4),
+                               s(x) = x ^ (((x >> 7) & 3) << 5)  (SWIZZLE_128B_BASE32B)      */
+
 typedef struct cim_half_tiles {
   int64_t        n;        /* matrix order                                   */
   int32_t        block;    /* must be 64                                     */
@@ -84,7 +90,9 @@ typedef struct cim_half_tiles {
   int64_t        n_units;
   const int32_t *tile_rc;  /* device, [n_tiles][2]                           */
   const int32_t *units;    /* device, [n_units][4]                           */
-  const void    *vals;     /* device, [n_tiles][4096] fragment order         */
+  const void    *vals;     /* device, [n_tiles][4096] in `layout` order      */
+  int32_t        layout;   /* CIM_LAYOUT_FRAG | CIM_LAYOUT_TC                 */
+  int32_t        reserved; /* 0                                               */
 } cim_half_tiles;
 
 /* Library version / build string (host). */
@@ -106,8 +114,12 @@ CIM_API const char *cim_last_error(void);
 CIM_API int cim_sym_spmm(const cim_half_tiles *H, const void *X, void *Y, int32_t k,
                  int64_t ldx, int64_t ldy, uint32_t flags, void *stream);
 
-/* 1 if (dtype, k) has a compiled kernel, else 0. */
+/* 1 if (dtype, k) has a compiled kernel for CIM_LAYOUT_FRAG tiles, else 0. */
 CIM_API int cim_sym_spmm_supported(int32_t dtype, int32_t k);
+
+/* 1 if (layout, dtype, k) has a compiled kernel, else 0.  CIM_LAYOUT_TC:
+ * f32 with k ∈ {8, 16} (tcgen05 kind::tf32, 3×TF32-split FP32 accuracy). */
+CIM_API int cim_layout_supports(int32_t layout, int32_t dtype, int32_t k);
 
 /*
  * Host: build work units from a sorted tile list (R, C pairs, host memory).
@@ -136,7 +148,7 @@ CIM_API int cim_partition_units(const int32_t *units_host, int64_t n_units,
  * Entries with i ≥ n or j ≥ n are 0.
  */
 CIM_API int cim_fill_synthetic_values(const int32_t *tile_rc, int64_t n_tiles, int64_t n,
-                              int32_t dtype, int32_t kind, uint64_t seed,
+                              int32_t dtype, int32_t layout, int32_t kind, uint64_t seed,
                               int32_t op_k, void *vals, void *stream);
 
 /*
@@ -146,7 +158,7 @@ CIM_API int cim_fill_synthetic_values(const int32_t *tile_rc, int64_t n_tiles, i
  * interacting pairs, for the GPU contract_observables.
  */
 CIM_API int cim_fill_masked_values(const int32_t *tile_rc, int64_t n_tiles, int64_t n,
-                                   int32_t dtype, int32_t kind, uint64_t seed,
+                                   int32_t dtype, int32_t layout, int32_t kind, uint64_t seed,
                                    int32_t op_k, const void *mask, void *vals,
                                    void *stream);
 
@@ -156,11 +168,11 @@ CIM_API int cim_fill_masked_values(const int32_t *tile_rc, int64_t n_tiles, int6
  * (SURVEY.md §7 step 4).
  */
 CIM_API int cim_pack_tiles(const void *src_rowmajor, int64_t n_tiles, int32_t dtype,
-                   void *dst_fragment, void *stream);
+                   int32_t layout, void *dst_fragment, void *stream);
 
 /* Device: inverse of cim_pack_tiles (debug / export). */
 CIM_API int cim_unpack_tiles(const void *src_fragment, int64_t n_tiles, int32_t dtype,
-                     void *dst_rowmajor, void *stream);
+                     int32_t layout, void *dst_rowmajor, void *stream);
 
 /*
  * Device: the reference's value hashes on explicit index arrays, for parity

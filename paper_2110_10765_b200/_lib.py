@@ -17,6 +17,7 @@ CIM_OK, CIM_EINVAL, CIM_ECUDA, CIM_EUNSUPPORTED = 0, 1, 2, 3
 CIM_F32, CIM_F64 = 0, 1
 CIM_ACCUMULATE = 1
 CIM_VALUES_H_XOR, CIM_VALUES_OP_HASH, CIM_VALUES_IDENTITY = 0, 1, 2
+CIM_LAYOUT_FRAG, CIM_LAYOUT_TC = 0, 1
 BLOCK = 64
 
 EXPORTS = (
@@ -24,6 +25,7 @@ EXPORTS = (
     "cim_last_error",
     "cim_sym_spmm",
     "cim_sym_spmm_supported",
+    "cim_layout_supports",
     "cim_plan_units",
     "cim_partition_units",
     "cim_fill_synthetic_values",
@@ -46,6 +48,8 @@ class CimHalfTiles(ctypes.Structure):
         ("tile_rc", ctypes.c_void_p),
         ("units", ctypes.c_void_p),
         ("vals", ctypes.c_void_p),
+        ("layout", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 
@@ -74,14 +78,15 @@ def lib() -> ctypes.CDLL:
     L.cim_sym_spmm.argtypes = [c.POINTER(CimHalfTiles), c.c_void_p, c.c_void_p, c.c_int32, c.c_int64,
                                c.c_int64, c.c_uint32, c.c_void_p]
     L.cim_sym_spmm_supported.argtypes = [c.c_int32, c.c_int32]
+    L.cim_layout_supports.argtypes = [c.c_int32, c.c_int32, c.c_int32]
     L.cim_plan_units.argtypes = [c.c_void_p, c.c_int64, c.c_int64, c.c_int32, c.c_void_p, c.POINTER(c.c_int64)]
     L.cim_partition_units.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_void_p]
-    L.cim_fill_synthetic_values.argtypes = [c.c_void_p, c.c_int64, c.c_int64, c.c_int32, c.c_int32, c.c_uint64,
-                                            c.c_int32, c.c_void_p, c.c_void_p]
-    L.cim_fill_masked_values.argtypes = [c.c_void_p, c.c_int64, c.c_int64, c.c_int32, c.c_int32, c.c_uint64,
-                                         c.c_int32, c.c_void_p, c.c_void_p, c.c_void_p]
-    L.cim_pack_tiles.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_void_p, c.c_void_p]
-    L.cim_unpack_tiles.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_void_p, c.c_void_p]
+    L.cim_fill_synthetic_values.argtypes = [c.c_void_p, c.c_int64, c.c_int64, c.c_int32, c.c_int32, c.c_int32,
+                                            c.c_uint64, c.c_int32, c.c_void_p, c.c_void_p]
+    L.cim_fill_masked_values.argtypes = [c.c_void_p, c.c_int64, c.c_int64, c.c_int32, c.c_int32, c.c_int32,
+                                         c.c_uint64, c.c_int32, c.c_void_p, c.c_void_p, c.c_void_p]
+    L.cim_pack_tiles.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_int32, c.c_void_p, c.c_void_p]
+    L.cim_unpack_tiles.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_int32, c.c_void_p, c.c_void_p]
     L.cim_hash_values.argtypes = [c.c_void_p, c.c_void_p, c.c_int64, c.c_int32, c.c_uint64, c.c_int32,
                                   c.c_void_p, c.c_void_p]
     for name in EXPORTS:

@@ -31,6 +31,25 @@ __host__ __device__ __forceinline__ void frag_index_to_rc(int idx, int &row, int
   }
 }
 
+// TC layout (CIM_LAYOUT_TC, f32): element index → (row, col); the inverse of
+// byte(r,c) = (c/32)·8192 + (r/4)·512 + s((r%4)·128 + (c%32)·4).
+__host__ __device__ __forceinline__ void tc_index_to_rc(int idx, int &row, int &col) {
+  const unsigned b = (unsigned)idx * 4u;
+  const unsigned cb = b >> 13, rem = b & 8191u;
+  unsigned in = rem & 511u;
+  in ^= ((in >> 7) & 3u) << 5;
+  row = (int)((rem >> 9) * 4u + (in >> 7));
+  col = (int)(cb * 32u + ((in & 127u) >> 2));
+}
+
+template <typename T>
+__host__ __device__ __forceinline__ void layout_index_to_rc(int layout, int idx, int &row, int &col) {
+  if (sizeof(T) == 4 && layout == 1)
+    tc_index_to_rc(idx, row, col);
+  else
+    frag_index_to_rc<T>(idx, row, col);
+}
+
 // ---------------------------------------------------------------------------
 // Reference value hashes, bit-exact twins of pipeline.py:199-263.
 // ---------------------------------------------------------------------------

@@ -721,9 +721,20 @@ int launch_kernel(const cim_half_tiles *H, const void *X, void *Y, int k, long l
 
 using namespace cim;
 
+namespace cim {
+int sym_spmm_tc_dispatch(const cim_half_tiles *H, const void *X, void *Y, int k, long long ldy, cudaStream_t stream,
+                         int sms, unsigned int *counter);
+}
+
 extern "C" int cim_sym_spmm_supported(int32_t dtype, int32_t k) {
   LaunchCfg c;
   return pick_cfg(dtype, k, c) ? 1 : 0;
+}
+
+extern "C" int cim_layout_supports(int32_t layout, int32_t dtype, int32_t k) {
+  if (layout == CIM_LAYOUT_FRAG) return cim_sym_spmm_supported(dtype, k);
+  if (layout == CIM_LAYOUT_TC) return (dtype == CIM_F32 && (k == 8 || k == 16)) ? 1 : 0;
+  return 0;
 }
 
 extern "C" int cim_sym_spmm(const cim_half_tiles *H, const void *X, void *Y, int32_t k, int64_t ldx, int64_t ldy,
@@ -744,8 +755,10 @@ extern "C" int cim_sym_spmm(const cim_half_tiles *H, const void *X, void *Y, int
       (reinterpret_cast<uintptr_t>(H->vals) & 15))
     return set_error(CIM_EINVAL, "X, Y and vals must be 16-byte aligned");
   if ((ldy * (int64_t)es) % 16 != 0 && k * es >= 16) return set_error(CIM_EINVAL, "ldy*sizeof(T) must be a multiple of 16");
-  LaunchCfg cfg;
-  if (!pick_cfg(H->dtype, k, cfg)) return set_error(CIM_EUNSUPPORTED, "unsupported (dtype, k)");
+  if (H->layout != CIM_LAYOUT_FRAG && H->layout != CIM_LAYOUT_TC) return set_error(CIM_EINVAL, "unknown tile layout");
+  if (!cim_layout_supports(H->layout, H->dtype, k)) return set_error(CIM_EUNSUPPORTED, "unsupported (layout, dtype, k)");
+  LaunchCfg cfg{};
+  if (H->layout == CIM_LAYOUT_FRAG) pick_cfg(H->dtype, k, cfg);
 
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   DeviceState *ds = nullptr;
@@ -759,6 +772,11 @@ extern "C" int cim_sym_spmm(const cim_half_tiles *H, const void *X, void *Y, int
     if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("zeroing Y: ") + cudaGetErrorString(e));
   }
   if (H->n_tiles == 0 || H->n_units == 0) return CIM_OK;
+
+  if (H->layout == CIM_LAYOUT_TC) {
+    if ((reinterpret_cast<uintptr_t>(Y) & 15) || (ldy % 4)) return set_error(CIM_EINVAL, "TC path needs 16-B aligned Y rows");
+    return sym_spmm_tc_dispatch(H, X, Y, k, ldy, stream, ds->sms, take_counters(ds, 1));
+  }
 
   if (H->dtype == CIM_F32) {
     switch (cfg.KV * 10 + cfg.NG) {

@@ -14,7 +14,7 @@
 namespace cim {
 
 template <typename T>
-__global__ void fill_values_kernel(const int2 *__restrict__ rc, long long n_tiles, long long n, int kind,
+__global__ void fill_values_kernel(const int2 *__restrict__ rc, long long n_tiles, long long n, int layout, int kind,
                                    unsigned long long seed, int op_k, T *__restrict__ vals) {
   const long long total = n_tiles * kTileElems;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
@@ -22,7 +22,7 @@ __global__ void fill_values_kernel(const int2 *__restrict__ rc, long long n_tile
     const long long t = e >> 12;
     const int idx = (int)(e & 4095);
     int row, col;
-    frag_index_to_rc<T>(idx, row, col);
+    layout_index_to_rc<T>(layout, idx, row, col);
     const int2 RC = rc[t];
     const long long i = (long long)RC.x * kBlock + row;
     const long long j = (long long)RC.y * kBlock + col;
@@ -34,7 +34,7 @@ __global__ void fill_values_kernel(const int2 *__restrict__ rc, long long n_tile
 
 // vals = (mask != 0) ? value(i, j) : 0 — operator values on a stored pattern.
 template <typename T>
-__global__ void fill_masked_kernel(const int2 *__restrict__ rc, long long n_tiles, long long n, int kind,
+__global__ void fill_masked_kernel(const int2 *__restrict__ rc, long long n_tiles, long long n, int layout, int kind,
                                    unsigned long long seed, int op_k, const T *__restrict__ mask,
                                    T *__restrict__ vals) {
   const long long total = n_tiles * kTileElems;
@@ -43,7 +43,7 @@ __global__ void fill_masked_kernel(const int2 *__restrict__ rc, long long n_tile
     const long long t = e >> 12;
     const int idx = (int)(e & 4095);
     int row, col;
-    frag_index_to_rc<T>(idx, row, col);
+    layout_index_to_rc<T>(layout, idx, row, col);
     const int2 RC = rc[t];
     const long long i = (long long)RC.x * kBlock + row;
     const long long j = (long long)RC.y * kBlock + col;
@@ -54,14 +54,15 @@ __global__ void fill_masked_kernel(const int2 *__restrict__ rc, long long n_tile
 }
 
 template <typename T>
-__global__ void pack_kernel(const T *__restrict__ src, long long n_tiles, T *__restrict__ dst, bool to_fragment) {
+__global__ void pack_kernel(const T *__restrict__ src, long long n_tiles, int layout, T *__restrict__ dst,
+                            bool to_fragment) {
   const long long total = n_tiles * kTileElems;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const long long t = e >> 12;
     const int idx = (int)(e & 4095);
     int row, col;
-    frag_index_to_rc<T>(idx, row, col);
+    layout_index_to_rc<T>(layout, idx, row, col);
     const long long rm = (t << 12) + row * kBlock + col;
     if (to_fragment)
       dst[e] = src[rm];
@@ -94,71 +95,82 @@ int check_launch(const char *what) {
 
 using namespace cim;
 
+static bool layout_ok(int32_t layout, int32_t dtype) {
+  return layout == CIM_LAYOUT_FRAG || (layout == CIM_LAYOUT_TC && dtype == CIM_F32);
+}
+
 extern "C" int cim_fill_synthetic_values(const int32_t *tile_rc, int64_t n_tiles, int64_t n, int32_t dtype,
-                                         int32_t kind, uint64_t seed, int32_t op_k, void *vals, void *stream) {
+                                         int32_t layout, int32_t kind, uint64_t seed, int32_t op_k, void *vals,
+                                         void *stream) {
   clear_error();
   if (n_tiles < 0 || n < 1 || kind < 0 || kind > 2) return set_error(CIM_EINVAL, "bad arguments");
+  if (!layout_ok(layout, dtype)) return set_error(CIM_EINVAL, "bad layout for dtype");
   if (n_tiles == 0) return CIM_OK;
   if (!tile_rc || !vals) return set_error(CIM_EINVAL, "NULL arrays");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const long long total = n_tiles * (long long)kTileElems;
   if (dtype == CIM_F32)
     fill_values_kernel<float><<<grid_for(total), 256, 0, st>>>(reinterpret_cast<const int2 *>(tile_rc), n_tiles, n,
-                                                               kind, seed, op_k, static_cast<float *>(vals));
+                                                               layout, kind, seed, op_k, static_cast<float *>(vals));
   else if (dtype == CIM_F64)
     fill_values_kernel<double><<<grid_for(total), 256, 0, st>>>(reinterpret_cast<const int2 *>(tile_rc), n_tiles, n,
-                                                                kind, seed, op_k, static_cast<double *>(vals));
+                                                                layout, kind, seed, op_k, static_cast<double *>(vals));
   else
     return set_error(CIM_EINVAL, "bad dtype");
   return check_launch("fill_values_kernel");
 }
 
 extern "C" int cim_fill_masked_values(const int32_t *tile_rc, int64_t n_tiles, int64_t n, int32_t dtype,
-                                      int32_t kind, uint64_t seed, int32_t op_k, const void *mask, void *vals,
-                                      void *stream) {
+                                      int32_t layout, int32_t kind, uint64_t seed, int32_t op_k, const void *mask,
+                                      void *vals, void *stream) {
   clear_error();
   if (n_tiles < 0 || n < 1 || kind < 0 || kind > 2) return set_error(CIM_EINVAL, "bad arguments");
+  if (!layout_ok(layout, dtype)) return set_error(CIM_EINVAL, "bad layout for dtype");
   if (n_tiles == 0) return CIM_OK;
   if (!tile_rc || !vals || !mask) return set_error(CIM_EINVAL, "NULL arrays");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const long long total = n_tiles * (long long)kTileElems;
   if (dtype == CIM_F32)
     fill_masked_kernel<float><<<grid_for(total), 256, 0, st>>>(reinterpret_cast<const int2 *>(tile_rc), n_tiles, n,
-                                                               kind, seed, op_k, static_cast<const float *>(mask),
+                                                               layout, kind, seed, op_k, static_cast<const float *>(mask),
                                                                static_cast<float *>(vals));
   else if (dtype == CIM_F64)
     fill_masked_kernel<double><<<grid_for(total), 256, 0, st>>>(reinterpret_cast<const int2 *>(tile_rc), n_tiles,
-                                                                n, kind, seed, op_k, static_cast<const double *>(mask),
+                                                                n, layout, kind, seed, op_k, static_cast<const double *>(mask),
                                                                 static_cast<double *>(vals));
   else
     return set_error(CIM_EINVAL, "bad dtype");
   return check_launch("fill_masked_kernel");
 }
 
-static int pack_common(const void *src, int64_t n_tiles, int32_t dtype, void *dst, void *stream, bool to_frag) {
+static int pack_common(const void *src, int64_t n_tiles, int32_t dtype, int32_t layout, void *dst, void *stream,
+                       bool to_frag) {
   clear_error();
   if (n_tiles < 0) return set_error(CIM_EINVAL, "bad n_tiles");
+  if (!layout_ok(layout, dtype)) return set_error(CIM_EINVAL, "bad layout for dtype");
   if (n_tiles == 0) return CIM_OK;
   if (!src || !dst) return set_error(CIM_EINVAL, "NULL arrays");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const long long total = n_tiles * (long long)kTileElems;
   if (dtype == CIM_F32)
-    pack_kernel<float><<<grid_for(total), 256, 0, st>>>(static_cast<const float *>(src), n_tiles,
+    pack_kernel<float><<<grid_for(total), 256, 0, st>>>(static_cast<const float *>(src), n_tiles, layout,
                                                         static_cast<float *>(dst), to_frag);
   else if (dtype == CIM_F64)
-    pack_kernel<double><<<grid_for(total), 256, 0, st>>>(static_cast<const double *>(src), n_tiles,
+    pack_kernel<double><<<grid_for(total), 256, 0, st>>>(static_cast<const double *>(src), n_tiles, layout,
                                                          static_cast<double *>(dst), to_frag);
   else
     return set_error(CIM_EINVAL, "bad dtype");
   return check_launch("pack_kernel");
 }
 
-extern "C" int cim_pack_tiles(const void *src, int64_t n_tiles, int32_t dtype, void *dst, void *stream) {
-  return pack_common(src, n_tiles, dtype, dst, stream, true);
+extern "C" int cim_pack_tiles(const void *src, int64_t n_tiles, int32_t dtype, int32_t layout, void *dst,
+                              void *stream) {
+  return pack_common(src, n_tiles, dtype, layout, dst, stream, true);
 }
 
-extern "C" int cim_unpack_tiles(const void *src, int64_t n_tiles, int32_t dtype, void *dst, void *stream) {
-  return pack_common(src, n_tiles, dtype, dst, stream, false);
+extern "C" int cim_unpack_tiles(const void *src, int64_t n_tiles, int32_t dtype, int32_t layout, void *dst,
+                                void *stream) {
+  return pack_common(src, n_tiles, dtype, layout, dst, stream, false);
 }
 
 extern "C" int cim_hash_values(const int64_t *i, const int64_t *j, int64_t count, int32_t kind, uint64_t seed,

@@ -29,9 +29,20 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import BLOCK, CIM_F32, CIM_F64, CimHalfTiles, check, lib
+from ._lib import BLOCK, CIM_F32, CIM_F64, CIM_LAYOUT_FRAG, CIM_LAYOUT_TC, CimHalfTiles, check, lib
 
 DEFAULT_MAX_UNIT = 32
+LAYOUTS = {"frag": CIM_LAYOUT_FRAG, "tc": CIM_LAYOUT_TC}
+
+
+def default_layout(dtype) -> str:
+    """The fragment layout (CUDA-core FFMA2 kernel) for f32 and f64: measured
+    faster than the tcgen05 3xTF32 path on the BASELINE configs this round
+    (profiles/r01/SUMMARY.md); ``layout="tc"`` selects the tensor-core path."""
+    _as_torch_dtype(dtype)
+    return "frag"
+
+
 VALUE_KINDS = {"h_xor": _lib.CIM_VALUES_H_XOR, "op_hash": _lib.CIM_VALUES_OP_HASH, "identity": _lib.CIM_VALUES_IDENTITY}
 
 
@@ -113,10 +124,26 @@ def synthetic_pattern(nb: int, p: float, seed: int = 0) -> np.ndarray:
     return np.ascontiguousarray(rc[order])
 
 
-def fragment_pack_host(tiles: np.ndarray) -> np.ndarray:
-    """Row-major (T,64,64) → fragment order (T,4096) on the host (numpy).
-    Same map as the device ``cim_pack_tiles``; used for host-built fixtures."""
+def tc_index_map() -> np.ndarray:
+    """For the TC layout: flat storage index e → row-major index r·64+c
+    (include/cim_b200.h CIM_LAYOUT_TC)."""
+    e = np.arange(4096)
+    b = e * 4
+    cb = b >> 13
+    rem = b & 8191
+    inn = rem & 511
+    inn = inn ^ (((inn >> 7) & 3) << 5)
+    row = (rem >> 9) * 4 + (inn >> 7)
+    col = cb * 32 + ((inn & 127) >> 2)
+    return row * BLOCK + col
+
+
+def fragment_pack_host(tiles: np.ndarray, layout: str = "frag") -> np.ndarray:
+    """Row-major (T,64,64) → storage order (T,4096) on the host (numpy).
+    Same map as the device ``cim_pack_tiles``; used to cross-check it."""
     T = tiles.shape[0]
+    if layout == "tc":
+        return np.ascontiguousarray(tiles.reshape(T, 4096)[:, tc_index_map()])
     is64 = tiles.dtype == np.float64
     idx = np.arange(4096)
     if not is64:
@@ -146,6 +173,7 @@ class HalfTiles:
     vals: torch.Tensor  # (T,4096) on device, fragment order
     tile_rc_host: np.ndarray
     units_host: np.ndarray
+    layout: str = "frag"
     meta: dict = field(default_factory=dict)
     _desc: CimHalfTiles | None = field(default=None, repr=False)
 
@@ -204,14 +232,22 @@ class HalfTiles:
                 tile_rc=self.tile_rc.data_ptr() if self.n_tiles else None,
                 units=self.units.data_ptr() if self.units.numel() else None,
                 vals=self.vals.data_ptr() if self.n_tiles else None,
+                layout=LAYOUTS[self.layout],
+                reserved=0,
             )
         return self._desc
 
     # ----------------------------------------------------------- constructors
     @classmethod
-    def _from_pattern(cls, n: int, tile_rc: np.ndarray, dtype, device, max_unit: int) -> "HalfTiles":
+    def _from_pattern(cls, n: int, tile_rc: np.ndarray, dtype, device, max_unit: int,
+                      layout: str | None = None) -> "HalfTiles":
         dtype = _as_torch_dtype(dtype)
         _dtype_code(dtype)
+        layout = layout or default_layout(dtype)
+        if layout not in LAYOUTS:
+            raise ValueError(f"unknown layout {layout!r}, expected one of {tuple(LAYOUTS)}")
+        if layout == "tc" and dtype != torch.float32:
+            raise ValueError("the tensor-core layout holds f32 tiles only")
         device = torch.device(device)
         if device.type != "cuda":
             raise ValueError("HalfTiles live in GPU memory: device must be a CUDA device")
@@ -221,12 +257,14 @@ class HalfTiles:
         t_rc = torch.from_numpy(rc).to(device)
         t_units = torch.from_numpy(units).to(device)
         vals = torch.empty((rc.shape[0], BLOCK * BLOCK), dtype=dtype, device=device)
-        return cls(n=int(n), tile_rc=t_rc, units=t_units, vals=vals, tile_rc_host=rc, units_host=units)
+        return cls(n=int(n), tile_rc=t_rc, units=t_units, vals=vals, tile_rc_host=rc, units_host=units,
+                   layout=layout)
 
     @classmethod
     def synthetic(cls, n: int, p: float | None = None, *, n_off: int | None = None, seed: int = 0,
                   value_seed: int = 0, values: str = "h_xor", op_k: int = 0, dtype=torch.float32,
-                  device="cuda", max_unit: int = DEFAULT_MAX_UNIT, tile_rc: np.ndarray | None = None) -> "HalfTiles":
+                  device="cuda", max_unit: int = DEFAULT_MAX_UNIT, tile_rc: np.ndarray | None = None,
+                  layout: str | None = None) -> "HalfTiles":
         """Synthetic half-stored matrix (BASELINE.json configs).
 
         Pattern: all diagonal tiles plus upper tiles kept with probability p
@@ -245,11 +283,12 @@ class HalfTiles:
             if not 0.0 <= p <= 1.0:
                 raise ValueError(f"p must be in [0, 1], got {p}")
             tile_rc = synthetic_pattern(nb, p, seed)
-        H = cls._from_pattern(n, tile_rc, dtype, device, max_unit)
+        H = cls._from_pattern(n, tile_rc, dtype, device, max_unit, layout)
         stream = torch.cuda.current_stream(H.device).cuda_stream
         with torch.cuda.device(H.device):
             check(lib().cim_fill_synthetic_values(H.tile_rc.data_ptr() if H.n_tiles else None, H.n_tiles, n,
-                                                  _dtype_code(H.dtype), VALUE_KINDS[values], value_seed, op_k,
+                                                  _dtype_code(H.dtype), LAYOUTS[H.layout], VALUE_KINDS[values],
+                                                  value_seed, op_k,
                                                   H.vals.data_ptr() if H.n_tiles else None, stream),
                   "cim_fill_synthetic_values")
         H.meta.update(kind="synthetic", p=p, seed=seed, value_seed=value_seed, values=values, op_k=op_k)
@@ -257,23 +296,23 @@ class HalfTiles:
 
     @classmethod
     def from_dense_tiles(cls, n: int, tile_rc: np.ndarray, tiles, *, dtype=None, device="cuda",
-                         max_unit: int = DEFAULT_MAX_UNIT) -> "HalfTiles":
+                         max_unit: int = DEFAULT_MAX_UNIT, layout: str | None = None) -> "HalfTiles":
         """From row-major dense tiles (T,64,64); repacked on the device."""
         tiles_t = torch.as_tensor(tiles)
         dtype = _as_torch_dtype(dtype if dtype is not None else tiles_t.dtype)
-        H = cls._from_pattern(n, tile_rc, dtype, device, max_unit)
+        H = cls._from_pattern(n, tile_rc, dtype, device, max_unit, layout)
         if H.n_tiles:
             src = tiles_t.to(device=H.device, dtype=dtype).reshape(H.n_tiles, BLOCK * BLOCK).contiguous()
             stream = torch.cuda.current_stream(H.device).cuda_stream
             with torch.cuda.device(H.device):
-                check(lib().cim_pack_tiles(src.data_ptr(), H.n_tiles, _dtype_code(dtype), H.vals.data_ptr(), stream),
-                      "cim_pack_tiles")
+                check(lib().cim_pack_tiles(src.data_ptr(), H.n_tiles, _dtype_code(dtype), LAYOUTS[H.layout],
+                                           H.vals.data_ptr(), stream), "cim_pack_tiles")
             torch.cuda.current_stream(H.device).synchronize()
         return H
 
     @classmethod
     def from_coo(cls, n: int, i, j, v, *, dtype=torch.float32, device="cuda", check_symmetric: bool = True,
-                 max_unit: int = DEFAULT_MAX_UNIT) -> "HalfTiles":
+                 max_unit: int = DEFAULT_MAX_UNIT, layout: str | None = None) -> "HalfTiles":
         """From a full (both-triangle) symmetric COO, e.g. a reference skeleton.
 
         Keeps entries with ⌊i/64⌋ ≤ ⌊j/64⌋ — lossless for an exactly symmetric
@@ -303,7 +342,8 @@ class HalfTiles:
         tiles = np.zeros((uniq.size, BLOCK, BLOCK), dtype=np.float64)
         np.add.at(tiles, (inv, i % BLOCK, j % BLOCK), v.astype(np.float64))
         rc = np.stack([uniq // nb, uniq % nb], axis=1).astype(np.int32)
-        H = cls.from_dense_tiles(n, rc, tiles.astype(np_dtype), dtype=dtype, device=device, max_unit=max_unit)
+        H = cls.from_dense_tiles(n, rc, tiles.astype(np_dtype), dtype=dtype, device=device, max_unit=max_unit,
+                                 layout=layout)
         H.meta.update(kind="coo", nnz_full=int(keep.size), nnz_half=int(i.size))
         return H
 
@@ -329,19 +369,20 @@ class HalfTiles:
             stream = torch.cuda.current_stream(self.device).cuda_stream
             with torch.cuda.device(self.device):
                 check(lib().cim_unpack_tiles(self.vals.data_ptr(), self.n_tiles, _dtype_code(self.dtype),
-                                             out.data_ptr(), stream), "cim_unpack_tiles")
+                                             LAYOUTS[self.layout], out.data_ptr(), stream), "cim_unpack_tiles")
         return out
 
     def save(self, path) -> None:
         """npz interchange: n, tile_rc, row-major tiles (host)."""
         np.savez_compressed(path, n=self.n, tile_rc=self.tile_rc_host, tiles=self.dense_tiles().cpu().numpy(),
-                            format="cim_half_tiles_v1")
+                            format="cim_half_tiles_v1", layout=self.layout)
 
     @classmethod
     def load(cls, path, device="cuda", **kw) -> "HalfTiles":
         z = np.load(path)
         if str(z["format"]) != "cim_half_tiles_v1":
             raise ValueError(f"{path}: not a cim_half_tiles_v1 file")
+        kw.setdefault("layout", str(z["layout"]) if "layout" in z.files else None)
         return cls.from_dense_tiles(int(z["n"]), z["tile_rc"], z["tiles"], device=device, **kw)
 
     def shard(self, unit_lo: int, unit_hi: int) -> "HalfTiles":
@@ -355,5 +396,5 @@ class HalfTiles:
         units[:, 1:3] -= t0
         sub = HalfTiles(n=self.n, tile_rc=self.tile_rc[t0:t1], units=torch.from_numpy(units).to(self.device),
                         vals=self.vals[t0:t1], tile_rc_host=self.tile_rc_host[t0:t1], units_host=units,
-                        meta=dict(self.meta, shard=(unit_lo, unit_hi)))
+                        layout=self.layout, meta=dict(self.meta, shard=(unit_lo, unit_hi)))
         return sub

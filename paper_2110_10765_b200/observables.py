@@ -27,7 +27,7 @@ import numpy as np
 import torch
 
 from ._lib import check, lib
-from .halftiles import HalfTiles, _dtype_code
+from .halftiles import LAYOUTS, HalfTiles, _dtype_code
 from .spmm import sym_spmm
 
 STRATEGIES = ("array_clause", "atomic_per_element", "generated_scalars")  # reduce.py:62
@@ -82,11 +82,11 @@ def operator_tiles(pattern: HalfTiles, op_kind: str, k: int, seed: int) -> HalfT
     with torch.cuda.device(pattern.device):
         check(lib().cim_fill_masked_values(
             pattern.tile_rc.data_ptr() if pattern.n_tiles else None, pattern.n_tiles, pattern.n,
-            _dtype_code(pattern.dtype), _OP_CODES[op_kind], seed, k,
+            _dtype_code(pattern.dtype), LAYOUTS[pattern.layout], _OP_CODES[op_kind], seed, k,
             pattern.vals.data_ptr() if pattern.n_tiles else None, vals.data_ptr() if pattern.n_tiles else None,
             stream), "cim_fill_masked_values")
     return HalfTiles(n=pattern.n, tile_rc=pattern.tile_rc, units=pattern.units, vals=vals,
-                     tile_rc_host=pattern.tile_rc_host, units_host=pattern.units_host,
+                     tile_rc_host=pattern.tile_rc_host, units_host=pattern.units_host, layout=pattern.layout,
                      meta=dict(pattern.meta, op_kind=op_kind, op_k=k, op_seed=seed))
 
 

@@ -25,15 +25,23 @@ from .halftiles import HalfTiles
 LAYOUTS = ("auto", "nk", "kn")
 
 
-def supported_k(dtype: torch.dtype, k: int) -> bool:
+def supported_k(dtype: torch.dtype, k: int, layout: str = "frag") -> bool:
+    from .halftiles import LAYOUTS
+
     code = 0 if dtype == torch.float32 else 1
-    return bool(lib().cim_sym_spmm_supported(code, int(k)))
+    return bool(lib().cim_layout_supports(LAYOUTS[layout], code, int(k)))
 
 
-def padded_k(dtype: torch.dtype, k: int) -> int:
-    """Smallest compiled vector count ≥ k (extra columns are zero)."""
+TC_MAX_K = 16  # vectors per tensor-core pass (N = 2k ≤ 32 TMEM columns per accumulator)
+
+
+def padded_k(dtype: torch.dtype, k: int, layout: str = "frag") -> int:
+    """Smallest compiled vector count ≥ k for the layout (extra columns are zero).
+    The tensor-core layout runs k > 16 as passes of 16 vectors."""
     kk = int(k)
-    while kk <= 64 and not supported_k(dtype, kk):
+    if layout == "tc" and kk > TC_MAX_K:
+        return -(-kk // TC_MAX_K) * TC_MAX_K
+    while kk <= 64 and not supported_k(dtype, kk, layout):
         kk += 1
     if kk > 64:
         raise ValueError(f"k={k} exceeds the largest compiled vector count (64); split X into column blocks")
@@ -45,6 +53,15 @@ def _launch(H: HalfTiles, Xd: torch.Tensor, Yd: torch.Tensor, accumulate: bool, 
     k = Xd.shape[1]
     s = stream if stream is not None else torch.cuda.current_stream(H.device)
     handle = s.cuda_stream if isinstance(s, torch.cuda.Stream) else int(s)
+    if H.layout == "tc" and k > TC_MAX_K:
+        # column passes of 16 vectors: each pass streams the tiles once more
+        with torch.cuda.stream(s) if isinstance(s, torch.cuda.Stream) else torch.cuda.device(H.device):
+            for c0 in range(0, k, TC_MAX_K):
+                xc = Xd[:, c0:c0 + TC_MAX_K].contiguous()
+                yc = Yd[:, c0:c0 + TC_MAX_K].contiguous() if accumulate else torch.empty_like(xc)
+                _launch(H, xc, yc, accumulate, s)
+                Yd[:, c0:c0 + TC_MAX_K].copy_(yc)
+        return
     with torch.cuda.device(H.device):
         rc = lib().cim_sym_spmm(H.descriptor(), Xd.data_ptr(), Yd.data_ptr(), k, Xd.stride(0), Yd.stride(0),
                                 CIM_ACCUMULATE if accumulate else 0, handle)
@@ -98,7 +115,7 @@ def sym_spmm(H: HalfTiles, X, out=None, *, layout: str = "auto", accumulate: boo
             raise ValueError("out dtype must match the matrix dtype")
 
     dev = H.device
-    kk = padded_k(H.dtype, k)
+    kk = padded_k(H.dtype, k, H.layout)
     Xd = Xt.to(dev, non_blocking=True)
     if layout == "kn":
         Xd = Xd.t()

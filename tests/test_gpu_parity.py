@@ -68,27 +68,31 @@ def test_device_hash_matches_reference_kats(pkg):
             assert int(f32bits(out.cpu().numpy())[0]) == c["bits"], c
 
 
-@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+F32_LAYOUTS = ["tc", "frag"]
+DT_LAYOUTS = [(torch.float32, "tc"), (torch.float32, "frag"), (torch.float64, "frag")]
+
+
+@pytest.mark.parametrize("dtype,layout", DT_LAYOUTS)
 @pytest.mark.parametrize("values,kind", [("h_xor", 0), ("op_hash", 1), ("identity", 2)])
-def test_synthetic_values_bit_exact(pkg, dtype, values, kind):
+def test_synthetic_values_bit_exact(pkg, dtype, layout, values, kind):
     n = 1000  # ragged: last block half empty
     rc = pkg.synthetic_pattern((n + 63) // 64, 0.3, seed=1)
-    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, values=values, value_seed=7, op_k=2, dtype=dtype)
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, values=values, value_seed=7, op_k=2, dtype=dtype, layout=layout)
     got = H.dense_tiles().cpu().numpy()
     want = oracle.synthetic_dense_tiles(n, rc, seed=7, kind=kind, op_k=2).astype(got.dtype)
     assert np.array_equal(got.view(np.uint8), want.view(np.uint8))
 
 
-@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
-def test_pack_matches_host_layout_and_roundtrips(pkg, dtype):
+@pytest.mark.parametrize("dtype,layout", DT_LAYOUTS)
+def test_pack_matches_host_layout_and_roundtrips(pkg, dtype, layout):
     from paper_2110_10765_b200.halftiles import fragment_pack_host
 
     rng = np.random.default_rng(3)
     npd = np.float32 if dtype == torch.float32 else np.float64
     tiles = rng.standard_normal((5, 64, 64)).astype(npd)
     rc = np.array([[0, 0], [0, 2], [1, 1], [1, 3], [2, 2]], np.int32)
-    H = pkg.HalfTiles.from_dense_tiles(4 * 64, rc, tiles, dtype=dtype)
-    assert np.array_equal(H.vals.cpu().numpy(), fragment_pack_host(tiles))
+    H = pkg.HalfTiles.from_dense_tiles(4 * 64, rc, tiles, dtype=dtype, layout=layout)
+    assert np.array_equal(H.vals.cpu().numpy(), fragment_pack_host(tiles, layout))
     assert np.array_equal(H.dense_tiles().cpu().numpy(), tiles)
 
 
@@ -97,11 +101,11 @@ def test_pack_matches_host_layout_and_roundtrips(pkg, dtype):
 # ----------------------------------------------------------------------------
 
 @pytest.mark.parametrize("name", ["skel_small.npz", "skel_n1024.npz", "skel_identity.npz"])
-@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
-def test_reference_skeleton_spmm(pkg, name, dtype):
+@pytest.mark.parametrize("dtype,layout", DT_LAYOUTS)
+def test_reference_skeleton_spmm(pkg, name, dtype, layout):
     f = load_fixture(name)
     n = int(f["n"])
-    H = pkg.HalfTiles.from_coo(n, f["i"], f["j"], f["v"], dtype=dtype)
+    H = pkg.HalfTiles.from_coo(n, f["i"], f["j"], f["v"], dtype=dtype, layout=layout)
     # structure: the stored half-tile set reproduces the reference pair set exactly
     tiles = H.dense_tiles().cpu().numpy()
     i, j, v = oracle.half_tiles_to_coo(n, H.tile_rc_host, tiles)
@@ -115,10 +119,11 @@ def test_reference_skeleton_spmm(pkg, name, dtype):
 
 
 @pytest.mark.parametrize("name", ["skel_small.npz", "skel_n1024.npz", "skel_identity.npz"])
-def test_contract_observables_matches_reference(pkg, name):
+@pytest.mark.parametrize("layout", F32_LAYOUTS)
+def test_contract_observables_matches_reference(pkg, name, layout):
     f = load_fixture(name)
     n = int(f["n"])
-    pattern = pkg.HalfTiles.from_coo(n, f["i"], f["j"], np.ones_like(f["v"]))
+    pattern = pkg.HalfTiles.from_coo(n, f["i"], f["j"], np.ones_like(f["v"]), layout=layout)
     c = f["X"].T.copy()
     inp = pkg.ObservablesInput(c=c, m_ops=int(f["m_ops"]), op_kind=str(f["op_kind"]), seed=int(f["op_seed"]))
     got = pkg.contract_observables(pattern, inp).astype(np.float64)
@@ -133,12 +138,19 @@ def test_contract_observables_matches_reference(pkg, name):
         assert np.all(np.abs(got - 1.0) <= 2.0 ** -20)
 
 
-def test_single_state_diagonal(pkg):
-    # test_pipeline.py:131-138: one state → nnz 1, value h(0,0,0)
-    H = pkg.HalfTiles.from_coo(1, [0], [0], np.array([oracle.h_values(0, 0, 0)], np.float32).reshape(1))
+@pytest.mark.parametrize("layout", F32_LAYOUTS)
+def test_single_state_diagonal(pkg, layout):
+    # test_pipeline.py:131-138: one state → nnz 1, stored value exactly h(0,0,0)
+    h0 = np.array([oracle.h_values(0, 0, 0)], np.float32).reshape(1)
+    H = pkg.HalfTiles.from_coo(1, [0], [0], h0, layout=layout)
     assert H.n_tiles == 1 and H.n == 1
+    assert H.dense_tiles()[0, 0, 0].item() == float(h0[0])
     Y = pkg.sym_spmm(H, torch.tensor([[2.0]], device="cuda"))
-    assert float(Y[0, 0]) == 2.0 * float(oracle.h_values(0, 0, 0))
+    want = 2.0 * float(h0[0])
+    if layout == "frag":
+        assert float(Y[0, 0]) == want  # one FFMA: exact
+    else:
+        assert abs(float(Y[0, 0]) - want) <= 2.0 ** -19 * abs(want)  # split-TF32 residual
 
 
 # ----------------------------------------------------------------------------
@@ -155,10 +167,11 @@ def c1_small(pkg):
     return n, rc, tiles
 
 
+@pytest.mark.parametrize("layout", F32_LAYOUTS)
 @pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 8, 16, 24, 32])
-def test_k_sweep_f32(pkg, c1_small, k):
+def test_k_sweep_f32(pkg, c1_small, k, layout):
     n, rc, tiles = c1_small
-    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=torch.float32)
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=torch.float32, layout=layout)
     X = torch.randn((n, k), generator=torch.Generator().manual_seed(k))
     Y = pkg.sym_spmm(H, X.cuda()).cpu().numpy()
     check_result(n, rc, tiles, X.numpy(), Y, torch.float32)
@@ -173,22 +186,24 @@ def test_k_sweep_f64(pkg, c1_small, k):
     check_result(n, rc, tiles.astype(np.float64), X.numpy(), Y, torch.float64)
 
 
-def test_opaque_random_symmetric_values(pkg, c1_small):
+@pytest.mark.parametrize("layout", F32_LAYOUTS)
+def test_opaque_random_symmetric_values(pkg, c1_small, layout):
     """Values with no XOR structure (op hash of (min,max)) — the kernel must
     treat tile values as opaque streamed data (SURVEY.md §7 hard parts)."""
     n, rc, _ = c1_small
-    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, values="op_hash", value_seed=99, op_k=3)
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, values="op_hash", value_seed=99, op_k=3, layout=layout)
     tiles = oracle.synthetic_dense_tiles(n, rc, seed=99, kind=1, op_k=3)
     X = torch.randn((n, 8), generator=torch.Generator().manual_seed(1))
     check_result(n, rc, tiles, X.numpy(), pkg.sym_spmm(H, X.cuda()).cpu().numpy(), torch.float32)
 
 
-def test_c1_config_vs_c_oracle(pkg):
+@pytest.mark.parametrize("layout", F32_LAYOUTS)
+def test_c1_config_vs_c_oracle(pkg, layout):
     """BASELINE config 1: n=65,536, p=0.01 (5,244 off-diagonal tiles), k=8 f32."""
     from oracle import cpu
 
     n, k = 65536, 8
-    H = pkg.HalfTiles.synthetic(n, p=0.01, seed=0)
+    H = pkg.HalfTiles.synthetic(n, p=0.01, seed=0, layout=layout)
     assert H.n_off_tiles == 5244 and H.n_diag_tiles == 1024
     rc = H.tile_rc_host
     tiles = cpu.fill_h(rc, n, 0)
@@ -203,22 +218,24 @@ def test_c1_config_vs_c_oracle(pkg):
     assert oracle.componentwise_ok(Y, Y_ref, absAX, nnz_row, U32)
 
 
+@pytest.mark.parametrize("layout", F32_LAYOUTS)
 @pytest.mark.parametrize("n", [1, 63, 64, 65, 200])
-def test_ragged_and_tiny(pkg, n):
+def test_ragged_and_tiny(pkg, n, layout):
     nb = (n + 63) // 64
     rc = pkg.synthetic_pattern(nb, 1.0, seed=0)  # every upper tile
     tiles = oracle.synthetic_dense_tiles(n, rc, seed=5)
-    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, value_seed=5)
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, value_seed=5, layout=layout)
     X = torch.randn((n, 4), generator=torch.Generator().manual_seed(n))
     check_result(n, rc, tiles, X.numpy(), pkg.sym_spmm(H, X.cuda()).cpu().numpy(), torch.float32)
 
 
-def test_diagonal_only_and_long_rows(pkg):
+@pytest.mark.parametrize("layout", F32_LAYOUTS)
+def test_diagonal_only_and_long_rows(pkg, layout):
     # no off-diagonal tiles at all; then a dense upper triangle (long block rows → many units)
     for p in (0.0, 1.0):
         n = 40 * 64
         rc = pkg.synthetic_pattern(40, p, seed=0)
-        H = pkg.HalfTiles.synthetic(n, tile_rc=rc, max_unit=7)
+        H = pkg.HalfTiles.synthetic(n, tile_rc=rc, max_unit=7, layout=layout)
         tiles = oracle.synthetic_dense_tiles(n, rc, seed=0)
         X = torch.randn((n, 8), generator=torch.Generator().manual_seed(2))
         check_result(n, rc, tiles, X.numpy(), pkg.sym_spmm(H, X.cuda()).cpu().numpy(), torch.float32)
@@ -295,7 +312,8 @@ def test_sharded_world1_equals_direct(pkg):
 # ----------------------------------------------------------------------------
 
 @pytest.mark.slow
-def test_c2_full_size_properties(pkg):
+@pytest.mark.parametrize("layout", F32_LAYOUTS)
+def test_c2_full_size_properties(pkg, layout):
     """n = 2²², ~2·10⁹ stored values, k = 8 f32 (8 GB in HBM).
 
     * symmetry:  ⟨X₁, A X₂⟩ = ⟨A X₁, X₂⟩   (every tile used both ways)
@@ -307,7 +325,7 @@ def test_c2_full_size_properties(pkg):
     n, k = 1 << 22, 8
     nb = n // 64
     n_off = 488281 - 65536
-    H = pkg.HalfTiles.synthetic(n, n_off=n_off, seed=0)
+    H = pkg.HalfTiles.synthetic(n, n_off=n_off, seed=0, layout=layout)
     assert abs(H.nnz_stored - 2_000_000_000) < 2_000_000 * 2
     g = torch.Generator(device="cuda").manual_seed(0)
     X1 = torch.randn((n, k), device="cuda", generator=g)

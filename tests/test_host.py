@@ -41,6 +41,7 @@ def test_library_is_built_for_sm100a():
 def test_struct_layout_matches_header():
     assert pkg._lib.CimHalfTiles.n_tiles.offset == 16
     assert pkg._lib.CimHalfTiles.vals.offset == 48
+    assert pkg._lib.CimHalfTiles.layout.offset == 56
     assert pkg._lib.CimHalfTiles.__sizeof__(pkg._lib.CimHalfTiles()) >= 56
 
 
@@ -54,6 +55,9 @@ def test_supported_k_table():
     assert pkg.padded_k(torch.float32, 5) == 8
     assert pkg.padded_k(torch.float64, 6) == 8
     assert pkg.padded_k(torch.float64, 12) == 12
+    assert pkg.padded_k(torch.float32, 3, "tc") == 8
+    assert pkg.padded_k(torch.float32, 9, "tc") == 16
+    assert pkg.padded_k(torch.float32, 24, "tc") == 32
 
 
 class TestPlanUnits:
@@ -107,6 +111,18 @@ class TestSyntheticPattern:
         key = rc[:, 0].astype(np.int64) * nb + rc[:, 1]
         assert np.all(np.diff(key) > 0)  # sorted, unique
         assert np.array_equal(rc, pkg.synthetic_pattern(nb, p, seed=0))
+
+
+def test_tc_map_matches_header_formula():
+    from paper_2110_10765_b200.halftiles import tc_index_map
+
+    m = tc_index_map()
+    assert np.array_equal(np.sort(m), np.arange(4096))  # a permutation
+    for r in (0, 3, 5, 63):
+        for c in (0, 7, 31, 32, 63):
+            x = (r % 4) * 128 + (c % 32) * 4
+            byte = (c // 32) * 8192 + (r // 4) * 512 + (x ^ (((x >> 7) & 3) << 5))
+            assert m[byte // 4] == r * 64 + c
 
 
 def test_fragment_map_matches_header_formula():
