@@ -11,10 +11,13 @@ C-ABI in ``libcim_b200.so``, include/cim_b200.h):
                           reduce-scatter Y)
 * ``contract_observables``, ``ObservablesInput``, ``random_coefficients``,
   ``STRATEGIES``, ``OP_KINDS`` — the reference's observables API on the GPU
+* ``lobpcg`` / ``lobpcg_sym`` — block LOBPCG eigensolver over the SpMM
+  (single GPU or row-sharded with the 3m×3m Gram all-reduce)
 """
 
 from ._lib import BLOCK, CimError, lib
 from .halftiles import HalfTiles, partition_units, plan_units, synthetic_pattern
+from .lobpcg import LobpcgResult, lobpcg, lobpcg_sym
 from .observables import (
     OP_KINDS,
     STRATEGIES,
@@ -31,12 +34,15 @@ __all__ = [
     "BLOCK",
     "CimError",
     "HalfTiles",
+    "LobpcgResult",
     "ObservablesInput",
     "OP_KINDS",
     "STRATEGIES",
     "ShardedSymSpmm",
     "contract_observables",
     "lib",
+    "lobpcg",
+    "lobpcg_sym",
     "padded_k",
     "partition_units",
     "plan_units",
