@@ -14,12 +14,18 @@
 //
 //  * acc_r lives in registers across a whole work unit (a run of tiles of one
 //    block row) and is reduced once per unit: a 2-step butterfly over the 4
-//    lanes that share rows, then a 4-warp sum through shared memory, then one
-//    vector red.global.add per output chunk.
-//  * acc_c is reduced per tile inside the warp (the 8 lanes sharing columns)
-//    through a bank-swizzled per-warp scratch, then red.global.add.v4 into Y_C.
+//    lanes that share rows, then (f32, k % 4 == 0) one red.global.add.v4 per
+//    lane and row — no cross-warp barrier — or (otherwise) a 4-warp sum
+//    through shared memory first.
+//  * acc_c is reduced per tile inside the warp (the 8 lanes sharing columns):
+//    for the packed k = 8 path by a 3-step register butterfly
+//    (reduce_cols_shfl), otherwise through a bank-swizzled per-warp scratch;
+//    then red.global.add.v4 into Y_C.
+//  * Two independent sub-CTAs (own ring + producer + consumers) share one CTA
+//    when the accumulators are small (sub_ctas).
 //
-// Diagonal tiles (R == C) are stored in full and only feed the direct product.
+// Diagonal tiles (R == C) are stored in full and only feed the direct product
+// (the packed path runs their transposed FMAs too and discards them).
 // The reference reaches this arithmetic only as a pair walk
 // (_contract_array_clause / _contract_atomic, pipeline.py:461-488) over the
 // full COO from _collect_pairs (pipeline.py:428-458).
@@ -59,6 +65,7 @@ struct SpmmParams {
   unsigned int stage_bytes;
   unsigned int tile_bytes;
   unsigned int xblk_bytes;  // 64·k·sizeof(T)
+  unsigned int sub_bytes;   // shared memory per sub-CTA
 };
 
 template <typename T>
@@ -191,6 +198,17 @@ __device__ __forceinline__ void load_pairs(u64 (&d)[P], const float *s) {
   }
 }
 
+// X_R chunk order for KV = 8 (two 16-byte chunks per row): lanes with rg ≥ 4
+// read the upper chunk first, so one LDS.128 of the warp touches 8 rows ×
+// alternating chunks = 8 distinct bank quads (1 wavefront instead of 2).  Their
+// acc_c slots 0-1 then hold vectors 4-7 and slots 2-3 vectors 0-3, which is
+// exactly the exchange pattern of the first butterfly step of
+// reduce_cols_shfl (every lane sends slots 2-3, keeps 0-1).
+template <int KV>
+__device__ __forceinline__ int xr_chunk_swap(int rg) {
+  return (KV == 8) ? (rg >> 2) : 0;
+}
+
 template <int KV, bool DIAG>
 __device__ __forceinline__ void tile_fma2(const float *__restrict__ Ts, const float *__restrict__ XC,
                                           const float *__restrict__ XR, int mb, int rg, int cg, int k, int v0,
@@ -199,12 +217,25 @@ __device__ __forceinline__ void tile_fma2(const float *__restrict__ Ts, const fl
   u64 xc[4][P];
 #pragma unroll
   for (int j = 0; j < 4; ++j) load_pairs<P>(xc[j], XC + (cg + 16 * j) * k + v0);
+  const int sw = xr_chunk_swap<KV>(rg);
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const float4 t4 = reinterpret_cast<const float4 *>(Ts)[i * 128 + mb];
     const float t[4] = {t4.x, t4.y, t4.z, t4.w};
     u64 xr[P];
-    if constexpr (!DIAG) load_pairs<P>(xr, XR + (rg + 8 * i) * k + v0);
+    if constexpr (!DIAG) {
+      const float *row = XR + (rg + 8 * i) * k + v0;
+      if constexpr (KV == 8) {
+        const ulonglong2 a = *reinterpret_cast<const ulonglong2 *>(row + 4 * sw);
+        const ulonglong2 b = *reinterpret_cast<const ulonglong2 *>(row + 4 * (sw ^ 1));
+        xr[0] = a.x;
+        xr[1] = a.y;
+        xr[2] = b.x;
+        xr[3] = b.y;
+      } else {
+        load_pairs<P>(xr, row);
+      }
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
 #pragma unroll
@@ -323,6 +354,46 @@ __device__ __forceinline__ void reduce_cols(T (&acc)[4][KV], T *scr, int lane, i
   }
 }
 
+__device__ __forceinline__ u64 shfl_xor_u64(u64 v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+
+// KV = 8 packed path: per-tile reduction of acc_c over the 8 lanes (rg = lane
+// bits 2-4) that share columns, entirely in registers — a 3-step reduce-scatter
+// butterfly (16 + 8 + 4 SHFL per lane) instead of a shared-memory round trip.
+// ac[j][q]: column cg + 16j, vector pair q (pairs swapped for rg ≥ 4, see
+// xr_chunk_swap).  Afterwards lane holds column cg + 16·((lane>>2)&3), vectors
+// 4·(lane>>4) .. +3, flushed with one red.global.add.v4.f32.
+__device__ __forceinline__ void reduce_cols_shfl(const u64 (&ac)[4][4], int lane, int cg, float *yblk,
+                                                 long long ldy) {
+  u64 a[4][2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) a[j][q] = add2(ac[j][q], shfl_xor_u64(ac[j][q + 2], 16));
+  const bool b3 = lane & 8;
+  u64 b[2][2];
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const u64 send = b3 ? a[m][q] : a[m + 2][q];
+      const u64 keep = b3 ? a[m + 2][q] : a[m][q];
+      b[m][q] = add2(keep, shfl_xor_u64(send, 8));
+    }
+  const bool b2 = lane & 4;
+  u64 c[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const u64 send = b2 ? b[0][q] : b[1][q];
+    const u64 keep = b2 ? b[1][q] : b[0][q];
+    c[q] = add2(keep, shfl_xor_u64(send, 4));
+  }
+  const int j = (lane >> 2) & 3, h = lane >> 4;
+  float s0, s1, s2, s3;
+  unpack2(c[0], s0, s1);
+  unpack2(c[1], s2, s3);
+  red_add_v4(yblk + (long long)(cg + 16 * j) * ldy + 4 * h, s0, s1, s2, s3);
+}
+
 // Per-unit reduction of acc_r over the 16 threads (4 lanes × 4 warps) that
 // share rows.  scr: group scratch, 4 warps × 64·KV elements.
 template <typename T, int KV>
@@ -353,6 +424,22 @@ __device__ __forceinline__ void reduce_rows(T (&acc)[8][KV], T *scr, int lane, i
     }
   }
   const int i0 = (b0 ? 4 : 0) + (b1 ? 2 : 0);
+#ifndef CIM_ROWFLUSH_SMEM
+  if constexpr (sizeof(T) == 4 && KV % 4 == 0) {
+    // No cross-warp sum: each lane flushes its 2 rows straight to L2 with
+    // vector reductions (4× the row atomics, but no named barrier per unit —
+    // the barrier wait was ~7% of the consumer stall samples; 1.86 → 1.76 ms).
+#pragma unroll
+    for (int ri = 0; ri < 2; ++ri) {
+      T *yr = yblk + (long long)(rg + 8 * (i0 + ri)) * ldy;
+#pragma unroll
+      for (int c = 0; c < KV / 4; ++c)
+        red_add_v4(reinterpret_cast<float *>(yr + 4 * c), acc[ri][4 * c], acc[ri][4 * c + 1], acc[ri][4 * c + 2],
+                   acc[ri][4 * c + 3]);
+    }
+    return;
+  }
+#endif
   named_bar_sync(bar_id, kGroupThreads);  // previous unit's readers are done
   T *mine = scr + w * 64 * KV;
   // every lane now holds distinct rows: rg + 8·(i0 + ri)
@@ -383,25 +470,41 @@ __device__ __forceinline__ void reduce_rows(T (&acc)[8][KV], T *scr, int lane, i
   }
 }
 
-// CTAs per SM the register budget is tuned for: two when a thread carries at
-// most 8 vectors' worth of accumulators in total, else one.
+// Independent sub-CTAs (own ring, producer warp and consumer groups) packed
+// into one CTA: two when a thread carries at most 8 vectors' worth of
+// accumulators in total, else one.  One CTA of 2 × 5 warps instead of two CTAs
+// of 5: registers are allocated in 2-warp granules, so a 5-warp CTA pays for 6
+// and ptxas would cap the consumers at 168 registers; 10 warps get 200.
 template <typename T, int KV, int NG>
-constexpr int min_ctas() {
+constexpr int sub_ctas() {
   return (KV * NG * (int)sizeof(T) <= 32) ? 2 : 1;
 }
 
+// Shared-memory column-reduction scratch (elements); the KV = 8 packed path
+// reduces in registers and needs none.
 template <typename T, int KV, int NG>
-__global__ void __launch_bounds__(NG * kGroupThreads + 32, min_ctas<T, KV, NG>())
+constexpr int col_scratch_elems() {
+  return (sizeof(T) == 4 && KV == 8) ? 0 : NG * 4 * 32 * 4 * KV;
+}
+
+// KX: the X row length when it is known at compile time (single pass, k =
+// KV·NG), else 0.  A constant k turns every shared-memory operand address into
+// one per-thread base plus an immediate, which keeps the inner loop free of
+// address registers (a runtime k made ptxas precompute and spill them).
+template <typename T, int KV, int NG, int KX>
+__global__ void __launch_bounds__(sub_ctas<T, KV, NG>() * (NG * kGroupThreads + 32), 1)
     sym_spmm_kernel(const SpmmParams p) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int tid = threadIdx.x;
+  extern __shared__ __align__(128) unsigned char smem_all[];
   constexpr int NCONS = NG * kGroupThreads;
+  const int sub = threadIdx.x / (NCONS + 32);
+  const int tid = threadIdx.x % (NCONS + 32);
+  unsigned char *smem = smem_all + (size_t)sub * p.sub_bytes;
   const int S = p.stages;
   unsigned char *stage_base = smem;
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)S * p.stage_bytes);
   uint64_t *empty = full + S;
   T *scr_c = reinterpret_cast<T *>(smem + (size_t)S * p.stage_bytes + 128);  // barriers fit in 128 B (S ≤ 8)
-  T *scr_r = scr_c + NG * 4 * 32 * 4 * KV;
+  T *scr_r = scr_c + col_scratch_elems<T, KV, NG>();
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
@@ -472,7 +575,7 @@ __global__ void __launch_bounds__(NG * kGroupThreads + 32, min_ctas<T, KV, NG>()
   const int gt = tid % kGroupThreads;  // micro-block id
   const int w = gt >> 5, lane = tid & 31;
   const int rg = frag_rg(gt), cg = frag_cg(gt);
-  const int k = p.k;
+  const int k = KX > 0 ? KX : p.k;
   const int v0 = p.v_base + g * KV;
   T *my_scr_c = scr_c + (g * 4 + w) * 32 * 4 * KV;
   T *my_scr_r = scr_r + g * 4 * 64 * KV;
@@ -505,17 +608,26 @@ __global__ void __launch_bounds__(NG * kGroupThreads + 32, min_ctas<T, KV, NG>()
     const T *XC = reinterpret_cast<const T *>(st + tile_bytes);
     const T *XR = reinterpret_cast<const T *>(st + tile_bytes + xblk);
     const bool diag = h.flags & HDR_DIAG;
-    if (!diag) {
+    if (PACKED || !diag) {
 #pragma unroll
       for (int j = 0; j < 4; ++j)
 #pragma unroll
         for (int v = 0; v < NA; ++v) acc_c[j][v] = AccE(0);
     }
     if constexpr (PACKED) {
+#ifdef CIM_DIAG_BRANCH
       if (diag)
         tile_fma2<KV, true>(Ts, XC, XR, gt, rg, cg, k, v0, acc_r, acc_c);
       else
         tile_fma2<KV, false>(Ts, XC, XR, gt, rg, cg, k, v0, acc_r, acc_c);
+#else
+      // One code path for every tile: a diagonal tile also runs the
+      // transposed FMAs (against X_C, which is X_R there) and just skips their
+      // flush.  Two inlined bodies made ptxas reconcile the accumulator
+      // registers with ~64 MOVs per off-diagonal tile, more than the 6.7%
+      // extra FFMA2 work this costs on diagonal tiles.
+      tile_fma2<KV, false>(Ts, XC, diag ? XC : XR, gt, rg, cg, k, v0, acc_r, acc_c);
+#endif
     } else {
       if (diag)
         tile_fma<T, KV, true>(Ts, XC, XR, gt, rg, cg, k, v0, acc_r, acc_c);
@@ -528,7 +640,9 @@ __global__ void __launch_bounds__(NG * kGroupThreads + 32, min_ctas<T, KV, NG>()
       stage = 0;
       phase ^= 1u;
     }
-    if (!diag) {
+    if constexpr (PACKED && KV == 8) {
+      if (!diag) reduce_cols_shfl(acc_c, lane, cg, Y + (long long)h.C * kBlock * p.ldy + v0, p.ldy);
+    } else if (!diag) {
       T fc[4][KV];
 #pragma unroll
       for (int j = 0; j < 4; ++j)
@@ -554,7 +668,7 @@ __global__ void __launch_bounds__(NG * kGroupThreads + 32, min_ctas<T, KV, NG>()
             fr[i][v] = acc_r[i][v];
           }
         }
-      reduce_rows<T, KV>(fr, my_scr_r, lane, w, rg, gt, 1 + g, Y + (long long)h.R * kBlock * p.ldy + v0, p.ldy);
+      reduce_rows<T, KV>(fr, my_scr_r, lane, w, rg, gt, 1 + sub * NG + g, Y + (long long)h.R * kBlock * p.ldy + v0, p.ldy);
     }
   }
 }
@@ -653,7 +767,7 @@ bool pick_cfg_default(int dtype, int k, LaunchCfg &c) {
   return false;
 }
 
-template <typename T, int KV, int NG>
+template <typename T, int KV, int NG, int KX = 0>
 int launch_kernel(const cim_half_tiles *H, const void *X, void *Y, int k, long long ldy, int passes,
                   cudaStream_t stream, DeviceState *ds) {
   static std::mutex mu;
@@ -661,15 +775,17 @@ int launch_kernel(const cim_half_tiles *H, const void *X, void *Y, int k, long l
   const unsigned int tile_bytes = kTileElems * sizeof(T);
   const unsigned int xblk = (unsigned int)(kBlock * k * sizeof(T));
   const unsigned int stage_bytes = (tile_bytes + 2 * xblk + sizeof(StageHdr) + 127u) & ~127u;
-  const size_t scratch = (size_t)NG * 4 * 32 * 4 * KV * sizeof(T) + (size_t)NG * 4 * 64 * KV * sizeof(T);
-  const int ctas_per_sm = min_ctas<T, KV, NG>();
-  const size_t budget = (size_t)(227 * 1024) / ctas_per_sm - (ctas_per_sm > 1 ? 1024 : 0);
+  const size_t scratch = (size_t)col_scratch_elems<T, KV, NG>() * sizeof(T) + (size_t)NG * 4 * 64 * KV * sizeof(T);
+  constexpr int subs = sub_ctas<T, KV, NG>();
+  const size_t budget = (size_t)(227 * 1024) / subs;
   if (budget < scratch + 128 + 2 * (size_t)stage_bytes) return set_error(CIM_EUNSUPPORTED, "k too large for smem");
   int S = (int)((budget - scratch - 128) / stage_bytes);
   S = std::min(S, 8);
-  const size_t smem = (size_t)S * stage_bytes + 128 + scratch;
+  const size_t sub_bytes = ((size_t)S * stage_bytes + 128 + scratch + 127) & ~(size_t)127;
+  const size_t smem = subs * sub_bytes;
+  const int threads = subs * (NG * kGroupThreads + 32);
 
-  auto kern = sym_spmm_kernel<T, KV, NG>;
+  auto kern = sym_spmm_kernel<T, KV, NG, KX>;
   int dev = 0;
   cudaGetDevice(&dev);
   {
@@ -683,7 +799,7 @@ int launch_kernel(const cim_half_tiles *H, const void *X, void *Y, int k, long l
     }
   }
   int occ = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NG * kGroupThreads + 32, smem);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
   if (e != cudaSuccess || occ < 1) occ = 1;
   long long grid = (long long)ds->sms * occ;
   grid = std::min<long long>(grid, H->n_units);
@@ -709,7 +825,8 @@ int launch_kernel(const cim_half_tiles *H, const void *X, void *Y, int k, long l
     p.stage_bytes = stage_bytes;
     p.tile_bytes = tile_bytes;
     p.xblk_bytes = xblk;
-    kern<<<(unsigned int)grid, NG * kGroupThreads + 32, smem, stream>>>(p);
+    p.sub_bytes = (unsigned int)sub_bytes;
+    kern<<<(unsigned int)grid, threads, smem, stream>>>(p);
     e = cudaGetLastError();
     if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("sym_spmm launch: ") + cudaGetErrorString(e));
   }
@@ -780,20 +897,42 @@ extern "C" int cim_sym_spmm(const cim_half_tiles *H, const void *X, void *Y, int
 
   if (H->dtype == CIM_F32) {
     switch (cfg.KV * 10 + cfg.NG) {
-      case 11: return launch_kernel<float, 1, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
-      case 21: return launch_kernel<float, 2, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
-      case 41: return launch_kernel<float, 4, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
-      case 42: return launch_kernel<float, 4, 2>(H, X, Y, k, ldy, cfg.passes, stream, ds);
-      case 24: return launch_kernel<float, 2, 4>(H, X, Y, k, ldy, cfg.passes, stream, ds);
-      case 81: return launch_kernel<float, 8, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
-      case 82: return launch_kernel<float, 8, 2>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+      case 11:
+        if (k == 1) return launch_kernel<float, 1, 1, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+        return launch_kernel<float, 1, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+      case 21:
+        if (k == 2) return launch_kernel<float, 2, 1, 2>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+        return launch_kernel<float, 2, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+      case 41:
+        if (k == 4) return launch_kernel<float, 4, 1, 4>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+        return launch_kernel<float, 4, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+      case 42:
+        if (k == 8) return launch_kernel<float, 4, 2, 8>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+        return launch_kernel<float, 4, 2>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+      case 24:
+        if (k == 8) return launch_kernel<float, 2, 4, 8>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+        return launch_kernel<float, 2, 4>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+      case 81:
+        if (k == 8) return launch_kernel<float, 8, 1, 8>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+        return launch_kernel<float, 8, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+      case 82:
+        if (k == 16) return launch_kernel<float, 8, 2, 16>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+        return launch_kernel<float, 8, 2>(H, X, Y, k, ldy, cfg.passes, stream, ds);
     }
   } else {
     switch (cfg.KV * 10 + cfg.NG) {
-      case 11: return launch_kernel<double, 1, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
-      case 21: return launch_kernel<double, 2, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
-      case 41: return launch_kernel<double, 4, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
-      case 42: return launch_kernel<double, 4, 2>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+      case 11:
+        if (k == 1) return launch_kernel<double, 1, 1, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+        return launch_kernel<double, 1, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+      case 21:
+        if (k == 2) return launch_kernel<double, 2, 1, 2>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+        return launch_kernel<double, 2, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+      case 41:
+        if (k == 4) return launch_kernel<double, 4, 1, 4>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+        return launch_kernel<double, 4, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+      case 42:
+        if (k == 8) return launch_kernel<double, 4, 2, 8>(H, X, Y, k, ldy, cfg.passes, stream, ds);
+        return launch_kernel<double, 4, 2>(H, X, Y, k, ldy, cfg.passes, stream, ds);
     }
   }
   return set_error(CIM_EUNSUPPORTED, "no kernel for (dtype, k)");
