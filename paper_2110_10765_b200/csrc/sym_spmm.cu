@@ -472,9 +472,8 @@ __device__ __forceinline__ void reduce_rows(T (&acc)[8][KV], T *scr, int lane, i
 
 // Independent sub-CTAs (own ring, producer warp and consumer groups) packed
 // into one CTA: two when a thread carries at most 8 vectors' worth of
-// accumulators in total, else one.  One CTA of 2 × 5 warps instead of two CTAs
-// of 5: registers are allocated in 2-warp granules, so a 5-warp CTA pays for 6
-// and ptxas would cap the consumers at 168 registers; 10 warps get 200.
+// accumulators in total, else one (same residency as two 5-warp CTAs per SM;
+// one launch slot, one shared-memory carve-out).
 template <typename T, int KV, int NG>
 constexpr int sub_ctas() {
   return (KV * NG * (int)sizeof(T) <= 32) ? 2 : 1;
@@ -673,6 +672,211 @@ __global__ void __launch_bounds__(sub_ctas<T, KV, NG>() * (NG * kGroupThreads + 
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// k = 8 f32 specialisation (the BASELINE headline): register-reallocated
+// warpgroups, X_R resident in registers for a whole work unit.
+//
+// CTA = 3 warpgroups.  WG0 and WG1 are the consumer groups of two independent
+// sub-rings (sub 0, sub 1); WG2 holds their two producer warps (warps 8, 9;
+// warps 10-11 leave at once).  setmaxnreg moves registers from WG2 (→ 40) to
+// the consumers (→ 232): per SM sub-partition 2 × 232 + 40 ≤ 512 registers
+// per lane.  With 232 registers a consumer keeps, besides acc_r (8 rows × 8
+// vectors) and acc_c (4 columns × 8), the unit's X_R rows (8 × 8) in
+// registers, so a tile costs 8 LDS.128 of T + 8 of X_C per thread instead of
+// 32, and the producer copies X_R only with a unit's first tile.
+// ---------------------------------------------------------------------------
+constexpr int kK8Threads = 384;
+constexpr int kK8ConsumerRegs = 232;
+constexpr int kK8ProducerRegs = 40;
+
+__global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmParams p) {
+  extern __shared__ __align__(128) unsigned char smem_all[];
+  constexpr int K = 8;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform
+  const int lane = threadIdx.x & 31;
+  const int wg = warp >> 2;
+  const int S = p.stages;
+  const unsigned int tile_bytes = p.tile_bytes, xblk = p.xblk_bytes;
+
+  if (threadIdx.x < 2) {
+    unsigned char *sm = smem_all + (size_t)threadIdx.x * p.sub_bytes;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm + (size_t)S * p.stage_bytes);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&full[S + s], 4);  // empty[s]: one arrival per consumer warp
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (wg == 2) {
+    // ======================= producer warps =======================
+    setmaxnreg_dec<kK8ProducerRegs>();
+    if (warp >= 10) return;
+    const int sub = warp - 8;
+    unsigned char *smem = smem_all + (size_t)sub * p.sub_bytes;
+    unsigned char *stage_base = smem;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)S * p.stage_bytes);
+    uint64_t *empty = full + S;
+    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_keep = policy_evict_last();
+    int stage = 0;
+    uint32_t phase = 0;
+    unsigned int u = 0;
+    if (lane == 0) u = atomicAdd(p.counter, 1u);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    while ((long long)u < p.n_units) {
+      const int4 unit = p.units[u];
+      unsigned int u_next = 0;
+      if (lane == 0) u_next = atomicAdd(p.counter, 1u);  // prefetch the next ticket
+      const int R = unit.x, t0 = unit.y, t1 = unit.z;
+      for (int tb = t0; tb < t1; tb += 32) {
+        const int t = tb + lane;
+        const int myC = (t < t1) ? p.tile_rc[t].y : 0;
+        const int cnt = min(32, t1 - tb);
+        for (int q = 0; q < cnt; ++q) {
+          const int C = __shfl_sync(0xffffffffu, myC, q);
+          if (lane == 0) {
+            mbar_wait_backoff(&empty[stage], phase ^ 1u);
+            unsigned char *st = stage_base + (size_t)stage * p.stage_bytes;
+            const int tt = tb + q;
+            const bool diag = (C == R), first = (tt == t0);
+            const int flags = (first ? HDR_FIRST : 0) | (tt == t1 - 1 ? HDR_LAST : 0) | (diag ? HDR_DIAG : 0);
+            StageHdr *h = reinterpret_cast<StageHdr *>(st + tile_bytes + 2 * xblk);
+            *h = StageHdr{R, C, flags, 0};
+            const bool need_xr = first && !diag;  // a diagonal first tile has X_R = X_C
+            mbar_arrive_expect_tx(&full[stage], tile_bytes + (need_xr ? 2 * xblk : xblk));
+            bulk_g2s(st, p.vals + (size_t)tt * tile_bytes, tile_bytes, &full[stage], pol_stream);
+            bulk_g2s(st + tile_bytes, p.X + (size_t)C * xblk, xblk, &full[stage], pol_keep);
+            if (need_xr) bulk_g2s(st + tile_bytes + xblk, p.X + (size_t)R * xblk, xblk, &full[stage], pol_keep);
+          }
+          __syncwarp();
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+      u = __shfl_sync(0xffffffffu, u_next, 0);
+    }
+    if (lane == 0) {
+      mbar_wait_backoff(&empty[stage], phase ^ 1u);
+      StageHdr *h = reinterpret_cast<StageHdr *>(stage_base + (size_t)stage * p.stage_bytes + tile_bytes + 2 * xblk);
+      *h = StageHdr{0, 0, HDR_TERM, 0};
+      mbar_arrive(&full[stage]);
+    }
+    return;
+  }
+
+  // ======================= consumer warpgroups =======================
+  setmaxnreg_inc<kK8ConsumerRegs>();
+  const int sub = wg;
+  unsigned char *smem = smem_all + (size_t)sub * p.sub_bytes;
+  unsigned char *stage_base = smem;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)S * p.stage_bytes);
+  uint64_t *empty = full + S;
+  const int gt = threadIdx.x & 127;  // micro-block id
+  const int rg = frag_rg(gt), cg = frag_cg(gt);
+  const int sw = xr_chunk_swap<8>(rg);
+  float *Y = reinterpret_cast<float *>(p.Y);
+  const long long ldy = p.ldy;
+
+  u64 ar[8][4], ac[4][4], xr[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ar[i][q] = 0ull, xr[i][q] = 0ull;
+
+  int stage = 0;
+  uint32_t phase = 0;
+  while (true) {
+    mbar_wait(&full[stage], phase);
+    const unsigned char *st = stage_base + (size_t)stage * p.stage_bytes;
+    const StageHdr h = *reinterpret_cast<const StageHdr *>(st + tile_bytes + 2 * xblk);
+    if (h.flags & HDR_TERM) break;
+    const float *Ts = reinterpret_cast<const float *>(st);
+    const float *XC = reinterpret_cast<const float *>(st + tile_bytes);
+    const bool diag = h.flags & HDR_DIAG;
+    if (h.flags & HDR_FIRST) {
+      const float *XR = diag ? XC : reinterpret_cast<const float *>(st + tile_bytes + xblk);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float *row = XR + (rg + 8 * i) * K;
+        const ulonglong2 a = *reinterpret_cast<const ulonglong2 *>(row + 4 * sw);
+        const ulonglong2 b = *reinterpret_cast<const ulonglong2 *>(row + 4 * (sw ^ 1));
+        xr[i][0] = a.x;
+        xr[i][1] = a.y;
+        xr[i][2] = b.x;
+        xr[i][3] = b.y;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ar[i][q] = 0ull;
+      }
+    }
+    u64 xc[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) load_pairs<4>(xc[j], XC + (cg + 16 * j) * K);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ac[j][q] = 0ull;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 t4 = reinterpret_cast<const float4 *>(Ts)[i * 128 + gt];
+      const float t[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          ar[i][q] = fma2(t[j], xc[j][q], ar[i][q]);
+          ac[j][q] = fma2(t[j], xr[i][q], ac[j][q]);
+        }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == S) {
+      stage = 0;
+      phase ^= 1u;
+    }
+    // a diagonal tile's transposed FMAs (against X_R = X_C) are discarded
+    if (!diag) reduce_cols_shfl(ac, lane, cg, Y + (long long)h.C * kBlock * ldy, ldy);
+    if (h.flags & HDR_LAST) {
+      // rows rg + 8i over the 4 lanes sharing them: 2 butterfly steps, then
+      // each lane flushes 2 rows × 8 vectors (no cross-warp barrier)
+      const bool b0 = lane & 1, b1 = lane & 2;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const u64 send = b0 ? ar[i][q] : ar[i + 4][q];
+          const u64 keep = b0 ? ar[i + 4][q] : ar[i][q];
+          ar[i][q] = add2(keep, shfl_xor_u64(send, 1));
+        }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const u64 send = b1 ? ar[i][q] : ar[i + 2][q];
+          const u64 keep = b1 ? ar[i + 2][q] : ar[i][q];
+          ar[i][q] = add2(keep, shfl_xor_u64(send, 2));
+        }
+      const int i0 = (b0 ? 4 : 0) + (b1 ? 2 : 0);
+      float *yblk = Y + (long long)h.R * kBlock * ldy;
+#pragma unroll
+      for (int ri = 0; ri < 2; ++ri) {
+        float *yr = yblk + (long long)(rg + 8 * (i0 + ri)) * ldy;
+        float a0, a1, a2, a3, a4, a5, a6, a7;
+        unpack2(ar[ri][0], a0, a1);
+        unpack2(ar[ri][1], a2, a3);
+        unpack2(ar[ri][2], a4, a5);
+        unpack2(ar[ri][3], a6, a7);
+        red_add_v4(yr, a0, a1, a2, a3);
+        red_add_v4(yr + 4, a4, a5, a6, a7);
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -833,6 +1037,49 @@ int launch_kernel(const cim_half_tiles *H, const void *X, void *Y, int k, long l
   return CIM_OK;
 }
 
+int launch_k8(const cim_half_tiles *H, const void *X, void *Y, long long ldy, cudaStream_t stream, DeviceState *ds) {
+  static std::once_flag attr_once[64];
+  const unsigned int tile_bytes = kTileElems * sizeof(float);
+  const unsigned int xblk = kBlock * 8 * sizeof(float);
+  const unsigned int stage_bytes = (tile_bytes + 2 * xblk + sizeof(StageHdr) + 127u) & ~127u;
+  const size_t budget = (size_t)(227 * 1024) / 2;
+  int S = std::min((int)((budget - 128) / stage_bytes), 8);
+  const size_t sub_bytes = ((size_t)S * stage_bytes + 128 + 127) & ~(size_t)127;
+  const size_t smem = 2 * sub_bytes;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaError_t e = cudaSuccess;
+  std::call_once(attr_once[dev & 63], [&] {
+    e = cudaFuncSetAttribute(sym_spmm_k8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("cudaFuncSetAttribute(k8): ") + cudaGetErrorString(e));
+  long long grid = std::min<long long>(ds->sms, (H->n_units + 1) / 2);
+  if (grid < 1) return CIM_OK;
+  unsigned int *ctr = take_counters(ds, 1);
+  e = cudaMemsetAsync(ctr, 0, sizeof(unsigned int), stream);
+  if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("cudaMemsetAsync counter: ") + cudaGetErrorString(e));
+  SpmmParams p;
+  p.units = reinterpret_cast<const int4 *>(H->units);
+  p.tile_rc = reinterpret_cast<const int2 *>(H->tile_rc);
+  p.vals = reinterpret_cast<const unsigned char *>(H->vals);
+  p.X = reinterpret_cast<const unsigned char *>(X);
+  p.Y = reinterpret_cast<unsigned char *>(Y);
+  p.counter = ctr;
+  p.n_units = H->n_units;
+  p.ldy = ldy;
+  p.k = 8;
+  p.v_base = 0;
+  p.stages = S;
+  p.stage_bytes = stage_bytes;
+  p.tile_bytes = tile_bytes;
+  p.xblk_bytes = xblk;
+  p.sub_bytes = (unsigned int)sub_bytes;
+  sym_spmm_k8_kernel<<<(unsigned int)grid, kK8Threads, smem, stream>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("sym_spmm_k8 launch: ") + cudaGetErrorString(e));
+  return CIM_OK;
+}
+
 }  // namespace
 }  // namespace cim
 
@@ -913,6 +1160,9 @@ extern "C" int cim_sym_spmm(const cim_half_tiles *H, const void *X, void *Y, int
         if (k == 8) return launch_kernel<float, 2, 4, 8>(H, X, Y, k, ldy, cfg.passes, stream, ds);
         return launch_kernel<float, 2, 4>(H, X, Y, k, ldy, cfg.passes, stream, ds);
       case 81:
+#ifndef CIM_NO_K8
+        if (k == 8) return launch_k8(H, X, Y, ldy, stream, ds);
+#endif
         if (k == 8) return launch_kernel<float, 8, 1, 8>(H, X, Y, k, ldy, cfg.passes, stream, ds);
         return launch_kernel<float, 8, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
       case 82:
