@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--tiles-per-gpu", type=int, default=TILES_PER_GPU)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget for the cpu_baseline leg")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=16)
     return ap.parse_args()
 
 
@@ -325,21 +325,27 @@ def impl_ours(args):
     Yh = torch.empty((S.rows_per_rank, k), dtype=dtype, pin_memory=True)
     e2e_steps = max(1, args.e2e_steps)
     if world == 1:
-        Xh1 = Xh[:n]
-        Yh1 = Yh[:n]
+        # public host-buffer API: each step = H2D of its own X block, the apply,
+        # D2H of its Y block; consecutive steps overlap inside the library
+        # (cim_sym_spmm_host_batch: H2D / kernel / D2H streams, PCIe duplex)
+        nbuf = min(3, e2e_steps)
+        Xhs = [Xh[:n]] + [torch.empty((n, k), dtype=dtype, pin_memory=True) for _ in range(nbuf - 1)]
+        for b in range(1, nbuf):
+            Xhs[b].copy_(Xh[:n] * (1.0 + 0.5 * b))
+        Yhs = [torch.empty((n, k), dtype=dtype, pin_memory=True) for _ in range(nbuf)]
 
-        def e2e_step():
-            pkg.sym_spmm(H, Xh1, out=Yh1)
+        def e2e_run(steps):
+            pkg.sym_spmm_host_batch(H, [Xhs[b % nbuf] for b in range(steps)], out=[Yhs[b % nbuf] for b in range(steps)])
     else:
-        def e2e_step():
-            Yh.copy_(S.apply(Xh.to(dev, non_blocking=True)), non_blocking=False)
-    e2e_step()
+        def e2e_run(steps):
+            for _ in range(steps):
+                Yh.copy_(S.apply(Xh.to(dev, non_blocking=True)), non_blocking=False)
+    e2e_run(min(2, e2e_steps))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        e2e_step()
+    e2e_run(e2e_steps)
     torch.cuda.synchronize()
     e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64, device=dev)
     if world > 1:
@@ -399,7 +405,10 @@ def impl_ours(args):
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6650",
                          "frac_of_8TBs_spec": achieved / 8000.0},
             "cpu_baseline": cpu_b,
-            "e2e": {"value": e2e_val, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": {"value": e2e_val, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "steps": e2e_steps,
+                    "api": "sym_spmm_host_batch (pinned host X/Y, H2D/kernel/D2H overlapped across steps)"
+                    if world == 1 else "ShardedSymSpmm.apply per step (host X in, host Y out)"},
             "gpu_launches": args.steps * (max(1, -(-S.k // 16)) if H.layout == "tc" else (1 if k <= 8 else max(1, k // 16))),
             "clocks": clocks.summary(),
         }

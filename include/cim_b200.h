@@ -114,6 +114,26 @@ CIM_API const char *cim_last_error(void);
 CIM_API int cim_sym_spmm(const cim_half_tiles *H, const void *X, void *Y, int32_t k,
                  int64_t ldx, int64_t ldy, uint32_t flags, void *stream);
 
+/*
+ * Host-buffer batch: Y_b = A·X_b for b < n_batch, where X_host[b] / Y_host[b]
+ * are HOST (n, k) row-major arrays of the tile dtype (pinned memory gives
+ * asynchronous copies; pageable memory still works, without overlap).
+ * Copies and kernels of consecutive blocks overlap on three internal streams
+ * (H2D, compute, D2H) through a caller-owned device `workspace` of
+ * cim_host_batch_workspace_bytes(H, k) bytes (2 X + 2 Y buffers).
+ * Synchronous: returns once every Y_b is on the host.
+ *
+ * Replaces: the reference's host-array operator boundary (numpy in, numpy
+ * out; contract_observables writes inputs.accum in place, pipeline.py:569)
+ * for a stream of independent vector blocks.
+ */
+CIM_API int cim_sym_spmm_host_batch(const cim_half_tiles *H, const void *const *X_host,
+                                    void *const *Y_host, int32_t n_batch, int32_t k,
+                                    void *workspace, uint64_t ws_bytes);
+
+/* Device workspace bytes cim_sym_spmm_host_batch needs for (H, k). */
+CIM_API uint64_t cim_host_batch_workspace_bytes(const cim_half_tiles *H, int32_t k);
+
 /* 1 if (dtype, k) has a compiled kernel for CIM_LAYOUT_FRAG tiles, else 0. */
 CIM_API int cim_sym_spmm_supported(int32_t dtype, int32_t k);
 

@@ -7,6 +7,8 @@ C-ABI in ``libcim_b200.so``, include/cim_b200.h):
                           pipeline.py:96-116)
 * ``sym_spmm``          — the operator (drop-in boundary of
                           contract_observables, pipeline.py:534-570)
+* ``sym_spmm_host_batch`` — the operator over a stream of host-resident vector
+                          blocks, copies and kernels pipelined (PCIe-bound)
 * ``ShardedSymSpmm``    — row-block sharding over GPUs (NCCL all-gather X /
                           reduce-scatter Y)
 * ``contract_observables``, ``ObservablesInput``, ``random_coefficients``,
@@ -26,7 +28,7 @@ from .observables import (
     random_coefficients,
 )
 from .sharded import ShardedSymSpmm, row_chunks
-from .spmm import padded_k, supported_k, sym_spmm
+from .spmm import padded_k, supported_k, sym_spmm, sym_spmm_host_batch
 
 __version__ = "1.0.0"
 
@@ -50,5 +52,6 @@ __all__ = [
     "row_chunks",
     "supported_k",
     "sym_spmm",
+    "sym_spmm_host_batch",
     "synthetic_pattern",
 ]

@@ -33,6 +33,8 @@ EXPORTS = (
     "cim_pack_tiles",
     "cim_unpack_tiles",
     "cim_hash_values",
+    "cim_sym_spmm_host_batch",
+    "cim_host_batch_workspace_bytes",
 )
 
 
@@ -89,9 +91,13 @@ def lib() -> ctypes.CDLL:
     L.cim_unpack_tiles.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_int32, c.c_void_p, c.c_void_p]
     L.cim_hash_values.argtypes = [c.c_void_p, c.c_void_p, c.c_int64, c.c_int32, c.c_uint64, c.c_int32,
                                   c.c_void_p, c.c_void_p]
+    L.cim_sym_spmm_host_batch.argtypes = [c.POINTER(CimHalfTiles), c.POINTER(c.c_void_p), c.POINTER(c.c_void_p),
+                                          c.c_int32, c.c_int32, c.c_void_p, c.c_uint64]
+    L.cim_host_batch_workspace_bytes.argtypes = [c.POINTER(CimHalfTiles), c.c_int32]
     for name in EXPORTS:
         if name not in ("cim_version", "cim_last_error"):
             getattr(L, name).restype = c.c_int
+    L.cim_host_batch_workspace_bytes.restype = c.c_uint64
     _lib = L
     return L
 

@@ -176,6 +176,7 @@ class HalfTiles:
     layout: str = "frag"
     meta: dict = field(default_factory=dict)
     _desc: CimHalfTiles | None = field(default=None, repr=False)
+    _ws: torch.Tensor | None = field(default=None, repr=False)
 
     # ------------------------------------------------------------------ props
     @property
@@ -236,6 +237,12 @@ class HalfTiles:
                 reserved=0,
             )
         return self._desc
+
+    def _workspace(self, nbytes: int) -> torch.Tensor:
+        """Cached device scratch (host-batch pipeline buffers), grown on demand."""
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=self.device)
+        return self._ws
 
     # ----------------------------------------------------------- constructors
     @classmethod

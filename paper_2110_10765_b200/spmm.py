@@ -152,3 +152,63 @@ def sym_spmm(H: HalfTiles, X, out=None, *, layout: str = "auto", accumulate: boo
     if is_numpy:
         return Y.cpu().numpy()
     return Y.contiguous() if layout == "kn" else (Y if direct else Y.contiguous())
+
+
+def _host_array(A, name: str, n: int, k: int, dtype: torch.dtype) -> torch.Tensor:
+    t = torch.from_numpy(A) if isinstance(A, np.ndarray) else A
+    if not isinstance(t, torch.Tensor):
+        raise ValueError(f"{name} must be a numpy array or CPU tensor, got {type(A).__name__}")
+    if t.device.type != "cpu":
+        raise ValueError(f"{name} must live in host memory (use sym_spmm for device tensors)")
+    if tuple(t.shape) != (n, k):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected ({n}, {k})")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} dtype {t.dtype} does not match the matrix dtype {dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be C-contiguous")
+    return t
+
+
+def sym_spmm_host_batch(H: HalfTiles, Xs, out=None):
+    """Y_b = A·X_b for a sequence of HOST (n, k) blocks, pipelined.
+
+    Host copies in, kernel, host copies out of consecutive blocks overlap on
+    three streams inside the C-ABI (``cim_sym_spmm_host_batch``): for a
+    host-resident workload the apply is PCIe-bound, and steady state costs
+    max(H2D, kernel, D2H) per block instead of their sum.  Pass pinned CPU
+    tensors (``pin_memory=True``) for asynchronous copies.  Returns the list
+    of outputs (``out`` if given, else fresh CPU tensors / numpy arrays
+    matching each input).  Synchronous.
+    """
+    if not isinstance(H, HalfTiles):
+        raise ValueError(f"H must be a HalfTiles, got {type(H).__name__}")
+    Xs = list(Xs)
+    if not Xs:
+        return [] if out is None else list(out)
+    k = Xs[0].shape[1] if len(Xs[0].shape) == 2 else -1
+    if k < 1:
+        raise ValueError("each X must be 2-D (n, k) with k >= 1")
+    if padded_k(H.dtype, k, H.layout) != k:
+        raise ValueError(f"k={k} has no compiled kernel; pad X to k={padded_k(H.dtype, k, H.layout)} vectors")
+    xt = [_host_array(X, f"Xs[{b}]", H.n, k, H.dtype) for b, X in enumerate(Xs)]
+    if out is None:
+        outs = [np.empty((H.n, k), dtype=X.dtype) if isinstance(X, np.ndarray)
+                else torch.empty((H.n, k), dtype=H.dtype, pin_memory=X.is_pinned()) for X in Xs]
+    else:
+        outs = list(out)
+        if len(outs) != len(Xs):
+            raise ValueError(f"out has {len(outs)} buffers for {len(Xs)} inputs")
+    yt = [_host_array(Y, f"out[{b}]", H.n, k, H.dtype) for b, Y in enumerate(outs)]
+    import ctypes
+
+    L = lib()
+    desc = H.descriptor()
+    need = int(L.cim_host_batch_workspace_bytes(desc, k))
+    ws = H._workspace(need)
+    nb = len(xt)
+    xp = (ctypes.c_void_p * nb)(*[t.data_ptr() for t in xt])
+    yp = (ctypes.c_void_p * nb)(*[t.data_ptr() for t in yt])
+    with torch.cuda.device(H.device):
+        rc = L.cim_sym_spmm_host_batch(desc, xp, yp, nb, k, ws.data_ptr(), need)
+    check(rc, "cim_sym_spmm_host_batch")
+    return outs

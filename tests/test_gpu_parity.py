@@ -352,3 +352,35 @@ def test_c2_full_size_properties(pkg, layout):
                 yr += tiles[t].T @ X1h[r * 64:(r + 1) * 64]
         got = Y1[R * 64:(R + 1) * 64].cpu().numpy()
         assert np.abs(got - yr).max() <= 1e-5 * max(1.0, np.abs(yr).max())
+
+
+@pytest.mark.parametrize("dtype,k", [(torch.float32, 8), (torch.float32, 4), (torch.float64, 8)])
+def test_host_batch_pipeline_matches_oracle(pkg, c1_small, dtype, k):
+    """cim_sym_spmm_host_batch: host (pinned and pageable, numpy and torch)
+    blocks in, host blocks out; every block checked against the oracle, and
+    against the single-call operator bit for bit (same kernel, same order)."""
+    n, rc, tiles = c1_small
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=dtype)
+    g = torch.Generator().manual_seed(5)
+    Xs = [torch.randn((n, k), generator=g, dtype=dtype).pin_memory() for _ in range(3)]
+    Xs.append(torch.randn((n, k), generator=g, dtype=dtype))  # pageable
+    Xs.append(Xs[0].numpy().copy())  # numpy
+    Ys = pkg.sym_spmm_host_batch(H, Xs)
+    assert isinstance(Ys[-1], np.ndarray) and Ys[0].is_pinned()
+    tl = tiles if dtype == torch.float32 else tiles.astype(np.float64)
+    for X, Y in zip(Xs, Ys):
+        Xn = X if isinstance(X, np.ndarray) else X.numpy()
+        Yn = Y if isinstance(Y, np.ndarray) else Y.numpy()
+        check_result(n, rc, tl, Xn, Yn, dtype)
+        Y1 = pkg.sym_spmm(H, torch.from_numpy(Xn).cuda()).cpu().numpy()
+        # atomics make the summation order of Y_C run-dependent: compare to the gate, not bits
+        assert np.abs(Y1 - Yn).max() <= 1e-5 * np.abs(Y1).max()
+    # caller-owned outputs, and validation before any compute
+    outs = [torch.empty((n, k), dtype=dtype) for _ in range(2)]
+    assert pkg.sym_spmm_host_batch(H, Xs[:2], out=outs) is not None
+    with pytest.raises(ValueError):
+        pkg.sym_spmm_host_batch(H, [torch.zeros((n + 1, k), dtype=dtype)])
+    with pytest.raises(ValueError):
+        pkg.sym_spmm_host_batch(H, [torch.zeros((n, k), dtype=dtype, device="cuda")])
+    with pytest.raises(ValueError):
+        pkg.sym_spmm_host_batch(H, Xs[:2], out=outs[:1])
