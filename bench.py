@@ -400,7 +400,9 @@ def impl_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
                          "kernel": "sym_spmm_tc_kernel (tcgen05 kind::tf32, 3xTF32 split)" if H.layout == "tc"
-                         else "sym_spmm_kernel (FFMA2)", "kernel_ms": kern_max,
+                         else ("sym_spmm_k8_kernel (FFMA2, setmaxnreg warpgroups, X_R in registers)"
+                               if (k == 8 and dtype == torch.float32) else "sym_spmm_kernel (FFMA2/FFMA)"),
+                         "kernel_ms": kern_max,
                          "algorithmic_bytes_per_launch": bytes_local,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6650",
                          "frac_of_8TBs_spec": achieved / 8000.0},

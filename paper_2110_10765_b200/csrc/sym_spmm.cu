@@ -363,7 +363,7 @@ __device__ __forceinline__ u64 shfl_xor_u64(u64 v, int m) { return __shfl_xor_sy
 // xr_chunk_swap).  Afterwards lane holds column cg + 16·((lane>>2)&3), vectors
 // 4·(lane>>4) .. +3, flushed with one red.global.add.v4.f32.
 __device__ __forceinline__ void reduce_cols_shfl(const u64 (&ac)[4][4], int lane, int cg, float *yblk,
-                                                 long long ldy) {
+                                                 long long ldy, uint64_t ypol) {
   u64 a[4][2];
 #pragma unroll
   for (int j = 0; j < 4; ++j)
@@ -391,7 +391,7 @@ __device__ __forceinline__ void reduce_cols_shfl(const u64 (&ac)[4][4], int lane
   float s0, s1, s2, s3;
   unpack2(c[0], s0, s1);
   unpack2(c[1], s2, s3);
-  red_add_v4(yblk + (long long)(cg + 16 * j) * ldy + 4 * h, s0, s1, s2, s3);
+  red_add_v4(yblk + (long long)(cg + 16 * j) * ldy + 4 * h, s0, s1, s2, s3, ypol);
 }
 
 // Per-unit reduction of acc_r over the 16 threads (4 lanes × 4 warps) that
@@ -640,7 +640,7 @@ __global__ void __launch_bounds__(sub_ctas<T, KV, NG>() * (NG * kGroupThreads + 
       phase ^= 1u;
     }
     if constexpr (PACKED && KV == 8) {
-      if (!diag) reduce_cols_shfl(acc_c, lane, cg, Y + (long long)h.C * kBlock * p.ldy + v0, p.ldy);
+      if (!diag) reduce_cols_shfl(acc_c, lane, cg, Y + (long long)h.C * kBlock * p.ldy + v0, p.ldy, policy_evict_normal());
     } else if (!diag) {
       T fc[4][KV];
 #pragma unroll
@@ -690,21 +690,26 @@ constexpr int kK8Threads = 384;
 constexpr int kK8ConsumerRegs = 232;
 constexpr int kK8ProducerRegs = 40;
 
+// G = 8-vector groups sharing one ring (k = 8·G): G = 1 → two independent
+// sub-rings (WG0, WG1); G = 2 → one ring whose every tile feeds both consumer
+// warpgroups (vectors 0-7 and 8-15), the tile streamed from HBM once.
+template <int G>
 __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmParams p) {
   extern __shared__ __align__(128) unsigned char smem_all[];
-  constexpr int K = 8;
+  constexpr int K = 8 * G;
+  constexpr int SUBS = 2 / G;
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform
   const int lane = threadIdx.x & 31;
   const int wg = warp >> 2;
   const int S = p.stages;
   const unsigned int tile_bytes = p.tile_bytes, xblk = p.xblk_bytes;
 
-  if (threadIdx.x < 2) {
+  if (threadIdx.x < SUBS) {
     unsigned char *sm = smem_all + (size_t)threadIdx.x * p.sub_bytes;
     uint64_t *full = reinterpret_cast<uint64_t *>(sm + (size_t)S * p.stage_bytes);
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&full[S + s], 4);  // empty[s]: one arrival per consumer warp
+      mbar_init(&full[S + s], 4 * G);  // empty[s]: one arrival per consumer warp
     }
     fence_mbar_init();
   }
@@ -713,14 +718,18 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
   if (wg == 2) {
     // ======================= producer warps =======================
     setmaxnreg_dec<kK8ProducerRegs>();
-    if (warp >= 10) return;
+    if (warp >= 8 + SUBS) return;
     const int sub = warp - 8;
     unsigned char *smem = smem_all + (size_t)sub * p.sub_bytes;
     unsigned char *stage_base = smem;
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)S * p.stage_bytes);
     uint64_t *empty = full + S;
     const uint64_t pol_stream = policy_evict_first();
+#ifdef CIM_K8_X_NORMAL
+    const uint64_t pol_keep = policy_evict_normal();
+#else
     const uint64_t pol_keep = policy_evict_last();
+#endif
     int stage = 0;
     uint32_t phase = 0;
     unsigned int u = 0;
@@ -771,7 +780,8 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
 
   // ======================= consumer warpgroups =======================
   setmaxnreg_inc<kK8ConsumerRegs>();
-  const int sub = wg;
+  const int sub = wg / G;
+  const int v0 = 8 * (wg % G);  // this warpgroup's vectors v0 .. v0+7
   unsigned char *smem = smem_all + (size_t)sub * p.sub_bytes;
   unsigned char *stage_base = smem;
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)S * p.stage_bytes);
@@ -781,6 +791,11 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
   const int sw = xr_chunk_swap<8>(rg);
   float *Y = reinterpret_cast<float *>(p.Y);
   const long long ldy = p.ldy;
+#ifdef CIM_K8_Y_LAST
+  const uint64_t ypol = policy_evict_last();
+#else
+  const uint64_t ypol = policy_evict_normal();
+#endif
 
   u64 ar[8][4], ac[4][4], xr[8][4];
 #pragma unroll
@@ -802,7 +817,7 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
       const float *XR = diag ? XC : reinterpret_cast<const float *>(st + tile_bytes + xblk);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float *row = XR + (rg + 8 * i) * K;
+        const float *row = XR + (rg + 8 * i) * K + v0;
         const ulonglong2 a = *reinterpret_cast<const ulonglong2 *>(row + 4 * sw);
         const ulonglong2 b = *reinterpret_cast<const ulonglong2 *>(row + 4 * (sw ^ 1));
         xr[i][0] = a.x;
@@ -815,7 +830,7 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
     }
     u64 xc[4][4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) load_pairs<4>(xc[j], XC + (cg + 16 * j) * K);
+    for (int j = 0; j < 4; ++j) load_pairs<4>(xc[j], XC + (cg + 16 * j) * K + v0);
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -839,7 +854,7 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
       phase ^= 1u;
     }
     // a diagonal tile's transposed FMAs (against X_R = X_C) are discarded
-    if (!diag) reduce_cols_shfl(ac, lane, cg, Y + (long long)h.C * kBlock * ldy, ldy);
+    if (!diag) reduce_cols_shfl(ac, lane, cg, Y + (long long)h.C * kBlock * ldy + v0, ldy, ypol);
     if (h.flags & HDR_LAST) {
       // rows rg + 8i over the 4 lanes sharing them: 2 butterfly steps, then
       // each lane flushes 2 rows × 8 vectors (no cross-warp barrier)
@@ -861,7 +876,7 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
           ar[i][q] = add2(keep, shfl_xor_u64(send, 2));
         }
       const int i0 = (b0 ? 4 : 0) + (b1 ? 2 : 0);
-      float *yblk = Y + (long long)h.R * kBlock * ldy;
+      float *yblk = Y + (long long)h.R * kBlock * ldy + v0;
 #pragma unroll
       for (int ri = 0; ri < 2; ++ri) {
         float *yr = yblk + (long long)(rg + 8 * (i0 + ri)) * ldy;
@@ -870,8 +885,8 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
         unpack2(ar[ri][1], a2, a3);
         unpack2(ar[ri][2], a4, a5);
         unpack2(ar[ri][3], a6, a7);
-        red_add_v4(yr, a0, a1, a2, a3);
-        red_add_v4(yr + 4, a4, a5, a6, a7);
+        red_add_v4(yr, a0, a1, a2, a3, ypol);
+        red_add_v4(yr + 4, a4, a5, a6, a7, ypol);
       }
     }
   }
@@ -1037,23 +1052,25 @@ int launch_kernel(const cim_half_tiles *H, const void *X, void *Y, int k, long l
   return CIM_OK;
 }
 
+template <int G>
 int launch_k8(const cim_half_tiles *H, const void *X, void *Y, long long ldy, cudaStream_t stream, DeviceState *ds) {
   static std::once_flag attr_once[64];
+  constexpr int SUBS = 2 / G;
   const unsigned int tile_bytes = kTileElems * sizeof(float);
-  const unsigned int xblk = kBlock * 8 * sizeof(float);
+  const unsigned int xblk = kBlock * 8 * G * sizeof(float);
   const unsigned int stage_bytes = (tile_bytes + 2 * xblk + sizeof(StageHdr) + 127u) & ~127u;
-  const size_t budget = (size_t)(227 * 1024) / 2;
+  const size_t budget = (size_t)(227 * 1024) / SUBS;
   int S = std::min((int)((budget - 128) / stage_bytes), 8);
   const size_t sub_bytes = ((size_t)S * stage_bytes + 128 + 127) & ~(size_t)127;
-  const size_t smem = 2 * sub_bytes;
+  const size_t smem = SUBS * sub_bytes;
   int dev = 0;
   cudaGetDevice(&dev);
   cudaError_t e = cudaSuccess;
   std::call_once(attr_once[dev & 63], [&] {
-    e = cudaFuncSetAttribute(sym_spmm_k8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(sym_spmm_k8_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   });
   if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("cudaFuncSetAttribute(k8): ") + cudaGetErrorString(e));
-  long long grid = std::min<long long>(ds->sms, (H->n_units + 1) / 2);
+  long long grid = std::min<long long>(ds->sms, (H->n_units + SUBS - 1) / SUBS);
   if (grid < 1) return CIM_OK;
   unsigned int *ctr = take_counters(ds, 1);
   e = cudaMemsetAsync(ctr, 0, sizeof(unsigned int), stream);
@@ -1067,14 +1084,14 @@ int launch_k8(const cim_half_tiles *H, const void *X, void *Y, long long ldy, cu
   p.counter = ctr;
   p.n_units = H->n_units;
   p.ldy = ldy;
-  p.k = 8;
+  p.k = 8 * G;
   p.v_base = 0;
   p.stages = S;
   p.stage_bytes = stage_bytes;
   p.tile_bytes = tile_bytes;
   p.xblk_bytes = xblk;
   p.sub_bytes = (unsigned int)sub_bytes;
-  sym_spmm_k8_kernel<<<(unsigned int)grid, kK8Threads, smem, stream>>>(p);
+  sym_spmm_k8_kernel<G><<<(unsigned int)grid, kK8Threads, smem, stream>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("sym_spmm_k8 launch: ") + cudaGetErrorString(e));
   return CIM_OK;
@@ -1161,11 +1178,14 @@ extern "C" int cim_sym_spmm(const cim_half_tiles *H, const void *X, void *Y, int
         return launch_kernel<float, 2, 4>(H, X, Y, k, ldy, cfg.passes, stream, ds);
       case 81:
 #ifndef CIM_NO_K8
-        if (k == 8) return launch_k8(H, X, Y, ldy, stream, ds);
+        if (k == 8) return launch_k8<1>(H, X, Y, ldy, stream, ds);
 #endif
         if (k == 8) return launch_kernel<float, 8, 1, 8>(H, X, Y, k, ldy, cfg.passes, stream, ds);
         return launch_kernel<float, 8, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
       case 82:
+#ifndef CIM_NO_K8
+        if (k == 16) return launch_k8<2>(H, X, Y, ldy, stream, ds);
+#endif
         if (k == 16) return launch_kernel<float, 8, 2, 16>(H, X, Y, k, ldy, cfg.passes, stream, ds);
         return launch_kernel<float, 8, 2>(H, X, Y, k, ldy, cfg.passes, stream, ds);
     }

@@ -44,7 +44,8 @@ def load(path):
     return {h: v for h, v in zip(rows[0], rows[2])}
 
 
-reps = [load(p) for p in sys.argv[1:]]
-for k in KEYS:
-    vals = [r.get(k, "-") for r in reps]
-    print(f"{k:80s} " + "  ".join(f"{v:>16s}" for v in vals))
+if __name__ == "__main__":
+    reps = [load(p) for p in sys.argv[1:]]
+    for k in KEYS:
+        vals = [r.get(k, "-") for r in reps]
+        print(f"{k:80s} " + "  ".join(f"{v:>16s}" for v in vals))
