@@ -134,6 +134,50 @@ CIM_API int cim_sym_spmm_host_batch(const cim_half_tiles *H, const void *const *
 /* Device workspace bytes cim_sym_spmm_host_batch needs for (H, k). */
 CIM_API uint64_t cim_host_batch_workspace_bytes(const cim_half_tiles *H, int32_t k);
 
+/*
+ * Device: G = Aᵀ·B in float64 for tall row-major blocks A (rows × ca, leading
+ * dimension lda) and B (rows × cb, ldb) of dtype CIM_F32 or CIM_F64, with
+ * 1 ≤ ca, cb ≤ 64; out is a device double[ca·cb] (row-major ca × cb).
+ * Accumulates in f64 with a fixed reduction order (reproducible).  The
+ * eigensolver's Gram / Rayleigh–Ritz products (lobpcg.py; BASELINE config 5).
+ * workspace: cim_gram_workspace_bytes(rows, ca, cb) device bytes.
+ *
+ * Replaces: the reference's float64 oracle reductions over pair lists
+ * (contract_oracle, pipeline.py:573-589) — here for the block products that
+ * wrap the SpMM.
+ */
+CIM_API int cim_gram(const void *A, int64_t lda, int32_t ca, const void *B, int64_t ldb,
+                     int32_t cb, int64_t rows, int32_t dtype, double *out,
+                     void *workspace, uint64_t ws_bytes, void *stream);
+
+/*
+ * Device: Out = alpha·A·C + beta·Out for a tall f32 block A (rows × q, lda),
+ * a small row-major f32 matrix C (q × p, device) and Out (rows × p, ldo),
+ * 1 ≤ q, p ≤ 64 (beta = 0: Out is not read).  The eigensolver's block
+ * updates, written straight into column slots of its work buffer.
+ */
+CIM_API int cim_tsmm(const float *A, int64_t lda, int32_t q, const float *C, int32_t p,
+                     float alpha, float beta, float *Out, int64_t ldo, int64_t rows,
+                     void *stream);
+
+/*
+ * Column-blocked variants: an operand of `cols` columns stored as blocks of
+ * bw ∈ {4,8,16,32,64} columns, element (r, c) at
+ * base + (c / bw)·bstride + r·ld + (c % bw)  (elements) — e.g. the eigensolver's
+ * block-major work buffer [slot][row][bw], where a column slice of a wide
+ * row-major buffer would waste most of every DRAM burst.
+ */
+CIM_API int cim_gram_blocked(const void *A, int64_t lda, int32_t a_bw, int64_t a_bstride, int32_t ca,
+                             const void *B, int64_t ldb, int32_t b_bw, int64_t b_bstride, int32_t cb,
+                             int64_t rows, int32_t dtype, double *out, void *workspace,
+                             uint64_t ws_bytes, void *stream);
+CIM_API int cim_tsmm_blocked(const float *A, int64_t lda, int32_t a_bw, int64_t a_bstride, int32_t q,
+                             const float *C, int32_t p, float alpha, float beta, float *Out,
+                             int64_t ldo, int32_t o_bw, int64_t o_bstride, int64_t rows, void *stream);
+
+/* Device workspace bytes cim_gram / cim_gram_blocked need. */
+CIM_API uint64_t cim_gram_workspace_bytes(int64_t rows, int32_t ca, int32_t cb);
+
 /* 1 if (dtype, k) has a compiled kernel for CIM_LAYOUT_FRAG tiles, else 0. */
 CIM_API int cim_sym_spmm_supported(int32_t dtype, int32_t k);
 

@@ -35,6 +35,11 @@ EXPORTS = (
     "cim_hash_values",
     "cim_sym_spmm_host_batch",
     "cim_host_batch_workspace_bytes",
+    "cim_gram",
+    "cim_gram_workspace_bytes",
+    "cim_tsmm",
+    "cim_gram_blocked",
+    "cim_tsmm_blocked",
 )
 
 
@@ -94,10 +99,22 @@ def lib() -> ctypes.CDLL:
     L.cim_sym_spmm_host_batch.argtypes = [c.POINTER(CimHalfTiles), c.POINTER(c.c_void_p), c.POINTER(c.c_void_p),
                                           c.c_int32, c.c_int32, c.c_void_p, c.c_uint64]
     L.cim_host_batch_workspace_bytes.argtypes = [c.POINTER(CimHalfTiles), c.c_int32]
+    L.cim_gram.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_void_p, c.c_int64, c.c_int32, c.c_int64, c.c_int32,
+                           c.c_void_p, c.c_void_p, c.c_uint64, c.c_void_p]
+    L.cim_gram_workspace_bytes.argtypes = [c.c_int64, c.c_int32, c.c_int32]
+    L.cim_tsmm.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_void_p, c.c_int32, c.c_float, c.c_float, c.c_void_p,
+                           c.c_int64, c.c_int64, c.c_void_p]
+    L.cim_gram_blocked.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_int64, c.c_int32, c.c_void_p, c.c_int64,
+                                   c.c_int32, c.c_int64, c.c_int32, c.c_int64, c.c_int32, c.c_void_p, c.c_void_p,
+                                   c.c_uint64, c.c_void_p]
+    L.cim_tsmm_blocked.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_int64, c.c_int32, c.c_void_p, c.c_int32,
+                                   c.c_float, c.c_float, c.c_void_p, c.c_int64, c.c_int32, c.c_int64, c.c_int64,
+                                   c.c_void_p]
     for name in EXPORTS:
         if name not in ("cim_version", "cim_last_error"):
             getattr(L, name).restype = c.c_int
     L.cim_host_batch_workspace_bytes.restype = c.c_uint64
+    L.cim_gram_workspace_bytes.restype = c.c_uint64
     _lib = L
     return L
 

@@ -1,0 +1,478 @@
+// Tall-skinny block products for the eigensolver (C-ABI cim_gram, cim_tsmm).
+//
+// cim_gram: G = Aᵀ·B in float64.
+//
+// LOBPCG (config C5, lobpcg.py) needs, per iteration, several Gram matrices of
+// row-distributed blocks with n = 2²² rows and ≤ 64 columns (Sᵀ·AS, Sᵀ·S,
+// Rᵀ·R, the Cholesky-QR passes).  cuBLAS treats them as M, N ≤ 64, K = 4M
+// GEMMs and torch first materialises float64 copies of both operands; this
+// kernel reads the f32 (or f64) operands once from HBM, widens them to f64 in
+// shared memory and accumulates in f64 — the product is HBM-bound
+// (rows·(ca+cb)·s bytes) with DFMA work rows·ca·cb.
+//
+// Grid-stride over 128-row slabs, double-buffered with cp.async; each CTA
+// stages slabs of A and B in shared memory (input dtype, widened on use), and each thread owns a 4×4 block of G for a residue
+// class of the slab's rows.  Per-CTA partials go to a workspace and a second
+// kernel sums them in a fixed order (bit-reproducible run to run).
+#include <algorithm>
+#include <cstdint>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "cim_b200.h"
+#include "host_util.h"
+
+namespace {
+
+constexpr int kGramThreads = 128;
+constexpr int kMaxCols = 64;
+
+// A column-blocked tall operand: element (r, c) at p + (c >> bw_shift)·bstride
+// + r·ld + (c & (bw-1)).  One plain row-major block is bw = 64, bstride = 0.
+struct Operand {
+  const void *p;
+  long long ld, bstride;
+  int bw_shift, cols;
+};
+
+__host__ __device__ __forceinline__ int pad8(int c) { return (c + 7) & ~7; }
+
+// Rows per slab: ~4K elements per operand pair (16 KB of f32 per stage;
+// kGramStages stages in flight per CTA whatever the column counts).
+constexpr int kGramStages = 4;
+__host__ __device__ __forceinline__ int slab_rows(int cap, int cbp) {
+  const int r = 4096 / (cap + cbp);
+  return r < 32 ? 32 : (r > 1024 ? 1024 : (r & ~7));
+}
+
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+
+// Shared-memory slab layout: each operand as 8-column blocks [blk][row][8],
+// consecutive blocks skewed by 8 elements so the 8×8 register tiles of one
+// warp (same row, different blocks) hit different banks.
+__host__ __device__ __forceinline__ int sblk_stride(int slab) { return slab * 8 + 8; }
+
+// Load modes of an operand for one slab (decided once per launch):
+//  0 = blocked, bw = 8, ld = 8: each 8-column block of the slab is one
+//      contiguous run → 16-byte copies with trivial addressing;
+//  1 = row-major, 16-byte aligned, ld % (16/s) == 0: 16-byte copies;
+//  2 = anything else: element copies.
+template <typename T>
+__device__ __forceinline__ void load_operand(T *dst, const Operand &o, int mode, int slab, long long r0, int nr,
+                                             float inv_c) {
+  constexpr int V = 16 / sizeof(T);  // elements per 16-byte chunk
+  const T *base = static_cast<const T *>(o.p);
+  const int sbs = sblk_stride(slab);
+  const int nb8 = (o.cols + 7) / 8;
+  if (mode == 0) {
+    const int per = nr * 8 / V;  // chunks per block
+    for (int b = 0; b < nb8; ++b) {
+      const T *src = base + (long long)b * o.bstride + r0 * 8;
+      T *d = dst + b * sbs;
+      for (int e = threadIdx.x; e < per; e += kGramThreads) cp_async16(d + e * V, src + e * V);
+    }
+  } else if (mode == 1) {
+    const int cpr = (o.cols + V - 1) / V;  // chunks per row
+    const int n = nr * cpr;
+    for (int e = threadIdx.x; e < n; e += kGramThreads) {
+      const int r = e / cpr, ch = e - r * cpr, c = ch * V;
+      cp_async16(dst + (c >> 3) * sbs + r * 8 + (c & 7), base + (r0 + r) * o.ld + c);
+    }
+  } else {
+    const int n = nr * o.cols, mask = (1 << o.bw_shift) - 1;
+    for (int e = threadIdx.x; e < n; e += kGramThreads) {
+      const int r = __float2int_rz(((float)e + 0.5f) * inv_c);
+      const int c = e - r * o.cols;
+      const T *src = base + (long long)(c >> o.bw_shift) * o.bstride + (r0 + r) * o.ld + (c & mask);
+      T *d = dst + (c >> 3) * sbs + r * 8 + (c & 7);
+      if constexpr (sizeof(T) == 4)
+        cp_async4(d, src);
+      else
+        cp_async8(d, src);
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void load8(double (&d)[8], const T *p) {
+  if constexpr (sizeof(T) == 4) {
+    const float4 a = *reinterpret_cast<const float4 *>(p);
+    const float4 b = *reinterpret_cast<const float4 *>(p + 4);
+    d[0] = a.x, d[1] = a.y, d[2] = a.z, d[3] = a.w, d[4] = b.x, d[5] = b.y, d[6] = b.z, d[7] = b.w;
+  } else {
+    const double4 a = *reinterpret_cast<const double4 *>(p);
+    const double4 b = *reinterpret_cast<const double4 *>(p + 4);
+    d[0] = a.x, d[1] = a.y, d[2] = a.z, d[3] = a.w, d[4] = b.x, d[5] = b.y, d[6] = b.z, d[7] = b.w;
+  }
+}
+
+// A kGramStages-deep cp.async ring of slabs (input dtype); each thread owns
+// an 8×8 block of G for one residue class of a slab's rows and widens its 16
+// operands per row to f64 on use (16 F2F per 64 DFMA).
+template <typename T>
+__global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const Operand A, const Operand B, int mode_a,
+                                                                    int mode_b, long long rows,
+                                                                    double *__restrict__ part) {
+  extern __shared__ __align__(32) unsigned char smem_raw[];
+  const int ca = A.cols, cb = B.cols;
+  const int cap = pad8(ca), cbp = pad8(cb);
+  const int kSlab = slab_rows(cap, cbp);
+  const int sbs = sblk_stride(kSlab);
+  const int nbi = cap / 8, nbj = cbp / 8, nblk = nbi * nbj;
+  const int stage_elems = (nbi + nbj) * sbs;
+  T *ring = reinterpret_cast<T *>(smem_raw);
+  const int red_cap = (int)((kGramStages * (size_t)stage_elems * sizeof(T)) / (sizeof(double) * cap * cbp));
+  const int split = min(kGramThreads / nblk, red_cap);  // row residue classes (≥ 1)
+  const int t = threadIdx.x;
+  const int blk = t % nblk, grp = t / nblk;
+  const bool active = grp < split;
+  const int bi = blk / nbj, bj = blk % nbj;
+  const float inv_ca = 1.0f / (float)ca, inv_cb = 1.0f / (float)cb;
+  for (int e = t; e < kGramStages * stage_elems; e += kGramThreads) ring[e] = T(0);  // pads stay zero
+  __syncthreads();
+  double acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+
+  const long long nslabs = (rows + kSlab - 1) / kSlab;
+  auto issue = [&](long long k) {  // this CTA's k-th slab into ring stage k % S (rows ≥ nr never read)
+    const long long sl = blockIdx.x + k * gridDim.x;
+    if (sl < nslabs) {
+      const long long r0 = sl * kSlab;
+      const int nr = (int)min((long long)kSlab, rows - r0);
+      T *st = ring + (size_t)(k % kGramStages) * stage_elems;
+      load_operand(st, A, mode_a, kSlab, r0, nr, inv_ca);
+      load_operand(st + nbi * sbs, B, mode_b, kSlab, r0, nr, inv_cb);
+    }
+    cp_async_commit();  // possibly empty group: keeps the wait arithmetic uniform
+  };
+  for (int k = 0; k < kGramStages - 1; ++k) issue(k);
+  for (long long k = 0;; ++k) {
+    const long long sl = blockIdx.x + k * gridDim.x;
+    if (sl >= nslabs) break;
+    cp_async_wait<kGramStages - 2>();  // slab k has landed (this thread's copies) ...
+    __syncthreads();                   // ... everyone's, and slab k-1's stage is free
+    issue(k + kGramStages - 1);
+    const long long r0 = sl * kSlab;
+    const int nr = (int)min((long long)kSlab, rows - r0);
+    const T *sa = ring + (size_t)(k % kGramStages) * stage_elems + bi * sbs;
+    const T *sb = ring + (size_t)(k % kGramStages) * stage_elems + (nbi + bj) * sbs;
+    if (active) {
+      for (int r = grp; r < nr; r += split) {
+        double av[8], bv[8];
+        load8<T>(av, sa + r * 8);
+        load8<T>(bv, sb + r * 8);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+      }
+    }
+  }
+  cp_async_wait<0>();
+  // CTA reduction over the row residue classes (fixed order) in the ring
+  __syncthreads();
+  double *red = reinterpret_cast<double *>(smem_raw);
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) red[(size_t)grp * cap * cbp + (8 * bi + i) * cbp + 8 * bj + j] = acc[i][j];
+  }
+  __syncthreads();
+  double *out = part + (size_t)blockIdx.x * ca * cb;
+  for (int e = t; e < ca * cb; e += kGramThreads) {
+    const int i = e / cb, j = e % cb;
+    double s = 0.0;
+    for (int g = 0; g < split; ++g) s += red[(size_t)g * cap * cbp + i * cbp + j];
+    out[e] = s;
+  }
+}
+
+__global__ void gram_sum_kernel(const double *__restrict__ part, int nparts, int count, double *__restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= count) return;
+  double s = 0.0;
+  for (int p = 0; p < nparts; ++p) s += part[(size_t)p * count + e];
+  out[e] = s;
+}
+
+size_t gram_smem(int ca, int cb, size_t es) {
+  const int cap = pad8(ca), cbp = pad8(cb);
+  return (size_t)kGramStages * ((cap + cbp) / 8) * sblk_stride(slab_rows(cap, cbp)) * es;
+}
+
+int load_mode(const Operand &o, size_t es) {
+  const int V = 16 / (int)es;
+  const bool aligned = !(reinterpret_cast<uintptr_t>(o.p) & 15);
+  if (aligned && o.bw_shift == 3 && o.ld == 8 && (o.bstride % V) == 0) return 0;
+  if (aligned && (o.cols <= (1 << o.bw_shift)) && (o.ld % V) == 0 && (o.cols % V) == 0) return 1;
+  return 2;
+}
+
+int gram_grid(long long rows, int ca, int cb) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int kSlab = slab_rows(pad8(ca), pad8(cb));
+  const long long slabs = (rows + kSlab - 1) / kSlab;
+  return (int)std::min<long long>(slabs > 0 ? slabs : 1, 2LL * sms);
+}
+
+int bw_shift_of(int32_t bw) {
+  for (int s = 2; s <= 6; ++s)
+    if (bw == (1 << s)) return s;
+  return -1;
+}
+
+int gram_impl(const Operand &A, const Operand &B, long long rows, int32_t dtype, double *out, void *workspace,
+              uint64_t ws_bytes, cudaStream_t stream) {
+  const int ca = A.cols, cb = B.cols;
+  if (ca < 1 || cb < 1 || ca > kMaxCols || cb > kMaxCols)
+    return cim::set_error(CIM_EINVAL, "column counts must be in [1, 64]");
+  if (rows < 0) return cim::set_error(CIM_EINVAL, "rows must be >= 0");
+  if (dtype != CIM_F32 && dtype != CIM_F64) return cim::set_error(CIM_EINVAL, "dtype must be CIM_F32 or CIM_F64");
+  if (!out || (rows > 0 && (!A.p || !B.p))) return cim::set_error(CIM_EINVAL, "NULL pointer");
+  const int grid = gram_grid(rows, ca, cb);
+  const uint64_t need = (uint64_t)grid * ca * cb * sizeof(double);
+  if (!workspace || ws_bytes < need)
+    return cim::set_error(CIM_EINVAL, "workspace must hold " + std::to_string(need) + " bytes");
+  const size_t es = dtype == CIM_F32 ? 4 : 8;
+  const size_t smem = gram_smem(ca, cb, es);
+  const int ma = load_mode(A, es), mb = load_mode(B, es);
+  cudaError_t e;
+  if (dtype == CIM_F32) {
+    e = cudaFuncSetAttribute(gram_partial_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      gram_partial_kernel<float><<<grid, kGramThreads, smem, stream>>>(A, B, ma, mb, rows,
+                                                                       static_cast<double *>(workspace));
+  } else {
+    e = cudaFuncSetAttribute(gram_partial_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      gram_partial_kernel<double><<<grid, kGramThreads, smem, stream>>>(A, B, ma, mb, rows,
+                                                                        static_cast<double *>(workspace));
+  }
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return cim::set_error(CIM_ECUDA, std::string("gram_partial_kernel: ") + cudaGetErrorString(e));
+  const int count = ca * cb;
+  gram_sum_kernel<<<(count + 127) / 128, 128, 0, stream>>>(static_cast<const double *>(workspace), grid, count, out);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cim::set_error(CIM_ECUDA, std::string("gram_sum_kernel: ") + cudaGetErrorString(e));
+  return CIM_OK;
+}
+
+}  // namespace
+
+extern "C" uint64_t cim_gram_workspace_bytes(int64_t rows, int32_t ca, int32_t cb) {
+  if (rows < 0 || ca < 1 || cb < 1) return 0;
+  return (uint64_t)gram_grid(rows, ca, cb) * (uint64_t)ca * (uint64_t)cb * sizeof(double);
+}
+
+extern "C" int cim_gram(const void *A, int64_t lda, int32_t ca, const void *B, int64_t ldb, int32_t cb, int64_t rows,
+                        int32_t dtype, double *out, void *workspace, uint64_t ws_bytes, void *stream_) {
+  cim::clear_error();
+  if (lda < ca || ldb < cb) return cim::set_error(CIM_EINVAL, "leading dimensions must cover the columns");
+  const Operand a{A, lda, 0, 6, ca}, b{B, ldb, 0, 6, cb};
+  return gram_impl(a, b, rows, dtype, out, workspace, ws_bytes, reinterpret_cast<cudaStream_t>(stream_));
+}
+
+extern "C" int cim_gram_blocked(const void *A, int64_t lda, int32_t a_bw, int64_t a_bstride, int32_t ca,
+                                const void *B, int64_t ldb, int32_t b_bw, int64_t b_bstride, int32_t cb, int64_t rows,
+                                int32_t dtype, double *out, void *workspace, uint64_t ws_bytes, void *stream_) {
+  cim::clear_error();
+  const int sa = bw_shift_of(a_bw), sb = bw_shift_of(b_bw);
+  if (sa < 0 || sb < 0) return cim::set_error(CIM_EINVAL, "block widths must be 4, 8, 16, 32 or 64");
+  if (lda < std::min(a_bw, ca) || ldb < std::min(b_bw, cb))
+    return cim::set_error(CIM_EINVAL, "leading dimensions must cover a block");
+  const Operand a{A, lda, a_bstride, sa, ca}, b{B, ldb, b_bstride, sb, cb};
+  return gram_impl(a, b, rows, dtype, out, workspace, ws_bytes, reinterpret_cast<cudaStream_t>(stream_));
+}
+
+// ---------------------------------------------------------------------------
+// Tall-skinny block times small matrix:  Out = alpha·A·C + beta·Out
+// (C-ABI cim_tsmm).  A: rows × q (lda), C: q × p row-major f32 (device),
+// Out: rows × p (ldo); q, p ≤ 64.  The eigensolver's block updates
+// (projections, Cholesky-QR back-substitution, Ritz-vector assembly) write
+// straight into column slots of a shared [P X W | AP AX AW] buffer; cuBLAS
+// needs dense outputs (and runs these K ≤ 64 shapes on SIMT tiles).  One
+// thread per row, C staged in shared memory: HBM-bound, rows·(q+p)·4 bytes.
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int kTsmmThreads = 256;
+
+struct MutOperand {
+  float *p;
+  long long ld, bstride;
+  int bw_shift;
+};
+
+__device__ __forceinline__ const float *elem(const Operand &o, long long r, int c) {
+  return static_cast<const float *>(o.p) + (long long)(c >> o.bw_shift) * o.bstride + r * o.ld +
+         (c & ((1 << o.bw_shift) - 1));
+}
+__device__ __forceinline__ float *elem(const MutOperand &o, long long r, int c) {
+  return o.p + (long long)(c >> o.bw_shift) * o.bstride + r * o.ld + (c & ((1 << o.bw_shift) - 1));
+}
+
+// Generic path (any q, p, alignment): one row per thread.
+__global__ void __launch_bounds__(kTsmmThreads) tsmm_scalar_kernel(const Operand A, const float *__restrict__ C,
+                                                                   int p, float alpha, float beta,
+                                                                   const MutOperand Out, long long rows) {
+  __shared__ float sc[64 * 64];
+  const int q = A.cols;
+  for (int e = threadIdx.x; e < q * p; e += kTsmmThreads) sc[e] = C[e];
+  __syncthreads();
+  for (long long r = (long long)blockIdx.x * kTsmmThreads + threadIdx.x; r < rows;
+       r += (long long)gridDim.x * kTsmmThreads) {
+    for (int j = 0; j < p; ++j) {
+      float acc = 0.f;
+      for (int i = 0; i < q; ++i) acc = fmaf(*elem(A, r, i), sc[i * p + j], acc);
+      float *o = elem(Out, r, j);
+      *o = (beta == 0.f) ? alpha * acc : fmaf(beta, *o, alpha * acc);
+    }
+  }
+}
+
+// Vector path (q, p, leading dimensions, block strides multiples of 4,
+// 16-byte aligned): each thread owns RB rows and a 16-column strip; A rows
+// arrive as float4, C rows as broadcast LDS.128 (one shared load feeds 4·RB FMAs).
+template <int RB>
+__global__ void __launch_bounds__(kTsmmThreads) tsmm_vec_kernel(const Operand A, const float *__restrict__ C, int p,
+                                                                float alpha, float beta, const MutOperand Out,
+                                                                long long rows) {
+  __shared__ __align__(16) float sc[64 * 64];
+  const int q = A.cols;
+  for (int e = threadIdx.x; e < q * p; e += kTsmmThreads) sc[e] = C[e];
+  __syncthreads();
+  const long long groups = (rows + RB - 1) / RB;
+  for (long long g = (long long)blockIdx.x * kTsmmThreads + threadIdx.x; g < groups;
+       g += (long long)gridDim.x * kTsmmThreads) {
+    const long long r0 = g * RB;
+    const int nr = (int)min((long long)RB, rows - r0);
+    for (int j0 = 0; j0 < p; j0 += 16) {
+      const int jq = min(16, p - j0) / 4;  // float4 column chunks in this strip
+      float4 acc[RB][4];
+#pragma unroll
+      for (int b = 0; b < RB; ++b)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[b][c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int i = 0; i < q; i += 4) {
+        float av[RB][4];
+#pragma unroll
+        for (int b = 0; b < RB; ++b) {
+          const float4 v =
+              (b < nr) ? *reinterpret_cast<const float4 *>(elem(A, r0 + b, i)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          av[b][0] = v.x, av[b][1] = v.y, av[b][2] = v.z, av[b][3] = v.w;
+        }
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            if (c < jq) {
+              const float4 cv = *reinterpret_cast<const float4 *>(sc + (i + ii) * p + j0 + 4 * c);
+#pragma unroll
+              for (int b = 0; b < RB; ++b) {
+                acc[b][c].x = fmaf(av[b][ii], cv.x, acc[b][c].x);
+                acc[b][c].y = fmaf(av[b][ii], cv.y, acc[b][c].y);
+                acc[b][c].z = fmaf(av[b][ii], cv.z, acc[b][c].z);
+                acc[b][c].w = fmaf(av[b][ii], cv.w, acc[b][c].w);
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < RB; ++b) {
+        if (b >= nr) break;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c < jq) {
+            float4 *o = reinterpret_cast<float4 *>(elem(Out, r0 + b, j0 + 4 * c));
+            float4 r = acc[b][c];
+            if (beta == 0.f) {
+              r.x *= alpha, r.y *= alpha, r.z *= alpha, r.w *= alpha;
+            } else {
+              const float4 prev = *o;
+              r.x = fmaf(beta, prev.x, alpha * r.x), r.y = fmaf(beta, prev.y, alpha * r.y);
+              r.z = fmaf(beta, prev.z, alpha * r.z), r.w = fmaf(beta, prev.w, alpha * r.w);
+            }
+            *o = r;
+          }
+        }
+      }
+    }
+  }
+}
+
+int tsmm_impl(const Operand &A, const float *C, int p, float alpha, float beta, const MutOperand &Out, long long rows,
+              int out_bw, cudaStream_t stream) {
+  const int q = A.cols;
+  if (q < 1 || p < 1 || q > 64 || p > 64) return cim::set_error(CIM_EINVAL, "q and p must be in [1, 64]");
+  if (rows < 0) return cim::set_error(CIM_EINVAL, "rows must be >= 0");
+  if (rows == 0) return CIM_OK;
+  if (!A.p || !C || !Out.p) return cim::set_error(CIM_EINVAL, "NULL pointer");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int a_bw = 1 << A.bw_shift;
+  const bool vec = (q % 4 == 0) && (p % 4 == 0) && (A.ld % 4 == 0) && (Out.ld % 4 == 0) && (A.bstride % 4 == 0) &&
+                   (Out.bstride % 4 == 0) && (a_bw % 4 == 0) && (out_bw % 4 == 0) &&
+                   !(reinterpret_cast<uintptr_t>(A.p) & 15) && !(reinterpret_cast<uintptr_t>(Out.p) & 15);
+  if (vec) {
+    constexpr int RB = 2;
+    const long long groups = (rows + RB - 1) / RB;
+    const long long blocks = std::min<long long>((groups + kTsmmThreads - 1) / kTsmmThreads, 8LL * sms);
+    tsmm_vec_kernel<RB><<<(unsigned)blocks, kTsmmThreads, 0, stream>>>(A, C, p, alpha, beta, Out, rows);
+  } else {
+    const long long blocks = std::min<long long>((rows + kTsmmThreads - 1) / kTsmmThreads, 8LL * sms);
+    tsmm_scalar_kernel<<<(unsigned)blocks, kTsmmThreads, 0, stream>>>(A, C, p, alpha, beta, Out, rows);
+  }
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cim::set_error(CIM_ECUDA, std::string("tsmm kernel: ") + cudaGetErrorString(e));
+  return CIM_OK;
+}
+
+}  // namespace
+
+extern "C" int cim_tsmm(const float *A, int64_t lda, int32_t q, const float *C, int32_t p, float alpha, float beta,
+                        float *Out, int64_t ldo, int64_t rows, void *stream_) {
+  cim::clear_error();
+  if (lda < q || ldo < p) return cim::set_error(CIM_EINVAL, "bad leading dimensions");
+  const Operand a{A, lda, 0, 6, q};
+  const MutOperand o{Out, ldo, 0, 6};
+  return tsmm_impl(a, C, p, alpha, beta, o, rows, 64, reinterpret_cast<cudaStream_t>(stream_));
+}
+
+extern "C" int cim_tsmm_blocked(const float *A, int64_t lda, int32_t a_bw, int64_t a_bstride, int32_t q,
+                                const float *C, int32_t p, float alpha, float beta, float *Out, int64_t ldo,
+                                int32_t o_bw, int64_t o_bstride, int64_t rows, void *stream_) {
+  cim::clear_error();
+  const int sa = bw_shift_of(a_bw), so = bw_shift_of(o_bw);
+  if (sa < 0 || so < 0) return cim::set_error(CIM_EINVAL, "block widths must be 4, 8, 16, 32 or 64");
+  if (lda < std::min(a_bw, q) || ldo < std::min(o_bw, p))
+    return cim::set_error(CIM_EINVAL, "leading dimensions must cover a block");
+  const Operand a{A, lda, a_bstride, sa, q};
+  const MutOperand o{Out, ldo, o_bstride, so};
+  return tsmm_impl(a, C, p, alpha, beta, o, rows, o_bw, reinterpret_cast<cudaStream_t>(stream_));
+}

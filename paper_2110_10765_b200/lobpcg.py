@@ -47,25 +47,85 @@ def _allreduce(t: torch.Tensor, group) -> torch.Tensor:
     return t
 
 
+_GRAM_WS: dict = {}
+
+
+def gram_f64(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """aᵀ·b in float64 on the device through the C-ABI ``cim_gram`` (f32/f64
+    tall blocks read once, f64 accumulation, fixed reduction order)."""
+    from ._lib import CIM_F32, CIM_F64, check, lib
+
+    if a.shape[0] != b.shape[0] or a.dtype != b.dtype or a.device != b.device:
+        raise ValueError("gram operands must share rows, dtype and device")
+    if a.dtype not in (torch.float32, torch.float64):
+        raise ValueError(f"gram needs float32/float64 blocks, got {a.dtype}")
+    if a.stride(1) != 1 or a.stride(0) < a.shape[1]:
+        a = a.contiguous()
+    if b.stride(1) != 1 or b.stride(0) < b.shape[1]:
+        b = b.contiguous()
+    rows, ca, cb = a.shape[0], a.shape[1], b.shape[1]
+    out = torch.empty((ca, cb), dtype=torch.float64, device=a.device)
+    if ca == 0 or cb == 0:
+        return out
+    L = lib()
+    need = int(L.cim_gram_workspace_bytes(rows, ca, cb))
+    ws = _GRAM_WS.get(a.device)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(max(need, 16), dtype=torch.uint8, device=a.device)
+        _GRAM_WS[a.device] = ws
+    with torch.cuda.device(a.device):
+        check(L.cim_gram(a.data_ptr(), a.stride(0), ca, b.data_ptr(), b.stride(0), cb, rows,
+                         CIM_F32 if a.dtype == torch.float32 else CIM_F64, out.data_ptr(), ws.data_ptr(), need,
+                         torch.cuda.current_stream(a.device).cuda_stream), "cim_gram")
+    return out
+
+
 def _gram(a: torch.Tensor, b: torch.Tensor, group) -> np.ndarray:
-    """aᵀ b summed over ranks, in float64 on the host."""
-    g = (a.to(torch.float64).T @ b.to(torch.float64)).contiguous()
+    """aᵀ b summed over ranks, in float64 on the host.  CUDA blocks go through
+    the native f64-accumulating kernel; CPU blocks (gloo tests, CPU operators)
+    through torch in float64."""
+    if a.is_cuda:
+        g = gram_f64(a, b)
+    else:
+        g = (a.to(torch.float64).T @ b.to(torch.float64)).contiguous()
     return _allreduce(g, group).cpu().numpy()
 
 
-def _orthonormalize(V: torch.Tensor, group, eps: float = 1e-12) -> torch.Tensor:
-    """Cholesky-QR (twice for stability) of a distributed tall block; columns
-    that are numerically dependent are dropped."""
-    for _ in range(2):
-        M = _gram(V, V, group)
-        M = 0.5 * (M + M.T)
-        w, U = np.linalg.eigh(M)
-        keep = w > eps * max(w.max(), 1e-300)
-        if not keep.any():
-            return V[:, :0]
-        T = U[:, keep] / np.sqrt(w[keep])  # V·T has orthonormal columns
-        V = V @ torch.from_numpy(T).to(V.device, V.dtype)
-    return V
+def tsmm(A: torch.Tensor, C: torch.Tensor, out: torch.Tensor, alpha: float = 1.0, beta: float = 0.0) -> None:
+    """out ← alpha·A·C + beta·out for a tall block A and a small C, writing in
+    place into ``out`` (which may be a column-slice view of a wider buffer).
+    CUDA float32 goes through the native ``cim_tsmm``; other cases (CPU
+    operators in tests, float64) through torch."""
+    if A.shape[1] == 0:
+        if beta == 0.0:
+            out.zero_()
+        elif beta != 1.0:
+            out.mul_(beta)
+        return
+    if (A.is_cuda and A.dtype == torch.float32 and A.stride(1) == 1 and out.stride(1) == 1
+            and A.shape[1] <= 64 and out.shape[1] <= 64):
+        from ._lib import check, lib
+
+        Cd = C.to(A.device, torch.float32).contiguous()
+        with torch.cuda.device(A.device):
+            check(lib().cim_tsmm(A.data_ptr(), A.stride(0), A.shape[1], Cd.data_ptr(), Cd.shape[1], float(alpha),
+                                 float(beta), out.data_ptr(), out.stride(0), A.shape[0],
+                                 torch.cuda.current_stream(A.device).cuda_stream), "cim_tsmm")
+        return
+    prod = A @ C.to(A.device, A.dtype)
+    if beta == 0.0:
+        out.copy_(prod if alpha == 1.0 else alpha * prod)
+    else:
+        out.mul_(beta).add_(prod, alpha=alpha)
+
+
+def _orth_factor(M: np.ndarray, eps: float = 1e-12) -> np.ndarray:
+    """T with (V·T)ᵀ(V·T) = I given M = VᵀV; numerically dependent columns
+    are dropped (T has ≤ M.shape[0] columns)."""
+    M = 0.5 * (M + M.T)
+    w, U = np.linalg.eigh(M)
+    keep = w > eps * max(w.max(), 1e-300)
+    return U[:, keep] / np.sqrt(w[keep])
 
 
 def _rayleigh_ritz(G: np.ndarray, M: np.ndarray, m: int, largest: bool, eps: float = 1e-10):
@@ -81,6 +141,121 @@ def _rayleigh_ritz(G: np.ndarray, M: np.ndarray, m: int, largest: bool, eps: flo
     return lam[sel], T @ Z[:, sel]
 
 
+class _Work:
+    """Block-major work buffer: six slots [P, X, W, AP, AX, AW], each a
+    contiguous (rows × bw) block, bw = m rounded up to a power of two (≥ 4;
+    padding columns stay zero).  Slot ranges are handed to the native
+    column-blocked kernels (``cim_gram_blocked`` / ``cim_tsmm_blocked``) as
+    one operand; a block-major layout keeps every DRAM burst useful, where
+    column slices of one wide row-major buffer fetched 4× their bytes."""
+
+    P, X, W, AP, AX, AW = range(6)
+
+    def __init__(self, rows: int, m: int, dtype, device):
+        self.m, self.rows = m, rows
+        self.bw = max(4, 1 << (m - 1).bit_length())
+        self.buf = torch.zeros((6, rows, self.bw), dtype=dtype, device=device)
+
+    def slot(self, s: int, ncols: int | None = None) -> torch.Tensor:
+        return self.buf[s][:, : (self.m if ncols is None else ncols)]
+
+    def vidx(self, slots, widths) -> np.ndarray:
+        """Virtual column indices (slot-range-relative) of the real columns."""
+        out = []
+        for k, (s, w) in enumerate(zip(slots, widths)):
+            out.extend(k * self.bw + j for j in range(w))
+        return np.asarray(out, dtype=np.int64)
+
+    def _native(self) -> bool:
+        return self.buf.is_cuda and self.buf.dtype in (torch.float32, torch.float64)
+
+    def dense(self, s0: int, s1: int) -> torch.Tensor:
+        return self.buf[s0:s1].permute(1, 0, 2).reshape(self.rows, (s1 - s0) * self.bw)
+
+    def gram(self, a0: int, a1: int, b0: int, b1: int, group) -> np.ndarray:
+        """[slots a0..a1)ᵀ·[slots b0..b1) in float64 (virtual columns), summed over ranks."""
+        ca, cb = (a1 - a0) * self.bw, (b1 - b0) * self.bw
+        if self._native() and ca <= 64 and cb <= 64:
+            from ._lib import CIM_F32, CIM_F64, check, lib
+
+            L = lib()
+            out = torch.empty((ca, cb), dtype=torch.float64, device=self.buf.device)
+            need = int(L.cim_gram_workspace_bytes(self.rows, ca, cb))
+            ws = _workspace(self.buf.device, need)
+            bs = self.rows * self.bw
+            with torch.cuda.device(self.buf.device):
+                check(L.cim_gram_blocked(self.buf[a0].data_ptr(), self.bw, self.bw, bs, ca, self.buf[b0].data_ptr(),
+                                         self.bw, self.bw, bs, cb, self.rows,
+                                         CIM_F32 if self.buf.dtype == torch.float32 else CIM_F64, out.data_ptr(),
+                                         ws.data_ptr(), need, torch.cuda.current_stream(self.buf.device).cuda_stream),
+                      "cim_gram_blocked")
+            return _allreduce(out, group).cpu().numpy()
+        if self.buf.is_cuda and (ca > 64 or cb > 64):  # wide blocks: one slot pair at a time, natively
+            G = np.zeros((ca, cb))
+            for i in range(a0, a1):
+                for j in range(b0, b1):
+                    G[(i - a0) * self.bw:(i - a0 + 1) * self.bw, (j - b0) * self.bw:(j - b0 + 1) * self.bw] = \
+                        self.gram(i, i + 1, j, j + 1, group)
+            return G
+        return _gram(self.dense(a0, a1), self.dense(b0, b1), group)
+
+    def tsmm(self, a0: int, a1: int, C: np.ndarray, dst: "_Work", o0: int, o1: int, alpha=1.0, beta=0.0) -> None:
+        """dst[slots o0..o1) ← alpha·[slots a0..a1)·C + beta·dst (virtual columns)."""
+        q, p = (a1 - a0) * self.bw, (o1 - o0) * self.bw
+        if self._native() and self.buf.dtype == torch.float32 and q <= 64 and p <= 64:
+            from ._lib import check, lib
+
+            Cd = torch.from_numpy(np.ascontiguousarray(C, dtype=np.float32)).to(self.buf.device)
+            with torch.cuda.device(self.buf.device):
+                check(lib().cim_tsmm_blocked(self.buf[a0].data_ptr(), self.bw, self.bw, self.rows * self.bw, q,
+                                             Cd.data_ptr(), p, float(alpha), float(beta), dst.buf[o0].data_ptr(),
+                                             self.bw, self.bw, self.rows * self.bw, self.rows,
+                                             torch.cuda.current_stream(self.buf.device).cuda_stream),
+                      "cim_tsmm_blocked")
+            return
+        prod = self.dense(a0, a1) @ torch.from_numpy(C).to(self.buf.device, self.buf.dtype)
+        for k, s in enumerate(range(o0, o1)):
+            blk = prod[:, k * self.bw:(k + 1) * self.bw]
+            if beta == 0.0:
+                dst.buf[s].copy_(alpha * blk)
+            else:
+                dst.buf[s].mul_(beta).add_(blk, alpha=alpha)
+
+
+_WS: dict = {}
+
+
+def _workspace(device, nbytes: int) -> torch.Tensor:
+    ws = _WS.get(device)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=device)
+        _WS[device] = ws
+    return ws
+
+
+def _embed(M: np.ndarray, rows_idx: np.ndarray, cols_idx: np.ndarray, shape) -> np.ndarray:
+    out = np.zeros(shape)
+    out[np.ix_(rows_idx, cols_idx)] = M
+    return out
+
+
+def _orthonormalize_slot(work: "_Work", s: int, nv: int, scratch: "_Work", group) -> int:
+    """Cholesky-QR twice on the first nv columns of slot s (scratch: the same
+    slot of another buffer).  Keeps the independent columns, zeroes the rest;
+    returns their count."""
+    bw = work.bw
+    for _ in range(2):
+        T = _orth_factor(work.gram(s, s + 1, s, s + 1, group)[:nv, :nv])
+        nk = T.shape[1]
+        if nk == 0:
+            work.buf[s].zero_()
+            return 0
+        work.tsmm(s, s + 1, _embed(T, np.arange(nv), np.arange(nk), (bw, bw)), scratch, s, s + 1)
+        work.buf[s].copy_(scratch.buf[s])
+        nv = nk
+    return nv
+
+
 def lobpcg(apply: Callable[[torch.Tensor], torch.Tensor], X0: torch.Tensor, *, tol: float = 1e-5,
            max_iter: int = 300, largest: bool = False, group=None,
            callback: Callable[[int, np.ndarray, np.ndarray], None] | None = None) -> LobpcgResult:
@@ -88,30 +263,46 @@ def lobpcg(apply: Callable[[torch.Tensor], torch.Tensor], X0: torch.Tensor, *, t
 
     ``X0`` holds this rank's rows of the initial block (n_local × m);
     convergence when every ‖r_j‖ ≤ tol · max(|λ_j|, ‖A‖-scale) where the
-    scale is the largest |Ritz value| seen.
+    scale is the largest |Ritz value| seen.  ``apply`` maps a contiguous
+    (n_local, w) block (w ≤ m) to its image.
+
+    Blocks live in two ping-pong block-major work buffers (``_Work``); Gram
+    products run in float64 on the device (``cim_gram_blocked``), block
+    updates write in place (``cim_tsmm_blocked``), and only the small
+    3m × 3m problems go to the host.
     """
     if X0.ndim != 2:
         raise ValueError("X0 must be (n_local, m)")
-    m = X0.shape[1]
+    rows, m = X0.shape
+    dev, dt = X0.device, X0.dtype
     calls = 0
-    X = _orthonormalize(X0, group)
-    if X.shape[1] < m:
+    cur, nxt = _Work(rows, m, dt, dev), _Work(rows, m, dt, dev)
+    bw = cur.bw
+    Wk = _Work
+    cur.slot(Wk.X).copy_(X0)
+    if _orthonormalize_slot(cur, Wk.X, m, nxt, group) < m:
         raise ValueError("initial block is rank deficient")
-    AX = apply(X)
+    cur.slot(Wk.AX).copy_(apply(cur.slot(Wk.X).contiguous()))
     calls += 1
-    lam, C = _rayleigh_ritz(_gram(X, AX, group), _gram(X, X, group), m, largest)
-    Ct = torch.from_numpy(C).to(X.device, X.dtype)
-    X, AX = X @ Ct, AX @ Ct
-    P = AP = None
+    xi = np.arange(m)
+    lam, C = _rayleigh_ritz(cur.gram(Wk.X, Wk.X + 1, Wk.AX, Wk.AX + 1, group)[:m, :m],
+                            cur.gram(Wk.X, Wk.X + 1, Wk.X, Wk.X + 1, group)[:m, :m], m, largest)
+    Cb = _embed(C, xi, xi, (bw, bw))
+    cur.tsmm(Wk.X, Wk.X + 1, Cb, nxt, Wk.X, Wk.X + 1)
+    cur.tsmm(Wk.AX, Wk.AX + 1, Cb, nxt, Wk.AX, Wk.AX + 1)
+    cur, nxt = nxt, cur
+    have_p = False
     history = []
     scale = float(np.abs(lam).max()) or 1.0
     rnorm = np.full(m, np.inf)
     it = 0
     converged = False
     for it in range(1, max_iter + 1):
-        lam_t = torch.from_numpy(lam).to(X.device, X.dtype)
-        R = AX - X * lam_t
-        rnorm = np.sqrt(np.maximum(np.diag(_gram(R, R, group)), 0.0))
+        # residuals R = AX − X·Λ into the W slot
+        lam_t = torch.from_numpy(lam).to(dev, dt)
+        cur.buf[Wk.W].zero_()
+        cur.slot(Wk.W).copy_(torch.addcmul(cur.slot(Wk.AX), cur.slot(Wk.X), lam_t, value=-1.0))
+        rnorm = np.sqrt(np.maximum(np.diag(cur.gram(Wk.W, Wk.W + 1, Wk.W, Wk.W + 1, group))[:m], 0.0))
         scale = max(scale, float(np.abs(lam).max()))
         history.append((lam.copy(), rnorm.copy()))
         if callback is not None:
@@ -120,33 +311,47 @@ def lobpcg(apply: Callable[[torch.Tensor], torch.Tensor], X0: torch.Tensor, *, t
         if not active.any():
             converged = True
             break
-        W = R[:, torch.from_numpy(np.flatnonzero(active)).to(R.device)]
-        # project out the current basis, then orthonormalise
-        basis = [X] if P is None else [X, P]
-        for B in basis:
-            W = W - B @ torch.from_numpy(_gram(B, W, group)).to(W.device, W.dtype)
-        W = _orthonormalize(W, group)
-        if W.shape[1] == 0:
+        nw = int(active.sum())
+        if nw < m:  # soft locking: keep only the active residual columns
+            idx = torch.from_numpy(np.flatnonzero(active)).to(dev)
+            Wa = cur.slot(Wk.W)[:, idx].clone()
+            cur.buf[Wk.W].zero_()
+            cur.slot(Wk.W, nw).copy_(Wa)
+        # project out the current basis [P X] (or [X]), then orthonormalise
+        b0 = Wk.P if have_p else Wk.X
+        bidx = cur.vidx(range(b0, Wk.W), [m] * (Wk.W - b0))
+        wi = np.arange(nw)
+        G_bw = cur.gram(b0, Wk.W, Wk.W, Wk.W + 1, group)[np.ix_(bidx, wi)]
+        cur.tsmm(b0, Wk.W, _embed(G_bw, bidx, wi, ((Wk.W - b0) * bw, bw)), cur, Wk.W, Wk.W + 1, alpha=-1.0, beta=1.0)
+        nw = _orthonormalize_slot(cur, Wk.W, nw, nxt, group)
+        if nw == 0:
             converged = True
             break
-        AW = apply(W)
+        cur.buf[Wk.AW].zero_()
+        cur.slot(Wk.AW, nw).copy_(apply(cur.slot(Wk.W, nw).contiguous()))
         calls += 1
-        S = [X, W] + ([P] if P is not None else [])
-        AS = [AX, AW] + ([AP] if AP is not None else [])
-        Sm = torch.cat(S, dim=1)
-        ASm = torch.cat(AS, dim=1)
-        lam, C = _rayleigh_ritz(_gram(Sm, ASm, group), _gram(Sm, Sm, group), m, largest)
-        Ct = torch.from_numpy(C).to(X.device, X.dtype)
-        Xn = Sm @ Ct
-        AXn = ASm @ Ct
-        # conjugate directions: the W and P parts of the new Ritz vectors
-        Cp = Ct.clone()
-        Cp[:m] = 0
-        P = Sm @ Cp
-        AP = ASm @ Cp
-        X, AX = Xn, AXn
-    return LobpcgResult(eigenvalues=lam, X=X, iterations=it, converged=converged, residual_norms=rnorm,
-                        history=history, spmm_calls=calls)
+        # Rayleigh–Ritz on S = [P X W] (or [X W]): one Gram pass of S against
+        # all six slots gives SᵀS and SᵀAS
+        sidx = cur.vidx(range(b0, Wk.AP), [m] * (Wk.W - b0) + [nw])
+        MG = cur.gram(b0, Wk.AP, Wk.P, Wk.AW + 1, group)
+        M = MG[np.ix_(sidx, sidx + b0 * bw)]
+        G = MG[np.ix_(sidx, sidx + (b0 + 3) * bw)]
+        lam, C = _rayleigh_ritz(G, M, m, largest)
+        # new [P | X] = S·[C_p | C] and [AP | AX] = AS·[C_p | C] into the other buffer,
+        # C_p = C with its X rows zeroed (conjugate directions)
+        Cp = C.copy()
+        xrows = np.flatnonzero((sidx >= (Wk.X - b0) * bw) & (sidx < (Wk.X - b0 + 1) * bw))
+        Cp[xrows] = 0.0
+        ns = (Wk.AP - b0) * bw
+        CC = np.zeros((ns, 2 * bw))
+        CC[sidx, :m] = Cp
+        CC[sidx, bw:bw + m] = C
+        cur.tsmm(b0, Wk.AP, CC, nxt, Wk.P, Wk.W)
+        cur.tsmm(b0 + 3, Wk.AW + 1, CC, nxt, Wk.AP, Wk.AW)
+        have_p = True
+        cur, nxt = nxt, cur
+    return LobpcgResult(eigenvalues=lam, X=cur.slot(Wk.X).clone(), iterations=it, converged=converged,
+                        residual_norms=rnorm, history=history, spmm_calls=calls)
 
 
 def lobpcg_sym(H, m: int = 8, *, seed: int = 0, dtype=None, **kw) -> LobpcgResult:

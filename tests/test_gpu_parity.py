@@ -384,3 +384,46 @@ def test_host_batch_pipeline_matches_oracle(pkg, c1_small, dtype, k):
         pkg.sym_spmm_host_batch(H, [torch.zeros((n, k), dtype=dtype, device="cuda")])
     with pytest.raises(ValueError):
         pkg.sym_spmm_host_batch(H, Xs[:2], out=outs[:1])
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("rows,ca,cb", [(1, 1, 1), (1000, 8, 8), (100_003, 24, 48), (70_000, 5, 13), (4096, 64, 64)])
+def test_gram_f64_matches_numpy(pkg, dtype, rows, ca, cb):
+    """cim_gram: Aᵀ·B with f64 accumulation (LOBPCG's Gram products),
+    including strided column views and ragged column counts; reproducible."""
+    from paper_2110_10765_b200.lobpcg import gram_f64
+
+    g = torch.Generator().manual_seed(rows + ca)
+    base = torch.randn((rows, ca + cb + 3), generator=g, dtype=dtype)
+    A, B = base[:, :ca], base[:, 3:3 + cb]  # strided views (lda = ldb = ca+cb+3)
+    want = A.double().numpy().T @ B.double().numpy()
+    got = gram_f64(A.cuda(), B.cuda()).cpu().numpy()
+    tol = 1e-12 * np.sqrt(rows) * (np.abs(A.double().numpy()).T @ np.abs(B.double().numpy())).max()
+    assert np.abs(got - want).max() <= tol + 1e-300
+    again = gram_f64(A.cuda(), B.cuda()).cpu().numpy()
+    assert np.array_equal(got, again)  # fixed reduction order
+    with pytest.raises(ValueError):
+        gram_f64(A.cuda(), B[:-1].cuda())
+
+
+@pytest.mark.parametrize("rows,q,p,off", [(1, 1, 1, 0), (1000, 8, 8, 0), (100_001, 24, 16, 8), (5000, 7, 5, 3),
+                                          (4096, 64, 64, 0)])
+def test_tsmm_matches_torch(pkg, rows, q, p, off):
+    """cim_tsmm: Out = alpha·A·C + beta·Out into column slices of a wider
+    buffer (vector path when everything is 16-byte aligned, scalar otherwise)."""
+    from paper_2110_10765_b200.lobpcg import tsmm
+
+    g = torch.Generator().manual_seed(rows + q + p)
+    buf = torch.randn((rows, off + q + p + 4), generator=g).cuda()
+    A = buf[:, off:off + q]
+    Out = buf[:, off + q:off + q + p]
+    C = torch.randn((q, p), generator=g, dtype=torch.float64)
+    want = (-0.5 * (A.double().cpu() @ C) + 2.0 * Out.double().cpu()).numpy()
+    untouched = buf[:, :off].clone()
+    tsmm(A, C, Out, alpha=-0.5, beta=2.0)
+    got = Out.double().cpu().numpy()
+    scale = (np.abs(A.double().cpu().numpy()) @ np.abs(C.numpy())).max() + 1.0
+    assert np.abs(got - want).max() <= 4e-6 * scale * q
+    assert torch.equal(buf[:, :off], untouched)
+    tsmm(A, C, Out)  # beta = 0: Out not read
+    assert np.abs(Out.double().cpu().numpy() - (A.double().cpu() @ C).numpy()).max() <= 4e-6 * scale * q
