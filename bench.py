@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget for the cpu_baseline leg")
     ap.add_argument("--e2e-steps", type=int, default=16)
+    ap.add_argument("--bands", type=int, default=1, help="column bands of the tile order (0 = auto)")
     return ap.parse_args()
 
 
@@ -237,7 +238,8 @@ def impl_ours(args):
     n, nb, n_off, p = workload(args, world)
 
     t_build = time.perf_counter()
-    S = ShardedSymSpmm.synthetic(n, k=k, p=p, seed=0, dtype=dtype, device=dev, layout=args.layout)
+    S = ShardedSymSpmm.synthetic(n, k=k, p=p, seed=0, dtype=dtype, device=dev, layout=args.layout,
+                                 bands=None if args.bands == 0 else args.bands)
     H = S.H
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t_build
@@ -392,6 +394,7 @@ def impl_ours(args):
                 "n": n, "k": k, "stored_tiles": g_tiles, "stored_nnz": g_tiles * 4096,
                 "parallelism": f"row-block shard x{world}" if world > 1 else "single GPU",
                 "layout": H.layout,
+                "bands": H.meta.get("bands", 1),
                 "l2": "inputs (8.3 GB per GPU) far larger than L2 (126 MB): no flush",
                 "gflop_per_apply": flops_global / 1e9,
                 "hbm_gbs_kernel": achieved,

@@ -198,6 +198,17 @@ CIM_API int cim_plan_units(const int32_t *tile_rc_host, int64_t n_tiles, int64_t
                    int32_t max_unit, int32_t *units_out, int64_t *n_units_out);
 
 /*
+ * Host: as cim_plan_units for tiles stored in column bands: tile order is
+ * (C / band_cols, R, C) and units never cross a band.  Streaming the
+ * matrix band by band keeps the random side of the transposed product
+ * (X_C gathers, Y_C atomics) inside an L2-sized slice of X and Y.
+ * band_cols ≥ nb gives the plain row-major order of cim_plan_units.
+ */
+CIM_API int cim_plan_units_banded(const int32_t *tile_rc_host, int64_t n_tiles, int64_t nb,
+                                  int32_t max_unit, int64_t band_cols, int32_t *units_out,
+                                  int64_t *n_units_out);
+
+/*
  * Host: split units into `parts` contiguous ranges with balanced tile counts
  * (row-block sharding over GPUs).  bounds_out[parts+1].
  */

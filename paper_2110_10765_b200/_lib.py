@@ -27,6 +27,7 @@ EXPORTS = (
     "cim_sym_spmm_supported",
     "cim_layout_supports",
     "cim_plan_units",
+    "cim_plan_units_banded",
     "cim_partition_units",
     "cim_fill_synthetic_values",
     "cim_fill_masked_values",
@@ -87,6 +88,8 @@ def lib() -> ctypes.CDLL:
     L.cim_sym_spmm_supported.argtypes = [c.c_int32, c.c_int32]
     L.cim_layout_supports.argtypes = [c.c_int32, c.c_int32, c.c_int32]
     L.cim_plan_units.argtypes = [c.c_void_p, c.c_int64, c.c_int64, c.c_int32, c.c_void_p, c.POINTER(c.c_int64)]
+    L.cim_plan_units_banded.argtypes = [c.c_void_p, c.c_int64, c.c_int64, c.c_int32, c.c_int64, c.c_void_p,
+                                        c.POINTER(c.c_int64)]
     L.cim_partition_units.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_void_p]
     L.cim_fill_synthetic_values.argtypes = [c.c_void_p, c.c_int64, c.c_int64, c.c_int32, c.c_int32, c.c_int32,
                                             c.c_uint64, c.c_int32, c.c_void_p, c.c_void_p]

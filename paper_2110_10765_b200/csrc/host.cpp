@@ -29,19 +29,31 @@ extern "C" const char *cim_version(void) { return "cim_b200 1.0 (sm_100a, fragme
 
 extern "C" const char *cim_last_error(void) { return cim::g_last_error.c_str(); }
 
-extern "C" int cim_plan_units(const int32_t *rc, int64_t n_tiles, int64_t nb, int32_t max_unit,
-                              int32_t *units_out, int64_t *n_units_out) {
+// Tiles must be grouped by column band (band = C / band_cols, ascending), and
+// inside a band sorted by R then C, unique, R ≤ C.  band_cols ≥ nb is the
+// plain row-major order.  Units never cross a band or a block row.
+extern "C" int cim_plan_units_banded(const int32_t *rc, int64_t n_tiles, int64_t nb, int32_t max_unit,
+                                     int64_t band_cols, int32_t *units_out, int64_t *n_units_out) {
   cim::clear_error();
-  if (n_tiles < 0 || nb < 1 || max_unit < 1 || !n_units_out) return set_error(CIM_EINVAL, "bad arguments");
+  if (n_tiles < 0 || nb < 1 || max_unit < 1 || band_cols < 1 || !n_units_out)
+    return set_error(CIM_EINVAL, "bad arguments");
   if (n_tiles > 0 && (!rc || !units_out)) return set_error(CIM_EINVAL, "NULL arrays");
   if (n_tiles > INT32_MAX) return set_error(CIM_EINVAL, "n_tiles exceeds int32 range");
   int64_t nu = 0;
   int64_t t = 0;
+  int64_t prev_band = -1;
+  int32_t prev_R = -1;
   while (t < n_tiles) {
     const int32_t R = rc[2 * t];
+    if (R < 0 || R >= nb) return set_error(CIM_EINVAL, "tile row out of range at index " + std::to_string(t));
+    const int32_t C0 = rc[2 * t + 1];
+    if (C0 < 0 || C0 >= nb) return set_error(CIM_EINVAL, "tile column out of range at index " + std::to_string(t));
+    const int64_t band = C0 / band_cols;
+    if (band < prev_band || (band == prev_band && R <= prev_R))
+      return set_error(CIM_EINVAL, "tiles not sorted by (band, row) at index " + std::to_string(t));
     int64_t e = t;
     int32_t prevC = -1;
-    while (e < n_tiles && rc[2 * e] == R) {
+    while (e < n_tiles && rc[2 * e] == R && rc[2 * e + 1] / band_cols == band) {
       const int32_t C = rc[2 * e + 1];
       if (C < R) return set_error(CIM_EINVAL, "tile below the diagonal (C < R) at index " + std::to_string(e));
       if (C >= nb) return set_error(CIM_EINVAL, "tile column out of range at index " + std::to_string(e));
@@ -49,8 +61,6 @@ extern "C" int cim_plan_units(const int32_t *rc, int64_t n_tiles, int64_t nb, in
       prevC = C;
       ++e;
     }
-    if (R < 0 || R >= nb) return set_error(CIM_EINVAL, "tile row out of range at index " + std::to_string(t));
-    if (e < n_tiles && rc[2 * e] < R) return set_error(CIM_EINVAL, "tiles not sorted by row at index " + std::to_string(e));
     for (int64_t s = t; s < e; s += max_unit) {
       const int64_t f = (s + max_unit < e) ? s + max_unit : e;
       units_out[4 * nu + 0] = R;
@@ -59,10 +69,17 @@ extern "C" int cim_plan_units(const int32_t *rc, int64_t n_tiles, int64_t nb, in
       units_out[4 * nu + 3] = 0;
       ++nu;
     }
+    prev_band = band;
+    prev_R = R;
     t = e;
   }
   *n_units_out = nu;
   return CIM_OK;
+}
+
+extern "C" int cim_plan_units(const int32_t *rc, int64_t n_tiles, int64_t nb, int32_t max_unit,
+                              int32_t *units_out, int64_t *n_units_out) {
+  return cim_plan_units_banded(rc, n_tiles, nb, max_unit, nb, units_out, n_units_out);
 }
 
 extern "C" int cim_partition_units(const int32_t *units, int64_t n_units, int32_t parts, int64_t *bounds) {

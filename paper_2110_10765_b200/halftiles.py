@@ -65,15 +65,33 @@ def _as_torch_dtype(dtype) -> torch.dtype:
     raise ValueError(f"dtype must be float32 or float64, got {dtype}")
 
 
-def plan_units(tile_rc: np.ndarray, nb: int, max_unit: int = DEFAULT_MAX_UNIT) -> np.ndarray:
-    """Work units (R, t0, t1, 0) via the native planner (validates tile order)."""
+def plan_units(tile_rc: np.ndarray, nb: int, max_unit: int = DEFAULT_MAX_UNIT,
+               band_cols: int | None = None) -> np.ndarray:
+    """Work units (R, t0, t1, 0) via the native planner (validates tile order:
+    (R, C) sorted, or (C // band_cols, R, C) when ``band_cols`` is given)."""
     rc = np.ascontiguousarray(tile_rc, dtype=np.int32)
     T = rc.shape[0]
     out = np.zeros((max(T, 1), 4), dtype=np.int32)
     nu = ctypes.c_int64(0)
-    check(lib().cim_plan_units(rc.ctypes.data if T else None, T, nb, max_unit, out.ctypes.data, ctypes.byref(nu)),
-          "cim_plan_units")
+    check(lib().cim_plan_units_banded(rc.ctypes.data if T else None, T, nb, max_unit,
+                                      int(band_cols) if band_cols else int(nb), out.ctypes.data, ctypes.byref(nu)),
+          "cim_plan_units_banded")
     return out[: nu.value].copy()
+
+
+def band_order(tile_rc: np.ndarray, band_cols: int) -> np.ndarray:
+    """Permutation putting (R, C)-sorted tiles into column-band order
+    (C // band_cols, R, C) — stable, so a single band keeps the input order."""
+    rc = np.asarray(tile_rc).reshape(-1, 2)
+    return np.lexsort((rc[:, 1], rc[:, 0], rc[:, 1] // max(1, int(band_cols))))
+
+
+def default_bands(n: int) -> int:
+    """Column bands for an order-n matrix: enough that one band's slice of X
+    and Y at k = 8 f32 (2·(n/bands)·32 B) stays within ~half of the 126 MB L2
+    (the random side of the transposed product); 1 below that."""
+    need = 2 * n * 8 * 4
+    return max(1, -(-need // (64 << 20)))
 
 
 def partition_units(units: np.ndarray, parts: int) -> np.ndarray:
@@ -247,7 +265,9 @@ class HalfTiles:
     # ----------------------------------------------------------- constructors
     @classmethod
     def _from_pattern(cls, n: int, tile_rc: np.ndarray, dtype, device, max_unit: int,
-                      layout: str | None = None) -> "HalfTiles":
+                      layout: str | None = None, bands: int | None = 1):
+        """Empty tile storage for the pattern.  Returns (H, perm): tiles are
+        stored in column-band order, ``perm[s]`` = input index of stored tile s."""
         dtype = _as_torch_dtype(dtype)
         _dtype_code(dtype)
         layout = layout or default_layout(dtype)
@@ -260,18 +280,24 @@ class HalfTiles:
             raise ValueError("HalfTiles live in GPU memory: device must be a CUDA device")
         nb = (n + BLOCK - 1) // BLOCK
         rc = np.ascontiguousarray(tile_rc, dtype=np.int32).reshape(-1, 2)
-        units = plan_units(rc, nb, max_unit)  # validates order / range
+        plan_units(rc, nb, max_unit)  # validates the (R, C) order / range of the input
+        bands = default_bands(n) if bands is None else max(1, int(bands))
+        band_cols = -(-nb // bands)
+        perm = band_order(rc, band_cols) if bands > 1 else np.arange(rc.shape[0])
+        rc = np.ascontiguousarray(rc[perm])
+        units = plan_units(rc, nb, max_unit, band_cols)
         t_rc = torch.from_numpy(rc).to(device)
         t_units = torch.from_numpy(units).to(device)
         vals = torch.empty((rc.shape[0], BLOCK * BLOCK), dtype=dtype, device=device)
-        return cls(n=int(n), tile_rc=t_rc, units=t_units, vals=vals, tile_rc_host=rc, units_host=units,
-                   layout=layout)
+        H = cls(n=int(n), tile_rc=t_rc, units=t_units, vals=vals, tile_rc_host=rc, units_host=units, layout=layout)
+        H.meta.update(bands=bands, band_cols=band_cols)
+        return H, perm
 
     @classmethod
     def synthetic(cls, n: int, p: float | None = None, *, n_off: int | None = None, seed: int = 0,
                   value_seed: int = 0, values: str = "h_xor", op_k: int = 0, dtype=torch.float32,
                   device="cuda", max_unit: int = DEFAULT_MAX_UNIT, tile_rc: np.ndarray | None = None,
-                  layout: str | None = None) -> "HalfTiles":
+                  layout: str | None = None, bands: int | None = 1) -> "HalfTiles":
         """Synthetic half-stored matrix (BASELINE.json configs).
 
         Pattern: all diagonal tiles plus upper tiles kept with probability p
@@ -290,7 +316,7 @@ class HalfTiles:
             if not 0.0 <= p <= 1.0:
                 raise ValueError(f"p must be in [0, 1], got {p}")
             tile_rc = synthetic_pattern(nb, p, seed)
-        H = cls._from_pattern(n, tile_rc, dtype, device, max_unit, layout)
+        H, _ = cls._from_pattern(n, tile_rc, dtype, device, max_unit, layout, bands)
         stream = torch.cuda.current_stream(H.device).cuda_stream
         with torch.cuda.device(H.device):
             check(lib().cim_fill_synthetic_values(H.tile_rc.data_ptr() if H.n_tiles else None, H.n_tiles, n,
@@ -303,13 +329,18 @@ class HalfTiles:
 
     @classmethod
     def from_dense_tiles(cls, n: int, tile_rc: np.ndarray, tiles, *, dtype=None, device="cuda",
-                         max_unit: int = DEFAULT_MAX_UNIT, layout: str | None = None) -> "HalfTiles":
-        """From row-major dense tiles (T,64,64); repacked on the device."""
+                         max_unit: int = DEFAULT_MAX_UNIT, layout: str | None = None,
+                         bands: int | None = 1) -> "HalfTiles":
+        """From row-major dense tiles (T,64,64) given in ``tile_rc`` order;
+        repacked on the device (stored in column-band order)."""
         tiles_t = torch.as_tensor(tiles)
         dtype = _as_torch_dtype(dtype if dtype is not None else tiles_t.dtype)
-        H = cls._from_pattern(n, tile_rc, dtype, device, max_unit, layout)
+        H, perm = cls._from_pattern(n, tile_rc, dtype, device, max_unit, layout, bands)
         if H.n_tiles:
-            src = tiles_t.to(device=H.device, dtype=dtype).reshape(H.n_tiles, BLOCK * BLOCK).contiguous()
+            src = tiles_t.to(device=H.device, dtype=dtype).reshape(H.n_tiles, BLOCK * BLOCK)
+            if H.meta["bands"] > 1:
+                src = src[torch.from_numpy(perm).to(H.device)]
+            src = src.contiguous()
             stream = torch.cuda.current_stream(H.device).cuda_stream
             with torch.cuda.device(H.device):
                 check(lib().cim_pack_tiles(src.data_ptr(), H.n_tiles, _dtype_code(dtype), LAYOUTS[H.layout],

@@ -81,7 +81,7 @@ class ShardedSymSpmm:
     @classmethod
     def synthetic(cls, n: int, *, k: int, p: float | None = None, n_off: int | None = None, seed: int = 0,
                   value_seed: int = 0, dtype=torch.float32, device=None, group=None, max_unit: int = 32,
-                  values: str = "h_xor", layout: str | None = None) -> "ShardedSymSpmm":
+                  values: str = "h_xor", layout: str | None = None, bands: int | None = 1) -> "ShardedSymSpmm":
         """Every rank draws the same global tile pattern (seeded), keeps its
         balanced panel, and generates only its own tile values on its GPU."""
         world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -95,7 +95,7 @@ class ShardedSymSpmm:
         _, _, t0, t1 = shard_tile_range(units, world, rank)
         device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         H = HalfTiles.synthetic(n, tile_rc=rc[t0:t1], value_seed=value_seed, values=values, dtype=dtype,
-                                device=device, max_unit=max_unit, layout=layout)
+                                device=device, max_unit=max_unit, layout=layout, bands=bands)
         H.meta.update(global_tiles=int(rc.shape[0]), global_off_tiles=int(np.count_nonzero(rc[:, 0] != rc[:, 1])),
                       p=p, seed=seed)
         return cls(n, k, dtype, device, H_local=H, group=group)

@@ -427,3 +427,29 @@ def test_tsmm_matches_torch(pkg, rows, q, p, off):
     assert torch.equal(buf[:, :off], untouched)
     tsmm(A, C, Out)  # beta = 0: Out not read
     assert np.abs(Out.double().cpu().numpy() - (A.double().cpu() @ C).numpy()).max() <= 4e-6 * scale * q
+
+
+@pytest.mark.parametrize("bands", [2, 3, 7])
+def test_column_banded_storage(pkg, c1_small, bands):
+    """Tiles stored in column-band order (C // band_cols, R, C): units never
+    cross a band, same operator (oracle gates), same tiles after a pack/unpack
+    round trip through the permutation."""
+    n, rc, tiles = c1_small
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, bands=bands, max_unit=5)
+    assert H.meta["bands"] == bands
+    bc = H.meta["band_cols"]
+    srt = H.tile_rc_host
+    key = (srt[:, 1] // bc).astype(np.int64) * (1 << 40) + srt[:, 0].astype(np.int64) * (1 << 20) + srt[:, 1]
+    assert np.all(np.diff(key) > 0)
+    assert sorted(map(tuple, srt)) == sorted(map(tuple, rc))
+    for u in H.units_host:
+        t = srt[u[1]:u[2]]
+        assert np.all(t[:, 0] == u[0]) and np.unique(t[:, 1] // bc).size == 1
+    for k in (4, 8, 16):
+        X = torch.randn((n, k), generator=torch.Generator().manual_seed(k))
+        check_result(n, rc, tiles, X.numpy(), pkg.sym_spmm(H, X.cuda()).cpu().numpy(), torch.float32)
+    H2 = pkg.HalfTiles.from_dense_tiles(n, rc, tiles, bands=bands)
+    back = H2.dense_tiles().cpu().numpy()
+    pos = {tuple(r): s for s, r in enumerate(H2.tile_rc_host)}
+    for t_in, r in enumerate(rc[:50]):
+        assert np.array_equal(back[pos[tuple(r)]], tiles[t_in])
