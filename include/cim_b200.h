@@ -82,6 +82,28 @@ extern "C" {
                                byte(r,c) = (c/32)·8192 + (r/4)·512 + s((r%4)·128 + (c%32)·4),
                                s(x) = x ^ (((x >> 7) & 3) << 5)  (SWIZZLE_128B_BASE32B)      */
 
+/*
+ * Sparse ("COO-in-tile") stored tiles, for 64-tiles below the dense
+ * break-even fill (⅔ for f32, 0.8 for f64: SURVEY §7 step 4) — the ragged
+ * orbital blocks of reference skeletons average 17% fill.  Per tile the
+ * entries are sorted by local row then column:
+ *   tile_rc    int32  [n_tiles][2]   (R, C), R ≤ C (any order)
+ *   entry_off  int64  [n_tiles+1]    first entry of each tile
+ *   rowptr     uint16 [n_tiles][65]  per local row, offsets relative to the tile
+ *   col        uint8  [n_entries]    local column
+ *   vals       f32|f64[n_entries]
+ * Bytes per entry: 1 + s (+ 138 B per tile), against 4096·s for a dense tile.
+ */
+typedef struct cim_sparse_tiles {
+  int64_t         n_tiles;
+  int64_t         n_entries;
+  const int32_t  *tile_rc;
+  const int64_t  *entry_off;
+  const uint16_t *rowptr;
+  const uint8_t  *col;
+  const void     *vals;     /* dtype of the enclosing cim_half_tiles */
+} cim_sparse_tiles;
+
 typedef struct cim_half_tiles {
   int64_t        n;        /* matrix order                                   */
   int32_t        block;    /* must be 64                                     */
@@ -93,6 +115,9 @@ typedef struct cim_half_tiles {
   const void    *vals;     /* device, [n_tiles][4096] in `layout` order      */
   int32_t        layout;   /* CIM_LAYOUT_FRAG | CIM_LAYOUT_TC                 */
   int32_t        reserved; /* 0                                               */
+  const cim_sparse_tiles *sparse; /* NULL, or the sparse tiles of the same
+                                     matrix (a tile is stored dense or sparse,
+                                     never both); device arrays              */
 } cim_half_tiles;
 
 /* Library version / build string (host). */
@@ -174,6 +199,16 @@ CIM_API int cim_gram_blocked(const void *A, int64_t lda, int32_t a_bw, int64_t a
 CIM_API int cim_tsmm_blocked(const float *A, int64_t lda, int32_t a_bw, int64_t a_bstride, int32_t q,
                              const float *C, int32_t p, float alpha, float beta, float *Out,
                              int64_t ldo, int32_t o_bw, int64_t o_bstride, int64_t rows, void *stream);
+
+/*
+ * Device: values on the entries of sparse tiles — vals_out[e] = value(i, j)
+ * of entry e where mask[e] != 0 (mask: the pattern's own values, or NULL =
+ * every entry), else 0.  Kinds as cim_fill_synthetic_values (the reference
+ * hashes, pipeline.py:199-263).
+ */
+CIM_API int cim_fill_sparse_values(const cim_sparse_tiles *S, int64_t n, int32_t dtype, int32_t kind,
+                                   uint64_t seed, int32_t op_k, const void *mask, void *vals_out,
+                                   void *stream);
 
 /* Device workspace bytes cim_gram / cim_gram_blocked need. */
 CIM_API uint64_t cim_gram_workspace_bytes(int64_t rows, int32_t ca, int32_t cb);

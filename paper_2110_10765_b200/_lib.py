@@ -36,12 +36,27 @@ EXPORTS = (
     "cim_hash_values",
     "cim_sym_spmm_host_batch",
     "cim_host_batch_workspace_bytes",
+    "cim_fill_sparse_values",
     "cim_gram",
     "cim_gram_workspace_bytes",
     "cim_tsmm",
     "cim_gram_blocked",
     "cim_tsmm_blocked",
 )
+
+
+class CimSparseTiles(ctypes.Structure):
+    """Mirror of ``struct cim_sparse_tiles``."""
+
+    _fields_ = [
+        ("n_tiles", ctypes.c_int64),
+        ("n_entries", ctypes.c_int64),
+        ("tile_rc", ctypes.c_void_p),
+        ("entry_off", ctypes.c_void_p),
+        ("rowptr", ctypes.c_void_p),
+        ("col", ctypes.c_void_p),
+        ("vals", ctypes.c_void_p),
+    ]
 
 
 class CimHalfTiles(ctypes.Structure):
@@ -58,6 +73,7 @@ class CimHalfTiles(ctypes.Structure):
         ("vals", ctypes.c_void_p),
         ("layout", ctypes.c_int32),
         ("reserved", ctypes.c_int32),
+        ("sparse", ctypes.POINTER(CimSparseTiles)),
     ]
 
 
@@ -102,6 +118,8 @@ def lib() -> ctypes.CDLL:
     L.cim_sym_spmm_host_batch.argtypes = [c.POINTER(CimHalfTiles), c.POINTER(c.c_void_p), c.POINTER(c.c_void_p),
                                           c.c_int32, c.c_int32, c.c_void_p, c.c_uint64]
     L.cim_host_batch_workspace_bytes.argtypes = [c.POINTER(CimHalfTiles), c.c_int32]
+    L.cim_fill_sparse_values.argtypes = [c.POINTER(CimSparseTiles), c.c_int64, c.c_int32, c.c_int32, c.c_uint64,
+                                         c.c_int32, c.c_void_p, c.c_void_p, c.c_void_p]
     L.cim_gram.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_void_p, c.c_int64, c.c_int32, c.c_int64, c.c_int32,
                            c.c_void_p, c.c_void_p, c.c_uint64, c.c_void_p]
     L.cim_gram_workspace_bytes.argtypes = [c.c_int64, c.c_int32, c.c_int32]

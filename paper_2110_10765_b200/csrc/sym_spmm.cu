@@ -1118,8 +1118,14 @@ extern "C" int cim_layout_supports(int32_t layout, int32_t dtype, int32_t k) {
   return 0;
 }
 
-extern "C" int cim_sym_spmm(const cim_half_tiles *H, const void *X, void *Y, int32_t k, int64_t ldx, int64_t ldy,
-                            uint32_t flags, void *stream_) {
+namespace cim {
+int sym_spmm_sparse(const cim_sparse_tiles *S, int dtype, const void *X, void *Y, int k, long long ldx,
+                    long long ldy, cudaStream_t stream);
+}
+
+// Dense tiles (and the Y zeroing); the sparse tiles follow in cim_sym_spmm.
+static int sym_spmm_dense(const cim_half_tiles *H, const void *X, void *Y, int32_t k, int64_t ldx, int64_t ldy,
+                          uint32_t flags, void *stream_) {
   clear_error();
   if (!H) return set_error(CIM_EINVAL, "H is NULL");
   if (H->block != kBlock) return set_error(CIM_EINVAL, "block must be 64");
@@ -1206,4 +1212,11 @@ extern "C" int cim_sym_spmm(const cim_half_tiles *H, const void *X, void *Y, int
     }
   }
   return set_error(CIM_EUNSUPPORTED, "no kernel for (dtype, k)");
+}
+
+extern "C" int cim_sym_spmm(const cim_half_tiles *H, const void *X, void *Y, int32_t k, int64_t ldx, int64_t ldy,
+                            uint32_t flags, void *stream_) {
+  const int rc = sym_spmm_dense(H, X, Y, k, ldx, ldy, flags, stream_);
+  if (rc != CIM_OK || !H->sparse || H->sparse->n_tiles == 0) return rc;
+  return sym_spmm_sparse(H->sparse, H->dtype, X, Y, k, ldx, ldy, reinterpret_cast<cudaStream_t>(stream_));
 }

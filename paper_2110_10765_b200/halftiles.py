@@ -29,7 +29,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import BLOCK, CIM_F32, CIM_F64, CIM_LAYOUT_FRAG, CIM_LAYOUT_TC, CimHalfTiles, check, lib
+from ._lib import BLOCK, CIM_F32, CIM_F64, CIM_LAYOUT_FRAG, CIM_LAYOUT_TC, CimHalfTiles, CimSparseTiles, check, lib
 
 DEFAULT_MAX_UNIT = 32
 LAYOUTS = {"frag": CIM_LAYOUT_FRAG, "tc": CIM_LAYOUT_TC}
@@ -181,9 +181,90 @@ def fragment_pack_host(tiles: np.ndarray, layout: str = "frag") -> np.ndarray:
     return np.ascontiguousarray(tiles.reshape(T, 4096)[:, row * BLOCK + col])
 
 
+def dense_break_even(dtype) -> float:
+    """Fill above which a 64-tile is stored dense: dense costs 4096·s bytes, a
+    sparse tile (1 + s) bytes per entry (+138 B) — ⅔ for f32, 0.8 for f64
+    (SURVEY.md §7 step 4)."""
+    return 2.0 / 3.0 if _as_torch_dtype(dtype) == torch.float32 else 0.8
+
+
+@dataclass
+class SparseTiles:
+    """COO-in-tile storage of the sparse stored tiles (include/cim_b200.h,
+    cim_sparse_tiles): per tile its entries sorted by local row, then column."""
+
+    tile_rc: torch.Tensor  # int32 (Ts,2) device
+    entry_off: torch.Tensor  # int64 (Ts+1) device
+    rowptr: torch.Tensor  # int16 (Ts,65) device (values ≤ 4096)
+    col: torch.Tensor  # uint8 (E,) device
+    vals: torch.Tensor  # (E,) device, matrix dtype
+    tile_rc_host: np.ndarray
+    entry_off_host: np.ndarray
+    _desc: CimSparseTiles | None = field(default=None, repr=False)
+
+    @property
+    def n_tiles(self) -> int:
+        return int(self.tile_rc_host.shape[0])
+
+    @property
+    def n_entries(self) -> int:
+        return int(self.entry_off_host[-1]) if self.entry_off_host.size else 0
+
+    def entries_per_tile(self) -> np.ndarray:
+        return np.diff(self.entry_off_host)
+
+    def descriptor(self) -> CimSparseTiles:
+        if self._desc is None:
+            self._desc = CimSparseTiles(n_tiles=self.n_tiles, n_entries=self.n_entries,
+                                        tile_rc=self.tile_rc.data_ptr(), entry_off=self.entry_off.data_ptr(),
+                                        rowptr=self.rowptr.data_ptr(), col=self.col.data_ptr() if self.n_entries else None,
+                                        vals=self.vals.data_ptr() if self.n_entries else None)
+        return self._desc
+
+    def with_values(self, vals: torch.Tensor) -> "SparseTiles":
+        return SparseTiles(self.tile_rc, self.entry_off, self.rowptr, self.col, vals, self.tile_rc_host,
+                           self.entry_off_host)
+
+    @classmethod
+    def from_entries(cls, tile_rc: np.ndarray, tile_id: np.ndarray, r: np.ndarray, c: np.ndarray, v: np.ndarray,
+                     dtype, device) -> "SparseTiles":
+        """Entries (tile_id, local row r, local col c, value v), any order, no
+        duplicates; tile_rc[t] = (R, C) of tile t."""
+        order = np.lexsort((c, r, tile_id))
+        tile_id, r, c, v = tile_id[order], r[order], c[order], v[order]
+        T = tile_rc.shape[0]
+        counts = np.bincount(tile_id, minlength=T)
+        off = np.zeros(T + 1, dtype=np.int64)
+        np.cumsum(counts, out=off[1:])
+        rowcnt = np.zeros((T, 64), dtype=np.int64)
+        np.add.at(rowcnt, (tile_id, r), 1)
+        rowptr = np.zeros((T, 65), dtype=np.int64)
+        np.cumsum(rowcnt, axis=1, out=rowptr[:, 1:])
+        dev = torch.device(device)
+        return cls(tile_rc=torch.from_numpy(np.ascontiguousarray(tile_rc, dtype=np.int32)).to(dev),
+                   entry_off=torch.from_numpy(off).to(dev),
+                   rowptr=torch.from_numpy(rowptr.astype(np.int16)).to(dev),
+                   col=torch.from_numpy(c.astype(np.uint8)).to(dev),
+                   vals=torch.from_numpy(np.asarray(v, dtype=np.float64)).to(dev, _as_torch_dtype(dtype)),
+                   tile_rc_host=np.ascontiguousarray(tile_rc, dtype=np.int32), entry_off_host=off)
+
+    def to_entries(self):
+        """Host (tile_id, r, c, v) of every entry (stored order)."""
+        rp = self.rowptr.cpu().numpy().astype(np.int64)
+        off = self.entry_off_host
+        T = self.n_tiles
+        tile_id = np.repeat(np.arange(T), np.diff(off))
+        local = np.arange(self.n_entries) - off[tile_id]
+        r = np.empty(self.n_entries, dtype=np.int64)
+        for t in range(T):  # host export only
+            r[off[t]:off[t + 1]] = np.repeat(np.arange(64), np.diff(rp[t]))
+        return tile_id, r, self.col.cpu().numpy().astype(np.int64), self.vals.cpu().numpy(), local
+
+
 @dataclass
 class HalfTiles:
-    """Half-stored symmetric block-sparse matrix resident in HBM."""
+    """Half-stored symmetric block-sparse matrix resident in HBM: dense 64-tiles
+    (``vals``, fragment order) plus, optionally, sparse tiles (``sparse``)."""
 
     n: int
     tile_rc: torch.Tensor  # int32 (T,2) on device
@@ -195,6 +276,7 @@ class HalfTiles:
     meta: dict = field(default_factory=dict)
     _desc: CimHalfTiles | None = field(default=None, repr=False)
     _ws: torch.Tensor | None = field(default=None, repr=False)
+    sparse: SparseTiles | None = None
 
     # ------------------------------------------------------------------ props
     @property
@@ -227,18 +309,37 @@ class HalfTiles:
         return self.n_tiles - self.n_diag_tiles
 
     @property
+    def n_sparse_tiles(self) -> int:
+        return self.sparse.n_tiles if self.sparse is not None else 0
+
+    def _sparse_split(self) -> tuple[int, int]:
+        """(off-diagonal, diagonal) entries of the sparse tiles."""
+        if self.sparse is None:
+            return 0, 0
+        rc = self.sparse.tile_rc_host
+        cnt = self.sparse.entries_per_tile()
+        diag = int(cnt[rc[:, 0] == rc[:, 1]].sum())
+        return int(cnt.sum()) - diag, diag
+
+    @property
     def nnz_stored(self) -> int:
-        """Stored entries (dense tiles: 4096 per tile)."""
-        return self.n_tiles * BLOCK * BLOCK
+        """Stored entries: 4096 per dense tile plus the sparse tiles' entries."""
+        return self.n_tiles * BLOCK * BLOCK + (self.sparse.n_entries if self.sparse is not None else 0)
 
     def flops(self, k: int) -> int:
         """Algorithmic FLOPs of one apply: 2·k·(2·nnz_off + nnz_diag)."""
-        return 2 * k * (2 * self.n_off_tiles + self.n_diag_tiles) * BLOCK * BLOCK
+        s_off, s_diag = self._sparse_split()
+        return 2 * k * ((2 * self.n_off_tiles + self.n_diag_tiles) * BLOCK * BLOCK + 2 * s_off + s_diag)
 
     def algorithmic_bytes(self, k: int) -> int:
-        """s·nnz_stored + 8·n_tiles + 2·n·k·s (dense tiles)."""
+        """s·nnz_stored + index bytes + 8·tiles + 2·n·k·s:
+        sparse entries carry a 1-byte column, sparse tiles a 130-byte row
+        pointer and an 8-byte entry offset."""
         s = self.vals.element_size()
-        return s * self.nnz_stored + 8 * self.n_tiles + 2 * self.n * k * s
+        idx = 0
+        if self.sparse is not None:
+            idx = self.sparse.n_entries + (130 + 8 + 8) * self.sparse.n_tiles
+        return s * self.nnz_stored + idx + 8 * self.n_tiles + 2 * self.n * k * s
 
     def descriptor(self) -> CimHalfTiles:
         if self._desc is None:
@@ -253,6 +354,7 @@ class HalfTiles:
                 vals=self.vals.data_ptr() if self.n_tiles else None,
                 layout=LAYOUTS[self.layout],
                 reserved=0,
+                sparse=ctypes.pointer(self.sparse.descriptor()) if self.n_sparse_tiles else None,
             )
         return self._desc
 
@@ -350,12 +452,17 @@ class HalfTiles:
 
     @classmethod
     def from_coo(cls, n: int, i, j, v, *, dtype=torch.float32, device="cuda", check_symmetric: bool = True,
-                 max_unit: int = DEFAULT_MAX_UNIT, layout: str | None = None) -> "HalfTiles":
+                 max_unit: int = DEFAULT_MAX_UNIT, layout: str | None = None, bands: int | None = 1,
+                 dense_fill: float | None = None) -> "HalfTiles":
         """From a full (both-triangle) symmetric COO, e.g. a reference skeleton.
 
         Keeps entries with ⌊i/64⌋ ≤ ⌊j/64⌋ — lossless for an exactly symmetric
-        matrix.  Raises ValueError if (i,j,v) is not exactly
-        symmetric (when check_symmetric) or indices fall outside [0, n).
+        matrix.  Tiles filled at least ``dense_fill`` (default
+        the dense break-even, ``dense_break_even``) are stored dense, the rest
+        as COO-in-tile sparse tiles (``dense_fill=0`` forces all-dense).
+        Duplicate (i, j) entries are summed.  Raises ValueError if (i,j,v) is
+        not exactly symmetric (when check_symmetric) or indices fall outside
+        [0, n).
         """
         i = np.asarray(i, dtype=np.int64)
         j = np.asarray(j, dtype=np.int64)
@@ -374,15 +481,36 @@ class HalfTiles:
         C = j // BLOCK
         keep = R <= C
         i, j, v, R, C = i[keep], j[keep], v[keep], R[keep], C[keep]
+        # merge duplicate entries, then group by tile
+        ekey, einv = np.unique(i * n + j, return_inverse=True)
+        vsum = np.zeros(ekey.size, dtype=np.float64)
+        np.add.at(vsum, einv, v.astype(np.float64))
+        i, j = ekey // n, ekey % n
+        R, C = i // BLOCK, j // BLOCK
         key = R * nb + C
-        uniq, inv = np.unique(key, return_inverse=True)
+        uniq, inv, counts = np.unique(key, return_inverse=True, return_counts=True)
+        thr = dense_break_even(dtype) if dense_fill is None else float(dense_fill)
+        is_dense = counts >= thr * BLOCK * BLOCK
         np_dtype = np.float64 if _as_torch_dtype(dtype) == torch.float64 else np.float32
-        tiles = np.zeros((uniq.size, BLOCK, BLOCK), dtype=np.float64)
-        np.add.at(tiles, (inv, i % BLOCK, j % BLOCK), v.astype(np.float64))
-        rc = np.stack([uniq // nb, uniq % nb], axis=1).astype(np.int32)
-        H = cls.from_dense_tiles(n, rc, tiles.astype(np_dtype), dtype=dtype, device=device, max_unit=max_unit,
-                                 layout=layout)
-        H.meta.update(kind="coo", nnz_full=int(keep.size), nnz_half=int(i.size))
+        rc_all = np.stack([uniq // nb, uniq % nb], axis=1).astype(np.int32)
+        d_ids = np.flatnonzero(is_dense)
+        d_map = np.full(uniq.size, -1, dtype=np.int64)
+        d_map[d_ids] = np.arange(d_ids.size)
+        de = is_dense[inv]
+        tiles = np.zeros((d_ids.size, BLOCK, BLOCK), dtype=np.float64)
+        np.add.at(tiles, (d_map[inv[de]], i[de] % BLOCK, j[de] % BLOCK), vsum[de])
+        H = cls.from_dense_tiles(n, rc_all[d_ids], tiles.astype(np_dtype), dtype=dtype, device=device,
+                                 max_unit=max_unit, layout=layout, bands=bands)
+        s_ids = np.flatnonzero(~is_dense)
+        if s_ids.size:
+            s_map = np.full(uniq.size, -1, dtype=np.int64)
+            s_map[s_ids] = np.arange(s_ids.size)
+            se = ~de
+            H.sparse = SparseTiles.from_entries(rc_all[s_ids], s_map[inv[se]], i[se] % BLOCK, j[se] % BLOCK,
+                                                vsum[se], H.dtype, H.device)
+            H._desc = None
+        H.meta.update(kind="coo", nnz_full=int(keep.size), nnz_half=int(i.size), dense_fill=thr,
+                      dense_tiles=int(d_ids.size), sparse_tiles=int(s_ids.size))
         return H
 
     @classmethod
@@ -410,21 +538,56 @@ class HalfTiles:
                                              LAYOUTS[self.layout], out.data_ptr(), stream), "cim_unpack_tiles")
         return out
 
+    def export_dense(self) -> tuple[np.ndarray, np.ndarray]:
+        """Host (tile_rc, row-major tiles) of every stored tile — dense and
+        sparse (expanded) — sorted by (R, C).  Export / checking only."""
+        rc = self.tile_rc_host
+        tiles = self.dense_tiles().cpu().numpy()
+        if self.sparse is not None and self.sparse.n_tiles:
+            tid, r, c, v, _ = self.sparse.to_entries()
+            st = np.zeros((self.sparse.n_tiles, BLOCK, BLOCK), dtype=tiles.dtype)
+            st[tid, r, c] = v
+            rc = np.concatenate([rc, self.sparse.tile_rc_host])
+            tiles = np.concatenate([tiles, st])
+        order = np.lexsort((rc[:, 1], rc[:, 0]))
+        return np.ascontiguousarray(rc[order]), tiles[order]
+
     def save(self, path) -> None:
-        """npz interchange: n, tile_rc, row-major tiles (host)."""
-        np.savez_compressed(path, n=self.n, tile_rc=self.tile_rc_host, tiles=self.dense_tiles().cpu().numpy(),
-                            format="cim_half_tiles_v1", layout=self.layout)
+        """npz interchange (host): n, dense tile_rc + row-major tiles, and the
+        sparse tiles (tile_rc, entry offsets, row pointers, columns, values)."""
+        extra = {}
+        if self.sparse is not None:
+            sp = self.sparse
+            extra = dict(sp_tile_rc=sp.tile_rc_host, sp_entry_off=sp.entry_off_host,
+                         sp_rowptr=sp.rowptr.cpu().numpy(), sp_col=sp.col.cpu().numpy(), sp_vals=sp.vals.cpu().numpy())
+        order = np.lexsort((self.tile_rc_host[:, 1], self.tile_rc_host[:, 0]))  # (R, C) order on disk
+        np.savez_compressed(path, n=self.n, tile_rc=self.tile_rc_host[order],
+                            tiles=self.dense_tiles().cpu().numpy()[order],
+                            format="cim_half_tiles_v2", layout=self.layout, **extra)
 
     @classmethod
     def load(cls, path, device="cuda", **kw) -> "HalfTiles":
         z = np.load(path)
-        if str(z["format"]) != "cim_half_tiles_v1":
-            raise ValueError(f"{path}: not a cim_half_tiles_v1 file")
+        fmt = str(z["format"])
+        if fmt not in ("cim_half_tiles_v1", "cim_half_tiles_v2"):
+            raise ValueError(f"{path}: not a cim_half_tiles file")
         kw.setdefault("layout", str(z["layout"]) if "layout" in z.files else None)
-        return cls.from_dense_tiles(int(z["n"]), z["tile_rc"], z["tiles"], device=device, **kw)
+        H = cls.from_dense_tiles(int(z["n"]), z["tile_rc"], z["tiles"], device=device, **kw)
+        if "sp_tile_rc" in z.files:
+            dev = H.device
+            H.sparse = SparseTiles(tile_rc=torch.from_numpy(z["sp_tile_rc"]).to(dev),
+                                   entry_off=torch.from_numpy(z["sp_entry_off"]).to(dev),
+                                   rowptr=torch.from_numpy(z["sp_rowptr"]).to(dev),
+                                   col=torch.from_numpy(z["sp_col"]).to(dev),
+                                   vals=torch.from_numpy(z["sp_vals"]).to(dev, H.dtype),
+                                   tile_rc_host=z["sp_tile_rc"], entry_off_host=z["sp_entry_off"])
+            H._desc = None
+        return H
 
     def shard(self, unit_lo: int, unit_hi: int) -> "HalfTiles":
         """View of the tiles of units [unit_lo, unit_hi) (same n; GPU panel)."""
+        if self.sparse is not None:
+            raise NotImplementedError("sharding a matrix with sparse tiles is not supported yet")
         u = self.units_host[unit_lo:unit_hi]
         if u.shape[0] == 0:
             t0 = t1 = 0

@@ -85,9 +85,19 @@ def operator_tiles(pattern: HalfTiles, op_kind: str, k: int, seed: int) -> HalfT
             _dtype_code(pattern.dtype), LAYOUTS[pattern.layout], _OP_CODES[op_kind], seed, k,
             pattern.vals.data_ptr() if pattern.n_tiles else None, vals.data_ptr() if pattern.n_tiles else None,
             stream), "cim_fill_masked_values")
+    sparse = None
+    if pattern.sparse is not None:
+        sp = pattern.sparse
+        svals = torch.empty_like(sp.vals)
+        with torch.cuda.device(pattern.device):
+            check(lib().cim_fill_sparse_values(sp.descriptor(), pattern.n, _dtype_code(pattern.dtype),
+                                               _OP_CODES[op_kind], seed, k, sp.vals.data_ptr() if sp.n_entries else None,
+                                               svals.data_ptr() if sp.n_entries else None, stream),
+                  "cim_fill_sparse_values")
+        sparse = sp.with_values(svals)
     return HalfTiles(n=pattern.n, tile_rc=pattern.tile_rc, units=pattern.units, vals=vals,
                      tile_rc_host=pattern.tile_rc_host, units_host=pattern.units_host, layout=pattern.layout,
-                     meta=dict(pattern.meta, op_kind=op_kind, op_k=k, op_seed=seed))
+                     meta=dict(pattern.meta, op_kind=op_kind, op_k=k, op_seed=seed), sparse=sparse)
 
 
 def contract_observables(pattern: HalfTiles, inputs: ObservablesInput, strategy: str = "array_clause",

@@ -106,13 +106,16 @@ def test_reference_skeleton_spmm(pkg, name, dtype, layout):
     f = load_fixture(name)
     n = int(f["n"])
     H = pkg.HalfTiles.from_coo(n, f["i"], f["j"], f["v"], dtype=dtype, layout=layout)
+    # ragged orbital blocks: most 64-tiles fall below the dense break-even → sparse tiles
+    if name == "skel_n1024.npz":
+        assert H.n_sparse_tiles > H.n_tiles
     # structure: the stored half-tile set reproduces the reference pair set exactly
-    tiles = H.dense_tiles().cpu().numpy()
-    i, j, v = oracle.half_tiles_to_coo(n, H.tile_rc_host, tiles)
+    rc, tiles = H.export_dense()
+    i, j, v = oracle.half_tiles_to_coo(n, rc, tiles)
     assert oracle.pair_set_digest(i, j) == str(f["pair_digest"])
     X = torch.from_numpy(f["X"]).to(dtype)
     Y = pkg.sym_spmm(H, X.cuda()).cpu().numpy()
-    check_result(n, H.tile_rc_host, tiles.astype(np.float64), f["X"], Y, dtype)
+    check_result(n, rc, tiles.astype(np.float64), f["X"], Y, dtype)
     # against the reference's matrix product computed by scipy from its COO
     rel = np.linalg.norm(Y - f["Y_ref"]) / np.linalg.norm(f["Y_ref"])
     assert rel <= (1e-5 if dtype == torch.float32 else 1e-12)
@@ -142,7 +145,7 @@ def test_contract_observables_matches_reference(pkg, name, layout):
 def test_single_state_diagonal(pkg, layout):
     # test_pipeline.py:131-138: one state → nnz 1, stored value exactly h(0,0,0)
     h0 = np.array([oracle.h_values(0, 0, 0)], np.float32).reshape(1)
-    H = pkg.HalfTiles.from_coo(1, [0], [0], h0, layout=layout)
+    H = pkg.HalfTiles.from_coo(1, [0], [0], h0, layout=layout, dense_fill=0.0)
     assert H.n_tiles == 1 and H.n == 1
     assert H.dense_tiles()[0, 0, 0].item() == float(h0[0])
     Y = pkg.sym_spmm(H, torch.tensor([[2.0]], device="cuda"))
@@ -295,6 +298,13 @@ def test_save_load_roundtrip(pkg, c1_small, tmp_path):
     H.save(tmp_path / "h.npz")
     H2 = pkg.HalfTiles.load(tmp_path / "h.npz")
     assert torch.equal(H.vals, H2.vals) and np.array_equal(H.tile_rc_host, H2.tile_rc_host)
+    # mixed dense + sparse storage round-trips too
+    f = load_fixture("skel_n1024.npz")
+    M = pkg.HalfTiles.from_coo(int(f["n"]), f["i"], f["j"], f["v"])
+    M.save(tmp_path / "m.npz")
+    M2 = pkg.HalfTiles.load(tmp_path / "m.npz")
+    a, b = M.export_dense(), M2.export_dense()
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and M2.n_sparse_tiles == M.n_sparse_tiles
 
 
 def test_sharded_world1_equals_direct(pkg):
@@ -453,3 +463,57 @@ def test_column_banded_storage(pkg, c1_small, bands):
     pos = {tuple(r): s for s, r in enumerate(H2.tile_rc_host)}
     for t_in, r in enumerate(rc[:50]):
         assert np.array_equal(back[pos[tuple(r)]], tiles[t_in])
+
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("fill", [0.0, 0.02, 0.3, 0.9])
+@pytest.mark.parametrize("k", [1, 2, 4, 8, 12, 16])
+def test_sparse_tiles_vs_oracle(pkg, dtype, fill, k):
+    """COO-in-tile storage: random symmetric matrices whose 64-tiles have a
+    given fill (ragged n, empty rows, diagonal and off-diagonal tiles), stored
+    with the break-even split (fill 0.9 → dense) and forced all-sparse; the
+    operator must match the oracle and the all-dense storage."""
+    rng = np.random.default_rng(int(fill * 100) + k)
+    n = 700
+    nb = (n + 63) // 64
+    rc = pkg.synthetic_pattern(nb, 0.4, seed=2)
+    ii, jj = [], []
+    for R, C in rc:
+        m = rng.random((64, 64)) < max(fill, 0.002)
+        if R == C:
+            m = m | m.T
+        a, b = np.nonzero(m)
+        ii.append(R * 64 + a)
+        jj.append(C * 64 + b)
+    i = np.concatenate(ii)
+    j = np.concatenate(jj)
+    ok = (i < n) & (j < n)
+    i, j = i[ok], j[ok]
+    key = np.unique(np.minimum(i, j) * n + np.maximum(i, j))
+    lo, hi = key // n, key % n
+    vals = rng.standard_normal(key.size)
+    I = np.concatenate([lo, hi[lo != hi]])
+    J = np.concatenate([hi, lo[lo != hi]])
+    V = np.concatenate([vals, vals[lo != hi]])
+    npd = np.float32 if dtype == torch.float32 else np.float64
+    V = V.astype(npd)
+    X = torch.randn((n, k), generator=torch.Generator().manual_seed(k), dtype=dtype)
+    H_mix = pkg.HalfTiles.from_coo(n, I, J, V, dtype=dtype)
+    H_sp = pkg.HalfTiles.from_coo(n, I, J, V, dtype=dtype, dense_fill=2.0)
+    H_dn = pkg.HalfTiles.from_coo(n, I, J, V, dtype=dtype, dense_fill=0.0)
+    assert H_sp.n_tiles == 0 and H_dn.n_sparse_tiles == 0
+    if fill < 0.5:
+        assert H_mix.n_sparse_tiles > 0
+    rc_all, tiles = H_dn.export_dense()
+    for H in (H_mix, H_sp, H_dn):
+        Y = pkg.sym_spmm(H, X.cuda()).cpu().numpy()
+        check_result(n, rc_all, tiles.astype(np.float64), X.numpy(), Y, dtype)
+    # accumulate path and host batch on the mixed storage
+    out = torch.ones((n, k), dtype=dtype, device="cuda")
+    pkg.sym_spmm(H_mix, X.cuda(), out=out, accumulate=True)
+    Y1 = pkg.sym_spmm(H_mix, X.cuda())
+    assert (out - 1.0 - Y1).abs().max().item() <= 1e-5 * Y1.abs().max().item() + 1e-6
+    if k in (4, 8):
+        Yb = pkg.sym_spmm_host_batch(H_mix, [X.pin_memory()])[0]
+        assert (Yb.cuda() - Y1).abs().max().item() <= 1e-5 * Y1.abs().max().item() + 1e-6
