@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget for the cpu_baseline leg")
     ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--bands", type=int, default=1, help="column bands of the tile order (0 = auto)")
+    ap.add_argument("--fill", type=float, default=None,
+                    help="store every tile sparse (COO-in-tile) with this entry fill (1 GPU); default: dense tiles")
     return ap.parse_args()
 
 
@@ -238,8 +240,16 @@ def impl_ours(args):
     n, nb, n_off, p = workload(args, world)
 
     t_build = time.perf_counter()
-    S = ShardedSymSpmm.synthetic(n, k=k, p=p, seed=0, dtype=dtype, device=dev, layout=args.layout,
-                                 bands=None if args.bands == 0 else args.bands)
+    if args.fill is not None:
+        if world != 1:
+            raise SystemExit("--fill (sparse tiles) is a single-GPU workload")
+        Hs = pkg.HalfTiles.synthetic_sparse(n, p=p, fill=args.fill, seed=0, dtype=dtype, device=dev)
+        Hs.meta.update(global_tiles=Hs.n_sparse_tiles,
+                       global_off_tiles=int(np.count_nonzero(Hs.sparse.tile_rc_host[:, 0] != Hs.sparse.tile_rc_host[:, 1])))
+        S = ShardedSymSpmm(n, k, dtype, dev, H_local=Hs)
+    else:
+        S = ShardedSymSpmm.synthetic(n, k=k, p=p, seed=0, dtype=dtype, device=dev, layout=args.layout,
+                                     bands=None if args.bands == 0 else args.bands)
     H = S.H
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t_build
@@ -248,9 +258,9 @@ def impl_ours(args):
     g_tiles = H.meta["global_tiles"]
     g_off = H.meta["global_off_tiles"]
     g_diag = g_tiles - g_off
-    flops_global = 2 * k * (2 * g_off + g_diag) * 4096
+    flops_global = 2 * k * (2 * g_off + g_diag) * 4096 if args.fill is None else H.flops(k)
     flops_local = H.flops(k)
-    bytes_local = es * H.nnz_stored + 8 * H.n_tiles + 2 * n * k * es
+    bytes_local = H.algorithmic_bytes(k)
 
     stream = torch.cuda.current_stream(dev)
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
@@ -364,11 +374,11 @@ def impl_ours(args):
         tf = ROOT / "profiles" / "roofline_traffic.json"
         if tf.exists():
             try:
-                traffic = json.loads(tf.read_text()).get(f"k{k}_{args.dtype}")
+                traffic = json.loads(tf.read_text()).get(f"k{k}_{args.dtype}" + ("" if args.fill is None else f"_fill{args.fill}"))
             except Exception:
                 traffic = None
         cpu_b = None
-        if not args.no_cpu_baseline and world == 1:
+        if not args.no_cpu_baseline and world == 1 and args.fill is None:
             try:
                 cpu_b = run_cpu(n, nb, p, k, args.cpu_seconds)
             except Exception as ex:  # never let the baseline kill the GPU line
@@ -389,9 +399,10 @@ def impl_ours(args):
             "config": {
                 "workload": ("C2" if world == 1 else f"C3-family weak scaling ({world}x C2 tiles, same n)")
                 + f": synthetic half-stored symmetric H, n={n}, block 64, {g_tiles} stored tiles "
-                  f"({g_diag} diagonal + {g_off} upper), {g_tiles * 4096 / 1e9:.3f}e9 stored values, "
-                  f"k={k}, values h(i XOR j; 0) on device, X ~ N(0,1)",
-                "n": n, "k": k, "stored_tiles": g_tiles, "stored_nnz": g_tiles * 4096,
+                  f"({g_diag} diagonal + {g_off} upper), {H.nnz_stored / 1e9:.3f}e9 stored values"
+                + (f" (all tiles sparse COO-in-tile, entry fill {args.fill})" if args.fill is not None else "")
+                + f", k={k}, values h(i XOR j; 0) on device, X ~ N(0,1)",
+                "n": n, "k": k, "stored_tiles": g_tiles, "stored_nnz": H.nnz_stored,
                 "parallelism": f"row-block shard x{world}" if world > 1 else "single GPU",
                 "layout": H.layout,
                 "bands": H.meta.get("bands", 1),
@@ -403,7 +414,8 @@ def impl_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
                          "kernel": "sym_spmm_tc_kernel (tcgen05 kind::tf32, 3xTF32 split)" if H.layout == "tc"
-                         else ("sym_spmm_k8_kernel (FFMA2, setmaxnreg warpgroups, X_R in registers)"
+                         else ("sparse_spmm_kernel (COO-in-tile, warp per tile)" if args.fill is not None else
+                               "sym_spmm_k8_kernel (FFMA2, setmaxnreg warpgroups, X_R in registers)"
                                if (k == 8 and dtype == torch.float32) else "sym_spmm_kernel (FFMA2/FFMA)"),
                          "kernel_ms": kern_max,
                          "algorithmic_bytes_per_launch": bytes_local,

@@ -84,15 +84,21 @@ extern "C" {
 
 /*
  * Sparse ("COO-in-tile") stored tiles, for 64-tiles below the dense
- * break-even fill (⅔ for f32, 0.8 for f64: SURVEY §7 step 4) — the ragged
+ * break-even fill (½ for f32, ⅔ for f64) — the ragged
  * orbital blocks of reference skeletons average 17% fill.  Per tile the
- * entries are sorted by local row then column:
+ * entries are sorted by local row, then column (row-major order); a column
+ * permutation lists them column by column for the transposed product, so
+ * both products are register reductions (no atomics inside a tile):
  *   tile_rc    int32  [n_tiles][2]   (R, C), R ≤ C (any order)
- *   entry_off  int64  [n_tiles+1]    first entry of each tile
+ *   entry_off  int64  [n_tiles+1]    first entry of each tile, a multiple of 16
+ *                                    (entries rowptr[t][64] .. next tile are zero
+ *                                    padding, so tiles stage with 16-byte copies)
  *   rowptr     uint16 [n_tiles][65]  per local row, offsets relative to the tile
- *   col        uint8  [n_entries]    local column
+ *   colptr     uint16 [n_tiles][65]  per local column, offsets into cperm
+ *   col, row   uint8  [n_entries]    local column / row of each entry
+ *   cperm      uint16 [n_entries]    tile-relative entry indices in column-major order
  *   vals       f32|f64[n_entries]
- * Bytes per entry: 1 + s (+ 138 B per tile), against 4096·s for a dense tile.
+ * Bytes per entry: 4 + s (+ 268 B per tile), against 4096·s for a dense tile.
  */
 typedef struct cim_sparse_tiles {
   int64_t         n_tiles;
@@ -100,7 +106,10 @@ typedef struct cim_sparse_tiles {
   const int32_t  *tile_rc;
   const int64_t  *entry_off;
   const uint16_t *rowptr;
+  const uint16_t *colptr;
   const uint8_t  *col;
+  const uint8_t  *row;
+  const uint16_t *cperm;
   const void     *vals;     /* dtype of the enclosing cim_half_tiles */
 } cim_sparse_tiles;
 
@@ -209,6 +218,24 @@ CIM_API int cim_tsmm_blocked(const float *A, int64_t lda, int32_t a_bw, int64_t 
 CIM_API int cim_fill_sparse_values(const cim_sparse_tiles *S, int64_t n, int32_t dtype, int32_t kind,
                                    uint64_t seed, int32_t op_k, const void *mask, void *vals_out,
                                    void *stream);
+
+/*
+ * Device construction of synthetic sparse tiles (count → scan → fill, the
+ * reference's build_skeleton motif, pipeline.py:290-377, on the GPU).
+ * cim_sparse_count_rows: rowcnt[t·64 + r] = kept entries of local row r of
+ * tile t, kept(i, j) = symmetric hash(min, max; seed) < fill·2⁶⁴ (i, j < n).
+ * The caller scans them into S->rowptr / S->entry_off and allocates the
+ * entry arrays; cim_sparse_fill_entries then writes row-sorted columns, rows
+ * and values of `kind` (as cim_fill_synthetic_values; h(i XOR j) bit-exact)
+ * and cim_sparse_build_columns the column index (colptr, cperm) of any
+ * row-sorted sparse tiles.
+ */
+CIM_API int cim_sparse_count_rows(const int32_t *tile_rc, int64_t n_tiles, int64_t n, double fill,
+                                  uint64_t seed, int32_t *rowcnt, void *stream);
+CIM_API int cim_sparse_fill_entries(const cim_sparse_tiles *S, int64_t n, int32_t dtype, double fill,
+                                    uint64_t seed, int32_t kind, uint64_t value_seed, int32_t op_k,
+                                    void *stream);
+CIM_API int cim_sparse_build_columns(const cim_sparse_tiles *S, void *stream);
 
 /* Device workspace bytes cim_gram / cim_gram_blocked need. */
 CIM_API uint64_t cim_gram_workspace_bytes(int64_t rows, int32_t ca, int32_t cb);

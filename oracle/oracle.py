@@ -154,6 +154,28 @@ def synthetic_dense_tiles(n: int, tile_rc, seed: int = 0, kind: int = 0, op_k: i
     return val.astype(dtype)
 
 
+def synthetic_sparse_tiles(n: int, tile_rc, fill: float, fill_seed: int, value_seed: int = 0,
+                           dtype=np.float32) -> np.ndarray:
+    """Host twin of HalfTiles.synthetic_sparse (cim_sparse_count_rows /
+    cim_sparse_fill_entries): dense row-major (T,64,64) tiles holding h(i XOR j;
+    value_seed) where mix64(mix64(min ⊕ 0x5bd1e995·max) ⊕ fill_seed) < fill·2⁶⁴
+    and i, j < n, else 0.  (Test infrastructure; the keep rule is the
+    generator's own, the values the reference hash, pipeline.py:216-222.)"""
+    rc = np.asarray(tile_rc, dtype=np.int64)
+    a = np.arange(BLOCK, dtype=np.int64)
+    i = rc[:, 0, None, None] * BLOCK + a[None, :, None]
+    j = rc[:, 1, None, None] * BLOCK + a[None, None, :]
+    i, j = np.broadcast_arrays(i, j)
+    lo = np.minimum(i, j).astype(np.uint64)
+    hi = np.maximum(i, j).astype(np.uint64)
+    with np.errstate(over="ignore"):
+        key = mix64(mix64(lo ^ (hi * np.uint64(0x5BD1E995))) ^ np.uint64(fill_seed))
+    thresh = np.uint64(min(int(fill * 18446744073709551616.0), (1 << 64) - 1)) if fill < 1.0 else None
+    keep = (i < n) & (j < n) & ((key < thresh) if thresh is not None else True)
+    val = np.where(keep, h_values(i, j, value_seed), np.float32(0))
+    return val.astype(dtype)
+
+
 # ----------------------------------------------------------------------------
 # the SpMM definition in float64
 # ----------------------------------------------------------------------------

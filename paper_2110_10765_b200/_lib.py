@@ -37,6 +37,9 @@ EXPORTS = (
     "cim_sym_spmm_host_batch",
     "cim_host_batch_workspace_bytes",
     "cim_fill_sparse_values",
+    "cim_sparse_count_rows",
+    "cim_sparse_fill_entries",
+    "cim_sparse_build_columns",
     "cim_gram",
     "cim_gram_workspace_bytes",
     "cim_tsmm",
@@ -54,7 +57,10 @@ class CimSparseTiles(ctypes.Structure):
         ("tile_rc", ctypes.c_void_p),
         ("entry_off", ctypes.c_void_p),
         ("rowptr", ctypes.c_void_p),
+        ("colptr", ctypes.c_void_p),
         ("col", ctypes.c_void_p),
+        ("row", ctypes.c_void_p),
+        ("cperm", ctypes.c_void_p),
         ("vals", ctypes.c_void_p),
     ]
 
@@ -120,6 +126,11 @@ def lib() -> ctypes.CDLL:
     L.cim_host_batch_workspace_bytes.argtypes = [c.POINTER(CimHalfTiles), c.c_int32]
     L.cim_fill_sparse_values.argtypes = [c.POINTER(CimSparseTiles), c.c_int64, c.c_int32, c.c_int32, c.c_uint64,
                                          c.c_int32, c.c_void_p, c.c_void_p, c.c_void_p]
+    L.cim_sparse_count_rows.argtypes = [c.c_void_p, c.c_int64, c.c_int64, c.c_double, c.c_uint64, c.c_void_p,
+                                        c.c_void_p]
+    L.cim_sparse_fill_entries.argtypes = [c.POINTER(CimSparseTiles), c.c_int64, c.c_int32, c.c_double, c.c_uint64,
+                                          c.c_int32, c.c_uint64, c.c_int32, c.c_void_p]
+    L.cim_sparse_build_columns.argtypes = [c.POINTER(CimSparseTiles), c.c_void_p]
     L.cim_gram.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_void_p, c.c_int64, c.c_int32, c.c_int64, c.c_int32,
                            c.c_void_p, c.c_void_p, c.c_uint64, c.c_void_p]
     L.cim_gram_workspace_bytes.argtypes = [c.c_int64, c.c_int32, c.c_int32]

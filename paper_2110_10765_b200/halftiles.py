@@ -181,11 +181,22 @@ def fragment_pack_host(tiles: np.ndarray, layout: str = "frag") -> np.ndarray:
     return np.ascontiguousarray(tiles.reshape(T, 4096)[:, row * BLOCK + col])
 
 
+SPARSE_ALIGN = 16  # entries: every sparse tile's entry range starts 16-entry aligned (vector staging)
+
+
 def dense_break_even(dtype) -> float:
-    """Fill above which a 64-tile is stored dense: dense costs 4096·s bytes, a
-    sparse tile (1 + s) bytes per entry (+138 B) — ⅔ for f32, 0.8 for f64
-    (SURVEY.md §7 step 4)."""
-    return 2.0 / 3.0 if _as_torch_dtype(dtype) == torch.float32 else 0.8
+    """Memory break-even fill of a 64-tile: dense costs 4096·s bytes, a sparse
+    tile (4 + s) bytes per entry (column, row, column permutation, value;
+    +268 B per tile) — ½ for f32, ⅔ for f64.  Pass it
+    as ``dense_fill`` to minimise HBM footprint."""
+    return 0.5 if _as_torch_dtype(dtype) == torch.float32 else 2.0 / 3.0
+
+
+# Time break-even on B200 (C2 pattern, k = 8 f32, profiles/r01/SUMMARY.md):
+# all-sparse storage runs 1.27 / 1.57 / 2.17 / 3.09 ms at 2 / 5 / 10 / 17%
+# entry fill against 1.63 ms for the same tiles stored dense, so tiles below
+# ~5% fill are faster sparse.  The default split optimises time.
+DEFAULT_DENSE_FILL = 0.05
 
 
 @dataclass
@@ -196,10 +207,14 @@ class SparseTiles:
     tile_rc: torch.Tensor  # int32 (Ts,2) device
     entry_off: torch.Tensor  # int64 (Ts+1) device
     rowptr: torch.Tensor  # int16 (Ts,65) device (values ≤ 4096)
+    colptr: torch.Tensor  # int16 (Ts,65) device
     col: torch.Tensor  # uint8 (E,) device
+    row: torch.Tensor  # uint8 (E,) device
+    cperm: torch.Tensor  # int16 (E,) device: tile-relative entry index, column-major order
     vals: torch.Tensor  # (E,) device, matrix dtype
     tile_rc_host: np.ndarray
-    entry_off_host: np.ndarray
+    entry_off_host: np.ndarray  # tile starts, multiples of SPARSE_ALIGN
+    counts_host: np.ndarray  # real entries per tile (the rest of a tile's range is zero padding)
     _desc: CimSparseTiles | None = field(default=None, repr=False)
 
     @property
@@ -208,22 +223,46 @@ class SparseTiles:
 
     @property
     def n_entries(self) -> int:
+        """Length of the entry arrays (real entries + per-tile padding)."""
         return int(self.entry_off_host[-1]) if self.entry_off_host.size else 0
 
+    @property
+    def n_real_entries(self) -> int:
+        return int(self.counts_host.sum())
+
     def entries_per_tile(self) -> np.ndarray:
-        return np.diff(self.entry_off_host)
+        return self.counts_host
 
     def descriptor(self) -> CimSparseTiles:
         if self._desc is None:
+            e = self.n_entries > 0
             self._desc = CimSparseTiles(n_tiles=self.n_tiles, n_entries=self.n_entries,
                                         tile_rc=self.tile_rc.data_ptr(), entry_off=self.entry_off.data_ptr(),
-                                        rowptr=self.rowptr.data_ptr(), col=self.col.data_ptr() if self.n_entries else None,
-                                        vals=self.vals.data_ptr() if self.n_entries else None)
+                                        rowptr=self.rowptr.data_ptr(), colptr=self.colptr.data_ptr(),
+                                        col=self.col.data_ptr() if e else None, row=self.row.data_ptr() if e else None,
+                                        cperm=self.cperm.data_ptr() if e else None,
+                                        vals=self.vals.data_ptr() if e else None)
         return self._desc
 
     def with_values(self, vals: torch.Tensor) -> "SparseTiles":
-        return SparseTiles(self.tile_rc, self.entry_off, self.rowptr, self.col, vals, self.tile_rc_host,
-                           self.entry_off_host)
+        return SparseTiles(self.tile_rc, self.entry_off, self.rowptr, self.colptr, self.col, self.row, self.cperm,
+                           vals, self.tile_rc_host, self.entry_off_host, self.counts_host)
+
+    def arrays(self) -> dict:
+        """Host copies of every array (npz interchange)."""
+        return dict(sp_tile_rc=self.tile_rc_host, sp_entry_off=self.entry_off_host, sp_counts=self.counts_host,
+                    sp_rowptr=self.rowptr.cpu().numpy(), sp_colptr=self.colptr.cpu().numpy(),
+                    sp_col=self.col.cpu().numpy(), sp_row=self.row.cpu().numpy(), sp_cperm=self.cperm.cpu().numpy(),
+                    sp_vals=self.vals.cpu().numpy())
+
+    @classmethod
+    def from_arrays(cls, z, dtype, device) -> "SparseTiles":
+        dev = torch.device(device)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+        return cls(tile_rc=t(z["sp_tile_rc"]), entry_off=t(z["sp_entry_off"]), rowptr=t(z["sp_rowptr"]),
+                   colptr=t(z["sp_colptr"]), col=t(z["sp_col"]), row=t(z["sp_row"]), cperm=t(z["sp_cperm"]),
+                   vals=t(z["sp_vals"]).to(dtype), tile_rc_host=np.asarray(z["sp_tile_rc"]),
+                   entry_off_host=np.asarray(z["sp_entry_off"]), counts_host=np.asarray(z["sp_counts"]))
 
     @classmethod
     def from_entries(cls, tile_rc: np.ndarray, tile_id: np.ndarray, r: np.ndarray, c: np.ndarray, v: np.ndarray,
@@ -233,32 +272,50 @@ class SparseTiles:
         order = np.lexsort((c, r, tile_id))
         tile_id, r, c, v = tile_id[order], r[order], c[order], v[order]
         T = tile_rc.shape[0]
-        counts = np.bincount(tile_id, minlength=T)
+        counts = np.bincount(tile_id, minlength=T).astype(np.int64)
         off = np.zeros(T + 1, dtype=np.int64)
-        np.cumsum(counts, out=off[1:])
+        np.cumsum((counts + SPARSE_ALIGN - 1) // SPARSE_ALIGN * SPARSE_ALIGN, out=off[1:])
+        start = np.zeros(T + 1, dtype=np.int64)
+        np.cumsum(counts, out=start[1:])
+        local = np.arange(tile_id.size, dtype=np.int64) - start[tile_id]
+        pos = off[tile_id] + local  # slot of each (sorted) entry in the padded arrays
         rowcnt = np.zeros((T, 64), dtype=np.int64)
         np.add.at(rowcnt, (tile_id, r), 1)
         rowptr = np.zeros((T, 65), dtype=np.int64)
         np.cumsum(rowcnt, axis=1, out=rowptr[:, 1:])
+        colcnt = np.zeros((T, 64), dtype=np.int64)
+        np.add.at(colcnt, (tile_id, c), 1)
+        colptr = np.zeros((T, 65), dtype=np.int64)
+        np.cumsum(colcnt, axis=1, out=colptr[:, 1:])
+        corder = np.lexsort((r, c, tile_id))  # column-major within each tile, rows ascending
+        E = int(off[-1])
+        col_a = np.zeros(max(E, 1), np.uint8)
+        row_a = np.zeros(max(E, 1), np.uint8)
+        cperm_a = np.zeros(max(E, 1), np.int16)
+        val_a = np.zeros(max(E, 1), np.float64)
+        col_a[pos], row_a[pos], val_a[pos] = c, r, v
+        cperm_a[off[tile_id] + local] = local[corder]  # k-th slot of tile t holds its k-th column-major entry
         dev = torch.device(device)
         return cls(tile_rc=torch.from_numpy(np.ascontiguousarray(tile_rc, dtype=np.int32)).to(dev),
                    entry_off=torch.from_numpy(off).to(dev),
                    rowptr=torch.from_numpy(rowptr.astype(np.int16)).to(dev),
-                   col=torch.from_numpy(c.astype(np.uint8)).to(dev),
-                   vals=torch.from_numpy(np.asarray(v, dtype=np.float64)).to(dev, _as_torch_dtype(dtype)),
-                   tile_rc_host=np.ascontiguousarray(tile_rc, dtype=np.int32), entry_off_host=off)
+                   colptr=torch.from_numpy(colptr.astype(np.int16)).to(dev),
+                   col=torch.from_numpy(col_a).to(dev), row=torch.from_numpy(row_a).to(dev),
+                   cperm=torch.from_numpy(cperm_a).to(dev),
+                   vals=torch.from_numpy(val_a).to(dev, _as_torch_dtype(dtype)),
+                   tile_rc_host=np.ascontiguousarray(tile_rc, dtype=np.int32), entry_off_host=off,
+                   counts_host=counts)
 
     def to_entries(self):
-        """Host (tile_id, r, c, v) of every entry (stored order)."""
-        rp = self.rowptr.cpu().numpy().astype(np.int64)
-        off = self.entry_off_host
-        T = self.n_tiles
-        tile_id = np.repeat(np.arange(T), np.diff(off))
-        local = np.arange(self.n_entries) - off[tile_id]
-        r = np.empty(self.n_entries, dtype=np.int64)
-        for t in range(T):  # host export only
-            r[off[t]:off[t + 1]] = np.repeat(np.arange(64), np.diff(rp[t]))
-        return tile_id, r, self.col.cpu().numpy().astype(np.int64), self.vals.cpu().numpy(), local
+        """Host (tile_id, r, c, v, tile-relative index) of every real entry (stored order)."""
+        off, cnt = self.entry_off_host, self.counts_host
+        tile_id = np.repeat(np.arange(self.n_tiles), cnt)
+        start = np.zeros(self.n_tiles + 1, dtype=np.int64)
+        np.cumsum(cnt, out=start[1:])
+        local = np.arange(int(cnt.sum())) - start[tile_id]
+        pos = off[tile_id] + local
+        return (tile_id, self.row.cpu().numpy().astype(np.int64)[pos], self.col.cpu().numpy().astype(np.int64)[pos],
+                self.vals.cpu().numpy()[pos], local)
 
 
 @dataclass
@@ -324,7 +381,7 @@ class HalfTiles:
     @property
     def nnz_stored(self) -> int:
         """Stored entries: 4096 per dense tile plus the sparse tiles' entries."""
-        return self.n_tiles * BLOCK * BLOCK + (self.sparse.n_entries if self.sparse is not None else 0)
+        return self.n_tiles * BLOCK * BLOCK + (self.sparse.n_real_entries if self.sparse is not None else 0)
 
     def flops(self, k: int) -> int:
         """Algorithmic FLOPs of one apply: 2·k·(2·nnz_off + nnz_diag)."""
@@ -333,12 +390,12 @@ class HalfTiles:
 
     def algorithmic_bytes(self, k: int) -> int:
         """s·nnz_stored + index bytes + 8·tiles + 2·n·k·s:
-        sparse entries carry a 1-byte column, sparse tiles a 130-byte row
-        pointer and an 8-byte entry offset."""
+        sparse entries carry a column, a row and a column-permutation index
+        (4 B), sparse tiles two 130-byte pointer arrays and an 8-byte offset."""
         s = self.vals.element_size()
         idx = 0
         if self.sparse is not None:
-            idx = self.sparse.n_entries + (130 + 8 + 8) * self.sparse.n_tiles
+            idx = 4 * self.sparse.n_real_entries + (260 + 8 + 8) * self.sparse.n_tiles
         return s * self.nnz_stored + idx + 8 * self.n_tiles + 2 * self.n * k * s
 
     def descriptor(self) -> CimHalfTiles:
@@ -430,6 +487,65 @@ class HalfTiles:
         return H
 
     @classmethod
+    def synthetic_sparse(cls, n: int, p: float | None = None, *, fill: float, n_off: int | None = None, seed: int = 0,
+                         fill_seed: int = 1, value_seed: int = 0, values: str = "h_xor", op_k: int = 0,
+                         dtype=torch.float32, device="cuda", tile_rc: np.ndarray | None = None) -> "HalfTiles":
+        """Synthetic matrix whose stored 64-tiles are all sparse: the tile
+        pattern of ``synthetic`` (seed, p / n_off), and inside each tile the
+        entries (i, j) kept with probability ``fill`` by a symmetric hash of
+        (min, max; fill_seed) — ragged rows like the reference's orbital
+        blocks.  Built on the device by count → scan → fill (the reference's
+        build_skeleton motif, pipeline.py:290-377): ``cim_sparse_count_rows``,
+        torch scans, ``cim_sparse_fill_entries``."""
+        if values not in VALUE_KINDS:
+            raise ValueError(f"unknown values {values!r}, expected one of {tuple(VALUE_KINDS)}")
+        if not 0.0 <= fill <= 1.0:
+            raise ValueError(f"fill must be in [0, 1], got {fill}")
+        nb = (n + BLOCK - 1) // BLOCK
+        if tile_rc is None:
+            n_pairs = nb * (nb - 1) // 2
+            if p is None:
+                p = 0.0 if n_pairs == 0 else float(n_off or 0) / n_pairs
+            tile_rc = synthetic_pattern(nb, p, seed)
+        dtype = _as_torch_dtype(dtype)
+        H, _ = cls._from_pattern(n, np.zeros((0, 2), np.int32), dtype, device, DEFAULT_MAX_UNIT, None, 1)
+        rc = np.ascontiguousarray(tile_rc, dtype=np.int32)
+        plan_units(rc, nb)  # validates the pattern
+        T = rc.shape[0]
+        dev = H.device
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        t_rc = torch.from_numpy(rc).to(dev)
+        rowcnt = torch.empty((max(T, 1), 64), dtype=torch.int32, device=dev)
+        L = lib()
+        with torch.cuda.device(dev):
+            check(L.cim_sparse_count_rows(t_rc.data_ptr() if T else None, T, n, float(fill), fill_seed,
+                                          rowcnt.data_ptr(), stream), "cim_sparse_count_rows")
+        rowcnt = rowcnt[:T]
+        rowptr = torch.zeros((T, 65), dtype=torch.int64, device=dev)
+        rowptr[:, 1:] = torch.cumsum(rowcnt, dim=1)
+        counts = rowptr[:, 64]
+        off = torch.zeros(T + 1, dtype=torch.int64, device=dev)
+        off[1:] = torch.cumsum((counts + SPARSE_ALIGN - 1) // SPARSE_ALIGN * SPARSE_ALIGN, dim=0)
+        off_host = off.cpu().numpy()
+        E = int(off_host[-1])
+        sp = SparseTiles(tile_rc=t_rc, entry_off=off, rowptr=rowptr.to(torch.int16),
+                         colptr=torch.empty((T, 65), dtype=torch.int16, device=dev),
+                         col=torch.zeros(max(E, 1), dtype=torch.uint8, device=dev),
+                         row=torch.zeros(max(E, 1), dtype=torch.uint8, device=dev),
+                         cperm=torch.zeros(max(E, 1), dtype=torch.int16, device=dev),
+                         vals=torch.zeros(max(E, 1), dtype=dtype, device=dev), tile_rc_host=rc, entry_off_host=off_host,
+                         counts_host=counts.cpu().numpy())
+        with torch.cuda.device(dev):
+            check(L.cim_sparse_fill_entries(sp.descriptor(), n, _dtype_code(dtype), float(fill), fill_seed,
+                                            VALUE_KINDS[values], value_seed, op_k, stream), "cim_sparse_fill_entries")
+            check(L.cim_sparse_build_columns(sp.descriptor(), stream), "cim_sparse_build_columns")
+        H.sparse = sp
+        H._desc = None
+        H.meta.update(kind="synthetic_sparse", p=p, seed=seed, fill=fill, fill_seed=fill_seed, value_seed=value_seed,
+                      values=values, op_k=op_k)
+        return H
+
+    @classmethod
     def from_dense_tiles(cls, n: int, tile_rc: np.ndarray, tiles, *, dtype=None, device="cuda",
                          max_unit: int = DEFAULT_MAX_UNIT, layout: str | None = None,
                          bands: int | None = 1) -> "HalfTiles":
@@ -458,8 +574,10 @@ class HalfTiles:
 
         Keeps entries with ⌊i/64⌋ ≤ ⌊j/64⌋ — lossless for an exactly symmetric
         matrix.  Tiles filled at least ``dense_fill`` (default
-        the dense break-even, ``dense_break_even``) are stored dense, the rest
+        below) are stored dense, the rest
         as COO-in-tile sparse tiles (``dense_fill=0`` forces all-dense).
+        The default is the measured time break-even (``DEFAULT_DENSE_FILL``);
+        ``dense_break_even(dtype)`` minimises memory instead.
         Duplicate (i, j) entries are summed.  Raises ValueError if (i,j,v) is
         not exactly symmetric (when check_symmetric) or indices fall outside
         [0, n).
@@ -489,7 +607,7 @@ class HalfTiles:
         R, C = i // BLOCK, j // BLOCK
         key = R * nb + C
         uniq, inv, counts = np.unique(key, return_inverse=True, return_counts=True)
-        thr = dense_break_even(dtype) if dense_fill is None else float(dense_fill)
+        thr = DEFAULT_DENSE_FILL if dense_fill is None else float(dense_fill)
         is_dense = counts >= thr * BLOCK * BLOCK
         np_dtype = np.float64 if _as_torch_dtype(dtype) == torch.float64 else np.float32
         rc_all = np.stack([uniq // nb, uniq % nb], axis=1).astype(np.int32)
@@ -555,11 +673,7 @@ class HalfTiles:
     def save(self, path) -> None:
         """npz interchange (host): n, dense tile_rc + row-major tiles, and the
         sparse tiles (tile_rc, entry offsets, row pointers, columns, values)."""
-        extra = {}
-        if self.sparse is not None:
-            sp = self.sparse
-            extra = dict(sp_tile_rc=sp.tile_rc_host, sp_entry_off=sp.entry_off_host,
-                         sp_rowptr=sp.rowptr.cpu().numpy(), sp_col=sp.col.cpu().numpy(), sp_vals=sp.vals.cpu().numpy())
+        extra = self.sparse.arrays() if self.sparse is not None else {}
         order = np.lexsort((self.tile_rc_host[:, 1], self.tile_rc_host[:, 0]))  # (R, C) order on disk
         np.savez_compressed(path, n=self.n, tile_rc=self.tile_rc_host[order],
                             tiles=self.dense_tiles().cpu().numpy()[order],
@@ -574,13 +688,7 @@ class HalfTiles:
         kw.setdefault("layout", str(z["layout"]) if "layout" in z.files else None)
         H = cls.from_dense_tiles(int(z["n"]), z["tile_rc"], z["tiles"], device=device, **kw)
         if "sp_tile_rc" in z.files:
-            dev = H.device
-            H.sparse = SparseTiles(tile_rc=torch.from_numpy(z["sp_tile_rc"]).to(dev),
-                                   entry_off=torch.from_numpy(z["sp_entry_off"]).to(dev),
-                                   rowptr=torch.from_numpy(z["sp_rowptr"]).to(dev),
-                                   col=torch.from_numpy(z["sp_col"]).to(dev),
-                                   vals=torch.from_numpy(z["sp_vals"]).to(dev, H.dtype),
-                                   tile_rc_host=z["sp_tile_rc"], entry_off_host=z["sp_entry_off"])
+            H.sparse = SparseTiles.from_arrays(z, H.dtype, H.device)
             H._desc = None
         return H
 

@@ -88,7 +88,7 @@ def operator_tiles(pattern: HalfTiles, op_kind: str, k: int, seed: int) -> HalfT
     sparse = None
     if pattern.sparse is not None:
         sp = pattern.sparse
-        svals = torch.empty_like(sp.vals)
+        svals = torch.zeros_like(sp.vals)  # tile padding stays zero
         with torch.cuda.device(pattern.device):
             check(lib().cim_fill_sparse_values(sp.descriptor(), pattern.n, _dtype_code(pattern.dtype),
                                                _OP_CODES[op_kind], seed, k, sp.vals.data_ptr() if sp.n_entries else None,

@@ -105,8 +105,10 @@ def test_pack_matches_host_layout_and_roundtrips(pkg, dtype, layout):
 def test_reference_skeleton_spmm(pkg, name, dtype, layout):
     f = load_fixture(name)
     n = int(f["n"])
-    H = pkg.HalfTiles.from_coo(n, f["i"], f["j"], f["v"], dtype=dtype, layout=layout)
-    # ragged orbital blocks: most 64-tiles fall below the dense break-even → sparse tiles
+    from paper_2110_10765_b200.halftiles import dense_break_even
+    H = pkg.HalfTiles.from_coo(n, f["i"], f["j"], f["v"], dtype=dtype, layout=layout,
+                               dense_fill=dense_break_even(dtype))
+    # ragged orbital blocks: most 64-tiles fall below the memory break-even → sparse tiles
     if name == "skel_n1024.npz":
         assert H.n_sparse_tiles > H.n_tiles
     # structure: the stored half-tile set reproduces the reference pair set exactly
@@ -300,7 +302,7 @@ def test_save_load_roundtrip(pkg, c1_small, tmp_path):
     assert torch.equal(H.vals, H2.vals) and np.array_equal(H.tile_rc_host, H2.tile_rc_host)
     # mixed dense + sparse storage round-trips too
     f = load_fixture("skel_n1024.npz")
-    M = pkg.HalfTiles.from_coo(int(f["n"]), f["i"], f["j"], f["v"])
+    M = pkg.HalfTiles.from_coo(int(f["n"]), f["i"], f["j"], f["v"], dense_fill=0.5)
     M.save(tmp_path / "m.npz")
     M2 = pkg.HalfTiles.load(tmp_path / "m.npz")
     a, b = M.export_dense(), M2.export_dense()
@@ -499,7 +501,8 @@ def test_sparse_tiles_vs_oracle(pkg, dtype, fill, k):
     npd = np.float32 if dtype == torch.float32 else np.float64
     V = V.astype(npd)
     X = torch.randn((n, k), generator=torch.Generator().manual_seed(k), dtype=dtype)
-    H_mix = pkg.HalfTiles.from_coo(n, I, J, V, dtype=dtype)
+    from paper_2110_10765_b200.halftiles import dense_break_even
+    H_mix = pkg.HalfTiles.from_coo(n, I, J, V, dtype=dtype, dense_fill=dense_break_even(dtype))
     H_sp = pkg.HalfTiles.from_coo(n, I, J, V, dtype=dtype, dense_fill=2.0)
     H_dn = pkg.HalfTiles.from_coo(n, I, J, V, dtype=dtype, dense_fill=0.0)
     assert H_sp.n_tiles == 0 and H_dn.n_sparse_tiles == 0
@@ -517,3 +520,27 @@ def test_sparse_tiles_vs_oracle(pkg, dtype, fill, k):
     if k in (4, 8):
         Yb = pkg.sym_spmm_host_batch(H_mix, [X.pin_memory()])[0]
         assert (Yb.cuda() - Y1).abs().max().item() <= 1e-5 * Y1.abs().max().item() + 1e-6
+
+
+@pytest.mark.parametrize("fill", [0.05, 0.17, 0.6])
+def test_synthetic_sparse_device_construction(pkg, fill):
+    """Device count → scan → fill (cim_sparse_count_rows / _fill_entries):
+    the entry set and values equal the host twin bit for bit, and the
+    operator matches the oracle."""
+    n = 3000 - 17
+    rc = pkg.synthetic_pattern((n + 63) // 64, 0.2, seed=5)
+    H = pkg.HalfTiles.synthetic_sparse(n, tile_rc=rc, fill=fill, fill_seed=9, value_seed=3)
+    assert H.n_tiles == 0 and H.n_sparse_tiles == rc.shape[0]
+    want = oracle.synthetic_sparse_tiles(n, rc, fill, 9, 3)
+    got_rc, got = H.export_dense()
+    assert np.array_equal(got_rc, rc)
+    assert np.array_equal(f32bits(got), f32bits(want))
+    assert H.sparse.n_real_entries == int(np.count_nonzero(want))  # h(i^j) is never exactly 0 here
+    # the device-built column index equals the host construction from the same entries
+    from paper_2110_10765_b200.halftiles import SparseTiles
+    tid, r, c, v, _ = H.sparse.to_entries()
+    ref = SparseTiles.from_entries(H.sparse.tile_rc_host, tid, r, c, v, torch.float32, "cuda")
+    for name in ("rowptr", "colptr", "col", "row", "cperm"):
+        assert torch.equal(getattr(H.sparse, name), getattr(ref, name)), name
+    X = torch.randn((n, 8), generator=torch.Generator().manual_seed(1))
+    check_result(n, rc, want.astype(np.float64), X.numpy(), pkg.sym_spmm(H, X.cuda()).cpu().numpy(), torch.float32)
