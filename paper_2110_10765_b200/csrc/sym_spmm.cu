@@ -686,6 +686,87 @@ __global__ void __launch_bounds__(sub_ctas<T, KV, NG>() * (NG * kGroupThreads + 
 // registers, so a tile costs 8 LDS.128 of T + 8 of X_C per thread instead of
 // 32, and the producer copies X_R only with a unit's first tile.
 // ---------------------------------------------------------------------------
+// Element traits of the wide-register kernel: every accumulator / operand
+// register slot is 8 bytes — a pair of f32 vectors (FFMA2 / FADD2 on register
+// pairs) or one f64 vector (DFMA).  A warpgroup covers 4 slots = 8 f32 or
+// 4 f64 vectors, so the thread map, the X_R chunk swap and the butterflies are
+// the same code for both dtypes.
+template <typename T>
+struct WideE;
+template <>
+struct WideE<float> {
+  using E = u64;
+  static constexpr int VPG = 8;  // vectors per warpgroup
+  static __device__ __forceinline__ E zero() { return 0ull; }
+  static __device__ __forceinline__ E fma(float t, E x, E acc) { return fma2(t, x, acc); }
+  static __device__ __forceinline__ E add(E a, E b) { return add2(a, b); }
+  static __device__ __forceinline__ E shfl_xor(E v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+  static __device__ __forceinline__ E from_bits(u64 b) { return b; }
+  static __device__ __forceinline__ void trow(float (&t)[4], const float *Ts, int i, int gt) {
+    const float4 v = reinterpret_cast<const float4 *>(Ts)[i * 128 + gt];
+    t[0] = v.x, t[1] = v.y, t[2] = v.z, t[3] = v.w;
+  }
+  // slots a, b (4 consecutive vectors) → Y
+  static __device__ __forceinline__ void flush(float *y, E a, E b, uint64_t pol) {
+    float s0, s1, s2, s3;
+    unpack2(a, s0, s1);
+    unpack2(b, s2, s3);
+    red_add_v4(y, s0, s1, s2, s3, pol);
+  }
+};
+template <>
+struct WideE<double> {
+  using E = double;
+  static constexpr int VPG = 4;
+  static __device__ __forceinline__ E zero() { return 0.0; }
+  static __device__ __forceinline__ E fma(double t, E x, E acc) { return ::fma(t, x, acc); }
+  static __device__ __forceinline__ E add(E a, E b) { return a + b; }
+  static __device__ __forceinline__ E shfl_xor(E v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+  static __device__ __forceinline__ E from_bits(u64 b) { return __longlong_as_double((long long)b); }
+  static __device__ __forceinline__ void trow(double (&t)[4], const double *Ts, int i, int gt) {
+    const double2 a = reinterpret_cast<const double2 *>(Ts)[(2 * i + 0) * 128 + gt];
+    const double2 b = reinterpret_cast<const double2 *>(Ts)[(2 * i + 1) * 128 + gt];
+    t[0] = a.x, t[1] = a.y, t[2] = b.x, t[3] = b.y;
+  }
+  static __device__ __forceinline__ void flush(double *y, E a, E b, uint64_t) {
+    red_add(y, a);
+    red_add(y + 1, b);
+  }
+};
+
+// The column butterfly of reduce_cols_shfl for any element type.
+template <typename T>
+__device__ __forceinline__ void reduce_cols_wide(const typename WideE<T>::E (&ac)[4][4], int lane, int cg, T *yblk,
+                                                 long long ldy, uint64_t ypol) {
+  using W = WideE<T>;
+  using E = typename W::E;
+  E a[4][2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) a[j][q] = W::add(ac[j][q], W::shfl_xor(ac[j][q + 2], 16));
+  const bool b3 = lane & 8;
+  E b[2][2];
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const E send = b3 ? a[m][q] : a[m + 2][q];
+      const E keep = b3 ? a[m + 2][q] : a[m][q];
+      b[m][q] = W::add(keep, W::shfl_xor(send, 8));
+    }
+  const bool b2 = lane & 4;
+  E c[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const E send = b2 ? b[0][q] : b[1][q];
+    const E keep = b2 ? b[1][q] : b[0][q];
+    c[q] = W::add(keep, W::shfl_xor(send, 4));
+  }
+  const int j = (lane >> 2) & 3, h = lane >> 4;
+  W::flush(yblk + (long long)(cg + 16 * j) * ldy + (W::VPG / 2) * h, c[0], c[1], ypol);
+}
+
 constexpr int kK8Threads = 384;
 constexpr int kK8ConsumerRegs = 232;
 constexpr int kK8ProducerRegs = 40;
@@ -693,10 +774,15 @@ constexpr int kK8ProducerRegs = 40;
 // G = 8-vector groups sharing one ring (k = 8·G): G = 1 → two independent
 // sub-rings (WG0, WG1); G = 2 → one ring whose every tile feeds both consumer
 // warpgroups (vectors 0-7 and 8-15), the tile streamed from HBM once.
-template <int G>
+// KROW: the X / Y row length (k); k > 8·G runs as passes of 8·G vectors
+// (v_base), each streaming the tiles once more.
+template <typename T, int G, int KROW>
 __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmParams p) {
+  using W = WideE<T>;
+  using E = typename W::E;
+  constexpr int VPG = W::VPG;
   extern __shared__ __align__(128) unsigned char smem_all[];
-  constexpr int K = 8 * G;
+  constexpr int K = KROW;
   constexpr int SUBS = 2 / G;
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform
   const int lane = threadIdx.x & 31;
@@ -781,7 +867,7 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
   // ======================= consumer warpgroups =======================
   setmaxnreg_inc<kK8ConsumerRegs>();
   const int sub = wg / G;
-  const int v0 = 8 * (wg % G);  // this warpgroup's vectors v0 .. v0+7
+  const int v0 = p.v_base + VPG * (wg % G);  // this warpgroup's vectors v0 .. v0+VPG-1
   unsigned char *smem = smem_all + (size_t)sub * p.sub_bytes;
   unsigned char *stage_base = smem;
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)S * p.stage_bytes);
@@ -789,7 +875,7 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
   const int gt = threadIdx.x & 127;  // micro-block id
   const int rg = frag_rg(gt), cg = frag_cg(gt);
   const int sw = xr_chunk_swap<8>(rg);
-  float *Y = reinterpret_cast<float *>(p.Y);
+  T *Y = reinterpret_cast<T *>(p.Y);
   const long long ldy = p.ldy;
 #ifdef CIM_K8_Y_LAST
   const uint64_t ypol = policy_evict_last();
@@ -797,11 +883,11 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
   const uint64_t ypol = policy_evict_normal();
 #endif
 
-  u64 ar[8][4], ac[4][4], xr[8][4];
+  E ar[8][4], ac[4][4], xr[8][4];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) ar[i][q] = 0ull, xr[i][q] = 0ull;
+    for (int q = 0; q < 4; ++q) ar[i][q] = W::zero(), xr[i][q] = W::zero();
 
   int stage = 0;
   uint32_t phase = 0;
@@ -810,41 +896,50 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
     const unsigned char *st = stage_base + (size_t)stage * p.stage_bytes;
     const StageHdr h = *reinterpret_cast<const StageHdr *>(st + tile_bytes + 2 * xblk);
     if (h.flags & HDR_TERM) break;
-    const float *Ts = reinterpret_cast<const float *>(st);
-    const float *XC = reinterpret_cast<const float *>(st + tile_bytes);
+    const T *Ts = reinterpret_cast<const T *>(st);
+    const T *XC = reinterpret_cast<const T *>(st + tile_bytes);
     const bool diag = h.flags & HDR_DIAG;
     if (h.flags & HDR_FIRST) {
-      const float *XR = diag ? XC : reinterpret_cast<const float *>(st + tile_bytes + xblk);
+      const T *XR = diag ? XC : reinterpret_cast<const T *>(st + tile_bytes + xblk);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float *row = XR + (rg + 8 * i) * K + v0;
-        const ulonglong2 a = *reinterpret_cast<const ulonglong2 *>(row + 4 * sw);
-        const ulonglong2 b = *reinterpret_cast<const ulonglong2 *>(row + 4 * (sw ^ 1));
-        xr[i][0] = a.x;
-        xr[i][1] = a.y;
-        xr[i][2] = b.x;
-        xr[i][3] = b.y;
+        // a row slice = 4 slots = two 16-byte chunks, read in swapped order for rg ≥ 4
+        const unsigned char *row = reinterpret_cast<const unsigned char *>(XR + (rg + 8 * i) * K + v0);
+        const ulonglong2 a = *reinterpret_cast<const ulonglong2 *>(row + 16 * sw);
+        const ulonglong2 b = *reinterpret_cast<const ulonglong2 *>(row + 16 * (sw ^ 1));
+        xr[i][0] = W::from_bits(a.x);
+        xr[i][1] = W::from_bits(a.y);
+        xr[i][2] = W::from_bits(b.x);
+        xr[i][3] = W::from_bits(b.y);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) ar[i][q] = 0ull;
+        for (int q = 0; q < 4; ++q) ar[i][q] = W::zero();
       }
     }
-    u64 xc[4][4];
+    E xc[4][4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) load_pairs<4>(xc[j], XC + (cg + 16 * j) * K + v0);
+    for (int j = 0; j < 4; ++j) {
+      const unsigned char *row = reinterpret_cast<const unsigned char *>(XC + (cg + 16 * j) * K + v0);
+      const ulonglong2 a = *reinterpret_cast<const ulonglong2 *>(row);
+      const ulonglong2 b = *reinterpret_cast<const ulonglong2 *>(row + 16);
+      xc[j][0] = W::from_bits(a.x);
+      xc[j][1] = W::from_bits(a.y);
+      xc[j][2] = W::from_bits(b.x);
+      xc[j][3] = W::from_bits(b.y);
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) ac[j][q] = 0ull;
+      for (int q = 0; q < 4; ++q) ac[j][q] = W::zero();
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const float4 t4 = reinterpret_cast<const float4 *>(Ts)[i * 128 + gt];
-      const float t[4] = {t4.x, t4.y, t4.z, t4.w};
+      T t[4];
+      W::trow(t, Ts, i, gt);
 #pragma unroll
       for (int j = 0; j < 4; ++j)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          ar[i][q] = fma2(t[j], xc[j][q], ar[i][q]);
-          ac[j][q] = fma2(t[j], xr[i][q], ac[j][q]);
+          ar[i][q] = W::fma(t[j], xc[j][q], ar[i][q]);
+          ac[j][q] = W::fma(t[j], xr[i][q], ac[j][q]);
         }
     }
     __syncwarp();
@@ -854,39 +949,34 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
       phase ^= 1u;
     }
     // a diagonal tile's transposed FMAs (against X_R = X_C) are discarded
-    if (!diag) reduce_cols_shfl(ac, lane, cg, Y + (long long)h.C * kBlock * ldy + v0, ldy, ypol);
+    if (!diag) reduce_cols_wide<T>(ac, lane, cg, Y + (long long)h.C * kBlock * ldy + v0, ldy, ypol);
     if (h.flags & HDR_LAST) {
       // rows rg + 8i over the 4 lanes sharing them: 2 butterfly steps, then
-      // each lane flushes 2 rows × 8 vectors (no cross-warp barrier)
+      // each lane flushes 2 rows × VPG vectors (no cross-warp barrier)
       const bool b0 = lane & 1, b1 = lane & 2;
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const u64 send = b0 ? ar[i][q] : ar[i + 4][q];
-          const u64 keep = b0 ? ar[i + 4][q] : ar[i][q];
-          ar[i][q] = add2(keep, shfl_xor_u64(send, 1));
+          const E send = b0 ? ar[i][q] : ar[i + 4][q];
+          const E keep = b0 ? ar[i + 4][q] : ar[i][q];
+          ar[i][q] = W::add(keep, W::shfl_xor(send, 1));
         }
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const u64 send = b1 ? ar[i][q] : ar[i + 2][q];
-          const u64 keep = b1 ? ar[i + 2][q] : ar[i][q];
-          ar[i][q] = add2(keep, shfl_xor_u64(send, 2));
+          const E send = b1 ? ar[i][q] : ar[i + 2][q];
+          const E keep = b1 ? ar[i + 2][q] : ar[i][q];
+          ar[i][q] = W::add(keep, W::shfl_xor(send, 2));
         }
       const int i0 = (b0 ? 4 : 0) + (b1 ? 2 : 0);
-      float *yblk = Y + (long long)h.R * kBlock * ldy + v0;
+      T *yblk = Y + (long long)h.R * kBlock * ldy + v0;
 #pragma unroll
       for (int ri = 0; ri < 2; ++ri) {
-        float *yr = yblk + (long long)(rg + 8 * (i0 + ri)) * ldy;
-        float a0, a1, a2, a3, a4, a5, a6, a7;
-        unpack2(ar[ri][0], a0, a1);
-        unpack2(ar[ri][1], a2, a3);
-        unpack2(ar[ri][2], a4, a5);
-        unpack2(ar[ri][3], a6, a7);
-        red_add_v4(yr, a0, a1, a2, a3, ypol);
-        red_add_v4(yr + 4, a4, a5, a6, a7, ypol);
+        T *yr = yblk + (long long)(rg + 8 * (i0 + ri)) * ldy;
+        W::flush(yr, ar[ri][0], ar[ri][1], ypol);
+        W::flush(yr + VPG / 2, ar[ri][2], ar[ri][3], ypol);
       }
     }
   }
@@ -1052,48 +1142,52 @@ int launch_kernel(const cim_half_tiles *H, const void *X, void *Y, int k, long l
   return CIM_OK;
 }
 
-template <int G>
+template <typename T, int G, int KROW>
 int launch_k8(const cim_half_tiles *H, const void *X, void *Y, long long ldy, cudaStream_t stream, DeviceState *ds) {
   static std::once_flag attr_once[64];
   constexpr int SUBS = 2 / G;
-  const unsigned int tile_bytes = kTileElems * sizeof(float);
-  const unsigned int xblk = kBlock * 8 * G * sizeof(float);
+  constexpr int passes = KROW / (WideE<T>::VPG * G);
+  const unsigned int tile_bytes = kTileElems * sizeof(T);
+  const unsigned int xblk = kBlock * KROW * sizeof(T);
   const unsigned int stage_bytes = (tile_bytes + 2 * xblk + sizeof(StageHdr) + 127u) & ~127u;
   const size_t budget = (size_t)(227 * 1024) / SUBS;
   int S = std::min((int)((budget - 128) / stage_bytes), 8);
+  if (S < 2) return set_error(CIM_EUNSUPPORTED, "k too large for the k8 kernel's stages");
   const size_t sub_bytes = ((size_t)S * stage_bytes + 128 + 127) & ~(size_t)127;
   const size_t smem = SUBS * sub_bytes;
   int dev = 0;
   cudaGetDevice(&dev);
   cudaError_t e = cudaSuccess;
   std::call_once(attr_once[dev & 63], [&] {
-    e = cudaFuncSetAttribute(sym_spmm_k8_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(sym_spmm_k8_kernel<T, G, KROW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   });
   if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("cudaFuncSetAttribute(k8): ") + cudaGetErrorString(e));
   long long grid = std::min<long long>(ds->sms, (H->n_units + SUBS - 1) / SUBS);
   if (grid < 1) return CIM_OK;
-  unsigned int *ctr = take_counters(ds, 1);
-  e = cudaMemsetAsync(ctr, 0, sizeof(unsigned int), stream);
+  unsigned int *ctr = take_counters(ds, passes);
+  e = cudaMemsetAsync(ctr, 0, passes * sizeof(unsigned int), stream);
   if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("cudaMemsetAsync counter: ") + cudaGetErrorString(e));
-  SpmmParams p;
-  p.units = reinterpret_cast<const int4 *>(H->units);
-  p.tile_rc = reinterpret_cast<const int2 *>(H->tile_rc);
-  p.vals = reinterpret_cast<const unsigned char *>(H->vals);
-  p.X = reinterpret_cast<const unsigned char *>(X);
-  p.Y = reinterpret_cast<unsigned char *>(Y);
-  p.counter = ctr;
-  p.n_units = H->n_units;
-  p.ldy = ldy;
-  p.k = 8 * G;
-  p.v_base = 0;
-  p.stages = S;
-  p.stage_bytes = stage_bytes;
-  p.tile_bytes = tile_bytes;
-  p.xblk_bytes = xblk;
-  p.sub_bytes = (unsigned int)sub_bytes;
-  sym_spmm_k8_kernel<G><<<(unsigned int)grid, kK8Threads, smem, stream>>>(p);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("sym_spmm_k8 launch: ") + cudaGetErrorString(e));
+  for (int ps = 0; ps < passes; ++ps) {
+    SpmmParams p;
+    p.units = reinterpret_cast<const int4 *>(H->units);
+    p.tile_rc = reinterpret_cast<const int2 *>(H->tile_rc);
+    p.vals = reinterpret_cast<const unsigned char *>(H->vals);
+    p.X = reinterpret_cast<const unsigned char *>(X);
+    p.Y = reinterpret_cast<unsigned char *>(Y);
+    p.counter = ctr + ps;
+    p.n_units = H->n_units;
+    p.ldy = ldy;
+    p.k = KROW;
+    p.v_base = ps * WideE<T>::VPG * G;
+    p.stages = S;
+    p.stage_bytes = stage_bytes;
+    p.tile_bytes = tile_bytes;
+    p.xblk_bytes = xblk;
+    p.sub_bytes = (unsigned int)sub_bytes;
+    sym_spmm_k8_kernel<T, G, KROW><<<(unsigned int)grid, kK8Threads, smem, stream>>>(p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("sym_spmm_k8 launch: ") + cudaGetErrorString(e));
+  }
   return CIM_OK;
 }
 
@@ -1184,13 +1278,17 @@ static int sym_spmm_dense(const cim_half_tiles *H, const void *X, void *Y, int32
         return launch_kernel<float, 2, 4>(H, X, Y, k, ldy, cfg.passes, stream, ds);
       case 81:
 #ifndef CIM_NO_K8
-        if (k == 8) return launch_k8<1>(H, X, Y, ldy, stream, ds);
+        if (k == 8) return launch_k8<float, 1, 8>(H, X, Y, ldy, stream, ds);
+        if (k == 24) return launch_k8<float, 1, 24>(H, X, Y, ldy, stream, ds);
 #endif
         if (k == 8) return launch_kernel<float, 8, 1, 8>(H, X, Y, k, ldy, cfg.passes, stream, ds);
         return launch_kernel<float, 8, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
       case 82:
 #ifndef CIM_NO_K8
-        if (k == 16) return launch_k8<2>(H, X, Y, ldy, stream, ds);
+        if (k == 16) return launch_k8<float, 2, 16>(H, X, Y, ldy, stream, ds);
+        if (k == 32) return launch_k8<float, 2, 32>(H, X, Y, ldy, stream, ds);
+        if (k == 48) return launch_k8<float, 2, 48>(H, X, Y, ldy, stream, ds);
+        if (k == 64) return launch_k8<float, 2, 64>(H, X, Y, ldy, stream, ds);
 #endif
         if (k == 16) return launch_kernel<float, 8, 2, 16>(H, X, Y, k, ldy, cfg.passes, stream, ds);
         return launch_kernel<float, 8, 2>(H, X, Y, k, ldy, cfg.passes, stream, ds);
@@ -1204,9 +1302,18 @@ static int sym_spmm_dense(const cim_half_tiles *H, const void *X, void *Y, int32
         if (k == 2) return launch_kernel<double, 2, 1, 2>(H, X, Y, k, ldy, cfg.passes, stream, ds);
         return launch_kernel<double, 2, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
       case 41:
+#ifndef CIM_NO_K8
+        if (k == 4) return launch_k8<double, 1, 4>(H, X, Y, ldy, stream, ds);
+        if (k == 12) return launch_k8<double, 1, 12>(H, X, Y, ldy, stream, ds);
+#endif
         if (k == 4) return launch_kernel<double, 4, 1, 4>(H, X, Y, k, ldy, cfg.passes, stream, ds);
         return launch_kernel<double, 4, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
       case 42:
+#ifndef CIM_NO_K8
+        if (k == 8) return launch_k8<double, 2, 8>(H, X, Y, ldy, stream, ds);
+        if (k == 16) return launch_k8<double, 2, 16>(H, X, Y, ldy, stream, ds);
+        if (k == 32) return launch_k8<double, 2, 32>(H, X, Y, ldy, stream, ds);
+#endif
         if (k == 8) return launch_kernel<double, 4, 2, 8>(H, X, Y, k, ldy, cfg.passes, stream, ds);
         return launch_kernel<double, 4, 2>(H, X, Y, k, ldy, cfg.passes, stream, ds);
     }
