@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget for the cpu_baseline leg")
     ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--bands", type=int, default=1, help="column bands of the tile order (0 = auto)")
+    ap.add_argument("--csv", default=None,
+                    help="also write the reference harness's 8-column CSV (cimotifs bench.py:54) to this path")
     ap.add_argument("--fill", type=float, default=None,
                     help="store every tile sparse (COO-in-tile) with this entry fill (1 GPU); default: dense tiles")
     return ap.parse_args()
@@ -430,10 +432,38 @@ def impl_ours(args):
             "clocks": clocks.summary(),
         }
         print(json.dumps(line))
+        if args.csv:
+            write_reference_csv(args.csv, line, variant=("sparse" if args.fill is not None else H.layout) + f"-{world}gpu")
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+CSV_COLUMNS = ("motif", "variant", "n", "m", "particles", "reps", "seconds", "rate")  # cimotifs bench.py:54
+
+
+def write_reference_csv(path, line: dict, variant: str) -> None:
+    """The reference harness's flat CSV (``motif,variant,n,m,particles,reps,
+    seconds,rate`` plus ``#`` metadata lines, cimotifs bench.py:1-24, :335-349)
+    so its plotting frontend can chart the SpMM next to the CPU motifs:
+    motif = spmm, m = k, rate = GFLOP/s, seconds = per apply; the roofline,
+    clocks and e2e figures travel as ``# key=value`` lines."""
+    import hashlib
+
+    cfg = line["config"]
+    meta = {"metric": line["metric"], "unit": line["unit"], "dtype": line["dtype"], "n_gpus": line["n_gpus"],
+            "workload": cfg["workload"], "roofline_frac": line["roofline"]["frac"],
+            "roofline_achieved_gbs": line["roofline"]["achieved"], "e2e_gflops": line["e2e"]["value"],
+            "sm_mhz": line["clocks"].get("sm_mhz"), "throttle": "+".join(line["clocks"].get("reasons", [])) or "none"}
+    row = ["spmm", variant, str(cfg["n"]), str(cfg["k"]), "", str(line["steps"]),
+           repr(line["ms_per_step"] / 1e3), repr(line["value"])]
+    h = hashlib.sha256()
+    h.update(f"spmm,{variant},{cfg['n']},{cfg['k']},None".encode())
+    h.update(b"|")
+    lines = [f"# {k}={v}" for k, v in meta.items()] + [",".join(CSV_COLUMNS), ",".join(row),
+                                                        f"# results-digest={h.hexdigest()[:16]}"]
+    Path(path).write_text("\n".join(lines) + "\n")
 
 
 def main():

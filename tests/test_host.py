@@ -144,3 +144,26 @@ def test_fragment_map_matches_header_formula():
 def test_halftiles_requires_cuda_device():
     with pytest.raises(ValueError):
         pkg.HalfTiles.synthetic(128, p=0.5, device="cpu")
+
+
+def test_bench_writes_reference_csv(tmp_path):
+    """bench.py --csv: the reference harness's 8-column CSV (cimotifs
+    bench.py:54, emit_csv :335-349) — header, one spmm row, '#' metadata."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("bench", ROOT / "bench.py")
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    line = {"metric": "m", "unit": "GFLOP/s", "dtype": "f32", "n_gpus": 1, "steps": 7, "ms_per_step": 1.5,
+            "value": 39000.0, "config": {"workload": "C2", "n": 4194304, "k": 8},
+            "roofline": {"frac": 0.77, "achieved": 5000.0}, "e2e": {"value": 19000.0},
+            "clocks": {"sm_mhz": 1965.0, "reasons": []}}
+    out = tmp_path / "b.csv"
+    bench.write_reference_csv(out, line, "frag-1gpu")
+    rows = [r for r in out.read_text().splitlines() if r and not r.startswith("#")]
+    assert tuple(rows[0].split(",")) == bench.CSV_COLUMNS == (
+        "motif", "variant", "n", "m", "particles", "reps", "seconds", "rate")
+    cells = rows[1].split(",")
+    assert len(cells) == 8 and cells[0] == "spmm" and cells[2] == "4194304" and cells[3] == "8"
+    assert float(cells[6]) == 1.5e-3 and float(cells[7]) == 39000.0 and cells[4] == ""
+    assert any(r.startswith("# results-digest=") for r in out.read_text().splitlines())
