@@ -68,6 +68,11 @@ extern "C" {
 
 /* cim_sym_spmm flags */
 #define CIM_ACCUMULATE    1u  /* Y += A·X instead of Y = A·X                */
+#define CIM_DETERMINISTIC 2u  /* no float atomics: every Y row block summed
+                                 in a fixed order by one CTA (bitwise
+                                 reproducible; needs the det_* tile lists,
+                                 dense fragment-layout tiles only; reads each
+                                 tile twice — a validation mode)           */
 
 /* value kinds for cim_fill_synthetic_values */
 #define CIM_VALUES_H_XOR      0  /* h(i XOR j; seed)      pipeline.py:216-222 */
@@ -127,6 +132,13 @@ typedef struct cim_half_tiles {
   const cim_sparse_tiles *sparse; /* NULL, or the sparse tiles of the same
                                      matrix (a tile is stored dense or sparse,
                                      never both); device arrays              */
+  /* CIM_DETERMINISTIC only (else NULL): per block row b, the tiles with
+     R == b (det_row_tiles[det_row_ptr[b] .. det_row_ptr[b+1]]) and the
+     tiles with C == b, R < b (det_col_*), each list in (R, C) order.     */
+  const int64_t *det_row_ptr;   /* [nb+1] */
+  const int32_t *det_row_tiles;
+  const int64_t *det_col_ptr;   /* [nb+1] */
+  const int32_t *det_col_tiles;
 } cim_half_tiles;
 
 /* Library version / build string (host). */

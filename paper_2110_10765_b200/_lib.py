@@ -16,6 +16,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libcim_b200.so"
 CIM_OK, CIM_EINVAL, CIM_ECUDA, CIM_EUNSUPPORTED = 0, 1, 2, 3
 CIM_F32, CIM_F64 = 0, 1
 CIM_ACCUMULATE = 1
+CIM_DETERMINISTIC = 2
 CIM_VALUES_H_XOR, CIM_VALUES_OP_HASH, CIM_VALUES_IDENTITY = 0, 1, 2
 CIM_LAYOUT_FRAG, CIM_LAYOUT_TC = 0, 1
 BLOCK = 64
@@ -80,6 +81,10 @@ class CimHalfTiles(ctypes.Structure):
         ("layout", ctypes.c_int32),
         ("reserved", ctypes.c_int32),
         ("sparse", ctypes.POINTER(CimSparseTiles)),
+        ("det_row_ptr", ctypes.c_void_p),
+        ("det_row_tiles", ctypes.c_void_p),
+        ("det_col_ptr", ctypes.c_void_p),
+        ("det_col_tiles", ctypes.c_void_p),
     ]
 
 

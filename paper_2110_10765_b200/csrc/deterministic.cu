@@ -1,0 +1,111 @@
+// CIM_DETERMINISTIC: the same operator without float atomics (SURVEY.md §7
+// "Nondeterminism"; §8(b) flags).  The fast kernels reduce Y_C with
+// red.global, so the summation order of a column block depends on timing and
+// Y is reproducible only to rounding; this validation mode is bitwise
+// reproducible.  One CTA owns block row b of Y and sums, in (R, C) order,
+//   direct      T·X_C   over the tiles of block row b,
+//   transposed  Tᵀ·X_R  over the tiles of block column b with R < b,
+// with thread (row r, vector group g) accumulating in registers in a fixed
+// order and writing Y once.  Every off-diagonal tile is read twice (once per
+// side) — a correctness mode, not the hot path.
+#include <cstdint>
+#include <string>
+
+#include "cim_b200.h"
+#include "common.cuh"
+#include "host_util.h"
+
+namespace cim {
+namespace {
+
+constexpr int kDetThreads = 256;  // 64 rows × 4 vector groups
+constexpr int kDetMaxK = 64;
+
+// Storage index of tile element (r, c) in fragment layout v1 (include/cim_b200.h).
+template <typename T>
+__device__ __forceinline__ int frag_index(int r, int c) {
+  const int rg = r & 7, i = r >> 3, cg = c & 15, j = c >> 4;
+  const int mb = 32 * (cg >> 2) + 4 * rg + (cg & 3);
+  if constexpr (sizeof(T) == 4)
+    return (i * 128 + mb) * 4 + j;
+  else
+    return ((2 * i + (j >> 1)) * 128 + mb) * 2 + (j & 1);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kDetThreads) det_spmm_kernel(const int2 *tile_rc, const T *vals,
+                                                               const long long *row_ptr, const int *row_tiles,
+                                                               const long long *col_ptr, const int *col_tiles,
+                                                               const T *X, T *Y, int k, long long ldy,
+                                                               bool accumulate) {
+  const int b = blockIdx.x;
+  const int r = threadIdx.x & 63, g = threadIdx.x >> 6;
+  constexpr int VMAX = kDetMaxK / 4;
+  T acc[VMAX];
+#pragma unroll
+  for (int q = 0; q < VMAX; ++q) acc[q] = T(0);
+  // direct: Y_b[r] += Σ_c T[r][c] X_C[c]
+  for (long long s = row_ptr[b]; s < row_ptr[b + 1]; ++s) {
+    const int t = row_tiles[s];
+    const int C = tile_rc[t].y;
+    const T *tv = vals + (size_t)t * kTileElems;
+    const T *xc = X + (long long)C * 64 * k;
+    for (int c = 0; c < 64; ++c) {
+      const T a = tv[frag_index<T>(r, c)];
+#pragma unroll
+      for (int q = 0; q < VMAX; ++q) {
+        const int v = g + 4 * q;
+        if (v < k) acc[q] = fma(a, xc[(long long)c * k + v], acc[q]);
+      }
+    }
+  }
+  // transposed: Y_b[r] += Σ_r' T[r'][r] X_R[r'] over tiles (R, b), R < b
+  for (long long s = col_ptr[b]; s < col_ptr[b + 1]; ++s) {
+    const int t = col_tiles[s];
+    const int R = tile_rc[t].x;
+    const T *tv = vals + (size_t)t * kTileElems;
+    const T *xr = X + (long long)R * 64 * k;
+    for (int rr = 0; rr < 64; ++rr) {
+      const T a = tv[frag_index<T>(rr, r)];
+#pragma unroll
+      for (int q = 0; q < VMAX; ++q) {
+        const int v = g + 4 * q;
+        if (v < k) acc[q] = fma(a, xr[(long long)rr * k + v], acc[q]);
+      }
+    }
+  }
+  T *y = Y + ((long long)b * 64 + r) * ldy;
+#pragma unroll
+  for (int q = 0; q < VMAX; ++q) {
+    const int v = g + 4 * q;
+    if (v < k) y[v] = accumulate ? y[v] + acc[q] : acc[q];
+  }
+}
+
+}  // namespace
+
+int sym_spmm_deterministic(const cim_half_tiles *H, const void *X, void *Y, int k, long long ldy, bool accumulate,
+                           cudaStream_t stream) {
+  if (H->layout != CIM_LAYOUT_FRAG) return set_error(CIM_EUNSUPPORTED, "CIM_DETERMINISTIC needs fragment-layout tiles");
+  if (H->sparse && H->sparse->n_tiles > 0) return set_error(CIM_EUNSUPPORTED, "CIM_DETERMINISTIC: dense tiles only");
+  if (k > kDetMaxK) return set_error(CIM_EUNSUPPORTED, "CIM_DETERMINISTIC supports k <= 64");
+  if (!H->det_row_ptr || !H->det_row_tiles || !H->det_col_ptr || !H->det_col_tiles)
+    return set_error(CIM_EINVAL, "CIM_DETERMINISTIC needs the det_* tile lists");
+  const long long nb = (H->n + kBlock - 1) / kBlock;
+  const int2 *rc = reinterpret_cast<const int2 *>(H->tile_rc);
+  if (H->dtype == CIM_F32)
+    det_spmm_kernel<float><<<(unsigned)nb, kDetThreads, 0, stream>>>(
+        rc, static_cast<const float *>(H->vals), reinterpret_cast<const long long *>(H->det_row_ptr), H->det_row_tiles,
+        reinterpret_cast<const long long *>(H->det_col_ptr), H->det_col_tiles, static_cast<const float *>(X),
+        static_cast<float *>(Y), k, ldy, accumulate);
+  else
+    det_spmm_kernel<double><<<(unsigned)nb, kDetThreads, 0, stream>>>(
+        rc, static_cast<const double *>(H->vals), reinterpret_cast<const long long *>(H->det_row_ptr),
+        H->det_row_tiles, reinterpret_cast<const long long *>(H->det_col_ptr), H->det_col_tiles,
+        static_cast<const double *>(X), static_cast<double *>(Y), k, ldy, accumulate);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("det_spmm_kernel: ") + cudaGetErrorString(e));
+  return CIM_OK;
+}
+
+}  // namespace cim

@@ -1215,6 +1215,8 @@ extern "C" int cim_layout_supports(int32_t layout, int32_t dtype, int32_t k) {
 namespace cim {
 int sym_spmm_sparse(const cim_sparse_tiles *S, int dtype, const void *X, void *Y, int k, long long ldx,
                     long long ldy, cudaStream_t stream);
+int sym_spmm_deterministic(const cim_half_tiles *H, const void *X, void *Y, int k, long long ldy, bool accumulate,
+                           cudaStream_t stream);
 }
 
 // Dense tiles (and the Y zeroing); the sparse tiles follow in cim_sym_spmm.
@@ -1247,6 +1249,8 @@ static int sym_spmm_dense(const cim_half_tiles *H, const void *X, void *Y, int32
   if (rc) return rc;
   const int64_t nb = (H->n + kBlock - 1) / kBlock;
   const int64_t n_pad = nb * kBlock;
+  if (flags & CIM_DETERMINISTIC)  // writes every row block itself: no zeroing, no atomics
+    return sym_spmm_deterministic(H, X, Y, k, ldy, (flags & CIM_ACCUMULATE) != 0, stream);
   if (!(flags & CIM_ACCUMULATE)) {
     cudaError_t e = (ldy == k) ? cudaMemsetAsync(Y, 0, (size_t)n_pad * k * es, stream)
                                : cudaMemset2DAsync(Y, (size_t)ldy * es, 0, (size_t)k * es, (size_t)n_pad, stream);
@@ -1324,6 +1328,6 @@ static int sym_spmm_dense(const cim_half_tiles *H, const void *X, void *Y, int32
 extern "C" int cim_sym_spmm(const cim_half_tiles *H, const void *X, void *Y, int32_t k, int64_t ldx, int64_t ldy,
                             uint32_t flags, void *stream_) {
   const int rc = sym_spmm_dense(H, X, Y, k, ldx, ldy, flags, stream_);
-  if (rc != CIM_OK || !H->sparse || H->sparse->n_tiles == 0) return rc;
+  if (rc != CIM_OK || (flags & CIM_DETERMINISTIC) || !H->sparse || H->sparse->n_tiles == 0) return rc;
   return sym_spmm_sparse(H->sparse, H->dtype, X, Y, k, ldx, ldy, reinterpret_cast<cudaStream_t>(stream_));
 }

@@ -334,6 +334,7 @@ class HalfTiles:
     _desc: CimHalfTiles | None = field(default=None, repr=False)
     _ws: torch.Tensor | None = field(default=None, repr=False)
     sparse: SparseTiles | None = None
+    _det: tuple | None = field(default=None, repr=False)
 
     # ------------------------------------------------------------------ props
     @property
@@ -413,7 +414,27 @@ class HalfTiles:
                 reserved=0,
                 sparse=ctypes.pointer(self.sparse.descriptor()) if self.n_sparse_tiles else None,
             )
+            if self._det is not None:
+                d = self._desc
+                d.det_row_ptr, d.det_row_tiles, d.det_col_ptr, d.det_col_tiles = (t.data_ptr() for t in self._det)
         return self._desc
+
+    def enable_deterministic(self) -> None:
+        """Build the per-block-row tile lists CIM_DETERMINISTIC reads (device):
+        tiles with R == b and tiles with C == b, R < b, each in (R, C) order."""
+        if self._det is not None:
+            return
+        rc = self.tile_rc_host.astype(np.int64)
+        nb = self.nb
+        by_row = np.lexsort((rc[:, 1], rc[:, 0]))
+        row_ptr = np.searchsorted(rc[by_row, 0], np.arange(nb + 1), side="left").astype(np.int64)
+        off = np.flatnonzero(rc[:, 0] < rc[:, 1])
+        by_col = off[np.lexsort((rc[off, 1], rc[off, 0], rc[off, 1]))]
+        col_ptr = np.searchsorted(rc[by_col, 1], np.arange(nb + 1), side="left").astype(np.int64)
+        dev = self.device
+        mk = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt) if a.size else np.zeros(1, dt)).to(dev)  # noqa: E731
+        self._det = (mk(row_ptr, np.int64), mk(by_row, np.int32), mk(col_ptr, np.int64), mk(by_col, np.int32))
+        self._desc = None
 
     def _workspace(self, nbytes: int) -> torch.Tensor:
         """Cached device scratch (host-batch pipeline buffers), grown on demand."""

@@ -19,7 +19,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from ._lib import BLOCK, CIM_ACCUMULATE, check, lib
+from ._lib import BLOCK, CIM_ACCUMULATE, CIM_DETERMINISTIC, check, lib
 from .halftiles import HalfTiles
 
 LAYOUTS = ("auto", "nk", "kn")
@@ -48,11 +48,19 @@ def padded_k(dtype: torch.dtype, k: int, layout: str = "frag") -> int:
     return kk
 
 
-def _launch(H: HalfTiles, Xd: torch.Tensor, Yd: torch.Tensor, accumulate: bool, stream) -> None:
+def _launch(H: HalfTiles, Xd: torch.Tensor, Yd: torch.Tensor, accumulate: bool, stream,
+            deterministic: bool = False) -> None:
     """Raw C-ABI call on device tensors of shape (n_pad, k) (k compiled)."""
     k = Xd.shape[1]
     s = stream if stream is not None else torch.cuda.current_stream(H.device)
     handle = s.cuda_stream if isinstance(s, torch.cuda.Stream) else int(s)
+    if deterministic:
+        H.enable_deterministic()
+        with torch.cuda.device(H.device):
+            rc = lib().cim_sym_spmm(H.descriptor(), Xd.data_ptr(), Yd.data_ptr(), k, Xd.stride(0), Yd.stride(0),
+                                    (CIM_ACCUMULATE if accumulate else 0) | CIM_DETERMINISTIC, handle)
+        check(rc, "cim_sym_spmm(deterministic)")
+        return
     if H.layout == "tc" and k > TC_MAX_K:
         # column passes of 16 vectors: each pass streams the tiles once more
         with torch.cuda.stream(s) if isinstance(s, torch.cuda.Stream) else torch.cuda.device(H.device):
@@ -68,7 +76,8 @@ def _launch(H: HalfTiles, Xd: torch.Tensor, Yd: torch.Tensor, accumulate: bool, 
     check(rc, "cim_sym_spmm")
 
 
-def sym_spmm(H: HalfTiles, X, out=None, *, layout: str = "auto", accumulate: bool = False, stream=None):
+def sym_spmm(H: HalfTiles, X, out=None, *, layout: str = "auto", accumulate: bool = False, stream=None,
+             deterministic: bool = False):
     """Y = H·X + Hᵀ·X = A·X for the symmetric A stored as block-half tiles.
 
     Parameters
@@ -79,6 +88,8 @@ def sym_spmm(H: HalfTiles, X, out=None, *, layout: str = "auto", accumulate: boo
         adds to it instead of overwriting)
     layout : "auto" | "nk" | "kn"
     stream : torch.cuda.Stream or raw cudaStream_t handle (default: current)
+    deterministic : no float atomics — bitwise reproducible Y (CIM_DETERMINISTIC;
+        dense fragment-layout tiles; a validation mode, ~2× the traffic)
     """
     if not isinstance(H, HalfTiles):
         raise ValueError(f"H must be a HalfTiles, got {type(H).__name__}")
@@ -137,7 +148,7 @@ def sym_spmm(H: HalfTiles, X, out=None, *, layout: str = "auto", accumulate: boo
             Yd[:n, :k] = o if layout == "nk" else o.t()
         elif accumulate:
             raise ValueError("accumulate=True needs an `out` buffer to add into")
-    _launch(H, Xd, Yd, accumulate, stream)
+    _launch(H, Xd, Yd, accumulate, stream, deterministic)
     Y = Yd[:n, :k]
     if layout == "kn":
         Y = Y.t()

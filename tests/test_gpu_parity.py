@@ -544,3 +544,22 @@ def test_synthetic_sparse_device_construction(pkg, fill):
         assert torch.equal(getattr(H.sparse, name), getattr(ref, name)), name
     X = torch.randn((n, 8), generator=torch.Generator().manual_seed(1))
     check_result(n, rc, want.astype(np.float64), X.numpy(), pkg.sym_spmm(H, X.cuda()).cpu().numpy(), torch.float32)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("k", [1, 4, 8, 16])
+def test_deterministic_mode_bitwise_reproducible(pkg, c1_small, dtype, k):
+    """CIM_DETERMINISTIC: no float atomics — repeated applies are bitwise
+    identical (the atomic path is not, in general), and the result passes the
+    oracle gates; accumulate adds onto Y."""
+    n, rc, tiles = c1_small
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=dtype, max_unit=3)
+    X = torch.randn((n, k), generator=torch.Generator().manual_seed(k), dtype=dtype).cuda()
+    Y1 = pkg.sym_spmm(H, X, deterministic=True)
+    Y2 = pkg.sym_spmm(H, X, deterministic=True)
+    assert torch.equal(Y1, Y2)
+    tl = tiles if dtype == torch.float32 else tiles.astype(np.float64)
+    check_result(n, rc, tl, X.cpu().numpy(), Y1.cpu().numpy(), dtype)
+    out = torch.ones_like(X)
+    pkg.sym_spmm(H, X, out=out, accumulate=True, deterministic=True)
+    assert torch.equal(out, Y1 + 1.0)
