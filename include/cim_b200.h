@@ -249,6 +249,31 @@ CIM_API int cim_sparse_fill_entries(const cim_sparse_tiles *S, int64_t n, int32_
                                     void *stream);
 CIM_API int cim_sparse_build_columns(const cim_sparse_tiles *S, void *stream);
 
+/*
+ * Device construction from a many-body basis (the reference's two-pass
+ * skeleton build, pipeline.py:290-377 / sparsity.py:131-193, into 64-tiles).
+ * bits_lo: [n] packed occupancy of single-particle states 1..64; occ:
+ * [n][n_particles] sorted 1-based occupied indices (mbstate.py Basis
+ * arrays, grouped order).  Entry (i, j) is kept iff
+ * popcount(bits_lo[i] ^ bits_lo[j]) ≤ threshold and the lockstep
+ * occupation-list difference ≤ threshold (threshold = 2·rank); its value
+ * is h(i XOR j; seed).  cim_basis_count_tiles: rowcnt[t·64 + r] = kept
+ * entries of local row r of candidate tile t; the caller keeps the tiles with
+ * entries, scans, and fills them dense (cim_basis_fill_dense, `layout`
+ * order) or sparse (cim_basis_fill_sparse: rowptr / entry_off prefilled,
+ * writes col, row, vals; then cim_sparse_build_columns).
+ */
+CIM_API int cim_basis_count_tiles(const uint64_t *bits_lo, const uint16_t *occ, int64_t n,
+                                  int32_t n_particles, int32_t threshold, const int32_t *tile_rc,
+                                  int64_t n_tiles, int32_t *rowcnt, void *stream);
+CIM_API int cim_basis_fill_dense(const uint64_t *bits_lo, const uint16_t *occ, int64_t n,
+                                 int32_t n_particles, int32_t threshold, const int32_t *tile_rc,
+                                 int64_t n_tiles, int32_t dtype, int32_t layout, uint64_t seed,
+                                 void *vals, void *stream);
+CIM_API int cim_basis_fill_sparse(const uint64_t *bits_lo, const uint16_t *occ, int64_t n,
+                                  int32_t n_particles, int32_t threshold, const cim_sparse_tiles *S,
+                                  int32_t dtype, uint64_t seed, void *stream);
+
 /* Device workspace bytes cim_gram / cim_gram_blocked need. */
 CIM_API uint64_t cim_gram_workspace_bytes(int64_t rows, int32_t ca, int32_t cb);
 

@@ -41,6 +41,9 @@ EXPORTS = (
     "cim_sparse_count_rows",
     "cim_sparse_fill_entries",
     "cim_sparse_build_columns",
+    "cim_basis_count_tiles",
+    "cim_basis_fill_dense",
+    "cim_basis_fill_sparse",
     "cim_gram",
     "cim_gram_workspace_bytes",
     "cim_tsmm",
@@ -136,6 +139,12 @@ def lib() -> ctypes.CDLL:
     L.cim_sparse_fill_entries.argtypes = [c.POINTER(CimSparseTiles), c.c_int64, c.c_int32, c.c_double, c.c_uint64,
                                           c.c_int32, c.c_uint64, c.c_int32, c.c_void_p]
     L.cim_sparse_build_columns.argtypes = [c.POINTER(CimSparseTiles), c.c_void_p]
+    L.cim_basis_count_tiles.argtypes = [c.c_void_p, c.c_void_p, c.c_int64, c.c_int32, c.c_int32, c.c_void_p, c.c_int64,
+                                        c.c_void_p, c.c_void_p]
+    L.cim_basis_fill_dense.argtypes = [c.c_void_p, c.c_void_p, c.c_int64, c.c_int32, c.c_int32, c.c_void_p, c.c_int64,
+                                       c.c_int32, c.c_int32, c.c_uint64, c.c_void_p, c.c_void_p]
+    L.cim_basis_fill_sparse.argtypes = [c.c_void_p, c.c_void_p, c.c_int64, c.c_int32, c.c_int32,
+                                        c.POINTER(CimSparseTiles), c.c_int32, c.c_uint64, c.c_void_p]
     L.cim_gram.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_void_p, c.c_int64, c.c_int32, c.c_int64, c.c_int32,
                            c.c_void_p, c.c_void_p, c.c_uint64, c.c_void_p]
     L.cim_gram_workspace_bytes.argtypes = [c.c_int64, c.c_int32, c.c_int32]

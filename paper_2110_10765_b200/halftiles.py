@@ -653,6 +653,15 @@ class HalfTiles:
         return H
 
     @classmethod
+    def from_basis(cls, basis_or_occ, bits_lo=None, **kw) -> "HalfTiles":
+        """Build on the device from a many-body basis (grouped order) — the
+        reference's count → scan → fill skeleton build into 64-tiles; see
+        ``paper_2110_10765_b200.construct.from_basis``."""
+        from .construct import from_basis
+
+        return from_basis(basis_or_occ, bits_lo, **kw)
+
+    @classmethod
     def from_skeleton(cls, skeleton, orbitals, n: int | None = None, **kw) -> "HalfTiles":
         """From a reference ``SparseSkeleton`` (pipeline.py:96-116) and its
         orbitals: rows are recovered from the per-(tile,row) segments

@@ -21,6 +21,10 @@ It imports the reference package ``cimotifs`` from
                         CALIBRATION_BIAS, identity operator with ±n^-½ sign
                         vectors (contraction exactly 1 ± 2⁻²⁰).
 
+Each skeleton fixture also carries its grouped basis (occupation lists and
+packed words) so the GPU construction (HalfTiles.from_basis) can be checked
+against the reference's own build_skeleton output.
+
 The GPU box never reads /root/reference: tests load only these files.
 """
 
@@ -132,6 +136,10 @@ def skeleton_fixture(name, n, particles, bias, group_bits, seed, n_vec, m_ops, o
         X=X, Y_ref=Y_ref, accum=acc, accum_transpose=acc_t, accum_oracle=acc_oracle,
         m_ops=m_ops, op_kind=np.array(op_kind), op_seed=op_seed,
         diag_value_bits=f32bits(_h_value(0, 0, value_seed)), value_seed=value_seed,
+        # the grouped basis itself (mbstate.py Basis arrays), for the GPU
+        # construction path: occupation lists (n, N) uint16, packed words
+        basis_occ=grouped.occ_mat.astype(np.uint16), basis_bits_lo=grouped.bits_lo.astype(np.uint64),
+        basis_n_sp=grouped.n_sp, rank_threshold=rank.threshold,
     )
     print(f"{name}: n={n} nnz={sk.nnz} tiles={len(tiles)} orbitals={len(orbs)} digest={pair_digest}")
 

@@ -167,3 +167,19 @@ def test_bench_writes_reference_csv(tmp_path):
     assert len(cells) == 8 and cells[0] == "spmm" and cells[2] == "4194304" and cells[3] == "8"
     assert float(cells[6]) == 1.5e-3 and float(cells[7]) == 39000.0 and cells[4] == ""
     assert any(r.startswith("# results-digest=") for r in out.read_text().splitlines())
+
+
+@pytest.mark.parametrize("name", ["skel_small.npz", "skel_n1024.npz", "skel_identity.npz"])
+def test_basis_block_bound_never_drops_an_entry(name):
+    """construct.candidate_tiles prunes 64-block pairs with a popcount lower
+    bound; every block pair holding a reference entry must survive it."""
+    from paper_2110_10765_b200.construct import block_bounds, candidate_tiles
+
+    f = np.load(ROOT / "tests" / "golden" / name)
+    a, o = block_bounds(f["basis_bits_lo"])
+    cand = candidate_tiles(a, o, int(f["rank_threshold"]))
+    R, C = f["i"].astype(np.int64) // 64, f["j"].astype(np.int64) // 64
+    keep = R <= C
+    need = set(zip(R[keep].tolist(), C[keep].tolist()))
+    assert need <= set(map(tuple, cand.tolist()))
+    assert np.all(cand[:, 0] <= cand[:, 1])

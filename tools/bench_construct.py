@@ -1,0 +1,63 @@
+"""Device construction of H from a many-body basis (HalfTiles.from_basis) vs
+the reference's CPU skeleton build (pipeline.py:290-377).
+
+    python tools/bench_construct.py [--n 4096] [--particles 6] [--bias 0.2]
+
+The basis sampler here follows mbstate.random_basis's description (N of
+n_sp = 128 indices without replacement, weight exp(-bias·k), grouped by the
+low 8 occupancy bits) but is not bit-identical to it; the reference's own
+build time on its sampler is quoted from SURVEY.md §8(a) (38.7 s for
+n = 4096, 1.52 M entries) and can be re-measured in the build container with
+tools/bench_construct.py --reference.
+"""
+import argparse, json, os, sys, time
+import numpy as np
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=4096)
+ap.add_argument("--particles", type=int, default=6)
+ap.add_argument("--bias", type=float, default=0.2, help="lower it for large n (the biased sampler runs out of distinct states)")
+ap.add_argument("--seed", type=int, default=0)
+ap.add_argument("--reference", action="store_true", help="time the reference build (needs /root/reference)")
+a = ap.parse_args()
+
+rng = np.random.default_rng(a.seed)
+n_sp = 128
+w = np.exp(-a.bias * np.arange(1, n_sp + 1))
+seen, rows = set(), []
+while len(rows) < a.n:  # distinct states only (a basis has no duplicates)
+    r = tuple(np.sort(rng.choice(np.arange(1, n_sp + 1), size=a.particles, replace=False, p=w / w.sum())).tolist())
+    if r not in seen:
+        seen.add(r)
+        rows.append(r)
+occ = np.array(rows, dtype=np.uint16)
+lo = np.zeros(a.n, np.uint64)
+for k in range(a.particles):
+    m = occ[:, k] <= 64
+    lo[m] |= np.left_shift(np.uint64(1), (occ[m, k] - 1).astype(np.uint64))
+order = np.argsort(lo & np.uint64(0xFF), kind="stable")  # group_orbitals by the low-8-bit key
+occ, lo = occ[order], lo[order]
+out = {"n": a.n, "particles": a.particles, "bias": a.bias}
+if a.reference:
+    sys.path.insert(0, "/root/reference/pkg/src")
+    from cimotifs.mbstate import make_basis
+    from cimotifs.pipeline import build_skeleton, enumerate_tiles, group_orbitals
+    from cimotifs.sparsity import InteractionRank
+    basis = make_basis([tuple(int(x) for x in r) for r in occ], n_sp)
+    g, orbs = group_orbitals(basis, group_bits=8)
+    t0 = time.perf_counter()
+    sk = build_skeleton(enumerate_tiles(orbs, orbs, InteractionRank()), orbs, g, InteractionRank())
+    out.update(reference_s=time.perf_counter() - t0, reference_nnz=int(sk.nnz))
+else:
+    import paper_2110_10765_b200 as pkg
+    pkg.HalfTiles.from_basis(occ[:256], lo[:256])  # warm-up (module load, kernels)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    H = pkg.HalfTiles.from_basis(occ, lo)
+    torch.cuda.synchronize()
+    rc, cnt = H.tile_rc_host, 4096
+    out.update(gpu_s=time.perf_counter() - t0, stored_entries=H.meta["stored_entries"], dense_tiles=H.n_tiles,
+               sparse_tiles=H.n_sparse_tiles, candidate_tiles=H.meta["candidate_tiles"])
+print(json.dumps(out))
