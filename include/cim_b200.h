@@ -98,12 +98,14 @@ extern "C" {
  *   entry_off  int64  [n_tiles+1]    first entry of each tile, a multiple of 16
  *                                    (entries rowptr[t][64] .. next tile are zero
  *                                    padding, so tiles stage with 16-byte copies)
- *   rowptr     uint16 [n_tiles][65]  per local row, offsets relative to the tile
- *   colptr     uint16 [n_tiles][65]  per local column, offsets into cperm
+ *   rowptr     uint16 [n_tiles][72]  per local row (first 65 used), offsets
+ *                                    relative to the tile; 144-byte rows so a
+ *                                    tile's pointers are one 16-B-aligned copy
+ *   colptr     uint16 [n_tiles][72]  per local column (first 65 used), offsets into cperm
  *   col, row   uint8  [n_entries]    local column / row of each entry
  *   cperm      uint16 [n_entries]    tile-relative entry indices in column-major order
  *   vals       f32|f64[n_entries]
- * Bytes per entry: 4 + s (+ 268 B per tile), against 4096·s for a dense tile.
+ * Bytes per entry: 4 + s (+ 296 B per tile), against 4096·s for a dense tile.
  */
 typedef struct cim_sparse_tiles {
   int64_t         n_tiles;

@@ -34,6 +34,7 @@ from .halftiles import (
     DEFAULT_MAX_UNIT,
     LAYOUTS,
     SPARSE_ALIGN,
+    SPARSE_PTR_STRIDE,
     HalfTiles,
     SparseTiles,
     _as_torch_dtype,
@@ -138,15 +139,15 @@ def from_basis(basis_or_occ, bits_lo=None, *, rank: int = 2, value_seed: int = 0
         Ts = s_idx.size
         rc_s = np.ascontiguousarray(cand[s_idx])
         rcnt = rowcnt[torch.from_numpy(s_idx).to(dev)].to(torch.int64)
-        rowptr = torch.zeros((Ts, 65), dtype=torch.int64, device=dev)
-        rowptr[:, 1:] = torch.cumsum(rcnt, dim=1)
+        rowptr = torch.zeros((Ts, SPARSE_PTR_STRIDE), dtype=torch.int64, device=dev)
+        rowptr[:, 1:65] = torch.cumsum(rcnt, dim=1)
         cnt = rowptr[:, 64]
         off = torch.zeros(Ts + 1, dtype=torch.int64, device=dev)
         off[1:] = torch.cumsum((cnt + SPARSE_ALIGN - 1) // SPARSE_ALIGN * SPARSE_ALIGN, dim=0)
         off_host = off.cpu().numpy()
         E = int(off_host[-1])
         sp = SparseTiles(tile_rc=torch.from_numpy(rc_s).to(dev), entry_off=off, rowptr=rowptr.to(torch.int16),
-                         colptr=torch.empty((Ts, 65), dtype=torch.int16, device=dev),
+                         colptr=torch.zeros((Ts, SPARSE_PTR_STRIDE), dtype=torch.int16, device=dev),
                          col=torch.zeros(max(E, 1), dtype=torch.uint8, device=dev),
                          row=torch.zeros(max(E, 1), dtype=torch.uint8, device=dev),
                          cperm=torch.zeros(max(E, 1), dtype=torch.int16, device=dev),

@@ -9,6 +9,7 @@ namespace cim {
 constexpr int kBlock = 64;          // tile edge
 constexpr int kTileElems = 4096;    // 64 × 64
 constexpr int kGroupThreads = 128;  // consumer threads per group = micro-blocks per tile
+constexpr int kSpPtrStride = 72;    // uint16 row / column pointers per sparse tile (65 used; 144 B, 16-B aligned)
 
 // ---------------------------------------------------------------------------
 // Fragment layout v1 (include/cim_b200.h): micro-block mb ∈ [0,128) owns rows

@@ -87,7 +87,7 @@ __global__ void basis_fill_sparse_kernel(const uint64_t *lo, const uint16_t *occ
   const int2 t = rc[tt];
   const long long i = (long long)t.x * 64 + r;
   if (i >= n) return;
-  long long e = entry_off[tt] + rowptr[tt * 65 + r];
+  long long e = entry_off[tt] + rowptr[tt * kSpPtrStride + r];
   for (int c = 0; c < 64; ++c) {
     const long long j = (long long)t.y * 64 + c;
     if (j < n && kept(lo, occ, npart, thr, i, j)) {

@@ -5,17 +5,16 @@
 // sparse: streaming them as dense tiles would move 4096 values per tile for
 // a few hundred entries.
 //
-// One warp per tile (persistent warps, global ticket counter), two passes,
-// both register reductions — no atomics inside a tile (shared-memory f32
-// atomicAdd is a CAS loop on sm_100; a first version built on it ran 4×
-// slower than streaming the tiles dense):
-//   * direct: lane ℓ owns local rows ℓ, ℓ+32 and walks their row-sorted
-//     entries, acc += v·X_C[col]; one vector red.global per row;
-//   * transposed (off-diagonal tiles): lane ℓ owns local columns ℓ, ℓ+32 and
-//     walks them through the column permutation, acc += v·X_R[row]; one
-//     vector red.global per column.
-// X rows are read through L1 (a tile's entries hit one 64-row X block
-// repeatedly).  k is processed in passes of KV vectors (8 f32 / 4 f64).
+// Ring design (v5, the dense kernel's structure with variable-size stages):
+// a producer warp bulk-copies each tile's pointers, entry arrays and X_C /
+// X_R blocks into shared memory; 128 consumer threads (local row / column r,
+// vector half h) then run both products as register reductions —
+//   * direct: thread r walks row r's row-sorted entries, acc += v·X_C[col];
+//   * transposed (off-diagonal tiles): thread r walks column r through the
+//     column permutation, acc += v·X_R[row];
+// one vector red.global per row / column and vector half.  No atomics inside
+// a tile (shared-memory f32 atomicAdd is a CAS loop on sm_100; a first
+// version built on it ran 4× slower than streaming the tiles dense).
 #include <cstdint>
 #include <mutex>
 #include <string>
@@ -28,7 +27,6 @@
 namespace cim {
 namespace {
 
-constexpr int kSpWarps = 4;  // warps per CTA
 
 template <typename T, int KV>
 __device__ __forceinline__ void ldg_vec(T (&d)[KV], const T *p) {
@@ -76,37 +74,57 @@ struct SparseParams {
   int k;
 };
 
-// Per-warp double-buffered shared staging: a tile's entry arrays (≤ kSpCap
-// entries) and the X_C / X_R slices, filled with cp.async while the previous
-// tile is being multiplied.
+// ---------------------------------------------------------------------------
+// Kernel v5: the dense kernel's producer / consumer ring with variable-size
+// stages.  A producer warp takes tiles from a ticket counter and bulk-copies
+// (cp.async.bulk, mbarrier complete_tx) each tile's row / column pointers,
+// entry arrays and X_C / X_R blocks into a ring of shared-memory stages; the
+// 4 consumer warps (128 threads: local row / column r, vector half h) walk
+// the tile from shared memory.  Tiles above kSpCap entries are flagged and
+// walked from global memory instead.
+// ---------------------------------------------------------------------------
 constexpr int kSpCap = 1024;
+constexpr int kSpConsumers = 128;
+constexpr unsigned kSpBig = 1u, kSpTerm = 2u;
 
-template <typename T, int KV>
-struct SpStage {
-  uint8_t col[kSpCap];
-  uint8_t row[kSpCap];
-  uint16_t cperm[kSpCap];
-  alignas(16) T val[kSpCap];
-  alignas(16) T xc[64 * KV];
-  alignas(16) T xr[64 * KV];
+struct SpStageHdr {
+  int R, C, ne;
+  unsigned flags;
+  long long t;  // tile index (global fallback)
+  long long pad;
 };
 
-__device__ __forceinline__ void cp16(void *dst, const void *src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+struct SpLayout {  // byte offsets inside one stage
+  unsigned rp, cp, col, row, cperm, val, xc, xr, bytes;
+};
 
-__device__ __forceinline__ void copy16_async(void *dst, const void *src, int bytes, int lane) {
-  const char *s = static_cast<const char *>(src);
-  char *d = static_cast<char *>(dst);
-  for (int q = lane; q < bytes / 16; q += 32) cp16(d + 16 * q, s + 16 * q);
+__host__ __device__ __forceinline__ SpLayout sp_layout(int k, int es) {
+  SpLayout L;
+  L.rp = 32;
+  L.cp = L.rp + 2 * kSpPtrStride;
+  L.col = L.cp + 2 * kSpPtrStride;
+  L.row = L.col + kSpCap;
+  L.cperm = L.row + kSpCap;
+  L.val = L.cperm + 2 * kSpCap;
+  L.xc = L.val + kSpCap * es;
+  L.xr = L.xc + 64 * k * es;
+  L.bytes = (L.xr + 64 * k * es + 127) & ~127u;
+  return L;
 }
 
-template <typename T, int KV>
-__device__ __forceinline__ void lds_vec(T (&d)[KV], const T *p) {
-  if constexpr (sizeof(T) == 4 && KV % 4 == 0) {
+template <bool GLOBAL, typename U>
+__device__ __forceinline__ U ld1(const U *p) {
+  if constexpr (GLOBAL)
+    return __ldg(p);
+  else
+    return *p;
+}
+
+template <bool GLOBAL, typename T, int KV>
+__device__ __forceinline__ void ldx(T (&d)[KV], const T *p) {
+  if constexpr (GLOBAL) {
+    ldg_vec<T, KV>(d, p);
+  } else if constexpr (sizeof(T) == 4 && KV % 4 == 0) {
 #pragma unroll
     for (int q = 0; q < KV / 4; ++q) {
       const float4 v = reinterpret_cast<const float4 *>(p)[q];
@@ -124,204 +142,176 @@ __device__ __forceinline__ void lds_vec(T (&d)[KV], const T *p) {
   }
 }
 
-// One tile's header, held in registers: its lane's row/column pointer
-// values (rows lane, lane+32, and 64), entry range, position.
-struct SpHdr {
-  int2 rc;
-  long long base;
-  int ne;             // padded entry count
-  uint16_t r0, r1, r64, c0, c1, c64;
-};
-
-__device__ __forceinline__ SpHdr load_hdr(const SparseParams &p, long long t, int lane) {
-  SpHdr h;
-  h.rc = p.tile_rc[t];
-  h.base = p.entry_off[t];
-  h.ne = (int)(p.entry_off[t + 1] - h.base);
-  const uint16_t *rp = p.rowptr + (size_t)t * 65, *cp = p.colptr + (size_t)t * 65;
-  h.r0 = rp[lane], h.r1 = rp[lane + 32], h.r64 = rp[64];
-  h.c0 = cp[lane], h.c1 = cp[lane + 32], h.c64 = cp[64];
-  return h;
-}
-
-// Bounds of a lane's two rows (or columns) from the held pointer values.
-__device__ __forceinline__ void bounds(int lane, int v0, int v1, int v64, int (&lo)[2], int (&hi)[2]) {
-  const int n0 = __shfl_down_sync(0xffffffffu, v0, 1), n1 = __shfl_down_sync(0xffffffffu, v1, 1);
-  const int b32 = __shfl_sync(0xffffffffu, v1, 0);
-  lo[0] = v0, lo[1] = v1;
-  hi[0] = lane < 31 ? n0 : b32;
-  hi[1] = lane < 31 ? n1 : v64;
-}
-
-// X slices are staged for every staged tile (kSpStageX = 0): reading the
-// few X rows of a sparse tile through L1 instead measured 2× slower at 2%
-// fill (dependent global loads per entry); the threshold stays as a knob.
-constexpr int kSpStageX = 0;
-
-template <typename T, int KV>
-__device__ __forceinline__ void issue_stage(SpStage<T, KV> &st, const SparseParams &p, const SpHdr &h, int v0,
-                                            int lane) {
-  const T *vals = static_cast<const T *>(p.vals);
-  const T *X = static_cast<const T *>(p.X);
-  // entries are re-staged for every vector pass (the other buffer holds them
-  // only for the previous step)
-  copy16_async(st.col, p.col + h.base, h.ne, lane);
-  copy16_async(st.row, p.row + h.base, h.ne, lane);
-  copy16_async(st.cperm, p.cperm + h.base, 2 * h.ne, lane);
-  copy16_async(st.val, vals + h.base, h.ne * (int)sizeof(T), lane);
-  if (h.ne < kSpStageX) return;
-  constexpr int CPR = KV * (int)sizeof(T) / 16;  // 16-byte chunks per X row slice
-  const T *xc = X + (long long)h.rc.y * 64 * p.ldx + v0;
-  const T *xr = X + (long long)h.rc.x * 64 * p.ldx + v0;
-  for (int q = lane; q < 64 * CPR; q += 32) {
-    const int r = q / CPR, c = q % CPR;
-    cp16(reinterpret_cast<char *>(st.xc) + 16 * q, reinterpret_cast<const char *>(xc + (long long)r * p.ldx) + 16 * c);
-    if (h.rc.x != h.rc.y)
-      cp16(reinterpret_cast<char *>(st.xr) + 16 * q,
-           reinterpret_cast<const char *>(xr + (long long)r * p.ldx) + 16 * c);
+// One tile, both products, by one warp: lane owns local rows / columns
+// lane and lane+32 and KV vectors per pass (k in passes of KV).
+template <bool GLOBAL, typename T, int KV>
+__device__ __forceinline__ void sp_tile(int lane, int R, int C, const uint16_t *rp, const uint16_t *cp,
+                                        const uint8_t *col, const uint8_t *row, const uint16_t *cperm,
+                                        const T *val, const T *xc, const T *xr, int k, T *Y, long long ldy) {
+  const bool diag = R == C;
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    const int r = lane + 32 * hh;
+    const int e0 = ld1<GLOBAL>(rp + r), e1 = ld1<GLOBAL>(rp + r + 1);
+    const int q0 = diag ? 0 : ld1<GLOBAL>(cp + r), q1 = diag ? 0 : ld1<GLOBAL>(cp + r + 1);
+    for (int v0 = 0; v0 < k; v0 += KV) {
+      if (e1 > e0) {  // direct: row r
+        T acc[KV];
+#pragma unroll
+        for (int q = 0; q < KV; ++q) acc[q] = T(0);
+        for (int e = e0; e < e1; ++e) {
+          const int c = ld1<GLOBAL>(col + e);
+          const T w = ld1<GLOBAL>(val + e);
+          T x[KV];
+          ldx<GLOBAL, T, KV>(x, xc + (long long)c * k + v0);
+#pragma unroll
+          for (int q = 0; q < KV; ++q) acc[q] = fma(w, x[q], acc[q]);
+        }
+        red_vec<T, KV>(Y + ((long long)R * 64 + r) * ldy + v0, acc);
+      }
+      if (q1 > q0) {  // transposed: column r
+        T acc[KV];
+#pragma unroll
+        for (int q = 0; q < KV; ++q) acc[q] = T(0);
+        for (int qi = q0; qi < q1; ++qi) {
+          const int e = ld1<GLOBAL>(cperm + qi);
+          const int rr = ld1<GLOBAL>(row + e);
+          const T w = ld1<GLOBAL>(val + e);
+          T x[KV];
+          ldx<GLOBAL, T, KV>(x, xr + (long long)rr * k + v0);
+#pragma unroll
+          for (int q = 0; q < KV; ++q) acc[q] = fma(w, x[q], acc[q]);
+        }
+        red_vec<T, KV>(Y + ((long long)C * 64 + r) * ldy + v0, acc);
+      }
+    }
   }
 }
 
-// Two register-reduction passes over one tile, operands in the stage
-// (STAGED) or straight from global memory (tiles above kSpCap entries).
-template <typename T, int KV, bool STAGED, bool XST>
-__device__ __forceinline__ void tile_passes(int lane, const SpHdr &h, const SparseParams &p, const SpStage<T, KV> *st,
-                                            int v0) {
-  const bool diag = h.rc.x == h.rc.y;
+template <typename T, int KV>
+__global__ void __launch_bounds__(kSpConsumers + 32) sparse_spmm_kernel(const SparseParams p, int S) {
+  extern __shared__ __align__(128) unsigned char sp_smem[];
+  const SpLayout L = sp_layout(p.k, (int)sizeof(T));
+  uint64_t *full = reinterpret_cast<uint64_t *>(sp_smem + (size_t)S * L.bytes);
+  uint64_t *empty = full + S;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);  // one consumer warp per stage
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
   const T *X = static_cast<const T *>(p.X);
   T *Y = static_cast<T *>(p.Y);
-  const uint8_t *col = STAGED ? st->col : p.col + h.base;
-  const uint8_t *row = STAGED ? st->row : p.row + h.base;
-  const uint16_t *cperm = STAGED ? st->cperm : p.cperm + h.base;
-  const T *val = STAGED ? st->val : static_cast<const T *>(p.vals) + h.base;
-  const T *xc = XST ? st->xc : X + (long long)h.rc.y * 64 * p.ldx + v0;
-  const T *xr = XST ? st->xr : X + (long long)h.rc.x * 64 * p.ldx + v0;
-  const long long xs = XST ? KV : p.ldx;
-  int lo[2], hi[2];
-  bounds(lane, h.r0, h.r1, h.r64, lo, hi);
-  T *y_r = Y + (long long)h.rc.x * 64 * p.ldy + v0;
-#pragma unroll
-  for (int k2 = 0; k2 < 2; ++k2) {  // direct: rows lane, lane+32
-    if (lo[k2] == hi[k2]) continue;
-    T acc[KV];
-#pragma unroll
-    for (int q = 0; q < KV; ++q) acc[q] = T(0);
-    int e = lo[k2];
-    for (; e + 2 <= hi[k2]; e += 2) {  // two independent load chains per iteration
-      const int c0 = col[e], c1 = col[e + 1];
-      const T v0_ = val[e], v1_ = val[e + 1];
-      T x0[KV], x1[KV];
-      if constexpr (XST) {
-        lds_vec<T, KV>(x0, xc + c0 * xs);
-        lds_vec<T, KV>(x1, xc + c1 * xs);
-      } else {
-        ldg_vec<T, KV>(x0, xc + c0 * xs);
-        ldg_vec<T, KV>(x1, xc + c1 * xs);
-      }
-#pragma unroll
-      for (int q = 0; q < KV; ++q) acc[q] = fma(v1_, x1[q], fma(v0_, x0[q], acc[q]));
-    }
-    if (e < hi[k2]) {
-      const int c = col[e];
-      const T v = val[e];
-      T x[KV];
-      if constexpr (XST)
-        lds_vec<T, KV>(x, xc + c * xs);
-      else
-        ldg_vec<T, KV>(x, xc + c * xs);
-#pragma unroll
-      for (int q = 0; q < KV; ++q) acc[q] = fma(v, x[q], acc[q]);
-    }
-    red_vec<T, KV>(y_r + (long long)(lane + 32 * k2) * p.ldy, acc);
-  }
-  if (diag) return;
-  bounds(lane, h.c0, h.c1, h.c64, lo, hi);
-  T *y_c = Y + (long long)h.rc.y * 64 * p.ldy + v0;
-#pragma unroll
-  for (int k2 = 0; k2 < 2; ++k2) {  // transposed: columns lane, lane+32
-    if (lo[k2] == hi[k2]) continue;
-    T acc[KV];
-#pragma unroll
-    for (int q = 0; q < KV; ++q) acc[q] = T(0);
-    int qi = lo[k2];
-    for (; qi + 2 <= hi[k2]; qi += 2) {
-      const int e0 = cperm[qi], e1 = cperm[qi + 1];
-      const int r0 = row[e0], r1 = row[e1];
-      const T v0_ = val[e0], v1_ = val[e1];
-      T x0[KV], x1[KV];
-      if constexpr (XST) {
-        lds_vec<T, KV>(x0, xr + r0 * xs);
-        lds_vec<T, KV>(x1, xr + r1 * xs);
-      } else {
-        ldg_vec<T, KV>(x0, xr + r0 * xs);
-        ldg_vec<T, KV>(x1, xr + r1 * xs);
-      }
-#pragma unroll
-      for (int q = 0; q < KV; ++q) acc[q] = fma(v1_, x1[q], fma(v0_, x0[q], acc[q]));
-    }
-    if (qi < hi[k2]) {
-      const int e = cperm[qi];
-      const int r = row[e];
-      const T v = val[e];
-      T x[KV];
-      if constexpr (XST)
-        lds_vec<T, KV>(x, xr + r * xs);
-      else
-        ldg_vec<T, KV>(x, xr + r * xs);
-#pragma unroll
-      for (int q = 0; q < KV; ++q) acc[q] = fma(v, x[q], acc[q]);
-    }
-    red_vec<T, KV>(y_c + (long long)(lane + 32 * k2) * p.ldy, acc);
-  }
-}
+  const T *vals = static_cast<const T *>(p.vals);
+  const unsigned xblk = 64u * (unsigned)p.k * (unsigned)sizeof(T);
 
-// Static contiguous tile chunks per warp; software pipeline: the header of
-// tile i+1 and its staged operands load while tile i is multiplied.
-template <typename T, int KV>
-__global__ void __launch_bounds__(kSpWarps * 32) sparse_spmm_kernel(const SparseParams p) {
-  extern __shared__ __align__(16) unsigned char sp_smem[];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  SpStage<T, KV> *stage = reinterpret_cast<SpStage<T, KV> *>(sp_smem) + 2 * w;
-  const long long gw = (long long)blockIdx.x * kSpWarps + w, nw = (long long)gridDim.x * kSpWarps;
-  const long long t_lo = p.n_tiles * gw / nw, t_hi = p.n_tiles * (gw + 1) / nw;
-  if (t_lo >= t_hi) return;
-  const int npass = (p.k + KV - 1) / KV;
-  // X slices stage in 16-byte chunks: narrower passes read X through L1
-  constexpr bool kStageable = (KV * sizeof(T)) % 16 == 0;
-  // flattened (tile, pass) steps; step s → tile t_lo + s / npass, pass s % npass
-  const long long nsteps = (t_hi - t_lo) * npass;
-  SpHdr cur = load_hdr(p, t_lo, lane);
-  bool cur_staged = kStageable && cur.ne <= kSpCap && (p.ldx * (long long)sizeof(T)) % 16 == 0;
-  if constexpr (kStageable)
-    if (cur_staged) issue_stage<T, KV>(stage[0], p, cur, 0, lane);
-  cp_commit();
-  for (long long s = 0; s < nsteps; ++s) {
-    const long long t = t_lo + s / npass;
-    const int v0 = (int)(s % npass) * KV;
-    // prefetch the next step (same tile next pass, or the next tile)
-    SpHdr nxt = cur;
-    bool nxt_staged = false;
-    if (s + 1 < nsteps) {
-      const long long tn = t_lo + (s + 1) / npass;
-      if (tn != t) nxt = load_hdr(p, tn, lane);
-      nxt_staged = kStageable && nxt.ne <= kSpCap && (p.ldx * (long long)sizeof(T)) % 16 == 0;
-      __syncwarp();  // everyone is done with the buffer being refilled (step s-1's)
-      if constexpr (kStageable)
-        if (nxt_staged) issue_stage<T, KV>(stage[(s + 1) & 1], p, nxt, (int)((s + 1) % npass) * KV, lane);
+  if (tid >= kSpConsumers) {
+    // ======================= producer warp =======================
+    // Tickets are chunks of 32 tiles: the whole warp loads a chunk's headers
+    // at once (one memory latency per 32 tiles), lane 0 then streams them.
+    const int lane = tid & 31;
+    const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
+    int stage = 0;
+    uint32_t phase = 0;
+    unsigned int t0 = 0;
+    if (lane == 0) t0 = atomicAdd(p.counter, 32u);
+    t0 = __shfl_sync(0xffffffffu, t0, 0);
+    while ((long long)t0 < p.n_tiles) {
+      unsigned int t_next = 0;
+      if (lane == 0) t_next = atomicAdd(p.counter, 32u);  // prefetch the next chunk's ticket
+      const long long t = (long long)t0 + lane;
+      const bool valid = t < p.n_tiles;
+      const int2 my_rc = valid ? p.tile_rc[t] : make_int2(0, 0);
+      const long long my_b = valid ? p.entry_off[t] : 0, my_e = valid ? p.entry_off[t + 1] : 0;
+      const int cnt = (int)min(32LL, p.n_tiles - (long long)t0);
+      for (int q = 0; q < cnt; ++q) {
+        const int R = __shfl_sync(0xffffffffu, my_rc.x, q), C = __shfl_sync(0xffffffffu, my_rc.y, q);
+        const long long base = __shfl_sync(0xffffffffu, my_b, q);
+        const int ne = (int)(__shfl_sync(0xffffffffu, my_e, q) - base);
+        if (lane == 0) {
+          const long long tt = (long long)t0 + q;
+          mbar_wait_backoff(&empty[stage], phase ^ 1u);
+          unsigned char *st = sp_smem + (size_t)stage * L.bytes;
+          SpStageHdr *h = reinterpret_cast<SpStageHdr *>(st);
+          const bool diag = R == C, big = ne > kSpCap;
+          h->R = R;
+          h->C = C;
+          h->ne = ne;
+          h->flags = big ? kSpBig : 0u;
+          h->t = tt;
+          if (big) {
+            mbar_arrive(&full[stage]);
+          } else {
+            const unsigned bytes = 4u * kSpPtrStride + 4u * (unsigned)ne + (unsigned)(ne * (int)sizeof(T)) + xblk +
+                                   (diag ? 0u : xblk);
+            mbar_arrive_expect_tx(&full[stage], bytes);
+            bulk_g2s(st + L.rp, p.rowptr + (size_t)tt * kSpPtrStride, 2 * kSpPtrStride, &full[stage], pol_stream);
+            bulk_g2s(st + L.cp, p.colptr + (size_t)tt * kSpPtrStride, 2 * kSpPtrStride, &full[stage], pol_stream);
+            if (ne > 0) {
+              bulk_g2s(st + L.col, p.col + base, ne, &full[stage], pol_stream);
+              bulk_g2s(st + L.row, p.row + base, ne, &full[stage], pol_stream);
+              bulk_g2s(st + L.cperm, p.cperm + base, 2 * ne, &full[stage], pol_stream);
+              bulk_g2s(st + L.val, vals + base, ne * (int)sizeof(T), &full[stage], pol_stream);
+            }
+            bulk_g2s(st + L.xc, X + (long long)C * 64 * p.k, xblk, &full[stage], pol_keep);
+            if (!diag) bulk_g2s(st + L.xr, X + (long long)R * 64 * p.k, xblk, &full[stage], pol_keep);
+          }
+        }
+        __syncwarp();
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+      t0 = __shfl_sync(0xffffffffu, t_next, 0);
     }
-    cp_commit();
-    cp_wait1();  // this step's stage has landed (this lane's copies) ...
-    __syncwarp();  // ... and everyone's
-    if (kStageable && cur_staged) {
-      if (cur.ne >= kSpStageX)
-        tile_passes<T, KV, true, true>(lane, cur, p, &stage[s & 1], v0);
-      else
-        tile_passes<T, KV, true, false>(lane, cur, p, &stage[s & 1], v0);
+    if (lane == 0)  // one terminator per consumer warp (stage s belongs to warp s % 4)
+      for (int q = 0; q < kSpConsumers / 32; ++q) {
+        mbar_wait_backoff(&empty[stage], phase ^ 1u);
+        reinterpret_cast<SpStageHdr *>(sp_smem + (size_t)stage * L.bytes)->flags = kSpTerm;
+        mbar_arrive(&full[stage]);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    return;
+  }
+
+  // ======================= consumer warps =======================
+  // warp w consumes stages w, w+4, w+8, ... (S is a multiple of 4): four
+  // tiles in flight per CTA, one per warp.
+  const int w = tid >> 5, lane = tid & 31;
+  constexpr int NW = kSpConsumers / 32;
+  int stage = w;
+  uint32_t phase = 0;
+  while (true) {
+    mbar_wait(&full[stage], phase);
+    const unsigned char *st = sp_smem + (size_t)stage * L.bytes;
+    const SpStageHdr h = *reinterpret_cast<const SpStageHdr *>(st);
+    if (h.flags & kSpTerm) break;
+    if (h.flags & kSpBig) {
+      const long long t = h.t, base = p.entry_off[t];
+      sp_tile<true, T, KV>(lane, h.R, h.C, p.rowptr + (size_t)t * kSpPtrStride, p.colptr + (size_t)t * kSpPtrStride,
+                           p.col + base, p.row + base, p.cperm + base, vals + base, X + (long long)h.C * 64 * p.k,
+                           X + (long long)h.R * 64 * p.k, p.k, Y, p.ldy);
     } else {
-      tile_passes<T, KV, false, false>(lane, cur, p, nullptr, v0);
+      sp_tile<false, T, KV>(lane, h.R, h.C, reinterpret_cast<const uint16_t *>(st + L.rp),
+                            reinterpret_cast<const uint16_t *>(st + L.cp), st + L.col, st + L.row,
+                            reinterpret_cast<const uint16_t *>(st + L.cperm), reinterpret_cast<const T *>(st + L.val),
+                            reinterpret_cast<const T *>(st + L.xc), reinterpret_cast<const T *>(st + L.xr), p.k, Y,
+                            p.ldy);
     }
-    cur = nxt;
-    cur_staged = nxt_staged;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    stage += NW;
+    if (stage >= S) {
+      stage -= S;
+      phase ^= 1u;
+    }
   }
 }
 
@@ -335,7 +325,7 @@ __global__ void fill_sparse_values_kernel(const int2 *tile_rc, const long long *
   for (long long t = warp; t < n_tiles; t += nwarps) {
     const int2 rc = tile_rc[t];
     const long long base = entry_off[t];
-    const uint16_t *rp = rowptr + (size_t)t * 65;
+    const uint16_t *rp = rowptr + (size_t)t * kSpPtrStride;
     for (int r = lane; r < 64; r += 32) {
       const uint64_t i = (uint64_t)rc.x * 64 + r;
       for (int e = rp[r]; e < rp[r + 1]; ++e) {
@@ -380,6 +370,20 @@ int launch_sparse(const cim_sparse_tiles *S, const void *X, void *Y, int k, long
   SpState *st = nullptr;
   int rc = sp_state(&st);
   if (rc) return rc;
+  if (ldx != k) return set_error(CIM_EINVAL, "sparse tiles need dense X rows (ldx == k)");
+  const SpLayout L = sp_layout(k, (int)sizeof(T));
+  // 8 stages (2 per consumer warp) when two CTAs fit per SM, else 4
+  int stages = ((size_t)8 * L.bytes + 128 <= 113 * 1024) ? 8 : 4;
+  const size_t smem = (size_t)stages * L.bytes + 128;
+  if (smem > 227 * 1024) return set_error(CIM_EUNSUPPORTED, "k too large for the sparse-tile stages");
+  unsigned int *ctr;
+  {
+    std::lock_guard<std::mutex> lk(g_sp_mu);
+    if (st->pos >= kSpRing) st->pos = 0;
+    ctr = st->counters + st->pos++;
+  }
+  cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(unsigned int), stream);
+  if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("sparse counter: ") + cudaGetErrorString(e));
   SparseParams p;
   p.tile_rc = reinterpret_cast<const int2 *>(S->tile_rc);
   p.entry_off = reinterpret_cast<const long long *>(S->entry_off);
@@ -391,24 +395,21 @@ int launch_sparse(const cim_sparse_tiles *S, const void *X, void *Y, int k, long
   p.vals = S->vals;
   p.X = X;
   p.Y = Y;
-  p.counter = nullptr;
+  p.counter = ctr;
   p.n_tiles = S->n_tiles;
   p.ldx = ldx;
   p.ldy = ldy;
   p.k = k;
-  const size_t smem = 2 * kSpWarps * sizeof(SpStage<T, KV>);
-  static std::once_flag attr_once;
-  std::call_once(attr_once, [&] {
-    cudaFuncSetAttribute(sparse_spmm_kernel<T, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  });
+  e = cudaFuncSetAttribute(sparse_spmm_kernel<T, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("sparse attr: ") + cudaGetErrorString(e));
   int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sparse_spmm_kernel<T, KV>, kSpWarps * 32, smem) != cudaSuccess ||
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sparse_spmm_kernel<T, KV>, kSpConsumers + 32, smem) !=
+          cudaSuccess ||
       occ < 1)
     occ = 1;
-  const long long warps = std::min<long long>(S->n_tiles, (long long)st->sms * occ * kSpWarps);
-  const unsigned grid = (unsigned)((warps + kSpWarps - 1) / kSpWarps);
-  sparse_spmm_kernel<T, KV><<<grid, kSpWarps * 32, smem, stream>>>(p);
-  const cudaError_t e = cudaGetLastError();
+  const long long grid = std::min<long long>(S->n_tiles, (long long)st->sms * occ);
+  sparse_spmm_kernel<T, KV><<<(unsigned)grid, kSpConsumers + 32, smem, stream>>>(p, stages);
+  e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("sparse_spmm launch: ") + cudaGetErrorString(e));
   return CIM_OK;
 }
@@ -509,7 +510,7 @@ __global__ void sparse_fill_entries_kernel(const int2 *tile_rc, const long long 
   const int r = (int)(g & 63);
   const int2 rc = tile_rc[t];
   const uint64_t i = (uint64_t)rc.x * 64 + r;
-  long long e = entry_off[t] + rowptr[t * 65 + r];
+  long long e = entry_off[t] + rowptr[t * kSpPtrStride + r];
   if (i >= (uint64_t)n) return;
   for (int c = 0; c < 64; ++c) {
     const uint64_t j = (uint64_t)rc.y * 64 + c;
@@ -588,7 +589,7 @@ __global__ void sparse_build_columns_kernel(const long long *entry_off, const ui
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
   for (long long t = warp; t < n_tiles; t += nwarps) {
     const long long base = entry_off[t];
-    const uint16_t *rp = rowptr + (size_t)t * 65;
+    const uint16_t *rp = rowptr + (size_t)t * kSpPtrStride;
     const uint8_t *cl = col + base;
     int cnt[2] = {0, 0};
     for (int r = 0; r < 64; ++r) {  // count: lane owns columns lane, lane+32
@@ -613,7 +614,7 @@ __global__ void sparse_build_columns_kernel(const long long *entry_off, const ui
       if (lane >= d) incl1 += y;
     }
     int pos[2] = {incl0 - cnt[0], tot0 + incl1 - cnt[1]};
-    uint16_t *cpt = colptr + (size_t)t * 65;
+    uint16_t *cpt = colptr + (size_t)t * kSpPtrStride;
     cpt[lane + 1] = (uint16_t)(pos[0] + cnt[0]);
     cpt[lane + 33] = (uint16_t)(pos[1] + cnt[1]);
     if (lane == 0) cpt[0] = 0;

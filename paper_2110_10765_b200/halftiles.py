@@ -182,6 +182,7 @@ def fragment_pack_host(tiles: np.ndarray, layout: str = "frag") -> np.ndarray:
 
 
 SPARSE_ALIGN = 16  # entries: every sparse tile's entry range starts 16-entry aligned (vector staging)
+SPARSE_PTR_STRIDE = 72  # uint16 row / column pointers per sparse tile (65 used): 144-byte, 16-B-aligned rows
 
 
 def dense_break_even(dtype) -> float:
@@ -206,8 +207,8 @@ class SparseTiles:
 
     tile_rc: torch.Tensor  # int32 (Ts,2) device
     entry_off: torch.Tensor  # int64 (Ts+1) device
-    rowptr: torch.Tensor  # int16 (Ts,65) device (values ≤ 4096)
-    colptr: torch.Tensor  # int16 (Ts,65) device
+    rowptr: torch.Tensor  # int16 (Ts,72) device (first 65 used; values ≤ 4096)
+    colptr: torch.Tensor  # int16 (Ts,72) device
     col: torch.Tensor  # uint8 (E,) device
     row: torch.Tensor  # uint8 (E,) device
     cperm: torch.Tensor  # int16 (E,) device: tile-relative entry index, column-major order
@@ -281,12 +282,12 @@ class SparseTiles:
         pos = off[tile_id] + local  # slot of each (sorted) entry in the padded arrays
         rowcnt = np.zeros((T, 64), dtype=np.int64)
         np.add.at(rowcnt, (tile_id, r), 1)
-        rowptr = np.zeros((T, 65), dtype=np.int64)
-        np.cumsum(rowcnt, axis=1, out=rowptr[:, 1:])
+        rowptr = np.zeros((T, SPARSE_PTR_STRIDE), dtype=np.int64)
+        rowptr[:, 1:65] = np.cumsum(rowcnt, axis=1)
         colcnt = np.zeros((T, 64), dtype=np.int64)
         np.add.at(colcnt, (tile_id, c), 1)
-        colptr = np.zeros((T, 65), dtype=np.int64)
-        np.cumsum(colcnt, axis=1, out=colptr[:, 1:])
+        colptr = np.zeros((T, SPARSE_PTR_STRIDE), dtype=np.int64)
+        colptr[:, 1:65] = np.cumsum(colcnt, axis=1)
         corder = np.lexsort((r, c, tile_id))  # column-major within each tile, rows ascending
         E = int(off[-1])
         col_a = np.zeros(max(E, 1), np.uint8)
@@ -542,15 +543,15 @@ class HalfTiles:
             check(L.cim_sparse_count_rows(t_rc.data_ptr() if T else None, T, n, float(fill), fill_seed,
                                           rowcnt.data_ptr(), stream), "cim_sparse_count_rows")
         rowcnt = rowcnt[:T]
-        rowptr = torch.zeros((T, 65), dtype=torch.int64, device=dev)
-        rowptr[:, 1:] = torch.cumsum(rowcnt, dim=1)
+        rowptr = torch.zeros((T, SPARSE_PTR_STRIDE), dtype=torch.int64, device=dev)
+        rowptr[:, 1:65] = torch.cumsum(rowcnt, dim=1)
         counts = rowptr[:, 64]
         off = torch.zeros(T + 1, dtype=torch.int64, device=dev)
         off[1:] = torch.cumsum((counts + SPARSE_ALIGN - 1) // SPARSE_ALIGN * SPARSE_ALIGN, dim=0)
         off_host = off.cpu().numpy()
         E = int(off_host[-1])
         sp = SparseTiles(tile_rc=t_rc, entry_off=off, rowptr=rowptr.to(torch.int16),
-                         colptr=torch.empty((T, 65), dtype=torch.int16, device=dev),
+                         colptr=torch.zeros((T, SPARSE_PTR_STRIDE), dtype=torch.int16, device=dev),
                          col=torch.zeros(max(E, 1), dtype=torch.uint8, device=dev),
                          row=torch.zeros(max(E, 1), dtype=torch.uint8, device=dev),
                          cperm=torch.zeros(max(E, 1), dtype=torch.int16, device=dev),
