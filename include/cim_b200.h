@@ -214,11 +214,14 @@ CIM_API int cim_tsmm(const float *A, int64_t lda, int32_t q, const float *C, int
  * base + (c / bw)·bstride + r·ld + (c % bw)  (elements) — e.g. the eigensolver's
  * block-major work buffer [slot][row][bw], where a column slice of a wide
  * row-major buffer would waste most of every DRAM burst.
+ * cim_gram_blocked's block_mask selects the 8×8 output blocks to compute
+ * (bit bi·⌈cb/8⌉ + bj; 0 = all; the rest are written as 0) so a caller can
+ * skip the mirror half of symmetric products; B == A is loaded once.
  */
 CIM_API int cim_gram_blocked(const void *A, int64_t lda, int32_t a_bw, int64_t a_bstride, int32_t ca,
                              const void *B, int64_t ldb, int32_t b_bw, int64_t b_bstride, int32_t cb,
                              int64_t rows, int32_t dtype, double *out, void *workspace,
-                             uint64_t ws_bytes, void *stream);
+                             uint64_t ws_bytes, uint64_t block_mask, void *stream);
 CIM_API int cim_tsmm_blocked(const float *A, int64_t lda, int32_t a_bw, int64_t a_bstride, int32_t q,
                              const float *C, int32_t p, float alpha, float beta, float *Out,
                              int64_t ldo, int32_t o_bw, int64_t o_bstride, int64_t rows, void *stream);

@@ -152,7 +152,7 @@ def lib() -> ctypes.CDLL:
                            c.c_int64, c.c_int64, c.c_void_p]
     L.cim_gram_blocked.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_int64, c.c_int32, c.c_void_p, c.c_int64,
                                    c.c_int32, c.c_int64, c.c_int32, c.c_int64, c.c_int32, c.c_void_p, c.c_void_p,
-                                   c.c_uint64, c.c_void_p]
+                                   c.c_uint64, c.c_uint64, c.c_void_p]
     L.cim_tsmm_blocked.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_int64, c.c_int32, c.c_void_p, c.c_int32,
                                    c.c_float, c.c_float, c.c_void_p, c.c_int64, c.c_int32, c.c_int64, c.c_int64,
                                    c.c_void_p]

@@ -127,23 +127,35 @@ __device__ __forceinline__ void load8(double (&d)[8], const T *p) {
 // A kGramStages-deep cp.async ring of slabs (input dtype); each thread owns
 // an 8×8 block of G for one residue class of a slab's rows and widens its 16
 // operands per row to f64 on use (16 F2F per 64 DFMA).
+// block_mask: bit (bi·nbj + bj) set ⇔ output block (bi, bj) is computed (a
+// caller exploiting symmetry skips the mirrored half; skipped blocks are 0).
+// same_ab: B is A (loaded once).
 template <typename T>
 __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const Operand A, const Operand B, int mode_a,
                                                                     int mode_b, long long rows,
-                                                                    double *__restrict__ part) {
+                                                                    double *__restrict__ part, uint64_t block_mask,
+                                                                    bool same_ab) {
   extern __shared__ __align__(32) unsigned char smem_raw[];
   const int ca = A.cols, cb = B.cols;
   const int cap = pad8(ca), cbp = pad8(cb);
   const int kSlab = slab_rows(cap, cbp);
   const int sbs = sblk_stride(kSlab);
   const int nbi = cap / 8, nbj = cbp / 8, nblk = nbi * nbj;
+  const uint64_t live = (nblk >= 64 ? ~0ull : ((1ull << nblk) - 1)) & block_mask;
+  const int nact = max(1, __popcll(live));
   const int stage_elems = (nbi + nbj) * sbs;
   T *ring = reinterpret_cast<T *>(smem_raw);
   const int red_cap = (int)((kGramStages * (size_t)stage_elems * sizeof(T)) / (sizeof(double) * cap * cbp));
-  const int split = min(kGramThreads / nblk, red_cap);  // row residue classes (≥ 1)
+  const int split = min(kGramThreads / nact, red_cap);  // row residue classes (≥ 1)
   const int t = threadIdx.x;
-  const int blk = t % nblk, grp = t / nblk;
-  const bool active = grp < split;
+  const int a_idx = t % nact, grp = t / nact;
+  const bool active = grp < split && live != 0;
+  int blk = 0;
+  {  // the a_idx-th live block
+    uint64_t m = live;
+    for (int q = 0; q < a_idx; ++q) m &= m - 1;
+    blk = m ? __ffsll((long long)m) - 1 : 0;
+  }
   const int bi = blk / nbj, bj = blk % nbj;
   const float inv_ca = 1.0f / (float)ca, inv_cb = 1.0f / (float)cb;
   for (int e = t; e < kGramStages * stage_elems; e += kGramThreads) ring[e] = T(0);  // pads stay zero
@@ -162,7 +174,7 @@ __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const Operan
       const int nr = (int)min((long long)kSlab, rows - r0);
       T *st = ring + (size_t)(k % kGramStages) * stage_elems;
       load_operand(st, A, mode_a, kSlab, r0, nr, inv_ca);
-      load_operand(st + nbi * sbs, B, mode_b, kSlab, r0, nr, inv_cb);
+      if (!same_ab) load_operand(st + nbi * sbs, B, mode_b, kSlab, r0, nr, inv_cb);
     }
     cp_async_commit();  // possibly empty group: keeps the wait arithmetic uniform
   };
@@ -176,7 +188,7 @@ __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const Operan
     const long long r0 = sl * kSlab;
     const int nr = (int)min((long long)kSlab, rows - r0);
     const T *sa = ring + (size_t)(k % kGramStages) * stage_elems + bi * sbs;
-    const T *sb = ring + (size_t)(k % kGramStages) * stage_elems + (nbi + bj) * sbs;
+    const T *sb = ring + (size_t)(k % kGramStages) * stage_elems + ((same_ab ? 0 : nbi) + bj) * sbs;
     if (active) {
       for (int r = grp; r < nr; r += split) {
         double av[8], bv[8];
@@ -204,7 +216,8 @@ __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const Operan
   for (int e = t; e < ca * cb; e += kGramThreads) {
     const int i = e / cb, j = e % cb;
     double s = 0.0;
-    for (int g = 0; g < split; ++g) s += red[(size_t)g * cap * cbp + i * cbp + j];
+    if ((live >> ((i >> 3) * nbj + (j >> 3))) & 1ull)
+      for (int g = 0; g < split; ++g) s += red[(size_t)g * cap * cbp + i * cbp + j];
     out[e] = s;
   }
 }
@@ -246,7 +259,7 @@ int bw_shift_of(int32_t bw) {
 }
 
 int gram_impl(const Operand &A, const Operand &B, long long rows, int32_t dtype, double *out, void *workspace,
-              uint64_t ws_bytes, cudaStream_t stream) {
+              uint64_t ws_bytes, cudaStream_t stream, uint64_t block_mask = ~0ull) {
   const int ca = A.cols, cb = B.cols;
   if (ca < 1 || cb < 1 || ca > kMaxCols || cb > kMaxCols)
     return cim::set_error(CIM_EINVAL, "column counts must be in [1, 64]");
@@ -260,17 +273,22 @@ int gram_impl(const Operand &A, const Operand &B, long long rows, int32_t dtype,
   const size_t es = dtype == CIM_F32 ? 4 : 8;
   const size_t smem = gram_smem(ca, cb, es);
   const int ma = load_mode(A, es), mb = load_mode(B, es);
+  const bool same_ab = A.p == B.p && A.ld == B.ld && A.bstride == B.bstride && A.bw_shift == B.bw_shift &&
+                       A.cols == B.cols;
+  if (block_mask == 0) block_mask = ~0ull;
   cudaError_t e;
   if (dtype == CIM_F32) {
     e = cudaFuncSetAttribute(gram_partial_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
       gram_partial_kernel<float><<<grid, kGramThreads, smem, stream>>>(A, B, ma, mb, rows,
-                                                                       static_cast<double *>(workspace));
+                                                                       static_cast<double *>(workspace), block_mask,
+                                                                       same_ab);
   } else {
     e = cudaFuncSetAttribute(gram_partial_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
       gram_partial_kernel<double><<<grid, kGramThreads, smem, stream>>>(A, B, ma, mb, rows,
-                                                                        static_cast<double *>(workspace));
+                                                                        static_cast<double *>(workspace), block_mask,
+                                                                        same_ab);
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return cim::set_error(CIM_ECUDA, std::string("gram_partial_kernel: ") + cudaGetErrorString(e));
@@ -298,14 +316,15 @@ extern "C" int cim_gram(const void *A, int64_t lda, int32_t ca, const void *B, i
 
 extern "C" int cim_gram_blocked(const void *A, int64_t lda, int32_t a_bw, int64_t a_bstride, int32_t ca,
                                 const void *B, int64_t ldb, int32_t b_bw, int64_t b_bstride, int32_t cb, int64_t rows,
-                                int32_t dtype, double *out, void *workspace, uint64_t ws_bytes, void *stream_) {
+                                int32_t dtype, double *out, void *workspace, uint64_t ws_bytes, uint64_t block_mask,
+                                void *stream_) {
   cim::clear_error();
   const int sa = bw_shift_of(a_bw), sb = bw_shift_of(b_bw);
   if (sa < 0 || sb < 0) return cim::set_error(CIM_EINVAL, "block widths must be 4, 8, 16, 32 or 64");
   if (lda < std::min(a_bw, ca) || ldb < std::min(b_bw, cb))
     return cim::set_error(CIM_EINVAL, "leading dimensions must cover a block");
   const Operand a{A, lda, a_bstride, sa, ca}, b{B, ldb, b_bstride, sb, cb};
-  return gram_impl(a, b, rows, dtype, out, workspace, ws_bytes, reinterpret_cast<cudaStream_t>(stream_));
+  return gram_impl(a, b, rows, dtype, out, workspace, ws_bytes, reinterpret_cast<cudaStream_t>(stream_), block_mask);
 }
 
 // ---------------------------------------------------------------------------

@@ -172,8 +172,10 @@ class _Work:
     def dense(self, s0: int, s1: int) -> torch.Tensor:
         return self.buf[s0:s1].permute(1, 0, 2).reshape(self.rows, (s1 - s0) * self.bw)
 
-    def gram(self, a0: int, a1: int, b0: int, b1: int, group) -> np.ndarray:
-        """[slots a0..a1)ᵀ·[slots b0..b1) in float64 (virtual columns), summed over ranks."""
+    def gram(self, a0: int, a1: int, b0: int, b1: int, group, block_mask: int = 0) -> np.ndarray:
+        """[slots a0..a1)ᵀ·[slots b0..b1) in float64 (virtual columns), summed over ranks.
+        ``block_mask`` (bw = 8 only): 8×8 output blocks to compute, bit
+        bi·(b1-b0) + bj; 0 = all (the others come back as 0)."""
         ca, cb = (a1 - a0) * self.bw, (b1 - b0) * self.bw
         if self._native() and ca <= 64 and cb <= 64:
             from ._lib import CIM_F32, CIM_F64, check, lib
@@ -187,7 +189,8 @@ class _Work:
                 check(L.cim_gram_blocked(self.buf[a0].data_ptr(), self.bw, self.bw, bs, ca, self.buf[b0].data_ptr(),
                                          self.bw, self.bw, bs, cb, self.rows,
                                          CIM_F32 if self.buf.dtype == torch.float32 else CIM_F64, out.data_ptr(),
-                                         ws.data_ptr(), need, torch.cuda.current_stream(self.buf.device).cuda_stream),
+                                         ws.data_ptr(), need, block_mask if self.bw == 8 else 0,
+                                         torch.cuda.current_stream(self.buf.device).cuda_stream),
                       "cim_gram_blocked")
             return _allreduce(out, group).cpu().numpy()
         if self.buf.is_cuda and (ca > 64 or cb > 64):  # wide blocks: one slot pair at a time, natively
@@ -333,9 +336,20 @@ def lobpcg(apply: Callable[[torch.Tensor], torch.Tensor], X0: torch.Tensor, *, t
         # Rayleigh–Ritz on S = [P X W] (or [X W]): one Gram pass of S against
         # all six slots gives SᵀS and SᵀAS
         sidx = cur.vidx(range(b0, Wk.AP), [m] * (Wk.W - b0) + [nw])
-        MG = cur.gram(b0, Wk.AP, Wk.P, Wk.AW + 1, group)
+        # SᵀS and SᵀAS are symmetric: compute the slot blocks on and above
+        # their diagonals only (bw = 8: one slot = one 8×8 block), mirror here
+        ns = Wk.AP - b0
+        mask = 0
+        for bi in range(ns):
+            for bj in range(bi, ns):
+                mask |= 1 << (bi * 6 + b0 + bj)
+                mask |= 1 << (bi * 6 + b0 + 3 + bj)
+        MG = cur.gram(b0, Wk.AP, Wk.P, Wk.AW + 1, group, block_mask=mask)
         M = MG[np.ix_(sidx, sidx + b0 * bw)]
         G = MG[np.ix_(sidx, sidx + (b0 + 3) * bw)]
+        if bw == 8:
+            M = np.triu(M) + np.triu(M, 1).T
+            G = np.triu(G) + np.triu(G, 1).T
         lam, C = _rayleigh_ritz(G, M, m, largest)
         # new [P | X] = S·[C_p | C] and [AP | AX] = AS·[C_p | C] into the other buffer,
         # C_p = C with its X rows zeroed (conjugate directions)

@@ -121,6 +121,11 @@ class ShardedSymSpmm:
             xl[:, : self.k_user] = X_local
         else:
             xl = X_local.contiguous()
+        if self.world == 1 and self.local_apply == self._cuda_apply and xl.data_ptr() % 16 == 0:
+            # one rank: the kernel reads X_local and writes Y_local directly
+            # (rows_per_rank = n_pad), no staging copies
+            self._cuda_apply(xl, self.Y_local)
+            return self.Y_local[:, : self.k_user]
         if self.world > 1:
             dist.all_gather_into_tensor(self.X_full, xl, group=self.group)
         else:
