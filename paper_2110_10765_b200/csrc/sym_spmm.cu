@@ -29,6 +29,13 @@
 // The reference reaches this arithmetic only as a pair walk
 // (_contract_array_clause / _contract_atomic, pipeline.py:461-488) over the
 // full COO from _collect_pairs (pipeline.py:428-458).
+//
+// Compile-time switches for A/B experiments (tools/build_variant.sh; the
+// shipped build defines none): CIM_NO_K8 (generic kernel for every k),
+// CIM_ROWFLUSH_SMEM (4-warp shared-memory row sum before the row flush),
+// CIM_DIAG_BRANCH (separate diagonal-tile body in the generic kernel),
+// CIM_K8_X_NORMAL / CIM_K8_Y_LAST (L2 policies of X copies / Y atomics).
+// Their measured effects are in profiles/r01/SUMMARY.md.
 #include <algorithm>
 #include <type_traits>
 #include <cstdlib>
