@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget for the cpu_baseline leg")
     ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--bands", type=int, default=1, help="column bands of the tile order (0 = auto)")
+    ap.add_argument("--fused", action="store_true",
+                    help="N > 1: fused apply (X / Y chunks in symmetric memory, the kernel reads / reduces peer "
+                         "chunks over NVLink) instead of NCCL all-gather + reduce-scatter")
     ap.add_argument("--csv", default=None,
                     help="also write the reference harness's 8-column CSV (cimotifs bench.py:54) to this path")
     ap.add_argument("--fill", type=float, default=None,
@@ -251,7 +254,7 @@ def impl_ours(args):
         S = ShardedSymSpmm(n, k, dtype, dev, H_local=Hs)
     else:
         S = ShardedSymSpmm.synthetic(n, k=k, p=p, seed=0, dtype=dtype, device=dev, layout=args.layout,
-                                     bands=None if args.bands == 0 else args.bands)
+                                     bands=None if args.bands == 0 else args.bands, fused=args.fused)
     H = S.H
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t_build
@@ -283,6 +286,16 @@ def impl_ours(args):
             with torch.cuda.device(dev):
                 check(lib().cim_sym_spmm(H.descriptor(), X_full.data_ptr(), S.Y_part.data_ptr(), S.k, S.k, S.k,
                                          CIM_ACCUMULATE, stream.cuda_stream), "cim_sym_spmm")
+            if timed:
+                e1.record(stream)
+                kern_ms.append((e0, e1))
+        elif S.fused:
+            # fused: events bracket copy-in, zeroing, barriers and the peer-memory kernel
+            if timed:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            S._apply_fused(X_local)
             if timed:
                 e1.record(stream)
                 kern_ms.append((e0, e1))
@@ -405,7 +418,9 @@ def impl_ours(args):
                 + (f" (all tiles sparse COO-in-tile, entry fill {args.fill})" if args.fill is not None else "")
                 + f", k={k}, values h(i XOR j; 0) on device, X ~ N(0,1)",
                 "n": n, "k": k, "stored_tiles": g_tiles, "stored_nnz": H.nnz_stored,
-                "parallelism": f"row-block shard x{world}" if world > 1 else "single GPU",
+                "parallelism": (f"row-block shard x{world}" + (" fused peer-memory apply" if S.fused else
+                                                                " NCCL all-gather/reduce-scatter"))
+                if world > 1 else "single GPU",
                 "layout": H.layout,
                 "bands": H.meta.get("bands", 1),
                 "l2": "inputs (8.3 GB per GPU) far larger than L2 (126 MB): no flush",

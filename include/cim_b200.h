@@ -282,6 +282,23 @@ CIM_API int cim_basis_fill_sparse(const uint64_t *bits_lo, const uint16_t *occ, 
 /* Device workspace bytes cim_gram / cim_gram_blocked need. */
 CIM_API uint64_t cim_gram_workspace_bytes(int64_t rows, int32_t ca, int32_t cb);
 
+/*
+ * Y += A·X with X and Y split into row chunks — the fused compute +
+ * exchange step of the multi-GPU apply: chunk c holds block rows
+ * [c·chunk_rows/64, (c+1)·chunk_rows/64) as (chunk_rows, k) row-major X
+ * (ldx = k) and (chunk_rows, ldy) Y, and the pointers may be peer-mapped
+ * memory of other GPUs (CUDA IPC / symmetric memory over NVLink): the
+ * kernel bulk-copies X_C / X_R blocks from, and red.global-adds Y blocks
+ * into, the owning rank's chunk directly — no all-gather of X, no
+ * reduce-scatter of Y.  Always accumulates (the caller zeroes every chunk
+ * and orders the ranks around the call).  n_chunks ≤ 8; dense
+ * fragment-layout tiles; (dtype, k) of the wide-register kernel (f32 k ∈
+ * {8,16,24,32,48,64}, f64 k ∈ {4,8,12,16,32}).
+ */
+CIM_API int cim_sym_spmm_chunked(const cim_half_tiles *H, const void *const *X_chunks,
+                                 void *const *Y_chunks, int32_t n_chunks, int64_t chunk_rows,
+                                 int32_t k, int64_t ldy, void *stream);
+
 /* 1 if (dtype, k) has a compiled kernel for CIM_LAYOUT_FRAG tiles, else 0. */
 CIM_API int cim_sym_spmm_supported(int32_t dtype, int32_t k);
 

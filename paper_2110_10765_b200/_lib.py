@@ -36,6 +36,7 @@ EXPORTS = (
     "cim_unpack_tiles",
     "cim_hash_values",
     "cim_sym_spmm_host_batch",
+    "cim_sym_spmm_chunked",
     "cim_host_batch_workspace_bytes",
     "cim_fill_sparse_values",
     "cim_sparse_count_rows",
@@ -131,6 +132,8 @@ def lib() -> ctypes.CDLL:
                                   c.c_void_p, c.c_void_p]
     L.cim_sym_spmm_host_batch.argtypes = [c.POINTER(CimHalfTiles), c.POINTER(c.c_void_p), c.POINTER(c.c_void_p),
                                           c.c_int32, c.c_int32, c.c_void_p, c.c_uint64]
+    L.cim_sym_spmm_chunked.argtypes = [c.POINTER(CimHalfTiles), c.POINTER(c.c_void_p), c.POINTER(c.c_void_p),
+                                       c.c_int32, c.c_int64, c.c_int32, c.c_int64, c.c_void_p]
     L.cim_host_batch_workspace_bytes.argtypes = [c.POINTER(CimHalfTiles), c.c_int32]
     L.cim_fill_sparse_values.argtypes = [c.POINTER(CimSparseTiles), c.c_int64, c.c_int32, c.c_int32, c.c_uint64,
                                          c.c_int32, c.c_void_p, c.c_void_p, c.c_void_p]

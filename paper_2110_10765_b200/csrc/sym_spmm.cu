@@ -57,6 +57,16 @@ struct __align__(16) StageHdr {
   int R, C, flags, pad;
 };
 
+// Wide-register kernel stage header: the Y row blocks this tile updates,
+// resolved by the producer (X / Y may live in per-rank chunks, possibly in
+// peer GPUs' memory — cim_sym_spmm_chunked).
+struct __align__(16) WideHdr {
+  int R, C, flags, pad;
+  unsigned char *yr, *yc;  // Y block rows of R and C (already offset to the chunk)
+};
+
+constexpr int kMaxChunks = 8;
+
 struct SpmmParams {
   const int4 *units;    // (R, t0, t1, 0)
   const int2 *tile_rc;  // (R, C)
@@ -73,6 +83,11 @@ struct SpmmParams {
   unsigned int tile_bytes;
   unsigned int xblk_bytes;  // 64·k·sizeof(T)
   unsigned int sub_bytes;   // shared memory per sub-CTA
+  // chunked X / Y (wide-register kernel): block row b lives in chunk
+  // b / chunk_blocks at block b % chunk_blocks; one chunk = plain X / Y
+  int n_chunks, chunk_blocks;
+  const unsigned char *xch[kMaxChunks];
+  unsigned char *ych[kMaxChunks];
 };
 
 template <typename T>
@@ -813,6 +828,7 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
     setmaxnreg_dec<kK8ProducerRegs>();
     if (warp >= 8 + SUBS) return;
     const int sub = warp - 8;
+    const size_t ybytes = (size_t)kBlock * p.ldy * sizeof(T);  // one Y block row
     unsigned char *smem = smem_all + (size_t)sub * p.sub_bytes;
     unsigned char *stage_base = smem;
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)S * p.stage_bytes);
@@ -845,13 +861,16 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
             const int tt = tb + q;
             const bool diag = (C == R), first = (tt == t0);
             const int flags = (first ? HDR_FIRST : 0) | (tt == t1 - 1 ? HDR_LAST : 0) | (diag ? HDR_DIAG : 0);
-            StageHdr *h = reinterpret_cast<StageHdr *>(st + tile_bytes + 2 * xblk);
-            *h = StageHdr{R, C, flags, 0};
+            const int oc = C / p.chunk_blocks, lc = C - oc * p.chunk_blocks;
+            const int orr = R / p.chunk_blocks, lr = R - orr * p.chunk_blocks;
+            WideHdr *h = reinterpret_cast<WideHdr *>(st + tile_bytes + 2 * xblk);
+            *h = WideHdr{R, C, flags, 0, p.ych[orr] + (size_t)lr * ybytes, p.ych[oc] + (size_t)lc * ybytes};
             const bool need_xr = first && !diag;  // a diagonal first tile has X_R = X_C
             mbar_arrive_expect_tx(&full[stage], tile_bytes + (need_xr ? 2 * xblk : xblk));
             bulk_g2s(st, p.vals + (size_t)tt * tile_bytes, tile_bytes, &full[stage], pol_stream);
-            bulk_g2s(st + tile_bytes, p.X + (size_t)C * xblk, xblk, &full[stage], pol_keep);
-            if (need_xr) bulk_g2s(st + tile_bytes + xblk, p.X + (size_t)R * xblk, xblk, &full[stage], pol_keep);
+            bulk_g2s(st + tile_bytes, p.xch[oc] + (size_t)lc * xblk, xblk, &full[stage], pol_keep);
+            if (need_xr)
+              bulk_g2s(st + tile_bytes + xblk, p.xch[orr] + (size_t)lr * xblk, xblk, &full[stage], pol_keep);
           }
           __syncwarp();
           if (++stage == S) {
@@ -864,8 +883,8 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
     }
     if (lane == 0) {
       mbar_wait_backoff(&empty[stage], phase ^ 1u);
-      StageHdr *h = reinterpret_cast<StageHdr *>(stage_base + (size_t)stage * p.stage_bytes + tile_bytes + 2 * xblk);
-      *h = StageHdr{0, 0, HDR_TERM, 0};
+      WideHdr *h = reinterpret_cast<WideHdr *>(stage_base + (size_t)stage * p.stage_bytes + tile_bytes + 2 * xblk);
+      *h = WideHdr{0, 0, HDR_TERM, 0, nullptr, nullptr};
       mbar_arrive(&full[stage]);
     }
     return;
@@ -882,7 +901,6 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
   const int gt = threadIdx.x & 127;  // micro-block id
   const int rg = frag_rg(gt), cg = frag_cg(gt);
   const int sw = xr_chunk_swap<8>(rg);
-  T *Y = reinterpret_cast<T *>(p.Y);
   const long long ldy = p.ldy;
 #ifdef CIM_K8_Y_LAST
   const uint64_t ypol = policy_evict_last();
@@ -901,8 +919,13 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
   while (true) {
     mbar_wait(&full[stage], phase);
     const unsigned char *st = stage_base + (size_t)stage * p.stage_bytes;
-    const StageHdr h = *reinterpret_cast<const StageHdr *>(st + tile_bytes + 2 * xblk);
-    if (h.flags & HDR_TERM) break;
+    const WideHdr h = *reinterpret_cast<const WideHdr *>(st + tile_bytes + 2 * xblk);
+    if (h.flags & HDR_TERM) {
+      // chunked (peer-memory) Y: make this thread's remote reductions visible
+      // system-wide before the kernel ends and the ranks' barrier follows
+      if (p.n_chunks > 1) __threadfence_system();
+      break;
+    }
     const T *Ts = reinterpret_cast<const T *>(st);
     const T *XC = reinterpret_cast<const T *>(st + tile_bytes);
     const bool diag = h.flags & HDR_DIAG;
@@ -956,7 +979,7 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
       phase ^= 1u;
     }
     // a diagonal tile's transposed FMAs (against X_R = X_C) are discarded
-    if (!diag) reduce_cols_wide<T>(ac, lane, cg, Y + (long long)h.C * kBlock * ldy + v0, ldy, ypol);
+    if (!diag) reduce_cols_wide<T>(ac, lane, cg, reinterpret_cast<T *>(h.yc) + v0, ldy, ypol);
     if (h.flags & HDR_LAST) {
       // rows rg + 8i over the 4 lanes sharing them: 2 butterfly steps, then
       // each lane flushes 2 rows × VPG vectors (no cross-warp barrier)
@@ -978,7 +1001,7 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
           ar[i][q] = W::add(keep, W::shfl_xor(send, 2));
         }
       const int i0 = (b0 ? 4 : 0) + (b1 ? 2 : 0);
-      T *yblk = Y + (long long)h.R * kBlock * ldy + v0;
+      T *yblk = reinterpret_cast<T *>(h.yr) + v0;
 #pragma unroll
       for (int ri = 0; ri < 2; ++ri) {
         T *yr = yblk + (long long)(rg + 8 * (i0 + ri)) * ldy;
@@ -1149,14 +1172,20 @@ int launch_kernel(const cim_half_tiles *H, const void *X, void *Y, int k, long l
   return CIM_OK;
 }
 
+struct Chunks {  // X / Y as per-rank chunks (cim_sym_spmm_chunked); n = 1: plain X / Y
+  int n = 1, blocks = 1 << 30;
+  const void *x[kMaxChunks] = {};
+  void *y[kMaxChunks] = {};
+};
+
 template <typename T, int G, int KROW>
-int launch_k8(const cim_half_tiles *H, const void *X, void *Y, long long ldy, cudaStream_t stream, DeviceState *ds) {
+int launch_k8(const cim_half_tiles *H, const Chunks &ck, long long ldy, cudaStream_t stream, DeviceState *ds) {
   static std::once_flag attr_once[64];
   constexpr int SUBS = 2 / G;
   constexpr int passes = KROW / (WideE<T>::VPG * G);
   const unsigned int tile_bytes = kTileElems * sizeof(T);
   const unsigned int xblk = kBlock * KROW * sizeof(T);
-  const unsigned int stage_bytes = (tile_bytes + 2 * xblk + sizeof(StageHdr) + 127u) & ~127u;
+  const unsigned int stage_bytes = (tile_bytes + 2 * xblk + sizeof(WideHdr) + 127u) & ~127u;
   const size_t budget = (size_t)(227 * 1024) / SUBS;
   int S = std::min((int)((budget - 128) / stage_bytes), 8);
   if (S < 2) return set_error(CIM_EUNSUPPORTED, "k too large for the k8 kernel's stages");
@@ -1179,8 +1208,8 @@ int launch_k8(const cim_half_tiles *H, const void *X, void *Y, long long ldy, cu
     p.units = reinterpret_cast<const int4 *>(H->units);
     p.tile_rc = reinterpret_cast<const int2 *>(H->tile_rc);
     p.vals = reinterpret_cast<const unsigned char *>(H->vals);
-    p.X = reinterpret_cast<const unsigned char *>(X);
-    p.Y = reinterpret_cast<unsigned char *>(Y);
+    p.X = reinterpret_cast<const unsigned char *>(ck.x[0]);
+    p.Y = reinterpret_cast<unsigned char *>(ck.y[0]);
     p.counter = ctr + ps;
     p.n_units = H->n_units;
     p.ldy = ldy;
@@ -1191,11 +1220,46 @@ int launch_k8(const cim_half_tiles *H, const void *X, void *Y, long long ldy, cu
     p.tile_bytes = tile_bytes;
     p.xblk_bytes = xblk;
     p.sub_bytes = (unsigned int)sub_bytes;
+    p.n_chunks = ck.n;
+    p.chunk_blocks = ck.blocks;
+    for (int c = 0; c < kMaxChunks; ++c) {
+      p.xch[c] = reinterpret_cast<const unsigned char *>(ck.x[c < ck.n ? c : 0]);
+      p.ych[c] = reinterpret_cast<unsigned char *>(ck.y[c < ck.n ? c : 0]);
+    }
     sym_spmm_k8_kernel<T, G, KROW><<<(unsigned int)grid, kK8Threads, smem, stream>>>(p);
     e = cudaGetLastError();
     if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("sym_spmm_k8 launch: ") + cudaGetErrorString(e));
   }
   return CIM_OK;
+}
+
+// The wide-register kernel for (dtype, k), or EUNSUPPORTED.
+int launch_wide(const cim_half_tiles *H, int k, const Chunks &ck, long long ldy, cudaStream_t stream,
+                DeviceState *ds) {
+  if (H->dtype == CIM_F32) {
+    switch (k) {
+      case 8: return launch_k8<float, 1, 8>(H, ck, ldy, stream, ds);
+      case 16: return launch_k8<float, 2, 16>(H, ck, ldy, stream, ds);
+      case 24: return launch_k8<float, 1, 24>(H, ck, ldy, stream, ds);
+      case 32: return launch_k8<float, 2, 32>(H, ck, ldy, stream, ds);
+      case 48: return launch_k8<float, 2, 48>(H, ck, ldy, stream, ds);
+      case 64: return launch_k8<float, 2, 64>(H, ck, ldy, stream, ds);
+    }
+  } else {
+    switch (k) {
+      case 4: return launch_k8<double, 1, 4>(H, ck, ldy, stream, ds);
+      case 8: return launch_k8<double, 2, 8>(H, ck, ldy, stream, ds);
+      case 12: return launch_k8<double, 1, 12>(H, ck, ldy, stream, ds);
+      case 16: return launch_k8<double, 2, 16>(H, ck, ldy, stream, ds);
+      case 32: return launch_k8<double, 2, 32>(H, ck, ldy, stream, ds);
+    }
+  }
+  return CIM_EUNSUPPORTED;
+}
+
+bool wide_supported(int dtype, int k) {
+  if (dtype == CIM_F32) return k == 8 || k == 16 || k == 24 || k == 32 || k == 48 || k == 64;
+  return k == 4 || k == 8 || k == 12 || k == 16 || k == 32;
 }
 
 }  // namespace
@@ -1270,6 +1334,14 @@ static int sym_spmm_dense(const cim_half_tiles *H, const void *X, void *Y, int32
     return sym_spmm_tc_dispatch(H, X, Y, k, ldy, stream, ds->sms, take_counters(ds, 1));
   }
 
+#ifndef CIM_NO_K8
+  if (H->layout == CIM_LAYOUT_FRAG && wide_supported(H->dtype, k)) {
+    Chunks ck;
+    ck.x[0] = X;
+    ck.y[0] = Y;
+    return launch_wide(H, k, ck, ldy, stream, ds);
+  }
+#endif
   if (H->dtype == CIM_F32) {
     switch (cfg.KV * 10 + cfg.NG) {
       case 11:
@@ -1288,19 +1360,9 @@ static int sym_spmm_dense(const cim_half_tiles *H, const void *X, void *Y, int32
         if (k == 8) return launch_kernel<float, 2, 4, 8>(H, X, Y, k, ldy, cfg.passes, stream, ds);
         return launch_kernel<float, 2, 4>(H, X, Y, k, ldy, cfg.passes, stream, ds);
       case 81:
-#ifndef CIM_NO_K8
-        if (k == 8) return launch_k8<float, 1, 8>(H, X, Y, ldy, stream, ds);
-        if (k == 24) return launch_k8<float, 1, 24>(H, X, Y, ldy, stream, ds);
-#endif
         if (k == 8) return launch_kernel<float, 8, 1, 8>(H, X, Y, k, ldy, cfg.passes, stream, ds);
         return launch_kernel<float, 8, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
       case 82:
-#ifndef CIM_NO_K8
-        if (k == 16) return launch_k8<float, 2, 16>(H, X, Y, ldy, stream, ds);
-        if (k == 32) return launch_k8<float, 2, 32>(H, X, Y, ldy, stream, ds);
-        if (k == 48) return launch_k8<float, 2, 48>(H, X, Y, ldy, stream, ds);
-        if (k == 64) return launch_k8<float, 2, 64>(H, X, Y, ldy, stream, ds);
-#endif
         if (k == 16) return launch_kernel<float, 8, 2, 16>(H, X, Y, k, ldy, cfg.passes, stream, ds);
         return launch_kernel<float, 8, 2>(H, X, Y, k, ldy, cfg.passes, stream, ds);
     }
@@ -1313,18 +1375,9 @@ static int sym_spmm_dense(const cim_half_tiles *H, const void *X, void *Y, int32
         if (k == 2) return launch_kernel<double, 2, 1, 2>(H, X, Y, k, ldy, cfg.passes, stream, ds);
         return launch_kernel<double, 2, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
       case 41:
-#ifndef CIM_NO_K8
-        if (k == 4) return launch_k8<double, 1, 4>(H, X, Y, ldy, stream, ds);
-        if (k == 12) return launch_k8<double, 1, 12>(H, X, Y, ldy, stream, ds);
-#endif
         if (k == 4) return launch_kernel<double, 4, 1, 4>(H, X, Y, k, ldy, cfg.passes, stream, ds);
         return launch_kernel<double, 4, 1>(H, X, Y, k, ldy, cfg.passes, stream, ds);
       case 42:
-#ifndef CIM_NO_K8
-        if (k == 8) return launch_k8<double, 2, 8>(H, X, Y, ldy, stream, ds);
-        if (k == 16) return launch_k8<double, 2, 16>(H, X, Y, ldy, stream, ds);
-        if (k == 32) return launch_k8<double, 2, 32>(H, X, Y, ldy, stream, ds);
-#endif
         if (k == 8) return launch_kernel<double, 4, 2, 8>(H, X, Y, k, ldy, cfg.passes, stream, ds);
         return launch_kernel<double, 4, 2>(H, X, Y, k, ldy, cfg.passes, stream, ds);
     }
@@ -1337,4 +1390,36 @@ extern "C" int cim_sym_spmm(const cim_half_tiles *H, const void *X, void *Y, int
   const int rc = sym_spmm_dense(H, X, Y, k, ldx, ldy, flags, stream_);
   if (rc != CIM_OK || (flags & CIM_DETERMINISTIC) || !H->sparse || H->sparse->n_tiles == 0) return rc;
   return sym_spmm_sparse(H->sparse, H->dtype, X, Y, k, ldx, ldy, reinterpret_cast<cudaStream_t>(stream_));
+}
+
+extern "C" int cim_sym_spmm_chunked(const cim_half_tiles *H, const void *const *X_chunks, void *const *Y_chunks,
+                                    int32_t n_chunks, int64_t chunk_rows, int32_t k, int64_t ldy, void *stream_) {
+  clear_error();
+  if (!H) return set_error(CIM_EINVAL, "H is NULL");
+  if (n_chunks < 1 || n_chunks > kMaxChunks) return set_error(CIM_EINVAL, "n_chunks must be in [1, 8]");
+  if (chunk_rows < kBlock || chunk_rows % kBlock) return set_error(CIM_EINVAL, "chunk_rows must be a positive multiple of 64");
+  if (!X_chunks || !Y_chunks) return set_error(CIM_EINVAL, "chunk arrays are NULL");
+  const int64_t nb = (H->n + kBlock - 1) / kBlock;
+  if ((int64_t)n_chunks * (chunk_rows / kBlock) < nb) return set_error(CIM_EINVAL, "chunks do not cover the matrix rows");
+  if (H->layout != CIM_LAYOUT_FRAG) return set_error(CIM_EUNSUPPORTED, "chunked apply needs fragment-layout tiles");
+  if (H->sparse && H->sparse->n_tiles > 0) return set_error(CIM_EUNSUPPORTED, "chunked apply: dense tiles only");
+  if (!wide_supported(H->dtype, k)) return set_error(CIM_EUNSUPPORTED, "chunked apply: (dtype, k) has no wide kernel");
+  if (ldy < k) return set_error(CIM_EINVAL, "ldy must be >= k");
+  const size_t es = H->dtype == CIM_F32 ? 4 : 8;
+  Chunks ck;
+  ck.n = n_chunks;
+  ck.blocks = (int)(chunk_rows / kBlock);
+  for (int c = 0; c < n_chunks; ++c) {
+    if (!X_chunks[c] || !Y_chunks[c]) return set_error(CIM_EINVAL, "NULL chunk pointer");
+    if ((reinterpret_cast<uintptr_t>(X_chunks[c]) & 15) || (reinterpret_cast<uintptr_t>(Y_chunks[c]) & 15))
+      return set_error(CIM_EINVAL, "chunks must be 16-byte aligned");
+    ck.x[c] = X_chunks[c];
+    ck.y[c] = Y_chunks[c];
+  }
+  if ((ldy * (int64_t)es) % 16) return set_error(CIM_EINVAL, "ldy*sizeof(T) must be a multiple of 16");
+  DeviceState *ds = nullptr;
+  int rc = device_state(&ds);
+  if (rc) return rc;
+  if (H->n_tiles == 0 || H->n_units == 0) return CIM_OK;
+  return launch_wide(H, k, ck, ldy, reinterpret_cast<cudaStream_t>(stream_), ds);
 }

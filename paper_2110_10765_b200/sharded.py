@@ -23,7 +23,9 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from ._lib import BLOCK
+import ctypes
+
+from ._lib import BLOCK, check, lib
 from .halftiles import HalfTiles, partition_units, plan_units, synthetic_pattern
 from .spmm import _launch, padded_k
 
@@ -44,6 +46,25 @@ def shard_tile_range(units: np.ndarray, world: int, rank: int) -> tuple[int, int
     return lo, hi, 0, 0
 
 
+def sym_spmm_chunked(H: HalfTiles, X_chunks, Y_chunks, chunk_rows: int, k: int | None = None, stream=None) -> None:
+    """Y += A·X with X and Y given as row chunks (``cim_sym_spmm_chunked``):
+    chunk c holds rows [c·chunk_rows, (c+1)·chunk_rows).  The chunks may be
+    tensors on this GPU or raw device pointers into peer GPUs' memory (the
+    fused multi-GPU apply); no chunk is zeroed."""
+    ptr = lambda t: t if isinstance(t, int) else t.data_ptr()  # noqa: E731
+    n = len(X_chunks)
+    if n != len(Y_chunks) or not 1 <= n <= 8:
+        raise ValueError("need 1..8 X and Y chunks, equally many")
+    if k is None:
+        k = X_chunks[0].shape[1]
+    xp = (ctypes.c_void_p * n)(*[ptr(t) for t in X_chunks])
+    yp = (ctypes.c_void_p * n)(*[ptr(t) for t in Y_chunks])
+    s = stream if stream is not None else torch.cuda.current_stream(H.device)
+    handle = s.cuda_stream if isinstance(s, torch.cuda.Stream) else int(s)
+    with torch.cuda.device(H.device):
+        check(lib().cim_sym_spmm_chunked(H.descriptor(), xp, yp, n, chunk_rows, k, k, handle), "cim_sym_spmm_chunked")
+
+
 class ShardedSymSpmm:
     """Distributed ``Y = A·X`` with A's tiles row-block sharded over ranks.
 
@@ -54,7 +75,7 @@ class ShardedSymSpmm:
     """
 
     def __init__(self, n: int, k: int, dtype: torch.dtype, device, H_local: HalfTiles | None = None,
-                 group=None, local_apply: Callable | None = None):
+                 group=None, local_apply: Callable | None = None, fused: bool = False):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -76,12 +97,42 @@ class ShardedSymSpmm:
         self.Y_part = torch.zeros((self.rows_total, self.k), dtype=dtype, device=self.device)
         self.Y_local = torch.zeros((self.rows_per_rank, self.k), dtype=dtype, device=self.device)
         self.n_pad = ((self.n + BLOCK - 1) // BLOCK) * BLOCK
+        self.fused = bool(fused) and self.world > 1 and local_apply == self._cuda_apply
+        if self.fused:
+            self._setup_fused()
+
+    # ------------------------------------------------------------ fused path
+    def _setup_fused(self) -> None:
+        """Symmetric-memory X / Y chunks (one per rank, peer-mapped over
+        NVLink) for the fused apply: the kernel reads X_C / X_R blocks from
+        and reduces Y blocks into the owning rank's chunk directly."""
+        import torch.distributed._symmetric_memory as symm_mem
+
+        if self.world > 8:
+            raise ValueError("the fused apply supports up to 8 ranks (one NVLink domain)")
+        group = self.group if self.group is not None else dist.group.WORLD
+        self.Xs = symm_mem.empty(self.rows_per_rank, self.k, dtype=self.dtype, device=self.device)
+        self.Ys = symm_mem.empty(self.rows_per_rank, self.k, dtype=self.dtype, device=self.device)
+        self.hx = symm_mem.rendezvous(self.Xs, group)
+        self.hy = symm_mem.rendezvous(self.Ys, group)
+        shape = (self.rows_per_rank, self.k)
+        self.x_ptrs = [self.hx.get_remote_tensor(r, shape, self.dtype).data_ptr() for r in range(self.world)]
+        self.y_ptrs = [self.hy.get_remote_tensor(r, shape, self.dtype).data_ptr() for r in range(self.world)]
+
+    def _apply_fused(self, xl: torch.Tensor) -> torch.Tensor:
+        self.Xs.copy_(xl)
+        self.Ys.zero_()
+        self.hy.barrier(channel=0)  # every rank's X chunk written and Y chunk zeroed
+        sym_spmm_chunked(self.H, self.x_ptrs, self.y_ptrs, self.rows_per_rank, self.k)
+        self.hy.barrier(channel=0)  # every rank's reductions into my chunk have landed
+        return self.Ys[:, : self.k_user]
 
     # ------------------------------------------------------------------ build
     @classmethod
     def synthetic(cls, n: int, *, k: int, p: float | None = None, n_off: int | None = None, seed: int = 0,
                   value_seed: int = 0, dtype=torch.float32, device=None, group=None, max_unit: int = 32,
-                  values: str = "h_xor", layout: str | None = None, bands: int | None = 1) -> "ShardedSymSpmm":
+                  values: str = "h_xor", layout: str | None = None, bands: int | None = 1,
+                  fused: bool = False) -> "ShardedSymSpmm":
         """Every rank draws the same global tile pattern (seeded), keeps its
         balanced panel, and generates only its own tile values on its GPU."""
         world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -98,7 +149,7 @@ class ShardedSymSpmm:
                                 device=device, max_unit=max_unit, layout=layout, bands=bands)
         H.meta.update(global_tiles=int(rc.shape[0]), global_off_tiles=int(np.count_nonzero(rc[:, 0] != rc[:, 1])),
                       p=p, seed=seed)
-        return cls(n, k, dtype, device, H_local=H, group=group)
+        return cls(n, k, dtype, device, H_local=H, group=group, fused=fused)
 
     # ------------------------------------------------------------------ apply
     def _cuda_apply(self, X_full: torch.Tensor, Y_part: torch.Tensor) -> None:
@@ -121,6 +172,8 @@ class ShardedSymSpmm:
             xl[:, : self.k_user] = X_local
         else:
             xl = X_local.contiguous()
+        if self.fused:
+            return self._apply_fused(xl)
         if self.world == 1 and self.local_apply == self._cuda_apply and xl.data_ptr() % 16 == 0:
             # one rank: the kernel reads X_local and writes Y_local directly
             # (rows_per_rank = n_pad), no staging copies

@@ -586,3 +586,34 @@ def test_from_basis_matches_reference_build(pkg, name, dense_fill):
     Y = pkg.sym_spmm(H, X).cpu().numpy()
     rel = np.linalg.norm(Y - f["Y_ref"]) / np.linalg.norm(f["Y_ref"])
     assert rel <= 1e-5
+
+
+@pytest.mark.parametrize("dtype,k", [(torch.float32, 8), (torch.float32, 16), (torch.float64, 8)])
+@pytest.mark.parametrize("world", [1, 3, 8])
+def test_chunked_apply_virtual_ranks(pkg, dtype, k, world):
+    """cim_sym_spmm_chunked — the fused multi-GPU apply's kernel — on one GPU
+    with `world` virtual ranks: each rank's balanced panel of tiles runs
+    against X / Y split into per-rank row chunks (separate allocations, as
+    peer-mapped chunks would be); the assembled Y must match the oracle."""
+    from paper_2110_10765_b200.sharded import row_chunks, shard_tile_range, sym_spmm_chunked
+
+    n = 4096 - 37
+    nb = (n + 63) // 64
+    rc = pkg.synthetic_pattern(nb, 0.2, seed=7)
+    units = pkg.plan_units(rc, nb, max_unit=5)
+    per, total = row_chunks(n, world)
+    g = torch.Generator().manual_seed(world + k)
+    X = torch.randn((total, k), generator=g, dtype=dtype)
+    X[n:] = 0
+    Xc = [X[c * per:(c + 1) * per].clone().cuda() for c in range(world)]
+    Yc = [torch.zeros((per, k), dtype=dtype, device="cuda") for _ in range(world)]
+    for r in range(world):
+        _, _, t0, t1 = shard_tile_range(units, world, r)
+        if t1 > t0:
+            H = pkg.HalfTiles.synthetic(n, tile_rc=rc[t0:t1], dtype=dtype, max_unit=5)
+            sym_spmm_chunked(H, Xc, Yc, per)
+    Y = torch.cat([y.cpu() for y in Yc])[:n].numpy()
+    tiles = oracle.synthetic_dense_tiles(n, rc, seed=0)
+    check_result(n, rc, tiles if dtype == torch.float32 else tiles.astype(np.float64), X[:n].numpy(), Y, dtype)
+    with pytest.raises(ValueError):
+        sym_spmm_chunked(H, Xc[:1], Yc[:1], 64)  # chunks must cover the rows
