@@ -138,12 +138,12 @@ __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const Operan
   extern __shared__ __align__(32) unsigned char smem_raw[];
   const int ca = A.cols, cb = B.cols;
   const int cap = pad8(ca), cbp = pad8(cb);
-  const int kSlab = slab_rows(cap, cbp);
+  const int kSlab = slab_rows(cap, same_ab ? 0 : cbp);  // B == A: only A is staged, so slabs grow
   const int sbs = sblk_stride(kSlab);
   const int nbi = cap / 8, nbj = cbp / 8, nblk = nbi * nbj;
   const uint64_t live = (nblk >= 64 ? ~0ull : ((1ull << nblk) - 1)) & block_mask;
   const int nact = max(1, __popcll(live));
-  const int stage_elems = (nbi + nbj) * sbs;
+  const int stage_elems = (nbi + (same_ab ? 0 : nbj)) * sbs;
   T *ring = reinterpret_cast<T *>(smem_raw);
   const int red_cap = (int)((kGramStages * (size_t)stage_elems * sizeof(T)) / (sizeof(double) * cap * cbp));
   const int split = min(kGramThreads / nact, red_cap);  // row residue classes (≥ 1)
@@ -230,8 +230,8 @@ __global__ void gram_sum_kernel(const double *__restrict__ part, int nparts, int
   out[e] = s;
 }
 
-size_t gram_smem(int ca, int cb, size_t es) {
-  const int cap = pad8(ca), cbp = pad8(cb);
+size_t gram_smem(int ca, int cb, size_t es, bool same_ab = false) {
+  const int cap = pad8(ca), cbp = same_ab ? 0 : pad8(cb);
   return (size_t)kGramStages * ((cap + cbp) / 8) * sblk_stride(slab_rows(cap, cbp)) * es;
 }
 
@@ -243,11 +243,11 @@ int load_mode(const Operand &o, size_t es) {
   return 2;
 }
 
-int gram_grid(long long rows, int ca, int cb) {
+int gram_grid(long long rows, int ca, int cb, bool same_ab = false) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int kSlab = slab_rows(pad8(ca), pad8(cb));
+  const int kSlab = slab_rows(pad8(ca), same_ab ? 0 : pad8(cb));
   const long long slabs = (rows + kSlab - 1) / kSlab;
   return (int)std::min<long long>(slabs > 0 ? slabs : 1, 2LL * sms);
 }
@@ -266,15 +266,15 @@ int gram_impl(const Operand &A, const Operand &B, long long rows, int32_t dtype,
   if (rows < 0) return cim::set_error(CIM_EINVAL, "rows must be >= 0");
   if (dtype != CIM_F32 && dtype != CIM_F64) return cim::set_error(CIM_EINVAL, "dtype must be CIM_F32 or CIM_F64");
   if (!out || (rows > 0 && (!A.p || !B.p))) return cim::set_error(CIM_EINVAL, "NULL pointer");
-  const int grid = gram_grid(rows, ca, cb);
+  const size_t es = dtype == CIM_F32 ? 4 : 8;
+  const bool same_ab = A.p == B.p && A.ld == B.ld && A.bstride == B.bstride && A.bw_shift == B.bw_shift &&
+                       A.cols == B.cols;
+  const int grid = gram_grid(rows, ca, cb, same_ab);  // ≤ the grid cim_gram_workspace_bytes assumed
   const uint64_t need = (uint64_t)grid * ca * cb * sizeof(double);
   if (!workspace || ws_bytes < need)
     return cim::set_error(CIM_EINVAL, "workspace must hold " + std::to_string(need) + " bytes");
-  const size_t es = dtype == CIM_F32 ? 4 : 8;
-  const size_t smem = gram_smem(ca, cb, es);
+  const size_t smem = gram_smem(ca, cb, es, same_ab);
   const int ma = load_mode(A, es), mb = load_mode(B, es);
-  const bool same_ab = A.p == B.p && A.ld == B.ld && A.bstride == B.bstride && A.bw_shift == B.bw_shift &&
-                       A.cols == B.cols;
   if (block_mask == 0) block_mask = ~0ull;
   cudaError_t e;
   if (dtype == CIM_F32) {
