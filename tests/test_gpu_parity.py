@@ -173,7 +173,7 @@ def c1_small(pkg):
 
 
 @pytest.mark.parametrize("layout", F32_LAYOUTS)
-@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 8, 16, 24, 32])
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 8, 16, 24, 32, 40, 48, 64])
 def test_k_sweep_f32(pkg, c1_small, k, layout):
     n, rc, tiles = c1_small
     H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=torch.float32, layout=layout)
