@@ -122,7 +122,11 @@ class ClockSampler:
                     r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
                 except Exception:
                     r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                self.samples.append((sm, r))
+                try:
+                    w = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                except Exception:
+                    w = float("nan")
+                self.samples.append((sm, r, w))
                 self._stop.wait(0.01)
         except Exception as ex:  # report, never fail the bench
             self.err = str(ex)
@@ -139,12 +143,14 @@ class ClockSampler:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [f"unavailable: {self.err}"]}
         reasons = set()
-        for _, r in self.samples:
+        for _, r, _ in self.samples:
             for bit, name in self.REASONS.items():
                 if r & bit:
                     reasons.add(name)
-        return {"sm_mhz": float(np.median([s for s, _ in self.samples])), "sm_max_mhz": float(self.max_mhz),
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+        watts = [w for _, _, w in self.samples if w == w]
+        return {"sm_mhz": float(np.median([s for s, _, _ in self.samples])), "sm_max_mhz": float(self.max_mhz),
+                "reasons": sorted(reasons), "samples": len(self.samples),
+                "power_w_median": float(np.median(watts)) if watts else None}
 
 
 # -----------------------------------------------------------------------------

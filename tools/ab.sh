@@ -9,7 +9,7 @@ for v in ${VARIANTS:-main}; do
     echo "$v parity: $(tail -1 gpurun_out/ab_pytest_$v.txt)"
   fi
   for rep in 1 2; do
-    CIM_B200_LIB=$L timeout 300 python bench.py --steps 50 --warmup 5 --no-cpu-baseline --e2e-steps 1 "$@" > gpurun_out/ab_$v.json 2> gpurun_out/ab_$v.err
-    python -c "import json;d=json.load(open('gpurun_out/ab_$v.json'));print('$v', round(d['roofline']['kernel_ms'],4), 'ms', round(d['roofline']['frac'],4), d['clocks']['sm_mhz'], d['clocks']['reasons'])" || tail -3 gpurun_out/ab_$v.err
+    CIM_B200_LIB=$L timeout 300 python bench.py --steps ${STEPS:-50} --warmup 5 --no-cpu-baseline --e2e-steps 1 "$@" > gpurun_out/ab_$v.json 2> gpurun_out/ab_$v.err
+    python -c "import json;d=json.load(open('gpurun_out/ab_$v.json'));print('$v', round(d['roofline']['kernel_ms'],4), 'ms', round(d['roofline']['frac'],4), d['clocks']['sm_mhz'], d['clocks'].get('power_w_median'), d['clocks']['reasons'])" || tail -3 gpurun_out/ab_$v.err
   done
 done
