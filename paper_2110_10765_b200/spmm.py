@@ -19,7 +19,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from ._lib import BLOCK, CIM_ACCUMULATE, CIM_DETERMINISTIC, check, lib
+from ._lib import CIM_ACCUMULATE, CIM_DETERMINISTIC, check, lib
 from .halftiles import HalfTiles
 
 LAYOUTS = ("auto", "nk", "kn")

@@ -4,7 +4,6 @@ Markers: ``gpu`` — needs a CUDA device (run on the B200 box with ``-m gpu``).
 Everything else runs on CPU in a few minutes.
 """
 
-import os
 import sys
 from pathlib import Path
 
