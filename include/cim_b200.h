@@ -71,7 +71,7 @@ extern "C" {
 #define CIM_DETERMINISTIC 2u  /* no float atomics: every Y row block summed
                                  in a fixed order by one CTA (bitwise
                                  reproducible; needs the det_* tile lists,
-                                 dense fragment-layout tiles only; reads each
+                                 fragment-layout tiles; reads each        
                                  tile twice — a validation mode)           */
 
 /* value kinds for cim_fill_synthetic_values */
@@ -136,7 +136,8 @@ typedef struct cim_half_tiles {
                                      never both); device arrays              */
   /* CIM_DETERMINISTIC only (else NULL): per block row b, the tiles with
      R == b (det_row_tiles[det_row_ptr[b] .. det_row_ptr[b+1]]) and the
-     tiles with C == b, R < b (det_col_*), each list in (R, C) order.     */
+     tiles with C == b, R < b (det_col_*), each list in (R, C) order.
+     Entries t < n_tiles name dense tiles, n_tiles + s sparse tile s.      */
   const int64_t *det_row_ptr;   /* [nb+1] */
   const int32_t *det_row_tiles;
   const int64_t *det_col_ptr;   /* [nb+1] */

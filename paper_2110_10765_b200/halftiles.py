@@ -417,15 +417,20 @@ class HalfTiles:
             )
             if self._det is not None:
                 d = self._desc
-                d.det_row_ptr, d.det_row_tiles, d.det_col_ptr, d.det_col_tiles = (t.data_ptr() for t in self._det)
+                d.det_row_ptr, d.det_row_tiles, d.det_col_ptr, d.det_col_tiles = (t.data_ptr() for t in self._det[:4])
         return self._desc
 
     def enable_deterministic(self) -> None:
         """Build the per-block-row tile lists CIM_DETERMINISTIC reads (device):
-        tiles with R == b and tiles with C == b, R < b, each in (R, C) order."""
-        if self._det is not None:
+        tiles with R == b and tiles with C == b, R < b, each in (R, C) order;
+        sparse tile s appears as ``n_tiles + s``."""
+        n_sp = self.sparse.n_tiles if self.sparse is not None else 0
+        if self._det is not None and self._det[4] == n_sp:
             return
-        rc = self.tile_rc_host.astype(np.int64)
+        rc = self.tile_rc_host.astype(np.int64).reshape(-1, 2)
+        if self.sparse is not None and self.sparse.n_tiles:
+            # one id space: dense tile t, sparse tile n_tiles + s
+            rc = np.concatenate([rc, self.sparse.tile_rc_host.astype(np.int64).reshape(-1, 2)])
         nb = self.nb
         by_row = np.lexsort((rc[:, 1], rc[:, 0]))
         row_ptr = np.searchsorted(rc[by_row, 0], np.arange(nb + 1), side="left").astype(np.int64)
@@ -434,7 +439,7 @@ class HalfTiles:
         col_ptr = np.searchsorted(rc[by_col, 1], np.arange(nb + 1), side="left").astype(np.int64)
         dev = self.device
         mk = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt) if a.size else np.zeros(1, dt)).to(dev)  # noqa: E731
-        self._det = (mk(row_ptr, np.int64), mk(by_row, np.int32), mk(col_ptr, np.int64), mk(by_col, np.int32))
+        self._det = (mk(row_ptr, np.int64), mk(by_row, np.int32), mk(col_ptr, np.int64), mk(by_col, np.int32), n_sp)
         self._desc = None
 
     def _workspace(self, nbytes: int) -> torch.Tensor:

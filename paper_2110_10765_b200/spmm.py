@@ -89,7 +89,8 @@ def sym_spmm(H: HalfTiles, X, out=None, *, layout: str = "auto", accumulate: boo
     layout : "auto" | "nk" | "kn"
     stream : torch.cuda.Stream or raw cudaStream_t handle (default: current)
     deterministic : no float atomics — bitwise reproducible Y (CIM_DETERMINISTIC;
-        dense fragment-layout tiles; a validation mode, ~2× the traffic)
+        fragment-layout dense and sparse tiles; a validation mode, ~2× the
+        traffic)
     """
     if not isinstance(H, HalfTiles):
         raise ValueError(f"H must be a HalfTiles, got {type(H).__name__}")

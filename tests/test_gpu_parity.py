@@ -520,6 +520,13 @@ def test_sparse_tiles_vs_oracle(pkg, dtype, fill, k):
     if k in (4, 8):
         Yb = pkg.sym_spmm_host_batch(H_mix, [X.pin_memory()])[0]
         assert (Yb.cuda() - Y1).abs().max().item() <= 1e-5 * Y1.abs().max().item() + 1e-6
+    # CIM_DETERMINISTIC over sparse tiles: rows / columns walked in stored
+    # (ascending) order, so every storage split gives the same bits as the
+    # all-dense walk (a zero tile element adds +0 exactly)
+    Yd = [pkg.sym_spmm(H, X.cuda(), deterministic=True) for H in (H_dn, H_mix, H_sp)]
+    check_result(n, rc_all, tiles.astype(np.float64), X.numpy(), Yd[1].cpu().numpy(), dtype)
+    assert torch.equal(Yd[0], Yd[1]) and torch.equal(Yd[0], Yd[2])
+    assert torch.equal(Yd[2], pkg.sym_spmm(H_sp, X.cuda(), deterministic=True))
 
 
 @pytest.mark.parametrize("fill", [0.05, 0.17, 0.6])
@@ -586,6 +593,9 @@ def test_from_basis_matches_reference_build(pkg, name, dense_fill):
     Y = pkg.sym_spmm(H, X).cpu().numpy()
     rel = np.linalg.norm(Y - f["Y_ref"]) / np.linalg.norm(f["Y_ref"])
     assert rel <= 1e-5
+    Yd = pkg.sym_spmm(H, X, deterministic=True)
+    assert torch.equal(Yd, pkg.sym_spmm(H, X, deterministic=True))
+    assert np.linalg.norm(Yd.cpu().numpy() - f["Y_ref"]) / np.linalg.norm(f["Y_ref"]) <= 1e-5
 
 
 @pytest.mark.parametrize("dtype,k", [(torch.float32, 8), (torch.float32, 16), (torch.float64, 8)])
