@@ -360,6 +360,22 @@ CIM_API int cim_fill_masked_values(const int32_t *tile_rc, int64_t n_tiles, int6
                                    void *stream);
 
 /*
+ * Device: the observables contraction in one tile walk (
+ * replaces contract_observables' kernels, pipeline.py:461-570):
+ *   accum[v*m_ops + k] (+)= Σ_(i,j) c[i*n_vec + v] · O_ij(k) · c[j*n_vec + v]
+ * over the full symmetric pattern of H (its nonzero stored elements, dense and
+ * sparse tiles; off-diagonal tiles count for both (i,j) and (j,i)), with
+ * O_ij(k) computed on the fly: kind CIM_VALUES_OP_HASH (_op_value,
+ * pipeline.py:224-232) or CIM_VALUES_IDENTITY.  c is f32 (n, n_vec)
+ * row-major on the device, accum f64 (n_vec, m_ops) on the device, zeroed
+ * first unless flags has CIM_ACCUMULATE.  Stream-ordered; accum is summed with
+ * f64 atomics (reproducible to rounding).
+ */
+CIM_API int cim_contract_observables(const cim_half_tiles *H, const float *c, int32_t n_vec,
+                                     int32_t m_ops, int32_t kind, uint64_t seed, double *accum,
+                                     uint32_t flags, void *stream);
+
+/*
  * Device: repack row-major dense tiles src[n_tiles][64][64] into fragment
  * order dst (same dtype).  The repacking layer's device half
  * (SURVEY.md §7 step 4).

@@ -50,6 +50,7 @@ EXPORTS = (
     "cim_tsmm",
     "cim_gram_blocked",
     "cim_tsmm_blocked",
+    "cim_contract_observables",
 )
 
 
@@ -126,6 +127,8 @@ def lib() -> ctypes.CDLL:
                                             c.c_uint64, c.c_int32, c.c_void_p, c.c_void_p]
     L.cim_fill_masked_values.argtypes = [c.c_void_p, c.c_int64, c.c_int64, c.c_int32, c.c_int32, c.c_int32,
                                          c.c_uint64, c.c_int32, c.c_void_p, c.c_void_p, c.c_void_p]
+    L.cim_contract_observables.argtypes = [c.POINTER(CimHalfTiles), c.c_void_p, c.c_int32, c.c_int32, c.c_int32,
+                                           c.c_uint64, c.c_void_p, c.c_uint32, c.c_void_p]
     L.cim_pack_tiles.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_int32, c.c_void_p, c.c_void_p]
     L.cim_unpack_tiles.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_int32, c.c_void_p, c.c_void_p]
     L.cim_hash_values.argtypes = [c.c_void_p, c.c_void_p, c.c_int64, c.c_int32, c.c_uint64, c.c_int32,

@@ -65,12 +65,13 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {  // pipeline.py
   return z ^ (z >> 31);
 }
 
-// top 53 bits → [0,1) → [-1,1), computed exactly in f64, rounded once to f32
-// (pipeline.py:212-215).
+// top 53 bits → [0,1) → [-1,1), rounded once to f32 (pipeline.py:212-215).
+// The reference's f64 value m·2⁻⁵³·2 − 1 (m = u >> 11) is exactly
+// (m − 2⁵²)·2⁻⁵², so one int64 → f32 round-to-nearest conversion and an exact
+// power-of-two scale give the same bits without f64 arithmetic.
 __host__ __device__ __forceinline__ float to_unit(uint64_t u) {
-  double d = static_cast<double>(u >> 11) * 0x1p-53;
-  d = d * 2.0 - 1.0;
-  return static_cast<float>(d);
+  const long long s = static_cast<long long>(u >> 11) - (1ll << 52);
+  return static_cast<float>(s) * 0x1p-52f;
 }
 
 __host__ __device__ __forceinline__ float h_value(uint64_t i, uint64_t j, uint64_t seed) {  // :218-221

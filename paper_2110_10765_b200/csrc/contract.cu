@@ -1,0 +1,268 @@
+// The observables contraction fused into one tile walk:
+//
+//   accum[v, k] = Σ_(i,j) c[v,i] · O_ij(k) · c[v,j]
+//
+// over the full symmetric pattern of a stored HalfTiles (contract_observables,
+// pipeline.py:534-570; kernels _contract_array_clause / _contract_atomic,
+// :461-531).  O_ij(k) is the reference's symmetric hash (_op_value,
+// pipeline.py:224-232) or the identity, computed on the fly — nothing is
+// materialised.  The pattern is the set of nonzero stored elements; an
+// off-diagonal tile (R < C) stands for its pairs and their mirror images
+// (weight 2, O and the c-products are symmetric), a diagonal tile is stored in
+// full (weight 1).
+//
+// One CTA (256 threads) walks tiles in a grid-stride loop.  Per tile the CTA
+// turns the stored values (dense fragment / tc layout, or COO-in-tile sparse
+// entries) into 64 row bitmasks in shared memory and stages the 64-row
+// blocks c[·, R] and c[·, C] (≤ 16 vectors).  Thread (row r, slot s) then walks
+// the set bits of its row in its column range: per pair it forms
+// p_v = w·c[v,i]·c[v,j] once, the k-independent hash prefix
+// mix64(lo + φ·hi) once, and for each of its ≤ 4 operators two mix64 and one
+// int→f32 conversion, accumulating acc[k][v] += p_v·O_ij(k) in f32 registers —
+// the "per-(v,k) register reduction".  Slots split the operators (GK groups of
+// 4) and, when there are fewer operator groups, the columns.  At the end each
+// warp reduces its accumulators with shuffles and adds them to the f64 accum
+// with one atomic per (v, k).  The host loops over chunks of 16 vectors and
+// 4·GK operators.  The work per pair is integer hashing (~25 ALU ops per
+// operator): the kernel is ALU-bound, not HBM-bound.
+#include <cstdint>
+#include <string>
+
+#include "cim_b200.h"
+#include "common.cuh"
+#include "host_util.h"
+
+namespace cim {
+namespace {
+
+constexpr int kCtThreads = 256;
+constexpr int kCtKs = 4;  // operators per thread
+
+template <typename T>
+struct ContractArgs {
+  long long n, n_dense;
+  const int2 *rc;
+  const T *vals;
+  int layout;
+  long long n_sparse;
+  const int2 *sp_rc;
+  const long long *sp_off;
+  const uint16_t *sp_rowptr;
+  const uint8_t *sp_col, *sp_row;
+  const T *sp_vals;
+  const float *c;  // (n, n_vec) row-major
+  int n_vec, v0, nv;
+  int m_ops, k0, kc;
+  int kind;  // CIM_VALUES_OP_HASH (1) or CIM_VALUES_IDENTITY (2)
+  uint64_t seed;
+  double *accum;  // (n_vec, m_ops) row-major
+};
+
+template <typename T, int NV, int GK>
+__global__ void __launch_bounds__(kCtThreads, 2) contract_kernel(ContractArgs<T> a) {
+  __shared__ unsigned long long rowmask[64];
+  __shared__ __align__(16) float xr[64][NV];
+  __shared__ __align__(16) float xc[64][NV];
+  const int tid = threadIdx.x;
+  const int r = tid & 63, slot = tid >> 6;
+  const int kg = slot % GK;
+  constexpr int S = 4 / GK;  // column splits
+  const int cs = slot / GK;
+  const unsigned long long colrange =
+      S == 1 ? ~0ull : (((1ull << (64 / S)) - 1ull) << (cs * (64 / S)));
+  uint64_t kq[kCtKs];
+  bool kon[kCtKs];
+#pragma unroll
+  for (int q = 0; q < kCtKs; ++q) {
+    const int kl = kg + GK * q;
+    kon[q] = kl < a.kc;
+    kq[q] = (uint64_t)(a.k0 + kl + 1) * kMix1;
+  }
+  float acc[kCtKs][NV];
+#pragma unroll
+  for (int q = 0; q < kCtKs; ++q)
+#pragma unroll
+    for (int v = 0; v < NV; ++v) acc[q][v] = 0.f;
+
+  const long long total = a.n_dense + a.n_sparse;
+  for (long long t = blockIdx.x; t < total; t += gridDim.x) {
+    const bool dense = t < a.n_dense;
+    const long long u = dense ? t : t - a.n_dense;
+    const int2 RC = dense ? a.rc[u] : a.sp_rc[u];
+    if (tid < 64) rowmask[tid] = 0ull;
+    // stage the two c blocks (zero outside the matrix / vector chunk)
+    for (int e = tid; e < 2 * 64 * NV; e += kCtThreads) {
+      const int side = e / (64 * NV), rr = (e / NV) & 63, v = e % NV;
+      const long long row = (long long)(side ? RC.y : RC.x) * 64 + rr;
+      const float x = (row < a.n && v < a.nv) ? a.c[row * a.n_vec + a.v0 + v] : 0.f;
+      (side ? xc : xr)[rr][v] = x;
+    }
+    __syncthreads();
+    if (dense) {
+      const T *tv = a.vals + u * kTileElems;
+#pragma unroll 4
+      for (int e = tid; e < kTileElems; e += kCtThreads) {
+        if (tv[e] != T(0)) {
+          int rr, cc;
+          layout_index_to_rc<T>(a.layout, e, rr, cc);
+          atomicOr(&rowmask[rr], 1ull << cc);
+        }
+      }
+    } else {
+      const long long base = a.sp_off[u];
+      const int cnt = a.sp_rowptr[u * kSpPtrStride + 64];
+      for (int e = tid; e < cnt; e += kCtThreads)
+        if (a.sp_vals[base + e] != T(0)) atomicOr(&rowmask[a.sp_row[base + e]], 1ull << a.sp_col[base + e]);
+    }
+    __syncthreads();
+    const long long i = (long long)RC.x * 64 + r;
+    unsigned long long m = rowmask[r] & colrange;
+    if (i >= a.n) m = 0ull;
+    const float w = RC.x == RC.y ? 1.f : 2.f;
+    float ci[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) ci[v] = w * xr[r][v];
+    while (m) {
+      const int cc = __ffsll((long long)m) - 1;
+      m &= m - 1;
+      const long long j = (long long)RC.y * 64 + cc;
+      float p[NV];
+#pragma unroll
+      for (int v = 0; v < NV; v += 4) {
+        const float4 x4 = *reinterpret_cast<const float4 *>(&xc[cc][v]);
+        p[v] = ci[v] * x4.x;
+        p[v + 1] = ci[v + 1] * x4.y;
+        p[v + 2] = ci[v + 2] * x4.z;
+        p[v + 3] = ci[v + 3] * x4.w;
+      }
+      if (a.kind == CIM_VALUES_IDENTITY) {
+        if (i != j) continue;
+#pragma unroll
+        for (int q = 0; q < kCtKs; ++q)
+          if (kon[q])
+#pragma unroll
+            for (int v = 0; v < NV; ++v) acc[q][v] += p[v];
+        continue;
+      }
+      const uint64_t lo = (uint64_t)(i < j ? i : j), hi = (uint64_t)(i < j ? j : i);
+      const uint64_t base = mix64(lo + kGolden * hi);
+#pragma unroll
+      for (int q = 0; q < kCtKs; ++q) {
+        if (!kon[q]) continue;
+        const float o = to_unit(mix64(mix64(base ^ kq[q]) ^ a.seed));
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[q][v] = fmaf(p[v], o, acc[q][v]);
+      }
+    }
+    __syncthreads();
+  }
+  // warp reduction (a warp's 32 threads share one slot), one f64 atomic per (v, k)
+  const int lane = tid & 31;
+#pragma unroll
+  for (int q = 0; q < kCtKs; ++q) {
+    if (!kon[q]) continue;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      float s = acc[q][v];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0 && v < a.nv)
+        atomicAdd(&a.accum[(long long)(a.v0 + v) * a.m_ops + a.k0 + kg + GK * q], (double)s);
+    }
+  }
+}
+
+template <typename T, int NV, int GK>
+void launch_contract(const ContractArgs<T> &a, int grid, cudaStream_t s) {
+  contract_kernel<T, NV, GK><<<grid, kCtThreads, 0, s>>>(a);
+}
+
+template <typename T, int NV>
+void launch_gk(const ContractArgs<T> &a, int gk, int grid, cudaStream_t s) {
+  if (gk == 1)
+    launch_contract<T, NV, 1>(a, grid, s);
+  else if (gk == 2)
+    launch_contract<T, NV, 2>(a, grid, s);
+  else
+    launch_contract<T, NV, 4>(a, grid, s);
+}
+
+template <typename T>
+int run_contract(const cim_half_tiles *H, const float *c, int n_vec, int m_ops, int kind, uint64_t seed,
+                 double *accum, cudaStream_t stream) {
+  ContractArgs<T> a{};
+  a.n = H->n;
+  a.n_dense = H->n_tiles;
+  a.rc = reinterpret_cast<const int2 *>(H->tile_rc);
+  a.vals = static_cast<const T *>(H->vals);
+  a.layout = H->layout;
+  const cim_sparse_tiles *S = H->sparse;
+  if (S && S->n_tiles > 0) {
+    a.n_sparse = S->n_tiles;
+    a.sp_rc = reinterpret_cast<const int2 *>(S->tile_rc);
+    a.sp_off = reinterpret_cast<const long long *>(S->entry_off);
+    a.sp_rowptr = S->rowptr;
+    a.sp_col = S->col;
+    a.sp_row = S->row;
+    a.sp_vals = static_cast<const T *>(S->vals);
+  }
+  a.c = c;
+  a.n_vec = n_vec;
+  a.m_ops = m_ops;
+  a.kind = kind;
+  a.seed = seed;
+  a.accum = accum;
+  const long long total = a.n_dense + a.n_sparse;
+  if (total == 0) return CIM_OK;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)(total < (long long)sms * 8 ? total : (long long)sms * 8);
+  for (int v0 = 0; v0 < n_vec; v0 += 16) {
+    a.v0 = v0;
+    a.nv = n_vec - v0 < 16 ? n_vec - v0 : 16;
+    for (int k0 = 0; k0 < m_ops; k0 += 16) {
+      a.k0 = k0;
+      a.kc = m_ops - k0 < 16 ? m_ops - k0 : 16;
+      const int gk = a.kc <= 4 ? 1 : (a.kc <= 8 ? 2 : 4);
+      if (a.nv <= 4)
+        launch_gk<T, 4>(a, gk, grid, stream);
+      else if (a.nv <= 8)
+        launch_gk<T, 8>(a, gk, grid, stream);
+      else
+        launch_gk<T, 16>(a, gk, grid, stream);
+      const cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("contract_kernel: ") + cudaGetErrorString(e));
+    }
+  }
+  return CIM_OK;
+}
+
+}  // namespace
+}  // namespace cim
+
+extern "C" int cim_contract_observables(const cim_half_tiles *H, const float *c, int32_t n_vec, int32_t m_ops,
+                                        int32_t kind, uint64_t seed, double *accum, uint32_t flags, void *stream_) {
+  cim::clear_error();
+  if (!H) return cim::set_error(CIM_EINVAL, "H is NULL");
+  if (H->block != cim::kBlock) return cim::set_error(CIM_EINVAL, "block must be 64");
+  if (H->n < 1) return cim::set_error(CIM_EINVAL, "n must be >= 1");
+  if (H->dtype != CIM_F32 && H->dtype != CIM_F64) return cim::set_error(CIM_EINVAL, "dtype must be CIM_F32 or CIM_F64");
+  if (H->layout != CIM_LAYOUT_FRAG && H->layout != CIM_LAYOUT_TC) return cim::set_error(CIM_EINVAL, "unknown tile layout");
+  if (n_vec < 1 || m_ops < 1) return cim::set_error(CIM_EINVAL, "n_vec and m_ops must be >= 1");
+  if (kind != CIM_VALUES_OP_HASH && kind != CIM_VALUES_IDENTITY)
+    return cim::set_error(CIM_EINVAL, "kind must be CIM_VALUES_OP_HASH or CIM_VALUES_IDENTITY");
+  if (!c || !accum) return cim::set_error(CIM_EINVAL, "c and accum must be non-NULL");
+  if (H->n_tiles > 0 && (!H->tile_rc || !H->vals)) return cim::set_error(CIM_EINVAL, "tile arrays are NULL");
+  const cim_sparse_tiles *S = H->sparse;
+  if (S && S->n_tiles > 0 &&
+      (!S->tile_rc || !S->entry_off || !S->rowptr || (S->n_entries > 0 && (!S->col || !S->row || !S->vals))))
+    return cim::set_error(CIM_EINVAL, "NULL sparse arrays");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream_);
+  if (!(flags & CIM_ACCUMULATE)) {
+    const cudaError_t e = cudaMemsetAsync(accum, 0, sizeof(double) * (size_t)n_vec * m_ops, s);
+    if (e != cudaSuccess) return cim::set_error(CIM_ECUDA, std::string("zeroing accum: ") + cudaGetErrorString(e));
+  }
+  if (H->dtype == CIM_F32) return cim::run_contract<float>(H, c, n_vec, m_ops, kind, seed, accum, s);
+  return cim::run_contract<double>(H, c, n_vec, m_ops, kind, seed, accum, s);
+}

@@ -7,10 +7,13 @@
 over the interacting pairs (i, j) of a stored pattern.  Where the reference
 re-walks every tile's pairs on the CPU, here the pattern is a ``HalfTiles``
 (its nonzero entries mark the pairs, e.g. ``HalfTiles.from_skeleton`` of a
-reference skeleton with unit values), each operator O_k is materialised on the
-device restricted to that pattern (``cim_fill_masked_values``, values
-bit-exact to ``_op_values_np``), and the contraction is one sym_spmm per
-operator followed by the per-vector dot product.
+reference skeleton with unit values) and ``cim_contract_observables`` walks
+its tiles once, computing O_ij(k) on the fly (bit-exact to
+``_op_values_np``) and reducing c[v,i]·O_ij(k)·c[v,j] per (v, k) in
+registers — no operator is materialised (csrc/contract.cu).
+``contract_materialized`` keeps the composition through ``sym_spmm`` (O_k
+filled on the pattern by ``cim_fill_masked_values``) as an independent
+cross-check.
 
 ``ObservablesInput``, ``random_coefficients``, ``STRATEGIES`` and
 ``OP_KINDS`` keep the reference's names and validation (pipeline.py:64,
@@ -116,11 +119,27 @@ def contract_observables(pattern: HalfTiles, inputs: ObservablesInput, strategy:
     if inputs.c.shape[1] != pattern.n:
         raise ValueError(f"coefficients cover {inputs.c.shape[1]} states, basis has {pattern.n}")
     dev = pattern.device
+    c = torch.from_numpy(inputs.c).to(dev).t().contiguous()  # (n, n_vec) f32
+    out = torch.empty((inputs.n_vec, inputs.m_ops), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    with torch.cuda.device(dev):
+        check(lib().cim_contract_observables(pattern.descriptor(), c.data_ptr(), inputs.n_vec, inputs.m_ops,
+                                             _OP_CODES[inputs.op_kind], inputs.seed, out.data_ptr(), 0, stream),
+              "cim_contract_observables")
+    inputs.accum[:] = out.cpu().numpy().astype(np.float32).reshape(-1)
+    return inputs.accum.reshape(inputs.n_vec, inputs.m_ops)
+
+
+def contract_materialized(pattern: HalfTiles, inputs: ObservablesInput) -> np.ndarray:
+    """The same contraction through materialised operators — O_k filled on the
+    pattern, one sym_spmm per operator, then c_vᵀ(O_k c_v) — an independent
+    GPU composition the tests cross-check the fused kernel with.  Returns the
+    (n_vec, m_ops) f64 result without touching ``inputs.accum``."""
+    dev = pattern.device
     X = torch.from_numpy(inputs.c).to(dev, dtype=pattern.dtype).t().contiguous()  # (n, n_vec)
     out = torch.empty((inputs.n_vec, inputs.m_ops), dtype=torch.float64, device=dev)
     for k in range(inputs.m_ops):
         O = operator_tiles(pattern, inputs.op_kind, k, inputs.seed)
         Y = sym_spmm(O, X)
         out[:, k] = (X.to(torch.float64) * Y.to(torch.float64)).sum(dim=0)
-    inputs.accum[:] = out.cpu().numpy().astype(np.float32).reshape(-1)
-    return inputs.accum.reshape(inputs.n_vec, inputs.m_ops)
+    return out.cpu().numpy()
