@@ -36,7 +36,6 @@ namespace cim {
 namespace {
 
 constexpr int kCtThreads = 256;
-constexpr int kCtKs = 4;  // operators per thread
 
 template <typename T>
 struct ContractArgs {
@@ -58,9 +57,12 @@ struct ContractArgs {
   double *accum;  // (n_vec, m_ops) row-major
 };
 
-template <typename T, int NV, int GK>
-__global__ void __launch_bounds__(kCtThreads, 2) contract_kernel(ContractArgs<T> a) {
-  __shared__ unsigned long long rowmask[64];
+// NV vectors per launch, GK operator groups of KS operators per thread
+// (GK·KS ≥ the launch's operator count), IDENT: the identity operator (same
+// value for every k — one walk, added to every column of accum).
+template <typename T, int NV, int GK, int KS, bool IDENT>
+__global__ void __launch_bounds__(kCtThreads, KS == 4 ? 2 : 3) contract_kernel(ContractArgs<T> a) {
+  __shared__ unsigned rowmask[64][2];  // 32-bit words: shared atomicOr is native at 32 bits
   __shared__ __align__(16) float xr[64][NV];
   __shared__ __align__(16) float xc[64][NV];
   const int tid = threadIdx.x;
@@ -70,17 +72,12 @@ __global__ void __launch_bounds__(kCtThreads, 2) contract_kernel(ContractArgs<T>
   const int cs = slot / GK;
   const unsigned long long colrange =
       S == 1 ? ~0ull : (((1ull << (64 / S)) - 1ull) << (cs * (64 / S)));
-  uint64_t kq[kCtKs];
-  bool kon[kCtKs];
+  uint64_t kq[KS];
 #pragma unroll
-  for (int q = 0; q < kCtKs; ++q) {
-    const int kl = kg + GK * q;
-    kon[q] = kl < a.kc;
-    kq[q] = (uint64_t)(a.k0 + kl + 1) * kMix1;
-  }
-  float acc[kCtKs][NV];
+  for (int q = 0; q < KS; ++q) kq[q] = (uint64_t)(a.k0 + kg + GK * q + 1) * kMix1;
+  float acc[KS][NV];
 #pragma unroll
-  for (int q = 0; q < kCtKs; ++q)
+  for (int q = 0; q < KS; ++q)
 #pragma unroll
     for (int v = 0; v < NV; ++v) acc[q][v] = 0.f;
 
@@ -89,7 +86,7 @@ __global__ void __launch_bounds__(kCtThreads, 2) contract_kernel(ContractArgs<T>
     const bool dense = t < a.n_dense;
     const long long u = dense ? t : t - a.n_dense;
     const int2 RC = dense ? a.rc[u] : a.sp_rc[u];
-    if (tid < 64) rowmask[tid] = 0ull;
+    if (tid < 128) rowmask[tid >> 1][tid & 1] = 0u;
     // stage the two c blocks (zero outside the matrix / vector chunk)
     for (int e = tid; e < 2 * 64 * NV; e += kCtThreads) {
       const int side = e / (64 * NV), rr = (e / NV) & 63, v = e % NV;
@@ -105,18 +102,21 @@ __global__ void __launch_bounds__(kCtThreads, 2) contract_kernel(ContractArgs<T>
         if (tv[e] != T(0)) {
           int rr, cc;
           layout_index_to_rc<T>(a.layout, e, rr, cc);
-          atomicOr(&rowmask[rr], 1ull << cc);
+          atomicOr(&rowmask[rr][cc >> 5], 1u << (cc & 31));
         }
       }
     } else {
       const long long base = a.sp_off[u];
       const int cnt = a.sp_rowptr[u * kSpPtrStride + 64];
       for (int e = tid; e < cnt; e += kCtThreads)
-        if (a.sp_vals[base + e] != T(0)) atomicOr(&rowmask[a.sp_row[base + e]], 1ull << a.sp_col[base + e]);
+        if (a.sp_vals[base + e] != T(0)) {
+          const int cc = a.sp_col[base + e];
+          atomicOr(&rowmask[a.sp_row[base + e]][cc >> 5], 1u << (cc & 31));
+        }
     }
     __syncthreads();
     const long long i = (long long)RC.x * 64 + r;
-    unsigned long long m = rowmask[r] & colrange;
+    unsigned long long m = (((unsigned long long)rowmask[r][1] << 32) | rowmask[r][0]) & colrange;
     if (i >= a.n) m = 0ull;
     const float w = RC.x == RC.y ? 1.f : 2.f;
     float ci[NV];
@@ -135,23 +135,19 @@ __global__ void __launch_bounds__(kCtThreads, 2) contract_kernel(ContractArgs<T>
         p[v + 2] = ci[v + 2] * x4.z;
         p[v + 3] = ci[v + 3] * x4.w;
       }
-      if (a.kind == CIM_VALUES_IDENTITY) {
-        if (i != j) continue;
+      if constexpr (IDENT) {
+        if (i == j)
 #pragma unroll
-        for (int q = 0; q < kCtKs; ++q)
-          if (kon[q])
+          for (int v = 0; v < NV; ++v) acc[0][v] += p[v];
+      } else {
+        const uint64_t lo = (uint64_t)(i < j ? i : j), hi = (uint64_t)(i < j ? j : i);
+        const uint64_t base = mix64(lo + kGolden * hi);
 #pragma unroll
-            for (int v = 0; v < NV; ++v) acc[q][v] += p[v];
-        continue;
-      }
-      const uint64_t lo = (uint64_t)(i < j ? i : j), hi = (uint64_t)(i < j ? j : i);
-      const uint64_t base = mix64(lo + kGolden * hi);
+        for (int q = 0; q < KS; ++q) {  // operators past the launch's count are computed and dropped
+          const float o = to_unit(mix64(mix64(base ^ kq[q]) ^ a.seed));
 #pragma unroll
-      for (int q = 0; q < kCtKs; ++q) {
-        if (!kon[q]) continue;
-        const float o = to_unit(mix64(mix64(base ^ kq[q]) ^ a.seed));
-#pragma unroll
-        for (int v = 0; v < NV; ++v) acc[q][v] = fmaf(p[v], o, acc[q][v]);
+          for (int v = 0; v < NV; ++v) acc[q][v] = fmaf(p[v], o, acc[q][v]);
+        }
       }
     }
     __syncthreads();
@@ -159,32 +155,39 @@ __global__ void __launch_bounds__(kCtThreads, 2) contract_kernel(ContractArgs<T>
   // warp reduction (a warp's 32 threads share one slot), one f64 atomic per (v, k)
   const int lane = tid & 31;
 #pragma unroll
-  for (int q = 0; q < kCtKs; ++q) {
-    if (!kon[q]) continue;
+  for (int q = 0; q < KS; ++q) {
+    const int kl = kg + GK * q;
+    if (!IDENT && kl >= a.kc) continue;
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       float s = acc[q][v];
 #pragma unroll
       for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0 && v < a.nv)
-        atomicAdd(&a.accum[(long long)(a.v0 + v) * a.m_ops + a.k0 + kg + GK * q], (double)s);
+      if (lane == 0 && v < a.nv) {
+        double *dst = a.accum + (long long)(a.v0 + v) * a.m_ops;
+        if (IDENT)
+          for (int k = 0; k < a.m_ops; ++k) atomicAdd(dst + k, (double)s);
+        else
+          atomicAdd(dst + a.k0 + kl, (double)s);
+      }
     }
   }
 }
 
-template <typename T, int NV, int GK>
-void launch_contract(const ContractArgs<T> &a, int grid, cudaStream_t s) {
-  contract_kernel<T, NV, GK><<<grid, kCtThreads, 0, s>>>(a);
-}
-
 template <typename T, int NV>
-void launch_gk(const ContractArgs<T> &a, int gk, int grid, cudaStream_t s) {
-  if (gk == 1)
-    launch_contract<T, NV, 1>(a, grid, s);
-  else if (gk == 2)
-    launch_contract<T, NV, 2>(a, grid, s);
+void launch_nv(const ContractArgs<T> &a, bool ident, int grid, cudaStream_t s) {
+  if (ident)
+    contract_kernel<T, NV, 1, 1, true><<<grid, kCtThreads, 0, s>>>(a);
+  else if (a.kc == 1)
+    contract_kernel<T, NV, 1, 1, false><<<grid, kCtThreads, 0, s>>>(a);
+  else if (a.kc == 2)
+    contract_kernel<T, NV, 1, 2, false><<<grid, kCtThreads, 0, s>>>(a);
+  else if (a.kc <= 4)
+    contract_kernel<T, NV, 1, 4, false><<<grid, kCtThreads, 0, s>>>(a);
+  else if (a.kc <= 8)
+    contract_kernel<T, NV, 2, 4, false><<<grid, kCtThreads, 0, s>>>(a);
   else
-    launch_contract<T, NV, 4>(a, grid, s);
+    contract_kernel<T, NV, 4, 4, false><<<grid, kCtThreads, 0, s>>>(a);
 }
 
 template <typename T>
@@ -218,19 +221,19 @@ int run_contract(const cim_half_tiles *H, const float *c, int n_vec, int m_ops, 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)(total < (long long)sms * 8 ? total : (long long)sms * 8);
+  const bool ident = kind == CIM_VALUES_IDENTITY;
   for (int v0 = 0; v0 < n_vec; v0 += 16) {
     a.v0 = v0;
     a.nv = n_vec - v0 < 16 ? n_vec - v0 : 16;
-    for (int k0 = 0; k0 < m_ops; k0 += 16) {
+    for (int k0 = 0; k0 < (ident ? 1 : m_ops); k0 += 16) {
       a.k0 = k0;
       a.kc = m_ops - k0 < 16 ? m_ops - k0 : 16;
-      const int gk = a.kc <= 4 ? 1 : (a.kc <= 8 ? 2 : 4);
       if (a.nv <= 4)
-        launch_gk<T, 4>(a, gk, grid, stream);
+        launch_nv<T, 4>(a, ident, grid, stream);
       else if (a.nv <= 8)
-        launch_gk<T, 8>(a, gk, grid, stream);
+        launch_nv<T, 8>(a, ident, grid, stream);
       else
-        launch_gk<T, 16>(a, gk, grid, stream);
+        launch_nv<T, 16>(a, ident, grid, stream);
       const cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("contract_kernel: ") + cudaGetErrorString(e));
     }
