@@ -223,6 +223,15 @@ CIM_API int cim_gram_blocked(const void *A, int64_t lda, int32_t a_bw, int64_t a
                              const void *B, int64_t ldb, int32_t b_bw, int64_t b_bstride, int32_t cb,
                              int64_t rows, int32_t dtype, double *out, void *workspace,
                              uint64_t ws_bytes, uint64_t block_mask, void *stream);
+/* cim_gram_blocked with flags: CIM_GRAM_FAST (f32 operands) forms products
+   and partial sums in f32 over runs of ≤ 32 rows, accumulating the runs in
+   f64 — ~2⁻²⁴·32 relative error per run instead of exact products, for
+   eigensolver Gram matrices of f32 blocks; without it, as cim_gram_blocked. */
+#define CIM_GRAM_FAST 1u
+CIM_API int cim_gram_blocked_ex(const void *A, int64_t lda, int32_t a_bw, int64_t a_bstride, int32_t ca,
+                                const void *B, int64_t ldb, int32_t b_bw, int64_t b_bstride, int32_t cb,
+                                int64_t rows, int32_t dtype, double *out, void *workspace,
+                                uint64_t ws_bytes, uint64_t block_mask, uint32_t flags, void *stream);
 CIM_API int cim_tsmm_blocked(const float *A, int64_t lda, int32_t a_bw, int64_t a_bstride, int32_t q,
                              const float *C, int32_t p, float alpha, float beta, float *Out,
                              int64_t ldo, int32_t o_bw, int64_t o_bstride, int64_t rows, void *stream);

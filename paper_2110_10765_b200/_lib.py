@@ -17,6 +17,7 @@ CIM_OK, CIM_EINVAL, CIM_ECUDA, CIM_EUNSUPPORTED = 0, 1, 2, 3
 CIM_F32, CIM_F64 = 0, 1
 CIM_ACCUMULATE = 1
 CIM_DETERMINISTIC = 2
+CIM_GRAM_FAST = 1
 CIM_VALUES_H_XOR, CIM_VALUES_OP_HASH, CIM_VALUES_IDENTITY = 0, 1, 2
 CIM_LAYOUT_FRAG, CIM_LAYOUT_TC = 0, 1
 BLOCK = 64
@@ -51,6 +52,7 @@ EXPORTS = (
     "cim_gram_blocked",
     "cim_tsmm_blocked",
     "cim_contract_observables",
+    "cim_gram_blocked_ex",
 )
 
 
@@ -159,6 +161,9 @@ def lib() -> ctypes.CDLL:
     L.cim_gram_blocked.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_int64, c.c_int32, c.c_void_p, c.c_int64,
                                    c.c_int32, c.c_int64, c.c_int32, c.c_int64, c.c_int32, c.c_void_p, c.c_void_p,
                                    c.c_uint64, c.c_uint64, c.c_void_p]
+    L.cim_gram_blocked_ex.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_int64, c.c_int32, c.c_void_p, c.c_int64,
+                                   c.c_int32, c.c_int64, c.c_int32, c.c_int64, c.c_int32, c.c_void_p, c.c_void_p,
+                                   c.c_uint64, c.c_uint64, c.c_uint32, c.c_void_p]
     L.cim_tsmm_blocked.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_int64, c.c_int32, c.c_void_p, c.c_int32,
                                    c.c_float, c.c_float, c.c_void_p, c.c_int64, c.c_int32, c.c_int64, c.c_int64,
                                    c.c_void_p]

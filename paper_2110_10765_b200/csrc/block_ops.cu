@@ -10,10 +10,13 @@
 // shared memory and accumulates in f64 — the product is HBM-bound
 // (rows·(ca+cb)·s bytes) with DFMA work rows·ca·cb.
 //
-// Grid-stride over 128-row slabs, double-buffered with cp.async; each CTA
-// stages slabs of A and B in shared memory (input dtype, widened on use), and each thread owns a 4×4 block of G for a residue
-// class of the slab's rows.  Per-CTA partials go to a workspace and a second
-// kernel sums them in a fixed order (bit-reproducible run to run).
+// Grid-stride over slabs of rows (~24 KB per stage), a kGramStages-deep ring
+// in shared memory: block-major operands (the eigensolver's work buffer) are
+// staged by one thread with one bulk copy per 8-column block (cp.async.bulk
+// on an mbarrier), other layouts by all threads with cp.async.  Each thread
+// owns an 8×8 block of G for a residue class of the slab's rows.  Per-CTA
+// partials go to a workspace and a second kernel sums them in a fixed order
+// (bit-reproducible run to run).
 #include <algorithm>
 #include <cstdint>
 #include <string>
@@ -21,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include "cim_b200.h"
+#include "common.cuh"
 #include "host_util.h"
 
 namespace {
@@ -38,11 +42,11 @@ struct Operand {
 
 __host__ __device__ __forceinline__ int pad8(int c) { return (c + 7) & ~7; }
 
-// Rows per slab: ~4K elements per operand pair (16 KB of f32 per stage;
-// kGramStages stages in flight per CTA whatever the column counts).
+// Rows per slab: ~24 KB per stage whatever the column counts (6K f32 or 3K
+// f64 elements), kGramStages stages in flight per CTA.
 constexpr int kGramStages = 4;
-__host__ __device__ __forceinline__ int slab_rows(int cap, int cbp) {
-  const int r = 4096 / (cap + cbp);
+__host__ __device__ __forceinline__ int slab_rows(int cap, int cbp, int es) {
+  const int r = (es == 4 ? 6144 : 3072) / (cap + cbp);
   return r < 32 ? 32 : (r > 1024 ? 1024 : (r & ~7));
 }
 
@@ -130,7 +134,21 @@ __device__ __forceinline__ void load8(double (&d)[8], const T *p) {
 // block_mask: bit (bi·nbj + bj) set ⇔ output block (bi, bj) is computed (a
 // caller exploiting symmetry skips the mirrored half; skipped blocks are 0).
 // same_ab: B is A (loaded once).
-template <typename T>
+// FAST (f32 operands, CIM_GRAM_FAST): products and partial sums in f32
+// (FFMA2 on register pairs) over at most kFastRun rows, then widened into the
+// f64 accumulators — 1/kFastRun of the conversions and no DFMA in the row
+// loop; each partial is a ≤ kFastRun-term f32 sum (relative error
+// ≲ kFastRun·2⁻²⁴ of its absolute sum), everything above it f64.
+constexpr int kFastRun = 32;
+
+__device__ __forceinline__ unsigned long long gfma2(float t, unsigned long long x, unsigned long long acc) {
+  unsigned long long tt, r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(tt) : "f"(t));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(tt), "l"(x), "l"(acc));
+  return r;
+}
+
+template <typename T, bool FAST>
 __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const Operand A, const Operand B, int mode_a,
                                                                     int mode_b, long long rows,
                                                                     double *__restrict__ part, uint64_t block_mask,
@@ -138,13 +156,19 @@ __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const Operan
   extern __shared__ __align__(32) unsigned char smem_raw[];
   const int ca = A.cols, cb = B.cols;
   const int cap = pad8(ca), cbp = pad8(cb);
-  const int kSlab = slab_rows(cap, same_ab ? 0 : cbp);  // B == A: only A is staged, so slabs grow
+  const int kSlab = slab_rows(cap, same_ab ? 0 : cbp, (int)sizeof(T));  // B == A: only A is staged
   const int sbs = sblk_stride(kSlab);
   const int nbi = cap / 8, nbj = cbp / 8, nblk = nbi * nbj;
   const uint64_t live = (nblk >= 64 ? ~0ull : ((1ull << nblk) - 1)) & block_mask;
   const int nact = max(1, __popcll(live));
   const int stage_elems = (nbi + (same_ab ? 0 : nbj)) * sbs;
   T *ring = reinterpret_cast<T *>(smem_raw);
+  __shared__ uint64_t full[kGramStages];  // bulk mode: slab k landed in stage k % S
+  const bool bulk = mode_a == 0 && (same_ab || mode_b == 0);
+  if (bulk && threadIdx.x == 0) {
+    for (int q = 0; q < kGramStages; ++q) cim::mbar_init(&full[q], 1);
+    cim::fence_mbar_init();
+  }
   const int red_cap = (int)((kGramStages * (size_t)stage_elems * sizeof(T)) / (sizeof(double) * cap * cbp));
   const int split = min(kGramThreads / nact, red_cap);  // row residue classes (≥ 1)
   const int t = threadIdx.x;
@@ -159,16 +183,56 @@ __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const Operan
   const int bi = blk / nbj, bj = blk % nbj;
   const float inv_ca = 1.0f / (float)ca, inv_cb = 1.0f / (float)cb;
   for (int e = t; e < kGramStages * stage_elems; e += kGramThreads) ring[e] = T(0);  // pads stay zero
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zeros before the bulk copies' writes
   __syncthreads();
   double acc[8][8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+  unsigned long long acc2[8][4];  // FAST: f32 pairs (row i, columns 2jp, 2jp+1)
+  int run = 0;
+  auto flush = [&]() {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int jp = 0; jp < 4; ++jp) {
+        float lo, hi;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc2[i][jp]));
+        acc[i][2 * jp] += (double)lo;
+        acc[i][2 * jp + 1] += (double)hi;
+        acc2[i][jp] = 0ull;
+      }
+    run = 0;
+  };
+  if constexpr (FAST) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int jp = 0; jp < 4; ++jp) acc2[i][jp] = 0ull;
+  }
 
   const long long nslabs = (rows + kSlab - 1) / kSlab;
+  const uint64_t pol = cim::policy_evict_first();  // streamed once
   auto issue = [&](long long k) {  // this CTA's k-th slab into ring stage k % S (rows ≥ nr never read)
     const long long sl = blockIdx.x + k * gridDim.x;
+    if (bulk) {  // one bulk copy per 8-column block, issued by thread 0
+      if (threadIdx.x == 0 && sl < nslabs) {
+        const long long r0 = sl * kSlab;
+        const int nr = (int)min((long long)kSlab, rows - r0);
+        T *st = ring + (size_t)(k % kGramStages) * stage_elems;
+        const uint32_t bytes = (uint32_t)nr * 8 * sizeof(T);
+        cim::mbar_arrive_expect_tx(&full[k % kGramStages], bytes * (nbi + (same_ab ? 0 : nbj)));
+        for (int b = 0; b < nbi; ++b)
+          cim::bulk_g2s(st + b * sbs, static_cast<const T *>(A.p) + (long long)b * A.bstride + r0 * 8, bytes,
+                        &full[k % kGramStages], pol);
+        if (!same_ab)
+          for (int b = 0; b < nbj; ++b)
+            cim::bulk_g2s(st + (nbi + b) * sbs, static_cast<const T *>(B.p) + (long long)b * B.bstride + r0 * 8,
+                          bytes, &full[k % kGramStages], pol);
+      }
+      return;
+    }
     if (sl < nslabs) {
       const long long r0 = sl * kSlab;
       const int nr = (int)min((long long)kSlab, rows - r0);
@@ -182,25 +246,45 @@ __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const Operan
   for (long long k = 0;; ++k) {
     const long long sl = blockIdx.x + k * gridDim.x;
     if (sl >= nslabs) break;
-    cp_async_wait<kGramStages - 2>();  // slab k has landed (this thread's copies) ...
-    __syncthreads();                   // ... everyone's, and slab k-1's stage is free
+    if (bulk)
+      cim::mbar_wait(&full[k % kGramStages], (uint32_t)((k / kGramStages) & 1));
+    else
+      cp_async_wait<kGramStages - 2>();  // slab k has landed (this thread's copies) ...
+    __syncthreads();                     // ... everyone's, and slab k-1's stage is free
     issue(k + kGramStages - 1);
     const long long r0 = sl * kSlab;
     const int nr = (int)min((long long)kSlab, rows - r0);
     const T *sa = ring + (size_t)(k % kGramStages) * stage_elems + bi * sbs;
     const T *sb = ring + (size_t)(k % kGramStages) * stage_elems + ((same_ab ? 0 : nbi) + bj) * sbs;
     if (active) {
-      for (int r = grp; r < nr; r += split) {
-        double av[8], bv[8];
-        load8<T>(av, sa + r * 8);
-        load8<T>(bv, sb + r * 8);
+      if constexpr (FAST) {
+        for (int r = grp; r < nr; r += split) {
+          const float4 a0 = *reinterpret_cast<const float4 *>(sa + r * 8);
+          const float4 a1 = *reinterpret_cast<const float4 *>(sa + r * 8 + 4);
+          const ulonglong2 b01 = *reinterpret_cast<const ulonglong2 *>(sb + r * 8);
+          const ulonglong2 b23 = *reinterpret_cast<const ulonglong2 *>(sb + r * 8 + 4);
+          const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+          const unsigned long long bv[4] = {b01.x, b01.y, b23.x, b23.y};
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+          for (int i = 0; i < 8; ++i)
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+            for (int jp = 0; jp < 4; ++jp) acc2[i][jp] = gfma2(av[i], bv[jp], acc2[i][jp]);
+          if (++run == kFastRun) flush();
+        }
+      } else {
+        for (int r = grp; r < nr; r += split) {
+          double av[8], bv[8];
+          load8<T>(av, sa + r * 8);
+          load8<T>(bv, sb + r * 8);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+        }
       }
     }
   }
+  if constexpr (FAST) flush();
   cp_async_wait<0>();
   // CTA reduction over the row residue classes (fixed order) in the ring
   __syncthreads();
@@ -222,17 +306,21 @@ __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const Operan
   }
 }
 
+// One warp per output entry: lane l sums partials l, l+32, … then a fixed
+// butterfly — deterministic, and ~nparts/32 dependent loads instead of nparts.
 __global__ void gram_sum_kernel(const double *__restrict__ part, int nparts, int count, double *__restrict__ out) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (e >= count) return;
   double s = 0.0;
-  for (int p = 0; p < nparts; ++p) s += part[(size_t)p * count + e];
-  out[e] = s;
+  for (int p = lane; p < nparts; p += 32) s += part[(size_t)p * count + e];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[e] = s;
 }
 
 size_t gram_smem(int ca, int cb, size_t es, bool same_ab = false) {
   const int cap = pad8(ca), cbp = same_ab ? 0 : pad8(cb);
-  return (size_t)kGramStages * ((cap + cbp) / 8) * sblk_stride(slab_rows(cap, cbp)) * es;
+  return (size_t)kGramStages * ((cap + cbp) / 8) * sblk_stride(slab_rows(cap, cbp, (int)es)) * es;
 }
 
 int load_mode(const Operand &o, size_t es) {
@@ -243,11 +331,11 @@ int load_mode(const Operand &o, size_t es) {
   return 2;
 }
 
-int gram_grid(long long rows, int ca, int cb, bool same_ab = false) {
+int gram_grid(long long rows, int ca, int cb, bool same_ab = false, int es = 4) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int kSlab = slab_rows(pad8(ca), same_ab ? 0 : pad8(cb));
+  const int kSlab = slab_rows(pad8(ca), same_ab ? 0 : pad8(cb), es);
   const long long slabs = (rows + kSlab - 1) / kSlab;
   return (int)std::min<long long>(slabs > 0 ? slabs : 1, 2LL * sms);
 }
@@ -259,7 +347,7 @@ int bw_shift_of(int32_t bw) {
 }
 
 int gram_impl(const Operand &A, const Operand &B, long long rows, int32_t dtype, double *out, void *workspace,
-              uint64_t ws_bytes, cudaStream_t stream, uint64_t block_mask = ~0ull) {
+              uint64_t ws_bytes, cudaStream_t stream, uint64_t block_mask = ~0ull, uint32_t flags = 0) {
   const int ca = A.cols, cb = B.cols;
   if (ca < 1 || cb < 1 || ca > kMaxCols || cb > kMaxCols)
     return cim::set_error(CIM_EINVAL, "column counts must be in [1, 64]");
@@ -269,7 +357,7 @@ int gram_impl(const Operand &A, const Operand &B, long long rows, int32_t dtype,
   const size_t es = dtype == CIM_F32 ? 4 : 8;
   const bool same_ab = A.p == B.p && A.ld == B.ld && A.bstride == B.bstride && A.bw_shift == B.bw_shift &&
                        A.cols == B.cols;
-  const int grid = gram_grid(rows, ca, cb, same_ab);  // ≤ the grid cim_gram_workspace_bytes assumed
+  const int grid = gram_grid(rows, ca, cb, same_ab, (int)es);  // ≤ the grid cim_gram_workspace_bytes assumed
   const uint64_t need = (uint64_t)grid * ca * cb * sizeof(double);
   if (!workspace || ws_bytes < need)
     return cim::set_error(CIM_EINVAL, "workspace must hold " + std::to_string(need) + " bytes");
@@ -277,23 +365,22 @@ int gram_impl(const Operand &A, const Operand &B, long long rows, int32_t dtype,
   const int ma = load_mode(A, es), mb = load_mode(B, es);
   if (block_mask == 0) block_mask = ~0ull;
   cudaError_t e;
-  if (dtype == CIM_F32) {
-    e = cudaFuncSetAttribute(gram_partial_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto run = [&](auto kern) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
-      gram_partial_kernel<float><<<grid, kGramThreads, smem, stream>>>(A, B, ma, mb, rows,
-                                                                       static_cast<double *>(workspace), block_mask,
-                                                                       same_ab);
-  } else {
-    e = cudaFuncSetAttribute(gram_partial_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-      gram_partial_kernel<double><<<grid, kGramThreads, smem, stream>>>(A, B, ma, mb, rows,
-                                                                        static_cast<double *>(workspace), block_mask,
-                                                                        same_ab);
-  }
+      kern<<<grid, kGramThreads, smem, stream>>>(A, B, ma, mb, rows, static_cast<double *>(workspace), block_mask,
+                                                 same_ab);
+  };
+  if (dtype == CIM_F32 && (flags & CIM_GRAM_FAST))
+    run(gram_partial_kernel<float, true>);
+  else if (dtype == CIM_F32)
+    run(gram_partial_kernel<float, false>);
+  else
+    run(gram_partial_kernel<double, false>);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return cim::set_error(CIM_ECUDA, std::string("gram_partial_kernel: ") + cudaGetErrorString(e));
   const int count = ca * cb;
-  gram_sum_kernel<<<(count + 127) / 128, 128, 0, stream>>>(static_cast<const double *>(workspace), grid, count, out);
+  gram_sum_kernel<<<(count * 32 + 255) / 256, 256, 0, stream>>>(static_cast<const double *>(workspace), grid, count, out);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cim::set_error(CIM_ECUDA, std::string("gram_sum_kernel: ") + cudaGetErrorString(e));
   return CIM_OK;
@@ -303,7 +390,8 @@ int gram_impl(const Operand &A, const Operand &B, long long rows, int32_t dtype,
 
 extern "C" uint64_t cim_gram_workspace_bytes(int64_t rows, int32_t ca, int32_t cb) {
   if (rows < 0 || ca < 1 || cb < 1) return 0;
-  return (uint64_t)gram_grid(rows, ca, cb) * (uint64_t)ca * (uint64_t)cb * sizeof(double);
+  // the largest grid any dtype / aliasing uses (f64: the smallest slabs)
+  return (uint64_t)gram_grid(rows, ca, cb, false, 8) * (uint64_t)ca * (uint64_t)cb * sizeof(double);
 }
 
 extern "C" int cim_gram(const void *A, int64_t lda, int32_t ca, const void *B, int64_t ldb, int32_t cb, int64_t rows,
@@ -314,17 +402,27 @@ extern "C" int cim_gram(const void *A, int64_t lda, int32_t ca, const void *B, i
   return gram_impl(a, b, rows, dtype, out, workspace, ws_bytes, reinterpret_cast<cudaStream_t>(stream_));
 }
 
-extern "C" int cim_gram_blocked(const void *A, int64_t lda, int32_t a_bw, int64_t a_bstride, int32_t ca,
-                                const void *B, int64_t ldb, int32_t b_bw, int64_t b_bstride, int32_t cb, int64_t rows,
-                                int32_t dtype, double *out, void *workspace, uint64_t ws_bytes, uint64_t block_mask,
-                                void *stream_) {
+extern "C" int cim_gram_blocked_ex(const void *A, int64_t lda, int32_t a_bw, int64_t a_bstride, int32_t ca,
+                                   const void *B, int64_t ldb, int32_t b_bw, int64_t b_bstride, int32_t cb,
+                                   int64_t rows, int32_t dtype, double *out, void *workspace, uint64_t ws_bytes,
+                                   uint64_t block_mask, uint32_t flags, void *stream_) {
   cim::clear_error();
   const int sa = bw_shift_of(a_bw), sb = bw_shift_of(b_bw);
   if (sa < 0 || sb < 0) return cim::set_error(CIM_EINVAL, "block widths must be 4, 8, 16, 32 or 64");
   if (lda < std::min(a_bw, ca) || ldb < std::min(b_bw, cb))
     return cim::set_error(CIM_EINVAL, "leading dimensions must cover a block");
+  if (flags & ~(uint32_t)CIM_GRAM_FAST) return cim::set_error(CIM_EINVAL, "unknown gram flags");
   const Operand a{A, lda, a_bstride, sa, ca}, b{B, ldb, b_bstride, sb, cb};
-  return gram_impl(a, b, rows, dtype, out, workspace, ws_bytes, reinterpret_cast<cudaStream_t>(stream_), block_mask);
+  return gram_impl(a, b, rows, dtype, out, workspace, ws_bytes, reinterpret_cast<cudaStream_t>(stream_), block_mask,
+                   flags);
+}
+
+extern "C" int cim_gram_blocked(const void *A, int64_t lda, int32_t a_bw, int64_t a_bstride, int32_t ca,
+                                const void *B, int64_t ldb, int32_t b_bw, int64_t b_bstride, int32_t cb, int64_t rows,
+                                int32_t dtype, double *out, void *workspace, uint64_t ws_bytes, uint64_t block_mask,
+                                void *stream_) {
+  return cim_gram_blocked_ex(A, lda, a_bw, a_bstride, ca, B, ldb, b_bw, b_bstride, cb, rows, dtype, out, workspace,
+                             ws_bytes, block_mask, 0u, stream_);
 }
 
 // ---------------------------------------------------------------------------

@@ -151,10 +151,11 @@ class _Work:
 
     P, X, W, AP, AX, AW = range(6)
 
-    def __init__(self, rows: int, m: int, dtype, device):
+    def __init__(self, rows: int, m: int, dtype, device, fast_gram: bool = False):
         self.m, self.rows = m, rows
         self.bw = max(4, 1 << (m - 1).bit_length())
         self.buf = torch.zeros((6, rows, self.bw), dtype=dtype, device=device)
+        self.fast_gram = fast_gram and dtype == torch.float32
 
     def slot(self, s: int, ncols: int | None = None) -> torch.Tensor:
         return self.buf[s][:, : (self.m if ncols is None else ncols)]
@@ -178,7 +179,7 @@ class _Work:
         bi·(b1-b0) + bj; 0 = all (the others come back as 0)."""
         ca, cb = (a1 - a0) * self.bw, (b1 - b0) * self.bw
         if self._native() and ca <= 64 and cb <= 64:
-            from ._lib import CIM_F32, CIM_F64, check, lib
+            from ._lib import CIM_F32, CIM_F64, CIM_GRAM_FAST, check, lib
 
             L = lib()
             out = torch.empty((ca, cb), dtype=torch.float64, device=self.buf.device)
@@ -186,12 +187,13 @@ class _Work:
             ws = _workspace(self.buf.device, need)
             bs = self.rows * self.bw
             with torch.cuda.device(self.buf.device):
-                check(L.cim_gram_blocked(self.buf[a0].data_ptr(), self.bw, self.bw, bs, ca, self.buf[b0].data_ptr(),
-                                         self.bw, self.bw, bs, cb, self.rows,
-                                         CIM_F32 if self.buf.dtype == torch.float32 else CIM_F64, out.data_ptr(),
-                                         ws.data_ptr(), need, block_mask if self.bw == 8 else 0,
-                                         torch.cuda.current_stream(self.buf.device).cuda_stream),
-                      "cim_gram_blocked")
+                check(L.cim_gram_blocked_ex(self.buf[a0].data_ptr(), self.bw, self.bw, bs, ca,
+                                            self.buf[b0].data_ptr(), self.bw, self.bw, bs, cb, self.rows,
+                                            CIM_F32 if self.buf.dtype == torch.float32 else CIM_F64, out.data_ptr(),
+                                            ws.data_ptr(), need, block_mask if self.bw == 8 else 0,
+                                            CIM_GRAM_FAST if self.fast_gram else 0,
+                                            torch.cuda.current_stream(self.buf.device).cuda_stream),
+                      "cim_gram_blocked_ex")
             return _allreduce(out, group).cpu().numpy()
         if self.buf.is_cuda and (ca > 64 or cb > 64):  # wide blocks: one slot pair at a time, natively
             G = np.zeros((ca, cb))
@@ -208,7 +210,7 @@ class _Work:
         if self._native() and self.buf.dtype == torch.float32 and q <= 64 and p <= 64:
             from ._lib import check, lib
 
-            Cd = torch.from_numpy(np.ascontiguousarray(C, dtype=np.float32)).to(self.buf.device)
+            Cd = _upload(C, torch.float32, self.buf.device)
             with torch.cuda.device(self.buf.device):
                 check(lib().cim_tsmm_blocked(self.buf[a0].data_ptr(), self.bw, self.bw, self.rows * self.bw, q,
                                              Cd.data_ptr(), p, float(alpha), float(beta), dst.buf[o0].data_ptr(),
@@ -216,7 +218,7 @@ class _Work:
                                              torch.cuda.current_stream(self.buf.device).cuda_stream),
                       "cim_tsmm_blocked")
             return
-        prod = self.dense(a0, a1) @ torch.from_numpy(C).to(self.buf.device, self.buf.dtype)
+        prod = self.dense(a0, a1) @ _upload(C, self.buf.dtype, self.buf.device)
         for k, s in enumerate(range(o0, o1)):
             blk = prod[:, k * self.bw:(k + 1) * self.bw]
             if beta == 0.0:
@@ -226,6 +228,42 @@ class _Work:
 
 
 _WS: dict = {}
+_UP: dict = {}
+
+
+class _Uploader:
+    """Small host → device uploads (the eigensolver's coefficient matrices)
+    through a pinned ring, asynchronously: a pageable ``.to(device)`` makes
+    torch synchronise the stream, which would stall the host behind every
+    queued kernel.  A slot is rewritten only after ``slots`` later uploads,
+    and the solver synchronises (Gram read-back) at least once per three
+    uploads, so a slot's previous copy has always completed."""
+
+    slots, slot_elems = 16, 64 * 64
+
+    def __init__(self, device):
+        self.device = device
+        self.host = torch.empty((self.slots, self.slot_elems), dtype=torch.float64, pin_memory=True)
+        self.k = 0
+
+    def put(self, a: np.ndarray, dtype) -> torch.Tensor:
+        a = np.ascontiguousarray(a)
+        if a.size > self.slot_elems:
+            return torch.from_numpy(a).to(self.device, dtype)
+        h = self.host[self.k % self.slots]
+        self.k += 1
+        hv = h.view(torch.float32)[: a.size] if dtype == torch.float32 else h[: a.size]
+        hv.copy_(torch.from_numpy(a.reshape(-1)).to(hv.dtype))
+        return hv.to(self.device, non_blocking=True).view(a.shape)
+
+
+def _upload(a: np.ndarray, dtype, device) -> torch.Tensor:
+    if device.type != "cuda":
+        return torch.from_numpy(np.ascontiguousarray(a)).to(device, dtype)
+    up = _UP.get(device)
+    if up is None:
+        up = _UP[device] = _Uploader(device)
+    return up.put(a, dtype)
 
 
 def _workspace(device, nbytes: int) -> torch.Tensor:
@@ -253,15 +291,20 @@ def _orthonormalize_slot(work: "_Work", s: int, nv: int, scratch: "_Work", group
         if nk == 0:
             work.buf[s].zero_()
             return 0
-        work.tsmm(s, s + 1, _embed(T, np.arange(nv), np.arange(nk), (bw, bw)), scratch, s, s + 1)
-        work.buf[s].copy_(scratch.buf[s])
+        Tb = _embed(T, np.arange(nv), np.arange(nk), (bw, bw))
+        if bw <= 16:  # cim_tsmm reads a row's inputs before writing it when p ≤ 16: in place
+            work.tsmm(s, s + 1, Tb, work, s, s + 1)
+        else:
+            work.tsmm(s, s + 1, Tb, scratch, s, s + 1)
+            work.buf[s].copy_(scratch.buf[s])
         nv = nk
     return nv
 
 
 def lobpcg(apply: Callable[[torch.Tensor], torch.Tensor], X0: torch.Tensor, *, tol: float = 1e-5,
            max_iter: int = 300, largest: bool = False, group=None,
-           callback: Callable[[int, np.ndarray, np.ndarray], None] | None = None) -> LobpcgResult:
+           callback: Callable[[int, np.ndarray, np.ndarray], None] | None = None,
+           exact_gram: bool = False) -> LobpcgResult:
     """Lowest (default) or largest eigenpairs of the symmetric operator.
 
     ``X0`` holds this rank's rows of the initial block (n_local × m);
@@ -272,15 +315,24 @@ def lobpcg(apply: Callable[[torch.Tensor], torch.Tensor], X0: torch.Tensor, *, t
     Blocks live in two ping-pong block-major work buffers (``_Work``); Gram
     products run in float64 on the device (``cim_gram_blocked``), block
     updates write in place (``cim_tsmm_blocked``), and only the small
-    3m × 3m problems go to the host.
+    3m × 3m problems go to the host.  f32 blocks use the fast Gram mode
+    (``CIM_GRAM_FAST``: f32 products over ≤ 32-row runs, f64 across runs)
+    unless ``exact_gram``.  An ``apply`` taking ``out=`` (e.g.
+    ``ShardedSymSpmm.apply``) writes AW straight into the work buffer.
     """
     if X0.ndim != 2:
         raise ValueError("X0 must be (n_local, m)")
     rows, m = X0.shape
     dev, dt = X0.device, X0.dtype
     calls = 0
-    cur, nxt = _Work(rows, m, dt, dev), _Work(rows, m, dt, dev)
+    cur, nxt = _Work(rows, m, dt, dev, not exact_gram), _Work(rows, m, dt, dev, not exact_gram)
     bw = cur.bw
+    import inspect
+
+    try:
+        apply_out = bw == m and "out" in inspect.signature(apply).parameters
+    except (TypeError, ValueError):
+        apply_out = False
     Wk = _Work
     cur.slot(Wk.X).copy_(X0)
     if _orthonormalize_slot(cur, Wk.X, m, nxt, group) < m:
@@ -302,10 +354,16 @@ def lobpcg(apply: Callable[[torch.Tensor], torch.Tensor], X0: torch.Tensor, *, t
     converged = False
     for it in range(1, max_iter + 1):
         # residuals R = AX − X·Λ into the W slot
-        lam_t = torch.from_numpy(lam).to(dev, dt)
-        cur.buf[Wk.W].zero_()
-        cur.slot(Wk.W).copy_(torch.addcmul(cur.slot(Wk.AX), cur.slot(Wk.X), lam_t, value=-1.0))
-        rnorm = np.sqrt(np.maximum(np.diag(cur.gram(Wk.W, Wk.W + 1, Wk.W, Wk.W + 1, group))[:m], 0.0))
+        # (full bw-wide blocks: padding columns of X / AX are zero, λ padded with 0)
+        lam_p = np.zeros(bw)
+        lam_p[:m] = lam
+        torch.addcmul(cur.buf[Wk.AX], cur.buf[Wk.X], _upload(lam_p, dt, dev), value=-1.0, out=cur.buf[Wk.W])
+        # one Gram pass gives both the residual norms (WᵀW) and the projection
+        # coefficients ([P X]ᵀW) — soft locking only selects columns of W
+        b0 = Wk.P if have_p else Wk.X
+        G_all = cur.gram(b0, Wk.W + 1, Wk.W, Wk.W + 1, group)
+        wb = (Wk.W - b0) * bw  # W's rows in G_all
+        rnorm = np.sqrt(np.maximum(np.diag(G_all[wb:wb + bw])[:m], 0.0))
         scale = max(scale, float(np.abs(lam).max()))
         history.append((lam.copy(), rnorm.copy()))
         if callback is not None:
@@ -315,23 +373,26 @@ def lobpcg(apply: Callable[[torch.Tensor], torch.Tensor], X0: torch.Tensor, *, t
             converged = True
             break
         nw = int(active.sum())
+        act = np.flatnonzero(active)
         if nw < m:  # soft locking: keep only the active residual columns
-            idx = torch.from_numpy(np.flatnonzero(active)).to(dev)
+            idx = torch.from_numpy(act).to(dev)
             Wa = cur.slot(Wk.W)[:, idx].clone()
             cur.buf[Wk.W].zero_()
             cur.slot(Wk.W, nw).copy_(Wa)
         # project out the current basis [P X] (or [X]), then orthonormalise
-        b0 = Wk.P if have_p else Wk.X
         bidx = cur.vidx(range(b0, Wk.W), [m] * (Wk.W - b0))
         wi = np.arange(nw)
-        G_bw = cur.gram(b0, Wk.W, Wk.W, Wk.W + 1, group)[np.ix_(bidx, wi)]
+        G_bw = G_all[np.ix_(bidx, act)]
         cur.tsmm(b0, Wk.W, _embed(G_bw, bidx, wi, ((Wk.W - b0) * bw, bw)), cur, Wk.W, Wk.W + 1, alpha=-1.0, beta=1.0)
         nw = _orthonormalize_slot(cur, Wk.W, nw, nxt, group)
         if nw == 0:
             converged = True
             break
-        cur.buf[Wk.AW].zero_()
-        cur.slot(Wk.AW, nw).copy_(apply(cur.slot(Wk.W, nw).contiguous()))
+        if apply_out:  # W's unused columns are zero, so A·W over the full block is AW
+            apply(cur.buf[Wk.W], out=cur.buf[Wk.AW])
+        else:
+            cur.buf[Wk.AW].zero_()
+            cur.slot(Wk.AW, nw).copy_(apply(cur.slot(Wk.W, nw).contiguous()))
         calls += 1
         # Rayleigh–Ritz on S = [P X W] (or [X W]): one Gram pass of S against
         # all six slots gives SᵀS and SᵀAS

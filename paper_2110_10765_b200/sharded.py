@@ -160,9 +160,22 @@ class ShardedSymSpmm:
         lo = self.rank * self.rows_per_rank
         return min(lo, self.n), min(lo + self.rows_per_rank, self.n)
 
-    def apply(self, X_local: torch.Tensor) -> torch.Tensor:
+    def apply(self, X_local: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """Y_local = (A·X)[local rows] given X_local = X[local rows]
-        (shape (rows_per_rank, k_user); rows ≥ n must be 0)."""
+        (shape (rows_per_rank, k_user); rows ≥ n must be 0).  ``out``: a
+        (rows_per_rank, k_user) buffer to receive Y_local (written in place
+        by the kernel / reduce-scatter where the layout allows)."""
+        if out is not None:
+            if out.shape != (self.rows_per_rank, self.k_user) or out.dtype != self.dtype or out.device != self.device:
+                raise ValueError("out must be a (rows_per_rank, k_user) tensor of the operator's dtype and device")
+            direct = out.is_contiguous() and self.k == self.k_user and out.data_ptr() % 16 == 0
+            if direct and not self.fused:
+                return self._apply_into(X_local, out)
+            out.copy_(self.apply(X_local))
+            return out
+        return self._apply_into(X_local, None)
+
+    def _apply_into(self, X_local: torch.Tensor, out: torch.Tensor | None) -> torch.Tensor:
         if X_local.shape[0] != self.rows_per_rank:
             raise ValueError(f"X_local must have {self.rows_per_rank} rows, got {X_local.shape[0]}")
         if X_local.shape[1] != self.k_user:
@@ -177,15 +190,17 @@ class ShardedSymSpmm:
         if self.world == 1 and self.local_apply == self._cuda_apply and xl.data_ptr() % 16 == 0:
             # one rank: the kernel reads X_local and writes Y_local directly
             # (rows_per_rank = n_pad), no staging copies
-            self._cuda_apply(xl, self.Y_local)
-            return self.Y_local[:, : self.k_user]
+            Y = self.Y_local if out is None else out
+            self._cuda_apply(xl, Y)
+            return Y[:, : self.k_user]
         if self.world > 1:
             dist.all_gather_into_tensor(self.X_full, xl, group=self.group)
         else:
             self.X_full.copy_(xl)
         self.local_apply(self.X_full, self.Y_part)
+        Y = self.Y_local if out is None else out
         if self.world > 1:
-            dist.reduce_scatter_tensor(self.Y_local, self.Y_part, op=dist.ReduceOp.SUM, group=self.group)
+            dist.reduce_scatter_tensor(Y, self.Y_part, op=dist.ReduceOp.SUM, group=self.group)
         else:
-            self.Y_local.copy_(self.Y_part)
-        return self.Y_local[:, : self.k_user]
+            Y.copy_(self.Y_part)
+        return Y[:, : self.k_user]

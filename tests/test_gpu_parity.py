@@ -473,6 +473,47 @@ def test_gram_f64_matches_numpy(pkg, dtype, rows, ca, cb):
         gram_f64(A.cuda(), B[:-1].cuda())
 
 
+@pytest.mark.parametrize("rows,nslots_a,nslots_b,mask", [(100_003, 1, 1, 0), (257, 2, 1, 0), (1_000_000, 3, 6, 0),
+                                                         (300_001, 3, 6, 0b000111_000111_000111)])
+def test_gram_fast_mode(pkg, rows, nslots_a, nslots_b, mask):
+    """cim_gram_blocked_ex with CIM_GRAM_FAST (the eigensolver's f32 Gram):
+    f32 products and ≤ 32-row f32 partial sums, f64 across runs — within
+    2⁻¹⁸·(|A|ᵀ|B|) of the f64 product, reproducible, masked blocks zero; the
+    exact mode on the same block-major operands stays at f64 accuracy."""
+    from paper_2110_10765_b200._lib import CIM_F32, CIM_GRAM_FAST, lib
+
+    g = torch.Generator().manual_seed(rows)
+    buf = torch.randn((6, rows, 8), generator=g).cuda()
+    L = lib()
+    ca, cb = 8 * nslots_a, 8 * nslots_b
+    need = int(L.cim_gram_workspace_bytes(rows, ca, cb))
+    ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+
+    def run(flags):
+        out = torch.empty((ca, cb), dtype=torch.float64, device="cuda")
+        assert L.cim_gram_blocked_ex(buf[0].data_ptr(), 8, 8, rows * 8, ca, buf[0].data_ptr(), 8, 8, rows * 8, cb,
+                                     rows, CIM_F32, out.data_ptr(), ws.data_ptr(), need, mask, flags, None) == 0
+        return out.cpu().numpy()
+
+    dense = buf.cpu().double().permute(1, 0, 2).reshape(rows, 48).numpy()
+    A, B = dense[:, :ca], dense[:, :cb]
+    want = A.T @ B
+    absprod = np.abs(A).T @ np.abs(B)
+    if mask:
+        keep = np.zeros((ca // 8, cb // 8), bool)
+        for bi in range(ca // 8):
+            for bj in range(cb // 8):
+                keep[bi, bj] = (mask >> (bi * (cb // 8) + bj)) & 1
+        want = want * np.kron(keep, np.ones((8, 8)))
+    fast = run(CIM_GRAM_FAST)
+    assert np.abs(fast - want).max() <= 2.0 ** -18 * absprod.max()
+    assert np.array_equal(fast, run(CIM_GRAM_FAST))
+    exact = run(0)
+    assert np.abs(exact - want).max() <= 1e-12 * np.sqrt(rows) * absprod.max()
+    assert L.cim_gram_blocked_ex(buf[0].data_ptr(), 8, 8, rows * 8, ca, buf[0].data_ptr(), 8, 8, rows * 8, cb, rows,
+                                 CIM_F32, ws.data_ptr(), ws.data_ptr(), need, 0, 4, None) == 1  # unknown flag
+
+
 @pytest.mark.parametrize("rows,q,p,off", [(1, 1, 1, 0), (1000, 8, 8, 0), (100_001, 24, 16, 8), (5000, 7, 5, 3),
                                           (4096, 64, 64, 0)])
 def test_tsmm_matches_torch(pkg, rows, q, p, off):

@@ -40,12 +40,22 @@ print(f"torch mm 24->16 (contiguous): {us:8.1f} us")
 # block-major work buffer (what lobpcg uses): 6 slots of (n, 8)
 import numpy as np
 from paper_2110_10765_b200.lobpcg import _Work
-w = _Work(n, 8, torch.float32, torch.device("cuda"))
+w = _Work(n, 8, torch.float32, torch.device("cuda"), fast_gram=True)
 w.buf.normal_()
+ex = _Work(n, 8, torch.float32, torch.device("cuda"))
+ex.buf.copy_(w.buf)
+# lobpcg's MG product: [P X W]ᵀ·[P X W AP AX AW], upper slot blocks of SᵀS and SᵀAS
+MG_MASK = 0
+for bi in range(3):
+    for bj in range(bi, 3):
+        MG_MASK |= 1 << (bi * 6 + bj)
+        MG_MASK |= 1 << (bi * 6 + 3 + bj)
 w2 = _Work(n, 8, torch.float32, torch.device("cuda"))
-for (a0, a1, b0, b1) in [(2, 3, 2, 3), (0, 2, 2, 3), (0, 3, 0, 6)]:
-    us = timeit(lambda: w.gram(a0, a1, b0, b1, None))
-    print(f"blocked gram {8*(a1-a0):2d}x{8*(b1-b0):2d}: {us:8.1f} us  {n*8*((a1-a0)+(b1-b0))*4/us/1e3:7.1f} GB/s")
+for (a0, a1, b0, b1, mask) in [(2, 3, 2, 3, 0), (0, 2, 2, 3, 0), (0, 3, 0, 6, 0), (0, 3, 0, 6, MG_MASK)]:
+    for name, ww in (("fast", w), ("exact", ex)):
+        us = timeit(lambda: ww.gram(a0, a1, b0, b1, None, block_mask=mask))
+        print(f"blocked gram {name:5s} {8*(a1-a0):2d}x{8*(b1-b0):2d} mask={mask:#x}: {us:8.1f} us  "
+              f"{n*8*max(a1, b1)*4/us/1e3:7.1f} GB/s (incl. host sync)")
 C = np.random.default_rng(0).standard_normal((24, 16))
 us = timeit(lambda: w.tsmm(0, 3, C, w2, 0, 2))
 print(f"blocked tsmm 24->16: {us:8.1f} us  {n*40*4/us/1e3:7.1f} GB/s")
