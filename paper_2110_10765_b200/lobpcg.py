@@ -280,12 +280,12 @@ def _embed(M: np.ndarray, rows_idx: np.ndarray, cols_idx: np.ndarray, shape) -> 
     return out
 
 
-def _orthonormalize_slot(work: "_Work", s: int, nv: int, scratch: "_Work", group) -> int:
+def _orthonormalize_slot(work: "_Work", s: int, nv: int, scratch: "_Work", group, passes: int = 2) -> int:
     """Cholesky-QR twice on the first nv columns of slot s (scratch: the same
     slot of another buffer).  Keeps the independent columns, zeroes the rest;
     returns their count."""
     bw = work.bw
-    for _ in range(2):
+    for _ in range(passes):
         T = _orth_factor(work.gram(s, s + 1, s, s + 1, group)[:nv, :nv])
         nk = T.shape[1]
         if nk == 0:
@@ -304,7 +304,7 @@ def _orthonormalize_slot(work: "_Work", s: int, nv: int, scratch: "_Work", group
 def lobpcg(apply: Callable[[torch.Tensor], torch.Tensor], X0: torch.Tensor, *, tol: float = 1e-5,
            max_iter: int = 300, largest: bool = False, group=None,
            callback: Callable[[int, np.ndarray, np.ndarray], None] | None = None,
-           exact_gram: bool = False) -> LobpcgResult:
+           exact_gram: bool = False, w_orth_passes: int = 1) -> LobpcgResult:
     """Lowest (default) or largest eigenpairs of the symmetric operator.
 
     ``X0`` holds this rank's rows of the initial block (n_local × m);
@@ -317,7 +317,11 @@ def lobpcg(apply: Callable[[torch.Tensor], torch.Tensor], X0: torch.Tensor, *, t
     updates write in place (``cim_tsmm_blocked``), and only the small
     3m × 3m problems go to the host.  f32 blocks use the fast Gram mode
     (``CIM_GRAM_FAST``: f32 products over ≤ 32-row runs, f64 across runs)
-    unless ``exact_gram``.  An ``apply`` taking ``out=`` (e.g.
+    unless ``exact_gram``.  The projected residual block W gets
+    ``w_orth_passes`` Cholesky-QR passes (default one: Rayleigh–Ritz solves
+    the generalised problem with the computed SᵀS, so W only needs to be
+    well conditioned, not orthonormal to rounding; the initial X gets two).
+    An ``apply`` taking ``out=`` (e.g.
     ``ShardedSymSpmm.apply``) writes AW straight into the work buffer.
     """
     if X0.ndim != 2:
@@ -384,7 +388,7 @@ def lobpcg(apply: Callable[[torch.Tensor], torch.Tensor], X0: torch.Tensor, *, t
         wi = np.arange(nw)
         G_bw = G_all[np.ix_(bidx, act)]
         cur.tsmm(b0, Wk.W, _embed(G_bw, bidx, wi, ((Wk.W - b0) * bw, bw)), cur, Wk.W, Wk.W + 1, alpha=-1.0, beta=1.0)
-        nw = _orthonormalize_slot(cur, Wk.W, nw, nxt, group)
+        nw = _orthonormalize_slot(cur, Wk.W, nw, nxt, group, passes=w_orth_passes)
         if nw == 0:
             converged = True
             break
