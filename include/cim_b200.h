@@ -118,6 +118,15 @@ typedef struct cim_sparse_tiles {
   const uint8_t  *row;
   const uint16_t *cperm;
   const void     *vals;     /* dtype of the enclosing cim_half_tiles */
+  /* Optional work split (NULL lists: derived on the fly by scanning
+     entry_off): tiles with more than cim_sparse_small_max() padded entries
+     (entry_off[t+1] − entry_off[t]) are staged through shared memory, the
+     non-empty rest walked entry-parallel from global memory.  Each list holds
+     tile indices; together they must cover every non-empty tile once. */
+  const int32_t  *staged_tiles;
+  int64_t         n_staged;
+  const int32_t  *small_tiles;
+  int64_t         n_small;
 } cim_sparse_tiles;
 
 typedef struct cim_half_tiles {
@@ -288,6 +297,10 @@ CIM_API int cim_basis_fill_dense(const uint64_t *bits_lo, const uint16_t *occ, i
 CIM_API int cim_basis_fill_sparse(const uint64_t *bits_lo, const uint16_t *occ, int64_t n,
                                   int32_t n_particles, int32_t threshold, const cim_sparse_tiles *S,
                                   int32_t dtype, uint64_t seed, void *stream);
+
+/* The small-tile threshold of the sparse path, in padded entries per tile
+   (the staged_tiles / small_tiles split of cim_sparse_tiles). */
+CIM_API int32_t cim_sparse_small_max(void);
 
 /* Device workspace bytes cim_gram / cim_gram_blocked need. */
 CIM_API uint64_t cim_gram_workspace_bytes(int64_t rows, int32_t ca, int32_t cb);

@@ -53,6 +53,7 @@ EXPORTS = (
     "cim_tsmm_blocked",
     "cim_contract_observables",
     "cim_gram_blocked_ex",
+    "cim_sparse_small_max",
 )
 
 
@@ -70,6 +71,10 @@ class CimSparseTiles(ctypes.Structure):
         ("row", ctypes.c_void_p),
         ("cperm", ctypes.c_void_p),
         ("vals", ctypes.c_void_p),
+        ("staged_tiles", ctypes.c_void_p),
+        ("n_staged", ctypes.c_int64),
+        ("small_tiles", ctypes.c_void_p),
+        ("n_small", ctypes.c_int64),
     ]
 
 
@@ -129,6 +134,8 @@ def lib() -> ctypes.CDLL:
                                             c.c_uint64, c.c_int32, c.c_void_p, c.c_void_p]
     L.cim_fill_masked_values.argtypes = [c.c_void_p, c.c_int64, c.c_int64, c.c_int32, c.c_int32, c.c_int32,
                                          c.c_uint64, c.c_int32, c.c_void_p, c.c_void_p, c.c_void_p]
+    L.cim_sparse_small_max.argtypes = []
+    L.cim_sparse_small_max.restype = c.c_int32
     L.cim_contract_observables.argtypes = [c.POINTER(CimHalfTiles), c.c_void_p, c.c_int32, c.c_int32, c.c_int32,
                                            c.c_uint64, c.c_void_p, c.c_uint32, c.c_void_p]
     L.cim_pack_tiles.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_int32, c.c_void_p, c.c_void_p]

@@ -16,6 +16,7 @@
 // a tile (shared-memory f32 atomicAdd is a CAS loop on sm_100; a first
 // version built on it ran 4× slower than streaming the tiles dense).
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -72,6 +73,9 @@ struct SparseParams {
   long long n_tiles;
   long long ldx, ldy;
   int k;
+  int small_max;  // tiles with ≤ small_max (padded) entries go to sparse_small_kernel
+  const int32_t *staged;  // optional list of the staged tiles (else scan all, skipping small ones)
+  long long n_staged;
 };
 
 // ---------------------------------------------------------------------------
@@ -84,6 +88,7 @@ struct SparseParams {
 // walked from global memory instead.
 // ---------------------------------------------------------------------------
 constexpr int kSpCap = 1024;
+constexpr int kSpSmallDefault = 128;
 constexpr int kSpConsumers = 128;
 constexpr unsigned kSpBig = 1u, kSpTerm = 2u;
 
@@ -217,22 +222,25 @@ __global__ void __launch_bounds__(kSpConsumers + 32) sparse_spmm_kernel(const Sp
     int stage = 0;
     uint32_t phase = 0;
     unsigned int t0 = 0;
+    const long long n_items = p.staged ? p.n_staged : p.n_tiles;
     if (lane == 0) t0 = atomicAdd(p.counter, 32u);
     t0 = __shfl_sync(0xffffffffu, t0, 0);
-    while ((long long)t0 < p.n_tiles) {
+    while ((long long)t0 < n_items) {
       unsigned int t_next = 0;
       if (lane == 0) t_next = atomicAdd(p.counter, 32u);  // prefetch the next chunk's ticket
-      const long long t = (long long)t0 + lane;
-      const bool valid = t < p.n_tiles;
+      const long long it = (long long)t0 + lane;
+      const bool valid = it < n_items;
+      const long long t = valid ? (p.staged ? (long long)__ldg(p.staged + it) : it) : 0;
       const int2 my_rc = valid ? p.tile_rc[t] : make_int2(0, 0);
       const long long my_b = valid ? p.entry_off[t] : 0, my_e = valid ? p.entry_off[t + 1] : 0;
-      const int cnt = (int)min(32LL, p.n_tiles - (long long)t0);
+      const int cnt = (int)min(32LL, n_items - (long long)t0);
       for (int q = 0; q < cnt; ++q) {
         const int R = __shfl_sync(0xffffffffu, my_rc.x, q), C = __shfl_sync(0xffffffffu, my_rc.y, q);
         const long long base = __shfl_sync(0xffffffffu, my_b, q);
         const int ne = (int)(__shfl_sync(0xffffffffu, my_e, q) - base);
+        const long long tt = __shfl_sync(0xffffffffu, t, q);
+        if (!p.staged && ne <= p.small_max) continue;  // empty, or walked by sparse_small_kernel (warp-uniform)
         if (lane == 0) {
-          const long long tt = (long long)t0 + q;
           mbar_wait_backoff(&empty[stage], phase ^ 1u);
           unsigned char *st = sp_smem + (size_t)stage * L.bytes;
           SpStageHdr *h = reinterpret_cast<SpStageHdr *>(st);
@@ -315,6 +323,57 @@ __global__ void __launch_bounds__(kSpConsumers + 32) sparse_spmm_kernel(const Sp
   }
 }
 
+// Small tiles (≤ small_max entries, typically a few dozen): staging them
+// through the ring costs the producer ~8 bulk copies and two 2 KB X blocks
+// per tile for a few dozen entries, so the producer lane becomes the
+// bottleneck on skeletons with millions of such tiles.  Here one warp takes
+// one tile straight from global memory, entry-parallel: lane e reads entry e
+// (row, col, value — coalesced), gathers X_C[col] and X_R[row] from L2 and
+// adds v·X_C[col] into Y_R[row] and v·X_R[row] into Y_C[col] with vector
+// reds.  One dependent load level instead of rowptr → entries → X, and every
+// lane busy; rows of a tiny tile rarely repeat, so per-entry reds cost about
+// what per-row reductions would.  Grid-stride over the small-tile list.
+template <typename T, int KV>
+__global__ void __launch_bounds__(256) sparse_small_kernel(const SparseParams p, const int32_t *list,
+                                                             long long n_list) {
+  const int lane = threadIdx.x & 31;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const T *X = static_cast<const T *>(p.X);
+  T *Y = static_cast<T *>(p.Y);
+  const T *vals = static_cast<const T *>(p.vals);
+  const long long n_items = list ? n_list : p.n_tiles;
+  for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_items; w += nw) {
+    const long long t = list ? (long long)__ldg(list + w) : w;
+    const long long base = __ldg(p.entry_off + t);
+    if (!list) {
+      const int ne = (int)(__ldg(p.entry_off + t + 1) - base);
+      if (ne == 0 || ne > p.small_max) continue;
+    }
+    const int cnt = __ldg(p.rowptr + (size_t)t * kSpPtrStride + 64);
+    const int2 rc = __ldg(p.tile_rc + t);
+    const bool diag = rc.x == rc.y;
+    const T *xr = X + (long long)rc.x * 64 * p.k, *xc = X + (long long)rc.y * 64 * p.k;
+    T *yr = Y + (long long)rc.x * 64 * p.ldy, *yc = Y + (long long)rc.y * 64 * p.ldy;
+    for (int e = lane; e < cnt; e += 32) {
+      const int c = __ldg(p.col + base + e), r = __ldg(p.row + base + e);
+      const T v = __ldg(vals + base + e);
+      for (int v0 = 0; v0 < p.k; v0 += KV) {
+        T x[KV], a[KV];
+        ldg_vec<T, KV>(x, xc + (long long)c * p.k + v0);
+#pragma unroll
+        for (int q = 0; q < KV; ++q) a[q] = v * x[q];
+        red_vec<T, KV>(yr + (long long)r * p.ldy + v0, a);
+        if (!diag) {
+          ldg_vec<T, KV>(x, xr + (long long)r * p.k + v0);
+#pragma unroll
+          for (int q = 0; q < KV; ++q) a[q] = v * x[q];
+          red_vec<T, KV>(yc + (long long)c * p.ldy + v0, a);
+        }
+      }
+    }
+  }
+}
+
 template <typename T>
 __global__ void fill_sparse_values_kernel(const int2 *tile_rc, const long long *entry_off, const uint16_t *rowptr,
                                           const uint8_t *col, long long n_tiles, long long n, int kind,
@@ -364,6 +423,16 @@ int sp_state(SpState **out) {
   return CIM_OK;
 }
 
+// Small-tile threshold in (padded) entries: CIM_SPARSE_SMALL overrides (A/B
+// sweeps; 0 = every tile through the ring).
+int sparse_small_max() {
+  static const int v = [] {
+    const char *e = std::getenv("CIM_SPARSE_SMALL");
+    return e ? std::atoi(e) : kSpSmallDefault;
+  }();
+  return v;
+}
+
 template <typename T, int KV>
 int launch_sparse(const cim_sparse_tiles *S, const void *X, void *Y, int k, long long ldx, long long ldy,
                   cudaStream_t stream) {
@@ -400,6 +469,10 @@ int launch_sparse(const cim_sparse_tiles *S, const void *X, void *Y, int k, long
   p.ldx = ldx;
   p.ldy = ldy;
   p.k = k;
+  p.small_max = sparse_small_max();
+  p.staged = S->staged_tiles;
+  p.n_staged = S->staged_tiles ? S->n_staged : 0;
+  const bool listed = S->staged_tiles != nullptr || S->small_tiles != nullptr;
   e = cudaFuncSetAttribute(sparse_spmm_kernel<T, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("sparse attr: ") + cudaGetErrorString(e));
   int occ = 0;
@@ -407,15 +480,30 @@ int launch_sparse(const cim_sparse_tiles *S, const void *X, void *Y, int k, long
           cudaSuccess ||
       occ < 1)
     occ = 1;
-  const long long grid = std::min<long long>(S->n_tiles, (long long)st->sms * occ);
-  sparse_spmm_kernel<T, KV><<<(unsigned)grid, kSpConsumers + 32, smem, stream>>>(p, stages);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("sparse_spmm launch: ") + cudaGetErrorString(e));
+  const long long n_ring = listed ? p.n_staged : S->n_tiles;
+  if (n_ring > 0) {
+    const long long grid = std::min<long long>(n_ring, (long long)st->sms * occ);
+    sparse_spmm_kernel<T, KV><<<(unsigned)grid, kSpConsumers + 32, smem, stream>>>(p, stages);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("sparse_spmm launch: ") + cudaGetErrorString(e));
+  }
+  const long long n_small = listed ? (S->small_tiles ? S->n_small : 0) : (p.small_max > 0 ? S->n_tiles : 0);
+  if (n_small > 0) {
+    const long long g2 = std::min<long long>((n_small + 7) / 8, (long long)st->sms * 16);
+    sparse_small_kernel<T, KV><<<(unsigned)g2, 256, 0, stream>>>(p, listed ? S->small_tiles : nullptr,
+                                                                 listed ? S->n_small : 0);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("sparse_small launch: ") + cudaGetErrorString(e));
+  }
   return CIM_OK;
 }
 
 }  // namespace
+}  // namespace cim
 
+extern "C" int32_t cim_sparse_small_max(void) { return cim::sparse_small_max(); }
+
+namespace cim {
 // Called by cim_sym_spmm after the dense tiles (Y already zeroed or accumulating).
 int sym_spmm_sparse(const cim_sparse_tiles *S, int dtype, const void *X, void *Y, int k, long long ldx,
                     long long ldy, cudaStream_t stream) {

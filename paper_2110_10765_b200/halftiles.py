@@ -217,6 +217,7 @@ class SparseTiles:
     entry_off_host: np.ndarray  # tile starts, multiples of SPARSE_ALIGN
     counts_host: np.ndarray  # real entries per tile (the rest of a tile's range is zero padding)
     _desc: CimSparseTiles | None = field(default=None, repr=False)
+    _split: tuple | None = field(default=None, repr=False)
 
     @property
     def n_tiles(self) -> int:
@@ -234,20 +235,41 @@ class SparseTiles:
     def entries_per_tile(self) -> np.ndarray:
         return self.counts_host
 
+    def work_split(self) -> tuple[torch.Tensor, torch.Tensor]:
+        """(staged, small): device int32 tile-index lists of the sparse
+        kernel's two paths — tiles above ``cim_sparse_small_max()`` padded
+        entries go through the shared-memory ring, the non-empty rest are
+        walked entry-parallel (cim_sparse_tiles.staged_tiles / small_tiles)."""
+        if self._split is None:
+            from ._lib import lib
+
+            thr = int(lib().cim_sparse_small_max())
+            ne = np.diff(self.entry_off_host)
+            staged = np.flatnonzero(ne > thr).astype(np.int32)
+            small = np.flatnonzero((ne > 0) & (ne <= thr)).astype(np.int32)
+            dev = self.tile_rc.device
+            mk = lambda a: torch.from_numpy(a if a.size else np.zeros(1, np.int32)).to(dev)  # noqa: E731
+            self._split = (mk(staged), staged.size, mk(small), small.size)
+        return self._split[0][: self._split[1]], self._split[2][: self._split[3]]
+
     def descriptor(self) -> CimSparseTiles:
         if self._desc is None:
             e = self.n_entries > 0
+            self.work_split()
+            st, n_st, sm, n_sm = self._split
             self._desc = CimSparseTiles(n_tiles=self.n_tiles, n_entries=self.n_entries,
                                         tile_rc=self.tile_rc.data_ptr(), entry_off=self.entry_off.data_ptr(),
                                         rowptr=self.rowptr.data_ptr(), colptr=self.colptr.data_ptr(),
                                         col=self.col.data_ptr() if e else None, row=self.row.data_ptr() if e else None,
                                         cperm=self.cperm.data_ptr() if e else None,
-                                        vals=self.vals.data_ptr() if e else None)
+                                        vals=self.vals.data_ptr() if e else None,
+                                        staged_tiles=st.data_ptr(), n_staged=n_st,
+                                        small_tiles=sm.data_ptr(), n_small=n_sm)
         return self._desc
 
     def with_values(self, vals: torch.Tensor) -> "SparseTiles":
         return SparseTiles(self.tile_rc, self.entry_off, self.rowptr, self.colptr, self.col, self.row, self.cperm,
-                           vals, self.tile_rc_host, self.entry_off_host, self.counts_host)
+                           vals, self.tile_rc_host, self.entry_off_host, self.counts_host, _split=self._split)
 
     def arrays(self) -> dict:
         """Host copies of every array (npz interchange)."""
