@@ -245,6 +245,18 @@ CIM_API int cim_tsmm_blocked(const float *A, int64_t lda, int32_t a_bw, int64_t 
                              const float *C, int32_t p, float alpha, float beta, float *Out,
                              int64_t ldo, int32_t o_bw, int64_t o_bstride, int64_t rows, void *stream);
 
+/* cim_tsmm_blocked with C (q × p row-major f32, q·p ≤ 1024) read from HOST
+   memory during the call and carried in the kernel parameters — no upload
+   or staging buffer for the eigensolver's per-iteration coefficients. */
+CIM_API int cim_tsmm_blocked_hc(const float *A, int64_t lda, int32_t a_bw, int64_t a_bstride, int32_t q,
+                                const float *C_host, int32_t p, float alpha, float beta, float *Out,
+                                int64_t ldo, int32_t o_bw, int64_t o_bstride, int64_t rows, void *stream);
+
+/* Device: W = AX − X·diag(λ) over whole (rows × bw) row-major f32 slots
+   (LOBPCG residuals; λ_j from HOST f64 lam[0..m), 0 for j ≥ m). */
+CIM_API int cim_block_residual(const float *X, const float *AX, const double *lam_host, int32_t m, float *W,
+                               int64_t rows, int32_t bw, void *stream);
+
 /*
  * Device: values on the entries of sparse tiles — vals_out[e] = value(i, j)
  * of entry e where mask[e] != 0 (mask: the pattern's own values, or NULL =

@@ -54,6 +54,8 @@ EXPORTS = (
     "cim_contract_observables",
     "cim_gram_blocked_ex",
     "cim_sparse_small_max",
+    "cim_tsmm_blocked_hc",
+    "cim_block_residual",
 )
 
 
@@ -174,9 +176,14 @@ def lib() -> ctypes.CDLL:
     L.cim_tsmm_blocked.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_int64, c.c_int32, c.c_void_p, c.c_int32,
                                    c.c_float, c.c_float, c.c_void_p, c.c_int64, c.c_int32, c.c_int64, c.c_int64,
                                    c.c_void_p]
+    L.cim_tsmm_blocked_hc.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_int64, c.c_int32, c.c_void_p, c.c_int32,
+                                      c.c_float, c.c_float, c.c_void_p, c.c_int64, c.c_int32, c.c_int64, c.c_int64,
+                                      c.c_void_p]
     for name in EXPORTS:
         if name not in ("cim_version", "cim_last_error"):
             getattr(L, name).restype = c.c_int
+    L.cim_block_residual.argtypes = [c.c_void_p, c.c_void_p, c.c_void_p, c.c_int32, c.c_void_p, c.c_int64, c.c_int32,
+                                     c.c_void_p]
     L.cim_host_batch_workspace_bytes.restype = c.c_uint64
     L.cim_gram_workspace_bytes.restype = c.c_uint64
     _lib = L

@@ -19,6 +19,7 @@
 // (bit-reproducible run to run).
 #include <algorithm>
 #include <cstdint>
+#include <cstring>
 #include <string>
 
 #include <cuda_runtime.h>
@@ -452,10 +453,24 @@ __device__ __forceinline__ float *elem(const MutOperand &o, long long r, int c) 
   return o.p + (long long)(c >> o.bw_shift) * o.bstride + r * o.ld + (c & ((1 << o.bw_shift) - 1));
 }
 
+// The small matrix C, read once per CTA into shared memory: from device
+// memory, or carried in the kernel parameters (≤ kCParMax values — the
+// eigensolver's coefficient matrices, computed on the host each iteration:
+// no separate upload, no staging buffer).
+constexpr int kCParMax = 1024;
+struct DevC {
+  const float *p;
+  __device__ __forceinline__ float operator[](int i) const { return p[i]; }
+};
+struct ParC {
+  float c[kCParMax];
+  __device__ __forceinline__ float operator[](int i) const { return c[i]; }
+};
+
 // Generic path (any q, p, alignment): one row per thread.
-__global__ void __launch_bounds__(kTsmmThreads) tsmm_scalar_kernel(const Operand A, const float *__restrict__ C,
-                                                                   int p, float alpha, float beta,
-                                                                   const MutOperand Out, long long rows) {
+template <typename CS>
+__global__ void __launch_bounds__(kTsmmThreads) tsmm_scalar_kernel(const Operand A, const CS C, int p, float alpha,
+                                                                   float beta, const MutOperand Out, long long rows) {
   __shared__ float sc[64 * 64];
   const int q = A.cols;
   for (int e = threadIdx.x; e < q * p; e += kTsmmThreads) sc[e] = C[e];
@@ -474,10 +489,9 @@ __global__ void __launch_bounds__(kTsmmThreads) tsmm_scalar_kernel(const Operand
 // Vector path (q, p, leading dimensions, block strides multiples of 4,
 // 16-byte aligned): each thread owns RB rows and a 16-column strip; A rows
 // arrive as float4, C rows as broadcast LDS.128 (one shared load feeds 4·RB FMAs).
-template <int RB>
-__global__ void __launch_bounds__(kTsmmThreads) tsmm_vec_kernel(const Operand A, const float *__restrict__ C, int p,
-                                                                float alpha, float beta, const MutOperand Out,
-                                                                long long rows) {
+template <int RB, typename CS>
+__global__ void __launch_bounds__(kTsmmThreads) tsmm_vec_kernel(const Operand A, const CS C, int p, float alpha,
+                                                                float beta, const MutOperand Out, long long rows) {
   __shared__ __align__(16) float sc[64 * 64];
   const int q = A.cols;
   for (int e = threadIdx.x; e < q * p; e += kTsmmThreads) sc[e] = C[e];
@@ -542,13 +556,14 @@ __global__ void __launch_bounds__(kTsmmThreads) tsmm_vec_kernel(const Operand A,
   }
 }
 
-int tsmm_impl(const Operand &A, const float *C, int p, float alpha, float beta, const MutOperand &Out, long long rows,
+template <typename CS>
+int tsmm_impl(const Operand &A, const CS &C, int p, float alpha, float beta, const MutOperand &Out, long long rows,
               int out_bw, cudaStream_t stream) {
   const int q = A.cols;
   if (q < 1 || p < 1 || q > 64 || p > 64) return cim::set_error(CIM_EINVAL, "q and p must be in [1, 64]");
   if (rows < 0) return cim::set_error(CIM_EINVAL, "rows must be >= 0");
   if (rows == 0) return CIM_OK;
-  if (!A.p || !C || !Out.p) return cim::set_error(CIM_EINVAL, "NULL pointer");
+  if (!A.p || !Out.p) return cim::set_error(CIM_EINVAL, "NULL pointer");
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -560,10 +575,10 @@ int tsmm_impl(const Operand &A, const float *C, int p, float alpha, float beta, 
     constexpr int RB = 2;
     const long long groups = (rows + RB - 1) / RB;
     const long long blocks = std::min<long long>((groups + kTsmmThreads - 1) / kTsmmThreads, 8LL * sms);
-    tsmm_vec_kernel<RB><<<(unsigned)blocks, kTsmmThreads, 0, stream>>>(A, C, p, alpha, beta, Out, rows);
+    tsmm_vec_kernel<RB, CS><<<(unsigned)blocks, kTsmmThreads, 0, stream>>>(A, C, p, alpha, beta, Out, rows);
   } else {
     const long long blocks = std::min<long long>((rows + kTsmmThreads - 1) / kTsmmThreads, 8LL * sms);
-    tsmm_scalar_kernel<<<(unsigned)blocks, kTsmmThreads, 0, stream>>>(A, C, p, alpha, beta, Out, rows);
+    tsmm_scalar_kernel<CS><<<(unsigned)blocks, kTsmmThreads, 0, stream>>>(A, C, p, alpha, beta, Out, rows);
   }
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cim::set_error(CIM_ECUDA, std::string("tsmm kernel: ") + cudaGetErrorString(e));
@@ -576,9 +591,10 @@ extern "C" int cim_tsmm(const float *A, int64_t lda, int32_t q, const float *C, 
                         float *Out, int64_t ldo, int64_t rows, void *stream_) {
   cim::clear_error();
   if (lda < q || ldo < p) return cim::set_error(CIM_EINVAL, "bad leading dimensions");
+  if (!C) return cim::set_error(CIM_EINVAL, "NULL pointer");
   const Operand a{A, lda, 0, 6, q};
   const MutOperand o{Out, ldo, 0, 6};
-  return tsmm_impl(a, C, p, alpha, beta, o, rows, 64, reinterpret_cast<cudaStream_t>(stream_));
+  return tsmm_impl(a, DevC{C}, p, alpha, beta, o, rows, 64, reinterpret_cast<cudaStream_t>(stream_));
 }
 
 extern "C" int cim_tsmm_blocked(const float *A, int64_t lda, int32_t a_bw, int64_t a_bstride, int32_t q,
@@ -589,7 +605,72 @@ extern "C" int cim_tsmm_blocked(const float *A, int64_t lda, int32_t a_bw, int64
   if (sa < 0 || so < 0) return cim::set_error(CIM_EINVAL, "block widths must be 4, 8, 16, 32 or 64");
   if (lda < std::min(a_bw, q) || ldo < std::min(o_bw, p))
     return cim::set_error(CIM_EINVAL, "leading dimensions must cover a block");
+  if (!C) return cim::set_error(CIM_EINVAL, "NULL pointer");
   const Operand a{A, lda, a_bstride, sa, q};
   const MutOperand o{Out, ldo, o_bstride, so};
-  return tsmm_impl(a, C, p, alpha, beta, o, rows, o_bw, reinterpret_cast<cudaStream_t>(stream_));
+  return tsmm_impl(a, DevC{C}, p, alpha, beta, o, rows, o_bw, reinterpret_cast<cudaStream_t>(stream_));
+}
+
+extern "C" int cim_tsmm_blocked_hc(const float *A, int64_t lda, int32_t a_bw, int64_t a_bstride, int32_t q,
+                                   const float *C_host, int32_t p, float alpha, float beta, float *Out, int64_t ldo,
+                                   int32_t o_bw, int64_t o_bstride, int64_t rows, void *stream_) {
+  cim::clear_error();
+  const int sa = bw_shift_of(a_bw), so = bw_shift_of(o_bw);
+  if (sa < 0 || so < 0) return cim::set_error(CIM_EINVAL, "block widths must be 4, 8, 16, 32 or 64");
+  if (lda < std::min(a_bw, q) || ldo < std::min(o_bw, p))
+    return cim::set_error(CIM_EINVAL, "leading dimensions must cover a block");
+  if (!C_host) return cim::set_error(CIM_EINVAL, "NULL pointer");
+  if (q < 1 || p < 1 || (long long)q * p > kCParMax)
+    return cim::set_error(CIM_EUNSUPPORTED, "host C holds at most 1024 values (q*p)");
+  ParC c;
+  std::memcpy(c.c, C_host, sizeof(float) * (size_t)q * p);
+  const Operand a{A, lda, a_bstride, sa, q};
+  const MutOperand o{Out, ldo, o_bstride, so};
+  return tsmm_impl(a, c, p, alpha, beta, o, rows, o_bw, reinterpret_cast<cudaStream_t>(stream_));
+}
+
+namespace {
+// ---------------------------------------------------------------------------
+// Block residual W = AX − X·diag(λ) over whole slots (rows × bw, row-major;
+// λ_j = 0 for j ≥ m keeps padding columns zero).  λ rides in the kernel
+// parameters.  Elementwise, HBM-bound: 3·rows·bw·4 bytes.
+// ---------------------------------------------------------------------------
+struct LamPar {
+  float l[64];
+};
+
+__global__ void __launch_bounds__(256) block_residual_kernel(const float4 *__restrict__ X,
+                                                             const float4 *__restrict__ AX, float4 *__restrict__ W,
+                                                             long long n4, int bw4, const LamPar lam) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n4; e += (long long)gridDim.x * blockDim.x) {
+    const int j = 4 * (int)(e % bw4);
+    const float4 x = X[e], ax = AX[e];
+    W[e] = make_float4(fmaf(-lam.l[j], x.x, ax.x), fmaf(-lam.l[j + 1], x.y, ax.y), fmaf(-lam.l[j + 2], x.z, ax.z),
+                       fmaf(-lam.l[j + 3], x.w, ax.w));
+  }
+}
+}  // namespace
+
+extern "C" int cim_block_residual(const float *X, const float *AX, const double *lam_host, int32_t m, float *W,
+                                  int64_t rows, int32_t bw, void *stream_) {
+  cim::clear_error();
+  if (bw < 4 || bw > 64 || (bw & 3) || m < 0 || m > bw) return cim::set_error(CIM_EINVAL, "need 4 <= bw <= 64, bw % 4 == 0, m <= bw");
+  if (rows < 0) return cim::set_error(CIM_EINVAL, "rows must be >= 0");
+  if (rows == 0) return CIM_OK;
+  if (!X || !AX || !W || (m > 0 && !lam_host)) return cim::set_error(CIM_EINVAL, "NULL pointer");
+  if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(AX) | reinterpret_cast<uintptr_t>(W)) & 15)
+    return cim::set_error(CIM_EINVAL, "X, AX and W must be 16-byte aligned");
+  LamPar lam{};
+  for (int j = 0; j < m; ++j) lam.l[j] = (float)lam_host[j];
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long n4 = rows * bw / 4;
+  const long long blocks = std::min<long long>((n4 + 255) / 256, 16LL * sms);
+  block_residual_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream_)>>>(
+      reinterpret_cast<const float4 *>(X), reinterpret_cast<const float4 *>(AX), reinterpret_cast<float4 *>(W), n4,
+      bw / 4, lam);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cim::set_error(CIM_ECUDA, std::string("block_residual: ") + cudaGetErrorString(e));
+  return CIM_OK;
 }

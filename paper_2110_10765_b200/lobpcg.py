@@ -156,6 +156,19 @@ class _Work:
         self.bw = max(4, 1 << (m - 1).bit_length())
         self.buf = torch.zeros((6, rows, self.bw), dtype=dtype, device=device)
         self.fast_gram = fast_gram and dtype == torch.float32
+        # launch state fixed for the solve (the host round trips are on the
+        # critical path: no per-call stream / device lookups)
+        if self.buf.is_cuda:
+            self._stream = torch.cuda.current_stream(self.buf.device).cuda_stream
+            self._same_dev = torch.cuda.current_device() == self.buf.device.index
+            self._base = self.buf.data_ptr()
+            self._slot_bytes = rows * self.bw * self.buf.element_size()
+        self._gram_out: dict = {}
+
+    def _ctx(self):
+        import contextlib
+
+        return contextlib.nullcontext() if self._same_dev else torch.cuda.device(self.buf.device)
 
     def slot(self, s: int, ncols: int | None = None) -> torch.Tensor:
         return self.buf[s][:, : (self.m if ncols is None else ncols)]
@@ -182,17 +195,22 @@ class _Work:
             from ._lib import CIM_F32, CIM_F64, CIM_GRAM_FAST, check, lib
 
             L = lib()
-            out = torch.empty((ca, cb), dtype=torch.float64, device=self.buf.device)
-            need = int(L.cim_gram_workspace_bytes(self.rows, ca, cb))
-            ws = _workspace(self.buf.device, need)
+            key = (ca, cb)
+            if key not in self._gram_out:
+                need = int(L.cim_gram_workspace_bytes(self.rows, ca, cb))
+                self._gram_out[key] = (torch.empty((ca, cb), dtype=torch.float64, device=self.buf.device), need,
+                                       _workspace(self.buf.device, need))
+            out, need, ws = self._gram_out[key]
+            if ws.numel() < need or ws is not _WS.get(self.buf.device):
+                ws = _workspace(self.buf.device, need)
+                self._gram_out[key] = (out, need, ws)
             bs = self.rows * self.bw
-            with torch.cuda.device(self.buf.device):
-                check(L.cim_gram_blocked_ex(self.buf[a0].data_ptr(), self.bw, self.bw, bs, ca,
-                                            self.buf[b0].data_ptr(), self.bw, self.bw, bs, cb, self.rows,
+            with self._ctx():
+                check(L.cim_gram_blocked_ex(self._base + a0 * self._slot_bytes, self.bw, self.bw, bs, ca,
+                                            self._base + b0 * self._slot_bytes, self.bw, self.bw, bs, cb, self.rows,
                                             CIM_F32 if self.buf.dtype == torch.float32 else CIM_F64, out.data_ptr(),
                                             ws.data_ptr(), need, block_mask if self.bw == 8 else 0,
-                                            CIM_GRAM_FAST if self.fast_gram else 0,
-                                            torch.cuda.current_stream(self.buf.device).cuda_stream),
+                                            CIM_GRAM_FAST if self.fast_gram else 0, self._stream),
                       "cim_gram_blocked_ex")
             return _allreduce(out, group).cpu().numpy()
         if self.buf.is_cuda and (ca > 64 or cb > 64):  # wide blocks: one slot pair at a time, natively
@@ -204,18 +222,45 @@ class _Work:
             return G
         return _gram(self.dense(a0, a1), self.dense(b0, b1), group)
 
+    def residual(self, lam: np.ndarray) -> None:
+        """W ← AX − X·diag(λ) over the full slots (padding columns of X / AX
+        are zero and λ is padded with 0, so W's padding stays zero)."""
+        if self._native() and self.buf.dtype == torch.float32:
+            from ._lib import check, lib
+
+            lam64 = np.ascontiguousarray(lam, dtype=np.float64)
+            with self._ctx():
+                check(lib().cim_block_residual(self._base + self.X * self._slot_bytes,
+                                               self._base + self.AX * self._slot_bytes, lam64.ctypes.data,
+                                               lam64.size, self._base + self.W * self._slot_bytes, self.rows, self.bw,
+                                               self._stream), "cim_block_residual")
+            return
+        lam_p = np.zeros(self.bw)
+        lam_p[: lam.size] = lam
+        torch.addcmul(self.buf[self.AX], self.buf[self.X], _upload(lam_p, self.buf.dtype, self.buf.device),
+                      value=-1.0, out=self.buf[self.W])
+
     def tsmm(self, a0: int, a1: int, C: np.ndarray, dst: "_Work", o0: int, o1: int, alpha=1.0, beta=0.0) -> None:
         """dst[slots o0..o1) ← alpha·[slots a0..a1)·C + beta·dst (virtual columns)."""
         q, p = (a1 - a0) * self.bw, (o1 - o0) * self.bw
         if self._native() and self.buf.dtype == torch.float32 and q <= 64 and p <= 64:
             from ._lib import check, lib
 
+            if q * p <= 1024:  # C rides in the kernel parameters: no upload
+                Ch = np.ascontiguousarray(C, dtype=np.float32)
+                with self._ctx():
+                    check(lib().cim_tsmm_blocked_hc(self._base + a0 * self._slot_bytes, self.bw, self.bw,
+                                                    self.rows * self.bw, q, Ch.ctypes.data, p, float(alpha),
+                                                    float(beta), dst._base + o0 * dst._slot_bytes, self.bw, self.bw,
+                                                    self.rows * self.bw, self.rows, self._stream),
+                          "cim_tsmm_blocked_hc")
+                return
             Cd = _upload(C, torch.float32, self.buf.device)
-            with torch.cuda.device(self.buf.device):
-                check(lib().cim_tsmm_blocked(self.buf[a0].data_ptr(), self.bw, self.bw, self.rows * self.bw, q,
-                                             Cd.data_ptr(), p, float(alpha), float(beta), dst.buf[o0].data_ptr(),
-                                             self.bw, self.bw, self.rows * self.bw, self.rows,
-                                             torch.cuda.current_stream(self.buf.device).cuda_stream),
+            with self._ctx():
+                check(lib().cim_tsmm_blocked(self._base + a0 * self._slot_bytes, self.bw, self.bw, self.rows * self.bw,
+                                             q, Cd.data_ptr(), p, float(alpha), float(beta),
+                                             dst._base + o0 * dst._slot_bytes, self.bw, self.bw, self.rows * self.bw,
+                                             self.rows, self._stream),
                       "cim_tsmm_blocked")
             return
         prod = self.dense(a0, a1) @ _upload(C, self.buf.dtype, self.buf.device)
@@ -359,9 +404,7 @@ def lobpcg(apply: Callable[[torch.Tensor], torch.Tensor], X0: torch.Tensor, *, t
     for it in range(1, max_iter + 1):
         # residuals R = AX − X·Λ into the W slot
         # (full bw-wide blocks: padding columns of X / AX are zero, λ padded with 0)
-        lam_p = np.zeros(bw)
-        lam_p[:m] = lam
-        torch.addcmul(cur.buf[Wk.AX], cur.buf[Wk.X], _upload(lam_p, dt, dev), value=-1.0, out=cur.buf[Wk.W])
+        cur.residual(lam)
         # one Gram pass gives both the residual norms (WᵀW) and the projection
         # coefficients ([P X]ᵀW) — soft locking only selects columns of W
         b0 = Wk.P if have_p else Wk.X

@@ -514,6 +514,55 @@ def test_gram_fast_mode(pkg, rows, nslots_a, nslots_b, mask):
                                  CIM_F32, ws.data_ptr(), ws.data_ptr(), need, 0, 4, None) == 1  # unknown flag
 
 
+@pytest.mark.parametrize("rows,qs,ps", [(1, 1, 1), (100_001, 3, 2), (4099, 2, 1), (70_000, 4, 4), (50_000, 2, 2)])
+def test_tsmm_host_c_and_residual(pkg, rows, qs, ps):
+    """cim_tsmm_blocked_hc (C from host memory, in the kernel parameters)
+    matches cim_tsmm_blocked on block-major slots, including in place
+    (p ≤ 16); cim_block_residual = AX − X·diag(λ) with zero padding columns."""
+    from paper_2110_10765_b200._lib import lib
+
+    L = lib()
+    g = torch.Generator().manual_seed(rows + qs)
+    bw = 8
+    buf = torch.randn((8, rows, bw), generator=g).cuda()
+    q, p = qs * bw, ps * bw
+    C = torch.randn((q, p), generator=g)
+    out_dev = torch.randn((ps, rows, bw), generator=g).cuda()
+    out_hc = out_dev.clone()
+    bs = rows * bw
+    Cd = C.cuda()
+    Ch = C.numpy().astype(np.float32)
+    assert L.cim_tsmm_blocked(buf.data_ptr(), bw, bw, bs, q, Cd.data_ptr(), p, -1.0, 1.0, out_dev.data_ptr(), bw, bw,
+                              bs, rows, None) == 0
+    assert L.cim_tsmm_blocked_hc(buf.data_ptr(), bw, bw, bs, q, Ch.ctypes.data, p, -1.0, 1.0, out_hc.data_ptr(), bw,
+                                 bw, bs, rows, None) == 0
+    assert torch.equal(out_dev, out_hc)
+    if qs == ps and p <= 16:  # in place (one 16-column strip per thread): Out = A·C over the same slots
+        want = (buf[:qs].permute(1, 0, 2).reshape(rows, q).double().cpu() @ C.double()).float()
+        assert L.cim_tsmm_blocked_hc(buf.data_ptr(), bw, bw, bs, q, Ch.ctypes.data, p, 1.0, 0.0, buf.data_ptr(), bw,
+                                     bw, bs, rows, None) == 0
+        got = buf[:ps].permute(1, 0, 2).reshape(rows, p).cpu()
+        assert (got - want).abs().max().item() <= 1e-4 * want.abs().max().item()
+    big = np.zeros((64, 64), np.float32)
+    assert L.cim_tsmm_blocked_hc(buf.data_ptr(), bw, bw, bs, 64, big.ctypes.data, 64, 1.0, 0.0, out_hc.data_ptr(), bw,
+                                 bw, bs, rows, None) == 3  # > 1024 values: unsupported
+    # residual
+    m = 5
+    lam = np.linspace(-2.0, 3.0, m)
+    X = torch.randn((rows, bw), generator=g)
+    AX = torch.randn((rows, bw), generator=g)
+    X[:, m:] = 0
+    AX[:, m:] = 0
+    W = torch.full((rows, bw), 7.0).cuda()
+    assert L.cim_block_residual(X.cuda().data_ptr(), AX.cuda().data_ptr(), lam.ctypes.data, m, W.data_ptr(), rows, bw,
+                                None) == 0
+    lam32 = torch.zeros(bw)
+    lam32[:m] = torch.from_numpy(lam).float()
+    want = AX - X * lam32
+    assert (W.cpu() - want).abs().max().item() <= 1e-6 * (want.abs().max().item() + 1)
+    assert torch.all(W[:, m:] == 0)
+
+
 @pytest.mark.parametrize("rows,q,p,off", [(1, 1, 1, 0), (1000, 8, 8, 0), (100_001, 24, 16, 8), (5000, 7, 5, 3),
                                           (4096, 64, 64, 0)])
 def test_tsmm_matches_torch(pkg, rows, q, p, off):

@@ -39,6 +39,8 @@ with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) / a.iters
 print(f"wall per iteration {wall*1e3:.2f} ms")
+os.makedirs("gpurun_out", exist_ok=True)
+prof.export_chrome_trace("gpurun_out/lobpcg_trace.json")
 print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=25, max_name_column_width=70))
 # the device-side sequence of one iteration (the last): kernel name, duration
 evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
