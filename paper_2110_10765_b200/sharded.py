@@ -82,6 +82,8 @@ class ShardedSymSpmm:
         self.n = int(n)
         self.dtype = dtype
         self.device = torch.device(device)
+        if self.device.type == "cuda" and self.device.index is None:  # "cuda" → the current device, explicitly
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self.H = H_local
         if local_apply is None:
             if H_local is None:

@@ -118,3 +118,31 @@ def test_lobpcg_gpu_vs_eigsh(dtype):
     got = np.sort(res.eigenvalues)
     scale = np.abs(want).max()
     assert np.abs(got - want).max() <= (2e-4 if dtype == torch.float32 else 1e-7) * scale, (got, want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("derived", [True, False])
+def test_lobpcg_gpu_f32_blocks_vs_eigsh(derived):
+    """The f32 native path the C5 bench runs (fast Gram, host-coefficient
+    tsmm, fused residual, SpMM into the work buffer, derived or read-back W
+    Gram) converges to scipy eigsh's lowest eigenvalues."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2110_10765_b200 as pkg
+    from paper_2110_10765_b200.lobpcg import lobpcg
+    from paper_2110_10765_b200.sharded import ShardedSymSpmm
+
+    n, m = 8192, 8
+    rc = pkg.synthetic_pattern(n // 64, 0.03, seed=11)
+    S = ShardedSymSpmm(n, m, torch.float32, torch.device("cuda"),
+                       H_local=pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=torch.float32))
+    tiles = oracle.synthetic_dense_tiles(n, rc, seed=0).astype(np.float64)
+    i, j, v = oracle.half_tiles_to_coo(n, rc, tiles)
+    A = sp.csr_matrix((v, (i, j)), shape=(n, n))
+    want = np.sort(spla.eigsh(A, k=m, which="SA", tol=1e-10)[0])
+    X0 = torch.randn((S.rows_per_rank, m), generator=torch.Generator().manual_seed(3)).cuda()
+    X0[n:] = 0
+    res = lobpcg(S.apply, X0, tol=2e-4, max_iter=2000, derived_w_gram=derived)
+    assert res.converged
+    got = np.sort(res.eigenvalues)
+    assert np.abs(got - want).max() <= 2e-5 * np.abs(want).max(), (got, want, res.iterations)
