@@ -556,6 +556,84 @@ __global__ void __launch_bounds__(kTsmmThreads) tsmm_vec_kernel(const Operand A,
   }
 }
 
+// Block-major bw = 8 operands with C in the kernel parameters and (Q, P)
+// compile-time (the eigensolver's shapes): one thread per row, the row's Q
+// inputs as float4 pairs, every FMA takes its C value as a constant-bank
+// operand — no shared-memory traffic, so L1 only carries the row stream
+// (the generic vector kernel was L1-bound at 84% on LDS + half-sector loads).
+// A row's inputs are all read before its outputs are written: in place is
+// safe for any P.
+template <int Q, int P>
+__global__ void __launch_bounds__(256) tsmm_b8_kernel(const float *__restrict__ A, long long a_bstride,
+                                                      float *Out, long long o_bstride, long long rows, float alpha,
+                                                      float beta, const ParC C) {
+  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += (long long)gridDim.x * blockDim.x) {
+    float a[Q];
+#pragma unroll
+    for (int s = 0; s < Q / 8; ++s) {
+      const float4 *src = reinterpret_cast<const float4 *>(A + s * a_bstride + r * 8);
+      const float4 u = src[0], v = src[1];
+      a[8 * s + 0] = u.x, a[8 * s + 1] = u.y, a[8 * s + 2] = u.z, a[8 * s + 3] = u.w;
+      a[8 * s + 4] = v.x, a[8 * s + 5] = v.y, a[8 * s + 6] = v.z, a[8 * s + 7] = v.w;
+    }
+    float o[P];
+#pragma unroll
+    for (int j = 0; j < P; ++j) o[j] = 0.f;
+#pragma unroll
+    for (int i = 0; i < Q; ++i)
+#pragma unroll
+      for (int j = 0; j < P; ++j) o[j] = fmaf(a[i], C.c[i * P + j], o[j]);
+#pragma unroll
+    for (int s = 0; s < P / 8; ++s) {
+      float4 *dst = reinterpret_cast<float4 *>(Out + s * o_bstride + r * 8);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float4 w = make_float4(alpha * o[8 * s + 4 * h], alpha * o[8 * s + 4 * h + 1], alpha * o[8 * s + 4 * h + 2],
+                               alpha * o[8 * s + 4 * h + 3]);
+        if (beta != 0.f) {
+          const float4 prev = dst[h];
+          w.x = fmaf(beta, prev.x, w.x), w.y = fmaf(beta, prev.y, w.y);
+          w.z = fmaf(beta, prev.z, w.z), w.w = fmaf(beta, prev.w, w.w);
+        }
+        dst[h] = w;
+      }
+    }
+  }
+}
+
+template <int Q, int P>
+void launch_b8(const Operand &A, const ParC &C, float alpha, float beta, const MutOperand &Out, long long rows,
+               int sms, cudaStream_t stream) {
+  const long long blocks = std::min<long long>((rows + 255) / 256, 16LL * sms);
+  tsmm_b8_kernel<Q, P><<<(unsigned)blocks, 256, 0, stream>>>(static_cast<const float *>(A.p), A.bstride, Out.p,
+                                                             Out.bstride, rows, alpha, beta, C);
+}
+
+// true if (q, p) has a specialised bw = 8 kernel (and it was launched)
+bool try_tsmm_b8(const Operand &A, const ParC &C, int p, float alpha, float beta, const MutOperand &Out,
+                 long long rows, int out_bw, cudaStream_t stream) {
+  const int q = A.cols;
+  if (A.bw_shift != 3 || out_bw != 8 || A.ld != 8 || Out.ld != 8 || (A.bstride & 3) || (Out.bstride & 3) ||
+      (reinterpret_cast<uintptr_t>(A.p) & 15) || (reinterpret_cast<uintptr_t>(Out.p) & 15))
+    return false;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+#define CIM_B8(QQ, PP) \
+  if (q == QQ && p == PP) { launch_b8<QQ, PP>(A, C, alpha, beta, Out, rows, sms, stream); return true; }
+  CIM_B8(8, 8)
+  CIM_B8(16, 8)
+  CIM_B8(24, 8)
+  CIM_B8(8, 16)
+  CIM_B8(16, 16)
+  CIM_B8(24, 16)
+  CIM_B8(32, 16)
+  CIM_B8(48, 16)
+#undef CIM_B8
+  return false;
+}
+
 template <typename CS>
 int tsmm_impl(const Operand &A, const CS &C, int p, float alpha, float beta, const MutOperand &Out, long long rows,
               int out_bw, cudaStream_t stream) {
@@ -626,6 +704,11 @@ extern "C" int cim_tsmm_blocked_hc(const float *A, int64_t lda, int32_t a_bw, in
   std::memcpy(c.c, C_host, sizeof(float) * (size_t)q * p);
   const Operand a{A, lda, a_bstride, sa, q};
   const MutOperand o{Out, ldo, o_bstride, so};
+  if (rows > 0 && try_tsmm_b8(a, c, p, alpha, beta, o, rows, o_bw, reinterpret_cast<cudaStream_t>(stream_))) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cim::set_error(CIM_ECUDA, std::string("tsmm_b8: ") + cudaGetErrorString(e));
+    return CIM_OK;
+  }
   return tsmm_impl(a, c, p, alpha, beta, o, rows, o_bw, reinterpret_cast<cudaStream_t>(stream_));
 }
 
