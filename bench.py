@@ -85,6 +85,20 @@ def workload(args, world):
     return n, nb, n_off, p
 
 
+def kernel_label(dtype, k: int) -> str:
+    """The dense-tile kernel the library dispatches for (dtype, k) (pick_cfg in csrc/sym_spmm.cu)."""
+    if dtype == torch.float32 and k in (8, 16, 24, 32, 48, 64):  # wide_supported()
+        g = 2 if (k // 8) % 2 == 0 else 1
+        passes = k // (8 * g)
+        return (f"sym_spmm_k8_kernel<float, G={g}> (FFMA2, setmaxnreg warpgroups, X_R in registers"
+                + (f", {passes} passes" if passes > 1 else "") + ")")
+    if dtype == torch.float64 and k in (4, 8, 12, 16, 32):
+        g = 2 if (k // 4) % 2 == 0 else 1
+        passes = k // (4 * g)
+        return f"sym_spmm_k8_kernel<double, G={g}> (DFMA)" + (f", {passes} passes" if passes > 1 else "")
+    return "sym_spmm_kernel (FFMA/DFMA, shared-memory column reduction)"
+
+
 def measured_peaks():
     try:
         return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -392,7 +406,8 @@ def impl_ours(args):
         achieved = bytes_local / (kern_max / 1e3) / 1e9
         traffic = None
         tf = ROOT / "profiles" / "roofline_traffic.json"
-        if tf.exists():
+        c2_shape = world == 1 and args.n == N_BASE and args.tiles_per_gpu == TILES_PER_GPU and H.layout == "frag"
+        if tf.exists() and c2_shape:  # the ncu capture was of the C2 launch
             try:
                 traffic = json.loads(tf.read_text()).get(f"k{k}_{args.dtype}" + ("" if args.fill is None else f"_fill{args.fill}"))
             except Exception:
@@ -417,7 +432,10 @@ def impl_ours(args):
             "dtype": "f32" if dtype == torch.float32 else "f64",
             "data": "synthetic",
             "config": {
-                "workload": ("C2" if world == 1 else f"C3-family weak scaling ({world}x C2 tiles, same n)")
+                "workload": (("C2" if args.tiles_per_gpu == TILES_PER_GPU else
+                              "C3 on one GPU (T(1) of the strong-scaling pair)"
+                              if abs(args.tiles_per_gpu - 8 * TILES_PER_GPU) <= 8 * nb else "custom tile count")
+                             if world == 1 else f"C3-family weak scaling ({world}x C2 tiles, same n)")
                 + f": synthetic half-stored symmetric H, n={n}, block 64, {g_tiles} stored tiles "
                   f"({g_diag} diagonal + {g_off} upper), {H.nnz_stored / 1e9:.3f}e9 stored values"
                 + (f" (all tiles sparse COO-in-tile, entry fill {args.fill})" if args.fill is not None else "")
@@ -428,7 +446,7 @@ def impl_ours(args):
                 if world > 1 else "single GPU",
                 "layout": H.layout,
                 "bands": H.meta.get("bands", 1),
-                "l2": "inputs (8.3 GB per GPU) far larger than L2 (126 MB): no flush",
+                "l2": f"inputs ({bytes_local / 1e9:.1f} GB per GPU) far larger than L2 (126 MB): no flush",
                 "gflop_per_apply": flops_global / 1e9,
                 "hbm_gbs_kernel": achieved,
                 "build_s": t_build,
@@ -436,9 +454,8 @@ def impl_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
                          "kernel": "sym_spmm_tc_kernel (tcgen05 kind::tf32, 3xTF32 split)" if H.layout == "tc"
-                         else ("sparse_spmm_kernel (COO-in-tile, warp per tile)" if args.fill is not None else
-                               "sym_spmm_k8_kernel (FFMA2, setmaxnreg warpgroups, X_R in registers)"
-                               if (k == 8 and dtype == torch.float32) else "sym_spmm_kernel (FFMA2/FFMA)"),
+                         else ("sparse_spmm_kernel + sparse_small_kernel (COO-in-tile)" if args.fill is not None else
+                               kernel_label(dtype, k)),
                          "kernel_ms": kern_max,
                          "algorithmic_bytes_per_launch": bytes_local,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6650",
