@@ -164,6 +164,7 @@ class _Work:
             self._base = self.buf.data_ptr()
             self._slot_bytes = rows * self.bw * self.buf.element_size()
         self._gram_out: dict = {}
+        self._vidx: dict = {}
 
     def _ctx(self):
         import contextlib
@@ -175,10 +176,13 @@ class _Work:
 
     def vidx(self, slots, widths) -> np.ndarray:
         """Virtual column indices (slot-range-relative) of the real columns."""
-        out = []
-        for k, (s, w) in enumerate(zip(slots, widths)):
-            out.extend(k * self.bw + j for j in range(w))
-        return np.asarray(out, dtype=np.int64)
+        key = (len(slots), tuple(widths))
+        out = self._vidx.get(key)
+        if out is None:
+            out = np.concatenate([k * self.bw + np.arange(w) for k, w in enumerate(widths)]).astype(np.int64)
+            out.setflags(write=False)
+            self._vidx[key] = out
+        return out
 
     def _native(self) -> bool:
         return self.buf.is_cuda and self.buf.dtype in (torch.float32, torch.float64)
@@ -317,6 +321,24 @@ def _workspace(device, nbytes: int) -> torch.Tensor:
         ws = torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=device)
         _WS[device] = ws
     return ws
+
+
+_RR_MASKS: dict = {}
+
+
+def _rr_mask(b0: int) -> int:
+    """Block mask of the Sᵀ[S AS] Gram (slots b0..W against P..AW): the 8×8
+    slot blocks on and above the diagonals of SᵀS and SᵀAS."""
+    mask = _RR_MASKS.get(b0)
+    if mask is None:
+        ns = _Work.AP - b0
+        mask = 0
+        for bi in range(ns):
+            for bj in range(bi, ns):
+                mask |= 1 << (bi * 6 + b0 + bj)
+                mask |= 1 << (bi * 6 + b0 + 3 + bj)
+        _RR_MASKS[b0] = mask
+    return mask
 
 
 def _embed(M: np.ndarray, rows_idx: np.ndarray, cols_idx: np.ndarray, shape) -> np.ndarray:
@@ -459,15 +481,15 @@ def lobpcg(apply: Callable[[torch.Tensor], torch.Tensor], X0: torch.Tensor, *, t
         sidx = cur.vidx(range(b0, Wk.AP), [m] * (Wk.W - b0) + [nw])
         # SᵀS and SᵀAS are symmetric: compute the slot blocks on and above
         # their diagonals only (bw = 8: one slot = one 8×8 block), mirror here
-        ns = Wk.AP - b0
-        mask = 0
-        for bi in range(ns):
-            for bj in range(bi, ns):
-                mask |= 1 << (bi * 6 + b0 + bj)
-                mask |= 1 << (bi * 6 + b0 + 3 + bj)
+        mask = _rr_mask(b0)
         MG = cur.gram(b0, Wk.AP, Wk.P, Wk.AW + 1, group, block_mask=mask)
-        M = MG[np.ix_(sidx, sidx + b0 * bw)]
-        G = MG[np.ix_(sidx, sidx + (b0 + 3) * bw)]
+        if sidx.size == sidx[-1] + 1:  # every column real (m = bw, nothing locked): plain slices
+            ns_r = sidx.size
+            M = MG[:ns_r, b0 * bw:b0 * bw + ns_r]
+            G = MG[:ns_r, (b0 + 3) * bw:(b0 + 3) * bw + ns_r]
+        else:
+            M = MG[np.ix_(sidx, sidx + b0 * bw)]
+            G = MG[np.ix_(sidx, sidx + (b0 + 3) * bw)]
         if bw == 8:
             M = np.triu(M) + np.triu(M, 1).T
             G = np.triu(G) + np.triu(G, 1).T
