@@ -184,6 +184,23 @@ def cpu_sample(n, nb, p, k, sample_tiles):
     return cpu.F32Problem(rc, tiles, X), rc.shape[0]
 
 
+def host_cpu_info() -> dict:
+    """The host the CPU legs ran on (core counts and model)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        affinity = len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        affinity = None
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(), "affinity_cpus": affinity}
+
+
 def run_cpu(n, nb, p, k, budget_s, sample_tiles=24576, min_reps=3):
     from oracle import cpu
 
@@ -208,6 +225,7 @@ def run_cpu(n, nb, p, k, budget_s, sample_tiles=24576, min_reps=3):
                    f"values, k={k} f32), median of {len(times)} reps after 1 warmup, OpenMP private-Y "
                    f"(array_clause discipline) on {threads} threads; os.cpu_count()={os.cpu_count()}"),
         "ms_per_apply": med * 1e3,
+        "host": host_cpu_info(),
     }
 
 
@@ -233,7 +251,7 @@ def impl_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"C2 sample: first {ntiles} tiles of the n={n} synthetic half-stored H, k={args.k}",
                    "n": n, "k": args.k, "sample_tiles": int(ntiles)},
-        "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": threads, "kind": "port", "host": host_cpu_info(),
                          "sample": f"{ntiles} tiles of C2 per step (oracle/sym_spmm_ref.c, OpenMP, "
                                    f"{threads} threads; reference has no SpMM — SPEC.md:388)"},
         "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
