@@ -51,6 +51,10 @@ def _worker(rank, world, port, n, p, seed, k, result_q):
         X[n:] = 0
         lo = rank * S.rows_per_rank
         Y_local = S.apply(X[lo:lo + S.rows_per_rank].clone())
+        # apply(out=): the reduce-scatter lands in the caller's buffer
+        out = torch.full((S.rows_per_rank, k), 7.0, dtype=torch.float64)
+        Y_out = S.apply(X[lo:lo + S.rows_per_rank].clone(), out=out)
+        assert Y_out.data_ptr() == out.data_ptr() and torch.equal(out, Y_local)
         result_q.put((rank, lo, Y_local.numpy().copy(), t1 - t0))
     finally:
         dist.destroy_process_group()
