@@ -15,9 +15,13 @@ C-ABI in ``libcim_b200.so``, include/cim_b200.h):
   ``STRATEGIES``, ``OP_KINDS`` — the reference's observables API on the GPU
 * ``lobpcg`` / ``lobpcg_sym`` — block LOBPCG eigensolver over the SpMM
   (single GPU or row-sharded with the 3m×3m Gram all-reduce)
+* ``load_basis`` / ``save_basis`` / ``group_basis`` and
+  ``HalfTiles.from_basis_file`` — reference basis files (mbstate.py:242-267)
+  to the device matrix without the Python skeleton build
 """
 
 from ._lib import BLOCK, CimError, lib
+from .construct import group_basis, load_basis, save_basis
 from .halftiles import HalfTiles, partition_units, plan_units, synthetic_pattern
 from .lobpcg import LobpcgResult, lobpcg, lobpcg_sym
 from .observables import (
@@ -42,7 +46,9 @@ __all__ = [
     "STRATEGIES",
     "ShardedSymSpmm",
     "contract_observables",
+    "group_basis",
     "lib",
+    "load_basis",
     "lobpcg",
     "lobpcg_sym",
     "padded_k",
@@ -50,6 +56,7 @@ __all__ = [
     "plan_units",
     "random_coefficients",
     "row_chunks",
+    "save_basis",
     "supported_k",
     "sym_spmm",
     "sym_spmm_host_batch",

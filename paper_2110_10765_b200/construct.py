@@ -42,6 +42,102 @@ from .halftiles import (
 )
 
 
+BITREP_WIDTH = 64  # mbstate.py: states 1..64 pack into bits_lo
+DEFAULT_GROUP_BITS = 16  # pipeline.py:64
+
+
+def _pack_lo(occ: np.ndarray) -> np.ndarray:
+    """bits_lo of each state: bit a-1 set iff a ≤ 64 is occupied (ManyBodyState.bitrep)."""
+    lo = np.zeros(occ.shape[0], dtype=np.uint64)
+    for q in range(occ.shape[1]):
+        a = occ[:, q].astype(np.int64)
+        m = a <= BITREP_WIDTH
+        lo[m] |= np.left_shift(np.uint64(1), (a[m] - 1).astype(np.uint64))
+    return lo
+
+
+def load_basis(path) -> tuple[np.ndarray, np.ndarray, int]:
+    """Read a reference basis file ("N n_sp" header, one space-separated
+    occupation list per line; mbstate.py:249-267) → (occ uint16 (n, N),
+    bits_lo uint64 (n,), n_sp), with the reference's validation and
+    ValueError messages (malformed header / state line, empty file, wrong
+    particle count, index out of 1..n_sp, not strictly increasing, duplicate
+    state)."""
+    from pathlib import Path
+
+    text = Path(path).read_text().splitlines()
+    if not text:
+        raise ValueError(f"{path}: empty basis file")
+    try:
+        n_particles, n_sp = (int(t) for t in text[0].split())
+    except ValueError as e:
+        raise ValueError(f"{path}:1: malformed header (want 'N n_sp'): {text[0]!r}") from e
+    rows = []
+    seen = set()
+    for lineno, line in enumerate(text[1:], start=2):
+        if not line.strip():
+            continue
+        try:
+            occ = tuple(int(t) for t in line.split())
+        except ValueError as e:
+            raise ValueError(f"{path}:{lineno}: malformed state line {line!r}") from e
+        for prev, cur in zip(occ, occ[1:]):
+            if cur <= prev:
+                raise ValueError(f"occupation list must be strictly increasing, got {occ}")
+        if occ and occ[0] < 1:
+            raise ValueError(f"occupation indices are 1-based, got {occ}")
+        if occ and occ[-1] > n_sp:
+            raise ValueError(f"occupied index {occ[-1]} out of range 1..{n_sp}")
+        if len(occ) != n_particles:
+            raise ValueError(f"state {len(rows)} has {len(occ)} particles, basis requires {n_particles}")
+        if occ in seen:
+            raise ValueError(f"duplicate state at position {len(rows)}: {occ}")
+        seen.add(occ)
+        rows.append(occ)
+    if not rows:
+        raise ValueError(f"{path}: no states after header")
+    occ = np.array(rows, dtype=np.uint16).reshape(len(rows), n_particles)
+    return occ, _pack_lo(occ), n_sp
+
+
+def save_basis(path, occ: np.ndarray, n_sp: int) -> None:
+    """Write a basis in the reference's file format (mbstate.py:242-246)."""
+    from pathlib import Path
+
+    occ = np.asarray(occ)
+    lines = [f"{occ.shape[1]} {int(n_sp)}"]
+    lines.extend(" ".join(str(int(a)) for a in row) for row in occ)
+    Path(path).write_text("\n".join(lines) + "\n")
+
+
+def group_basis(occ: np.ndarray, bits_lo: np.ndarray, group_bits: int = DEFAULT_GROUP_BITS):
+    """The reference's grouping (group_orbitals with bitrep_prefix_key,
+    pipeline.py:123-159): states reordered so equal keys bits_lo & (2^gb − 1)
+    are contiguous, groups by ascending key, input order inside a group.
+    Returns (occ, bits_lo, perm, orbital_starts) in grouped order."""
+    if not 1 <= group_bits <= 64:
+        raise ValueError(f"group_bits must be in 1..64, got {group_bits}")
+    mask = np.uint64((1 << group_bits) - 1) if group_bits < 64 else np.uint64(0xFFFFFFFFFFFFFFFF)
+    keys = np.asarray(bits_lo, dtype=np.uint64) & mask
+    perm = np.argsort(keys, kind="stable")
+    k = keys[perm]
+    starts = np.flatnonzero(np.concatenate([[True], k[1:] != k[:-1]]))
+    return np.ascontiguousarray(occ[perm]), np.ascontiguousarray(bits_lo[perm]), perm, starts
+
+
+def from_basis_file(path, *, group_bits: int = DEFAULT_GROUP_BITS, **kw) -> HalfTiles:
+    """A reference basis file straight to the device matrix: load_basis →
+    group_basis (the reference's state order) → from_basis.  The result's
+    meta records the grouping permutation (``perm[i]`` = file line of grouped
+    state i)."""
+    occ, lo, n_sp = load_basis(path)
+    g_occ, g_lo, perm, starts = group_basis(occ, lo, group_bits)
+    H = from_basis(g_occ, g_lo, **kw)
+    H.meta.update(basis_file=str(path), group_bits=group_bits, n_sp=n_sp, n_orbitals=int(starts.size))
+    H.basis_perm = perm
+    return H
+
+
 def _words(basis_or_occ, bits_lo):
     """(occ uint16 (n, N), bits_lo uint64 (n,)) from a reference ``Basis``
     (mbstate.py: occ_mat / bits_lo) or from raw arrays."""

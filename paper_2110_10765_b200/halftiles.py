@@ -690,6 +690,15 @@ class HalfTiles:
         return from_basis(basis_or_occ, bits_lo, **kw)
 
     @classmethod
+    def from_basis_file(cls, path, **kw) -> "HalfTiles":
+        """A reference basis file (mbstate.py save_basis format) → grouped
+        (group_orbitals order) → built on the device; see
+        ``paper_2110_10765_b200.construct.from_basis_file``."""
+        from .construct import from_basis_file
+
+        return from_basis_file(path, **kw)
+
+    @classmethod
     def from_skeleton(cls, skeleton, orbitals, n: int | None = None, **kw) -> "HalfTiles":
         """From a reference ``SparseSkeleton`` (pipeline.py:96-116) and its
         orbitals: rows are recovered from the per-(tile,row) segments

@@ -23,7 +23,9 @@ It imports the reference package ``cimotifs`` from
 
 Each skeleton fixture also carries its grouped basis (occupation lists and
 packed words) so the GPU construction (HalfTiles.from_basis) can be checked
-against the reference's own build_skeleton output.
+against the reference's own build_skeleton output, and basis_<name>.txt is
+the same basis in sampled order written by the reference's save_basis
+(mbstate.py:242-246; `--basis-files` regenerates only these).
 
 The GPU box never reads /root/reference: tests load only these files.
 """
@@ -44,7 +46,7 @@ os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_golden")
 sys.path.insert(0, str(REF))
 
 from cimotifs._util import digest  # noqa: E402
-from cimotifs.mbstate import CALIBRATION_BIAS, random_basis  # noqa: E402
+from cimotifs.mbstate import CALIBRATION_BIAS, random_basis, save_basis  # noqa: E402
 from cimotifs.pipeline import (  # noqa: E402
     ObservablesInput,
     _h_value,
@@ -144,8 +146,26 @@ def skeleton_fixture(name, n, particles, bias, group_bits, seed, n_vec, m_ops, o
     print(f"{name}: n={n} nnz={sk.nnz} tiles={len(tiles)} orbitals={len(orbs)} digest={pair_digest}")
 
 
+def basis_files():
+    """The fixtures' bases as reference basis files (save_basis, mbstate.py:242-246),
+    in sampled (ungrouped) order, plus the grouping they were built with."""
+    meta = {}
+    for name, n, particles, bias, group_bits, seed in (
+            ("skel_small", 192, 6, 0.2, 8, 13), ("skel_n1024", 1024, 6, 0.2, 8, 0),
+            ("skel_identity", 1024, 8, CALIBRATION_BIAS, 8, 0)):
+        basis = random_basis(n, particles, bias=bias, seed=seed)
+        save_basis(basis, OUT / f"basis_{name}.txt")
+        meta[name] = {"group_bits": group_bits, "n": n}
+    (OUT / "basis_files.json").write_text(json.dumps(meta, indent=1))
+    print("basis files:", sorted(meta))
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["--basis-files"]:
+        basis_files()
+        sys.exit(0)
     hash_kat()
+    basis_files()
     skeleton_fixture("skel_small.npz", n=192, particles=6, bias=0.2, group_bits=8, seed=13,
                      n_vec=4, m_ops=3, op_kind="symmetric_hash", coeff_kind="gauss",
                      coeff_seed=2, op_seed=4)

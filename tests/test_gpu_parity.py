@@ -743,6 +743,25 @@ def test_from_basis_matches_reference_build(pkg, name, dense_fill):
     assert np.linalg.norm(Yd.cpu().numpy() - f["Y_ref"]) / np.linalg.norm(f["Y_ref"]) <= 1e-5
 
 
+@pytest.mark.parametrize("name", ["skel_small", "skel_n1024", "skel_identity"])
+def test_from_basis_file_matches_reference_build(pkg, name):
+    """A reference basis file (save_basis format, sampled order) → grouped →
+    built on the device: the reference skeleton's pair set and value bits,
+    and the operator matches the reference product."""
+    meta = json.loads((GOLDEN / "basis_files.json").read_text())[name]
+    f = load_fixture(f"{name}.npz")
+    H = pkg.HalfTiles.from_basis_file(GOLDEN / f"basis_{name}.txt", group_bits=meta["group_bits"],
+                                      rank=int(f["rank_threshold"]) // 2, value_seed=int(f["value_seed"]))
+    n = int(f["n"])
+    rc, tiles = H.export_dense()
+    i, j, v = oracle.half_tiles_to_coo(n, rc, tiles)
+    assert oracle.pair_set_digest(i, j) == str(f["pair_digest"])
+    X = torch.from_numpy(f["X"]).cuda()
+    Y = pkg.sym_spmm(H, X).cpu().numpy()
+    assert np.linalg.norm(Y - f["Y_ref"]) / np.linalg.norm(f["Y_ref"]) <= 1e-5
+    assert H.meta["n_orbitals"] == f["orb"].shape[0]
+
+
 @pytest.mark.parametrize("dtype,k", [(torch.float32, 8), (torch.float32, 16), (torch.float64, 8)])
 @pytest.mark.parametrize("world", [1, 3, 8])
 def test_chunked_apply_virtual_ranks(pkg, dtype, k, world):
