@@ -20,11 +20,14 @@
 // mix64(lo + φ·hi) once, and for each of its ≤ 4 operators two mix64 and one
 // int→f32 conversion, accumulating acc[k][v] += p_v·O_ij(k) in f32 registers —
 // the "per-(v,k) register reduction".  Slots split the operators (GK groups of
-// 4) and, when there are fewer operator groups, the columns.  At the end each
-// warp reduces its accumulators with shuffles and adds them to the f64 accum
-// with one atomic per (v, k).  The host loops over chunks of 16 vectors and
-// 4·GK operators.  The work per pair is integer hashing (~25 ALU ops per
-// operator): the kernel is ALU-bound, not HBM-bound.
+// KS ≤ 4, chosen from m so no hash is computed for nothing when m < 4) and,
+// when there are fewer operator groups, the columns; the identity operator
+// is one walk added to every column.  At the end each warp reduces its
+// accumulators with shuffles and adds them to the f64 accum with one atomic
+// per (v, k).  The host loops over chunks of 16 vectors and 16 operators.
+// The work per pair is integer hashing (~34 ALU-pipe ops per operator for
+// two 64-bit mix64 and the conversion): the kernel is ALU-bound (ncu: ALU
+// pipe 71%), not HBM-bound.
 #include <cstdint>
 #include <string>
 
@@ -52,7 +55,6 @@ struct ContractArgs {
   const float *c;  // (n, n_vec) row-major
   int n_vec, v0, nv;
   int m_ops, k0, kc;
-  int kind;  // CIM_VALUES_OP_HASH (1) or CIM_VALUES_IDENTITY (2)
   uint64_t seed;
   double *accum;  // (n_vec, m_ops) row-major
 };
@@ -212,7 +214,6 @@ int run_contract(const cim_half_tiles *H, const float *c, int n_vec, int m_ops, 
   a.c = c;
   a.n_vec = n_vec;
   a.m_ops = m_ops;
-  a.kind = kind;
   a.seed = seed;
   a.accum = accum;
   const long long total = a.n_dense + a.n_sparse;
