@@ -15,6 +15,9 @@
 // one vector red.global per row / column and vector half.  No atomics inside
 // a tile (shared-memory f32 atomicAdd is a CAS loop on sm_100; a first
 // version built on it ran 4× slower than streaming the tiles dense).
+// Tiles of at most cim_sparse_small_max() padded entries skip the ring and go
+// to sparse_small_kernel (entry-parallel, straight from global memory); the
+// split is the staged_tiles / small_tiles lists of cim_sparse_tiles.
 #include <cstdint>
 #include <cstdlib>
 #include <mutex>
