@@ -1021,6 +1021,9 @@ struct DeviceState {
   int sms = 0;
   unsigned int *counters = nullptr;  // ring of scheduler counters
   int ring_pos = 0;
+  // grow-only scratch per stream (pass-major X copies): work on one stream is
+  // ordered, so reusing that stream's buffer across calls is race-free
+  std::vector<std::pair<cudaStream_t, std::pair<void *, size_t>>> scratch;
 };
 constexpr int kCounterRing = 4096;
 std::mutex g_mu;
@@ -1052,6 +1055,30 @@ unsigned int *take_counters(DeviceState *d, int n) {
   unsigned int *p = d->counters + d->ring_pos;
   d->ring_pos += n;
   return p;
+}
+
+// This stream's scratch buffer of at least `bytes` (grown on demand; the old
+// buffer is released after the stream's queued work, cudaFreeAsync).
+int stream_scratch(DeviceState *d, cudaStream_t stream, size_t bytes, void **out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (auto &e : d->scratch)
+    if (e.first == stream) {
+      if (e.second.second < bytes) {
+        cudaFreeAsync(e.second.first, stream);
+        void *p = nullptr;
+        const cudaError_t err = cudaMallocAsync(&p, bytes, stream);
+        if (err != cudaSuccess) return set_error(CIM_ECUDA, std::string("scratch: ") + cudaGetErrorString(err));
+        e.second = {p, bytes};
+      }
+      *out = e.second.first;
+      return CIM_OK;
+    }
+  void *p = nullptr;
+  const cudaError_t err = cudaMallocAsync(&p, bytes, stream);
+  if (err != cudaSuccess) return set_error(CIM_ECUDA, std::string("scratch: ") + cudaGetErrorString(err));
+  d->scratch.push_back({stream, {p, bytes}});
+  *out = p;
+  return CIM_OK;
 }
 
 struct LaunchCfg {
@@ -1233,6 +1260,48 @@ int launch_k8(const cim_half_tiles *H, const Chunks &ck, long long ldy, cudaStre
   return CIM_OK;
 }
 
+// X (n_pad × k, row-major) → pass-major slices Xp[ps] (n_pad × W): each
+// 16-byte chunk of a row goes to its pass slice.
+__global__ void pass_major_kernel(const uint4 *__restrict__ X, uint4 *__restrict__ Xp, long long rows, int row_chunks,
+                                  int w_chunks) {
+  const long long total = rows * row_chunks;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / row_chunks;
+    const int c = (int)(e - r * row_chunks);
+    const int ps = c / w_chunks, cc = c - ps * w_chunks;
+    Xp[((long long)ps * rows + r) * w_chunks + cc] = X[e];
+  }
+}
+
+// k = passes × W with W = the kernel's vectors per pass: run each pass as its
+// own W-wide apply on a pass-major copy of X (Y written in place with its
+// row stride), so a pass stages only its W columns of X_C / X_R instead of
+// whole k-wide rows.
+template <typename T, int G>
+int launch_k8_passes(const cim_half_tiles *H, const void *X, void *Y, int k, long long ldy, cudaStream_t stream,
+                     DeviceState *ds) {
+  constexpr int W = WideE<T>::VPG * G;
+  const int passes = k / W;
+  const long long n_pad = (H->n + kBlock - 1) / kBlock * kBlock;
+  void *Xp = nullptr;
+  int rc = stream_scratch(ds, stream, (size_t)n_pad * k * sizeof(T), &Xp);
+  if (rc) return rc;
+  const int row_chunks = k * (int)sizeof(T) / 16, w_chunks = W * (int)sizeof(T) / 16;
+  const long long total = n_pad * row_chunks;
+  pass_major_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 16LL * ds->sms), 256, 0, stream>>>(
+      static_cast<const uint4 *>(X), static_cast<uint4 *>(Xp), n_pad, row_chunks, w_chunks);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("pass_major_kernel: ") + cudaGetErrorString(e));
+  for (int ps = 0; ps < passes && rc == CIM_OK; ++ps) {
+    Chunks ck;
+    ck.x[0] = static_cast<const T *>(Xp) + (size_t)ps * n_pad * W;
+    ck.y[0] = static_cast<T *>(Y) + ps * W;
+    rc = launch_k8<T, G, W>(H, ck, ldy, stream, ds);
+  }
+  return rc;
+}
+
 // The wide-register kernel for (dtype, k), or EUNSUPPORTED.
 int launch_wide(const cim_half_tiles *H, int k, const Chunks &ck, long long ldy, cudaStream_t stream,
                 DeviceState *ds) {
@@ -1336,6 +1405,13 @@ static int sym_spmm_dense(const cim_half_tiles *H, const void *X, void *Y, int32
 
 #ifndef CIM_NO_K8
   if (H->layout == CIM_LAYOUT_FRAG && wide_supported(H->dtype, k)) {
+#ifndef CIM_K8_ROW_PASSES
+    // multi-pass widths: one W-wide apply per pass on a pass-major copy of X
+    if (H->dtype == CIM_F32 && (k == 32 || k == 48 || k == 64)) return launch_k8_passes<float, 2>(H, X, Y, k, ldy, stream, ds);
+    if (H->dtype == CIM_F32 && k == 24) return launch_k8_passes<float, 1>(H, X, Y, k, ldy, stream, ds);
+    if (H->dtype == CIM_F64 && (k == 16 || k == 32)) return launch_k8_passes<double, 2>(H, X, Y, k, ldy, stream, ds);
+    if (H->dtype == CIM_F64 && k == 12) return launch_k8_passes<double, 1>(H, X, Y, k, ldy, stream, ds);
+#endif
     Chunks ck;
     ck.x[0] = X;
     ck.y[0] = Y;
