@@ -34,8 +34,10 @@
 // shipped build defines none): CIM_NO_K8 (generic kernel for every k),
 // CIM_ROWFLUSH_SMEM (4-warp shared-memory row sum before the row flush),
 // CIM_DIAG_BRANCH (separate diagonal-tile body in the generic kernel),
-// CIM_K8_X_NORMAL / CIM_K8_Y_LAST (L2 policies of X copies / Y atomics).
-// Their measured effects are in profiles/r01/SUMMARY.md.
+// CIM_K8_X_NORMAL / CIM_K8_Y_LAST (L2 policies of X copies / Y atomics),
+// CIM_K8_ROW_PASSES (multi-pass widths over whole k-wide X rows instead of a
+// pass-major copy).  Their measured effects are in profiles/r01/SUMMARY.md
+// and DESIGN.md §5.
 #include <algorithm>
 #include <type_traits>
 #include <cstdlib>
