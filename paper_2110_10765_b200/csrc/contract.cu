@@ -28,6 +28,7 @@
 // The work per pair is integer hashing (~34 ALU-pipe ops per operator for
 // two 64-bit mix64 and the conversion): the kernel is ALU-bound (ncu: ALU
 // pipe 71%), not HBM-bound.
+#include <algorithm>
 #include <cstdint>
 #include <string>
 
@@ -52,6 +53,7 @@ struct ContractArgs {
   const uint16_t *sp_rowptr;
   const uint8_t *sp_col, *sp_row;
   const T *sp_vals;
+  const int32_t *sp_list;  // optional: the sparse tiles this kernel walks (else all n_sparse)
   const float *c;  // (n, n_vec) row-major
   int n_vec, v0, nv;
   int m_ops, k0, kc;
@@ -86,7 +88,7 @@ __global__ void __launch_bounds__(kCtThreads, KS == 4 ? 2 : 3) contract_kernel(C
   const long long total = a.n_dense + a.n_sparse;
   for (long long t = blockIdx.x; t < total; t += gridDim.x) {
     const bool dense = t < a.n_dense;
-    const long long u = dense ? t : t - a.n_dense;
+    const long long u = dense ? t : (a.sp_list ? (long long)a.sp_list[t - a.n_dense] : t - a.n_dense);
     const int2 RC = dense ? a.rc[u] : a.sp_rc[u];
     if (tid < 128) rowmask[tid >> 1][tid & 1] = 0u;
     // stage the two c blocks (zero outside the matrix / vector chunk)
@@ -176,6 +178,92 @@ __global__ void __launch_bounds__(kCtThreads, KS == 4 ? 2 : 3) contract_kernel(C
   }
 }
 
+// Small sparse tiles (the cim_sparse_tiles.small_tiles list — basis-built
+// skeletons hold millions of tiles of a few dozen entries): staging two
+// 64-row c blocks and 64 row masks per tile would cost more than the tile's
+// pairs.  One warp per tile, lane per entry: c[i, ·] and c[j, ·] are read
+// straight from global memory (L2-resident for these n), then the same
+// per-pair work as contract_kernel into per-thread accumulators for KS
+// operators.  The host loops over operator chunks of KS.
+template <typename T, int NV, int KS, bool IDENT>
+__global__ void __launch_bounds__(256) contract_small_kernel(ContractArgs<T> a, const int32_t *list, long long n_list) {
+  const int lane = threadIdx.x & 31;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  uint64_t kq[KS];
+#pragma unroll
+  for (int q = 0; q < KS; ++q) kq[q] = (uint64_t)(a.k0 + q + 1) * kMix1;
+  float acc[KS][NV];
+#pragma unroll
+  for (int q = 0; q < KS; ++q)
+#pragma unroll
+    for (int v = 0; v < NV; ++v) acc[q][v] = 0.f;
+  for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_list; w += nw) {
+    const long long u = __ldg(list + w);
+    const long long base = __ldg(a.sp_off + u);
+    const int cnt = __ldg(a.sp_rowptr + u * kSpPtrStride + 64);
+    const int2 RC = __ldg(a.sp_rc + u);
+    const float wgt = RC.x == RC.y ? 1.f : 2.f;
+    for (int e = lane; e < cnt; e += 32) {
+      if (__ldg(a.sp_vals + base + e) == T(0)) continue;
+      const long long i = (long long)RC.x * 64 + __ldg(a.sp_row + base + e);
+      const long long j = (long long)RC.y * 64 + __ldg(a.sp_col + base + e);
+      if (i >= a.n || j >= a.n) continue;
+      float p[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const bool on = v < a.nv;
+        const float ci = on ? __ldg(a.c + i * a.n_vec + a.v0 + v) : 0.f;
+        const float cj = on ? __ldg(a.c + j * a.n_vec + a.v0 + v) : 0.f;
+        p[v] = wgt * ci * cj;
+      }
+      if constexpr (IDENT) {
+        if (i == j)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) acc[0][v] += p[v];
+      } else {
+        const uint64_t lo = (uint64_t)(i < j ? i : j), hi = (uint64_t)(i < j ? j : i);
+        const uint64_t hb = mix64(lo + kGolden * hi);
+#pragma unroll
+        for (int q = 0; q < KS; ++q) {
+          const float o = to_unit(mix64(mix64(hb ^ kq[q]) ^ a.seed));
+#pragma unroll
+          for (int v = 0; v < NV; ++v) acc[q][v] = fmaf(p[v], o, acc[q][v]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < KS; ++q) {
+    if (!IDENT && q >= a.kc) continue;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      float s = acc[q][v];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0 && v < a.nv) {
+        double *dst = a.accum + (long long)(a.v0 + v) * a.m_ops;
+        if (IDENT)
+          for (int k = 0; k < a.m_ops; ++k) atomicAdd(dst + k, (double)s);
+        else
+          atomicAdd(dst + a.k0 + q, (double)s);
+      }
+    }
+  }
+}
+
+template <typename T, int NV>
+void launch_small_nv(const ContractArgs<T> &a, bool ident, const int32_t *list, long long n_list, int grid,
+                     cudaStream_t s) {
+  if (ident)
+    contract_small_kernel<T, NV, 1, true><<<grid, 256, 0, s>>>(a, list, n_list);
+  else if (a.kc == 1)
+    contract_small_kernel<T, NV, 1, false><<<grid, 256, 0, s>>>(a, list, n_list);
+  else if (a.kc <= 4)
+    contract_small_kernel<T, NV, 4, false><<<grid, 256, 0, s>>>(a, list, n_list);
+  else
+    contract_small_kernel<T, NV, 8, false><<<grid, 256, 0, s>>>(a, list, n_list);
+}
+
 template <typename T, int NV>
 void launch_nv(const ContractArgs<T> &a, bool ident, int grid, cudaStream_t s) {
   if (ident)
@@ -216,13 +304,42 @@ int run_contract(const cim_half_tiles *H, const float *c, int n_vec, int m_ops, 
   a.m_ops = m_ops;
   a.seed = seed;
   a.accum = accum;
+  // the sparse split of cim_sparse_tiles: staged tiles through the mask
+  // kernel, small ones entry-parallel (NULL lists: every tile in the mask kernel)
+  const bool listed = S && S->n_tiles > 0 && (S->staged_tiles || S->small_tiles);
+  const int32_t *small = listed ? S->small_tiles : nullptr;
+  const long long n_small = (listed && S->small_tiles) ? S->n_small : 0;
+  if (listed) {
+    a.sp_list = S->staged_tiles;
+    a.n_sparse = S->staged_tiles ? S->n_staged : 0;
+  }
   const long long total = a.n_dense + a.n_sparse;
-  if (total == 0) return CIM_OK;
+  if (total == 0 && n_small == 0) return CIM_OK;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)(total < (long long)sms * 8 ? total : (long long)sms * 8);
+  const int grid_small = (int)std::min<long long>((n_small + 7) / 8, (long long)sms * 16);
   const bool ident = kind == CIM_VALUES_IDENTITY;
+  if (n_small > 0) {
+    constexpr int kSmallKs = 8;
+    for (int v0 = 0; v0 < n_vec; v0 += 8) {
+      a.v0 = v0;
+      a.nv = n_vec - v0 < 8 ? n_vec - v0 : 8;
+      for (int k0 = 0; k0 < (ident ? 1 : m_ops); k0 += kSmallKs) {
+        a.k0 = k0;
+        a.kc = m_ops - k0 < kSmallKs ? m_ops - k0 : kSmallKs;
+        if (a.nv <= 4)
+          launch_small_nv<T, 4>(a, ident, small, n_small, grid_small, stream);
+        else
+          launch_small_nv<T, 8>(a, ident, small, n_small, grid_small, stream);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess)
+          return set_error(CIM_ECUDA, std::string("contract_small_kernel: ") + cudaGetErrorString(e));
+      }
+    }
+  }
+  if (total == 0) return CIM_OK;
   for (int v0 = 0; v0 < n_vec; v0 += 16) {
     a.v0 = v0;
     a.nv = n_vec - v0 < 16 ? n_vec - v0 : 16;
