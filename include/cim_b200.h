@@ -127,6 +127,9 @@ typedef struct cim_sparse_tiles {
   int64_t         n_staged;
   const int32_t  *small_tiles;
   int64_t         n_small;
+  /* Largest padded entry count among the staged tiles (0 = unknown); at
+     ≤ 512 the staged kernel uses smaller shared-memory stages. */
+  int64_t         staged_max_entries;
 } cim_sparse_tiles;
 
 typedef struct cim_half_tiles {

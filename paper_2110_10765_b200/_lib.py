@@ -77,6 +77,7 @@ class CimSparseTiles(ctypes.Structure):
         ("n_staged", ctypes.c_int64),
         ("small_tiles", ctypes.c_void_p),
         ("n_small", ctypes.c_int64),
+        ("staged_max_entries", ctypes.c_int64),
     ]
 
 

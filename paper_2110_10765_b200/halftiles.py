@@ -249,14 +249,15 @@ class SparseTiles:
             small = np.flatnonzero((ne > 0) & (ne <= thr)).astype(np.int32)
             dev = self.tile_rc.device
             mk = lambda a: torch.from_numpy(a if a.size else np.zeros(1, np.int32)).to(dev)  # noqa: E731
-            self._split = (mk(staged), staged.size, mk(small), small.size)
+            self._split = (mk(staged), staged.size, mk(small), small.size,
+                           int(ne[staged].max()) if staged.size else 0)
         return self._split[0][: self._split[1]], self._split[2][: self._split[3]]
 
     def descriptor(self) -> CimSparseTiles:
         if self._desc is None:
             e = self.n_entries > 0
             self.work_split()
-            st, n_st, sm, n_sm = self._split
+            st, n_st, sm, n_sm, st_max = self._split
             self._desc = CimSparseTiles(n_tiles=self.n_tiles, n_entries=self.n_entries,
                                         tile_rc=self.tile_rc.data_ptr(), entry_off=self.entry_off.data_ptr(),
                                         rowptr=self.rowptr.data_ptr(), colptr=self.colptr.data_ptr(),
@@ -264,7 +265,7 @@ class SparseTiles:
                                         cperm=self.cperm.data_ptr() if e else None,
                                         vals=self.vals.data_ptr() if e else None,
                                         staged_tiles=st.data_ptr(), n_staged=n_st,
-                                        small_tiles=sm.data_ptr(), n_small=n_sm)
+                                        small_tiles=sm.data_ptr(), n_small=n_sm, staged_max_entries=st_max)
         return self._desc
 
     def with_values(self, vals: torch.Tensor) -> "SparseTiles":
