@@ -193,11 +193,12 @@ def dense_break_even(dtype) -> float:
     return 0.5 if _as_torch_dtype(dtype) == torch.float32 else 2.0 / 3.0
 
 
-# Time break-even on B200 (C2 pattern, k = 8 f32, profiles/r01/SUMMARY.md):
-# all-sparse storage runs 1.27 / 1.57 / 2.17 / 3.09 ms at 2 / 5 / 10 / 17%
-# entry fill against 1.63 ms for the same tiles stored dense, so tiles below
-# ~5% fill are faster sparse.  The default split optimises time.
-DEFAULT_DENSE_FILL = 0.05
+# Time break-even on B200 (C2 pattern, k = 8 f32, profiles/r01/sparse_small.md):
+# all-sparse storage runs 1.25 / 1.16 / 1.74 / 2.41 / 3.03 ms at
+# 3 / 5 / 9 / 13 / 17% entry fill against 1.61 ms for the same tiles stored
+# dense, so tiles below ~8% fill are faster sparse.  The default split
+# optimises time (with a margin).
+DEFAULT_DENSE_FILL = 0.075
 
 
 @dataclass
