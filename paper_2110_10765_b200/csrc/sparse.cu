@@ -452,8 +452,12 @@ int launch_sparse(const cim_sparse_tiles *S, const void *X, void *Y, int k, long
   const int cap = (S->staged_max_entries > 0 && S->staged_max_entries <= kSpCapSmall) ? kSpCapSmall : kSpCap;
   const SpLayout L = sp_layout(k, (int)sizeof(T), cap);
   // 8 stages (2 per consumer warp) when two CTAs fit per SM, else 4
+#ifdef CIM_SP_STAGES
+  int stages = CIM_SP_STAGES;  // A/B experiments (a multiple of 4)
+#else
   int stages = ((size_t)8 * L.bytes + 128 <= 113 * 1024) ? 8 : 4;
-  const size_t smem = (size_t)stages * L.bytes + 128;
+#endif
+  const size_t smem = (size_t)stages * L.bytes + 16 * (size_t)stages;  // + full / empty mbarriers
   if (smem > 227 * 1024) return set_error(CIM_EUNSUPPORTED, "k too large for the sparse-tile stages");
   unsigned int *ctr;
   {
