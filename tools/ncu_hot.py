@@ -1,9 +1,16 @@
 """Top SASS instructions by warp-stall samples from an ncu source-page CSV.
-Usage: ncu -i X.ncu-rep --page source --csv --print-source sass > s.csv; python tools/ncu_hot.py s.csv [N]"""
+Usage: ncu -i X.ncu-rep --page source --csv --print-source sass > s.csv; python tools/ncu_hot.py s.csv [N] [KERNEL]
+A report with several kernels has one "Kernel Name" section each; KERNEL
+(0-based, default 0) picks the section."""
 import csv, sys
 from collections import Counter
 
-rows = list(csv.reader(open(sys.argv[1])))
+_all = list(csv.reader(open(sys.argv[1], errors="replace")))
+_sec = [i for i, r in enumerate(_all) if r and r[0] == "Kernel Name"] or [-1]
+_pick = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+_start = _sec[_pick]
+_end = _sec[_pick + 1] if _pick + 1 < len(_sec) else len(_all)
+rows = _all[max(_start, 0):_end] if _start >= 0 else [[""]] + _all
 hdr = rows[1]
 ix = {h: i for i, h in enumerate(hdr)}
 data = rows[2:]
