@@ -8,6 +8,8 @@ from collections import Counter
 _all = list(csv.reader(open(sys.argv[1], errors="replace")))
 _sec = [i for i, r in enumerate(_all) if r and r[0] == "Kernel Name"] or [-1]
 _pick = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+if _pick >= len(_sec):
+    sys.exit(f"the report has {len(_sec)} kernel section(s)")
 _start = _sec[_pick]
 _end = _sec[_pick + 1] if _pick + 1 < len(_sec) else len(_all)
 rows = _all[max(_start, 0):_end] if _start >= 0 else [[""]] + _all
