@@ -134,7 +134,8 @@ __device__ __forceinline__ void load8(double (&d)[8], const T *p) {
 // operands per row to f64 on use (16 F2F per 64 DFMA).
 // block_mask: bit (bi·nbj + bj) set ⇔ output block (bi, bj) is computed (a
 // caller exploiting symmetry skips the mirrored half; skipped blocks are 0).
-// same_ab: B is A (loaded once).
+// a_in_b: A is the first ca columns of B (same buffer and block layout; B == A
+// is the special case): only B is staged and A's blocks alias B's first ones.
 // FAST (f32 operands, CIM_GRAM_FAST): products and partial sums in f32
 // (FFMA2 on register pairs) over at most kFastRun rows, then widened into the
 // f64 accumulators — 1/kFastRun of the conversions and no DFMA in the row
@@ -153,19 +154,20 @@ template <typename T, bool FAST>
 __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const Operand A, const Operand B, int mode_a,
                                                                     int mode_b, long long rows,
                                                                     double *__restrict__ part, uint64_t block_mask,
-                                                                    bool same_ab) {
+                                                                    bool a_in_b) {
   extern __shared__ __align__(32) unsigned char smem_raw[];
   const int ca = A.cols, cb = B.cols;
   const int cap = pad8(ca), cbp = pad8(cb);
-  const int kSlab = slab_rows(cap, same_ab ? 0 : cbp, (int)sizeof(T));  // B == A: only A is staged
+  const int nbi_st = a_in_b ? 0 : cap / 8;  // staged A blocks (B's are always staged)
+  const int kSlab = slab_rows(8 * nbi_st, cbp, (int)sizeof(T));
   const int sbs = sblk_stride(kSlab);
   const int nbi = cap / 8, nbj = cbp / 8, nblk = nbi * nbj;
   const uint64_t live = (nblk >= 64 ? ~0ull : ((1ull << nblk) - 1)) & block_mask;
   const int nact = max(1, __popcll(live));
-  const int stage_elems = (nbi + (same_ab ? 0 : nbj)) * sbs;
+  const int stage_elems = (nbi_st + nbj) * sbs;
   T *ring = reinterpret_cast<T *>(smem_raw);
   __shared__ uint64_t full[kGramStages];  // bulk mode: slab k landed in stage k % S
-  const bool bulk = mode_a == 0 && (same_ab || mode_b == 0);
+  const bool bulk = mode_b == 0 && (a_in_b || mode_a == 0);
   if (bulk && threadIdx.x == 0) {
     for (int q = 0; q < kGramStages; ++q) cim::mbar_init(&full[q], 1);
     cim::fence_mbar_init();
@@ -223,14 +225,13 @@ __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const Operan
         const int nr = (int)min((long long)kSlab, rows - r0);
         T *st = ring + (size_t)(k % kGramStages) * stage_elems;
         const uint32_t bytes = (uint32_t)nr * 8 * sizeof(T);
-        cim::mbar_arrive_expect_tx(&full[k % kGramStages], bytes * (nbi + (same_ab ? 0 : nbj)));
-        for (int b = 0; b < nbi; ++b)
+        cim::mbar_arrive_expect_tx(&full[k % kGramStages], bytes * (nbi_st + nbj));
+        for (int b = 0; b < nbi_st; ++b)
           cim::bulk_g2s(st + b * sbs, static_cast<const T *>(A.p) + (long long)b * A.bstride + r0 * 8, bytes,
                         &full[k % kGramStages], pol);
-        if (!same_ab)
-          for (int b = 0; b < nbj; ++b)
-            cim::bulk_g2s(st + (nbi + b) * sbs, static_cast<const T *>(B.p) + (long long)b * B.bstride + r0 * 8,
-                          bytes, &full[k % kGramStages], pol);
+        for (int b = 0; b < nbj; ++b)
+          cim::bulk_g2s(st + (nbi_st + b) * sbs, static_cast<const T *>(B.p) + (long long)b * B.bstride + r0 * 8,
+                        bytes, &full[k % kGramStages], pol);
       }
       return;
     }
@@ -238,8 +239,8 @@ __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const Operan
       const long long r0 = sl * kSlab;
       const int nr = (int)min((long long)kSlab, rows - r0);
       T *st = ring + (size_t)(k % kGramStages) * stage_elems;
-      load_operand(st, A, mode_a, kSlab, r0, nr, inv_ca);
-      if (!same_ab) load_operand(st + nbi * sbs, B, mode_b, kSlab, r0, nr, inv_cb);
+      if (!a_in_b) load_operand(st, A, mode_a, kSlab, r0, nr, inv_ca);
+      load_operand(st + nbi_st * sbs, B, mode_b, kSlab, r0, nr, inv_cb);
     }
     cp_async_commit();  // possibly empty group: keeps the wait arithmetic uniform
   };
@@ -256,7 +257,7 @@ __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const Operan
     const long long r0 = sl * kSlab;
     const int nr = (int)min((long long)kSlab, rows - r0);
     const T *sa = ring + (size_t)(k % kGramStages) * stage_elems + bi * sbs;
-    const T *sb = ring + (size_t)(k % kGramStages) * stage_elems + ((same_ab ? 0 : nbi) + bj) * sbs;
+    const T *sb = ring + (size_t)(k % kGramStages) * stage_elems + (nbi_st + bj) * sbs;
     if (active) {
       if constexpr (FAST) {
         for (int r = grp; r < nr; r += split) {
@@ -319,8 +320,8 @@ __global__ void gram_sum_kernel(const double *__restrict__ part, int nparts, int
   if (lane == 0) out[e] = s;
 }
 
-size_t gram_smem(int ca, int cb, size_t es, bool same_ab = false) {
-  const int cap = pad8(ca), cbp = same_ab ? 0 : pad8(cb);
+size_t gram_smem(int ca, int cb, size_t es, bool a_in_b = false) {
+  const int cap = a_in_b ? 0 : pad8(ca), cbp = pad8(cb);
   return (size_t)kGramStages * ((cap + cbp) / 8) * sblk_stride(slab_rows(cap, cbp, (int)es)) * es;
 }
 
@@ -332,11 +333,11 @@ int load_mode(const Operand &o, size_t es) {
   return 2;
 }
 
-int gram_grid(long long rows, int ca, int cb, bool same_ab = false, int es = 4) {
+int gram_grid(long long rows, int ca, int cb, bool a_in_b = false, int es = 4) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int kSlab = slab_rows(pad8(ca), same_ab ? 0 : pad8(cb), es);
+  const int kSlab = slab_rows(a_in_b ? 0 : pad8(ca), pad8(cb), es);
   const long long slabs = (rows + kSlab - 1) / kSlab;
   return (int)std::min<long long>(slabs > 0 ? slabs : 1, 2LL * sms);
 }
@@ -356,13 +357,14 @@ int gram_impl(const Operand &A, const Operand &B, long long rows, int32_t dtype,
   if (dtype != CIM_F32 && dtype != CIM_F64) return cim::set_error(CIM_EINVAL, "dtype must be CIM_F32 or CIM_F64");
   if (!out || (rows > 0 && (!A.p || !B.p))) return cim::set_error(CIM_EINVAL, "NULL pointer");
   const size_t es = dtype == CIM_F32 ? 4 : 8;
-  const bool same_ab = A.p == B.p && A.ld == B.ld && A.bstride == B.bstride && A.bw_shift == B.bw_shift &&
-                       A.cols == B.cols;
-  const int grid = gram_grid(rows, ca, cb, same_ab, (int)es);  // ≤ the grid cim_gram_workspace_bytes assumed
+  // A = the first ca columns of B (B == A, or SᵀAS-style [S]ᵀ[S AS]): stage B only
+  const bool a_in_b = A.p == B.p && A.ld == B.ld && A.bstride == B.bstride && A.bw_shift == B.bw_shift &&
+                      A.cols <= B.cols;
+  const int grid = gram_grid(rows, ca, cb, a_in_b, (int)es);  // ≤ the grid cim_gram_workspace_bytes assumed
   const uint64_t need = (uint64_t)grid * ca * cb * sizeof(double);
   if (!workspace || ws_bytes < need)
     return cim::set_error(CIM_EINVAL, "workspace must hold " + std::to_string(need) + " bytes");
-  const size_t smem = gram_smem(ca, cb, es, same_ab);
+  const size_t smem = gram_smem(ca, cb, es, a_in_b);
   const int ma = load_mode(A, es), mb = load_mode(B, es);
   if (block_mask == 0) block_mask = ~0ull;
   cudaError_t e;
@@ -370,7 +372,7 @@ int gram_impl(const Operand &A, const Operand &B, long long rows, int32_t dtype,
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
       kern<<<grid, kGramThreads, smem, stream>>>(A, B, ma, mb, rows, static_cast<double *>(workspace), block_mask,
-                                                 same_ab);
+                                                 a_in_b);
   };
   if (dtype == CIM_F32 && (flags & CIM_GRAM_FAST))
     run(gram_partial_kernel<float, true>);
