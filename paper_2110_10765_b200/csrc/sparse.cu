@@ -351,32 +351,52 @@ __global__ void __launch_bounds__(256) sparse_small_kernel(const SparseParams p,
   T *Y = static_cast<T *>(p.Y);
   const T *vals = static_cast<const T *>(p.vals);
   const long long n_items = list ? n_list : p.n_tiles;
-  for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_items; w += nw) {
-    const long long t = list ? (long long)__ldg(list + w) : w;
-    const long long base = __ldg(p.entry_off + t);
-    if (!list) {
-      const int ne = (int)(__ldg(p.entry_off + t + 1) - base);
-      if (ne == 0 || ne > p.small_max) continue;
+  // Chunks of 32 tiles per warp: lane l fetches tile l's metadata (list
+  // entry, entry offset, count, (R, C)) in one round of loads, then the warp
+  // walks the chunk's tiles with the metadata broadcast by shuffles — one
+  // dependent load level per tile (entries → X) instead of four.
+  for (long long c0 = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; c0 < n_items; c0 += nw * 32) {
+    const long long it = c0 + lane;
+    long long my_base = 0;
+    int my_cnt = 0;
+    int2 my_rc = make_int2(0, 0);
+    if (it < n_items) {
+      const long long t = list ? (long long)__ldg(list + it) : it;
+      my_base = __ldg(p.entry_off + t);
+      bool take = true;
+      if (!list) {
+        const int ne = (int)(__ldg(p.entry_off + t + 1) - my_base);
+        take = ne > 0 && ne <= p.small_max;
+      }
+      if (take) {
+        my_cnt = __ldg(p.rowptr + (size_t)t * kSpPtrStride + 64);
+        my_rc = __ldg(p.tile_rc + t);
+      }
     }
-    const int cnt = __ldg(p.rowptr + (size_t)t * kSpPtrStride + 64);
-    const int2 rc = __ldg(p.tile_rc + t);
-    const bool diag = rc.x == rc.y;
-    const T *xr = X + (long long)rc.x * 64 * p.k, *xc = X + (long long)rc.y * 64 * p.k;
-    T *yr = Y + (long long)rc.x * 64 * p.ldy, *yc = Y + (long long)rc.y * 64 * p.ldy;
-    for (int e = lane; e < cnt; e += 32) {
-      const int c = __ldg(p.col + base + e), r = __ldg(p.row + base + e);
-      const T v = __ldg(vals + base + e);
-      for (int v0 = 0; v0 < p.k; v0 += KV) {
-        T x[KV], a[KV];
-        ldg_vec<T, KV>(x, xc + (long long)c * p.k + v0);
+    const int n_here = (int)min(32LL, n_items - c0);
+    for (int q = 0; q < n_here; ++q) {
+      const int cnt = __shfl_sync(0xffffffffu, my_cnt, q);
+      if (cnt == 0) continue;
+      const long long base = __shfl_sync(0xffffffffu, my_base, q);
+      const int R = __shfl_sync(0xffffffffu, my_rc.x, q), C = __shfl_sync(0xffffffffu, my_rc.y, q);
+      const bool diag = R == C;
+      const T *xr = X + (long long)R * 64 * p.k, *xc = X + (long long)C * 64 * p.k;
+      T *yr = Y + (long long)R * 64 * p.ldy, *yc = Y + (long long)C * 64 * p.ldy;
+      for (int e = lane; e < cnt; e += 32) {
+        const int c = __ldg(p.col + base + e), r = __ldg(p.row + base + e);
+        const T v = __ldg(vals + base + e);
+        for (int v0 = 0; v0 < p.k; v0 += KV) {
+          T x[KV], a[KV];
+          ldg_vec<T, KV>(x, xc + (long long)c * p.k + v0);
 #pragma unroll
-        for (int q = 0; q < KV; ++q) a[q] = v * x[q];
-        red_vec<T, KV>(yr + (long long)r * p.ldy + v0, a);
-        if (!diag) {
-          ldg_vec<T, KV>(x, xr + (long long)r * p.k + v0);
+          for (int qq = 0; qq < KV; ++qq) a[qq] = v * x[qq];
+          red_vec<T, KV>(yr + (long long)r * p.ldy + v0, a);
+          if (!diag) {
+            ldg_vec<T, KV>(x, xr + (long long)r * p.k + v0);
 #pragma unroll
-          for (int q = 0; q < KV; ++q) a[q] = v * x[q];
-          red_vec<T, KV>(yc + (long long)c * p.ldy + v0, a);
+            for (int qq = 0; qq < KV; ++qq) a[qq] = v * x[qq];
+            red_vec<T, KV>(yc + (long long)c * p.ldy + v0, a);
+          }
         }
       }
     }
@@ -504,7 +524,7 @@ int launch_sparse(const cim_sparse_tiles *S, const void *X, void *Y, int k, long
   }
   const long long n_small = listed ? (S->small_tiles ? S->n_small : 0) : (p.small_max > 0 ? S->n_tiles : 0);
   if (n_small > 0) {
-    const long long g2 = std::min<long long>((n_small + 7) / 8, (long long)st->sms * 16);
+    const long long g2 = std::min<long long>((n_small + 255) / 256, (long long)st->sms * 16);  // 32 tiles / warp
     sparse_small_kernel<T, KV><<<(unsigned)g2, 256, 0, stream>>>(p, listed ? S->small_tiles : nullptr,
                                                                  listed ? S->n_small : 0);
     e = cudaGetLastError();
