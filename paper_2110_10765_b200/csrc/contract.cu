@@ -197,37 +197,50 @@ __global__ void __launch_bounds__(256) contract_small_kernel(ContractArgs<T> a, 
   for (int q = 0; q < KS; ++q)
 #pragma unroll
     for (int v = 0; v < NV; ++v) acc[q][v] = 0.f;
-  for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_list; w += nw) {
-    const long long u = __ldg(list + w);
-    const long long base = __ldg(a.sp_off + u);
-    const int cnt = __ldg(a.sp_rowptr + u * kSpPtrStride + 64);
-    const int2 RC = __ldg(a.sp_rc + u);
-    const float wgt = RC.x == RC.y ? 1.f : 2.f;
-    for (int e = lane; e < cnt; e += 32) {
-      if (__ldg(a.sp_vals + base + e) == T(0)) continue;
-      const long long i = (long long)RC.x * 64 + __ldg(a.sp_row + base + e);
-      const long long j = (long long)RC.y * 64 + __ldg(a.sp_col + base + e);
-      if (i >= a.n || j >= a.n) continue;
-      float p[NV];
+  // 32 tiles' metadata per warp load round (lane = tile), broadcast by shuffles
+  for (long long c0 = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; c0 < n_list; c0 += nw * 32) {
+    long long my_base = 0;
+    int my_cnt = 0;
+    int2 my_rc = make_int2(0, 0);
+    if (c0 + lane < n_list) {
+      const long long u = __ldg(list + c0 + lane);
+      my_base = __ldg(a.sp_off + u);
+      my_cnt = __ldg(a.sp_rowptr + u * kSpPtrStride + 64);
+      my_rc = __ldg(a.sp_rc + u);
+    }
+    const int n_here = (int)(n_list - c0 < 32 ? n_list - c0 : 32);
+    for (int t = 0; t < n_here; ++t) {
+      const int cnt = __shfl_sync(0xffffffffu, my_cnt, t);
+      if (cnt == 0) continue;
+      const long long base = __shfl_sync(0xffffffffu, my_base, t);
+      const int2 RC = make_int2(__shfl_sync(0xffffffffu, my_rc.x, t), __shfl_sync(0xffffffffu, my_rc.y, t));
+      const float wgt = RC.x == RC.y ? 1.f : 2.f;
+      for (int e = lane; e < cnt; e += 32) {
+        if (__ldg(a.sp_vals + base + e) == T(0)) continue;
+        const long long i = (long long)RC.x * 64 + __ldg(a.sp_row + base + e);
+        const long long j = (long long)RC.y * 64 + __ldg(a.sp_col + base + e);
+        if (i >= a.n || j >= a.n) continue;
+        float p[NV];
 #pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const bool on = v < a.nv;
-        const float ci = on ? __ldg(a.c + i * a.n_vec + a.v0 + v) : 0.f;
-        const float cj = on ? __ldg(a.c + j * a.n_vec + a.v0 + v) : 0.f;
-        p[v] = wgt * ci * cj;
-      }
-      if constexpr (IDENT) {
-        if (i == j)
+        for (int v = 0; v < NV; ++v) {
+          const bool on = v < a.nv;
+          const float ci = on ? __ldg(a.c + i * a.n_vec + a.v0 + v) : 0.f;
+          const float cj = on ? __ldg(a.c + j * a.n_vec + a.v0 + v) : 0.f;
+          p[v] = wgt * ci * cj;
+        }
+        if constexpr (IDENT) {
+          if (i == j)
 #pragma unroll
-          for (int v = 0; v < NV; ++v) acc[0][v] += p[v];
-      } else {
-        const uint64_t lo = (uint64_t)(i < j ? i : j), hi = (uint64_t)(i < j ? j : i);
-        const uint64_t hb = mix64(lo + kGolden * hi);
+            for (int v = 0; v < NV; ++v) acc[0][v] += p[v];
+        } else {
+          const uint64_t lo = (uint64_t)(i < j ? i : j), hi = (uint64_t)(i < j ? j : i);
+          const uint64_t hb = mix64(lo + kGolden * hi);
 #pragma unroll
-        for (int q = 0; q < KS; ++q) {
-          const float o = to_unit(mix64(mix64(hb ^ kq[q]) ^ a.seed));
+          for (int q = 0; q < KS; ++q) {
+            const float o = to_unit(mix64(mix64(hb ^ kq[q]) ^ a.seed));
 #pragma unroll
-          for (int v = 0; v < NV; ++v) acc[q][v] = fmaf(p[v], o, acc[q][v]);
+            for (int v = 0; v < NV; ++v) acc[q][v] = fmaf(p[v], o, acc[q][v]);
+          }
         }
       }
     }
@@ -319,7 +332,7 @@ int run_contract(const cim_half_tiles *H, const float *c, int n_vec, int m_ops, 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)(total < (long long)sms * 8 ? total : (long long)sms * 8);
-  const int grid_small = (int)std::min<long long>((n_small + 7) / 8, (long long)sms * 16);
+  const int grid_small = (int)std::min<long long>((n_small + 255) / 256, (long long)sms * 16);  // 32 tiles / warp
   const bool ident = kind == CIM_VALUES_IDENTITY;
   if (n_small > 0) {
     constexpr int kSmallKs = 8;
