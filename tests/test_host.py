@@ -38,11 +38,35 @@ def test_library_is_built_for_sm100a():
     assert "sm_100a" in out.stdout
 
 
-def test_struct_layout_matches_header():
-    assert pkg._lib.CimHalfTiles.n_tiles.offset == 16
-    assert pkg._lib.CimHalfTiles.vals.offset == 48
-    assert pkg._lib.CimHalfTiles.layout.offset == 56
-    assert pkg._lib.CimHalfTiles.__sizeof__(pkg._lib.CimHalfTiles()) >= 56
+def test_struct_layout_matches_header(tmp_path):
+    """Every field of the ctypes mirrors sits where a C compiler puts it in
+    include/cim_b200.h (offsets and sizes from gcc on the header itself)."""
+    import ctypes
+    import shutil
+    import subprocess
+
+    structs = {"cim_half_tiles": pkg._lib.CimHalfTiles, "cim_sparse_tiles": pkg._lib.CimSparseTiles}
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "cim_b200.h"', "int main(void) {"]
+    for cname, cls in structs.items():
+        lines.append(f'printf("{cname} sizeof %zu\\n", sizeof({cname}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    root = Path(__file__).resolve().parent.parent
+    subprocess.run(["gcc", "-std=c11", "-I", str(root / "include"), str(src), "-o", str(exe)], check=True)
+    got = {}
+    for line in subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.splitlines():
+        cname, field, val = line.split()
+        got[(cname, field)] = int(val)
+    for cname, cls in structs.items():
+        assert got[(cname, "sizeof")] == ctypes.sizeof(cls), cname
+        for fname, _ in cls._fields_:
+            assert got[(cname, fname)] == getattr(cls, fname).offset, (cname, fname)
 
 
 def test_supported_k_table():
