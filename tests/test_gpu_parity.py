@@ -614,8 +614,8 @@ def test_column_banded_storage(pkg, c1_small, bands):
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
-@pytest.mark.parametrize("fill", [0.0, 0.02, 0.3, 0.9])
-@pytest.mark.parametrize("k", [1, 2, 4, 8, 12, 16])
+@pytest.mark.parametrize("fill", [0.0, 0.02, 0.05, 0.3, 0.9])  # 0.05: every staged tile fits 512-entry stages
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 8, 12, 16, 24])
 def test_sparse_tiles_vs_oracle(pkg, dtype, fill, k):
     """COO-in-tile storage: random symmetric matrices whose 64-tiles have a
     given fill (ragged n, empty rows, diagonal and off-diagonal tiles), stored
@@ -653,6 +653,9 @@ def test_sparse_tiles_vs_oracle(pkg, dtype, fill, k):
     assert H_sp.n_tiles == 0 and H_dn.n_sparse_tiles == 0
     if fill < 0.5:
         assert H_mix.n_sparse_tiles > 0
+    if fill == 0.05:  # the forced-sparse storage runs the staged kernel with 512-entry stages
+        staged, _ = H_sp.sparse.work_split()
+        assert staged.numel() > 0 and H_sp.sparse.descriptor().staged_max_entries <= 512
     rc_all, tiles = H_dn.export_dense()
     for H in (H_mix, H_sp, H_dn):
         Y = pkg.sym_spmm(H, X.cuda()).cpu().numpy()
