@@ -99,7 +99,8 @@ constexpr int kSpCap = 1024;
 constexpr int kSpCapSmall = 512;
 constexpr int kSpSmallDefault = 128;
 constexpr int kSpConsumers = 128;
-constexpr unsigned kSpBig = 1u, kSpTerm = 2u;
+constexpr unsigned kSpBig = 1u, kSpTerm = 2u, kSpSkew = 4u;
+constexpr int kSpSkewMin = 256;  // tiles above this many (padded) entries stage X in skewed chunks
 
 struct SpStageHdr {
   int R, C, ne;
@@ -107,6 +108,16 @@ struct SpStageHdr {
   long long t;  // tile index (global fallback)
   long long pad;
 };
+
+// X_C / X_R blocks are staged as kXChunks copies of 64/kXChunks rows, chunk q
+// shifted by q·kXSkew bytes: lanes gathering random rows then spread over
+// more banks (ncu: 44% of the shared-load wavefronts were bank conflicts
+// with one contiguous 2 KB copy).  Row c lives at c·k + (c / rows-per-chunk)·skew.
+#ifdef CIM_SP_NO_SKEW
+constexpr int kXChunks = 1, kXSkew = 0;
+#else
+constexpr int kXChunks = 4, kXSkew = 16;
+#endif
 
 struct SpLayout {  // byte offsets inside one stage
   unsigned rp, cp, col, row, cperm, val, xc, xr, bytes;
@@ -121,8 +132,8 @@ __host__ __device__ __forceinline__ SpLayout sp_layout(int k, int es, int cap) {
   L.cperm = L.row + cap;
   L.val = L.cperm + 2 * cap;
   L.xc = L.val + cap * es;
-  L.xr = L.xc + 64 * k * es;
-  L.bytes = (L.xr + 64 * k * es + 127) & ~127u;
+  L.xr = L.xc + 64 * k * es + kXChunks * kXSkew;
+  L.bytes = (L.xr + 64 * k * es + kXChunks * kXSkew + 127) & ~127u;
   return L;
 }
 
@@ -161,7 +172,8 @@ __device__ __forceinline__ void ldx(T (&d)[KV], const T *p) {
 template <bool GLOBAL, typename T, int KV>
 __device__ __forceinline__ void sp_tile(int lane, int R, int C, const uint16_t *rp, const uint16_t *cp,
                                         const uint8_t *col, const uint8_t *row, const uint16_t *cperm,
-                                        const T *val, const T *xc, const T *xr, int k, T *Y, long long ldy) {
+                                        const T *val, const T *xc, const T *xr, int k, T *Y, long long ldy,
+                                        int skew = 0) {  // skew: elements added per 64/kXChunks rows of X
   const bool diag = R == C;
 #pragma unroll
   for (int hh = 0; hh < 2; ++hh) {
@@ -177,7 +189,7 @@ __device__ __forceinline__ void sp_tile(int lane, int R, int C, const uint16_t *
           const int c = ld1<GLOBAL>(col + e);
           const T w = ld1<GLOBAL>(val + e);
           T x[KV];
-          ldx<GLOBAL, T, KV>(x, xc + (long long)c * k + v0);
+          ldx<GLOBAL, T, KV>(x, xc + (long long)c * k + (GLOBAL ? 0 : (c / (64 / kXChunks)) * skew) + v0);
 #pragma unroll
           for (int q = 0; q < KV; ++q) acc[q] = fma(w, x[q], acc[q]);
         }
@@ -192,7 +204,7 @@ __device__ __forceinline__ void sp_tile(int lane, int R, int C, const uint16_t *
           const int rr = ld1<GLOBAL>(row + e);
           const T w = ld1<GLOBAL>(val + e);
           T x[KV];
-          ldx<GLOBAL, T, KV>(x, xr + (long long)rr * k + v0);
+          ldx<GLOBAL, T, KV>(x, xr + (long long)rr * k + (GLOBAL ? 0 : (rr / (64 / kXChunks)) * skew) + v0);
 #pragma unroll
           for (int q = 0; q < KV; ++q) acc[q] = fma(w, x[q], acc[q]);
         }
@@ -257,7 +269,8 @@ __global__ void __launch_bounds__(kSpConsumers + 32) sparse_spmm_kernel(const Sp
           h->R = R;
           h->C = C;
           h->ne = ne;
-          h->flags = big ? kSpBig : 0u;
+          const bool skew = ne > kSpSkewMin;  // denser tiles: more random X rows per tile, spread the banks
+          h->flags = big ? kSpBig : (skew ? kSpSkew : 0u);
           h->t = tt;
           if (big) {
             mbar_arrive(&full[stage]);
@@ -273,8 +286,19 @@ __global__ void __launch_bounds__(kSpConsumers + 32) sparse_spmm_kernel(const Sp
               bulk_g2s(st + L.cperm, p.cperm + base, 2 * ne, &full[stage], pol_stream);
               bulk_g2s(st + L.val, vals + base, ne * (int)sizeof(T), &full[stage], pol_stream);
             }
-            bulk_g2s(st + L.xc, X + (long long)C * 64 * p.k, xblk, &full[stage], pol_keep);
-            if (!diag) bulk_g2s(st + L.xr, X + (long long)R * 64 * p.k, xblk, &full[stage], pol_keep);
+            if (skew) {
+              const unsigned xch = xblk / kXChunks;
+              for (int q = 0; q < kXChunks; ++q) {
+                bulk_g2s(st + L.xc + q * (xch + kXSkew), X + ((long long)C * 64 + q * (64 / kXChunks)) * p.k, xch,
+                         &full[stage], pol_keep);
+                if (!diag)
+                  bulk_g2s(st + L.xr + q * (xch + kXSkew), X + ((long long)R * 64 + q * (64 / kXChunks)) * p.k, xch,
+                           &full[stage], pol_keep);
+              }
+            } else {
+              bulk_g2s(st + L.xc, X + (long long)C * 64 * p.k, xblk, &full[stage], pol_keep);
+              if (!diag) bulk_g2s(st + L.xr, X + (long long)R * 64 * p.k, xblk, &full[stage], pol_keep);
+            }
           }
         }
         __syncwarp();
@@ -320,7 +344,7 @@ __global__ void __launch_bounds__(kSpConsumers + 32) sparse_spmm_kernel(const Sp
                             reinterpret_cast<const uint16_t *>(st + L.cp), st + L.col, st + L.row,
                             reinterpret_cast<const uint16_t *>(st + L.cperm), reinterpret_cast<const T *>(st + L.val),
                             reinterpret_cast<const T *>(st + L.xc), reinterpret_cast<const T *>(st + L.xr), p.k, Y,
-                            p.ldy);
+                            p.ldy, (h.flags & kSpSkew) ? kXSkew / (int)sizeof(T) : 0);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);

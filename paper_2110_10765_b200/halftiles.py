@@ -194,11 +194,11 @@ def dense_break_even(dtype) -> float:
 
 
 # Time break-even on B200 (C2 pattern, k = 8 f32, profiles/r01/sparse_small.md):
-# all-sparse storage runs 1.25 / 1.16 / 1.74 / 2.41 / 3.03 ms at
+# all-sparse storage runs 1.24 / 1.11 / 1.45 / 2.01 / 2.43 ms at
 # 3 / 5 / 9 / 13 / 17% entry fill against 1.61 ms for the same tiles stored
-# dense, so tiles below ~8% fill are faster sparse.  The default split
+# dense, so tiles below ~10% fill are faster sparse.  The default split
 # optimises time (with a margin).
-DEFAULT_DENSE_FILL = 0.075
+DEFAULT_DENSE_FILL = 0.10
 
 
 @dataclass
