@@ -246,6 +246,29 @@ def test_k_sweep_f64(pkg, c1_small, k):
     check_result(n, rc, tiles.astype(np.float64), X.numpy(), Y, torch.float64)
 
 
+@pytest.mark.parametrize("dtype,k", [(torch.float32, 32), (torch.float32, 64), (torch.float64, 16)])
+def test_multipass_widths_on_concurrent_streams(pkg, c1_small, dtype, k):
+    """Widths above one pass stage a pass-major copy of X in a per-stream
+    scratch buffer: applies queued on two streams at once (different X, same
+    H) must each match their own oracle product, and repeated calls on one
+    stream (the buffer reused) stay exact."""
+    n, rc, tiles = c1_small
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=dtype)
+    g = torch.Generator().manual_seed(k)
+    Xs = [torch.randn((n, k), generator=g, dtype=dtype) for _ in range(2)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = []
+    for X, st in zip(Xs, streams):
+        with torch.cuda.stream(st):
+            outs.append(pkg.sym_spmm(H, X.cuda(non_blocking=False), stream=st))
+    torch.cuda.synchronize()
+    tl = tiles if dtype == torch.float32 else tiles.astype(np.float64)
+    for X, Y in zip(Xs, outs):
+        check_result(n, rc, tl, X.numpy(), Y.cpu().numpy(), dtype)
+    again = pkg.sym_spmm(H, Xs[0].cuda())
+    assert (again - outs[0]).abs().max().item() <= 1e-5 * outs[0].abs().max().item()
+
+
 @pytest.mark.parametrize("layout", F32_LAYOUTS)
 def test_opaque_random_symmetric_values(pkg, c1_small, layout):
     """Values with no XOR structure (op hash of (min,max)) — the kernel must
