@@ -119,6 +119,7 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
         self.err = None
+        self.mem_max_mhz = None
 
     def _run(self):
         try:
@@ -129,8 +130,16 @@ class ClockSampler:
             idx = int(vis.split(",")[self.idx]) if vis and vis.split(",")[0].isdigit() else self.idx
             h = nv.nvmlDeviceGetHandleByIndex(idx)
             self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            try:
+                self.mem_max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_MEM)
+            except Exception:
+                self.mem_max_mhz = None
             while not self._stop.is_set():
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                try:
+                    mem = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_MEM)
+                except Exception:
+                    mem = float("nan")
                 try:
                     r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
                 except Exception:
@@ -139,7 +148,7 @@ class ClockSampler:
                     w = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
                 except Exception:
                     w = float("nan")
-                self.samples.append((sm, r, w))
+                self.samples.append((sm, r, w, mem))
                 self._stop.wait(0.01)
         except Exception as ex:  # report, never fail the bench
             self.err = str(ex)
@@ -156,14 +165,17 @@ class ClockSampler:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [f"unavailable: {self.err}"]}
         reasons = set()
-        for _, r, _ in self.samples:
+        for _, r, _, _ in self.samples:
             for bit, name in self.REASONS.items():
                 if r & bit:
                     reasons.add(name)
-        watts = [w for _, _, w in self.samples if w == w]
-        return {"sm_mhz": float(np.median([s for s, _, _ in self.samples])), "sm_max_mhz": float(self.max_mhz),
+        watts = [w for _, _, w, _ in self.samples if w == w]
+        mems = [m for _, _, _, m in self.samples if m == m]
+        return {"sm_mhz": float(np.median([s for s, _, _, _ in self.samples])), "sm_max_mhz": float(self.max_mhz),
                 "reasons": sorted(reasons), "samples": len(self.samples),
-                "power_w_median": float(np.median(watts)) if watts else None}
+                "power_w_median": float(np.median(watts)) if watts else None,
+                "mem_mhz": float(np.median(mems)) if mems else None,
+                "mem_max_mhz": float(self.mem_max_mhz) if getattr(self, "mem_max_mhz", None) else None}
 
 
 # -----------------------------------------------------------------------------
