@@ -163,7 +163,8 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [f"unavailable: {self.err}"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [f"unavailable: {self.err}"], "samples": 0,
+                    "power_w_median": None, "mem_mhz": None, "mem_max_mhz": None}
         reasons = set()
         for _, r, _, _ in self.samples:
             for bit, name in self.REASONS.items():
