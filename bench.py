@@ -121,45 +121,65 @@ class ClockSampler:
         self.err = None
         self.mem_max_mhz = None
 
-    def _run(self):
+    def _open(self):
+        """NVML handle and maxima, before the timed region (nvmlInit can take
+        longer than a short timed region)."""
         try:
             import pynvml as nv
 
             nv.nvmlInit()
             vis = os.environ.get("CUDA_VISIBLE_DEVICES")
             idx = int(vis.split(",")[self.idx]) if vis and vis.split(",")[0].isdigit() else self.idx
-            h = nv.nvmlDeviceGetHandleByIndex(idx)
-            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self._nv, self._h = nv, nv.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
             try:
-                self.mem_max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_MEM)
+                self.mem_max_mhz = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_MEM)
             except Exception:
                 self.mem_max_mhz = None
+        except Exception as ex:  # report, never fail the bench
+            self.err = str(ex)
+            self._h = None
+
+    def _sample(self):
+        nv, h = self._nv, self._h
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        try:
+            mem = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_MEM)
+        except Exception:
+            mem = float("nan")
+        try:
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        try:
+            w = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+        except Exception:
+            w = float("nan")
+        self.samples.append((sm, r, w, mem))
+
+    def _run(self):
+        try:
             while not self._stop.is_set():
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                try:
-                    mem = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_MEM)
-                except Exception:
-                    mem = float("nan")
-                try:
-                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                except Exception:
-                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                try:
-                    w = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
-                except Exception:
-                    w = float("nan")
-                self.samples.append((sm, r, w, mem))
+                self._sample()
                 self._stop.wait(0.01)
         except Exception as ex:  # report, never fail the bench
             self.err = str(ex)
 
     def __enter__(self):
-        self._t.start()
+        self._open()
+        if self._h is not None:
+            self._t.start()
         return self
 
     def __exit__(self, *a):
         self._stop.set()
-        self._t.join(timeout=10)
+        if self._t.is_alive():
+            self._t.join(timeout=10)
+        if self._h is not None and not self.samples:
+            try:
+                self._sample()  # a timed region shorter than one sampling period
+            except Exception as ex:
+                self.err = str(ex)
 
     def summary(self):
         if not self.samples:
