@@ -444,7 +444,7 @@ def test_c2_full_size_properties(pkg, layout):
         assert np.abs(got - yr).max() <= 1e-5 * max(1.0, np.abs(yr).max())
 
 
-@pytest.mark.parametrize("dtype,k", [(torch.float32, 8), (torch.float32, 4), (torch.float64, 8)])
+@pytest.mark.parametrize("dtype,k", [(torch.float32, 8), (torch.float32, 4), (torch.float64, 8), (torch.float32, 32), (torch.float64, 16)])
 def test_host_batch_pipeline_matches_oracle(pkg, c1_small, dtype, k):
     """cim_sym_spmm_host_batch: host (pinned and pageable, numpy and torch)
     blocks in, host blocks out; every block checked against the oracle, and
