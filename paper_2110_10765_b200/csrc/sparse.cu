@@ -100,7 +100,8 @@ constexpr int kSpCapSmall = 512;
 constexpr int kSpSmallDefault = 128;
 constexpr int kSpConsumers = 128;
 constexpr unsigned kSpBig = 1u, kSpTerm = 2u, kSpSkew = 4u;
-constexpr int kSpSkewMin = 256;  // tiles above this many (padded) entries stage X in skewed chunks
+constexpr int kSpSkewMin = 256;
+constexpr int kSpFlatMax = 24;  // small-tile chunks whose tiles all hold ≤ this many entries walk one flat entry range  // tiles above this many (padded) entries stage X in skewed chunks
 
 struct SpStageHdr {
   int R, C, ne;
@@ -397,13 +398,54 @@ __global__ void __launch_bounds__(256) sparse_small_kernel(const SparseParams p,
         my_rc = __ldg(p.tile_rc + t);
       }
     }
+    if (__all_sync(0xffffffffu, my_cnt <= kSpFlatMax)) {
+      // the chunk's entries as one flat range (inclusive scan of the counts),
+      // lanes striding over it — a warp stays busy however small the tiles
+      int my_end = my_cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, my_end, o);
+        if (lane >= o) my_end += v;
+      }
+      const int total = __shfl_sync(0xffffffffu, my_end, 31);
+      for (int f0 = 0; f0 < total; f0 += 32) {  // warp-uniform trip count: the shuffles need every lane
+        const int f = f0 + lane;
+        const bool on = f < total;
+        const int fq = on ? f : total - 1;
+        int q = 0;  // first tile whose inclusive end exceeds fq
+#pragma unroll
+        for (int step = 16; step; step >>= 1)
+          if (__shfl_sync(0xffffffffu, my_end, q + step - 1) <= fq) q += step;
+        const int end_q = __shfl_sync(0xffffffffu, my_end, q), cnt_q = __shfl_sync(0xffffffffu, my_cnt, q);
+        const long long base = __shfl_sync(0xffffffffu, my_base, q) + (fq - (end_q - cnt_q));
+        const int R = __shfl_sync(0xffffffffu, my_rc.x, q), C = __shfl_sync(0xffffffffu, my_rc.y, q);
+        if (!on) continue;
+        const T *xr = X + (long long)R * 64 * p.k, *xc = X + (long long)C * 64 * p.k;
+        T *yr = Y + (long long)R * 64 * p.ldy, *yc = Y + (long long)C * 64 * p.ldy;
+        const int c = __ldg(p.col + base), r = __ldg(p.row + base);
+        const T v = __ldg(vals + base);
+        for (int v0 = 0; v0 < p.k; v0 += KV) {
+          T x[KV], a[KV];
+          ldg_vec<T, KV>(x, xc + (long long)c * p.k + v0);
+#pragma unroll
+          for (int qq = 0; qq < KV; ++qq) a[qq] = v * x[qq];
+          red_vec<T, KV>(yr + (long long)r * p.ldy + v0, a);
+          if (R != C) {
+            ldg_vec<T, KV>(x, xr + (long long)r * p.k + v0);
+#pragma unroll
+            for (int qq = 0; qq < KV; ++qq) a[qq] = v * x[qq];
+            red_vec<T, KV>(yc + (long long)c * p.ldy + v0, a);
+          }
+        }
+      }
+      continue;
+    }
     const int n_here = (int)min(32LL, n_items - c0);
-    for (int q = 0; q < n_here; ++q) {
+    for (int q = 0; q < n_here; ++q) {  // larger tiles: one tile at a time, lanes over its entries
       const int cnt = __shfl_sync(0xffffffffu, my_cnt, q);
       if (cnt == 0) continue;
       const long long base = __shfl_sync(0xffffffffu, my_base, q);
       const int R = __shfl_sync(0xffffffffu, my_rc.x, q), C = __shfl_sync(0xffffffffu, my_rc.y, q);
-      const bool diag = R == C;
       const T *xr = X + (long long)R * 64 * p.k, *xc = X + (long long)C * 64 * p.k;
       T *yr = Y + (long long)R * 64 * p.ldy, *yc = Y + (long long)C * 64 * p.ldy;
       for (int e = lane; e < cnt; e += 32) {
@@ -415,7 +457,7 @@ __global__ void __launch_bounds__(256) sparse_small_kernel(const SparseParams p,
 #pragma unroll
           for (int qq = 0; qq < KV; ++qq) a[qq] = v * x[qq];
           red_vec<T, KV>(yr + (long long)r * p.ldy + v0, a);
-          if (!diag) {
+          if (R != C) {
             ldg_vec<T, KV>(x, xr + (long long)r * p.k + v0);
 #pragma unroll
             for (int qq = 0; qq < KV; ++qq) a[qq] = v * x[qq];
