@@ -208,41 +208,66 @@ __global__ void __launch_bounds__(256) contract_small_kernel(ContractArgs<T> a, 
       my_cnt = __ldg(a.sp_rowptr + u * kSpPtrStride + 64);
       my_rc = __ldg(a.sp_rc + u);
     }
+    // one stored entry (tile RC, entry index eidx) into the accumulators
+    auto entry = [&](int2 RC, long long eidx) {
+      if (__ldg(a.sp_vals + eidx) == T(0)) return;
+      const long long i = (long long)RC.x * 64 + __ldg(a.sp_row + eidx);
+      const long long j = (long long)RC.y * 64 + __ldg(a.sp_col + eidx);
+      if (i >= a.n || j >= a.n) return;
+      const float wgt = RC.x == RC.y ? 1.f : 2.f;
+      float p[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const bool on = v < a.nv;
+        const float ci = on ? __ldg(a.c + i * a.n_vec + a.v0 + v) : 0.f;
+        const float cj = on ? __ldg(a.c + j * a.n_vec + a.v0 + v) : 0.f;
+        p[v] = wgt * ci * cj;
+      }
+      if constexpr (IDENT) {
+        if (i == j)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) acc[0][v] += p[v];
+      } else {
+        const uint64_t lo = (uint64_t)(i < j ? i : j), hi = (uint64_t)(i < j ? j : i);
+        const uint64_t hb = mix64(lo + kGolden * hi);
+#pragma unroll
+        for (int q = 0; q < KS; ++q) {
+          const float o = to_unit(mix64(mix64(hb ^ kq[q]) ^ a.seed));
+#pragma unroll
+          for (int v = 0; v < NV; ++v) acc[q][v] = fmaf(p[v], o, acc[q][v]);
+        }
+      }
+    };
+    if (__all_sync(0xffffffffu, my_cnt <= 24)) {
+      // tiny tiles: the chunk's entries as one flat range (as sparse_small_kernel)
+      int my_end = my_cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, my_end, o);
+        if (lane >= o) my_end += v;
+      }
+      const int total = __shfl_sync(0xffffffffu, my_end, 31);
+      for (int f0 = 0; f0 < total; f0 += 32) {  // warp-uniform trip count for the shuffles
+        const int f = f0 + lane;
+        const int fq = f < total ? f : total - 1;
+        int q = 0;
+#pragma unroll
+        for (int step = 16; step; step >>= 1)
+          if (__shfl_sync(0xffffffffu, my_end, q + step - 1) <= fq) q += step;
+        const int end_q = __shfl_sync(0xffffffffu, my_end, q), cnt_q = __shfl_sync(0xffffffffu, my_cnt, q);
+        const long long eidx = __shfl_sync(0xffffffffu, my_base, q) + (fq - (end_q - cnt_q));
+        const int2 RC = make_int2(__shfl_sync(0xffffffffu, my_rc.x, q), __shfl_sync(0xffffffffu, my_rc.y, q));
+        if (f < total) entry(RC, eidx);
+      }
+      continue;
+    }
     const int n_here = (int)(n_list - c0 < 32 ? n_list - c0 : 32);
     for (int t = 0; t < n_here; ++t) {
       const int cnt = __shfl_sync(0xffffffffu, my_cnt, t);
       if (cnt == 0) continue;
       const long long base = __shfl_sync(0xffffffffu, my_base, t);
       const int2 RC = make_int2(__shfl_sync(0xffffffffu, my_rc.x, t), __shfl_sync(0xffffffffu, my_rc.y, t));
-      const float wgt = RC.x == RC.y ? 1.f : 2.f;
-      for (int e = lane; e < cnt; e += 32) {
-        if (__ldg(a.sp_vals + base + e) == T(0)) continue;
-        const long long i = (long long)RC.x * 64 + __ldg(a.sp_row + base + e);
-        const long long j = (long long)RC.y * 64 + __ldg(a.sp_col + base + e);
-        if (i >= a.n || j >= a.n) continue;
-        float p[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const bool on = v < a.nv;
-          const float ci = on ? __ldg(a.c + i * a.n_vec + a.v0 + v) : 0.f;
-          const float cj = on ? __ldg(a.c + j * a.n_vec + a.v0 + v) : 0.f;
-          p[v] = wgt * ci * cj;
-        }
-        if constexpr (IDENT) {
-          if (i == j)
-#pragma unroll
-            for (int v = 0; v < NV; ++v) acc[0][v] += p[v];
-        } else {
-          const uint64_t lo = (uint64_t)(i < j ? i : j), hi = (uint64_t)(i < j ? j : i);
-          const uint64_t hb = mix64(lo + kGolden * hi);
-#pragma unroll
-          for (int q = 0; q < KS; ++q) {
-            const float o = to_unit(mix64(mix64(hb ^ kq[q]) ^ a.seed));
-#pragma unroll
-            for (int v = 0; v < NV; ++v) acc[q][v] = fmaf(p[v], o, acc[q][v]);
-          }
-        }
-      }
+      for (int e = lane; e < cnt; e += 32) entry(RC, base + e);
     }
   }
 #pragma unroll
