@@ -40,6 +40,10 @@ namespace cim {
 namespace {
 
 constexpr int kCtThreads = 256;
+// small-tile kernel: ~150 registers per thread (8 operators × 8 vectors of
+// accumulators), so 4-warp blocks let three blocks share an SM where one
+// 8-warp block left 8 warps resident
+constexpr int kCtSmallThreads = 128;
 
 template <typename T>
 struct ContractArgs {
@@ -186,7 +190,7 @@ __global__ void __launch_bounds__(kCtThreads, KS == 4 ? 2 : 3) contract_kernel(C
 // per-pair work as contract_kernel into per-thread accumulators for KS
 // operators.  The host loops over operator chunks of KS.
 template <typename T, int NV, int KS, bool IDENT>
-__global__ void __launch_bounds__(256) contract_small_kernel(ContractArgs<T> a, const int32_t *list, long long n_list) {
+__global__ void __launch_bounds__(kCtSmallThreads) contract_small_kernel(ContractArgs<T> a, const int32_t *list, long long n_list) {
   const int lane = threadIdx.x & 31;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   uint64_t kq[KS];
@@ -293,13 +297,13 @@ template <typename T, int NV>
 void launch_small_nv(const ContractArgs<T> &a, bool ident, const int32_t *list, long long n_list, int grid,
                      cudaStream_t s) {
   if (ident)
-    contract_small_kernel<T, NV, 1, true><<<grid, 256, 0, s>>>(a, list, n_list);
+    contract_small_kernel<T, NV, 1, true><<<grid, kCtSmallThreads, 0, s>>>(a, list, n_list);
   else if (a.kc == 1)
-    contract_small_kernel<T, NV, 1, false><<<grid, 256, 0, s>>>(a, list, n_list);
+    contract_small_kernel<T, NV, 1, false><<<grid, kCtSmallThreads, 0, s>>>(a, list, n_list);
   else if (a.kc <= 4)
-    contract_small_kernel<T, NV, 4, false><<<grid, 256, 0, s>>>(a, list, n_list);
+    contract_small_kernel<T, NV, 4, false><<<grid, kCtSmallThreads, 0, s>>>(a, list, n_list);
   else
-    contract_small_kernel<T, NV, 8, false><<<grid, 256, 0, s>>>(a, list, n_list);
+    contract_small_kernel<T, NV, 8, false><<<grid, kCtSmallThreads, 0, s>>>(a, list, n_list);
 }
 
 template <typename T, int NV>
@@ -357,7 +361,8 @@ int run_contract(const cim_half_tiles *H, const float *c, int n_vec, int m_ops, 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)(total < (long long)sms * 8 ? total : (long long)sms * 8);
-  const int grid_small = (int)std::min<long long>((n_small + 255) / 256, (long long)sms * 16);  // 32 tiles / warp
+  const int grid_small = (int)std::min<long long>((n_small + kCtSmallThreads - 1) / kCtSmallThreads,
+                                                  (long long)sms * 32);  // 32 tiles per warp
   const bool ident = kind == CIM_VALUES_IDENTITY;
   if (n_small > 0) {
     constexpr int kSmallKs = 8;
