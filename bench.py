@@ -506,9 +506,12 @@ def impl_ours(args):
             "dtype": "f32" if dtype == torch.float32 else "f64",
             "data": "synthetic",
             "config": {
-                "workload": (("C2" if args.tiles_per_gpu == TILES_PER_GPU else
+                "workload": (("C1 (the reference's CPU-runnable size; L2-sized working set)"
+                              if n == 65536 and abs(args.tiles_per_gpu - 6268) <= 64 else
+                              "C2" if args.tiles_per_gpu == TILES_PER_GPU and n == N_BASE else
                               "C3 on one GPU (T(1) of the strong-scaling pair)"
-                              if abs(args.tiles_per_gpu - 8 * TILES_PER_GPU) <= 8 * nb else "custom tile count")
+                              if n == N_BASE and abs(args.tiles_per_gpu - 8 * TILES_PER_GPU) <= 8 * nb
+                              else "custom size")
                              if world == 1 else f"C3-family weak scaling ({world}x C2 tiles, same n)")
                 + f": synthetic half-stored symmetric H, n={n}, block 64, {g_tiles} stored tiles "
                   f"({g_diag} diagonal + {g_off} upper), {H.nnz_stored / 1e9:.3f}e9 stored values"
