@@ -207,3 +207,16 @@ def test_basis_block_bound_never_drops_an_entry(name):
     need = set(zip(R[keep].tolist(), C[keep].tolist()))
     assert need <= set(map(tuple, cand.tolist()))
     assert np.all(cand[:, 0] <= cand[:, 1])
+
+
+def test_integration_doc_struct_matches_header():
+    """The ctypes stub INTEGRATION.md tells reference maintainers to add lists
+    every cim_half_tiles field in order (a short struct would let the library
+    read past it)."""
+    import re
+
+    doc = (Path(__file__).resolve().parent.parent / "INTEGRATION.md").read_text()
+    block = doc[doc.index("class cim_half_tiles(ctypes.Structure):"):]
+    block = block[:block.index("\n\n")]  # the class body ends at the first blank line
+    names = re.findall(r'\("([a-z_]+)", ctypes\.', block)
+    assert names == [f for f, _ in pkg._lib.CimHalfTiles._fields_]
