@@ -171,6 +171,13 @@ CIM_API const char *cim_last_error(void);
  * that walks every stored pair once per call; its validation contract
  * (ValueError before compute, pipeline.py:550-555) maps to CIM_EINVAL.
  * Supported k: f32 {1,2,4} ∪ 8ℕ (≤ 64); f64 {1,2} ∪ 4ℕ (≤ 64).
+ *
+ * Ownership and state: the caller owns X, Y and every array of H; the call
+ * is stream-ordered and asynchronous, re-entrant for distinct Y.  Library
+ * state per device: the SM count, a ring of scheduler counters, and, for
+ * widths above one kernel pass (f32 k ∈ {24, 32, 48, 64}, f64 k ∈ {12, 16,
+ * 32}), a grow-only scratch buffer per stream for a pass-major copy of X
+ * (n_pad · k elements; kept until process exit).
  */
 CIM_API int cim_sym_spmm(const cim_half_tiles *H, const void *X, void *Y, int32_t k,
                  int64_t ldx, int64_t ldy, uint32_t flags, void *stream);
