@@ -40,6 +40,10 @@ namespace cim {
 namespace {
 
 constexpr int kCtThreads = 256;
+#ifndef CIM_CT_MINB4
+#define CIM_CT_MINB4 2  // resident CTAs per SM the register budget targets (KS = 4; A/B knob)
+#endif
+#define CIM_CT_MINB(KS) ((KS) == 4 ? CIM_CT_MINB4 : 3)
 // small-tile kernel: ~150 registers per thread (8 operators × 8 vectors of
 // accumulators), so 4-warp blocks let three blocks share an SM where one
 // 8-warp block left 8 warps resident
@@ -69,7 +73,7 @@ struct ContractArgs {
 // (GK·KS ≥ the launch's operator count), IDENT: the identity operator (same
 // value for every k — one walk, added to every column of accum).
 template <typename T, int NV, int GK, int KS, bool IDENT>
-__global__ void __launch_bounds__(kCtThreads, KS == 4 ? 2 : 3) contract_kernel(ContractArgs<T> a) {
+__global__ void __launch_bounds__(kCtThreads, CIM_CT_MINB(KS)) contract_kernel(ContractArgs<T> a) {
   __shared__ unsigned rowmask[64][2];  // 32-bit words: shared atomicOr is native at 32 bits
   __shared__ __align__(16) float xr[64][NV];
   __shared__ __align__(16) float xc[64][NV];
