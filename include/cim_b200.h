@@ -74,6 +74,11 @@ extern "C" {
                                  fragment-layout tiles; reads each        
                                  tile twice — a validation mode)           */
 
+/* cim_contract_tiles flags (with CIM_ACCUMULATE) */
+#define CIM_CONTRACT_EXACT_F64 4u  /* products and sums in f64: contract_oracle
+                                      (pipeline.py:573-589) instead of the
+                                      reference's f32 products (:470-474)  */
+
 /* value kinds for cim_fill_synthetic_values */
 #define CIM_VALUES_H_XOR      0  /* h(i XOR j; seed)      pipeline.py:216-222 */
 #define CIM_VALUES_OP_HASH    1  /* O_ij(k=op_k; seed)    pipeline.py:224-232 */
@@ -176,8 +181,17 @@ CIM_API const char *cim_last_error(void);
  * is stream-ordered and asynchronous, re-entrant for distinct Y.  Library
  * state per device: the SM count, a ring of scheduler counters, and, for
  * widths above one kernel pass (f32 k ∈ {24, 32, 48, 64}, f64 k ∈ {12, 16,
- * 32}), a grow-only scratch buffer per stream for a pass-major copy of X
- * (n_pad · k elements; kept until process exit).
+ * 32}), one grow-only scratch buffer per device for a pass-major copy of X
+ * (n_pad · k elements; kept until process exit) whose users on different
+ * streams are ordered by an event.  Counter slots are reused only after the
+ * kernels that last used them finished (event-guarded ring), so concurrent
+ * calls on any number of streams never share a live counter.
+ *
+ * Subnormals: a tile's products accumulate in registers (IEEE), but they land
+ * in Y through red.global.add.f32, which PTX defines as flushing subnormal
+ * operands and results to zero — an absolute error below 2⁻¹²⁶ per reduction,
+ * visible only when partial sums of A·X fall under 1.2e-38.  CIM_DETERMINISTIC
+ * (plain stores) keeps gradual underflow.
  */
 CIM_API int cim_sym_spmm(const cim_half_tiles *H, const void *X, void *Y, int32_t k,
                  int64_t ldx, int64_t ldy, uint32_t flags, void *stream);
@@ -189,7 +203,10 @@ CIM_API int cim_sym_spmm(const cim_half_tiles *H, const void *X, void *Y, int32_
  * Copies and kernels of consecutive blocks overlap on three internal streams
  * (H2D, compute, D2H) through a caller-owned device `workspace` of
  * cim_host_batch_workspace_bytes(H, k) bytes (2 X + 2 Y buffers).
- * Synchronous: returns once every Y_b is on the host.
+ * Synchronous: returns once every Y_b is on the host.  The internal streams
+ * first wait for all work queued on the legacy default stream (e.g. the fill
+ * of H); work the caller queued on other streams must be complete (the
+ * Python wrapper synchronises the current stream).
  *
  * Replaces: the reference's host-array operator boundary (numpy in, numpy
  * out; contract_observables writes inputs.accum in place, pipeline.py:569)
@@ -418,6 +435,52 @@ CIM_API int cim_fill_masked_values(const int32_t *tile_rc, int64_t n_tiles, int6
 CIM_API int cim_contract_observables(const cim_half_tiles *H, const float *c, int32_t n_vec,
                                      int32_t m_ops, int32_t kind, uint64_t seed, double *accum,
                                      uint32_t flags, void *stream);
+
+/*
+ * Device: contract_observables / contract_oracle over the reference's own
+ * ORBITAL tiles — the literal drop-in of pipeline.py:534-589 (a Tile list,
+ * its Orbitals, the Basis and the InteractionRank):
+ *   accum[v*m_ops + k] (+)= Σ_t Σ_(i∈[r0,r1), j∈[c0,c1), kept(i,j)) c[i*ldc+v]·O_ij(k)·c[j*ldc+v]
+ * tile_ranges int32 (n_tiles, 4) on the device = (r0, r1, c0, c1) of each
+ * tile's row / column orbital (0 ≤ r0 < r1 ≤ n, same for c; the caller swaps
+ * them for the transposed walk, pipeline.py:446-447); kept(i, j) is the
+ * count predicate of _collect_pairs (popcount(bits_lo[i] ^ bits_lo[j]) ≤
+ * threshold and the lockstep occupation difference ≤ threshold,
+ * pipeline.py:270-280 / sparsity.py:132-151); bits_lo uint64 (n,) and occ
+ * uint16 (n, n_particles) in grouped order on the device.  c f32 (n, ldc)
+ * row-major on the device.  kind CIM_VALUES_OP_HASH or CIM_VALUES_IDENTITY.
+ * Products are the reference's f32 (c_vi·o)·c_vj, summed in f32 per lane and
+ * f64 across lanes, or all-f64 with CIM_CONTRACT_EXACT_F64.  accum f64
+ * (n_vec, m_ops) on the device, zeroed first unless CIM_ACCUMULATE.
+ */
+CIM_API int cim_contract_tiles(const uint64_t *bits_lo, const uint16_t *occ, int64_t n,
+                               int32_t n_particles, int32_t threshold, const int32_t *tile_ranges,
+                               int64_t n_tiles, const float *c, int64_t ldc, int32_t n_vec,
+                               int32_t m_ops, int32_t kind, uint64_t seed, double *accum,
+                               uint32_t flags, void *stream);
+
+/*
+ * Device: exclusive prefix sum of int64 counts — the reference's scan motif
+ * (scan_serial, scan.py:131-139; CountsAndOffsets, scan.py:45-65) for the
+ * count → scan → fill construction: y[i] = Σ_(j<i) x[j] for i < n and
+ * y[n] = the total (so y is offsets followed by total; y has n+1 slots).
+ * Reduce-then-scan in three stream-ordered launches (fixed summation order:
+ * bitwise deterministic); x may alias y[0..n) only if x == y.  Scratch for
+ * the per-block sums is stream-ordered (cudaMallocAsync).
+ */
+CIM_API int cim_exclusive_scan_i64(const int64_t *x, int64_t n, int64_t *y, void *stream);
+
+/*
+ * Device: the per-tile row scan of the sparse-tile build.  rowcnt int32
+ * [n_tiles][64] (entries per local row) → rowptr int16 [n_tiles][72]
+ * (rowptr[t][r] = Σ_(r'<r) rowcnt[t][r'], r ≤ 64; slots 65..71 zero),
+ * counts int64 [n_tiles] (real entries per tile) and entry_off int64
+ * [n_tiles+1] = exclusive scan of counts rounded up to `align` (the padded
+ * tile ranges of cim_sparse_tiles), via cim_exclusive_scan_i64.
+ */
+CIM_API int cim_sparse_tile_offsets(const int32_t *rowcnt, int64_t n_tiles, int32_t align,
+                                    int16_t *rowptr, int64_t *counts, int64_t *entry_off,
+                                    void *stream);
 
 /*
  * Device: repack row-major dense tiles src[n_tiles][64][64] into fragment

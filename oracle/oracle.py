@@ -244,6 +244,48 @@ def contract_vmv(c, pairs_i, pairs_j, m_ops: int, op_code: int, seed: int) -> np
     return out
 
 
+def occ_diff(a, b) -> int:
+    """Lockstep walk of two sorted occupation lists: 2·max(#only-in-a,
+    #only-in-b) (_occ_diff, sparsity.py:132-151)."""
+    i1 = i2 = d1 = d2 = 0
+    while i1 < len(a) and i2 < len(b):
+        if a[i1] == b[i2]:
+            i1 += 1
+            i2 += 1
+        elif a[i1] < b[i2]:
+            d1 += 1
+            i1 += 1
+        else:
+            d2 += 1
+            i2 += 1
+    return 2 * max(d1, d2)
+
+
+def scan_serial(x) -> np.ndarray:
+    """Exclusive prefix sum, sequential (scan_serial, scan.py:131-139): y[i] =
+    Σ_(j<i) x[j] in int64 (wrapping like the reference's njit int64 adds)."""
+    x = np.ascontiguousarray(x, dtype=np.int64)
+    y = np.empty_like(x)
+    s = np.int64(0)
+    if x.size <= 4096:
+        for i in range(x.size):
+            y[i] = s
+            s = np.int64(s + x[i])
+        return y
+    with np.errstate(over="ignore"):
+        c = np.cumsum(x, dtype=np.int64)  # same wrapping integer sums, vectorised
+    y[0] = 0
+    y[1:] = c[:-1]
+    return y
+
+
+def counts_to_offsets(counts):
+    """(offsets, total) of a CountsAndOffsets (scan.py:45-65) built from counts."""
+    off = scan_serial(counts)
+    total = int(off[-1] + np.int64(counts[-1])) if off.size else 0
+    return off, total
+
+
 def contraction_tolerance(c, n_pairs: int) -> float:
     """2⁻²⁰·n_pairs·max|c|² (test_pipeline.py:33-36)."""
     return TOLERANCE_EPS * max(n_pairs, 1) * float(np.abs(c).max()) ** 2

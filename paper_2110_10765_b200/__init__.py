@@ -11,8 +11,12 @@ C-ABI in ``libcim_b200.so``, include/cim_b200.h):
                           blocks, copies and kernels pipelined (PCIe-bound)
 * ``ShardedSymSpmm``    — row-block sharding over GPUs (NCCL all-gather X /
                           reduce-scatter Y)
-* ``contract_observables``, ``ObservablesInput``, ``random_coefficients``,
-  ``STRATEGIES``, ``OP_KINDS`` — the reference's observables API on the GPU
+* ``contract_observables`` / ``contract_oracle`` (the reference's exact
+  signatures over orbital tiles, pipeline.py:534-589), ``contract_pattern``
+  (over a stored HalfTiles pattern), ``ObservablesInput``,
+  ``random_coefficients``, ``STRATEGIES``, ``OP_KINDS``, and the argument
+  types ``Orbital`` / ``Tile`` / ``InteractionRank`` with ``group_orbitals`` /
+  ``enumerate_tiles`` — the reference's observables API on the GPU
 * ``lobpcg`` / ``lobpcg_sym`` — block LOBPCG eigensolver over the SpMM
   (single GPU or row-sharded with the 3m×3m Gram all-reduce)
 * ``load_basis`` / ``save_basis`` / ``group_basis`` and
@@ -27,8 +31,16 @@ from .lobpcg import LobpcgResult, lobpcg, lobpcg_sym
 from .observables import (
     OP_KINDS,
     STRATEGIES,
+    BasisArrays,
+    InteractionRank,
     ObservablesInput,
+    Orbital,
+    Tile,
     contract_observables,
+    contract_oracle,
+    contract_pattern,
+    enumerate_tiles,
+    group_orbitals,
     random_coefficients,
 )
 from .sharded import ShardedSymSpmm, row_chunks
@@ -45,7 +57,15 @@ __all__ = [
     "OP_KINDS",
     "STRATEGIES",
     "ShardedSymSpmm",
+    "BasisArrays",
+    "InteractionRank",
+    "Orbital",
+    "Tile",
     "contract_observables",
+    "contract_oracle",
+    "contract_pattern",
+    "enumerate_tiles",
+    "group_orbitals",
     "group_basis",
     "lib",
     "load_basis",

@@ -18,6 +18,7 @@ CIM_F32, CIM_F64 = 0, 1
 CIM_ACCUMULATE = 1
 CIM_DETERMINISTIC = 2
 CIM_GRAM_FAST = 1
+CIM_CONTRACT_EXACT_F64 = 4
 CIM_VALUES_H_XOR, CIM_VALUES_OP_HASH, CIM_VALUES_IDENTITY = 0, 1, 2
 CIM_LAYOUT_FRAG, CIM_LAYOUT_TC = 0, 1
 BLOCK = 64
@@ -56,6 +57,9 @@ EXPORTS = (
     "cim_sparse_small_max",
     "cim_tsmm_blocked_hc",
     "cim_block_residual",
+    "cim_contract_tiles",
+    "cim_exclusive_scan_i64",
+    "cim_sparse_tile_offsets",
 )
 
 
@@ -180,6 +184,12 @@ def lib() -> ctypes.CDLL:
     L.cim_tsmm_blocked_hc.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_int64, c.c_int32, c.c_void_p, c.c_int32,
                                       c.c_float, c.c_float, c.c_void_p, c.c_int64, c.c_int32, c.c_int64, c.c_int64,
                                       c.c_void_p]
+    L.cim_contract_tiles.argtypes = [c.c_void_p, c.c_void_p, c.c_int64, c.c_int32, c.c_int32, c.c_void_p, c.c_int64,
+                                     c.c_void_p, c.c_int64, c.c_int32, c.c_int32, c.c_int32, c.c_uint64, c.c_void_p,
+                                     c.c_uint32, c.c_void_p]
+    L.cim_exclusive_scan_i64.argtypes = [c.c_void_p, c.c_int64, c.c_void_p, c.c_void_p]
+    L.cim_sparse_tile_offsets.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_void_p, c.c_void_p, c.c_void_p,
+                                          c.c_void_p]
     for name in EXPORTS:
         if name not in ("cim_version", "cim_last_error"):
             getattr(L, name).restype = c.c_int

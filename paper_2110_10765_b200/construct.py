@@ -14,7 +14,8 @@ streams:
    over-accepts);
 2. device: ``cim_basis_count_tiles`` counts kept entries per (tile, row) with
    the reference predicate (popcount prefilter + exact occupation walk);
-3. torch scans the counts; tiles above the dense fill go dense
+3. the device scan (``cim_sparse_tile_offsets`` / ``cim_exclusive_scan_i64``,
+   the reference's scan motif) turns the counts into offsets; tiles above the dense fill go dense
    (``cim_basis_fill_dense``), the rest sparse (``cim_basis_fill_sparse`` +
    ``cim_sparse_build_columns``); values are h(i XOR j; seed).
 
@@ -38,6 +39,7 @@ from .halftiles import (
     HalfTiles,
     SparseTiles,
     _as_torch_dtype,
+    sparse_tile_offsets,
     _dtype_code,
 )
 
@@ -234,15 +236,11 @@ def from_basis(basis_or_occ, bits_lo=None, *, rank: int = 2, value_seed: int = 0
     if s_idx.size:
         Ts = s_idx.size
         rc_s = np.ascontiguousarray(cand[s_idx])
-        rcnt = rowcnt[torch.from_numpy(s_idx).to(dev)].to(torch.int64)
-        rowptr = torch.zeros((Ts, SPARSE_PTR_STRIDE), dtype=torch.int64, device=dev)
-        rowptr[:, 1:65] = torch.cumsum(rcnt, dim=1)
-        cnt = rowptr[:, 64]
-        off = torch.zeros(Ts + 1, dtype=torch.int64, device=dev)
-        off[1:] = torch.cumsum((cnt + SPARSE_ALIGN - 1) // SPARSE_ALIGN * SPARSE_ALIGN, dim=0)
+        rcnt = rowcnt[torch.from_numpy(s_idx).to(dev)]
+        rowptr, cnt, off = sparse_tile_offsets(rcnt, Ts)
         off_host = off.cpu().numpy()
         E = int(off_host[-1])
-        sp = SparseTiles(tile_rc=torch.from_numpy(rc_s).to(dev), entry_off=off, rowptr=rowptr.to(torch.int16),
+        sp = SparseTiles(tile_rc=torch.from_numpy(rc_s).to(dev), entry_off=off, rowptr=rowptr,
                          colptr=torch.zeros((Ts, SPARSE_PTR_STRIDE), dtype=torch.int16, device=dev),
                          col=torch.zeros(max(E, 1), dtype=torch.uint8, device=dev),
                          row=torch.zeros(max(E, 1), dtype=torch.uint8, device=dev),

@@ -29,6 +29,7 @@ struct PipeState {
   bool init = false;
   cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
   cudaEvent_t x_ready[2], comp_done[2], y_free[2];
+  cudaEvent_t entry = nullptr;  // the caller's prior work (legacy default stream)
 };
 std::mutex g_pipe_mu;
 std::vector<PipeState> g_pipe;
@@ -43,6 +44,7 @@ int pipe_state(PipeState **out) {
     cudaError_t e = cudaSuccess;
     for (cudaStream_t *s : {&p.h2d, &p.comp, &p.d2h})
       if (e == cudaSuccess) e = cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.entry, cudaEventDisableTiming);
     for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
       e = cudaEventCreateWithFlags(&p.x_ready[i], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.comp_done[i], cudaEventDisableTiming);
@@ -94,6 +96,12 @@ extern "C" int cim_sym_spmm_host_batch(const cim_half_tiles *H, const void *cons
     return cim::set_error(CIM_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
   };
   cudaError_t e = cudaSuccess;
+  // The library's streams are non-blocking: order them after everything the
+  // caller queued on the legacy default stream (e.g. the tile-value fill of a
+  // freshly built matrix) — the pipeline must not read H before it is written.
+  if ((e = cudaEventRecord(ps->entry, cudaStreamLegacy)) != cudaSuccess) return cuda_fail(e, "record entry");
+  for (cudaStream_t st : {ps->h2d, ps->comp})
+    if ((e = cudaStreamWaitEvent(st, ps->entry, 0)) != cudaSuccess) return cuda_fail(e, "wait entry");
   // pad rows of the X buffers meet zero matrix entries but must be finite
   if (buf > live) {
     for (int s = 0; s < 2 && e == cudaSuccess; ++s) e = cudaMemsetAsync(Xd[s] + live, 0, buf - live, ps->h2d);

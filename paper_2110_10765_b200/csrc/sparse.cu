@@ -26,6 +26,7 @@
 
 #include "cim_b200.h"
 #include "common.cuh"
+#include "counter_ring.h"
 #include "host_util.h"
 
 namespace cim {
@@ -493,12 +494,12 @@ __global__ void fill_sparse_values_kernel(const int2 *tile_rc, const long long *
 
 struct SpState {
   int sms = 0;
-  unsigned int *counters = nullptr;
-  int pos = 0;
+  CounterRing *ring = nullptr;  // ticket counters (counter_ring.h)
 };
 std::mutex g_sp_mu;
 std::vector<SpState> g_sp;
-constexpr int kSpRing = 1024;
+CounterRing g_sp_rings[64];
+constexpr int kSpRingBlocks = 256;
 
 int sp_state(SpState **out) {
   int dev = 0;
@@ -507,11 +508,17 @@ int sp_state(SpState **out) {
   if ((int)g_sp.size() <= dev) g_sp.resize(dev + 1);
   SpState &s = g_sp[dev];
   if (s.sms == 0) {
+    if (dev >= 64) return set_error(CIM_EUNSUPPORTED, "device index >= 64");
     cudaError_t e = cudaDeviceGetAttribute(&s.sms, cudaDevAttrMultiProcessorCount, dev);
-    if (e == cudaSuccess) e = cudaMalloc(&s.counters, kSpRing * sizeof(unsigned int));
     if (e != cudaSuccess) {
       s.sms = 0;
       return set_error(CIM_ECUDA, std::string("sparse state: ") + cudaGetErrorString(e));
+    }
+    s.ring = &g_sp_rings[dev];
+    const int rc = s.ring->init(kSpRingBlocks);
+    if (rc) {
+      s.sms = 0;
+      return rc;
     }
   }
   *out = &s;
@@ -545,14 +552,10 @@ int launch_sparse(const cim_sparse_tiles *S, const void *X, void *Y, int k, long
 #endif
   const size_t smem = (size_t)stages * L.bytes + 16 * (size_t)stages;  // + full / empty mbarriers
   if (smem > 227 * 1024) return set_error(CIM_EUNSUPPORTED, "k too large for the sparse-tile stages");
-  unsigned int *ctr;
-  {
-    std::lock_guard<std::mutex> lk(g_sp_mu);
-    if (st->pos >= kSpRing) st->pos = 0;
-    ctr = st->counters + st->pos++;
-  }
-  cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(unsigned int), stream);
-  if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("sparse counter: ") + cudaGetErrorString(e));
+  CounterLease lease;
+  if (const int lrc = lease.take(*st->ring, stream, 1)) return lrc;
+  unsigned int *ctr = lease.ctr;
+  cudaError_t e = cudaSuccess;
   SparseParams p;
   p.tile_rc = reinterpret_cast<const int2 *>(S->tile_rc);
   p.entry_off = reinterpret_cast<const long long *>(S->entry_off);

@@ -49,6 +49,7 @@
 
 #include "cim_b200.h"
 #include "common.cuh"
+#include "counter_ring.h"
 #include "host_util.h"
 
 namespace cim {
@@ -1021,13 +1022,16 @@ namespace {
 
 struct DeviceState {
   int sms = 0;
-  unsigned int *counters = nullptr;  // ring of scheduler counters
-  int ring_pos = 0;
-  // grow-only scratch per stream (pass-major X copies): work on one stream is
-  // ordered, so reusing that stream's buffer across calls is race-free
-  std::vector<std::pair<cudaStream_t, std::pair<void *, size_t>>> scratch;
+  CounterRing *ring = nullptr;  // scheduler ticket counters (counter_ring.h)
+  // one grow-only scratch buffer per device (pass-major X copies); users on
+  // any stream are ordered through scratch_ev (waited before use, recorded
+  // after the user's kernels are queued) under scratch_mu
+  void *scratch = nullptr;
+  size_t scratch_bytes = 0;
+  cudaEvent_t scratch_ev = nullptr;
 };
-constexpr int kCounterRing = 4096;
+constexpr int kCounterBlocks = 512;
+CounterRing g_rings[64];
 std::mutex g_mu;
 std::vector<DeviceState> g_dev;
 
@@ -1041,46 +1045,42 @@ int device_state(DeviceState **out) {
     int sms = 0;
     cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("cudaDeviceGetAttribute: ") + cudaGetErrorString(e));
-    e = cudaMalloc(&d.counters, kCounterRing * sizeof(unsigned int));
-    if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("cudaMalloc counters: ") + cudaGetErrorString(e));
+    if (dev >= 64) return set_error(CIM_EUNSUPPORTED, "device index >= 64");
+    d.ring = &g_rings[dev];
+    const int rc = d.ring->init(kCounterBlocks);
+    if (rc) return rc;
     d.sms = sms;
   }
   *out = &d;
   return CIM_OK;
 }
 
-// take `n` consecutive counter slots (host-side ring; slots are memset on the
-// caller's stream before use, so concurrent streams never share a slot)
-unsigned int *take_counters(DeviceState *d, int n) {
-  std::lock_guard<std::mutex> lk(g_mu);
-  if (d->ring_pos + n > kCounterRing) d->ring_pos = 0;
-  unsigned int *p = d->counters + d->ring_pos;
-  d->ring_pos += n;
-  return p;
+std::mutex g_scratch_mu;
+
+// The device's scratch buffer of at least `bytes` for work queued on
+// `stream` (call with g_scratch_mu held until scratch_done): `stream` first
+// waits for the buffer's previous user; a too-small buffer is released after
+// that user (cudaFreeAsync on the now-ordered stream) and regrown.
+int scratch_begin(DeviceState *d, cudaStream_t stream, size_t bytes, void **out) {
+  cudaError_t e = cudaSuccess;
+  if (d->scratch_ev) e = cudaStreamWaitEvent(stream, d->scratch_ev, 0);
+  else e = cudaEventCreateWithFlags(&d->scratch_ev, cudaEventDisableTiming);
+  if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("scratch event: ") + cudaGetErrorString(e));
+  if (d->scratch_bytes < bytes) {
+    if (d->scratch) cudaFreeAsync(d->scratch, stream);
+    d->scratch = nullptr;
+    d->scratch_bytes = 0;
+    e = cudaMallocAsync(&d->scratch, bytes, stream);
+    if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("scratch: ") + cudaGetErrorString(e));
+    d->scratch_bytes = bytes;
+  }
+  *out = d->scratch;
+  return CIM_OK;
 }
 
-// This stream's scratch buffer of at least `bytes` (grown on demand; the old
-// buffer is released after the stream's queued work, cudaFreeAsync).
-int stream_scratch(DeviceState *d, cudaStream_t stream, size_t bytes, void **out) {
-  std::lock_guard<std::mutex> lk(g_mu);
-  for (auto &e : d->scratch)
-    if (e.first == stream) {
-      if (e.second.second < bytes) {
-        cudaFreeAsync(e.second.first, stream);
-        void *p = nullptr;
-        const cudaError_t err = cudaMallocAsync(&p, bytes, stream);
-        if (err != cudaSuccess) return set_error(CIM_ECUDA, std::string("scratch: ") + cudaGetErrorString(err));
-        e.second = {p, bytes};
-      }
-      *out = e.second.first;
-      return CIM_OK;
-    }
-  void *p = nullptr;
-  const cudaError_t err = cudaMallocAsync(&p, bytes, stream);
-  if (err != cudaSuccess) return set_error(CIM_ECUDA, std::string("scratch: ") + cudaGetErrorString(err));
-  d->scratch.push_back({stream, {p, bytes}});
-  *out = p;
-  return CIM_OK;
+int scratch_done(DeviceState *d, cudaStream_t stream) {
+  const cudaError_t e = cudaEventRecord(d->scratch_ev, stream);
+  return e == cudaSuccess ? CIM_OK : set_error(CIM_ECUDA, std::string("scratch event: ") + cudaGetErrorString(e));
 }
 
 struct LaunchCfg {
@@ -1173,9 +1173,9 @@ int launch_kernel(const cim_half_tiles *H, const void *X, void *Y, int k, long l
   grid = std::min<long long>(grid, H->n_units);
   if (grid < 1) return CIM_OK;
 
-  unsigned int *ctr = take_counters(ds, passes);
-  e = cudaMemsetAsync(ctr, 0, passes * sizeof(unsigned int), stream);
-  if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("cudaMemsetAsync counter: ") + cudaGetErrorString(e));
+  CounterLease lease;
+  if (const int rc = lease.take(*ds->ring, stream, passes)) return rc;
+  unsigned int *ctr = lease.ctr;
 
   for (int ps = 0; ps < passes; ++ps) {
     SpmmParams p;
@@ -1209,7 +1209,8 @@ struct Chunks {  // X / Y as per-rank chunks (cim_sym_spmm_chunked); n = 1: plai
 
 template <typename T, int G, int KROW>
 int launch_k8(const cim_half_tiles *H, const Chunks &ck, long long ldy, cudaStream_t stream, DeviceState *ds) {
-  static std::once_flag attr_once[64];
+  static std::mutex attr_mu;
+  static bool attr_done[64] = {};
   constexpr int SUBS = 2 / G;
   constexpr int passes = KROW / (WideE<T>::VPG * G);
   const unsigned int tile_bytes = kTileElems * sizeof(T);
@@ -1223,15 +1224,21 @@ int launch_k8(const cim_half_tiles *H, const Chunks &ck, long long ldy, cudaStre
   int dev = 0;
   cudaGetDevice(&dev);
   cudaError_t e = cudaSuccess;
-  std::call_once(attr_once[dev & 63], [&] {
-    e = cudaFuncSetAttribute(sym_spmm_k8_kernel<T, G, KROW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  });
-  if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("cudaFuncSetAttribute(k8): ") + cudaGetErrorString(e));
+  {
+    // set once per device; a failure is reported on every call (and retried)
+    std::lock_guard<std::mutex> lk(attr_mu);
+    if (!attr_done[dev & 63]) {
+      e = cudaFuncSetAttribute(sym_spmm_k8_kernel<T, G, KROW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess)
+        return set_error(CIM_ECUDA, std::string("cudaFuncSetAttribute(k8): ") + cudaGetErrorString(e));
+      attr_done[dev & 63] = true;
+    }
+  }
   long long grid = std::min<long long>(ds->sms, (H->n_units + SUBS - 1) / SUBS);
   if (grid < 1) return CIM_OK;
-  unsigned int *ctr = take_counters(ds, passes);
-  e = cudaMemsetAsync(ctr, 0, passes * sizeof(unsigned int), stream);
-  if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("cudaMemsetAsync counter: ") + cudaGetErrorString(e));
+  CounterLease lease;
+  if (const int rc = lease.take(*ds->ring, stream, passes)) return rc;
+  unsigned int *ctr = lease.ctr;
   for (int ps = 0; ps < passes; ++ps) {
     SpmmParams p;
     p.units = reinterpret_cast<const int4 *>(H->units);
@@ -1287,7 +1294,8 @@ int launch_k8_passes(const cim_half_tiles *H, const void *X, void *Y, int k, lon
   const int passes = k / W;
   const long long n_pad = (H->n + kBlock - 1) / kBlock * kBlock;
   void *Xp = nullptr;
-  int rc = stream_scratch(ds, stream, (size_t)n_pad * k * sizeof(T), &Xp);
+  std::lock_guard<std::mutex> lk(g_scratch_mu);
+  int rc = scratch_begin(ds, stream, (size_t)n_pad * k * sizeof(T), &Xp);
   if (rc) return rc;
   const int row_chunks = k * (int)sizeof(T) / 16, w_chunks = W * (int)sizeof(T) / 16;
   const long long total = n_pad * row_chunks;
@@ -1301,7 +1309,8 @@ int launch_k8_passes(const cim_half_tiles *H, const void *X, void *Y, int k, lon
     ck.y[0] = static_cast<T *>(Y) + ps * W;
     rc = launch_k8<T, G, W>(H, ck, ldy, stream, ds);
   }
-  return rc;
+  const int rc2 = scratch_done(ds, stream);
+  return rc ? rc : rc2;
 }
 
 // The wide-register kernel for (dtype, k), or EUNSUPPORTED.
@@ -1402,7 +1411,9 @@ static int sym_spmm_dense(const cim_half_tiles *H, const void *X, void *Y, int32
 
   if (H->layout == CIM_LAYOUT_TC) {
     if ((reinterpret_cast<uintptr_t>(Y) & 15) || (ldy % 4)) return set_error(CIM_EINVAL, "TC path needs 16-B aligned Y rows");
-    return sym_spmm_tc_dispatch(H, X, Y, k, ldy, stream, ds->sms, take_counters(ds, 1));
+    CounterLease lease;
+    if (const int lrc = lease.take(*ds->ring, stream, 1)) return lrc;
+    return sym_spmm_tc_dispatch(H, X, Y, k, ldy, stream, ds->sms, lease.ctr);
   }
 
 #ifndef CIM_NO_K8

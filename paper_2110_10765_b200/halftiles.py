@@ -103,6 +103,39 @@ def partition_units(units: np.ndarray, parts: int) -> np.ndarray:
     return b
 
 
+def sparse_tile_offsets(rowcnt: torch.Tensor, n_tiles: int):
+    """Device scan step of the sparse-tile build (the reference's
+    counts_to_offsets / scan motif, scan.py:45-65, :131-139, on the GPU):
+    rowcnt int32 (≥T, 64) per-row entry counts → (rowptr int16 (T, 72),
+    counts int64 (T,), entry_off int64 (T+1,)) via ``cim_sparse_tile_offsets``
+    (warp row scans + ``cim_exclusive_scan_i64`` over the padded tile sizes)."""
+    dev = rowcnt.device
+    T = int(n_tiles)
+    rc = rowcnt.to(torch.int32).contiguous()
+    rowptr = torch.empty((max(T, 1), SPARSE_PTR_STRIDE), dtype=torch.int16, device=dev)
+    counts = torch.empty(max(T, 1), dtype=torch.int64, device=dev)
+    off = torch.empty(T + 1, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        check(lib().cim_sparse_tile_offsets(rc.data_ptr() if T else None, T, SPARSE_ALIGN,
+                                            rowptr.data_ptr() if T else None, counts.data_ptr() if T else None,
+                                            off.data_ptr(), torch.cuda.current_stream(dev).cuda_stream),
+              "cim_sparse_tile_offsets")
+    return rowptr[:T], counts[:T], off
+
+
+def exclusive_scan(x: torch.Tensor) -> torch.Tensor:
+    """Offsets + total of int64 device counts (scan_serial, scan.py:131-139,
+    followed by the total, as CountsAndOffsets holds them): y[i] = Σ_(j<i) x[j],
+    y[n] = Σ x — ``cim_exclusive_scan_i64``."""
+    x = x.to(torch.int64).contiguous()
+    n = x.numel()
+    y = torch.empty(n + 1, dtype=torch.int64, device=x.device)
+    with torch.cuda.device(x.device):
+        check(lib().cim_exclusive_scan_i64(x.data_ptr() if n else None, n, y.data_ptr(),
+                                           torch.cuda.current_stream(x.device).cuda_stream), "cim_exclusive_scan_i64")
+    return y
+
+
 def synthetic_pattern(nb: int, p: float, seed: int = 0) -> np.ndarray:
     """Tile pattern of the BASELINE configs: every diagonal tile, plus each
     upper pair (R<C) kept with probability p.
@@ -268,6 +301,40 @@ class SparseTiles:
                                         staged_tiles=st.data_ptr(), n_staged=n_st,
                                         small_tiles=sm.data_ptr(), n_small=n_sm, staged_max_entries=st_max)
         return self._desc
+
+    def select_rows(self, r_lo: int, r_hi: int) -> "SparseTiles":
+        """Sparse tiles with R in [r_lo, r_hi): a zero-copy slice (entry
+        offsets rebased) when the tiles are (R, C)-ordered, else a gather."""
+        rc = self.tile_rc_host
+        sel = np.flatnonzero((rc[:, 0] >= r_lo) & (rc[:, 0] < r_hi))
+        contiguous = sel.size == 0 or (sel[-1] - sel[0] + 1 == sel.size)
+        if contiguous:
+            s0 = int(sel[0]) if sel.size else 0
+            s1 = s0 + sel.size
+            e0, e1 = int(self.entry_off_host[s0]), int(self.entry_off_host[s1])
+            off_host = self.entry_off_host[s0:s1 + 1] - e0
+            ev = lambda t: t[e0:max(e1, e0 + 1)]  # noqa: E731  (entry arrays keep ≥ 1 slot)
+            return SparseTiles(tile_rc=self.tile_rc[s0:s1], entry_off=self.entry_off[s0:s1 + 1] - e0,
+                               rowptr=self.rowptr[s0:s1], colptr=self.colptr[s0:s1], col=ev(self.col),
+                               row=ev(self.row), cperm=ev(self.cperm), vals=ev(self.vals),
+                               tile_rc_host=rc[s0:s1], entry_off_host=off_host, counts_host=self.counts_host[s0:s1])
+        tid, r, c, v, _ = self.to_entries()
+        m = np.isin(tid, sel)
+        remap = np.full(self.n_tiles, -1, np.int64)
+        remap[sel] = np.arange(sel.size)
+        return SparseTiles.from_entries(rc[sel], remap[tid[m]], r[m], c[m], v[m], self.vals.dtype,
+                                        self.tile_rc.device)
+
+    def with_lists(self, staged: np.ndarray, small: np.ndarray) -> "SparseTiles":
+        """The same tiles with the kernel work lists restricted to ``staged`` /
+        ``small`` (subsets of ``work_split()``'s lists) — a schedule group."""
+        self.work_split()
+        st_max = self._split[4]
+        dev = self.tile_rc.device
+        mk = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.int32) if a.size else np.zeros(1, np.int32)).to(dev)  # noqa: E731
+        return SparseTiles(self.tile_rc, self.entry_off, self.rowptr, self.colptr, self.col, self.row, self.cperm,
+                           self.vals, self.tile_rc_host, self.entry_off_host, self.counts_host,
+                           _split=(mk(staged), int(staged.size), mk(small), int(small.size), st_max))
 
     def with_values(self, vals: torch.Tensor) -> "SparseTiles":
         return SparseTiles(self.tile_rc, self.entry_off, self.rowptr, self.colptr, self.col, self.row, self.cperm,
@@ -571,15 +638,10 @@ class HalfTiles:
         with torch.cuda.device(dev):
             check(L.cim_sparse_count_rows(t_rc.data_ptr() if T else None, T, n, float(fill), fill_seed,
                                           rowcnt.data_ptr(), stream), "cim_sparse_count_rows")
-        rowcnt = rowcnt[:T]
-        rowptr = torch.zeros((T, SPARSE_PTR_STRIDE), dtype=torch.int64, device=dev)
-        rowptr[:, 1:65] = torch.cumsum(rowcnt, dim=1)
-        counts = rowptr[:, 64]
-        off = torch.zeros(T + 1, dtype=torch.int64, device=dev)
-        off[1:] = torch.cumsum((counts + SPARSE_ALIGN - 1) // SPARSE_ALIGN * SPARSE_ALIGN, dim=0)
+        rowptr, counts, off = sparse_tile_offsets(rowcnt, T)
         off_host = off.cpu().numpy()
         E = int(off_host[-1])
-        sp = SparseTiles(tile_rc=t_rc, entry_off=off, rowptr=rowptr.to(torch.int16),
+        sp = SparseTiles(tile_rc=t_rc, entry_off=off, rowptr=rowptr,
                          colptr=torch.zeros((T, SPARSE_PTR_STRIDE), dtype=torch.int16, device=dev),
                          col=torch.zeros(max(E, 1), dtype=torch.uint8, device=dev),
                          row=torch.zeros(max(E, 1), dtype=torch.uint8, device=dev),
@@ -707,12 +769,24 @@ class HalfTiles:
         (pipeline.py:319-330), then ``from_coo``."""
         start = {o.id: o.start for o in orbitals}
         size = {o.id: o.stop - o.start for o in orbitals}
+        tiles = list(skeleton.tiles)
         seg_row = np.concatenate(
-            [start[t.row_orbital] + np.arange(size[t.row_orbital], dtype=np.int64) for t in skeleton.tiles])
-        i = np.repeat(seg_row, np.asarray(skeleton.segments.counts, dtype=np.int64))
+            [start[t.row_orbital] + np.arange(size[t.row_orbital], dtype=np.int64) for t in tiles]
+            or [np.zeros(0, np.int64)])
+        counts = np.asarray(skeleton.segments.counts, dtype=np.int64)
+        colind = np.asarray(skeleton.colind, dtype=np.int64)
+        values = np.asarray(skeleton.values)
+        # the skeleton invariants (pipeline.py:106-112, scan.py:57-65): one
+        # segment per (tile, row), Σ counts = len(colind) = len(values)
+        if counts.shape != seg_row.shape:
+            raise ValueError(f"skeleton has {counts.size} segments, its tiles span {seg_row.size} rows")
+        if not (int(counts.sum()) == colind.size == values.size):
+            raise ValueError(f"segment counts ({int(counts.sum())}) and array lengths "
+                             f"({colind.size}, {values.size}) disagree")
+        i = np.repeat(seg_row, counts)
         if n is None:
             n = max(o.stop for o in orbitals)
-        return cls.from_coo(n, i, skeleton.colind, skeleton.values, **kw)
+        return cls.from_coo(n, i, colind, values, **kw)
 
     # ----------------------------------------------------------------- export
     def dense_tiles(self) -> torch.Tensor:
@@ -760,6 +834,51 @@ class HalfTiles:
             H.sparse = SparseTiles.from_arrays(z, H.dtype, H.device)
             H._desc = None
         return H
+
+    def row_costs(self) -> np.ndarray:
+        """Streamed bytes per block row (dense tiles at their full size, sparse
+        tiles at value + index bytes per entry) — the balance weight of the
+        row-block partition."""
+        s = self.vals.element_size()
+        cost = np.bincount(self.tile_rc_host[:, 0], minlength=self.nb).astype(np.float64) * (BLOCK * BLOCK * s)
+        if self.sparse is not None and self.sparse.n_tiles:
+            cost += np.bincount(self.sparse.tile_rc_host[:, 0], weights=self.sparse.counts_host * (s + 4.0),
+                                minlength=self.nb)
+        return cost
+
+    def partition_rows(self, parts: int) -> np.ndarray:
+        """Block-row boundaries (len parts+1) of `parts` contiguous panels with
+        balanced streamed bytes (dense and sparse tiles); rows never straddle."""
+        if parts < 1:
+            raise ValueError("parts must be >= 1")
+        pre = np.concatenate([[0.0], np.cumsum(self.row_costs())])
+        total = pre[-1]
+        b = np.zeros(parts + 1, dtype=np.int64)
+        for q in range(1, parts):
+            b[q] = max(int(np.searchsorted(pre, total * q / parts, side="left")), b[q - 1])
+        b[parts] = self.nb
+        return np.minimum(b, self.nb)
+
+    def shard_rows(self, r_lo: int, r_hi: int) -> "HalfTiles":
+        """The tiles of block rows [r_lo, r_hi) (dense and sparse; same n) —
+        a GPU's panel.  Dense tiles and their arrays are views; sparse tiles
+        are a contiguous slice when stored in (R, C) order (every constructor
+        here), else gathered."""
+        if self.meta.get("bands", 1) > 1:
+            raise ValueError("row sharding needs (R, C)-ordered tiles (bands=1)")
+        rc = self.tile_rc_host
+        t0 = int(np.searchsorted(rc[:, 0], r_lo, side="left"))
+        t1 = int(np.searchsorted(rc[:, 0], r_hi, side="left"))
+        u = self.units_host
+        keep = (u[:, 0] >= r_lo) & (u[:, 0] < r_hi)
+        units = u[keep].copy()
+        units[:, 1:3] -= t0
+        sub = HalfTiles(n=self.n, tile_rc=self.tile_rc[t0:t1], units=torch.from_numpy(units).to(self.device),
+                        vals=self.vals[t0:t1], tile_rc_host=rc[t0:t1], units_host=units, layout=self.layout,
+                        meta=dict(self.meta, shard_rows=(int(r_lo), int(r_hi))))
+        if self.sparse is not None and self.sparse.n_tiles:
+            sub.sparse = self.sparse.select_rows(r_lo, r_hi)
+        return sub
 
     def shard(self, unit_lo: int, unit_hi: int) -> "HalfTiles":
         """View of the tiles of units [unit_lo, unit_hi) (same n; GPU panel)."""

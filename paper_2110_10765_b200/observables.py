@@ -20,16 +20,32 @@ cross-check.
 :384-425; reduce.py:62) so reference callers switch by changing an import.
 The strategy names are accepted for compatibility; on the GPU the merge
 discipline is the kernel's (register/shared-memory reduction + red.global).
+
+Two entry points:
+
+* ``contract_observables(tiles, orbitals, basis, rank, inputs, strategy,
+  workers, transpose)`` and ``contract_oracle(tiles, orbitals, basis, rank,
+  inputs)`` — the reference's exact signatures (pipeline.py:534-589): the
+  pair set is the reference's own (each orbital Tile re-walked with the
+  count predicate, _collect_pairs :428-458), evaluated on the device by
+  ``cim_contract_tiles`` — a reference caller switches by changing the
+  import.  ``Orbital``, ``Tile``, ``InteractionRank``, ``group_orbitals`` and
+  ``enumerate_tiles`` mirror the reference types and host helpers that build
+  those arguments (pipeline.py:68-192, sparsity.py:49-60).
+* ``contract_pattern(pattern, inputs, ...)`` — the same contraction over a
+  stored ``HalfTiles`` pattern (``cim_contract_observables``), the fast path
+  when the pattern is already on the device.
 """
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
 import torch
 
-from ._lib import check, lib
+from ._lib import CIM_ACCUMULATE, CIM_CONTRACT_EXACT_F64, check, lib
 from .halftiles import LAYOUTS, HalfTiles, _dtype_code
 from .spmm import sym_spmm
 
@@ -103,8 +119,8 @@ def operator_tiles(pattern: HalfTiles, op_kind: str, k: int, seed: int) -> HalfT
                      meta=dict(pattern.meta, op_kind=op_kind, op_k=k, op_seed=seed), sparse=sparse)
 
 
-def contract_observables(pattern: HalfTiles, inputs: ObservablesInput, strategy: str = "array_clause",
-                         workers: int | None = None, transpose: bool = False) -> np.ndarray:
+def contract_pattern(pattern: HalfTiles, inputs: ObservablesInput, strategy: str = "array_clause",
+                     workers: int | None = None, transpose: bool = False) -> np.ndarray:
     """accum[v,k] = Σ over stored pairs (i,j) of c[v,i]·O[i,j,k]·c[v,j].
 
     Fills ``inputs.accum`` in place and returns its (n_vec, m_ops) view, as
@@ -115,7 +131,8 @@ def contract_observables(pattern: HalfTiles, inputs: ObservablesInput, strategy:
     if strategy not in STRATEGIES:
         raise ValueError(f"unknown strategy {strategy!r}, expected one of {STRATEGIES}")
     if not isinstance(pattern, HalfTiles):
-        raise ValueError("pattern must be a HalfTiles (e.g. HalfTiles.from_skeleton(...))")
+        raise ValueError("pattern must be a HalfTiles (e.g. HalfTiles.from_skeleton(...)); reference-style "
+                         "(tiles, orbitals, basis, rank, inputs) arguments go to contract_observables")
     if inputs.c.shape[1] != pattern.n:
         raise ValueError(f"coefficients cover {inputs.c.shape[1]} states, basis has {pattern.n}")
     dev = pattern.device
@@ -143,3 +160,190 @@ def contract_materialized(pattern: HalfTiles, inputs: ObservablesInput) -> np.nd
         Y = sym_spmm(O, X)
         out[:, k] = (X.to(torch.float64) * Y.to(torch.float64)).sum(dim=0)
     return out.cpu().numpy()
+
+
+# ----------------------------------------------------------------------------
+# The reference's own signature: orbital tiles + basis + rank (pipeline.py)
+# ----------------------------------------------------------------------------
+
+MAX_WORKERS_ENV = "CIMOTIFS_MAX_WORKERS"  # _util.py:22
+
+
+@dataclass(frozen=True)
+class Orbital:
+    """A contiguous run [start, stop) of basis states sharing a grouping key
+    (pipeline.py:68-83)."""
+
+    id: int
+    key: object
+    start: int
+    stop: int
+
+    def __post_init__(self):
+        if self.stop <= self.start:
+            raise ValueError(f"orbital {self.id} is empty: [{self.start}, {self.stop})")
+
+    @property
+    def size(self) -> int:
+        return self.stop - self.start
+
+
+@dataclass
+class Tile:
+    """A row-orbital/col-orbital pair that may hold interacting state pairs
+    (pipeline.py:86-93)."""
+
+    row_orbital: int
+    col_orbital: int
+    cnt: int = 0
+    offset: int = 0
+
+
+@dataclass(frozen=True)
+class InteractionRank:
+    """Particle rank d of the operator; pairs connect iff they differ in ≤ 2d
+    (sparsity.py:49-60)."""
+
+    d: int = 2
+
+    def __post_init__(self):
+        if self.d < 1:
+            raise ValueError(f"rank must be >= 1, got d={self.d}")
+
+    @property
+    def threshold(self) -> int:
+        return 2 * self.d
+
+
+@dataclass(frozen=True)
+class BasisArrays:
+    """The kernel-side views of a reference ``Basis`` (mbstate.py:140-190):
+    ``occ_mat`` (n, N) uint16 and ``bits_lo`` (n,) uint64 — what the device
+    predicate reads.  Anything with those two attributes and ``len()`` (the
+    reference ``Basis`` itself) is accepted where a basis is expected."""
+
+    occ_mat: np.ndarray
+    bits_lo: np.ndarray
+    n_sp: int = 0
+
+    def __len__(self) -> int:
+        return int(self.occ_mat.shape[0])
+
+
+def group_orbitals(basis, group_bits: int = 16):
+    """The reference's default grouping (group_orbitals with
+    bitrep_prefix_key, pipeline.py:123-159) on the basis arrays: states
+    reordered so equal keys ``bits_lo & (2^group_bits − 1)`` are contiguous
+    (ascending keys, input order inside a group).  Returns
+    (BasisArrays in grouped order, [Orbital])."""
+    from .construct import group_basis
+
+    occ = np.ascontiguousarray(basis.occ_mat, dtype=np.uint16)
+    lo = np.ascontiguousarray(basis.bits_lo, dtype=np.uint64)
+    g_occ, g_lo, _, starts = group_basis(occ, lo, group_bits)
+    mask = (1 << group_bits) - 1
+    stops = np.append(starts[1:], g_occ.shape[0])
+    orbs = [Orbital(id=q, key=int(g_lo[a]) & mask, start=int(a), stop=int(b))
+            for q, (a, b) in enumerate(zip(starts, stops))]
+    return BasisArrays(g_occ, g_lo, int(getattr(basis, "n_sp", 0))), orbs
+
+
+def enumerate_tiles(row_orbs, col_orbs, rank: InteractionRank = InteractionRank()) -> list:
+    """Orbital pairs passing the coarse ≤ 2d key test, row-major
+    (enumerate_tiles / _orbital_pair_passes, pipeline.py:162-192): integer
+    keys pass iff popcount(key_r ^ key_c) ≤ threshold; other keys always pass."""
+    thr = rank.threshold
+    out = []
+    int_c = [isinstance(c.key, int) for c in col_orbs]
+    for r in row_orbs:
+        for c, ci in zip(col_orbs, int_c):
+            if not (ci and isinstance(r.key, int)) or (r.key ^ c.key).bit_count() <= thr:
+                out.append(Tile(row_orbital=r.id, col_orbital=c.id))
+    return out
+
+
+def _check_workers(workers) -> None:
+    """The reference's worker validation (resolve_workers / env_worker_cap,
+    _util.py:27-48).  On the GPU the grid is sized by the SM count; the value
+    is validated and otherwise unused."""
+    raw = os.environ.get(MAX_WORKERS_ENV)
+    if raw is not None and raw.strip() and int(raw) < 1:
+        raise ValueError(f"{MAX_WORKERS_ENV} must be >= 1, got {raw!r}")
+    if workers is not None and workers < 1:
+        raise ValueError(f"workers must be >= 1, got {workers}")
+
+
+def _tile_ranges(tiles, orbitals, transpose: bool) -> np.ndarray:
+    """(T, 4) int32 (r0, r1, c0, c1) of each tile's orbitals, swapped for the
+    transposed walk (pipeline.py:437-447)."""
+    orb_by_id = {o.id: (o.start, o.stop) for o in orbitals}
+    rows = np.empty((len(tiles), 4), dtype=np.int64)
+    for q, t in enumerate(tiles):
+        r = orb_by_id[t.row_orbital]
+        c = orb_by_id[t.col_orbital]
+        if transpose:
+            r, c = c, r
+        rows[q] = (r[0], r[1], c[0], c[1])
+    return rows
+
+
+def _contract_tiles(tiles, orbitals, basis, rank, inputs: ObservablesInput, transpose: bool, exact: bool,
+                    device=None) -> np.ndarray:
+    n = len(basis)
+    occ = np.ascontiguousarray(basis.occ_mat, dtype=np.uint16)
+    lo = np.ascontiguousarray(basis.bits_lo, dtype=np.uint64)
+    if occ.ndim != 2 or occ.shape[0] != n or lo.shape != (n,):
+        raise ValueError(f"basis arrays must be occ_mat (n, N) and bits_lo (n,), got {occ.shape} and {lo.shape}")
+    rng = _tile_ranges(tiles, orbitals, transpose)
+    if rng.size and (rng[:, [0, 2]].min() < 0 or rng[:, [1, 3]].max() > n
+                     or np.any(rng[:, 1] <= rng[:, 0]) or np.any(rng[:, 3] <= rng[:, 2])):
+        raise ValueError(f"orbital ranges must lie in [0, {n}) and be non-empty")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    T = rng.shape[0]
+    d_rng = torch.from_numpy(rng.astype(np.int32)).to(dev)
+    d_lo = torch.from_numpy(lo.view(np.int64)).to(dev)
+    d_occ = torch.from_numpy(occ.view(np.int16)).to(dev)
+    c = torch.from_numpy(inputs.c).to(dev).t().contiguous()  # (n, n_vec) f32
+    out = torch.empty((inputs.n_vec, inputs.m_ops), dtype=torch.float64, device=dev)
+    code = _OP_CODES[inputs.op_kind]
+    flags = CIM_CONTRACT_EXACT_F64 if exact else 0
+    with torch.cuda.device(dev):
+        check(lib().cim_contract_tiles(d_lo.data_ptr(), d_occ.data_ptr(), n, occ.shape[1], int(rank.threshold),
+                                       d_rng.data_ptr() if T else None, T, c.data_ptr(), inputs.n_vec,
+                                       inputs.n_vec, inputs.m_ops, code, inputs.seed, out.data_ptr(), flags,
+                                       torch.cuda.current_stream(dev).cuda_stream), "cim_contract_tiles")
+    return out.cpu().numpy()
+
+
+def contract_observables(tiles, orbitals, basis, rank, inputs: ObservablesInput, strategy: str = "array_clause",
+                         workers: int | None = None, transpose: bool = False) -> np.ndarray:
+    """accum[v,k] = Σ over interacting pairs (i,j) of c[v,i]·O[i,j,k]·c[v,j]
+    — the reference operator with its exact signature and checks
+    (pipeline.py:534-570).
+
+    Walks ``tiles`` (orbital pairs; ``transpose`` walks each as (col, row))
+    with the count predicate of ``rank`` over ``basis`` (grouped order) on the
+    device (``cim_contract_tiles``): the reference's f32 products, summed in
+    f32 per lane and f64 across lanes.  Raises ``ValueError`` for an unknown
+    strategy, a coefficient/basis size mismatch and a bad worker count, in the
+    reference's order.  ``strategy`` names the reference's CPU merge
+    discipline (validated; the device reduction is the kernel's).  Fills
+    ``inputs.accum`` in place and returns its (n_vec, m_ops) view.
+    """
+    if strategy not in STRATEGIES:
+        raise ValueError(f"unknown strategy {strategy!r}, expected one of {STRATEGIES}")
+    if inputs.c.shape[1] != len(basis):
+        raise ValueError(f"coefficients cover {inputs.c.shape[1]} states, basis has {len(basis)}")
+    _check_workers(workers)
+    a = _contract_tiles(tiles, orbitals, basis, rank, inputs, transpose, exact=False)
+    inputs.accum[:] = a.astype(np.float32).reshape(-1)
+    return inputs.accum.reshape(inputs.n_vec, inputs.m_ops)
+
+
+def contract_oracle(tiles, orbitals, basis, rank, inputs: ObservablesInput) -> np.ndarray:
+    """Double-precision contraction over the same pair set
+    (pipeline.py:573-589): f64 products and sums on the device
+    (``CIM_CONTRACT_EXACT_F64``).  Returns a fresh (n_vec, m_ops) f64 array."""
+    if inputs.c.shape[1] != len(basis):
+        raise ValueError(f"coefficients cover {inputs.c.shape[1]} states, basis has {len(basis)}")
+    return _contract_tiles(tiles, orbitals, basis, rank, inputs, False, exact=True)

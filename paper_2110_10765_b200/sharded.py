@@ -1,32 +1,44 @@
 """Row-block sharding of the half-stored SpMM over the GPUs of one box.
 
 SURVEY.md §8(e): GPU g owns a contiguous run of block rows chosen so the
-stored-tile counts are balanced (upper-triangular storage puts ~p·(nb−R)
-tiles in block row R, so equal row counts would be badly unbalanced).  The
-vectors are distributed separately, in equal 64-aligned row chunks, so the
-two exchange steps are plain fixed-size NCCL collectives over NVLink:
+streamed tile bytes are balanced (upper-triangular storage puts ~p·(nb−R)
+tiles in block row R, so equal row counts would be badly unbalanced; sparse
+tiles weigh their entries).  The vectors are distributed separately, in
+equal 64-aligned row chunks, so the two exchange steps are plain fixed-size
+NCCL collectives over NVLink:
 
     X_full  = all_gather(X_local)                  (every rank needs any X_C)
-    Y_part  = U_g·X_full + U_g,offᵀ·X_full          (local sm_100a kernel)
+    Y_part  = U_g·X_full + U_g,offᵀ·X_full          (local sm_100a kernels)
     Y_local = reduce_scatter(Y_part, SUM)           (Hᵀ·X lands on other ranks)
 
-One process per GPU, ``torch.distributed`` with the NCCL backend.  The
+``overlap=True`` hides both exchanges behind the kernels (§8(e)4):
+
+* the panel's tiles whose R and C blocks both lie in this rank's own X chunk
+  run first, straight from ``X_local``, while the all-gather is in flight;
+* the rest run in column groups, C's chunk descending (G−1, …, 0).  Y chunk q
+  receives direct products only from tiles with R in q (their C ≥ R, so
+  chunk(C) ≥ q) and transposed products only from tiles with C in q, so it
+  is final once group q has run: its reduction to rank q (``dist.reduce``,
+  async on NCCL's stream) overlaps the groups after it, and only chunk 0's
+  reduction is exposed.
+
+One process per GPU, ``torch.distributed`` with the NCCL backend (under gloo
+— CPU test harnesses — CUDA buffers are staged through host memory).  The
 reference has no distribution at all; its only parallelism is
 numba's thread pool (_util.py:37-62).
 """
 
 from __future__ import annotations
 
+import ctypes
 from typing import Callable
 
 import numpy as np
 import torch
 import torch.distributed as dist
 
-import ctypes
-
-from ._lib import BLOCK, check, lib
-from .halftiles import HalfTiles, partition_units, plan_units, synthetic_pattern
+from ._lib import BLOCK, CIM_ACCUMULATE, check, lib
+from .halftiles import DEFAULT_MAX_UNIT, HalfTiles, partition_units, plan_units, synthetic_pattern
 from .spmm import _launch, padded_k
 
 
@@ -65,6 +77,51 @@ def sym_spmm_chunked(H: HalfTiles, X_chunks, Y_chunks, chunk_rows: int, k: int |
         check(lib().cim_sym_spmm_chunked(H.descriptor(), xp, yp, n, chunk_rows, k, k, handle), "cim_sym_spmm_chunked")
 
 
+def column_groups(H: HalfTiles, rows_per_rank: int, world: int, rank: int, max_unit: int = DEFAULT_MAX_UNIT):
+    """Split a panel's tiles into the overlap schedule's groups.
+
+    Returns ``(local, groups)``: ``local`` holds the tiles whose R and C
+    blocks both lie in this rank's X chunk; ``groups[q]`` the remaining tiles
+    whose C block lies in chunk q.  Each is a ``HalfTiles`` view sharing the
+    panel's arrays — dense tiles through their own work units (a row's tiles
+    are C-sorted, so every group is a contiguous run of each row's tiles),
+    sparse tiles through restricted kernel work lists."""
+    bpr = rows_per_rank // BLOCK  # blocks per chunk
+    rc = H.tile_rc_host
+    chunk_r, chunk_c = rc[:, 0] // bpr, rc[:, 1] // bpr
+    gid = np.where((chunk_r == rank) & (chunk_c == rank), -1, chunk_c)
+    units = []
+    for u in H.units_host:
+        R, t0, t1 = int(u[0]), int(u[1]), int(u[2])
+        g = gid[t0:t1]
+        cuts = np.flatnonzero(np.diff(g)) + 1
+        for a, b in zip(np.concatenate([[0], cuts]), np.concatenate([cuts, [t1 - t0]])):
+            units.append((int(g[a]), R, t0 + int(a), t0 + int(b)))
+    U = np.array(units, dtype=np.int64).reshape(-1, 4)
+    sp = H.sparse if (H.sparse is not None and H.sparse.n_tiles) else None
+    if sp is not None:
+        src = sp.tile_rc_host
+        s_gid = np.where((src[:, 0] // bpr == rank) & (src[:, 1] // bpr == rank), -1, src[:, 1] // bpr)
+        st, sm = (t.cpu().numpy() for t in sp.work_split())
+
+    def view(g: int) -> HalfTiles | None:
+        u = U[U[:, 0] == g][:, 1:]
+        units = np.zeros((u.shape[0], 4), dtype=np.int32)
+        units[:, :3] = u
+        sub = HalfTiles(n=H.n, tile_rc=H.tile_rc, units=torch.from_numpy(units if units.size else np.zeros((1, 4), np.int32)).to(H.device),
+                        vals=H.vals, tile_rc_host=H.tile_rc_host, units_host=units, layout=H.layout,
+                        meta=dict(H.meta, group=g))
+        empty = units.shape[0] == 0
+        if sp is not None:
+            sst, ssm = st[s_gid[st] == g], sm[s_gid[sm] == g]
+            if sst.size or ssm.size:
+                sub.sparse = sp.with_lists(sst, ssm)
+                empty = False
+        return None if empty else sub
+
+    return view(-1), [view(q) for q in range(world)]
+
+
 class ShardedSymSpmm:
     """Distributed ``Y = A·X`` with A's tiles row-block sharded over ranks.
 
@@ -75,7 +132,7 @@ class ShardedSymSpmm:
     """
 
     def __init__(self, n: int, k: int, dtype: torch.dtype, device, H_local: HalfTiles | None = None,
-                 group=None, local_apply: Callable | None = None, fused: bool = False):
+                 group=None, local_apply: Callable | None = None, fused: bool = False, overlap: bool = False):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -101,7 +158,15 @@ class ShardedSymSpmm:
         self.n_pad = ((self.n + BLOCK - 1) // BLOCK) * BLOCK
         self.fused = bool(fused) and self.world > 1 and local_apply == self._cuda_apply
         if self.fused:
+            if H_local.n_sparse_tiles:
+                raise ValueError("the fused peer-memory apply streams dense tiles only; use the NCCL exchange "
+                                 "(fused=False) for matrices with sparse tiles")
             self._setup_fused()
+        self.overlap = bool(overlap) and self.world > 1 and local_apply == self._cuda_apply and not self.fused
+        if self.overlap:
+            self.g_local, self.g_cols = column_groups(H_local, self.rows_per_rank, self.world, self.rank)
+        self._staged = (self.world > 1 and self.device.type == "cuda"
+                        and dist.get_backend(group) == dist.Backend.GLOO)
 
     # ------------------------------------------------------------ fused path
     def _setup_fused(self) -> None:
@@ -134,7 +199,7 @@ class ShardedSymSpmm:
     def synthetic(cls, n: int, *, k: int, p: float | None = None, n_off: int | None = None, seed: int = 0,
                   value_seed: int = 0, dtype=torch.float32, device=None, group=None, max_unit: int = 32,
                   values: str = "h_xor", layout: str | None = None, bands: int | None = 1,
-                  fused: bool = False) -> "ShardedSymSpmm":
+                  fused: bool = False, overlap: bool = False) -> "ShardedSymSpmm":
         """Every rank draws the same global tile pattern (seeded), keeps its
         balanced panel, and generates only its own tile values on its GPU."""
         world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -151,11 +216,62 @@ class ShardedSymSpmm:
                                 device=device, max_unit=max_unit, layout=layout, bands=bands)
         H.meta.update(global_tiles=int(rc.shape[0]), global_off_tiles=int(np.count_nonzero(rc[:, 0] != rc[:, 1])),
                       p=p, seed=seed)
-        return cls(n, k, dtype, device, H_local=H, group=group, fused=fused)
+        return cls(n, k, dtype, device, H_local=H, group=group, fused=fused, overlap=overlap)
+
+    @classmethod
+    def from_halftiles(cls, H: HalfTiles, *, k: int, group=None, fused: bool = False,
+                       overlap: bool = False) -> "ShardedSymSpmm":
+        """Shard a matrix every rank holds (e.g. built by ``from_basis`` /
+        ``from_coo``, dense and sparse tiles): rows are split into panels of
+        balanced streamed bytes (``HalfTiles.partition_rows``) and this rank
+        keeps its panel (``shard_rows``; views, no copies of dense tiles)."""
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        b = H.partition_rows(world)
+        sub = H.shard_rows(int(b[rank]), int(b[rank + 1]))
+        return cls(H.n, k, H.dtype, H.device, H_local=sub, group=group, fused=fused, overlap=overlap)
+
+    def local_tiles(self) -> int:
+        """Stored tiles (dense + sparse) in this rank's panel."""
+        return self.H.n_tiles + self.H.n_sparse_tiles if self.H is not None else 0
+
+    # ------------------------------------------------------------ exchanges
+    def _all_gather(self, out: torch.Tensor, inp: torch.Tensor, async_op: bool = False):
+        if self._staged:  # gloo moves host tensors: stage the CUDA buffers
+            o = out.cpu()
+            dist.all_gather_into_tensor(o, inp.cpu(), group=self.group)
+            out.copy_(o)
+            return None
+        return dist.all_gather_into_tensor(out, inp, group=self.group, async_op=async_op)
+
+    def _reduce_scatter(self, out: torch.Tensor, inp: torch.Tensor) -> None:
+        if self._staged:
+            o = out.cpu()
+            dist.reduce_scatter_tensor(o, inp.cpu(), op=dist.ReduceOp.SUM, group=self.group)
+            out.copy_(o)
+            return
+        dist.reduce_scatter_tensor(out, inp, op=dist.ReduceOp.SUM, group=self.group)
+
+    def _reduce(self, t: torch.Tensor, dst: int, async_op: bool):
+        gdst = dist.get_global_rank(self.group, dst) if self.group is not None else dst
+        if self._staged:
+            h = t.cpu()
+            dist.reduce(h, gdst, op=dist.ReduceOp.SUM, group=self.group)
+            if self.rank == dst:
+                t.copy_(h)
+            return None
+        return dist.reduce(t, gdst, op=dist.ReduceOp.SUM, group=self.group, async_op=async_op)
 
     # ------------------------------------------------------------------ apply
     def _cuda_apply(self, X_full: torch.Tensor, Y_part: torch.Tensor) -> None:
         _launch(self.H, X_full[: self.n_pad], Y_part[: self.n_pad], False, None)
+
+    def _launch_ptr(self, H: HalfTiles, x_ptr: int, y: torch.Tensor) -> None:
+        """Accumulating apply of a schedule group with X given by its base
+        address (global row r at x_ptr + r·k·s)."""
+        with torch.cuda.device(self.device):
+            check(lib().cim_sym_spmm(H.descriptor(), x_ptr, y.data_ptr(), self.k, self.k, self.k, CIM_ACCUMULATE,
+                                     torch.cuda.current_stream(self.device).cuda_stream), "cim_sym_spmm(group)")
 
     def local_rows(self) -> tuple[int, int]:
         """Global row range [lo, hi) of this rank's X/Y chunk (clipped to n)."""
@@ -171,38 +287,62 @@ class ShardedSymSpmm:
             if out.shape != (self.rows_per_rank, self.k_user) or out.dtype != self.dtype or out.device != self.device:
                 raise ValueError("out must be a (rows_per_rank, k_user) tensor of the operator's dtype and device")
             direct = out.is_contiguous() and self.k == self.k_user and out.data_ptr() % 16 == 0
-            if direct and not self.fused:
+            if direct and not self.fused and not self.overlap:
                 return self._apply_into(X_local, out)
             out.copy_(self.apply(X_local))
             return out
         return self._apply_into(X_local, None)
+
+    def _apply_overlapped(self, xl: torch.Tensor) -> torch.Tensor:
+        s = self.X_full.element_size()
+        lo = self.rank * self.rows_per_rank
+        self.Y_part.zero_()
+        work = self._all_gather(self.X_full, xl, async_op=True)
+        if self.g_local is not None:  # own-chunk tiles from X_local while the gather is in flight
+            self._launch_ptr(self.g_local, xl.data_ptr() - lo * self.k * s, self.Y_part)
+        if work is not None:
+            work.wait()
+        pending = []
+        for q in range(self.world - 1, -1, -1):
+            g = self.g_cols[q]
+            if g is not None:
+                self._launch_ptr(g, self.X_full.data_ptr(), self.Y_part)
+            sl = self.Y_part[q * self.rows_per_rank:(q + 1) * self.rows_per_rank]
+            w = self._reduce(sl, q, async_op=True)  # chunk q is final: reduce it to its owner
+            if w is not None:
+                pending.append(w)
+        for w in pending:
+            w.wait()
+        return self.Y_part[lo:lo + self.rows_per_rank, : self.k_user]
 
     def _apply_into(self, X_local: torch.Tensor, out: torch.Tensor | None) -> torch.Tensor:
         if X_local.shape[0] != self.rows_per_rank:
             raise ValueError(f"X_local must have {self.rows_per_rank} rows, got {X_local.shape[0]}")
         if X_local.shape[1] != self.k_user:
             raise ValueError(f"X_local must have {self.k_user} columns, got {X_local.shape[1]}")
-        if self.k != self.k_user:
+        if self.k != self.k_user or not X_local.is_contiguous() or X_local.data_ptr() % 16:
             xl = torch.zeros((self.rows_per_rank, self.k), dtype=self.dtype, device=self.device)
             xl[:, : self.k_user] = X_local
         else:
-            xl = X_local.contiguous()
+            xl = X_local
         if self.fused:
             return self._apply_fused(xl)
-        if self.world == 1 and self.local_apply == self._cuda_apply and xl.data_ptr() % 16 == 0:
+        if self.overlap:
+            return self._apply_overlapped(xl)
+        if self.world == 1 and self.local_apply == self._cuda_apply:
             # one rank: the kernel reads X_local and writes Y_local directly
             # (rows_per_rank = n_pad), no staging copies
             Y = self.Y_local if out is None else out
             self._cuda_apply(xl, Y)
             return Y[:, : self.k_user]
         if self.world > 1:
-            dist.all_gather_into_tensor(self.X_full, xl, group=self.group)
+            self._all_gather(self.X_full, xl)
         else:
             self.X_full.copy_(xl)
         self.local_apply(self.X_full, self.Y_part)
         Y = self.Y_local if out is None else out
         if self.world > 1:
-            dist.reduce_scatter_tensor(Y, self.Y_part, op=dist.ReduceOp.SUM, group=self.group)
+            self._reduce_scatter(Y, self.Y_part)
         else:
             Y.copy_(self.Y_part)
         return Y[:, : self.k_user]

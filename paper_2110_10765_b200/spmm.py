@@ -87,13 +87,21 @@ def sym_spmm(H: HalfTiles, X, out=None, *, layout: str = "auto", accumulate: boo
     out : optional tensor/array of X's shape to write into (``accumulate``
         adds to it instead of overwriting)
     layout : "auto" | "nk" | "kn"
-    stream : torch.cuda.Stream or raw cudaStream_t handle (default: current)
+    stream : torch.cuda.Stream or raw cudaStream_t handle (default: current);
+        staging, the kernel and the copy-back all run on it
     deterministic : no float atomics — bitwise reproducible Y (CIM_DETERMINISTIC;
         fragment-layout dense and sparse tiles; a validation mode, ~2× the
         traffic)
     """
     if not isinstance(H, HalfTiles):
         raise ValueError(f"H must be a HalfTiles, got {type(H).__name__}")
+    if stream is not None:
+        # stage X, launch and read back Y all on the caller's stream, so the
+        # padding copy, the kernel and the copy-back are ordered (ADVICE r1)
+        s = stream if isinstance(stream, torch.cuda.Stream) else torch.cuda.ExternalStream(int(stream), device=H.device)
+        with torch.cuda.stream(s):
+            return sym_spmm(H, X, out, layout=layout, accumulate=accumulate, stream=None,
+                            deterministic=deterministic)
     if layout not in LAYOUTS:
         raise ValueError(f"unknown layout {layout!r}, expected one of {LAYOUTS}")
     is_numpy = isinstance(X, np.ndarray)
@@ -138,7 +146,9 @@ def sym_spmm(H: HalfTiles, X, out=None, *, layout: str = "auto", accumulate: boo
         Xd = Xp
     # output buffer on device, (n_pad, kk) row-major
     out_is_dev_nk = (isinstance(out, torch.Tensor) and out.device == dev and layout == "nk" and direct
-                     and out.is_contiguous())
+                     and out.is_contiguous() and out.data_ptr() % 16 == 0)
+    if isinstance(out, torch.Tensor) and out.device == dev and _overlaps(out, Xd):
+        raise ValueError("out must not overlap X (Y is zeroed before X is read)")
     if out_is_dev_nk:
         Yd = out
     else:
@@ -164,6 +174,17 @@ def sym_spmm(H: HalfTiles, X, out=None, *, layout: str = "auto", accumulate: boo
     if is_numpy:
         return Y.cpu().numpy()
     return Y.contiguous() if layout == "kn" else (Y if direct else Y.contiguous())
+
+
+def _overlaps(a: torch.Tensor, b: torch.Tensor) -> bool:
+    """Do the byte ranges of two device tensors intersect?"""
+    if a.numel() == 0 or b.numel() == 0:
+        return False
+    a0 = a.data_ptr()
+    a1 = a0 + (sum((s - 1) * st for s, st in zip(a.shape, a.stride())) + 1) * a.element_size()
+    b0 = b.data_ptr()
+    b1 = b0 + (sum((s - 1) * st for s, st in zip(b.shape, b.stride())) + 1) * b.element_size()
+    return a0 < b1 and b0 < a1
 
 
 def _host_array(A, name: str, n: int, k: int, dtype: torch.dtype) -> torch.Tensor:
@@ -220,6 +241,9 @@ def sym_spmm_host_batch(H: HalfTiles, Xs, out=None):
     nb = len(xt)
     xp = (ctypes.c_void_p * nb)(*[t.data_ptr() for t in xt])
     yp = (ctypes.c_void_p * nb)(*[t.data_ptr() for t in yt])
+    # the library's streams must not overtake work queued on ours (e.g. the
+    # tile-value fill of a matrix built just before this call)
+    torch.cuda.current_stream(H.device).synchronize()
     with torch.cuda.device(H.device):
         rc = L.cim_sym_spmm_host_batch(desc, xp, yp, nb, k, ws.data_ptr(), need)
     check(rc, "cim_sym_spmm_host_batch")

@@ -27,6 +27,18 @@ against the reference's own build_skeleton output, and basis_<name>.txt is
 the same basis in sampled order written by the reference's save_basis
 (mbstate.py:242-246; `--basis-files` regenerates only these).
 
+* contraction_cases.npz — the bases of the reference's TestContraction
+                        problems (test_pipeline.py:244-305: small_problem
+                        n=64 / n=128 and the n=256 identity basis) as
+                        random_basis produced them (ungrouped occupation
+                        lists and words), the reference's grouping and tile
+                        list for each, and the reference's own outputs of
+                        contract_observables (every strategy, forward and
+                        transposed) and contract_oracle on the tests' inputs,
+                        so the test bodies rerun against the GPU package with
+                        only the import swapped (`--contraction` regenerates
+                        only this file).
+
 The GPU box never reads /root/reference: tests load only these files.
 """
 
@@ -160,12 +172,50 @@ def basis_files():
     print("basis files:", sorted(meta))
 
 
+def contraction_cases():
+    """The reference TestContraction problems and outputs (test_pipeline.py:39-44, :244-305)."""
+    out = {}
+
+    def put(name, basis, group_bits):
+        grouped, orbs = group_orbitals(basis, group_bits=group_bits)
+        rank = InteractionRank()
+        tiles = enumerate_tiles(orbs, orbs, rank)
+        out[f"{name}_occ"] = basis.occ_mat.astype(np.uint16)
+        out[f"{name}_bits_lo"] = basis.bits_lo.astype(np.uint64)
+        out[f"{name}_n_sp"] = basis.n_sp
+        out[f"{name}_group_bits"] = group_bits
+        out[f"{name}_grouped_occ"] = grouped.occ_mat.astype(np.uint16)
+        out[f"{name}_orb"] = np.array([(o.id, o.start, o.stop, o.key) for o in orbs], np.int64)
+        out[f"{name}_tiles"] = np.array([(t.row_orbital, t.col_orbital) for t in tiles], np.int64)
+        out[f"{name}_n_pairs"] = count_pairs(grouped, grouped, rank).total
+        return grouped, orbs, tiles, rank
+
+    put("p64", random_basis(64, 6, bias=0.2, seed=13), 8)
+    g, o, t, r = put("p128", random_basis(128, 6, bias=0.2, seed=13), 8)
+    put("p256", random_basis(256, 8, bias=0.1, seed=17), 8)
+    # test_strategies_match_oracle inputs and the reference's outputs
+    c = random_coefficients(4, 128, seed=2)
+    for strat in ("array_clause", "atomic_per_element", "generated_scalars"):
+        out[f"strat_{strat}"] = contract_observables(t, o, g, r, ObservablesInput(c=c, m_ops=3, seed=4), strat).copy()
+    out["strat_oracle"] = contract_oracle(t, o, g, r, ObservablesInput(c=c, m_ops=3, seed=4))
+    # test_hermitian_symmetry
+    c3 = random_coefficients(4, 128, seed=3)
+    out["herm_fwd"] = contract_observables(t, o, g, r, ObservablesInput(c=c3, m_ops=2, seed=6)).copy()
+    out["herm_rev"] = contract_observables(t, o, g, r, ObservablesInput(c=c3, m_ops=2, seed=6), transpose=True).copy()
+    np.savez_compressed(OUT / "contraction_cases.npz", **out)
+    print("contraction_cases.npz:", {k: v.shape for k, v in out.items() if hasattr(v, "shape")})
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["--contraction"]:
+        contraction_cases()
+        sys.exit(0)
     if sys.argv[1:] == ["--basis-files"]:
         basis_files()
         sys.exit(0)
     hash_kat()
     basis_files()
+    contraction_cases()
     skeleton_fixture("skel_small.npz", n=192, particles=6, bias=0.2, group_bits=8, seed=13,
                      n_vec=4, m_ops=3, op_kind="symmetric_hash", coeff_kind="gauss",
                      coeff_seed=2, op_seed=4)

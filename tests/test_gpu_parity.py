@@ -131,11 +131,11 @@ def test_contract_observables_matches_reference(pkg, name, layout):
     pattern = pkg.HalfTiles.from_coo(n, f["i"], f["j"], np.ones_like(f["v"]), layout=layout)
     c = f["X"].T.copy()
     inp = pkg.ObservablesInput(c=c, m_ops=int(f["m_ops"]), op_kind=str(f["op_kind"]), seed=int(f["op_seed"]))
-    got = pkg.contract_observables(pattern, inp).astype(np.float64)
+    got = pkg.contract_pattern(pattern, inp).astype(np.float64)
     tol = oracle.contraction_tolerance(c, int(f["nnz"]))
     assert np.abs(got - f["accum_oracle"]).max() <= tol
     assert np.abs(got - f["accum"]).max() <= tol
-    got_t = pkg.contract_observables(pattern, pkg.ObservablesInput(c=c, m_ops=int(f["m_ops"]),
+    got_t = pkg.contract_pattern(pattern, pkg.ObservablesInput(c=c, m_ops=int(f["m_ops"]),
                                                                   op_kind=str(f["op_kind"]), seed=int(f["op_seed"])),
                                      transpose=True)
     assert np.abs(got_t - got).max() <= tol
@@ -179,7 +179,7 @@ def test_contract_fused_vs_oracle(pkg, dtype, layout, n_vec, m_ops, op_kind):
     c = pkg.random_coefficients(n_vec, n, seed=n_vec, kind="gauss")
     seed = 11
     inp = pkg.ObservablesInput(c=c, m_ops=m_ops, op_kind=op_kind, seed=seed)
-    got = pkg.contract_observables(pattern, inp).astype(np.float64)
+    got = pkg.contract_pattern(pattern, inp).astype(np.float64)
     code = {"symmetric_hash": 1, "identity": 2}[op_kind]  # C ABI (CIM_VALUES_*)
     want = oracle.contract_vmv(c, I, J, m_ops, {"symmetric_hash": 1, "identity": 0}[op_kind], seed)
     tol = oracle.contraction_tolerance(c, I.size)

@@ -1,0 +1,352 @@
+"""Round-2 GPU parity: the configs and entry points round 1 left unchecked.
+
+* ``HalfTiles.from_skeleton`` on skeleton objects rebuilt from the reference
+  fixtures (tiles, orbitals, per-(tile,row) segments, colind, values —
+  pipeline.py:96-116, :319-330);
+* the device scan (``cim_exclusive_scan_i64``, ``cim_sparse_tile_offsets``)
+  against ``scan_serial`` (scan.py:131-139);
+* subnormal-range partial sums: ``red.global.add.f32`` flushes them (PTX
+  defines f32 float atomics as flush-to-zero), the deterministic mode does not;
+* ``ShardedSymSpmm`` with its default CUDA panel kernel in two ranks that
+  share the one GPU (gloo, host-staged exchange), dense and sparse panels;
+* BASELINE C2 and C3 at full size on 256 random block rows each against the
+  hash oracle (direct and transposed contributions, normwise and
+  componentwise), plus the forward/transposed symmetry pin
+  ⟨X₁, A X₂⟩ = ⟨A X₁, X₂⟩ (test_pipeline.py:278-286).
+"""
+
+import os
+import socket
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+import torch
+
+from golden_util import load_fixture
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+U32 = 2.0 ** -24
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2110_10765_b200 as p
+
+    p.lib()
+    return p
+
+
+# ----------------------------------------------------------------------------
+# from_skeleton on reference skeleton objects
+# ----------------------------------------------------------------------------
+
+def skeleton_objects(f):
+    """SparseSkeleton / Orbital / Tile stand-ins with the reference's fields,
+    rebuilt from a golden fixture written by the reference's build_skeleton."""
+    from paper_2110_10765_b200 import Orbital, Tile
+
+    orbs = [Orbital(id=int(a), key=None, start=int(b), stop=int(c)) for a, b, c in f["orb"]]
+    tiles = tuple(Tile(int(r), int(c), int(cnt), int(off)) for r, c, cnt, off in f["tiles_rc"])
+    seg = SimpleNamespace(counts=f["seg_counts"], offsets=f["seg_offsets"], total=int(f["seg_counts"].sum()))
+    sk = SimpleNamespace(tiles=tiles, colind=f["j"].astype(np.int64), values=f["v"], segments=seg,
+                         nnz=int(f["j"].size))
+    return sk, orbs
+
+
+@pytest.mark.parametrize("name", ["skel_small.npz", "skel_n1024.npz", "skel_identity.npz"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_from_skeleton_reference_objects(pkg, name, dtype):
+    f = load_fixture(name)
+    n = int(f["n"])
+    sk, orbs = skeleton_objects(f)
+    H = pkg.HalfTiles.from_skeleton(sk, orbs, dtype=dtype)
+    assert H.n == n
+    rc, tiles = H.export_dense()
+    i, j, v = oracle.half_tiles_to_coo(n, rc, tiles)
+    assert oracle.pair_set_digest(i, j) == str(f["pair_digest"])  # exact reference pair set
+    # stored values are the reference's bits
+    ref = {(int(a), int(b)): float(c) for a, b, c in zip(f["i"], f["j"], f["v"])}
+    got = {(int(a), int(b)): float(c) for a, b, c in zip(i, j, v)}
+    assert got == ref
+    Y = pkg.sym_spmm(H, torch.from_numpy(f["X"]).to(dtype).cuda()).cpu().numpy()
+    rel = np.linalg.norm(Y - f["Y_ref"]) / np.linalg.norm(f["Y_ref"])
+    assert rel <= (1e-5 if dtype == torch.float32 else 1e-12)
+
+
+def test_from_skeleton_rejects_inconsistent_segments(pkg):
+    f = load_fixture("skel_small.npz")
+    sk, orbs = skeleton_objects(f)
+    bad = SimpleNamespace(**{**vars(sk), "segments": SimpleNamespace(counts=f["seg_counts"][:-1],
+                                                                      offsets=f["seg_offsets"][:-1])})
+    with pytest.raises(ValueError):
+        pkg.HalfTiles.from_skeleton(bad, orbs)
+    bad2 = SimpleNamespace(**{**vars(sk), "values": f["v"][:-1]})
+    with pytest.raises(ValueError):
+        pkg.HalfTiles.from_skeleton(bad2, orbs)
+
+
+# ----------------------------------------------------------------------------
+# device scan
+# ----------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [0, 1, 5, 4095, 4096, 4097, 100_000, 4096 * 4096 + 123])
+def test_exclusive_scan_matches_scan_serial(pkg, n):
+    from paper_2110_10765_b200.halftiles import exclusive_scan
+
+    rng = np.random.default_rng(n)
+    x = rng.integers(-(1 << 40), 1 << 40, size=n, dtype=np.int64)
+    y = exclusive_scan(torch.from_numpy(x).cuda()).cpu().numpy()
+    want = oracle.scan_serial(x)
+    assert np.array_equal(y[:n], want)
+    assert int(y[n]) == int(x.sum()) if n else int(y[0]) == 0
+    if n == 4:
+        assert y[:4].tolist() == [0, 1, 3, 6]
+
+
+def test_scan_doctest_and_in_place(pkg):
+    L = pkg.lib()
+    x = torch.tensor([1, 2, 3, 4, 0], dtype=torch.int64, device="cuda")  # slot 4 receives the total
+    assert L.cim_exclusive_scan_i64(x.data_ptr(), 4, x.data_ptr(), None) == 0
+    assert x.cpu().tolist() == [0, 1, 3, 6, 10]  # scan.py:131-136 doctest + total
+    y = torch.empty(5, dtype=torch.int64, device="cuda")
+    assert L.cim_exclusive_scan_i64(x.data_ptr(), 4, x[1:].data_ptr(), None) == 1  # overlapping, not in place
+
+
+@pytest.mark.parametrize("T", [1, 7, 5000])
+def test_sparse_tile_offsets(pkg, T):
+    from paper_2110_10765_b200.halftiles import SPARSE_ALIGN, sparse_tile_offsets
+
+    rng = np.random.default_rng(T)
+    rowcnt = rng.integers(0, 65, size=(T, 64)).astype(np.int32)
+    rowcnt[::3] = 0  # empty tiles
+    rowptr, counts, off = sparse_tile_offsets(torch.from_numpy(rowcnt).cuda(), T)
+    rp = rowptr.cpu().numpy().astype(np.int64)
+    assert np.array_equal(rp[:, :64], np.stack([oracle.scan_serial(r) for r in rowcnt]))
+    assert np.array_equal(rp[:, 64], rowcnt.sum(1)) and not rp[:, 65:].any()
+    assert np.array_equal(counts.cpu().numpy(), rowcnt.sum(1))
+    padded = (rowcnt.sum(1) + SPARSE_ALIGN - 1) // SPARSE_ALIGN * SPARSE_ALIGN
+    o, total = oracle.counts_to_offsets(padded)
+    assert np.array_equal(off.cpu().numpy(), np.append(o, total))
+
+
+# ----------------------------------------------------------------------------
+# subnormal partial sums (flush-to-zero float atomics)
+# ----------------------------------------------------------------------------
+
+def test_subnormal_partial_sums(pkg):
+    """X scaled into the f32 subnormal range (|A·X| ~ 1e-39 < 2⁻¹²⁶).
+
+    The fast kernels accumulate a tile's products in registers (IEEE, no
+    flush) but land them with ``red.global.add.f32``, which PTX defines as
+    flushing subnormal inputs and results to zero.  So the fast path's error
+    is bounded absolutely — at most one flushed value (< 2⁻¹²⁶) per
+    reduction into a Y element — while the deterministic mode (plain
+    stores, fixed order) matches the f64 oracle to the IEEE bound.  On
+    normal-range data (every other test) the flush never triggers."""
+    n, k = 1000, 8
+    rc = pkg.synthetic_pattern((n + 63) // 64, 0.3, seed=1)
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc)
+    tiles = oracle.synthetic_dense_tiles(n, rc, seed=0)
+    X = (np.random.default_rng(0).standard_normal((n, k)) * 1e-41).astype(np.float32)  # subnormal inputs
+    Y_ref = oracle.sym_spmm(n, rc, tiles, X.astype(np.float64))
+    assert np.abs(Y_ref).max() < 2.0 ** -126  # the whole result is subnormal
+    Yd = pkg.sym_spmm(H, torch.from_numpy(X).cuda(), deterministic=True).cpu().numpy().astype(np.float64)
+    absAX = oracle.abs_product(n, rc, tiles, np.abs(X.astype(np.float64)))
+    nnz_row = 64 * int(np.bincount(np.concatenate([rc[:, 0], rc[rc[:, 0] != rc[:, 1], 1]])).max())
+    # IEEE gradual underflow: absolute error per op ≤ 2⁻¹⁵⁰ (half the smallest subnormal)
+    assert np.all(np.abs(Yd - Y_ref) <= (nnz_row + 2) * (U32 * absAX + 2.0 ** -149))
+    Yf = pkg.sym_spmm(H, torch.from_numpy(X).cuda()).cpu().numpy().astype(np.float64)
+    reductions = 2 * np.bincount(np.concatenate([rc[:, 0], rc[:, 1]]), minlength=H.nb).max() + 2
+    assert np.all(np.abs(Yf - Y_ref) <= reductions * 2.0 ** -126 + (nnz_row + 2) * U32 * absAX)
+    # scaled back into the normal range the fast path is exact to the usual gate
+    Xs = X * np.float32(2.0 ** 60)
+    Ys = pkg.sym_spmm(H, torch.from_numpy(Xs).cuda()).cpu().numpy()
+    err = oracle.normwise_error(Ys, oracle.sym_spmm(n, rc, tiles, Xs.astype(np.float64)),
+                                oracle.frobenius_full(rc, tiles), Xs)
+    assert err <= 1e-5
+
+
+# ----------------------------------------------------------------------------
+# ShardedSymSpmm with the CUDA kernel, two ranks on one GPU
+# ----------------------------------------------------------------------------
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _sharded_worker(rank, world, port, kind, overlap, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2110_10765_b200 as pkg
+
+        torch.cuda.set_device(0)
+        n, k = 3000, 8
+        if kind == "synthetic":
+            S = pkg.ShardedSymSpmm.synthetic(n, k=k, p=0.2, seed=5, device="cuda:0", max_unit=4, overlap=overlap)
+        else:  # mixed dense + sparse tiles, every rank builds the global matrix and keeps its panel
+            H = pkg.HalfTiles.synthetic_sparse(n, 0.2, fill=0.07, seed=5, fill_seed=3)
+            D = pkg.HalfTiles.synthetic(n, p=0.05, seed=9)
+            Hm = merge_dense_sparse(pkg, D, H)
+            S = pkg.ShardedSymSpmm.from_halftiles(Hm, k=k, overlap=overlap)
+        g = torch.Generator().manual_seed(7)
+        X = torch.randn((S.rows_total, k), generator=g)
+        X[n:] = 0
+        lo = rank * S.rows_per_rank
+        Y = S.apply(X[lo:lo + S.rows_per_rank].cuda()).cpu().numpy()
+        Y2 = S.apply(X[lo:lo + S.rows_per_rank].cuda()).cpu().numpy()  # buffers reused
+        q.put((rank, lo, Y, Y2, S.local_tiles()))
+    finally:
+        dist.destroy_process_group()
+
+
+def merge_dense_sparse(pkg, D, Sp):
+    """A matrix holding D's dense tiles and Sp's sparse tiles where the two
+    patterns do not overlap (test helper)."""
+    d_keys = set(map(tuple, D.tile_rc_host.tolist()))
+    rc_s = Sp.sparse.tile_rc_host
+    keep = np.array([tuple(t) not in d_keys for t in rc_s.tolist()])
+    tid, r, c, v, _ = Sp.sparse.to_entries()
+    sel = keep[tid]
+    new_id = np.cumsum(keep) - 1
+    from paper_2110_10765_b200.halftiles import SparseTiles
+
+    D.sparse = SparseTiles.from_entries(rc_s[keep], new_id[tid[sel]], r[sel], c[sel], v[sel], D.dtype, D.device)
+    D._desc = None
+    return D
+
+
+def _global_reference(pkg, kind, n):
+    if kind == "synthetic":
+        rc = pkg.synthetic_pattern((n + 63) // 64, 0.2, seed=5)
+        return rc, oracle.synthetic_dense_tiles(n, rc, seed=0)
+    H = pkg.HalfTiles.synthetic_sparse(n, 0.2, fill=0.07, seed=5, fill_seed=3)
+    D = pkg.HalfTiles.synthetic(n, p=0.05, seed=9)
+    return merge_dense_sparse(pkg, D, H).export_dense()
+
+
+@pytest.mark.parametrize("kind,overlap", [("synthetic", False), ("synthetic", True), ("mixed", False),
+                                          ("mixed", True)])
+def test_sharded_cuda_two_ranks_one_gpu(pkg, kind, overlap):
+    """Two processes, one GPU, the product's default CUDA panel kernel: the
+    balanced partition, the exchange (host-staged under gloo) and — with
+    ``overlap`` — the column-group schedule with per-chunk reductions; the
+    assembled Y equals the f64 oracle of the global matrix."""
+    import torch.multiprocessing as mp
+
+    world, n, k = 2, 3000, 8
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, world, port, kind, overlap, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    rc, tiles = _global_reference(pkg, kind, n)
+    per = res[0][2].shape[0]
+    Xg = torch.randn((per * world, k), generator=torch.Generator().manual_seed(7))
+    Xg[n:] = 0
+    Y_ref = oracle.sym_spmm(n, rc, tiles.astype(np.float64), Xg[:n].numpy().astype(np.float64))
+    Y = np.zeros((per * world, k))
+    owned = 0
+    for rank, lo, yl, yl2, nt in res:
+        Y[lo:lo + per] = yl
+        assert np.abs(yl2 - yl).max() <= 1e-5 * max(1.0, np.abs(yl).max())
+        owned += nt
+    assert owned == rc.shape[0]  # every stored tile on exactly one rank
+    err = oracle.normwise_error(Y[:n], Y_ref, oracle.frobenius_full(rc, tiles.astype(np.float64)), Xg[:n].numpy())
+    assert err <= 1e-5
+    assert np.all(Y[n:] == 0)
+
+
+# ----------------------------------------------------------------------------
+# C2 / C3 at full size: 256 random block rows against the hash oracle
+# ----------------------------------------------------------------------------
+
+def rows_oracle(n, rc, X, rows, seed=0):
+    """(Y rows, |A||X| rows) of block rows `rows` in f64: Y[R] = Σ_(R,C) T·X_C
+    + Σ_(C',R), C'<R Tᵀ·X_C' with T = h(i XOR j; seed) (pipeline.py:216-222)."""
+    k = X.shape[1]
+    rows = np.asarray(rows)
+    rset = np.zeros(int(rc.max()) + 1, bool)
+    rset[rows] = True
+    sel = np.flatnonzero(rset[rc[:, 0]] | rset[rc[:, 1]])
+    out = {int(R): np.zeros((64, k)) for R in rows}
+    absout = {int(R): np.zeros((64, k)) for R in rows}
+    for c0 in range(0, sel.size, 512):
+        sub = rc[sel[c0:c0 + 512]]
+        T = oracle.synthetic_dense_tiles(n, sub, seed=seed).astype(np.float64)
+        for t, (r, c) in enumerate(sub):
+            if rset[r]:
+                xc = X[c * 64:(c + 1) * 64].astype(np.float64)
+                out[int(r)] += T[t] @ xc
+                absout[int(r)] += np.abs(T[t]) @ np.abs(xc)
+            if r != c and rset[c]:
+                xr = X[r * 64:(r + 1) * 64].astype(np.float64)
+                out[int(c)] += T[t].T @ xr
+                absout[int(c)] += np.abs(T[t]).T @ np.abs(xr)
+    return out, absout
+
+
+def check_rows(pkg, H, n, k, n_rows, seed):
+    nb = H.nb
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    X1 = torch.randn((n, k), device="cuda", generator=g)
+    X2 = torch.randn((n, k), device="cuda", generator=g)
+    Y1 = pkg.sym_spmm(H, X1)
+    Y2 = pkg.sym_spmm(H, X2)
+    # forward/transposed symmetry (test_pipeline.py:278-286 at scale): every tile used both ways
+    a = (X1.double() * Y2.double()).sum(0)
+    b = (Y1.double() * X2.double()).sum(0)
+    assert torch.all((a - b).abs() <= 1e-5 * (X1.double().abs() * Y2.double().abs()).sum(0))
+    rng = np.random.default_rng(seed)
+    rows = np.unique(np.concatenate([[0, nb - 1], rng.choice(nb, n_rows - 2, replace=False)]))
+    rc = H.tile_rc_host
+    Xh = X1.cpu().numpy()
+    want, absw = rows_oracle(n, rc, Xh, rows)
+    Yh = Y1.cpu().numpy().astype(np.float64)
+    cnt = np.bincount(np.concatenate([rc[:, 0], rc[rc[:, 0] != rc[:, 1], 1]]), minlength=nb)
+    for R in rows:
+        got = Yh[R * 64:(R + 1) * 64]
+        c = 64 * int(cnt[R])
+        assert np.all(np.abs(got - want[R]) <= (c + 2) * U32 * absw[R]), f"block row {R}"
+        assert np.linalg.norm(got - want[R]) <= 1e-5 * np.linalg.norm(absw[R])
+    return rows.size
+
+
+@pytest.mark.slow
+def test_c2_full_size_256_rows(pkg):
+    """C2: n = 2²², 488,281 tiles (~2·10⁹ stored values), k = 8 f32."""
+    n, k = 1 << 22, 8
+    H = pkg.HalfTiles.synthetic(n, n_off=488281 - 65536, seed=0)
+    assert check_rows(pkg, H, n, k, 256, seed=1) >= 256
+
+
+@pytest.mark.slow
+def test_c3_full_size_256_rows(pkg):
+    """C3: n = 2²², p_off = 1.7885e-3 → 3.9 M tiles, 16·10⁹ stored values
+    (64 GB of f32 tiles on one B200 — the strong-scaling T(1) config)."""
+    free, _ = torch.cuda.mem_get_info()
+    if free < 72 << 30:
+        pytest.skip(f"C3 needs ~70 GB of device memory, {free >> 30} GB free")
+    n, k = 1 << 22, 8
+    H = pkg.HalfTiles.synthetic(n, p=1.7885e-3, seed=0)
+    assert abs(H.nnz_stored - 16.0e9) < 0.05e9
+    assert check_rows(pkg, H, n, k, 256, seed=2) >= 256
+    del H
+    torch.cuda.empty_cache()

@@ -35,7 +35,7 @@ for case in a.cases.split(","):
     c = b2.random_coefficients(nv, a.n, seed=1)
     inp = b2.ObservablesInput(c=c, m_ops=m, seed=3)
     row = {"n_vec": nv, "m_ops": m, "pairs": pairs}
-    for name, fn in (("fused", lambda: b2.contract_observables(H, inp)),
+    for name, fn in (("fused", lambda: b2.contract_pattern(H, inp)),
                      ("materialized", lambda: contract_materialized(H, inp))):
         fn()
         torch.cuda.synchronize()
@@ -48,7 +48,7 @@ for case in a.cases.split(","):
         ms = e0.elapsed_time(e1) / a.reps
         row[name] = {"ms": round(ms, 3), "Mpair_per_s": round(pairs / ms / 1e3, 1),
                      "Gpair_op_per_s": round(pairs * m / ms / 1e6, 1)}
-    d = np.abs(b2.contract_observables(H, inp).astype(np.float64) - contract_materialized(H, inp)).max()
+    d = np.abs(b2.contract_pattern(H, inp).astype(np.float64) - contract_materialized(H, inp)).max()
     row["max_abs_diff"] = float(d)
     out.append(row)
     print(json.dumps(row), flush=True)

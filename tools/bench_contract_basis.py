@@ -39,12 +39,12 @@ stored = H.meta["stored_entries"]
 diag = int((H.tile_rc_host[:, 0] == H.tile_rc_host[:, 1]).sum()) if H.n_tiles else 0
 c = b2.random_coefficients(a.nvec, a.n, seed=1)
 inp = b2.ObservablesInput(c=c, m_ops=a.m, seed=3)
-b2.contract_observables(H, inp)
+b2.contract_pattern(H, inp)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 for _ in range(a.reps):
-    b2.contract_observables(H, inp)
+    b2.contract_pattern(H, inp)
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / a.reps
