@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget for the cpu_baseline leg")
     ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--bands", type=int, default=1, help="column bands of the tile order (0 = auto)")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="N > 1: serial all-gather → kernel → reduce-scatter instead of the overlapped schedule")
+    ap.add_argument("--no-t1", action="store_true", help="N > 1: skip the one-GPU T(1) measurement on rank 0")
     ap.add_argument("--fused", action="store_true",
                     help="N > 1: fused apply (X / Y chunks in symmetric memory, the kernel reads / reduces peer "
                          "chunks over NVLink) instead of NCCL all-gather + reduce-scatter")
@@ -441,6 +444,9 @@ def impl_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # NCCL's init lines (transport, NVLS / CollNet use) go to stderr for the record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
     dtype = torch.float32 if args.dtype == "f32" else torch.float64
     k = args.k
@@ -456,7 +462,8 @@ def impl_ours(args):
         S = ShardedSymSpmm(n, k, dtype, dev, H_local=Hs)
     else:
         S = ShardedSymSpmm.synthetic(n, k=k, p=p, seed=0, dtype=dtype, device=dev, layout=args.layout,
-                                     bands=None if args.bands == 0 else args.bands, fused=args.fused)
+                                     bands=None if args.bands == 0 else args.bands, fused=args.fused,
+                                     overlap=world > 1 and not args.no_overlap and not args.fused)
     H = S.H
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t_build
@@ -505,6 +512,18 @@ def impl_ours(args):
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
             S._apply_fused(X_local)
+            if timed:
+                e1.record(stream)
+                kern_ms.append((e0, e1))
+        elif S.overlap:
+            # overlapped schedule (sharded.py): own-chunk tiles during the
+            # all-gather, column groups with per-chunk reductions behind them —
+            # the events bracket the whole apply, exchanges included
+            if timed:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            S._apply_overlapped(X_local)
             if timed:
                 e1.record(stream)
                 kern_ms.append((e0, e1))
@@ -590,6 +609,33 @@ def impl_ours(args):
     h2d = (n if world == 1 else S.rows_per_rank) * k * es
     d2h = h2d
 
+    t1 = None
+    if world > 1 and not args.no_t1 and args.fill is None:
+        # strong-scaling base on this box: the same global matrix (N × C2 tiles
+        # — at N = 8 config C3) applied by rank 0's GPU alone, other ranks idle
+        dist.barrier()
+        if rank == 0:
+            try:
+                H1 = pkg.HalfTiles.synthetic(n, p=p, seed=0, dtype=dtype, device=dev, layout=args.layout)
+                X1 = torch.randn((H1.n_pad, k), device=dev, dtype=dtype, generator=gen)
+                Y1 = torch.empty_like(X1)
+                for _ in range(2):
+                    pkg.sym_spmm(H1, X1, out=Y1)
+                a1, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                reps = 5
+                a1.record(stream)
+                for _ in range(reps):
+                    pkg.sym_spmm(H1, X1, out=Y1)
+                b1.record(stream)
+                torch.cuda.synchronize()
+                t1 = {"t1_ms": a1.elapsed_time(b1) / reps, "tiles": H1.n_tiles, "reps": reps,
+                      "what": "the same global matrix on rank 0's GPU alone (sym_spmm, zero Y + kernel)"}
+                del H1, X1, Y1
+                torch.cuda.empty_cache()
+            except Exception as ex:  # report, never fail the bench
+                t1 = {"unavailable": f"{type(ex).__name__}: {ex}"}
+        dist.barrier()
+
     if rank == 0:
         peaks = measured_peaks()
         try:
@@ -646,6 +692,8 @@ def impl_ours(args):
                 + f", k={k}, values h(i XOR j; 0) on device, X ~ N(0,1)",
                 "n": n, "k": k, "stored_tiles": g_tiles, "stored_nnz": H.nnz_stored,
                 "parallelism": (f"row-block shard x{world}" + (" fused peer-memory apply" if S.fused else
+                                                                " NCCL all-gather + per-chunk reduce, overlapped "
+                                                                "with column-group kernels" if S.overlap else
                                                                 " NCCL all-gather/reduce-scatter"))
                 if world > 1 else "single GPU",
                 "layout": H.layout,
@@ -674,7 +722,11 @@ def impl_ours(args):
                     "steps": e2e_steps,
                     "api": "sym_spmm_host_batch (pinned host X/Y, H2D/kernel/D2H overlapped across steps)"
                     if world == 1 else "ShardedSymSpmm.apply per step (host X in, host Y out)"},
-            "gpu_launches": args.steps * (max(1, -(-S.k // 16)) if H.layout == "tc" else (1 if k <= 8 else max(1, k // 16))),
+            "strong_scaling": (dict(t1, tn_ms=ms_step, efficiency=t1["t1_ms"] / (world * ms_step))
+                               if t1 and "t1_ms" in t1 else t1),
+            "gpu_launches": args.steps * (
+                (int(S.g_local is not None) + sum(g is not None for g in S.g_cols)) if S.overlap else
+                max(1, -(-S.k // 16)) if H.layout == "tc" else (1 if k <= 8 else max(1, k // 16))),
             "clocks": clocks.summary(),
         }
         print(json.dumps(line))
