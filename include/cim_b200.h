@@ -135,6 +135,17 @@ typedef struct cim_sparse_tiles {
   /* Largest padded entry count among the staged tiles (0 = unknown); at
      ≤ 512 the staged kernel uses smaller shared-memory stages. */
   int64_t         staged_max_entries;
+  /* Optional row-CSR of the small tiles (built by cim_sparse_csr_count /
+     cim_exclusive_scan_i64 / cim_sparse_csr_fill).  When csr_ptr is set the
+     small tiles are applied from it — row i's entries csr_ptr[i] ..
+     csr_ptr[i+1] hold global columns csr_col and values csr_val (tile
+     dtype), one reduction per row for the direct product — instead of
+     entry-parallel from the tiles.  csr_rows = n_pad. */
+  const int64_t  *csr_ptr;
+  const int32_t  *csr_col;
+  const void     *csr_val;
+  int64_t         csr_rows;
+  int64_t         csr_nnz;
 } cim_sparse_tiles;
 
 typedef struct cim_half_tiles {
@@ -458,6 +469,23 @@ CIM_API int cim_contract_tiles(const uint64_t *bits_lo, const uint16_t *occ, int
                                int64_t n_tiles, const float *c, int64_t ldc, int32_t n_vec,
                                int32_t m_ops, int32_t kind, uint64_t seed, double *accum,
                                uint32_t flags, void *stream);
+
+/*
+ * Device: the row-CSR of a sparse tile set's SMALL tiles (small_tiles list),
+ * for the row-walk apply (cim_sparse_tiles.csr_*).  cim_sparse_csr_count:
+ * row_cnt int64 [n_pad] = small-tile entries per global row (zeroed first).
+ * The caller scans it (cim_exclusive_scan_i64 → csr_ptr [n_pad+1]), then
+ * cim_sparse_csr_fill copies the entries: one thread per (panel, local row)
+ * walks the panel's small tiles in list order, so the entry order is
+ * deterministic.  Panels: the block rows holding small tiles, panel p =
+ * small_tiles[panel_ptr[p] .. panel_ptr[p+1]) all of block row panel_R[p]
+ * (the list is grouped by block row).  csr_col int32 global columns,
+ * csr_val in `dtype`.
+ */
+CIM_API int cim_sparse_csr_count(const cim_sparse_tiles *S, int64_t n_pad, int64_t *row_cnt, void *stream);
+CIM_API int cim_sparse_csr_fill(const cim_sparse_tiles *S, int32_t dtype, const int32_t *panel_R,
+                                const int64_t *panel_ptr, int64_t n_panels, const int64_t *csr_ptr,
+                                int32_t *csr_col, void *csr_val, void *stream);
 
 /*
  * Device: exclusive prefix sum of int64 counts — the reference's scan motif

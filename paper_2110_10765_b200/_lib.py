@@ -60,6 +60,8 @@ EXPORTS = (
     "cim_contract_tiles",
     "cim_exclusive_scan_i64",
     "cim_sparse_tile_offsets",
+    "cim_sparse_csr_count",
+    "cim_sparse_csr_fill",
 )
 
 
@@ -82,6 +84,11 @@ class CimSparseTiles(ctypes.Structure):
         ("small_tiles", ctypes.c_void_p),
         ("n_small", ctypes.c_int64),
         ("staged_max_entries", ctypes.c_int64),
+        ("csr_ptr", ctypes.c_void_p),
+        ("csr_col", ctypes.c_void_p),
+        ("csr_val", ctypes.c_void_p),
+        ("csr_rows", ctypes.c_int64),
+        ("csr_nnz", ctypes.c_int64),
     ]
 
 
@@ -190,6 +197,9 @@ def lib() -> ctypes.CDLL:
     L.cim_exclusive_scan_i64.argtypes = [c.c_void_p, c.c_int64, c.c_void_p, c.c_void_p]
     L.cim_sparse_tile_offsets.argtypes = [c.c_void_p, c.c_int64, c.c_int32, c.c_void_p, c.c_void_p, c.c_void_p,
                                           c.c_void_p]
+    L.cim_sparse_csr_count.argtypes = [c.POINTER(CimSparseTiles), c.c_int64, c.c_void_p, c.c_void_p]
+    L.cim_sparse_csr_fill.argtypes = [c.POINTER(CimSparseTiles), c.c_int32, c.c_void_p, c.c_void_p, c.c_int64,
+                                      c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p]
     for name in EXPORTS:
         if name not in ("cim_version", "cim_last_error"):
             getattr(L, name).restype = c.c_int

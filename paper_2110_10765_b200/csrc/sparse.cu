@@ -492,6 +492,11 @@ __global__ void fill_sparse_values_kernel(const int2 *tile_rc, const long long *
   }
 }
 
+}  // namespace
+int sym_spmm_sparse_csr(const cim_sparse_tiles *S, int dtype, const void *X, void *Y, int k, long long ldy, int sms,
+                        cudaStream_t stream);  // sparse_csr.cu
+namespace {
+
 struct SpState {
   int sms = 0;
   CounterRing *ring = nullptr;  // ticket counters (counter_ring.h)
@@ -592,6 +597,8 @@ int launch_sparse(const cim_sparse_tiles *S, const void *X, void *Y, int k, long
     if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("sparse_spmm launch: ") + cudaGetErrorString(e));
   }
   const long long n_small = listed ? (S->small_tiles ? S->n_small : 0) : (p.small_max > 0 ? S->n_tiles : 0);
+  if (S->csr_ptr && S->csr_rows > 0) return sym_spmm_sparse_csr(S, sizeof(T) == 4 ? CIM_F32 : CIM_F64, X, Y, k, ldy,
+                                                                st->sms, stream);
   if (n_small > 0) {
     const long long g2 = std::min<long long>((n_small + 255) / 256, (long long)st->sms * 16);  // 32 tiles / warp
     sparse_small_kernel<T, KV><<<(unsigned)g2, 256, 0, stream>>>(p, listed ? S->small_tiles : nullptr,

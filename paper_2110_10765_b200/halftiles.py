@@ -23,6 +23,7 @@ bit-exactly on the device, pipeline.py:216-222).
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -252,6 +253,10 @@ class SparseTiles:
     counts_host: np.ndarray  # real entries per tile (the rest of a tile's range is zero padding)
     _desc: CimSparseTiles | None = field(default=None, repr=False)
     _split: tuple | None = field(default=None, repr=False)
+    # row-CSR copy of the small tiles (csr_ptr, csr_col, csr_val, nnz), built
+    # lazily for the row-walk apply; use_csr=False keeps the entry-parallel path
+    use_csr: bool = field(default_factory=lambda: os.environ.get("CIM_SPARSE_CSR", "1") != "0")
+    _csr: tuple | None = field(default=None, repr=False)
 
     @property
     def n_tiles(self) -> int:
@@ -287,19 +292,70 @@ class SparseTiles:
                            int(ne[staged].max()) if staged.size else 0)
         return self._split[0][: self._split[1]], self._split[2][: self._split[3]]
 
-    def descriptor(self) -> CimSparseTiles:
-        if self._desc is None:
-            e = self.n_entries > 0
+    def build_csr(self, n_pad: int):
+        """The row-CSR of the small tiles on the device (cim_sparse_csr_count →
+        cim_exclusive_scan_i64 → cim_sparse_csr_fill): (csr_ptr int64
+        (n_pad+1), csr_col int32 (nnz), csr_val (nnz), nnz).  Entry order per
+        row: the block row's small tiles in list order, then column order."""
+        from ._lib import lib
+
+        self.work_split()
+        st, n_st, sm, n_sm, st_max = self._split
+        dev = self.tile_rc.device
+        L = lib()
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        base = self._base_descriptor()
+        cnt = torch.empty(max(n_pad, 1), dtype=torch.int64, device=dev)
+        with torch.cuda.device(dev):
+            check(L.cim_sparse_csr_count(ctypes.byref(base), n_pad, cnt.data_ptr(), stream), "cim_sparse_csr_count")
+        ptr = exclusive_scan(cnt[:n_pad])
+        nnz = int(ptr[-1].item())
+        col = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+        val = torch.empty(max(nnz, 1), dtype=self.vals.dtype, device=dev)
+        small = sm[:n_sm].cpu().numpy() if n_sm else np.zeros(0, np.int32)
+        R = self.tile_rc_host[small, 0] if small.size else np.zeros(0, np.int32)
+        if R.size and np.any(np.diff(R) < 0):
+            raise ValueError("small-tile list must be grouped by block row")
+        starts = np.flatnonzero(np.concatenate([[True], R[1:] != R[:-1]])) if R.size else np.zeros(0, np.int64)
+        panel_R = torch.from_numpy(np.ascontiguousarray(R[starts], dtype=np.int32)).to(dev)
+        panel_ptr = torch.from_numpy(np.append(starts, R.size).astype(np.int64)).to(dev)
+        from ._lib import CIM_F32, CIM_F64
+
+        with torch.cuda.device(dev):
+            check(L.cim_sparse_csr_fill(ctypes.byref(base), CIM_F32 if self.vals.dtype == torch.float32 else CIM_F64,
+                                        panel_R.data_ptr(), panel_ptr.data_ptr(), int(starts.size), ptr.data_ptr(),
+                                        col.data_ptr(), val.data_ptr(), stream), "cim_sparse_csr_fill")
+        self._csr = (ptr, col, val, nnz, int(n_pad))
+        self._desc = None
+        return self._csr
+
+    def _base_descriptor(self) -> CimSparseTiles:
+        e = self.n_entries > 0
+        self.work_split()
+        st, n_st, sm, n_sm, st_max = self._split
+        return CimSparseTiles(n_tiles=self.n_tiles, n_entries=self.n_entries,
+                              tile_rc=self.tile_rc.data_ptr(), entry_off=self.entry_off.data_ptr(),
+                              rowptr=self.rowptr.data_ptr(), colptr=self.colptr.data_ptr(),
+                              col=self.col.data_ptr() if e else None, row=self.row.data_ptr() if e else None,
+                              cperm=self.cperm.data_ptr() if e else None,
+                              vals=self.vals.data_ptr() if e else None,
+                              staged_tiles=st.data_ptr(), n_staged=n_st,
+                              small_tiles=sm.data_ptr(), n_small=n_sm, staged_max_entries=st_max)
+
+    def descriptor(self, n_pad: int | None = None) -> CimSparseTiles:
+        """C-ABI view; with ``n_pad`` (the matrix's padded order) and
+        ``use_csr`` the small tiles' row-CSR is built once and attached."""
+        if self._desc is None or (n_pad is not None and self.use_csr and self._csr is None
+                                  and self._split is not None and self._split[3] > 0):
             self.work_split()
-            st, n_st, sm, n_sm, st_max = self._split
-            self._desc = CimSparseTiles(n_tiles=self.n_tiles, n_entries=self.n_entries,
-                                        tile_rc=self.tile_rc.data_ptr(), entry_off=self.entry_off.data_ptr(),
-                                        rowptr=self.rowptr.data_ptr(), colptr=self.colptr.data_ptr(),
-                                        col=self.col.data_ptr() if e else None, row=self.row.data_ptr() if e else None,
-                                        cperm=self.cperm.data_ptr() if e else None,
-                                        vals=self.vals.data_ptr() if e else None,
-                                        staged_tiles=st.data_ptr(), n_staged=n_st,
-                                        small_tiles=sm.data_ptr(), n_small=n_sm, staged_max_entries=st_max)
+            if n_pad is not None and self.use_csr and self._csr is None and self._split[3] > 0:
+                self.build_csr(n_pad)
+            d = self._base_descriptor()
+            if self.use_csr and self._csr is not None:
+                ptr, col, val, nnz, rows = self._csr
+                d.csr_ptr, d.csr_col, d.csr_val = ptr.data_ptr(), col.data_ptr(), val.data_ptr()
+                d.csr_rows, d.csr_nnz = rows, nnz
+            self._desc = d
         return self._desc
 
     def select_rows(self, r_lo: int, r_hi: int) -> "SparseTiles":
@@ -504,7 +560,7 @@ class HalfTiles:
                 vals=self.vals.data_ptr() if self.n_tiles else None,
                 layout=LAYOUTS[self.layout],
                 reserved=0,
-                sparse=ctypes.pointer(self.sparse.descriptor()) if self.n_sparse_tiles else None,
+                sparse=ctypes.pointer(self.sparse.descriptor(self.n_pad)) if self.n_sparse_tiles else None,
             )
             if self._det is not None:
                 d = self._desc

@@ -350,3 +350,58 @@ def test_c3_full_size_256_rows(pkg):
     assert check_rows(pkg, H, n, k, 256, seed=2) >= 256
     del H
     torch.cuda.empty_cache()
+
+
+# ----------------------------------------------------------------------------
+# small sparse tiles: the row-CSR apply against the entry-parallel kernel
+# ----------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dtype,k", [(torch.float32, 8), (torch.float32, 3), (torch.float32, 16),
+                                     (torch.float64, 4), (torch.float64, 1)])
+@pytest.mark.parametrize("fill", [0.004, 0.02])
+def test_small_tiles_csr_path(pkg, dtype, k, fill):
+    """Tiles of a few dozen entries go through the row-CSR of the small tiles
+    (cim_sparse_csr_*): the CSR holds exactly the small tiles' entries, and
+    the apply matches the f64 oracle and the entry-parallel kernel."""
+    n = 5000
+    H = pkg.HalfTiles.synthetic_sparse(n, 0.3, fill=fill, seed=4, fill_seed=2, dtype=dtype)
+    sp = H.sparse
+    st, sm = sp.work_split()
+    assert sm.numel() > 0
+    H.descriptor()  # builds the CSR
+    assert sp._csr is not None
+    ptr, col, val, nnz, rows = sp._csr
+    assert rows == H.n_pad and nnz == int(sp.counts_host[sm.cpu().numpy()].sum())
+    # CSR == the small tiles' entries (set of (i, j, v))
+    tid, r, c, v, _ = sp.to_entries()
+    small = np.isin(tid, sm.cpu().numpy())
+    rc = sp.tile_rc_host
+    want = sorted(zip((rc[tid[small], 0] * 64 + r[small]).tolist(), (rc[tid[small], 1] * 64 + c[small]).tolist(),
+                      v[small].tolist()))
+    p_ = ptr.cpu().numpy()
+    rows_i = np.repeat(np.arange(rows), np.diff(p_))
+    got = sorted(zip(rows_i.tolist(), col[:nnz].cpu().numpy().tolist(), val[:nnz].cpu().numpy().tolist()))
+    assert got == want
+    rcd, tiles = H.export_dense()
+    X = torch.randn((n, k), generator=torch.Generator().manual_seed(k), dtype=dtype)
+    Y = pkg.sym_spmm(H, X.cuda()).cpu().numpy()
+    Y_ref = oracle.sym_spmm(n, rcd, tiles.astype(np.float64), X.numpy().astype(np.float64))
+    err = oracle.normwise_error(Y, Y_ref, oracle.frobenius_full(rcd, tiles.astype(np.float64)), X.numpy())
+    assert err <= (1e-5 if dtype == torch.float32 else 1e-12)
+    H2 = pkg.HalfTiles.synthetic_sparse(n, 0.3, fill=fill, seed=4, fill_seed=2, dtype=dtype)
+    H2.sparse.use_csr = False
+    Y2 = pkg.sym_spmm(H2, X.cuda()).cpu().numpy()
+    assert np.abs(Y2 - Y).max() <= (1e-5 if dtype == torch.float32 else 1e-12) * max(1.0, np.abs(Y).max())
+
+
+def test_basis_skeleton_csr_path(pkg):
+    """A reference-style basis skeleton (the golden n=1024 fixture's basis,
+    device-built) through the CSR small-tile path vs the reference's scipy
+    product."""
+    f = load_fixture("skel_n1024.npz")
+    H = pkg.HalfTiles.from_basis(f["basis_occ"], f["basis_bits_lo"], rank=int(f["rank_threshold"]) // 2)
+    X = torch.from_numpy(f["X"]).cuda()
+    Y = pkg.sym_spmm(H, X).cpu().numpy()
+    assert H.sparse is not None and H.sparse._csr is not None
+    rel = np.linalg.norm(Y - f["Y_ref"]) / np.linalg.norm(f["Y_ref"])
+    assert rel <= 1e-5

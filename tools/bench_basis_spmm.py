@@ -52,7 +52,10 @@ torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / a.reps
 stored = H.meta["stored_entries"]
 n_diag_entries = None
-out = {"n": a.n, "bias": a.bias, "k": a.k, "stored_entries": stored, "dense_tiles": H.n_tiles,
+ab = H.algorithmic_bytes(a.k)
+out = {"n": a.n, "bias": a.bias, "k": a.k, "csr": os.environ.get("CIM_SPARSE_CSR", "1") != "0",
+       "stored_entries": stored, "dense_tiles": H.n_tiles, "algorithmic_bytes": ab,
+       "hbm_frac": round(ab / (ms / 1e3) / 1e9 / 6548.5, 4),
        "sparse_tiles": H.n_sparse_tiles, "ms_per_apply": round(ms, 4),
        "G_stored_entries_per_s": round(stored / ms / 1e6, 2),
        "GFLOP_per_s_approx": round(4 * a.k * stored / ms / 1e6, 1)}
