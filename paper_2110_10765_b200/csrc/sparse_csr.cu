@@ -70,7 +70,21 @@ __global__ void csr_fill_kernel(const int32_t *small, const int2 *tile_rc, const
 
 template <typename T, int KV>
 __device__ __forceinline__ void ld_vec(T (&d)[KV], const T *p) {
-  if constexpr (sizeof(T) == 4 && KV % 4 == 0) {
+  if constexpr (sizeof(T) * KV == 32) {
+    // one 256-bit load per row slice (LDG.E.ENL2.256, sm_100): half the L1
+    // requests of two 128-bit loads for the random X gathers
+    uint32_t u[8];
+    asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7])
+                 : "l"(p));
+    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) d[q] = __uint_as_float(u[q]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) d[q] = __hiloint2double((int)u[2 * q + 1], (int)u[2 * q]);
+    }
+  } else if constexpr (sizeof(T) == 4 && KV % 4 == 0) {
 #pragma unroll
     for (int q = 0; q < KV / 4; ++q) {
       const float4 v = __ldg(reinterpret_cast<const float4 *>(p) + q);

@@ -215,6 +215,7 @@ def fragment_pack_host(tiles: np.ndarray, layout: str = "frag") -> np.ndarray:
     return np.ascontiguousarray(tiles.reshape(T, 4096)[:, row * BLOCK + col])
 
 
+CSR_MIN_ROW_ENTRIES = 12  # mean entries per non-empty row below which small tiles stay entry-parallel
 SPARSE_ALIGN = 16  # entries: every sparse tile's entry range starts 16-entry aligned (vector staging)
 SPARSE_PTR_STRIDE = 72  # uint16 row / column pointers per sparse tile (65 used): 144-byte, 16-B-aligned rows
 
@@ -310,6 +311,14 @@ class SparseTiles:
             check(L.cim_sparse_csr_count(ctypes.byref(base), n_pad, cnt.data_ptr(), stream), "cim_sparse_csr_count")
         ptr = exclusive_scan(cnt[:n_pad])
         nnz = int(ptr[-1].item())
+        busy = int((cnt[:n_pad] > 0).sum().item())
+        if nnz < CSR_MIN_ROW_ENTRIES * max(busy, 1):
+            # rows this short leave most lanes of a row group idle: the
+            # entry-parallel small-tile kernel is faster (1%-fill C2 family:
+            # 4.8 entries per row, 0.52 vs 0.57 ms) — keep it
+            self.use_csr = False
+            self._desc = None
+            return None
         col = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
         val = torch.empty(max(nnz, 1), dtype=self.vals.dtype, device=dev)
         small = sm[:n_sm].cpu().numpy() if n_sm else np.zeros(0, np.int32)
