@@ -546,6 +546,28 @@ def impl_ours(args):
     X_full = S.X_full
     if world == 1:
         X_full.copy_(X_local[: X_full.shape[0]])
+    overlap_check = None
+    if S.overlap:
+        # the overlapped schedule is checked against the serial exchange on
+        # this box before it is timed; a mismatch (or an error) falls back
+        try:
+            Yo = S._apply_overlapped(X_local).clone()
+            S.overlap = False
+            Ys = S.apply(X_local).clone()
+            S.overlap = True
+            diff = (Yo - Ys).abs().max()
+            scale = Ys.abs().max().clamp_min(1e-30)
+            if world > 1:
+                dist.all_reduce(diff, op=dist.ReduceOp.MAX)
+                dist.all_reduce(scale, op=dist.ReduceOp.MAX)
+            overlap_check = float(diff / scale)
+            if not overlap_check <= 1e-5:
+                S.overlap = False
+        except Exception as ex:  # report and time the serial exchange instead
+            S.overlap = False
+            overlap_check = f"{type(ex).__name__}: {ex}"
+        if not S.overlap:
+            print(f"warning: overlapped schedule disabled ({overlap_check})", file=sys.stderr)
 
     for _ in range(args.warmup):
         step(False)
@@ -722,6 +744,7 @@ def impl_ours(args):
                     "steps": e2e_steps,
                     "api": "sym_spmm_host_batch (pinned host X/Y, H2D/kernel/D2H overlapped across steps)"
                     if world == 1 else "ShardedSymSpmm.apply per step (host X in, host Y out)"},
+            "overlap_check_rel_diff": overlap_check,
             "strong_scaling": (dict(t1, tn_ms=ms_step, efficiency=t1["t1_ms"] / (world * ms_step))
                                if t1 and "t1_ms" in t1 else t1),
             "gpu_launches": args.steps * (
