@@ -1016,6 +1016,236 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
 }
 
 // ---------------------------------------------------------------------------
+// Three-ring variant of the wide-register kernel (KROW = one warpgroup's
+// vectors: f32 k = 8, f64 k = 4).  The two-ring kernel above keeps a unit's
+// X_R rows in registers, which costs 64 of its 232 registers and leaves room
+// for only two consumer warps per scheduler; ncu shows it issue-limited
+// (51% issue, FMA pipe 59%, `wait` the top stall) while DRAM runs at 92% of
+// the copy peak, so at k = 8 it is simultaneously at its byte and its issue
+// bound.  Here X_R rows are read from the stage with every tile instead
+// (the producer copies X_R per tile: an L2 hit after the unit's first tile),
+// which brings the consumers to 160 registers and a CTA to three
+// independent rings (WG0-WG2 consumers, WG3 = three producer warps):
+// three consumer warps per scheduler for the same FFMA2 stream.  The first
+// micro-row of a tile initialises the transposed accumulators with a
+// multiply (no zeroing moves).
+// ---------------------------------------------------------------------------
+constexpr int kR3Threads = 512;
+constexpr int kR3ConsumerRegs = 160;
+constexpr int kR3ProducerRegs = 32;
+
+__device__ __forceinline__ u64 mul2s(float t, u64 x) {
+  u64 tt, r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(tt) : "f"(t));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(tt), "l"(x));
+  return r;
+}
+
+template <typename T>
+__device__ __forceinline__ typename WideE<T>::E wide_mul(T t, typename WideE<T>::E x) {
+  if constexpr (sizeof(T) == 4)
+    return mul2s(t, x);
+  else
+    return t * x;
+}
+
+template <typename T, int KROW>
+__global__ void __launch_bounds__(kR3Threads, 1) sym_spmm_k8r3_kernel(const SpmmParams p) {
+  using W = WideE<T>;
+  using E = typename W::E;
+  constexpr int VPG = W::VPG;
+  static_assert(KROW == VPG, "one warpgroup's vectors per row");
+  extern __shared__ __align__(128) unsigned char smem_all[];
+  constexpr int K = KROW;
+  constexpr int SUBS = 3;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform
+  const int lane = threadIdx.x & 31;
+  const int wg = warp >> 2;
+  const int S = p.stages;
+  const unsigned int tile_bytes = p.tile_bytes, xblk = p.xblk_bytes;
+
+  if (threadIdx.x < SUBS) {
+    unsigned char *sm = smem_all + (size_t)threadIdx.x * p.sub_bytes;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm + (size_t)S * p.stage_bytes);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&full[S + s], 4);  // empty[s]: one arrival per consumer warp
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (wg == 3) {
+    // ======================= producer warps (12, 13, 14) =======================
+    setmaxnreg_dec<kR3ProducerRegs>();
+    if (warp >= 12 + SUBS) return;
+    const int sub = warp - 12;
+    const size_t ybytes = (size_t)kBlock * p.ldy * sizeof(T);
+    unsigned char *smem = smem_all + (size_t)sub * p.sub_bytes;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)S * p.stage_bytes);
+    uint64_t *empty = full + S;
+    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_keep = policy_evict_last();
+    int stage = 0;
+    uint32_t phase = 0;
+    unsigned int u = 0;
+    if (lane == 0) u = atomicAdd(p.counter, 1u);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    while ((long long)u < p.n_units) {
+      const int4 unit = p.units[u];
+      unsigned int u_next = 0;
+      if (lane == 0) u_next = atomicAdd(p.counter, 1u);
+      const int R = unit.x, t0 = unit.y, t1 = unit.z;
+      const int orr = R / p.chunk_blocks, lr = R - orr * p.chunk_blocks;
+      for (int tb = t0; tb < t1; tb += 32) {
+        const int t = tb + lane;
+        const int myC = (t < t1) ? p.tile_rc[t].y : 0;
+        const int cnt = min(32, t1 - tb);
+        for (int q = 0; q < cnt; ++q) {
+          const int C = __shfl_sync(0xffffffffu, myC, q);
+          if (lane == 0) {
+            mbar_wait_backoff(&empty[stage], phase ^ 1u);
+            unsigned char *st = smem + (size_t)stage * p.stage_bytes;
+            const int tt = tb + q;
+            const bool diag = (C == R);
+            const int flags = (tt == t0 ? HDR_FIRST : 0) | (tt == t1 - 1 ? HDR_LAST : 0) | (diag ? HDR_DIAG : 0);
+            const int oc = C / p.chunk_blocks, lc = C - oc * p.chunk_blocks;
+            WideHdr *h = reinterpret_cast<WideHdr *>(st + tile_bytes + 2 * xblk);
+            *h = WideHdr{R, C, flags, 0, p.ych[orr] + (size_t)lr * ybytes, p.ych[oc] + (size_t)lc * ybytes};
+            mbar_arrive_expect_tx(&full[stage], tile_bytes + (diag ? xblk : 2 * xblk));
+            bulk_g2s(st, p.vals + (size_t)tt * tile_bytes, tile_bytes, &full[stage], pol_stream);
+            bulk_g2s(st + tile_bytes, p.xch[oc] + (size_t)lc * xblk, xblk, &full[stage], pol_keep);
+            if (!diag)  // X_R with every tile (L2-resident across the unit)
+              bulk_g2s(st + tile_bytes + xblk, p.xch[orr] + (size_t)lr * xblk, xblk, &full[stage], pol_keep);
+          }
+          __syncwarp();
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+      u = __shfl_sync(0xffffffffu, u_next, 0);
+    }
+    if (lane == 0) {
+      mbar_wait_backoff(&empty[stage], phase ^ 1u);
+      WideHdr *h = reinterpret_cast<WideHdr *>(smem + (size_t)stage * p.stage_bytes + tile_bytes + 2 * xblk);
+      *h = WideHdr{0, 0, HDR_TERM, 0, nullptr, nullptr};
+      mbar_arrive(&full[stage]);
+    }
+    return;
+  }
+
+  // ======================= consumer warpgroups (rings 0, 1, 2) =======================
+  setmaxnreg_inc<kR3ConsumerRegs>();
+  const int sub = wg;
+  const int v0 = p.v_base;
+  unsigned char *smem = smem_all + (size_t)sub * p.sub_bytes;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)S * p.stage_bytes);
+  uint64_t *empty = full + S;
+  const int gt = threadIdx.x & 127;
+  const int rg = frag_rg(gt), cg = frag_cg(gt);
+  const int sw = xr_chunk_swap<8>(rg);
+  const long long ldy = p.ldy;
+  const uint64_t ypol = policy_evict_normal();
+
+  E ar[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ar[i][q] = W::zero();
+
+  int stage = 0;
+  uint32_t phase = 0;
+  while (true) {
+    mbar_wait(&full[stage], phase);
+    const unsigned char *st = smem + (size_t)stage * p.stage_bytes;
+    const WideHdr h = *reinterpret_cast<const WideHdr *>(st + tile_bytes + 2 * xblk);
+    if (h.flags & HDR_TERM) {
+      if (p.n_chunks > 1) __threadfence_system();
+      break;
+    }
+    const T *Ts = reinterpret_cast<const T *>(st);
+    const T *XC = reinterpret_cast<const T *>(st + tile_bytes);
+    const bool diag = h.flags & HDR_DIAG;
+    const T *XR = diag ? XC : reinterpret_cast<const T *>(st + tile_bytes + xblk);
+    if (h.flags & HDR_FIRST) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ar[i][q] = W::zero();
+    }
+    E xc[4][4], ac[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const unsigned char *row = reinterpret_cast<const unsigned char *>(XC + (cg + 16 * j) * K + v0);
+      const ulonglong2 a = *reinterpret_cast<const ulonglong2 *>(row);
+      const ulonglong2 b = *reinterpret_cast<const ulonglong2 *>(row + 16);
+      xc[j][0] = W::from_bits(a.x);
+      xc[j][1] = W::from_bits(a.y);
+      xc[j][2] = W::from_bits(b.x);
+      xc[j][3] = W::from_bits(b.y);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      T t[4];
+      W::trow(t, Ts, i, gt);
+      E xr[4];
+      {
+        const unsigned char *row = reinterpret_cast<const unsigned char *>(XR + (rg + 8 * i) * K + v0);
+        const ulonglong2 a = *reinterpret_cast<const ulonglong2 *>(row + 16 * sw);
+        const ulonglong2 b = *reinterpret_cast<const ulonglong2 *>(row + 16 * (sw ^ 1));
+        xr[0] = W::from_bits(a.x);
+        xr[1] = W::from_bits(a.y);
+        xr[2] = W::from_bits(b.x);
+        xr[3] = W::from_bits(b.y);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          ar[i][q] = W::fma(t[j], xc[j][q], ar[i][q]);
+          ac[j][q] = (i == 0) ? wide_mul<T>(t[j], xr[q]) : W::fma(t[j], xr[q], ac[j][q]);
+        }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == S) {
+      stage = 0;
+      phase ^= 1u;
+    }
+    if (!diag) reduce_cols_wide<T>(ac, lane, cg, reinterpret_cast<T *>(h.yc) + v0, ldy, ypol);
+    if (h.flags & HDR_LAST) {
+      const bool b0 = lane & 1, b1 = lane & 2;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const E send = b0 ? ar[i][q] : ar[i + 4][q];
+          const E keep = b0 ? ar[i + 4][q] : ar[i][q];
+          ar[i][q] = W::add(keep, W::shfl_xor(send, 1));
+        }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const E send = b1 ? ar[i][q] : ar[i + 2][q];
+          const E keep = b1 ? ar[i + 2][q] : ar[i][q];
+          ar[i][q] = W::add(keep, W::shfl_xor(send, 2));
+        }
+      const int i0 = (b0 ? 4 : 0) + (b1 ? 2 : 0);
+      T *yblk = reinterpret_cast<T *>(h.yr) + v0;
+#pragma unroll
+      for (int ri = 0; ri < 2; ++ri) {
+        T *yr = yblk + (long long)(rg + 8 * (i0 + ri)) * ldy;
+        W::flush(yr, ar[ri][0], ar[ri][1], ypol);
+        W::flush(yr + VPG / 2, ar[ri][2], ar[ri][3], ypol);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 namespace {
@@ -1269,6 +1499,73 @@ int launch_k8(const cim_half_tiles *H, const Chunks &ck, long long ldy, cudaStre
   return CIM_OK;
 }
 
+template <typename T, int KROW>
+int launch_k8r3(const cim_half_tiles *H, const Chunks &ck, long long ldy, cudaStream_t stream, DeviceState *ds) {
+  static std::mutex attr_mu;
+  static bool attr_done[64] = {};
+  constexpr int SUBS = 3;
+  const unsigned int tile_bytes = kTileElems * sizeof(T);
+  const unsigned int xblk = kBlock * KROW * sizeof(T);
+  const unsigned int stage_bytes = (tile_bytes + 2 * xblk + sizeof(WideHdr) + 127u) & ~127u;
+  const size_t budget = (size_t)(227 * 1024) / SUBS;
+  int S = std::min((int)((budget - 128) / stage_bytes), 8);
+  if (S < 2) return set_error(CIM_EUNSUPPORTED, "k too large for the three-ring kernel's stages");
+  const size_t sub_bytes = ((size_t)S * stage_bytes + 128 + 127) & ~(size_t)127;
+  const size_t smem = SUBS * sub_bytes;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaError_t e = cudaSuccess;
+  {
+    std::lock_guard<std::mutex> lk(attr_mu);
+    if (!attr_done[dev & 63]) {
+      e = cudaFuncSetAttribute(sym_spmm_k8r3_kernel<T, KROW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess)
+        return set_error(CIM_ECUDA, std::string("cudaFuncSetAttribute(k8r3): ") + cudaGetErrorString(e));
+      attr_done[dev & 63] = true;
+    }
+  }
+  long long grid = std::min<long long>(ds->sms, (H->n_units + SUBS - 1) / SUBS);
+  if (grid < 1) return CIM_OK;
+  CounterLease lease;
+  if (const int rc = lease.take(*ds->ring, stream, 1)) return rc;
+  SpmmParams p;
+  p.units = reinterpret_cast<const int4 *>(H->units);
+  p.tile_rc = reinterpret_cast<const int2 *>(H->tile_rc);
+  p.vals = reinterpret_cast<const unsigned char *>(H->vals);
+  p.X = reinterpret_cast<const unsigned char *>(ck.x[0]);
+  p.Y = reinterpret_cast<unsigned char *>(ck.y[0]);
+  p.counter = lease.ctr;
+  p.n_units = H->n_units;
+  p.ldy = ldy;
+  p.k = KROW;
+  p.v_base = 0;
+  p.stages = S;
+  p.stage_bytes = stage_bytes;
+  p.tile_bytes = tile_bytes;
+  p.xblk_bytes = xblk;
+  p.sub_bytes = (unsigned int)sub_bytes;
+  p.n_chunks = ck.n;
+  p.chunk_blocks = ck.blocks;
+  for (int c = 0; c < kMaxChunks; ++c) {
+    p.xch[c] = reinterpret_cast<const unsigned char *>(ck.x[c < ck.n ? c : 0]);
+    p.ych[c] = reinterpret_cast<unsigned char *>(ck.y[c < ck.n ? c : 0]);
+  }
+  sym_spmm_k8r3_kernel<T, KROW><<<(unsigned int)grid, kR3Threads, smem, stream>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("sym_spmm_k8r3 launch: ") + cudaGetErrorString(e));
+  return CIM_OK;
+}
+
+// CIM_K8_RINGS=2 selects the two-ring kernel for the one-warpgroup widths
+// (A/B); the three-ring kernel is the default.
+bool use_r3() {
+  static const bool v = [] {
+    const char *e = std::getenv("CIM_K8_RINGS");
+    return !(e && std::atoi(e) == 2);
+  }();
+  return v;
+}
+
 // X (n_pad × k, row-major) → pass-major slices Xp[ps] (n_pad × W): each
 // 16-byte chunk of a row goes to its pass slice.
 __global__ void pass_major_kernel(const uint4 *__restrict__ X, uint4 *__restrict__ Xp, long long rows, int row_chunks,
@@ -1318,7 +1615,7 @@ int launch_wide(const cim_half_tiles *H, int k, const Chunks &ck, long long ldy,
                 DeviceState *ds) {
   if (H->dtype == CIM_F32) {
     switch (k) {
-      case 8: return launch_k8<float, 1, 8>(H, ck, ldy, stream, ds);
+      case 8: return use_r3() ? launch_k8r3<float, 8>(H, ck, ldy, stream, ds) : launch_k8<float, 1, 8>(H, ck, ldy, stream, ds);
       case 16: return launch_k8<float, 2, 16>(H, ck, ldy, stream, ds);
       case 24: return launch_k8<float, 1, 24>(H, ck, ldy, stream, ds);
       case 32: return launch_k8<float, 2, 32>(H, ck, ldy, stream, ds);
@@ -1327,7 +1624,7 @@ int launch_wide(const cim_half_tiles *H, int k, const Chunks &ck, long long ldy,
     }
   } else {
     switch (k) {
-      case 4: return launch_k8<double, 1, 4>(H, ck, ldy, stream, ds);
+      case 4: return launch_k8<double, 1, 4>(H, ck, ldy, stream, ds);  // HBM-bound (0.96): the two-ring kernel is 1% faster
       case 8: return launch_k8<double, 2, 8>(H, ck, ldy, stream, ds);
       case 12: return launch_k8<double, 1, 12>(H, ck, ldy, stream, ds);
       case 16: return launch_k8<double, 2, 16>(H, ck, ldy, stream, ds);
