@@ -91,6 +91,11 @@ struct SpmmParams {
   int n_chunks, chunk_blocks;
   const unsigned char *xch[kMaxChunks];
   unsigned char *ych[kMaxChunks];
+  // three-ring kernel, paired passes: work item i = (unit i / n_pass, pass
+  // i % n_pass); pass q stages X from the pass-major slice at q·xpass_bytes
+  // and writes Y columns q·KROW … (n_pass = 1: plain single pass)
+  int n_pass;
+  long long xpass_bytes;
 };
 
 template <typename T>
@@ -1084,19 +1089,24 @@ __global__ void __launch_bounds__(kR3Threads, 1) sym_spmm_k8r3_kernel(const Spmm
     unsigned char *smem = smem_all + (size_t)sub * p.sub_bytes;
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)S * p.stage_bytes);
     uint64_t *empty = full + S;
-    const uint64_t pol_stream = policy_evict_first();
+    // paired passes read every tile n_pass times back to back: keep tiles in
+    // L2 (evict_normal) so the later passes of a unit hit; one pass streams
+    const uint64_t pol_tile = p.n_pass > 1 ? policy_evict_normal() : policy_evict_first();
     const uint64_t pol_keep = policy_evict_last();
     int stage = 0;
     uint32_t phase = 0;
     unsigned int u = 0;
+    const long long n_items = p.n_units * p.n_pass;
     if (lane == 0) u = atomicAdd(p.counter, 1u);
     u = __shfl_sync(0xffffffffu, u, 0);
-    while ((long long)u < p.n_units) {
-      const int4 unit = p.units[u];
+    while ((long long)u < n_items) {
+      const unsigned int ui = u / (unsigned)p.n_pass, pass = u - ui * (unsigned)p.n_pass;
+      const int4 unit = p.units[ui];
       unsigned int u_next = 0;
       if (lane == 0) u_next = atomicAdd(p.counter, 1u);
       const int R = unit.x, t0 = unit.y, t1 = unit.z;
       const int orr = R / p.chunk_blocks, lr = R - orr * p.chunk_blocks;
+      const unsigned char *xs = p.xch[0] + (size_t)pass * (size_t)p.xpass_bytes;  // pass slice (n_chunks = 1)
       for (int tb = t0; tb < t1; tb += 32) {
         const int t = tb + lane;
         const int myC = (t < t1) ? p.tile_rc[t].y : 0;
@@ -1111,12 +1121,18 @@ __global__ void __launch_bounds__(kR3Threads, 1) sym_spmm_k8r3_kernel(const Spmm
             const int flags = (tt == t0 ? HDR_FIRST : 0) | (tt == t1 - 1 ? HDR_LAST : 0) | (diag ? HDR_DIAG : 0);
             const int oc = C / p.chunk_blocks, lc = C - oc * p.chunk_blocks;
             WideHdr *h = reinterpret_cast<WideHdr *>(st + tile_bytes + 2 * xblk);
-            *h = WideHdr{R, C, flags, 0, p.ych[orr] + (size_t)lr * ybytes, p.ych[oc] + (size_t)lc * ybytes};
+            *h = WideHdr{R, C, flags, (int)pass * KROW, p.ych[orr] + (size_t)lr * ybytes,
+                         p.ych[oc] + (size_t)lc * ybytes};
             mbar_arrive_expect_tx(&full[stage], tile_bytes + (diag ? xblk : 2 * xblk));
-            bulk_g2s(st, p.vals + (size_t)tt * tile_bytes, tile_bytes, &full[stage], pol_stream);
-            bulk_g2s(st + tile_bytes, p.xch[oc] + (size_t)lc * xblk, xblk, &full[stage], pol_keep);
-            if (!diag)  // X_R with every tile (L2-resident across the unit)
-              bulk_g2s(st + tile_bytes + xblk, p.xch[orr] + (size_t)lr * xblk, xblk, &full[stage], pol_keep);
+            bulk_g2s(st, p.vals + (size_t)tt * tile_bytes, tile_bytes, &full[stage], pol_tile);
+            if (p.n_pass == 1) {
+              bulk_g2s(st + tile_bytes, p.xch[oc] + (size_t)lc * xblk, xblk, &full[stage], pol_keep);
+              if (!diag)  // X_R with every tile (L2-resident across the unit)
+                bulk_g2s(st + tile_bytes + xblk, p.xch[orr] + (size_t)lr * xblk, xblk, &full[stage], pol_keep);
+            } else {
+              bulk_g2s(st + tile_bytes, xs + (size_t)C * xblk, xblk, &full[stage], pol_keep);
+              if (!diag) bulk_g2s(st + tile_bytes + xblk, xs + (size_t)R * xblk, xblk, &full[stage], pol_keep);
+            }
           }
           __syncwarp();
           if (++stage == S) {
@@ -1139,7 +1155,7 @@ __global__ void __launch_bounds__(kR3Threads, 1) sym_spmm_k8r3_kernel(const Spmm
   // ======================= consumer warpgroups (rings 0, 1, 2) =======================
   setmaxnreg_inc<kR3ConsumerRegs>();
   const int sub = wg;
-  const int v0 = p.v_base;
+  constexpr int v0 = 0;  // staged X rows hold exactly this item's KROW vectors
   unsigned char *smem = smem_all + (size_t)sub * p.sub_bytes;
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)S * p.stage_bytes);
   uint64_t *empty = full + S;
@@ -1214,7 +1230,7 @@ __global__ void __launch_bounds__(kR3Threads, 1) sym_spmm_k8r3_kernel(const Spmm
       stage = 0;
       phase ^= 1u;
     }
-    if (!diag) reduce_cols_wide<T>(ac, lane, cg, reinterpret_cast<T *>(h.yc) + v0, ldy, ypol);
+    if (!diag) reduce_cols_wide<T>(ac, lane, cg, reinterpret_cast<T *>(h.yc) + h.pad, ldy, ypol);
     if (h.flags & HDR_LAST) {
       const bool b0 = lane & 1, b1 = lane & 2;
 #pragma unroll
@@ -1234,7 +1250,7 @@ __global__ void __launch_bounds__(kR3Threads, 1) sym_spmm_k8r3_kernel(const Spmm
           ar[i][q] = W::add(keep, W::shfl_xor(send, 2));
         }
       const int i0 = (b0 ? 4 : 0) + (b1 ? 2 : 0);
-      T *yblk = reinterpret_cast<T *>(h.yr) + v0;
+      T *yblk = reinterpret_cast<T *>(h.yr) + h.pad;
 #pragma unroll
       for (int ri = 0; ri < 2; ++ri) {
         T *yr = yblk + (long long)(rg + 8 * (i0 + ri)) * ldy;
@@ -1488,6 +1504,8 @@ int launch_k8(const cim_half_tiles *H, const Chunks &ck, long long ldy, cudaStre
     p.sub_bytes = (unsigned int)sub_bytes;
     p.n_chunks = ck.n;
     p.chunk_blocks = ck.blocks;
+    p.n_pass = 1;
+    p.xpass_bytes = 0;
     for (int c = 0; c < kMaxChunks; ++c) {
       p.xch[c] = reinterpret_cast<const unsigned char *>(ck.x[c < ck.n ? c : 0]);
       p.ych[c] = reinterpret_cast<unsigned char *>(ck.y[c < ck.n ? c : 0]);
@@ -1500,7 +1518,8 @@ int launch_k8(const cim_half_tiles *H, const Chunks &ck, long long ldy, cudaStre
 }
 
 template <typename T, int KROW>
-int launch_k8r3(const cim_half_tiles *H, const Chunks &ck, long long ldy, cudaStream_t stream, DeviceState *ds) {
+int launch_k8r3(const cim_half_tiles *H, const Chunks &ck, long long ldy, cudaStream_t stream, DeviceState *ds,
+                int n_pass = 1, long long xpass_bytes = 0) {
   static std::mutex attr_mu;
   static bool attr_done[64] = {};
   constexpr int SUBS = 3;
@@ -1524,11 +1543,13 @@ int launch_k8r3(const cim_half_tiles *H, const Chunks &ck, long long ldy, cudaSt
       attr_done[dev & 63] = true;
     }
   }
-  long long grid = std::min<long long>(ds->sms, (H->n_units + SUBS - 1) / SUBS);
+  long long grid = std::min<long long>(ds->sms, (H->n_units * n_pass + SUBS - 1) / SUBS);
   if (grid < 1) return CIM_OK;
   CounterLease lease;
   if (const int rc = lease.take(*ds->ring, stream, 1)) return rc;
   SpmmParams p;
+  p.n_pass = n_pass;
+  p.xpass_bytes = xpass_bytes;
   p.units = reinterpret_cast<const int4 *>(H->units);
   p.tile_rc = reinterpret_cast<const int2 *>(H->tile_rc);
   p.vals = reinterpret_cast<const unsigned char *>(H->vals);
@@ -1608,6 +1629,51 @@ int launch_k8_passes(const cim_half_tiles *H, const void *X, void *Y, int k, lon
   }
   const int rc2 = scratch_done(ds, stream);
   return rc ? rc : rc2;
+}
+
+// k = passes × KROW on the three-ring kernel in ONE launch: work items are
+// (unit, pass) pairs, the passes of a unit adjacent in the ticket order, so
+// a tile read from HBM by its first pass is still in L2 for the others.
+template <typename T, int KROW>
+int launch_k8r3_paired(const cim_half_tiles *H, const void *X, void *Y, int k, long long ldy, cudaStream_t stream,
+                       DeviceState *ds) {
+  const int passes = k / KROW;
+  const long long n_pad = (H->n + kBlock - 1) / kBlock * kBlock;
+  void *Xp = nullptr;
+  std::lock_guard<std::mutex> lk(g_scratch_mu);
+  int rc = scratch_begin(ds, stream, (size_t)n_pad * k * sizeof(T), &Xp);
+  if (rc) return rc;
+  const int row_chunks = k * (int)sizeof(T) / 16, w_chunks = KROW * (int)sizeof(T) / 16;
+  const long long total = n_pad * row_chunks;
+  pass_major_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 16LL * ds->sms), 256, 0, stream>>>(
+      static_cast<const uint4 *>(X), static_cast<uint4 *>(Xp), n_pad, row_chunks, w_chunks);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("pass_major_kernel: ") + cudaGetErrorString(e));
+  Chunks ck;
+  ck.x[0] = Xp;
+  ck.y[0] = Y;
+  rc = launch_k8r3<T, KROW>(H, ck, ldy, stream, ds, passes, n_pad * KROW * (long long)sizeof(T));
+  const int rc2 = scratch_done(ds, stream);
+  return rc ? rc : rc2;
+}
+
+// CIM_K8_PAIRED=0 keeps the per-pass launches (A/B).
+bool use_paired() {
+  static const bool v = [] {
+    const char *e = std::getenv("CIM_K8_PAIRED");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return v;
+}
+
+// CIM_K8_PAIRED_F64=1 runs f64 k > 4 as paired four-vector passes on the
+// three-ring kernel (A/B; off by default until measured faster).
+bool use_paired_f64() {
+  static const bool v = [] {
+    const char *e = std::getenv("CIM_K8_PAIRED_F64");
+    return e && std::atoi(e) == 1;
+  }();
+  return v;
 }
 
 // The wide-register kernel for (dtype, k), or EUNSUPPORTED.
@@ -1717,6 +1783,10 @@ static int sym_spmm_dense(const cim_half_tiles *H, const void *X, void *Y, int32
   if (H->layout == CIM_LAYOUT_FRAG && wide_supported(H->dtype, k)) {
 #ifndef CIM_K8_ROW_PASSES
     // multi-pass widths: one W-wide apply per pass on a pass-major copy of X
+    if (H->dtype == CIM_F32 && k > 8 && k % 8 == 0 && use_r3() && use_paired())
+      return launch_k8r3_paired<float, 8>(H, X, Y, k, ldy, stream, ds);
+    if (H->dtype == CIM_F64 && k > 4 && k % 4 == 0 && use_r3() && use_paired_f64())
+      return launch_k8r3_paired<double, 4>(H, X, Y, k, ldy, stream, ds);
     if (H->dtype == CIM_F32 && (k == 32 || k == 48 || k == 64)) return launch_k8_passes<float, 2>(H, X, Y, k, ldy, stream, ds);
     if (H->dtype == CIM_F32 && k == 24) return launch_k8_passes<float, 1>(H, X, Y, k, ldy, stream, ds);
     if (H->dtype == CIM_F64 && (k == 16 || k == 32)) return launch_k8_passes<double, 2>(H, X, Y, k, ldy, stream, ds);
