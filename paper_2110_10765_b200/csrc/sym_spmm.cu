@@ -841,7 +841,8 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
     unsigned char *stage_base = smem;
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)S * p.stage_bytes);
     uint64_t *empty = full + S;
-    const uint64_t pol_stream = policy_evict_first();
+    // paired passes (n_pass > 1) re-read each tile right away: keep it in L2
+    const uint64_t pol_stream = p.n_pass > 1 ? policy_evict_normal() : policy_evict_first();
 #ifdef CIM_K8_X_NORMAL
     const uint64_t pol_keep = policy_evict_normal();
 #else
@@ -850,13 +851,16 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
     int stage = 0;
     uint32_t phase = 0;
     unsigned int u = 0;
+    const long long n_items = p.n_units * p.n_pass;
     if (lane == 0) u = atomicAdd(p.counter, 1u);
     u = __shfl_sync(0xffffffffu, u, 0);
-    while ((long long)u < p.n_units) {
-      const int4 unit = p.units[u];
+    while ((long long)u < n_items) {
+      const unsigned int ui = u / (unsigned)p.n_pass, pass = u - ui * (unsigned)p.n_pass;
+      const int4 unit = p.units[ui];
       unsigned int u_next = 0;
       if (lane == 0) u_next = atomicAdd(p.counter, 1u);  // prefetch the next ticket
       const int R = unit.x, t0 = unit.y, t1 = unit.z;
+      const size_t xpo = (size_t)pass * (size_t)p.xpass_bytes;  // pass slice of X (paired passes: n_chunks = 1)
       for (int tb = t0; tb < t1; tb += 32) {
         const int t = tb + lane;
         const int myC = (t < t1) ? p.tile_rc[t].y : 0;
@@ -872,13 +876,14 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
             const int oc = C / p.chunk_blocks, lc = C - oc * p.chunk_blocks;
             const int orr = R / p.chunk_blocks, lr = R - orr * p.chunk_blocks;
             WideHdr *h = reinterpret_cast<WideHdr *>(st + tile_bytes + 2 * xblk);
-            *h = WideHdr{R, C, flags, 0, p.ych[orr] + (size_t)lr * ybytes, p.ych[oc] + (size_t)lc * ybytes};
+            *h = WideHdr{R, C, flags, (int)pass * KROW, p.ych[orr] + (size_t)lr * ybytes,
+                         p.ych[oc] + (size_t)lc * ybytes};
             const bool need_xr = first && !diag;  // a diagonal first tile has X_R = X_C
             mbar_arrive_expect_tx(&full[stage], tile_bytes + (need_xr ? 2 * xblk : xblk));
             bulk_g2s(st, p.vals + (size_t)tt * tile_bytes, tile_bytes, &full[stage], pol_stream);
-            bulk_g2s(st + tile_bytes, p.xch[oc] + (size_t)lc * xblk, xblk, &full[stage], pol_keep);
+            bulk_g2s(st + tile_bytes, p.xch[oc] + xpo + (size_t)lc * xblk, xblk, &full[stage], pol_keep);
             if (need_xr)
-              bulk_g2s(st + tile_bytes + xblk, p.xch[orr] + (size_t)lr * xblk, xblk, &full[stage], pol_keep);
+              bulk_g2s(st + tile_bytes + xblk, p.xch[orr] + xpo + (size_t)lr * xblk, xblk, &full[stage], pol_keep);
           }
           __syncwarp();
           if (++stage == S) {
@@ -987,7 +992,7 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
       phase ^= 1u;
     }
     // a diagonal tile's transposed FMAs (against X_R = X_C) are discarded
-    if (!diag) reduce_cols_wide<T>(ac, lane, cg, reinterpret_cast<T *>(h.yc) + v0, ldy, ypol);
+    if (!diag) reduce_cols_wide<T>(ac, lane, cg, reinterpret_cast<T *>(h.yc) + v0 + h.pad, ldy, ypol);
     if (h.flags & HDR_LAST) {
       // rows rg + 8i over the 4 lanes sharing them: 2 butterfly steps, then
       // each lane flushes 2 rows × VPG vectors (no cross-warp barrier)
@@ -1009,7 +1014,7 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
           ar[i][q] = W::add(keep, W::shfl_xor(send, 2));
         }
       const int i0 = (b0 ? 4 : 0) + (b1 ? 2 : 0);
-      T *yblk = reinterpret_cast<T *>(h.yr) + v0;
+      T *yblk = reinterpret_cast<T *>(h.yr) + v0 + h.pad;
 #pragma unroll
       for (int ri = 0; ri < 2; ++ri) {
         T *yr = yblk + (long long)(rg + 8 * (i0 + ri)) * ldy;
@@ -1454,7 +1459,8 @@ struct Chunks {  // X / Y as per-rank chunks (cim_sym_spmm_chunked); n = 1: plai
 };
 
 template <typename T, int G, int KROW>
-int launch_k8(const cim_half_tiles *H, const Chunks &ck, long long ldy, cudaStream_t stream, DeviceState *ds) {
+int launch_k8(const cim_half_tiles *H, const Chunks &ck, long long ldy, cudaStream_t stream, DeviceState *ds,
+              int n_pass = 1, long long xpass_bytes = 0) {
   static std::mutex attr_mu;
   static bool attr_done[64] = {};
   constexpr int SUBS = 2 / G;
@@ -1480,7 +1486,7 @@ int launch_k8(const cim_half_tiles *H, const Chunks &ck, long long ldy, cudaStre
       attr_done[dev & 63] = true;
     }
   }
-  long long grid = std::min<long long>(ds->sms, (H->n_units + SUBS - 1) / SUBS);
+  long long grid = std::min<long long>(ds->sms, (H->n_units * n_pass + SUBS - 1) / SUBS);
   if (grid < 1) return CIM_OK;
   CounterLease lease;
   if (const int rc = lease.take(*ds->ring, stream, passes)) return rc;
@@ -1504,8 +1510,8 @@ int launch_k8(const cim_half_tiles *H, const Chunks &ck, long long ldy, cudaStre
     p.sub_bytes = (unsigned int)sub_bytes;
     p.n_chunks = ck.n;
     p.chunk_blocks = ck.blocks;
-    p.n_pass = 1;
-    p.xpass_bytes = 0;
+    p.n_pass = n_pass;
+    p.xpass_bytes = xpass_bytes;
     for (int c = 0; c < kMaxChunks; ++c) {
       p.xch[c] = reinterpret_cast<const unsigned char *>(ck.x[c < ck.n ? c : 0]);
       p.ych[c] = reinterpret_cast<unsigned char *>(ck.y[c < ck.n ? c : 0]);
@@ -1577,6 +1583,15 @@ int launch_k8r3(const cim_half_tiles *H, const Chunks &ck, long long ldy, cudaSt
   return CIM_OK;
 }
 
+// CIM_K8_PAIRED=0 keeps one launch per pass for multi-pass widths (A/B).
+bool use_paired() {
+  static const bool v = [] {
+    const char *e = std::getenv("CIM_K8_PAIRED");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return v;
+}
+
 // CIM_K8_RINGS=2 selects the two-ring kernel for the one-warpgroup widths
 // (A/B); the three-ring kernel is the default.
 bool use_r3() {
@@ -1621,11 +1636,18 @@ int launch_k8_passes(const cim_half_tiles *H, const void *X, void *Y, int k, lon
       static_cast<const uint4 *>(X), static_cast<uint4 *>(Xp), n_pad, row_chunks, w_chunks);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("pass_major_kernel: ") + cudaGetErrorString(e));
-  for (int ps = 0; ps < passes && rc == CIM_OK; ++ps) {
+  if (use_paired()) {  // one launch, a unit's passes adjacent in the ticket order (tiles hit L2)
     Chunks ck;
-    ck.x[0] = static_cast<const T *>(Xp) + (size_t)ps * n_pad * W;
-    ck.y[0] = static_cast<T *>(Y) + ps * W;
-    rc = launch_k8<T, G, W>(H, ck, ldy, stream, ds);
+    ck.x[0] = Xp;
+    ck.y[0] = Y;
+    rc = launch_k8<T, G, W>(H, ck, ldy, stream, ds, passes, n_pad * W * (long long)sizeof(T));
+  } else {
+    for (int ps = 0; ps < passes && rc == CIM_OK; ++ps) {
+      Chunks ck;
+      ck.x[0] = static_cast<const T *>(Xp) + (size_t)ps * n_pad * W;
+      ck.y[0] = static_cast<T *>(Y) + ps * W;
+      rc = launch_k8<T, G, W>(H, ck, ldy, stream, ds);
+    }
   }
   const int rc2 = scratch_done(ds, stream);
   return rc ? rc : rc2;
@@ -1655,15 +1677,6 @@ int launch_k8r3_paired(const cim_half_tiles *H, const void *X, void *Y, int k, l
   rc = launch_k8r3<T, KROW>(H, ck, ldy, stream, ds, passes, n_pad * KROW * (long long)sizeof(T));
   const int rc2 = scratch_done(ds, stream);
   return rc ? rc : rc2;
-}
-
-// CIM_K8_PAIRED=0 keeps the per-pass launches (A/B).
-bool use_paired() {
-  static const bool v = [] {
-    const char *e = std::getenv("CIM_K8_PAIRED");
-    return !(e && std::atoi(e) == 0);
-  }();
-  return v;
 }
 
 // CIM_K8_PAIRED_F64=1 runs f64 k > 4 as paired four-vector passes on the
