@@ -14,7 +14,7 @@
  * interface it replaces.  No torch types appear here: every buffer is a plain
  * device (or host, where stated) pointer plus sizes, owned by the caller.
  *
- * Storage ("HalfTiles", fragment layout v2)
+ * Storage ("HalfTiles", fragment layout v1)
  * -----------------------------------------
  *   tile_rc  int32 [n_tiles][2]  (R, C) with R ≤ C, sorted by R then C,
  *                                unique.  Replaces SparseSkeleton.tiles +
@@ -26,12 +26,10 @@
  *   vals     f32|f64 [n_tiles][4096] in fragment order: for tile t,
  *                                micro-row i∈[0,8), micro-block mb∈[0,128),
  *                                column slot j∈[0,4):
- *                                  vals[t][i][mb][j] = T[rg + 8i][cg + 16·(j ^ (rg & 3))]
+ *                                  vals[t][i][mb][j] = T[rg + 8i][cg + 16j]
  *                                with rg = (mb & 31) >> 2,
  *                                     cg = 4·(mb >> 5) + (mb & 3).
  *                                (f64: vals[t][i][h][mb][jj] with j = 2h+jj.)
- *                                The per-row-group slot permutation makes
- *                                the kernels' column butterflies select-free.
  *                                Rows/cols ≥ n inside the last block are 0.
  *
  * Vectors: X and Y are row-major (n_pad, k) with n_pad = 64·ceil(n/64).
@@ -89,7 +87,7 @@ extern "C" {
 #define CIM_BLOCK 64
 
 /* tile value layouts (cim_half_tiles.layout) */
-#define CIM_LAYOUT_FRAG 0   /* fragment order v2: CUDA-core FFMA/FFMA2 kernels (f32, f64)  */
+#define CIM_LAYOUT_FRAG 0   /* fragment order v1: CUDA-core FFMA/FFMA2 kernel (f32, f64)   */
 #define CIM_LAYOUT_TC   1   /* tcgen05 TF32 operand layout (f32 only): per tile,
                                byte(r,c) = (c/32)·8192 + (r/4)·512 + s((r%4)·128 + (c%32)·4),
                                s(x) = x ^ (((x >> 7) & 3) << 5)  (SWIZZLE_128B_BASE32B)      */

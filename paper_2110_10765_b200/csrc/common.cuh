@@ -12,29 +12,23 @@ constexpr int kGroupThreads = 128;  // consumer threads per group = micro-blocks
 constexpr int kSpPtrStride = 72;    // uint16 row / column pointers per sparse tile (65 used; 144 B, 16-B aligned)
 
 // ---------------------------------------------------------------------------
-// Fragment layout v2 (include/cim_b200.h): micro-block mb ∈ [0,128) owns rows
-// rg + 8i (i < 8) and columns cg + 16j (j < 4); its column SLOT s holds
-// column cg + 16·(s ^ frag_jp(mb)), frag_jp = rg & 3.  The 8 lanes of a warp
-// that share a column group differ exactly in rg, and the per-tile column
-// butterfly exchanges slots over rg bit 1 then rg bit 0: with the slots
-// permuted by those bits every lane keeps slots {0, 1} and then slot 0, so
-// the exchange needs no per-lane selects (v1, s = j, needed 24 SEL per tile).
+// Fragment layout v1 (include/cim_b200.h): micro-block mb ∈ [0,128) owns rows
+// rg + 8i (i < 8) and columns cg + 16j (j < 4).
 // ---------------------------------------------------------------------------
 __host__ __device__ __forceinline__ int frag_rg(int mb) { return (mb & 31) >> 2; }
 __host__ __device__ __forceinline__ int frag_cg(int mb) { return ((mb >> 5) << 2) | (mb & 3); }
-__host__ __device__ __forceinline__ int frag_jp(int rg) { return rg & 3; }
 
 // Element index inside a tile's fragment-ordered storage → (row, col).
 template <typename T>
 __host__ __device__ __forceinline__ void frag_index_to_rc(int idx, int &row, int &col) {
   if constexpr (sizeof(T) == 4) {
-    const int s = idx & 3, mb = (idx >> 2) & 127, i = idx >> 9;
+    const int j = idx & 3, mb = (idx >> 2) & 127, i = idx >> 9;
     row = frag_rg(mb) + 8 * i;
-    col = frag_cg(mb) + 16 * (s ^ frag_jp(frag_rg(mb)));
+    col = frag_cg(mb) + 16 * j;
   } else {
     const int jj = idx & 1, mb = (idx >> 1) & 127, h = (idx >> 8) & 1, i = idx >> 9;
     row = frag_rg(mb) + 8 * i;
-    col = frag_cg(mb) + 16 * ((2 * h + jj) ^ frag_jp(frag_rg(mb)));
+    col = frag_cg(mb) + 16 * (2 * h + jj);
   }
 }
 

@@ -24,11 +24,10 @@ namespace {
 constexpr int kDetThreads = 256;  // 64 rows × 4 vector groups
 constexpr int kDetMaxK = 64;
 
-// Storage index of tile element (r, c) in fragment layout v2 (include/cim_b200.h):
-// column c = cg + 16·jc sits in slot jc ^ frag_jp(rg).
+// Storage index of tile element (r, c) in fragment layout v1 (include/cim_b200.h).
 template <typename T>
 __device__ __forceinline__ int frag_index(int r, int c) {
-  const int rg = r & 7, i = r >> 3, cg = c & 15, j = (c >> 4) ^ frag_jp(rg);
+  const int rg = r & 7, i = r >> 3, cg = c & 15, j = c >> 4;
   const int mb = 32 * (cg >> 2) + 4 * rg + (cg & 3);
   if constexpr (sizeof(T) == 4)
     return (i * 128 + mb) * 4 + j;

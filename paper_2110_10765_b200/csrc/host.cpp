@@ -25,7 +25,7 @@ void clear_error() { g_last_error.clear(); }
 
 using cim::set_error;
 
-extern "C" const char *cim_version(void) { return "cim_b200 1.0 (sm_100a, fragment layout v2)"; }
+extern "C" const char *cim_version(void) { return "cim_b200 1.0 (sm_100a, fragment layout v1)"; }
 
 extern "C" const char *cim_last_error(void) { return cim::g_last_error.c_str(); }
 

@@ -8,7 +8,7 @@
 //   direct      acc_r[row][v] += T[row][col] · X_C[col][v]   (Y_R, block row)
 //   transposed  acc_c[col][v] += T[row][col] · X_R[row][v]   (Y_C, block col)
 //
-// Thread ↔ data map (fragment layout v2, include/cim_b200.h): consumer mb owns
+// Thread ↔ data map (fragment layout v1, include/cim_b200.h): consumer mb owns
 // rows rg+8i (i<8) and columns cg+16j (j<4) of every tile, so one LDS.128 per
 // micro-row feeds 4·2·KV FMAs with all operands in registers.
 //
@@ -164,9 +164,8 @@ __device__ __forceinline__ void tile_fma(const T *__restrict__ Ts, const T *__re
                                          const T *__restrict__ XR, int mb, int rg, int cg, int k, int v0,
                                          T (&acc_r)[8][KV], T (&acc_c)[4][KV]) {
   T xc[4][KV];
-  const int jp = frag_jp(rg);  // slot j holds column cg + 16·(j ^ jp)
 #pragma unroll
-  for (int j = 0; j < 4; ++j) load_vec<T, KV>(xc[j], XC + (cg + 16 * (j ^ jp)) * k + v0);
+  for (int j = 0; j < 4; ++j) load_vec<T, KV>(xc[j], XC + (cg + 16 * j) * k + v0);
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     T t[4];
@@ -246,9 +245,8 @@ __device__ __forceinline__ void tile_fma2(const float *__restrict__ Ts, const fl
                                           u64 (&ar)[8][KV / 2], u64 (&ac)[4][KV / 2]) {
   constexpr int P = KV / 2;
   u64 xc[4][P];
-  const int jp = frag_jp(rg);  // slot j holds column cg + 16·(j ^ jp)
 #pragma unroll
-  for (int j = 0; j < 4; ++j) load_pairs<P>(xc[j], XC + (cg + 16 * (j ^ jp)) * k + v0);
+  for (int j = 0; j < 4; ++j) load_pairs<P>(xc[j], XC + (cg + 16 * j) * k + v0);
   const int sw = xr_chunk_swap<KV>(rg);
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -310,45 +308,18 @@ __device__ __forceinline__ void reduce_cols(T (&acc)[4][KV], T *scr, int lane, i
   constexpr int C = Chunk<T>::N;
   constexpr int NCH = (4 * KV) / C;  // chunks per lane
   static_assert((4 * KV) % C == 0, "KV too small for chunking");
+  const T *flat = &acc[0][0];
   V *sv = reinterpret_cast<V *>(scr);
-  const int jp = frag_jp((lane >> 2) & 7);  // acc slot j holds column j ^ jp (layout v2)
   __syncwarp();
-  if constexpr (KV >= C) {
-    // a chunk lies inside one slot: move whole chunks to their column's place
 #pragma unroll
-    for (int q = 0; q < NCH; ++q) {
-      const int j = (q * C) / KV, vq = (q * C) % KV;
-      const T *f = &acc[j][vq];
-      V v;
-      if constexpr (C == 4) {
-        v = make_float4(f[0], f[1], f[2], f[3]);
-      } else {
-        v = make_double2(f[0], f[1]);
-      }
-      const int dq = ((j ^ jp) * KV + vq) / C;
-      sv[dq * 32 + (lane ^ ((dq & 1) << 2))] = v;
+  for (int q = 0; q < NCH; ++q) {
+    V v;
+    if constexpr (C == 4) {
+      v = make_float4(flat[4 * q], flat[4 * q + 1], flat[4 * q + 2], flat[4 * q + 3]);
+    } else {
+      v = make_double2(flat[2 * q], flat[2 * q + 1]);
     }
-  } else {
-    // several slots per chunk (KV < C): gather the columns in order
-    T col[4][KV];
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-#pragma unroll
-      for (int v = 0; v < KV; ++v) {
-        const int j = c ^ jp;
-        col[c][v] = j == 0 ? acc[0][v] : j == 1 ? acc[1][v] : j == 2 ? acc[2][v] : acc[3][v];
-      }
-    const T *flat = &col[0][0];
-#pragma unroll
-    for (int q = 0; q < NCH; ++q) {
-      V v;
-      if constexpr (C == 4) {
-        v = make_float4(flat[4 * q], flat[4 * q + 1], flat[4 * q + 2], flat[4 * q + 3]);
-      } else {
-        v = make_double2(flat[2 * q], flat[2 * q + 1]);
-      }
-      sv[q * 32 + (lane ^ ((q & 1) << 2))] = v;
-    }
+    sv[q * 32 + (lane ^ ((q & 1) << 2))] = v;
   }
   __syncwarp();
   if (lane < 4 * NCH) {
@@ -428,18 +399,25 @@ __device__ __forceinline__ void reduce_cols_shfl(const u64 (&ac)[4][4], int lane
   for (int j = 0; j < 4; ++j)
 #pragma unroll
     for (int q = 0; q < 2; ++q) a[j][q] = add2(ac[j][q], shfl_xor_u64(ac[j][q + 2], 16));
-  // layout v2: a partner's slots m + 2 hold the columns of my slots m (rg
-  // bit 1), then its slot 1 holds my slot 0's column (rg bit 0): keep the low
-  // slots, send the high ones — no selects
+  const bool b3 = lane & 8;
   u64 b[2][2];
 #pragma unroll
   for (int m = 0; m < 2; ++m)
 #pragma unroll
-    for (int q = 0; q < 2; ++q) b[m][q] = add2(a[m][q], shfl_xor_u64(a[m + 2][q], 8));
+    for (int q = 0; q < 2; ++q) {
+      const u64 send = b3 ? a[m][q] : a[m + 2][q];
+      const u64 keep = b3 ? a[m + 2][q] : a[m][q];
+      b[m][q] = add2(keep, shfl_xor_u64(send, 8));
+    }
+  const bool b2 = lane & 4;
   u64 c[2];
 #pragma unroll
-  for (int q = 0; q < 2; ++q) c[q] = add2(b[0][q], shfl_xor_u64(b[1][q], 4));
-  const int j = (lane >> 2) & 3, h = lane >> 4;  // slot 0's column: jp = rg & 3
+  for (int q = 0; q < 2; ++q) {
+    const u64 send = b2 ? b[0][q] : b[1][q];
+    const u64 keep = b2 ? b[1][q] : b[0][q];
+    c[q] = add2(keep, shfl_xor_u64(send, 4));
+  }
+  const int j = (lane >> 2) & 3, h = lane >> 4;
   float s0, s1, s2, s3;
   unpack2(c[0], s0, s1);
   unpack2(c[1], s2, s3);
@@ -797,16 +775,25 @@ __device__ __forceinline__ void reduce_cols_wide(const typename WideE<T>::E (&ac
   for (int j = 0; j < 4; ++j)
 #pragma unroll
     for (int q = 0; q < 2; ++q) a[j][q] = W::add(ac[j][q], W::shfl_xor(ac[j][q + 2], 16));
-  // layout v2 (frag_jp): keep the low slots, send the high ones — no selects
+  const bool b3 = lane & 8;
   E b[2][2];
 #pragma unroll
   for (int m = 0; m < 2; ++m)
 #pragma unroll
-    for (int q = 0; q < 2; ++q) b[m][q] = W::add(a[m][q], W::shfl_xor(a[m + 2][q], 8));
+    for (int q = 0; q < 2; ++q) {
+      const E send = b3 ? a[m][q] : a[m + 2][q];
+      const E keep = b3 ? a[m + 2][q] : a[m][q];
+      b[m][q] = W::add(keep, W::shfl_xor(send, 8));
+    }
+  const bool b2 = lane & 4;
   E c[2];
 #pragma unroll
-  for (int q = 0; q < 2; ++q) c[q] = W::add(b[0][q], W::shfl_xor(b[1][q], 4));
-  const int j = (lane >> 2) & 3, h = lane >> 4;  // slot 0's column: jp = rg & 3
+  for (int q = 0; q < 2; ++q) {
+    const E send = b2 ? b[0][q] : b[1][q];
+    const E keep = b2 ? b[1][q] : b[0][q];
+    c[q] = W::add(keep, W::shfl_xor(send, 4));
+  }
+  const int j = (lane >> 2) & 3, h = lane >> 4;
   W::flush(yblk + (long long)(cg + 16 * j) * ldy + (W::VPG / 2) * h, c[0], c[1], ypol);
 }
 
@@ -927,7 +914,6 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
   const int gt = threadIdx.x & 127;  // micro-block id
   const int rg = frag_rg(gt), cg = frag_cg(gt);
   const int sw = xr_chunk_swap<8>(rg);
-  const int jp = frag_jp(rg);  // X_C slot j = column cg + 16·(j ^ jp) (layout v2)
   const long long ldy = p.ldy;
 #ifdef CIM_K8_Y_LAST
   const uint64_t ypol = policy_evict_last();
@@ -975,7 +961,7 @@ __global__ void __launch_bounds__(kK8Threads, 1) sym_spmm_k8_kernel(const SpmmPa
     E xc[4][4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const unsigned char *row = reinterpret_cast<const unsigned char *>(XC + (cg + 16 * (j ^ jp)) * K + v0);
+      const unsigned char *row = reinterpret_cast<const unsigned char *>(XC + (cg + 16 * j) * K + v0);
       const ulonglong2 a = *reinterpret_cast<const ulonglong2 *>(row);
       const ulonglong2 b = *reinterpret_cast<const ulonglong2 *>(row + 16);
       xc[j][0] = W::from_bits(a.x);
@@ -1181,7 +1167,6 @@ __global__ void __launch_bounds__(kR3Threads, 1) sym_spmm_k8r3_kernel(const Spmm
   const int gt = threadIdx.x & 127;
   const int rg = frag_rg(gt), cg = frag_cg(gt);
   const int sw = xr_chunk_swap<8>(rg);
-  const int jp = frag_jp(rg);  // X_C slot j = column cg + 16·(j ^ jp) (layout v2)
   const long long ldy = p.ldy;
   const uint64_t ypol = policy_evict_normal();
 
@@ -1214,7 +1199,7 @@ __global__ void __launch_bounds__(kR3Threads, 1) sym_spmm_k8r3_kernel(const Spmm
     E xc[4][4], ac[4][4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const unsigned char *row = reinterpret_cast<const unsigned char *>(XC + (cg + 16 * (j ^ jp)) * K + v0);
+      const unsigned char *row = reinterpret_cast<const unsigned char *>(XC + (cg + 16 * j) * K + v0);
       const ulonglong2 a = *reinterpret_cast<const ulonglong2 *>(row);
       const ulonglong2 b = *reinterpret_cast<const ulonglong2 *>(row + 16);
       xc[j][0] = W::from_bits(a.x);

@@ -211,7 +211,7 @@ def fragment_pack_host(tiles: np.ndarray, layout: str = "frag") -> np.ndarray:
     rg = (mb & 31) >> 2
     cg = ((mb >> 5) << 2) | (mb & 3)
     row = rg + 8 * i
-    col = cg + 16 * (j ^ (rg & 3))  # layout v2: slot j holds column cg + 16·(j ^ (rg & 3))
+    col = cg + 16 * j
     return np.ascontiguousarray(tiles.reshape(T, 4096)[:, row * BLOCK + col])
 
 

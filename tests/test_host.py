@@ -152,14 +152,13 @@ def test_tc_map_matches_header_formula():
 def test_fragment_map_matches_header_formula():
     t = np.arange(4096, dtype=np.float32).reshape(1, 64, 64)
     f = fragment_pack_host(t)[0]
-    # layout v2: vals[t][i][mb][j] = T[rg + 8i][cg + 16·(j ^ (rg & 3))],
-    # rg=(mb&31)>>2, cg=4(mb>>5)+(mb&3)
+    # vals[t][i][mb][j] = T[rg + 8i][cg + 16j], rg=(mb&31)>>2, cg=4(mb>>5)+(mb&3)
     for i in (0, 3, 7):
         for mb in (0, 5, 37, 127):
             for j in range(4):
                 rg = (mb & 31) >> 2
                 cg = 4 * (mb >> 5) + (mb & 3)
-                assert f[(i * 128 + mb) * 4 + j] == t[0, rg + 8 * i, cg + 16 * (j ^ (rg & 3))]
+                assert f[(i * 128 + mb) * 4 + j] == t[0, rg + 8 * i, cg + 16 * j]
     assert np.array_equal(np.sort(f), np.arange(4096, dtype=np.float32))  # a permutation
     t64 = t.astype(np.float64)
     f64 = fragment_pack_host(t64)[0]
