@@ -276,15 +276,23 @@ def _check_workers(workers) -> None:
 def _tile_ranges(tiles, orbitals, transpose: bool) -> np.ndarray:
     """(T, 4) int32 (r0, r1, c0, c1) of each tile's orbitals, swapped for the
     transposed walk (pipeline.py:437-447)."""
-    orb_by_id = {o.id: (o.start, o.stop) for o in orbitals}
-    rows = np.empty((len(tiles), 4), dtype=np.int64)
-    for q, t in enumerate(tiles):
-        r = orb_by_id[t.row_orbital]
-        c = orb_by_id[t.col_orbital]
-        if transpose:
-            r, c = c, r
-        rows[q] = (r[0], r[1], c[0], c[1])
-    return rows
+    no, nt = len(orbitals), len(tiles)
+    ids = np.fromiter((o.id for o in orbitals), np.int64, no)
+    start = np.fromiter((o.start for o in orbitals), np.int64, no)
+    stop = np.fromiter((o.stop for o in orbitals), np.int64, no)
+    r = np.fromiter((t.row_orbital for t in tiles), np.int64, nt)
+    c = np.fromiter((t.col_orbital for t in tiles), np.int64, nt)
+    order = np.argsort(ids, kind="stable")
+    sid = ids[order]
+    pos_r = np.minimum(np.searchsorted(sid, r), max(no - 1, 0))
+    pos_c = np.minimum(np.searchsorted(sid, c), max(no - 1, 0))
+    if nt and (no == 0 or np.any(sid[pos_r] != r) or np.any(sid[pos_c] != c)):
+        bad = [int(x) for x in np.concatenate([r, c]) if no == 0 or x not in set(ids.tolist())][:1]
+        raise KeyError(bad[0] if bad else -1)  # the reference's orb_by_id lookup (pipeline.py:436-443)
+    ri, ci = order[pos_r], order[pos_c]
+    if transpose:
+        ri, ci = ci, ri
+    return np.stack([start[ri], stop[ri], start[ci], stop[ci]], axis=1)
 
 
 def _contract_tiles(tiles, orbitals, basis, rank, inputs: ObservablesInput, transpose: bool, exact: bool,
