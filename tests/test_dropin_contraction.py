@@ -109,6 +109,20 @@ def test_coefficient_basis_size_checked():  # test_pipeline.py:301-305 (raises b
         contract_observables(tiles, orbs, grouped, rank, inputs)
 
 
+def test_unknown_orbital_id_raises_keyerror():
+    """A Tile naming an orbital that is not in the list fails like the
+    reference's orb_by_id lookup (pipeline.py:436-443)."""
+    from paper_2110_10765_b200 import Tile
+    from paper_2110_10765_b200.observables import _tile_ranges
+
+    grouped, orbs, tiles, rank = small_problem(n=64)
+    with pytest.raises(KeyError):
+        _tile_ranges(list(tiles) + [Tile(10_000, orbs[0].id)], orbs, False)
+    r = _tile_ranges(tiles, orbs, True)
+    f = _tile_ranges(tiles, orbs, False)
+    assert np.array_equal(r[:, :2], f[:, 2:]) and np.array_equal(r[:, 2:], f[:, :2])
+
+
 def test_validation_order_and_messages():
     """pipeline.py:550-555: strategy first, then the coefficient size; then
     the worker count (resolve_workers, _util.py:41-42)."""

@@ -237,16 +237,18 @@ def _global_reference(pkg, kind, n):
     return merge_dense_sparse(pkg, D, H).export_dense()
 
 
-@pytest.mark.parametrize("kind,overlap", [("synthetic", False), ("synthetic", True), ("mixed", False),
-                                          ("mixed", True)])
-def test_sharded_cuda_two_ranks_one_gpu(pkg, kind, overlap):
-    """Two processes, one GPU, the product's default CUDA panel kernel: the
-    balanced partition, the exchange (host-staged under gloo) and — with
-    ``overlap`` — the column-group schedule with per-chunk reductions; the
-    assembled Y equals the f64 oracle of the global matrix."""
+@pytest.mark.parametrize("world,kind,overlap", [(2, "synthetic", False), (2, "synthetic", True), (2, "mixed", False),
+                                                (2, "mixed", True), (3, "synthetic", True), (3, "mixed", True),
+                                                (3, "mixed", False)])
+def test_sharded_cuda_ranks_one_gpu(pkg, world, kind, overlap):
+    """Two or three processes, one GPU, the product's default CUDA panel
+    kernels: the balanced partition (dense and mixed dense + sparse panels),
+    the exchange (host-staged under gloo) and — with ``overlap`` — the
+    column-group schedule with per-chunk reductions; the assembled Y equals
+    the f64 oracle of the global matrix."""
     import torch.multiprocessing as mp
 
-    world, n, k = 2, 3000, 8
+    n, k = 3000, 8
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
