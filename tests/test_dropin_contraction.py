@@ -266,3 +266,18 @@ def test_tile_subset_and_many_vectors(device):
     assert np.abs(got - want).max() <= contraction_tolerance(c, I.size)
     exact = contract_oracle(sub, orbs, grouped, rank, ObservablesInput(c=c, m_ops=10, seed=3))
     assert np.abs(exact - want).max() <= 1e-12 * max(1.0, np.abs(want).max())
+
+
+@gpu
+@pytest.mark.parametrize("name,n,seed,particles", [("p64", 64, 13, 6), ("p128", 128, 13, 6), ("p256", 256, 17, 8)])
+def test_pair_count_matches_reference(device, name, n, seed, particles):
+    """The device build of the fixture basis holds exactly the reference's
+    count_pairs(...).total interacting pairs (both triangles; the stand-in
+    count_pairs above returns the recorded number)."""
+    grouped, _ = group_orbitals(random_basis(n, particles, seed=seed), group_bits=int(CASES[f"{name}_group_bits"]))
+    H = pkg.HalfTiles.from_basis(grouped, rank=InteractionRank())
+    rc, tiles = H.export_dense()
+    nz = tiles != 0
+    per_tile = nz.reshape(nz.shape[0], -1).sum(1)
+    full = int(per_tile[rc[:, 0] == rc[:, 1]].sum() + 2 * per_tile[rc[:, 0] != rc[:, 1]].sum())
+    assert full == int(CASES[f"{name}_n_pairs"])
