@@ -722,9 +722,11 @@ def impl_ours(args):
                 + f", k={k}, values h(i XOR j; 0) on device, X ~ N(0,1)",
                 "n": n, "k": k, "stored_tiles": g_tiles, "stored_nnz": H.nnz_stored,
                 "parallelism": (f"row-block shard x{world}" + (" fused peer-memory apply" if S.fused else
-                                                                " NCCL all-gather + per-chunk reduce, overlapped "
-                                                                "with column-group kernels" if S.overlap else
-                                                                " NCCL all-gather/reduce-scatter"))
+                                                                f" {backend.upper()} all-gather + per-chunk reduce, "
+                                                                "overlapped with column-group kernels" if S.overlap else
+                                                                f" {backend.upper()} all-gather/reduce-scatter")
+                                + (" (gloo harness check: host-staged exchange, not a measurement)"
+                                   if backend == "gloo" else ""))
                 if world > 1 else "single GPU",
                 "layout": H.layout,
                 "bands": H.meta.get("bands", 1),
