@@ -190,7 +190,7 @@ def candidate_tiles(and_: np.ndarray, or_: np.ndarray, threshold: int) -> np.nda
 
 
 def from_basis(basis_or_occ, bits_lo=None, *, rank: int = 2, value_seed: int = 0, dtype=torch.float32,
-               device="cuda", dense_fill: float | None = None, max_unit: int = DEFAULT_MAX_UNIT,
+               device="cuda", dense_fill: float | None = None, max_unit: int | None = None,
                layout: str | None = None) -> HalfTiles:
     """The reference skeleton of ``basis`` (grouped order; rank-``rank``
     operator: pairs within 2·rank differences) as a HalfTiles, built on the

@@ -66,12 +66,27 @@ def _as_torch_dtype(dtype) -> torch.dtype:
     raise ValueError(f"dtype must be float32 or float64, got {dtype}")
 
 
-def plan_units(tile_rc: np.ndarray, nb: int, max_unit: int = DEFAULT_MAX_UNIT,
+SMALL_MATRIX_TILES = 32768  # below this many tiles the planner cuts finer units
+SMALL_MATRIX_MAX_UNIT = 4
+
+
+def auto_max_unit(n_tiles: int) -> int:
+    """Work-unit size for a matrix of n_tiles stored tiles: 32 tiles (one
+    direct-accumulator flush per unit) once there is enough work to fill
+    every ring; 4 for small matrices, which are latency-bound with a few
+    tiles per ring — C1 (6,268 tiles, L2 flushed): 41.0 → 34.9 µs
+    (`tools/c1_units.py`)."""
+    return DEFAULT_MAX_UNIT if n_tiles >= SMALL_MATRIX_TILES else SMALL_MATRIX_MAX_UNIT
+
+
+def plan_units(tile_rc: np.ndarray, nb: int, max_unit: int | None = DEFAULT_MAX_UNIT,
                band_cols: int | None = None) -> np.ndarray:
     """Work units (R, t0, t1, 0) via the native planner (validates tile order:
     (R, C) sorted, or (C // band_cols, R, C) when ``band_cols`` is given)."""
     rc = np.ascontiguousarray(tile_rc, dtype=np.int32)
     T = rc.shape[0]
+    if max_unit is None:
+        max_unit = auto_max_unit(T)
     out = np.zeros((max(T, 1), 4), dtype=np.int32)
     nu = ctypes.c_int64(0)
     check(lib().cim_plan_units_banded(rc.ctypes.data if T else None, T, nb, max_unit,
@@ -606,7 +621,7 @@ class HalfTiles:
 
     # ----------------------------------------------------------- constructors
     @classmethod
-    def _from_pattern(cls, n: int, tile_rc: np.ndarray, dtype, device, max_unit: int,
+    def _from_pattern(cls, n: int, tile_rc: np.ndarray, dtype, device, max_unit: int | None,
                       layout: str | None = None, bands: int | None = 1):
         """Empty tile storage for the pattern.  Returns (H, perm): tiles are
         stored in column-band order, ``perm[s]`` = input index of stored tile s."""
@@ -638,7 +653,7 @@ class HalfTiles:
     @classmethod
     def synthetic(cls, n: int, p: float | None = None, *, n_off: int | None = None, seed: int = 0,
                   value_seed: int = 0, values: str = "h_xor", op_k: int = 0, dtype=torch.float32,
-                  device="cuda", max_unit: int = DEFAULT_MAX_UNIT, tile_rc: np.ndarray | None = None,
+                  device="cuda", max_unit: int | None = None, tile_rc: np.ndarray | None = None,
                   layout: str | None = None, bands: int | None = 1) -> "HalfTiles":
         """Synthetic half-stored matrix (BASELINE.json configs).
 
@@ -725,7 +740,7 @@ class HalfTiles:
 
     @classmethod
     def from_dense_tiles(cls, n: int, tile_rc: np.ndarray, tiles, *, dtype=None, device="cuda",
-                         max_unit: int = DEFAULT_MAX_UNIT, layout: str | None = None,
+                         max_unit: int | None = None, layout: str | None = None,
                          bands: int | None = 1) -> "HalfTiles":
         """From row-major dense tiles (T,64,64) given in ``tile_rc`` order;
         repacked on the device (stored in column-band order)."""
@@ -746,7 +761,7 @@ class HalfTiles:
 
     @classmethod
     def from_coo(cls, n: int, i, j, v, *, dtype=torch.float32, device="cuda", check_symmetric: bool = True,
-                 max_unit: int = DEFAULT_MAX_UNIT, layout: str | None = None, bands: int | None = 1,
+                 max_unit: int | None = None, layout: str | None = None, bands: int | None = 1,
                  dense_fill: float | None = None) -> "HalfTiles":
         """From a full (both-triangle) symmetric COO, e.g. a reference skeleton.
 

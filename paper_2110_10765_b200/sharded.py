@@ -197,7 +197,7 @@ class ShardedSymSpmm:
     # ------------------------------------------------------------------ build
     @classmethod
     def synthetic(cls, n: int, *, k: int, p: float | None = None, n_off: int | None = None, seed: int = 0,
-                  value_seed: int = 0, dtype=torch.float32, device=None, group=None, max_unit: int = 32,
+                  value_seed: int = 0, dtype=torch.float32, device=None, group=None, max_unit: int | None = None,
                   values: str = "h_xor", layout: str | None = None, bands: int | None = 1,
                   fused: bool = False, overlap: bool = False) -> "ShardedSymSpmm":
         """Every rank draws the same global tile pattern (seeded), keeps its
@@ -209,8 +209,12 @@ class ShardedSymSpmm:
             n_pairs = nb * (nb - 1) // 2
             p = 0.0 if n_pairs == 0 else float(n_off or 0) / n_pairs
         rc = synthetic_pattern(nb, p, seed)
-        units = plan_units(rc, nb, max_unit)
+        units = plan_units(rc, nb, max_unit)  # None: sized for the global tile count
         _, _, t0, t1 = shard_tile_range(units, world, rank)
+        if max_unit is None:
+            from .halftiles import auto_max_unit
+
+            max_unit = auto_max_unit(rc.shape[0])
         device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         H = HalfTiles.synthetic(n, tile_rc=rc[t0:t1], value_seed=value_seed, values=values, dtype=dtype,
                                 device=device, max_unit=max_unit, layout=layout, bands=bands)
