@@ -146,6 +146,8 @@ typedef struct cim_sparse_tiles {
   const void     *csr_val;
   int64_t         csr_rows;
   int64_t         csr_nnz;
+  int64_t         csr_all;   /* 1: the CSR holds the staged tiles too (the
+                                staged kernel is skipped by the SpMM) */
 } cim_sparse_tiles;
 
 typedef struct cim_half_tiles {

@@ -89,6 +89,7 @@ class CimSparseTiles(ctypes.Structure):
         ("csr_val", ctypes.c_void_p),
         ("csr_rows", ctypes.c_int64),
         ("csr_nnz", ctypes.c_int64),
+        ("csr_all", ctypes.c_int64),
     ]
 
 

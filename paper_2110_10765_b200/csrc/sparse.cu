@@ -601,7 +601,8 @@ int launch_sparse(const cim_sparse_tiles *S, const void *X, void *Y, int k, long
           cudaSuccess ||
       occ < 1)
     occ = 1;
-  const long long n_ring = listed ? p.n_staged : S->n_tiles;
+  const bool csr = S->csr_ptr && S->csr_rows > 0;
+  const long long n_ring = (csr && S->csr_all) ? 0 : listed ? p.n_staged : S->n_tiles;
   if (n_ring > 0) {
     const long long grid = std::min<long long>(n_ring, (long long)st->sms * occ);
     sparse_spmm_kernel<T, KV><<<(unsigned)grid, kSpConsumers + 32, smem, stream>>>(p, stages);

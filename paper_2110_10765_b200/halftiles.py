@@ -308,6 +308,15 @@ class SparseTiles:
                            int(ne[staged].max()) if staged.size else 0)
         return self._split[0][: self._split[1]], self._split[2][: self._split[3]]
 
+    def _small_dominated(self) -> bool:
+        """Do small tiles hold at least half the (padded) sparse entries?  The
+        row-CSR then takes every sparse tile (basis skeletons); matrices of
+        mostly staged tiles keep the shared-memory ring."""
+        ne = np.diff(self.entry_off_host)
+        _, n_st, sm, n_sm, _ = self._split
+        small_entries = int(ne[sm[:n_sm].cpu().numpy()].sum()) if n_sm else 0
+        return 2 * small_entries >= int(ne.sum())
+
     def build_csr(self, n_pad: int):
         """The row-CSR of the small tiles on the device (cim_sparse_csr_count →
         cim_exclusive_scan_i64 → cim_sparse_csr_fill): (csr_ptr int64
@@ -321,6 +330,12 @@ class SparseTiles:
         L = lib()
         stream = torch.cuda.current_stream(dev).cuda_stream
         base = self._base_descriptor()
+        # the CSR takes every non-empty tile (staged ones too): on basis
+        # skeletons one row walk is faster than the row walk + the staged ring
+        # (n = 262,144: 0.739 → 0.716 ms)
+        allt = np.sort(np.concatenate([st[:n_st].cpu().numpy(), sm[:n_sm].cpu().numpy()])).astype(np.int32)
+        all_dev = torch.from_numpy(allt if allt.size else np.zeros(1, np.int32)).to(dev)
+        base.small_tiles, base.n_small = all_dev.data_ptr(), int(allt.size)
         cnt = torch.empty(max(n_pad, 1), dtype=torch.int64, device=dev)
         with torch.cuda.device(dev):
             check(L.cim_sparse_csr_count(ctypes.byref(base), n_pad, cnt.data_ptr(), stream), "cim_sparse_csr_count")
@@ -336,7 +351,7 @@ class SparseTiles:
             return None
         col = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
         val = torch.empty(max(nnz, 1), dtype=self.vals.dtype, device=dev)
-        small = sm[:n_sm].cpu().numpy() if n_sm else np.zeros(0, np.int32)
+        small = allt
         R = self.tile_rc_host[small, 0] if small.size else np.zeros(0, np.int32)
         if R.size and np.any(np.diff(R) < 0):
             raise ValueError("small-tile list must be grouped by block row")
@@ -350,6 +365,7 @@ class SparseTiles:
                                         panel_R.data_ptr(), panel_ptr.data_ptr(), int(starts.size), ptr.data_ptr(),
                                         col.data_ptr(), val.data_ptr(), stream), "cim_sparse_csr_fill")
         self._csr = (ptr, col, val, nnz, int(n_pad))
+        self._csr_list = all_dev  # keeps the merged list alive for the fill
         self._desc = None
         return self._csr
 
@@ -373,12 +389,15 @@ class SparseTiles:
                                   and self._split is not None and self._split[3] > 0):
             self.work_split()
             if n_pad is not None and self.use_csr and self._csr is None and self._split[3] > 0:
-                self.build_csr(n_pad)
+                if self._small_dominated():
+                    self.build_csr(n_pad)
+                else:  # mostly staged tiles: the shared-memory ring is the faster walk for them
+                    self.use_csr = False
             d = self._base_descriptor()
             if self.use_csr and self._csr is not None:
                 ptr, col, val, nnz, rows = self._csr
                 d.csr_ptr, d.csr_col, d.csr_val = ptr.data_ptr(), col.data_ptr(), val.data_ptr()
-                d.csr_rows, d.csr_nnz = rows, nnz
+                d.csr_rows, d.csr_nnz, d.csr_all = rows, nnz, 1
             self._desc = d
         return self._desc
 
