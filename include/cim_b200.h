@@ -88,9 +88,9 @@ extern "C" {
 
 /* tile value layouts (cim_half_tiles.layout) */
 #define CIM_LAYOUT_FRAG 0   /* fragment order v1: CUDA-core FFMA/FFMA2 kernel (f32, f64)   */
-#define CIM_LAYOUT_TC   1   /* tcgen05 TF32 operand layout (f32 only): per tile,
-                               byte(r,c) = (c/32)·8192 + (r/4)·512 + s((r%4)·128 + (c%32)·4),
-                               s(x) = x ^ (((x >> 7) & 3) << 5)  (SWIZZLE_128B_BASE32B)      */
+#define CIM_LAYOUT_TC   1   /* tcgen05 split-TF32 kernel layout (f32 only): per tile, row-major
+                               rows of 256 B with the 16-byte chunks XOR-swizzled by row:
+                               byte(r,c) = r·256 + ((c/4 ^ r%8)·16) + (c%4)·4             */
 
 /*
  * Sparse ("COO-in-tile") stored tiles, for 64-tiles below the dense
@@ -378,7 +378,7 @@ CIM_API int cim_sym_spmm_chunked(const cim_half_tiles *H, const void *const *X_c
 CIM_API int cim_sym_spmm_supported(int32_t dtype, int32_t k);
 
 /* 1 if (layout, dtype, k) has a compiled kernel, else 0.  CIM_LAYOUT_TC:
- * f32 with k ∈ {8, 16} (tcgen05 kind::tf32, 3×TF32-split FP32 accuracy). */
+ * f32 with k ∈ {8, 16, …, 64} (tcgen05 kind::tf32, 3×TF32-split FP32 accuracy). */
 CIM_API int cim_layout_supports(int32_t layout, int32_t dtype, int32_t k);
 
 /*

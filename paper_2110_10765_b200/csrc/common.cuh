@@ -32,15 +32,18 @@ __host__ __device__ __forceinline__ void frag_index_to_rc(int idx, int &row, int
   }
 }
 
-// TC layout (CIM_LAYOUT_TC, f32): element index → (row, col); the inverse of
-// byte(r,c) = (c/32)·8192 + (r/4)·512 + s((r%4)·128 + (c%32)·4).
+// TC layout (CIM_LAYOUT_TC, f32): row-major rows of 256 B whose 16-byte
+// chunks are XOR-swizzled by the row: byte(r,c) = r·256 + ((c/4 ^ r%8)·16) +
+// (c%4)·4.  Row r read as 16-byte chunks by 32 threads (one row each) and
+// one row read as words by 32 threads (one column each) are both
+// bank-conflict-free — the two access patterns of the split-TF32 kernel.
+__host__ __device__ __forceinline__ int tc_byte(int row, int col) {
+  return row * 256 + ((((col >> 2) ^ (row & 7)) & 15) << 4) + (col & 3) * 4;
+}
 __host__ __device__ __forceinline__ void tc_index_to_rc(int idx, int &row, int &col) {
-  const unsigned b = (unsigned)idx * 4u;
-  const unsigned cb = b >> 13, rem = b & 8191u;
-  unsigned in = rem & 511u;
-  in ^= ((in >> 7) & 3u) << 5;
-  row = (int)((rem >> 9) * 4u + (in >> 7));
-  col = (int)(cb * 32u + ((in & 127u) >> 2));
+  row = idx >> 6;
+  const int pc = (idx >> 2) & 15;
+  col = ((pc ^ (row & 7)) << 2) | (idx & 3);
 }
 
 template <typename T>

@@ -1735,7 +1735,7 @@ extern "C" int cim_sym_spmm_supported(int32_t dtype, int32_t k) {
 
 extern "C" int cim_layout_supports(int32_t layout, int32_t dtype, int32_t k) {
   if (layout == CIM_LAYOUT_FRAG) return cim_sym_spmm_supported(dtype, k);
-  if (layout == CIM_LAYOUT_TC) return (dtype == CIM_F32 && (k == 8 || k == 16)) ? 1 : 0;
+  if (layout == CIM_LAYOUT_TC) return (dtype == CIM_F32 && k >= 8 && k <= 64 && k % 8 == 0) ? 1 : 0;
   return 0;
 }
 

@@ -193,15 +193,11 @@ def synthetic_pattern(nb: int, p: float, seed: int = 0) -> np.ndarray:
 
 def tc_index_map() -> np.ndarray:
     """For the TC layout: flat storage index e → row-major index r·64+c
-    (include/cim_b200.h CIM_LAYOUT_TC)."""
+    (include/cim_b200.h CIM_LAYOUT_TC: rows of 256 B, 16-byte chunks
+    XOR-swizzled by row % 8)."""
     e = np.arange(4096)
-    b = e * 4
-    cb = b >> 13
-    rem = b & 8191
-    inn = rem & 511
-    inn = inn ^ (((inn >> 7) & 3) << 5)
-    row = (rem >> 9) * 4 + (inn >> 7)
-    col = cb * 32 + ((inn & 127) >> 2)
+    row = e >> 6
+    col = (((e >> 2) & 15) ^ (row & 7)) * 4 + (e & 3)
     return row * BLOCK + col
 
 

@@ -32,12 +32,12 @@ def supported_k(dtype: torch.dtype, k: int, layout: str = "frag") -> bool:
     return bool(lib().cim_layout_supports(LAYOUTS[layout], code, int(k)))
 
 
-TC_MAX_K = 16  # vectors per tensor-core pass (N = 2k ≤ 32 TMEM columns per accumulator)
+TC_MAX_K = 64  # vectors per tensor-core apply (N = 2k ≤ 128 TMEM columns per accumulator)
 
 
 def padded_k(dtype: torch.dtype, k: int, layout: str = "frag") -> int:
     """Smallest compiled vector count ≥ k for the layout (extra columns are zero).
-    The tensor-core layout runs k > 16 as passes of 16 vectors."""
+    The tensor-core layout takes multiples of 8 up to 64."""
     kk = int(k)
     if layout == "tc" and kk > TC_MAX_K:
         return -(-kk // TC_MAX_K) * TC_MAX_K
