@@ -81,7 +81,8 @@ def test_supported_k_table():
     assert pkg.padded_k(torch.float64, 12) == 12
     assert pkg.padded_k(torch.float32, 3, "tc") == 8
     assert pkg.padded_k(torch.float32, 9, "tc") == 16
-    assert pkg.padded_k(torch.float32, 24, "tc") == 32
+    assert pkg.padded_k(torch.float32, 24, "tc") == 24
+    assert pkg.padded_k(torch.float32, 33, "tc") == 40
 
 
 class TestPlanUnits:
