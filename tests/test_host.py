@@ -145,8 +145,7 @@ def test_tc_map_matches_header_formula():
     assert np.array_equal(np.sort(m), np.arange(4096))  # a permutation
     for r in (0, 3, 5, 63):
         for c in (0, 7, 31, 32, 63):
-            x = (r % 4) * 128 + (c % 32) * 4
-            byte = (c // 32) * 8192 + (r // 4) * 512 + (x ^ (((x >> 7) & 3) << 5))
+            byte = r * 256 + (((c // 4) ^ (r % 8)) * 16) + (c % 4) * 4
             assert m[byte // 4] == r * 64 + c
 
 
