@@ -54,7 +54,7 @@
 namespace cim {
 namespace tc {
 
-enum : int { HDR_FIRST = 1, HDR_LAST = 2, HDR_DIAG = 4, HDR_TERM = 8, HDR_TERM2 = 16 };
+enum : int { HDR_FIRST = 1, HDR_LAST = 2, HDR_DIAG = 4, HDR_TERM = 8, HDR_TERM2 = 16, HDR_XR = 32 };
 
 struct TcParams {
   const int4 *units;
@@ -75,6 +75,26 @@ struct TcParams {
   unsigned int off_bars;
   unsigned int off_tmem;
 };
+
+// Role timers (tools/tc_profile.py; compiled in only with -DCIM_TC_PROF): lane 0
+// of one warp per role accumulates clock64 deltas per slot.  Roles: 0 MMA
+// issuer, 1 splitter row warp, 2 splitter column warp, 3 epilogue direct
+// warp, 4 epilogue transposed warp.
+enum : int { P_WAIT0 = 0, P_WAIT1, P_WAIT2, P_WORK0, P_WORK1, P_WORK2, P_WORK3, P_TILES = 14, P_TOTAL = 15, P_SLOTS = 16 };
+constexpr int kProfRoles = 5, kProfCtas = 160;
+#ifdef CIM_TC_PROF
+__device__ unsigned long long g_prof[kProfCtas][kProfRoles][P_SLOTS];
+#define TPROF_DECL long long _pa[P_SLOTS] = {0}; long long _pt = clock64(); const long long _p0 = _pt
+#define TPROF(slot) do { const long long _n = clock64(); _pa[slot] += _n - _pt; _pt = _n; } while (0)
+#define TPROF_TILE() (_pa[P_TILES] += 1)
+#define TPROF_DUMP(role) do { if (lane == 0 && blockIdx.x < kProfCtas) { _pa[P_TOTAL] = clock64() - _p0; \
+    for (int _i = 0; _i < P_SLOTS; ++_i) g_prof[blockIdx.x][role][_i] = (unsigned long long)_pa[_i]; } } while (0)
+#else
+#define TPROF_DECL
+#define TPROF(slot)
+#define TPROF_TILE()
+#define TPROF_DUMP(role)
+#endif
 
 // ----------------------------------------------------------------------------
 // tcgen05 wrappers
@@ -130,6 +150,18 @@ __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.
 // lo(x) = x − (x with the low 13 mantissa bits cleared): exact in FP32
 __device__ __forceinline__ float lo_tf32(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
+// lo() of 16 words, two at a time (FADD2: x − trunc(x) per lane pair)
+__device__ __forceinline__ void lo16(const uint32_t (&hi)[16], uint32_t (&lo)[16]) {
+#pragma unroll
+  for (int e = 0; e < 16; e += 2) {
+    unsigned long long a, b, r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "r"(hi[e]), "r"(hi[e + 1]));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "r"(hi[e] & 0xFFFFE000u), "r"(hi[e + 1] & 0xFFFFE000u));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo[e]), "=r"(lo[e + 1]) : "l"(r));
+  }
+}
+
 // instruction descriptor: D f32, A/B tf32 (K-major), M = 128, N = 2·K
 template <int K>
 __host__ __device__ constexpr uint32_t idesc_tf32() {
@@ -155,26 +187,36 @@ __device__ __forceinline__ unsigned b_off(int n, int kk) {
 }
 
 // Build B = [X_C,hi | X_R,hi | X_C,lo | X_R,lo] (N = 4K rows, K-major) from
-// the staged row-major X blocks; t = 0..127.  A warp handles 32 (n, kk)
-// pairs per step: lane → (n % 8, kk % 4), so each store hits 32 banks.
+// the staged row-major X blocks (the X_R rows only when `with_r`: a B buffer
+// keeps the X_R part of the last block row it was built for); t = 0..127.
+// One item = (vector v, four K-values kk0..kk0+3): four word loads, one
+// 16-byte store of the hi values and one of the lo values.  Lanes take
+// consecutive v, so a warp's 16-byte stores land in 8 distinct bank groups
+// (4 wavefronts for 512 B, the minimum).
 template <int K>
 __device__ __forceinline__ void build_b(const float *__restrict__ Xc, const float *__restrict__ Xr,
-                                        unsigned char *B, int t, bool diag) {
-  const int lane = t & 31, w = t >> 5;
-  const int v8 = lane >> 2, kq = lane & 3;
-  constexpr int GROUPS = 16 * (K / 8);  // per source block: kk/4 ∈ [0,16) × v/8 ∈ [0, K/8)
+                                        unsigned char *B, int t, bool with_r) {
+  constexpr int ITEMS = 16 * K;  // per source block
 #pragma unroll
   for (int src = 0; src < 2; ++src) {
-    if (src == 1 && diag) break;
+    if (src == 1 && !with_r) break;
     const float *Xs = src ? Xr : Xc;
-#pragma unroll 4
-    for (int g = w; g < GROUPS; g += 4) {
-      const int kk = (g & 15) * 4 + kq;
-      const int v = (g >> 4) * 8 + v8;
-      const float x = Xs[kk * K + v];
+#pragma unroll
+    for (int e = t; e < ITEMS; e += 128) {
+      const int v = e % K, kk4 = e / K;
+      const float *x = Xs + (4 * kk4) * K + v;
+      float4 hi, lo;
+      hi.x = x[0];
+      hi.y = x[K];
+      hi.z = x[2 * K];
+      hi.w = x[3 * K];
+      lo.x = lo_tf32(hi.x);
+      lo.y = lo_tf32(hi.y);
+      lo.z = lo_tf32(hi.z);
+      lo.w = lo_tf32(hi.w);
       const int n = src * K + v;
-      *reinterpret_cast<float *>(B + b_off(n, kk)) = x;
-      *reinterpret_cast<float *>(B + b_off(n + 2 * K, kk)) = lo_tf32(x);
+      *reinterpret_cast<float4 *>(B + b_off(n, 4 * kk4)) = hi;
+      *reinterpret_cast<float4 *>(B + b_off(n + 2 * K, 4 * kk4)) = lo;
     }
   }
 }
@@ -238,6 +280,12 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
     int stage = 0;
     uint32_t phase = 0;
     unsigned int u = 0;
+    // B buffer j = (tile seq) % NA keeps the X_R part of the last non-diagonal
+    // tile built into it: X_R is staged and split only when that row changes
+    int xr_of[NA];
+#pragma unroll
+    for (int b = 0; b < NA; ++b) xr_of[b] = -1;
+    uint32_t seq = 0;
     if (lane == 0) u = atomicAdd(p.counter, 1u);
     u = __shfl_sync(0xffffffffu, u, 0);
     while ((long long)u < p.n_units) {
@@ -256,14 +304,25 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
             unsigned char *st = smem + (size_t)stage * SB;
             const int tt = tb + q;
             const bool diag = Cb == R;
-            const int flags = (tt == t0 ? HDR_FIRST : 0) | (tt == t1 - 1 ? HDR_LAST : 0) | (diag ? HDR_DIAG : 0);
+            const int jb = (int)(seq % NA);
+            int have = -1;
+#pragma unroll
+            for (int b = 0; b < NA; ++b) have = (b == jb) ? xr_of[b] : have;
+            const bool need_xr = !diag && have != R;
+            if (need_xr) {
+#pragma unroll
+              for (int b = 0; b < NA; ++b) xr_of[b] = (b == jb) ? R : xr_of[b];
+            }
+            const int flags = (tt == t0 ? HDR_FIRST : 0) | (tt == t1 - 1 ? HDR_LAST : 0) | (diag ? HDR_DIAG : 0) |
+                              (need_xr ? HDR_XR : 0);
             *reinterpret_cast<int4 *>(st + p.off_hdr) = make_int4(R, Cb, flags, 0);
-            mbar_arrive_expect_tx(&full[stage], 16384u + (diag ? xblk : 2u * xblk));
+            mbar_arrive_expect_tx(&full[stage], 16384u + (need_xr ? 2u * xblk : xblk));
             bulk_g2s(st, p.vals + (size_t)tt * 16384u, 16384u, &full[stage], pol_stream);
             bulk_g2s(st + p.off_xc, p.X + (size_t)Cb * xblk, xblk, &full[stage], pol_keep);
-            if (!diag) bulk_g2s(st + p.off_xr, p.X + (size_t)R * xblk, xblk, &full[stage], pol_keep);
+            if (need_xr) bulk_g2s(st + p.off_xr, p.X + (size_t)R * xblk, xblk, &full[stage], pol_keep);
           }
           __syncwarp();
+          ++seq;
           if (++stage == S) {
             stage = 0;
             phase ^= 1u;
@@ -290,12 +349,16 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
     constexpr uint32_t idesc = idesc_tf32<K>();
     const uint32_t b_base = smem_u32(smem + p.off_b);
     uint32_t t = 0;
+    TPROF_DECL;
     while (true) {
       const uint32_t j = t % NA, d = t % ND;
+      TPROF(P_WORK0);
       mbar_wait(&splitf[j], (t / NA) & 1u);
+      TPROF(P_WAIT0);
       tc_fence_after();
       const int4 h = hdrj[j];
       mbar_wait(&d_empty[d], ((t / ND) & 1u) ^ 1u);  // the epilogue has drained D_d (and read meta[d])
+      TPROF(P_WAIT1);
       tc_fence_after();
       if (elect_one()) {
         meta[d] = h;
@@ -308,6 +371,7 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
       const uint64_t bdesc_lo = sdesc(bh + (uint32_t)(N / 8) * 2048u, 128, 2048, 0);
       const uint32_t a = t_a + j * 128, dd = t_d + d * N;
       if (elect_one()) {
+#ifndef CIM_TC_NO_MMA
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
           // K step ks: 8 K-values = two core matrices along K (256 B → +16 in desc units)
@@ -315,12 +379,15 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
           mma_ts(dd, a + 64 + ks * 8, bdesc_hi + (uint64_t)(ks * 16), idesc, 1u);
           mma_ts(dd, a + ks * 8, bdesc_lo + (uint64_t)(ks * 16), idesc, 1u);
         }
+#endif
         tc_commit(&ab_empty[j]);
         tc_commit(&d_full[d]);
       }
       __syncwarp();
+      TPROF_TILE();
       ++t;
     }
+    TPROF_DUMP(0);
   } else if (warp >= 4 && warp < 12) {
     // =============================== splitters ===============================
     const int grp = (warp - 4) >> 2;  // group 0: tiles 0,2,4,…  group 1: tiles 1,3,5,…
@@ -336,13 +403,17 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
     uint32_t t = grp;
     int stage = grp % S;
     uint32_t phase = (uint32_t)(grp / S) & 1u;
+    TPROF_DECL;
     while (true) {
+      TPROF(P_WORK3);
       mbar_wait(&full[stage], phase);
+      TPROF(P_WAIT0);
       unsigned char *st = smem + (size_t)stage * SB;
       const int4 h = *reinterpret_cast<const int4 *>(st + p.off_hdr);
       const uint32_t j = t % NA;
       if (h.z & HDR_TERM2) break;
       mbar_wait(&ab_empty[j], ((t / NA) & 1u) ^ 1u);
+      TPROF(P_WAIT1);
       if (h.z & HDR_TERM) {
         if (t128 == 0) hdrj[j] = h;
         __syncwarp();
@@ -352,7 +423,11 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
       tc_fence_after();
       const bool diag = h.z & HDR_DIAG;
       const uint32_t a = t_a + j * 128 + lane_field;
+#ifndef CIM_TC_NO_ROWS
       if (m < 64) {
+#else
+      if (false) {
+#endif
         // row m: 16 chunks of 4 values, chunk j at (j ^ m%8)·16
         const unsigned char *row = st + m * 256;
 #pragma unroll
@@ -368,11 +443,16 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
             hi[4 * cc + 3] = __float_as_uint(v.w);
           }
 #pragma unroll
-          for (int e = 0; e < 16; ++e) lo[e] = __float_as_uint(lo_tf32(__uint_as_float(hi[e])));
+          lo16(hi, lo);
           tmem_st16(a + 16 * jj, hi);
           tmem_st16(a + 64 + 16 * jj, lo);
         }
-      } else if (!diag) {
+      }
+#ifndef CIM_TC_NO_COLS
+      else if (!diag) {
+#else
+      else if (false) {
+#endif
         // column c: one word per row; a warp reads 32 consecutive columns of one row
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
@@ -383,22 +463,28 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
             hi[rr] = *reinterpret_cast<const uint32_t *>(st + r * 256 + coff[r & 7]);
           }
 #pragma unroll
-          for (int e = 0; e < 16; ++e) lo[e] = __float_as_uint(lo_tf32(__uint_as_float(hi[e])));
+          lo16(hi, lo);
           tmem_st16(a + 16 * jj, hi);
           tmem_st16(a + 64 + 16 * jj, lo);
         }
       }
+      TPROF(P_WORK0);
+#ifndef CIM_TC_NO_BUILDB
       build_b<K>(reinterpret_cast<const float *>(st + p.off_xc), reinterpret_cast<const float *>(st + p.off_xr),
-                 smem + p.off_b + j * C::BBYTES, t128, diag);
+                 smem + p.off_b + j * C::BBYTES, t128, (h.z & HDR_XR) != 0);
+#endif
       if (t128 == 0) hdrj[j] = h;
       // stage consumed: the producer may refill it
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
+      TPROF(P_WORK1);
       tmem_wait_st();
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // B stores → async proxy (MMA)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&splitf[j]);
+      TPROF(P_WORK2);
+      TPROF_TILE();
       t += 2;
       stage += 2;
       if (stage >= S) {
@@ -406,6 +492,7 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
         phase ^= 1u;
       }
     }
+    if (grp == 0 && (q == 0 || q == 2)) TPROF_DUMP(q == 0 ? 1 : 2);
   } else if (warp >= 12) {
     // =============================== epilogue ================================
     const int q = warp & 3;
@@ -417,13 +504,17 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
 #pragma unroll
     for (int e = 0; e < K; ++e) acc[e] = 0.0f;
     uint32_t t = 0;
+    TPROF_DECL;
     while (true) {
       const uint32_t d = t % ND;
       const uint32_t ph = (t / ND) & 1u;
+      TPROF(P_WORK0);
       mbar_wait(&meta_f[d], ph);
+      TPROF(P_WAIT0);
       const int4 h = meta[d];
       if (h.z & HDR_TERM) break;
       mbar_wait(&d_full[d], ph);
+      TPROF(P_WAIT1);
       tc_fence_after();
       const bool diag = h.z & HDR_DIAG;
       const uint32_t dcol = t_d + d * N + lane_field;
@@ -444,7 +535,11 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&d_empty[d]);
+#ifndef CIM_TC_NO_RED
         if (h.z & HDR_LAST) {
+#else
+        if (false) {
+#endif
           float *yp = Y + ((long long)h.x * kBlock + m) * ldy;
 #pragma unroll
           for (int e = 0; e < K; e += 4) red_add_v4(yp + e, acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
@@ -458,18 +553,22 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
             uint32_t r8[8];
             tmem_ld8(dcol + K + 8 * cb, r8);
             tmem_wait_ld();
+#ifndef CIM_TC_NO_RED
             red_add_v4(yp + 8 * cb, __uint_as_float(r8[0]), __uint_as_float(r8[1]), __uint_as_float(r8[2]),
                        __uint_as_float(r8[3]));
             red_add_v4(yp + 8 * cb + 4, __uint_as_float(r8[4]), __uint_as_float(r8[5]), __uint_as_float(r8[6]),
                        __uint_as_float(r8[7]));
+#endif
           }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&d_empty[d]);
       }
+      TPROF_TILE();
       ++t;
     }
+    if (q == 0 || q == 2) TPROF_DUMP(q == 0 ? 3 : 4);
   }
   tc_fence_before();
   __syncthreads();
@@ -564,3 +663,18 @@ int sym_spmm_tc_dispatch(const cim_half_tiles *H, const void *X, void *Y, int k,
 }
 
 }  // namespace cim
+
+// Role timers of the last CIM_TC_PROF launch (tools/tc_profile.py): copies
+// [ctas][5 roles][16 slots] cycle counts; 0 when profiling is not compiled in.
+extern "C" CIM_API int cim_tc_profile_read(unsigned long long *host_out, int max_ctas) {
+#ifdef CIM_TC_PROF
+  const int n = max_ctas < cim::tc::kProfCtas ? max_ctas : cim::tc::kProfCtas;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(host_out, cim::tc::g_prof, (size_t)n * cim::tc::kProfRoles * cim::tc::P_SLOTS * 8);
+  return n;
+#else
+  (void)host_out;
+  (void)max_ctas;
+  return 0;
+#endif
+}
