@@ -88,18 +88,22 @@ def workload(args, world):
     return n, nb, n_off, p
 
 
-def kernel_label(dtype, k: int) -> str:
-    """The dense-tile kernel the library dispatches for (dtype, k) (pick_cfg in csrc/sym_spmm.cu)."""
-    if dtype == torch.float32 and k in (8, 16, 24, 32, 48, 64):  # wide_supported()
-        g = 2 if (k // 8) % 2 == 0 else 1
-        passes = k // (8 * g)
-        return (f"sym_spmm_k8_kernel<float, G={g}> (FFMA2, setmaxnreg warpgroups, X_R in registers"
-                + (f", {passes} passes" if passes > 1 else "") + ")")
-    if dtype == torch.float64 and k in (4, 8, 12, 16, 32):
+def kernel_label(dtype, k: int, layout: str = "frag") -> tuple[str, int]:
+    """(the dense-tile kernel the library dispatches for (dtype, k, layout),
+    our kernel launches per apply besides the Y memset) — the dispatch of
+    sym_spmm_dense in csrc/sym_spmm.cu."""
+    if layout == "tc":
+        return "sym_spmm_tc_kernel<%d> (tcgen05 kind::tf32, A = [T; Tᵀ] in TMEM, 3xTF32 along K)" % k, 1
+    if dtype == torch.float32 and k == 8:
+        return "sym_spmm_k8r3_kernel<float, 8> (FFMA2, three rings per CTA)", 1
+    if dtype == torch.float32 and k in (16, 24, 32, 48, 64):
+        return (f"sym_spmm_k8r3_kernel<float, 8> (FFMA2, {k // 8} paired passes) + pass_major_kernel", 2)
+    if dtype == torch.float64 and k in (4, 8):
+        return f"sym_spmm_k8_kernel<double, G={k // 4}> (DFMA, two rings)", 1
+    if dtype == torch.float64 and k in (12, 16, 32):
         g = 2 if (k // 4) % 2 == 0 else 1
-        passes = k // (4 * g)
-        return f"sym_spmm_k8_kernel<double, G={g}> (DFMA)" + (f", {passes} passes" if passes > 1 else "")
-    return "sym_spmm_kernel (FFMA/DFMA, shared-memory column reduction)"
+        return f"sym_spmm_k8_kernel<double, G={g}> (DFMA, {k // (4 * g)} paired passes) + pass_major_kernel", 2
+    return "sym_spmm_kernel (FFMA/DFMA, shared-memory column reduction)", 1
 
 
 def box_copy_gbs(dev, nbytes: int = 1 << 31, reps: int = 5) -> float:
@@ -741,9 +745,8 @@ def impl_ours(args):
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
-                         "kernel": "sym_spmm_tc_kernel (tcgen05 kind::tf32, 3xTF32 split)" if H.layout == "tc"
-                         else ("sparse_spmm_kernel + sparse_small_kernel (COO-in-tile)" if args.fill is not None else
-                               kernel_label(dtype, k)),
+                         "kernel": ("sparse_spmm_kernel + sparse_small_kernel (COO-in-tile)" if args.fill is not None
+                                    else kernel_label(dtype, k, H.layout)[0]),
                          "kernel_ms": kern_max,
                          "algorithmic_bytes_per_launch": bytes_local,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6650",
@@ -759,7 +762,7 @@ def impl_ours(args):
                                if t1 and "t1_ms" in t1 else t1),
             "gpu_launches": args.steps * (
                 (int(S.g_local is not None) + sum(g is not None for g in S.g_cols)) if S.overlap else
-                max(1, -(-S.k // 16)) if H.layout == "tc" else (1 if k <= 8 else max(1, k // 16))),
+                kernel_label(dtype, k, H.layout)[1]),
             "clocks": clocks.summary(),
         }
         print(json.dumps(line))
