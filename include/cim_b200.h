@@ -88,9 +88,9 @@ extern "C" {
 
 /* tile value layouts (cim_half_tiles.layout) */
 #define CIM_LAYOUT_FRAG 0   /* fragment order v1: CUDA-core FFMA/FFMA2 kernel (f32, f64)   */
-#define CIM_LAYOUT_TC   1   /* tcgen05 split-TF32 kernel layout (f32 only): per tile, row-major
-                               rows of 256 B with the 16-byte chunks XOR-swizzled by row:
-                               byte(r,c) = r·256 + ((c/4 ^ r%8)·16) + (c%4)·4             */
+#define CIM_LAYOUT_TC   1   /* tensor-core kernels' layout (f32: tcgen05 split-TF32, f64:
+                               DMMA): per tile, row-major rows whose 4-element chunks are
+                               XOR-swizzled by row: element(r,c) = r·64 + (c/4 ^ r%8)·4 + c%4 */
 
 /*
  * Sparse ("COO-in-tile") stored tiles, for 64-tiles below the dense
@@ -378,7 +378,8 @@ CIM_API int cim_sym_spmm_chunked(const cim_half_tiles *H, const void *const *X_c
 CIM_API int cim_sym_spmm_supported(int32_t dtype, int32_t k);
 
 /* 1 if (layout, dtype, k) has a compiled kernel, else 0.  CIM_LAYOUT_TC:
- * f32 with k ∈ {8, 16, …, 64} (tcgen05 kind::tf32, 3×TF32-split FP32 accuracy). */
+ * f32 with k ∈ {8, 16, …, 64} (tcgen05 kind::tf32, 3×TF32-split FP32 accuracy);
+ * f64 with k ∈ {8, 16, 24, 32} (mma.sync DMMA m8n8k4). */
 CIM_API int cim_layout_supports(int32_t layout, int32_t dtype, int32_t k);
 
 /*

@@ -48,7 +48,7 @@ __host__ __device__ __forceinline__ void tc_index_to_rc(int idx, int &row, int &
 
 template <typename T>
 __host__ __device__ __forceinline__ void layout_index_to_rc(int layout, int idx, int &row, int &col) {
-  if (sizeof(T) == 4 && layout == 1)
+  if (layout == 1)  // the same element map for f32 (16-byte chunks) and f64 (32-byte chunks)
     tc_index_to_rc(idx, row, col);
   else
     frag_index_to_rc<T>(idx, row, col);

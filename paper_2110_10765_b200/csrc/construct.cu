@@ -132,7 +132,7 @@ extern "C" int cim_basis_fill_dense(const uint64_t *bits_lo, const uint16_t *occ
   int rc = cim::check_basis(bits_lo, occ, n, n_particles, threshold);
   if (rc) return rc;
   if (dtype != CIM_F32 && dtype != CIM_F64) return cim::set_error(CIM_EINVAL, "dtype must be CIM_F32 or CIM_F64");
-  if (layout != CIM_LAYOUT_FRAG && !(layout == CIM_LAYOUT_TC && dtype == CIM_F32))
+  if (layout != CIM_LAYOUT_FRAG && layout != CIM_LAYOUT_TC)
     return cim::set_error(CIM_EINVAL, "unknown layout for dtype");
   if (n_tiles == 0) return CIM_OK;
   if (!tile_rc || !vals) return cim::set_error(CIM_EINVAL, "NULL tile arrays");

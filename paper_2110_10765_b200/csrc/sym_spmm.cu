@@ -1726,6 +1726,8 @@ using namespace cim;
 namespace cim {
 int sym_spmm_tc_dispatch(const cim_half_tiles *H, const void *X, void *Y, int k, long long ldy, cudaStream_t stream,
                          int sms, unsigned int *counter);
+int sym_spmm_dmma_dispatch(const cim_half_tiles *H, const void *X, void *Y, int k, long long ldy,
+                           cudaStream_t stream, int sms, unsigned int *counter);
 }
 
 extern "C" int cim_sym_spmm_supported(int32_t dtype, int32_t k) {
@@ -1735,7 +1737,10 @@ extern "C" int cim_sym_spmm_supported(int32_t dtype, int32_t k) {
 
 extern "C" int cim_layout_supports(int32_t layout, int32_t dtype, int32_t k) {
   if (layout == CIM_LAYOUT_FRAG) return cim_sym_spmm_supported(dtype, k);
-  if (layout == CIM_LAYOUT_TC) return (dtype == CIM_F32 && k >= 8 && k <= 64 && k % 8 == 0) ? 1 : 0;
+  if (layout == CIM_LAYOUT_TC) {
+    if (dtype == CIM_F32) return (k >= 8 && k <= 64 && k % 8 == 0) ? 1 : 0;
+    return (k >= 8 && k <= 32 && k % 8 == 0) ? 1 : 0;  // f64: DMMA kernel
+  }
   return 0;
 }
 
@@ -1789,6 +1794,7 @@ static int sym_spmm_dense(const cim_half_tiles *H, const void *X, void *Y, int32
     if ((reinterpret_cast<uintptr_t>(Y) & 15) || (ldy % 4)) return set_error(CIM_EINVAL, "TC path needs 16-B aligned Y rows");
     CounterLease lease;
     if (const int lrc = lease.take(*ds->ring, stream, 1)) return lrc;
+    if (H->dtype == CIM_F64) return sym_spmm_dmma_dispatch(H, X, Y, k, ldy, stream, ds->sms, lease.ctr);
     return sym_spmm_tc_dispatch(H, X, Y, k, ldy, stream, ds->sms, lease.ctr);
   }
 

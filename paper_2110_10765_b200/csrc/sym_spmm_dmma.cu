@@ -1,0 +1,311 @@
+// FP64 tensor-core (DMMA) half-stored symmetric SpMM
+//   Y = U·X + U_offᵀ·X          (f64 tiles and vectors, k ∈ {8, 16, 24, 32})
+//
+// The FP64 path of the tile layout CIM_LAYOUT_TC (row-major tiles whose
+// 4-element chunks are XOR-swizzled by row % 8 — 32-byte chunks for f64).
+// mma.sync m8n8k4 f64 (SASS DMMA.8x8x4) does 256 FMAs per warp instruction
+// against 32 for DFMA at the same FP64 peak on B200 (tools/dmma_probe.cu:
+// 37.1 TFLOP/s vs the measured DFMA 34.1), so the kernel is no longer bound
+// by issue slots and register-resident accumulators: the DFMA kernel ran the
+// compute-bound widths at ~42% of the FP64 pipe, shared-memory bound
+// (L1/TEX 94%: each warpgroup re-read the 32 KB tile per 4 vectors).
+//
+// Per stored tile (T, 64 × 64) and 8·NB vectors, consumer warp w (0..3):
+//   direct      rows 16w..16w+15:  D[r][v] += Σ_c T[r][c] · X_C[c][v]
+//               A = T (8×4 fragments, row-major), B = X_C (4×8, col-major)
+//   transposed  cols 16w..16w+15:  E[c][v]  = Σ_r T[r][c] · X_R[r][v]
+//               A = Tᵀ (the same smem tile read transposed), B = X_R
+// Each tile element is read from shared memory once per product for all k
+// vectors (the A fragment is reused across the NB column blocks).  D stays
+// in registers across the tiles of one block row (flushed with red.global
+// when the row changes), E is reduced into Y_C per tile.
+//
+// Roles (one CTA per SM, persistent): warp 8 is the producer (work units by
+// ticket, bulk copies of tile / X_C / X_R into an S-stage ring); warps 0-3
+// and 4-7 are two consumer groups taking alternate tiles.
+// The reference reaches this arithmetic only as its per-pair contraction
+// kernels (pipeline.py:461-531) over the COO of _collect_pairs (:428-458).
+#include <algorithm>
+#include <cstdlib>
+#include <cstdio>
+#include <mutex>
+#include <string>
+
+#include "cim_b200.h"
+#include "common.cuh"
+#include "host_util.h"
+
+namespace cim {
+namespace dmma {
+
+enum : int { HDR_DIAG = 4, HDR_TERM = 8 };
+
+struct DmParams {
+  const int4 *units;
+  const int2 *tile_rc;
+  const unsigned char *vals;
+  const unsigned char *X;
+  double *Y;
+  unsigned int *counter;
+  long long n_units;
+  long long ldy;
+  unsigned int stages, stage_bytes, xblk;
+  unsigned int off_xc, off_xr, off_hdr, off_bars;
+};
+
+constexpr int kTileBytes = 4096 * 8;
+constexpr int kThreads = 288;  // 2 consumer groups × 4 warps + 1 producer warp
+
+__device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int K>
+__global__ void __launch_bounds__(kThreads, 1) sym_spmm_dmma_kernel(const DmParams p) {
+  constexpr int NB = K / 8;  // 8-vector column blocks
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const int S = (int)p.stages;
+  const unsigned SB = p.stage_bytes;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + p.off_bars), *empty = full + S;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == 8) {
+    // ================================ producer ================================
+    const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
+    const unsigned xblk = p.xblk;
+    int stage = 0;
+    uint32_t phase = 0;
+    unsigned int u = 0;
+    if (lane == 0) u = atomicAdd(p.counter, 1u);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    while ((long long)u < p.n_units) {
+      const int4 unit = p.units[u];
+      unsigned int u_next = 0;
+      if (lane == 0) u_next = atomicAdd(p.counter, 1u);
+      const int R = unit.x, t0 = unit.y, t1 = unit.z;
+      for (int tb = t0; tb < t1; tb += 32) {
+        const int t = tb + lane;
+        const int myC = (t < t1) ? p.tile_rc[t].y : 0;
+        const int cnt = min(32, t1 - tb);
+        for (int q = 0; q < cnt; ++q) {
+          const int Cb = __shfl_sync(0xffffffffu, myC, q);
+          if (lane == 0) {
+            mbar_wait_backoff(&empty[stage], phase ^ 1u);
+            unsigned char *st = smem + (size_t)stage * SB;
+            const bool diag = Cb == R;
+            *reinterpret_cast<int4 *>(st + p.off_hdr) = make_int4(R, Cb, diag ? HDR_DIAG : 0, 0);
+            mbar_arrive_expect_tx(&full[stage], (unsigned)kTileBytes + (diag ? xblk : 2u * xblk));
+            bulk_g2s(st, p.vals + (size_t)(tb + q) * kTileBytes, kTileBytes, &full[stage], pol_stream);
+            bulk_g2s(st + p.off_xc, p.X + (size_t)Cb * xblk, xblk, &full[stage], pol_keep);
+            if (!diag) bulk_g2s(st + p.off_xr, p.X + (size_t)R * xblk, xblk, &full[stage], pol_keep);
+          }
+          __syncwarp();
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+      u = __shfl_sync(0xffffffffu, u_next, 0);
+    }
+    if (lane == 0)
+      for (int e = 0; e < 2; ++e) {  // one terminator per consumer group
+        mbar_wait_backoff(&empty[stage], phase ^ 1u);
+        *reinterpret_cast<int4 *>(smem + (size_t)stage * SB + p.off_hdr) = make_int4(0, 0, HDR_TERM, 0);
+        mbar_arrive(&full[stage]);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    return;
+  }
+  if (warp > 8) return;
+
+  // ============================== consumers ==============================
+  const int grp = warp >> 2, w = warp & 3;
+  const int g = lane >> 2, q4 = lane & 3;  // fragment row / column group of this lane
+  const long long ldy = p.ldy;
+  // direct A: row 16w + 8rb + g, chunk kb swizzled by g (= row % 8)
+  const unsigned a_dir = (unsigned)((16 * w + g) * 512 + q4 * 8 + (g << 5));
+  // transposed A: T[4kb + q4][16w + 8cb + g]; row % 8 = 4(kb&1) + q4, chunk 4w + 2cb + g/4
+  unsigned a_tr[2][2];
+#pragma unroll
+  for (int cb = 0; cb < 2; ++cb)
+#pragma unroll
+    for (int par = 0; par < 2; ++par) {
+      const int chunk = 4 * w + 2 * cb + (g >> 2);
+      a_tr[cb][par] = (unsigned)(q4 * 512 + ((chunk ^ (4 * par + q4)) << 5) + (g & 3) * 8);
+    }
+  // B fragments: X[4kb + q4][8nb + g]
+  const unsigned b_off = (unsigned)(q4 * K * 8 + g * 8);
+
+  double acc[2][NB][2];
+#pragma unroll
+  for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) acc[rb][nb][0] = acc[rb][nb][1] = 0.0;
+  int curR = -1;
+  auto flush_direct = [&](int R) {
+#pragma unroll
+    for (int rb = 0; rb < 2; ++rb) {
+      double *y = p.Y + ((long long)R * kBlock + 16 * w + 8 * rb + g) * ldy + 2 * q4;
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) {
+        red_add(y + 8 * nb, acc[rb][nb][0]);
+        red_add(y + 8 * nb + 1, acc[rb][nb][1]);
+        acc[rb][nb][0] = acc[rb][nb][1] = 0.0;
+      }
+    }
+  };
+
+  int stage = grp % S;
+  uint32_t phase = (uint32_t)(grp / S) & 1u;
+  while (true) {
+    mbar_wait(&full[stage], phase);
+    const unsigned char *st = smem + (size_t)stage * SB;
+    const int4 h = *reinterpret_cast<const int4 *>(st + p.off_hdr);
+    if (h.z & HDR_TERM) {
+      if (curR >= 0) flush_direct(curR);
+      break;
+    }
+    if (h.x != curR) {
+      if (curR >= 0) flush_direct(curR);
+      curR = h.x;
+    }
+    const unsigned char *Xc = st + p.off_xc, *Xr = st + p.off_xr;
+    // ---- direct: acc[rb][nb] += T[rows] · X_C ----
+#pragma unroll 4
+    for (int kb = 0; kb < 16; ++kb) {
+      double b[NB];
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) b[nb] = *reinterpret_cast<const double *>(Xc + b_off + kb * 32 * K + nb * 64);
+#pragma unroll
+      for (int rb = 0; rb < 2; ++rb) {
+        const double a = *reinterpret_cast<const double *>(st + ((a_dir + rb * 8 * 512) ^ (unsigned)(kb << 5)));
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) dmma(acc[rb][nb][0], acc[rb][nb][1], a, b[nb]);
+      }
+    }
+    const bool diag = h.z & HDR_DIAG;
+    if (!diag) {
+      // ---- transposed: E[cb][nb] = Tᵀ[cols] · X_R ----
+      double e[2][NB][2];
+#pragma unroll
+      for (int cb = 0; cb < 2; ++cb)
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) e[cb][nb][0] = e[cb][nb][1] = 0.0;
+#pragma unroll 4
+      for (int kb = 0; kb < 16; ++kb) {
+        double b[NB];
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) b[nb] = *reinterpret_cast<const double *>(Xr + b_off + kb * 32 * K + nb * 64);
+#pragma unroll
+        for (int cb = 0; cb < 2; ++cb) {
+          const double a = *reinterpret_cast<const double *>(st + kb * 2048 + a_tr[cb][kb & 1]);
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) dmma(e[cb][nb][0], e[cb][nb][1], a, b[nb]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+#pragma unroll
+      for (int cb = 0; cb < 2; ++cb) {
+        double *y = p.Y + ((long long)h.y * kBlock + 16 * w + 8 * cb + g) * ldy + 2 * q4;
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) {
+          red_add(y + 8 * nb, e[cb][nb][0]);
+          red_add(y + 8 * nb + 1, e[cb][nb][1]);
+        }
+      }
+    } else {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+    }
+    stage += 2;
+    if (stage >= S) {
+      stage -= S;
+      phase ^= 1u;
+    }
+  }
+}
+
+template <int K>
+int launch(const cim_half_tiles *H, const void *X, void *Y, long long ldy, cudaStream_t stream, int sms,
+           unsigned int *counter) {
+  static std::mutex mu;
+  static int attr_mask = 0;
+  const unsigned xblk = 64u * K * 8u;
+  DmParams p{};
+  p.off_xc = kTileBytes;
+  p.off_xr = p.off_xc + xblk;
+  p.off_hdr = p.off_xr + xblk;
+  p.stage_bytes = (p.off_hdr + 16 + 127) & ~127u;
+  const size_t budget = 227 * 1024 - 256;
+  int S = (int)(budget / p.stage_bytes);
+  S = std::min(S, 8);
+  // The two consumer groups take alternate tiles; with an odd ring a stage
+  // would alternate between the groups, and a group running ahead could
+  // pass a parity wait on a stage one fill behind (phase aliasing).  An even
+  // ring keeps every stage with one group.
+  S &= ~1;
+  if (S < 2) return set_error(CIM_EUNSUPPORTED, "DMMA path: k too large for shared memory");
+  p.stages = (unsigned)S;
+  p.off_bars = (unsigned)S * p.stage_bytes;
+  const size_t smem = p.off_bars + 16 * (size_t)S;
+  auto kern = sym_spmm_dmma_kernel<K>;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!(attr_mask & (1 << dev))) {
+      const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      if (e != cudaSuccess)
+        return set_error(CIM_ECUDA, std::string("cudaFuncSetAttribute(dmma): ") + cudaGetErrorString(e));
+      attr_mask |= (1 << dev);
+    }
+  }
+  p.units = reinterpret_cast<const int4 *>(H->units);
+  p.tile_rc = reinterpret_cast<const int2 *>(H->tile_rc);
+  p.vals = reinterpret_cast<const unsigned char *>(H->vals);
+  p.X = reinterpret_cast<const unsigned char *>(X);
+  p.Y = reinterpret_cast<double *>(Y);
+  p.counter = counter;
+  p.n_units = H->n_units;
+  p.ldy = ldy;
+  p.xblk = xblk;
+  const long long grid = std::min<long long>(sms, H->n_units);
+  cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned int), stream);
+  if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("counter memset: ") + cudaGetErrorString(e));
+  kern<<<(unsigned)grid, kThreads, smem, stream>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("sym_spmm_dmma launch: ") + cudaGetErrorString(e));
+  return CIM_OK;
+}
+
+}  // namespace dmma
+
+// Entry used by cim_sym_spmm for f64 CIM_LAYOUT_TC tiles.
+int sym_spmm_dmma_dispatch(const cim_half_tiles *H, const void *X, void *Y, int k, long long ldy,
+                           cudaStream_t stream, int sms, unsigned int *counter) {
+  switch (k) {
+    case 8: return dmma::launch<8>(H, X, Y, ldy, stream, sms, counter);
+    case 16: return dmma::launch<16>(H, X, Y, ldy, stream, sms, counter);
+    case 24: return dmma::launch<24>(H, X, Y, ldy, stream, sms, counter);
+    case 32: return dmma::launch<32>(H, X, Y, ldy, stream, sms, counter);
+  }
+  return set_error(CIM_EUNSUPPORTED, "f64 tensor-core path supports k in {8, 16, 24, 32}");
+}
+
+}  // namespace cim

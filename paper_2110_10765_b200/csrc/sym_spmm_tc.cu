@@ -597,6 +597,11 @@ int launch(const cim_half_tiles *H, const void *X, void *Y, long long ldy, cudaS
   const size_t budget = 227 * 1024 - 1024;  // minus the manual 1 KB alignment slack
   int S = (int)((budget - fixed - 8 * 2 * 8) / p.stage_bytes);
   S = std::min(S, 8);
+  // The two consumer groups take alternate tiles; with an odd ring a stage
+  // would alternate between the groups, and a group running ahead could
+  // pass a parity wait on a stage one fill behind (phase aliasing).  An even
+  // ring keeps every stage with one group.
+  S &= ~1;
   if (S < 2) return set_error(CIM_EUNSUPPORTED, "tensor-core path: k too large for shared memory");
   p.stages = (unsigned)S;
   size_t off = (size_t)S * p.stage_bytes;

@@ -96,7 +96,7 @@ int check_launch(const char *what) {
 using namespace cim;
 
 static bool layout_ok(int32_t layout, int32_t dtype) {
-  return layout == CIM_LAYOUT_FRAG || (layout == CIM_LAYOUT_TC && dtype == CIM_F32);
+  return layout == CIM_LAYOUT_FRAG || layout == CIM_LAYOUT_TC;
 }
 
 extern "C" int cim_fill_synthetic_values(const int32_t *tile_rc, int64_t n_tiles, int64_t n, int32_t dtype,

@@ -645,8 +645,6 @@ class HalfTiles:
         layout = layout or default_layout(dtype)
         if layout not in LAYOUTS:
             raise ValueError(f"unknown layout {layout!r}, expected one of {tuple(LAYOUTS)}")
-        if layout == "tc" and dtype != torch.float32:
-            raise ValueError("the tensor-core layout holds f32 tiles only")
         device = torch.device(device)
         if device.type != "cuda":
             raise ValueError("HalfTiles live in GPU memory: device must be a CUDA device")

@@ -32,15 +32,21 @@ def supported_k(dtype: torch.dtype, k: int, layout: str = "frag") -> bool:
     return bool(lib().cim_layout_supports(LAYOUTS[layout], code, int(k)))
 
 
-TC_MAX_K = 64  # vectors per tensor-core apply (N = 2k ≤ 128 TMEM columns per accumulator)
+TC_MAX_K = 64  # f32 vectors per tensor-core apply (N = 2k ≤ 128 TMEM columns per accumulator)
+TC_MAX_K_F64 = 32  # f64 (DMMA kernel, register-resident accumulators)
+
+
+def tc_max_k(dtype: torch.dtype) -> int:
+    return TC_MAX_K if dtype == torch.float32 else TC_MAX_K_F64
 
 
 def padded_k(dtype: torch.dtype, k: int, layout: str = "frag") -> int:
     """Smallest compiled vector count ≥ k for the layout (extra columns are zero).
-    The tensor-core layout takes multiples of 8 up to 64."""
+    The tensor-core layout takes multiples of 8 up to 64 (f32) / 32 (f64);
+    wider f64 blocks run as column passes of 32."""
     kk = int(k)
-    if layout == "tc" and kk > TC_MAX_K:
-        return -(-kk // TC_MAX_K) * TC_MAX_K
+    if layout == "tc" and kk > tc_max_k(dtype):
+        return -(-kk // tc_max_k(dtype)) * tc_max_k(dtype)
     while kk <= 64 and not supported_k(dtype, kk, layout):
         kk += 1
     if kk > 64:
@@ -61,14 +67,15 @@ def _launch(H: HalfTiles, Xd: torch.Tensor, Yd: torch.Tensor, accumulate: bool, 
                                     (CIM_ACCUMULATE if accumulate else 0) | CIM_DETERMINISTIC, handle)
         check(rc, "cim_sym_spmm(deterministic)")
         return
-    if H.layout == "tc" and k > TC_MAX_K:
-        # column passes of 16 vectors: each pass streams the tiles once more
+    w = tc_max_k(H.dtype)
+    if H.layout == "tc" and k > w:
+        # column passes of w vectors: each pass streams the tiles once more
         with torch.cuda.stream(s) if isinstance(s, torch.cuda.Stream) else torch.cuda.device(H.device):
-            for c0 in range(0, k, TC_MAX_K):
-                xc = Xd[:, c0:c0 + TC_MAX_K].contiguous()
-                yc = Yd[:, c0:c0 + TC_MAX_K].contiguous() if accumulate else torch.empty_like(xc)
+            for c0 in range(0, k, w):
+                xc = Xd[:, c0:c0 + w].contiguous()
+                yc = Yd[:, c0:c0 + w].contiguous() if accumulate else torch.empty_like(xc)
                 _launch(H, xc, yc, accumulate, s)
-                Yd[:, c0:c0 + TC_MAX_K].copy_(yc)
+                Yd[:, c0:c0 + w].copy_(yc)
         return
     with torch.cuda.device(H.device):
         rc = lib().cim_sym_spmm(H.descriptor(), Xd.data_ptr(), Yd.data_ptr(), k, Xd.stride(0), Yd.stride(0),

@@ -69,7 +69,7 @@ def test_device_hash_matches_reference_kats(pkg):
 
 
 F32_LAYOUTS = ["tc", "frag"]
-DT_LAYOUTS = [(torch.float32, "tc"), (torch.float32, "frag"), (torch.float64, "frag")]
+DT_LAYOUTS = [(torch.float32, "tc"), (torch.float32, "frag"), (torch.float64, "frag"), (torch.float64, "tc")]
 
 
 @pytest.mark.parametrize("dtype,layout", DT_LAYOUTS)
@@ -237,10 +237,11 @@ def test_k_sweep_f32(pkg, c1_small, k, layout):
     check_result(n, rc, tiles, X.numpy(), Y, torch.float32)
 
 
-@pytest.mark.parametrize("k", [1, 2, 4, 8, 12, 16, 32])
-def test_k_sweep_f64(pkg, c1_small, k):
+@pytest.mark.parametrize("layout", ["frag", "tc"])
+@pytest.mark.parametrize("k", [1, 2, 4, 8, 12, 16, 24, 32, 40])
+def test_k_sweep_f64(pkg, c1_small, k, layout):
     n, rc, tiles = c1_small
-    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=torch.float64)
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=torch.float64, layout=layout)
     X = torch.randn((n, k), generator=torch.Generator().manual_seed(k), dtype=torch.float64)
     Y = pkg.sym_spmm(H, X.cuda()).cpu().numpy()
     check_result(n, rc, tiles.astype(np.float64), X.numpy(), Y, torch.float64)

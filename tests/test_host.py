@@ -79,6 +79,8 @@ def test_supported_k_table():
     assert pkg.padded_k(torch.float32, 5) == 8
     assert pkg.padded_k(torch.float64, 6) == 8
     assert pkg.padded_k(torch.float64, 12) == 12
+    assert pkg.padded_k(torch.float64, 20, "tc") == 24
+    assert pkg.padded_k(torch.float64, 40, "tc") == 64  # two DMMA column passes of 32
     assert pkg.padded_k(torch.float32, 3, "tc") == 8
     assert pkg.padded_k(torch.float32, 9, "tc") == 16
     assert pkg.padded_k(torch.float32, 24, "tc") == 24
