@@ -464,6 +464,10 @@ def impl_ours(args):
     k = args.k
     n, nb, n_off, p = workload(args, world)
 
+    # tile storage: the faster kernel family for this (dtype, k) unless --layout
+    # says otherwise (halftiles.default_layout; the fused peer-memory apply
+    # needs the fragment layout)
+    layout = args.layout or ("frag" if args.fused else pkg.default_layout(dtype, k))
     t_build = time.perf_counter()
     if args.fill is not None:
         if world != 1:
@@ -473,7 +477,7 @@ def impl_ours(args):
                        global_off_tiles=int(np.count_nonzero(Hs.sparse.tile_rc_host[:, 0] != Hs.sparse.tile_rc_host[:, 1])))
         S = ShardedSymSpmm(n, k, dtype, dev, H_local=Hs)
     else:
-        S = ShardedSymSpmm.synthetic(n, k=k, p=p, seed=0, dtype=dtype, device=dev, layout=args.layout,
+        S = ShardedSymSpmm.synthetic(n, k=k, p=p, seed=0, dtype=dtype, device=dev, layout=layout,
                                      bands=None if args.bands == 0 else args.bands, fused=args.fused,
                                      overlap=world > 1 and not args.no_overlap and not args.fused)
     H = S.H
@@ -650,7 +654,7 @@ def impl_ours(args):
         dist.barrier()
         if rank == 0:
             try:
-                H1 = pkg.HalfTiles.synthetic(n, p=p, seed=0, dtype=dtype, device=dev, layout=args.layout)
+                H1 = pkg.HalfTiles.synthetic(n, p=p, seed=0, dtype=dtype, device=dev, layout=layout)
                 X1 = torch.randn((H1.n_pad, k), device=dev, dtype=dtype, generator=gen)
                 Y1 = torch.empty_like(X1)
                 for _ in range(2):

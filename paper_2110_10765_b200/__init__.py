@@ -26,7 +26,7 @@ C-ABI in ``libcim_b200.so``, include/cim_b200.h):
 
 from ._lib import BLOCK, CimError, lib
 from .construct import group_basis, load_basis, save_basis
-from .halftiles import HalfTiles, partition_units, plan_units, synthetic_pattern
+from .halftiles import HalfTiles, default_layout, partition_units, plan_units, synthetic_pattern
 from .lobpcg import LobpcgResult, lobpcg, lobpcg_sym
 from .observables import (
     OP_KINDS,
@@ -49,6 +49,7 @@ from .spmm import padded_k, supported_k, sym_spmm, sym_spmm_host_batch
 __version__ = "1.0.0"
 
 __all__ = [
+    "default_layout",
     "BLOCK",
     "CimError",
     "HalfTiles",

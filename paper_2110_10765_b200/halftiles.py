@@ -36,12 +36,20 @@ DEFAULT_MAX_UNIT = 32
 LAYOUTS = {"frag": CIM_LAYOUT_FRAG, "tc": CIM_LAYOUT_TC}
 
 
-def default_layout(dtype) -> str:
-    """The fragment layout (CUDA-core FFMA2 kernel) for f32 and f64: measured
-    faster than the tcgen05 3xTF32 path on the BASELINE configs this round
-    (profiles/r01/SUMMARY.md); ``layout="tc"`` selects the tensor-core path."""
-    _as_torch_dtype(dtype)
-    return "frag"
+def default_layout(dtype, k: int | None = None) -> str:
+    """Tile layout for vector blocks of width k (the storage is fixed at
+    construction, so callers that know their k pass it).  Measured on one
+    B200, C2 (profiles/r02/SUMMARY.md): the fragment layout's CUDA-core
+    kernels win at f32 k ≤ 8 (FFMA2, at the DRAM bound) and f64 k ≤ 4; the
+    tensor-core layout wins above — f32 k ≥ 16 through the split-TF32 tcgen05
+    kernel, f64 k ≥ 8 through the DMMA kernel.  Without k: "frag"."""
+    dt = _as_torch_dtype(dtype)
+    if k is None:
+        return "frag"
+    k = int(k)
+    if dt == torch.float32:
+        return "tc" if k > 8 else "frag"
+    return "tc" if k > 4 else "frag"
 
 
 VALUE_KINDS = {"h_xor": _lib.CIM_VALUES_H_XOR, "op_hash": _lib.CIM_VALUES_OP_HASH, "identity": _lib.CIM_VALUES_IDENTITY}

@@ -13,3 +13,4 @@ run() {  # DT K LAYOUT
 for K in 1 4 8 16 32 64; do run f32 $K frag; done
 for K in 8 16 32 64; do run f32 $K tc; done
 for K in 1 4 8 16 32; do run f64 $K frag; done
+for K in 8 16 24 32; do run f64 $K tc; done
