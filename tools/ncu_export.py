@@ -9,7 +9,12 @@ EXTRA = ["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram__bytes.
          "lts__t_sector_hit_rate.pct", "lts__t_sectors_evict_last_lookup_hit.sum",
          "lts__t_sectors_evict_last_lookup_miss.sum", "lts__t_sectors_evict_normal_lookup_hit.sum",
          "lts__t_sectors_evict_normal_lookup_miss.sum", "lts__t_sectors_srcunit_ltcfabric.sum",
-         "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_dynamic"]
+         "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_dynamic",
+         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+         "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+         "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+         "sm__inst_executed_pipe_uma.avg.pct_of_peak_sustained_active",
+         "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active"]
 out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 h, u, v = rows[0], rows[1], rows[2]
