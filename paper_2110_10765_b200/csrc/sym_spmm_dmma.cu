@@ -51,6 +51,7 @@ struct DmParams {
   long long ldy;
   unsigned int stages, stage_bytes, xblk;
   unsigned int off_xc, off_xr, off_hdr, off_bars;
+  unsigned int off_ebuf;  // 2 groups × 2 staging blocks of 64·K doubles (bulk flush), 0 = scalar reds
 };
 
 constexpr int kTileBytes = 4096 * 8;
@@ -61,6 +62,19 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
+
+// One 64 × K block of partial sums → Y rows Rb·64 … Rb·64+63 (dense, ldy = K)
+// with one bulk reduction: UBLKRED.ADD.F64 does the read-modify-write of the
+// whole contiguous 64·K·8-byte block at the L2, where scalar red.global.add.f64
+// (there is no vector form for f64) needed 64·K separate atomic operations.
+__device__ __forceinline__ void bulk_red_f64(double *dst, const void *src, unsigned bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_le1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 template <int K>
 __global__ void __launch_bounds__(kThreads, 1) sym_spmm_dmma_kernel(const DmParams p) {
@@ -157,17 +171,44 @@ __global__ void __launch_bounds__(kThreads, 1) sym_spmm_dmma_kernel(const DmPara
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb) acc[rb][nb][0] = acc[rb][nb][1] = 0.0;
   int curR = -1;
-  auto flush_direct = [&](int R) {
+  // partial sums of one 64-row block (fragments f[2][NB][2] of rows / columns
+  // 16w + 8·blk + g) → Y block row Rb
+  const bool bulk = p.off_ebuf != 0;
+  const bool issuer = w == 0 && lane == 0;
+  int eb = 0;  // staging buffer of this group's next bulk flush
+  auto flush = [&](int Rb, double (&f)[2][NB][2]) {
+    if (bulk) {
+      double *ebuf = reinterpret_cast<double *>(smem + p.off_ebuf + (size_t)(2 * grp + eb) * 64 * K * 8);
+      if (issuer) bulk_wait_read_le1();  // the flush that last used this buffer has read it
+      named_bar_sync(1 + grp, 128);
 #pragma unroll
-    for (int rb = 0; rb < 2; ++rb) {
-      double *y = p.Y + ((long long)R * kBlock + 16 * w + 8 * rb + g) * ldy + 2 * q4;
+      for (int blk = 0; blk < 2; ++blk)
 #pragma unroll
-      for (int nb = 0; nb < NB; ++nb) {
-        red_add(y + 8 * nb, acc[rb][nb][0]);
-        red_add(y + 8 * nb + 1, acc[rb][nb][1]);
-        acc[rb][nb][0] = acc[rb][nb][1] = 0.0;
+        for (int nb = 0; nb < NB; ++nb)
+          *reinterpret_cast<double2 *>(ebuf + (16 * w + 8 * blk + g) * K + 8 * nb + 2 * q4) =
+              make_double2(f[blk][nb][0], f[blk][nb][1]);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      named_bar_sync(1 + grp, 128);
+      if (issuer) bulk_red_f64(p.Y + (long long)Rb * kBlock * K, ebuf, 64u * K * 8u);
+      eb ^= 1;
+    } else {
+#pragma unroll
+      for (int blk = 0; blk < 2; ++blk) {
+        double *y = p.Y + ((long long)Rb * kBlock + 16 * w + 8 * blk + g) * ldy + 2 * q4;
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) {
+          red_add(y + 8 * nb, f[blk][nb][0]);
+          red_add(y + 8 * nb + 1, f[blk][nb][1]);
+        }
       }
     }
+  };
+  auto flush_direct = [&](int R) {
+    flush(R, acc);
+#pragma unroll
+    for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) acc[rb][nb][0] = acc[rb][nb][1] = 0.0;
   };
 
   int stage = grp % S;
@@ -178,6 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1) sym_spmm_dmma_kernel(const DmPara
     const int4 h = *reinterpret_cast<const int4 *>(st + p.off_hdr);
     if (h.z & HDR_TERM) {
       if (curR >= 0) flush_direct(curR);
+      if (bulk && issuer) bulk_wait_all();
       break;
     }
     if (h.x != curR) {
@@ -220,15 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1) sym_spmm_dmma_kernel(const DmPara
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
-#pragma unroll
-      for (int cb = 0; cb < 2; ++cb) {
-        double *y = p.Y + ((long long)h.y * kBlock + 16 * w + 8 * cb + g) * ldy + 2 * q4;
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb) {
-          red_add(y + 8 * nb, e[cb][nb][0]);
-          red_add(y + 8 * nb + 1, e[cb][nb][1]);
-        }
-      }
+      flush(h.y, e);
     } else {
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
@@ -253,8 +287,13 @@ int launch(const cim_half_tiles *H, const void *X, void *Y, long long ldy, cudaS
   p.off_hdr = p.off_xr + xblk;
   p.stage_bytes = (p.off_hdr + 16 + 127) & ~127u;
   const size_t budget = 227 * 1024 - 256;
-  int S = (int)(budget / p.stage_bytes);
-  S = std::min(S, 8);
+  // bulk flushes need dense Y rows and 2 groups × 2 staging blocks; keep them
+  // unless they would cost ring stages
+  const size_t ebytes = 4 * (size_t)64 * K * 8;
+  const int S_scalar = std::min(8, (int)(budget / p.stage_bytes)) & ~1;
+  const int S_bulk = std::min(8, (int)((budget - ebytes) / p.stage_bytes)) & ~1;
+  const bool use_bulk = ldy == K && (S_bulk >= 4 || S_bulk == S_scalar) && !std::getenv("CIM_DMMA_SCALAR_RED");
+  int S = use_bulk ? S_bulk : S_scalar;
   // The two consumer groups take alternate tiles; with an odd ring a stage
   // would alternate between the groups, and a group running ahead could
   // pass a parity wait on a stage one fill behind (phase aliasing).  An even
@@ -262,7 +301,8 @@ int launch(const cim_half_tiles *H, const void *X, void *Y, long long ldy, cudaS
   S &= ~1;
   if (S < 2) return set_error(CIM_EUNSUPPORTED, "DMMA path: k too large for shared memory");
   p.stages = (unsigned)S;
-  p.off_bars = (unsigned)S * p.stage_bytes;
+  p.off_ebuf = use_bulk ? (unsigned)S * p.stage_bytes : 0u;
+  p.off_bars = (unsigned)((size_t)S * p.stage_bytes + (use_bulk ? ebytes : 0));
   const size_t smem = p.off_bars + 16 * (size_t)S;
   auto kern = sym_spmm_dmma_kernel<K>;
   int dev = 0;
