@@ -74,6 +74,7 @@ struct TcParams {
   unsigned int off_meta;              // ND int4 headers (MMA → epilogue)
   unsigned int off_bars;
   unsigned int off_tmem;
+  unsigned int off_ebuf;  // 4 staging blocks of 64·k floats for bulk Y reductions (0 = red.v4 per row)
 };
 
 // Role timers (tools/tc_profile.py; compiled in only with -DCIM_TC_PROF): lane 0
@@ -144,8 +145,20 @@ __device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&r)[8]) {
                : "memory");
 }
 
+__device__ __forceinline__ void bulk_wait_read_le1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// One 64 × k block of partial sums (staged in shared memory) → the 64
+// contiguous rows of a dense Y block: one bulk reduction (UBLKRED.ADD.F32)
+// instead of 64·k/4 red.global.add.v4.f32 from the epilogue warps.
+__device__ __forceinline__ void bulk_red_f32(float *dst, const void *src, unsigned bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
 
 // lo(x) = x − (x with the low 13 mantissa bits cleared): exact in FP32
 __device__ __forceinline__ float lo_tf32(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
@@ -503,6 +516,12 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
     float acc[K];
 #pragma unroll
     for (int e = 0; e < K; ++e) acc[e] = 0.0f;
+    // bulk Y reductions: warps 12-13 (direct) and 14-15 (transposed) each
+    // stage a 64 × K block, their lane 0 of warp 12 / 14 issues it
+    const bool bulk = p.off_ebuf != 0;
+    const bool issuer = (q == 0 || q == 2) && lane == 0;
+    float *ebuf = reinterpret_cast<float *>(smem + p.off_ebuf);
+    int eb_dir = 0, eb_tr = 0;
     uint32_t t = 0;
     TPROF_DECL;
     while (true) {
@@ -512,7 +531,10 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
       mbar_wait(&meta_f[d], ph);
       TPROF(P_WAIT0);
       const int4 h = meta[d];
-      if (h.z & HDR_TERM) break;
+      if (h.z & HDR_TERM) {
+        if (bulk && issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        break;
+      }
       mbar_wait(&d_full[d], ph);
       TPROF(P_WAIT1);
       tc_fence_after();
@@ -540,13 +562,31 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
 #else
         if (false) {
 #endif
-          float *yp = Y + ((long long)h.x * kBlock + m) * ldy;
+          if (bulk) {
+            float *eb = ebuf + (size_t)eb_dir * 64 * K;
+            if (issuer) bulk_wait_read_le1();
+            named_bar_sync(1, 64);
 #pragma unroll
-          for (int e = 0; e < K; e += 4) red_add_v4(yp + e, acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
+            for (int e = 0; e < K; e += 4)
+              *reinterpret_cast<float4 *>(eb + m * K + e) = make_float4(acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            named_bar_sync(1, 64);
+            if (issuer) bulk_red_f32(Y + (long long)h.x * kBlock * K, eb, 64u * K * 4u);
+            eb_dir ^= 1;
+          } else {
+            float *yp = Y + ((long long)h.x * kBlock + m) * ldy;
+#pragma unroll
+            for (int e = 0; e < K; e += 4) red_add_v4(yp + e, acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
+          }
         }
       } else {
         // transposed product column m − 64 of the tile: D columns K..2K-1 → Y_C
         if (!diag) {
+          float *eb = ebuf + (size_t)(2 + eb_tr) * 64 * K;
+          if (bulk) {
+            if (issuer) bulk_wait_read_le1();
+            named_bar_sync(2, 64);
+          }
           float *yp = Y + ((long long)h.y * kBlock + (m - 64)) * ldy;
 #pragma unroll
           for (int cb = 0; cb < K / 8; ++cb) {
@@ -554,16 +594,34 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
             tmem_ld8(dcol + K + 8 * cb, r8);
             tmem_wait_ld();
 #ifndef CIM_TC_NO_RED
-            red_add_v4(yp + 8 * cb, __uint_as_float(r8[0]), __uint_as_float(r8[1]), __uint_as_float(r8[2]),
-                       __uint_as_float(r8[3]));
-            red_add_v4(yp + 8 * cb + 4, __uint_as_float(r8[4]), __uint_as_float(r8[5]), __uint_as_float(r8[6]),
-                       __uint_as_float(r8[7]));
+            if (bulk) {
+              float *row = eb + (m - 64) * K + 8 * cb;
+              *reinterpret_cast<float4 *>(row) = make_float4(__uint_as_float(r8[0]), __uint_as_float(r8[1]),
+                                                             __uint_as_float(r8[2]), __uint_as_float(r8[3]));
+              *reinterpret_cast<float4 *>(row + 4) = make_float4(__uint_as_float(r8[4]), __uint_as_float(r8[5]),
+                                                                 __uint_as_float(r8[6]), __uint_as_float(r8[7]));
+            } else {
+              red_add_v4(yp + 8 * cb, __uint_as_float(r8[0]), __uint_as_float(r8[1]), __uint_as_float(r8[2]),
+                         __uint_as_float(r8[3]));
+              red_add_v4(yp + 8 * cb + 4, __uint_as_float(r8[4]), __uint_as_float(r8[5]), __uint_as_float(r8[6]),
+                         __uint_as_float(r8[7]));
+            }
 #endif
           }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&d_empty[d]);
+          if (bulk) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            named_bar_sync(2, 64);
+            if (issuer) bulk_red_f32(Y + (long long)h.y * kBlock * K, eb, 64u * K * 4u);
+            eb_tr ^= 1;
+          }
+        } else {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&d_empty[d]);
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&d_empty[d]);
       }
       TPROF_TILE();
       ++t;
@@ -595,8 +653,13 @@ int launch(const cim_half_tiles *H, const void *X, void *Y, long long ldy, cudaS
   p.stage_bytes = (p.off_hdr + 16 + 127) & ~127u;
   const size_t fixed = (size_t)Cf::NA * Cf::BBYTES + 16 * (Cf::NA + Cf::ND) + 8 * (3 * Cf::NA + 3 * Cf::ND) + 64;
   const size_t budget = 227 * 1024 - 1024;  // minus the manual 1 KB alignment slack
-  int S = (int)((budget - fixed - 8 * 2 * 8) / p.stage_bytes);
-  S = std::min(S, 8);
+  // bulk Y reductions need dense Y rows and 4 staging blocks; keep them unless
+  // they would cost ring stages below 4
+  const size_t ebytes = 4 * (size_t)64 * K * 4;
+  const int S_scalar = std::min(8, (int)((budget - fixed - 8 * 2 * 8) / p.stage_bytes)) & ~1;
+  const int S_bulk = std::min(8, (int)((budget - fixed - ebytes - 8 * 2 * 8) / p.stage_bytes)) & ~1;
+  const bool use_bulk = ldy == K && (S_bulk >= 4 || S_bulk == S_scalar) && !std::getenv("CIM_TC_SCALAR_RED");
+  int S = use_bulk ? S_bulk : S_scalar;
   // The two consumer groups take alternate tiles; with an odd ring a stage
   // would alternate between the groups, and a group running ahead could
   // pass a parity wait on a stage one fill behind (phase aliasing).  An even
@@ -616,6 +679,9 @@ int launch(const cim_half_tiles *H, const void *X, void *Y, long long ldy, cudaS
   off = (off + 15) & ~size_t(15);
   p.off_tmem = (unsigned int)off;
   off += 16;
+  off = (off + 127) & ~size_t(127);
+  p.off_ebuf = use_bulk ? (unsigned int)off : 0u;
+  if (use_bulk) off += ebytes;
   const size_t smem = off + 1024;
   if (smem > 227 * 1024) return set_error(CIM_EUNSUPPORTED, "tensor-core path: shared-memory plan too large");
 
