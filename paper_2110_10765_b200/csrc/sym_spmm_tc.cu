@@ -75,6 +75,7 @@ struct TcParams {
   unsigned int off_bars;
   unsigned int off_tmem;
   unsigned int off_ebuf;  // 4 staging blocks of 64·k floats for bulk Y reductions (0 = red.v4 per row)
+  int xpol, ypol;         // L2 policies (A/B, CIM_TC_XPOL / CIM_TC_YPOL): 0 evict_last/normal, 1 evict_first, 2 evict_normal/last
 };
 
 // Role timers (tools/tc_profile.py; compiled in only with -DCIM_TC_PROF): lane 0
@@ -153,10 +154,17 @@ __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.
 // One 64 × k block of partial sums (staged in shared memory) → the 64
 // contiguous rows of a dense Y block: one bulk reduction (UBLKRED.ADD.F32)
 // instead of 64·k/4 red.global.add.v4.f32 from the epilogue warps.
-__device__ __forceinline__ void bulk_red_f32(float *dst, const void *src, unsigned bytes) {
-  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
-               "r"(smem_u32(src)), "r"(bytes)
-               : "memory");
+__device__ __forceinline__ void bulk_red_f32(float *dst, const void *src, unsigned bytes, int ypol = 0) {
+  if (ypol == 0) {
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+  } else {
+    const uint64_t pol = ypol == 1 ? policy_evict_first() : policy_evict_last();
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.L2::cache_hint.add.f32 [%0], [%1], %2, %3;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes), "l"(pol)
+                 : "memory");
+  }
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
@@ -288,7 +296,7 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
   if (warp == 0) {
     // ================================ producer ================================
     const uint64_t pol_stream = policy_evict_first();
-    const uint64_t pol_keep = policy_evict_last();
+    const uint64_t pol_keep = p.xpol == 1 ? policy_evict_first() : p.xpol == 2 ? policy_evict_normal() : policy_evict_last();
     const unsigned int xblk = p.xblk;
     int stage = 0;
     uint32_t phase = 0;
@@ -571,7 +579,7 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
               *reinterpret_cast<float4 *>(eb + m * K + e) = make_float4(acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             named_bar_sync(1, 64);
-            if (issuer) bulk_red_f32(Y + (long long)h.x * kBlock * K, eb, 64u * K * 4u);
+            if (issuer) bulk_red_f32(Y + (long long)h.x * kBlock * K, eb, 64u * K * 4u, p.ypol);
             eb_dir ^= 1;
           } else {
             float *yp = Y + ((long long)h.x * kBlock + m) * ldy;
@@ -614,7 +622,7 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
           if (bulk) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             named_bar_sync(2, 64);
-            if (issuer) bulk_red_f32(Y + (long long)h.y * kBlock * K, eb, 64u * K * 4u);
+            if (issuer) bulk_red_f32(Y + (long long)h.y * kBlock * K, eb, 64u * K * 4u, p.ypol);
             eb_tr ^= 1;
           }
         } else {
@@ -706,6 +714,8 @@ int launch(const cim_half_tiles *H, const void *X, void *Y, long long ldy, cudaS
   p.n_units = H->n_units;
   p.ldy = ldy;
   p.xblk = xblk;
+  p.xpol = std::getenv("CIM_TC_XPOL") ? std::atoi(std::getenv("CIM_TC_XPOL")) : 0;
+  p.ypol = std::getenv("CIM_TC_YPOL") ? std::atoi(std::getenv("CIM_TC_YPOL")) : 0;
   const long long grid = std::min<long long>(sms, H->n_units);
   cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned int), stream);
   if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("counter memset: ") + cudaGetErrorString(e));

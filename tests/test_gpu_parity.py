@@ -388,12 +388,13 @@ def test_save_load_roundtrip(pkg, c1_small, tmp_path):
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and M2.n_sparse_tiles == M.n_sparse_tiles
 
 
-def test_sharded_world1_equals_direct(pkg):
+@pytest.mark.parametrize("dtype,k,layout", [(torch.float32, 8, "frag"), (torch.float32, 16, "tc"), (torch.float64, 8, "tc")])
+def test_sharded_world1_equals_direct(pkg, dtype, k, layout):
     n = 4096
-    S = pkg.ShardedSymSpmm.synthetic(n, k=8, p=0.1, seed=3)
+    S = pkg.ShardedSymSpmm.synthetic(n, k=k, p=0.1, seed=3, dtype=dtype, layout=layout)
     rc = pkg.synthetic_pattern(64, 0.1, seed=3)
-    H = pkg.HalfTiles.synthetic(n, tile_rc=rc)
-    X = torch.randn((n, 8), generator=torch.Generator().manual_seed(0)).cuda()
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=dtype, layout=layout)
+    X = torch.randn((n, k), generator=torch.Generator().manual_seed(0), dtype=dtype).cuda()
     Y = S.apply(X)
     assert torch.allclose(Y, pkg.sym_spmm(H, X), rtol=0, atol=1e-5 * pkg.sym_spmm(H, X).abs().max().item())
 
@@ -445,13 +446,15 @@ def test_c2_full_size_properties(pkg, layout):
         assert np.abs(got - yr).max() <= 1e-5 * max(1.0, np.abs(yr).max())
 
 
-@pytest.mark.parametrize("dtype,k", [(torch.float32, 8), (torch.float32, 4), (torch.float64, 8), (torch.float32, 32), (torch.float64, 16)])
-def test_host_batch_pipeline_matches_oracle(pkg, c1_small, dtype, k):
+@pytest.mark.parametrize("dtype,k,layout", [(torch.float32, 8, "frag"), (torch.float32, 4, "frag"), (torch.float64, 8, "frag"),
+                                             (torch.float32, 32, "frag"), (torch.float64, 16, "frag"),
+                                             (torch.float32, 16, "tc"), (torch.float64, 8, "tc")])
+def test_host_batch_pipeline_matches_oracle(pkg, c1_small, dtype, k, layout):
     """cim_sym_spmm_host_batch: host (pinned and pageable, numpy and torch)
     blocks in, host blocks out; every block checked against the oracle, and
     against the single-call operator bit for bit (same kernel, same order)."""
     n, rc, tiles = c1_small
-    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=dtype)
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=dtype, layout=layout)
     g = torch.Generator().manual_seed(5)
     Xs = [torch.randn((n, k), generator=g, dtype=dtype).pin_memory() for _ in range(3)]
     Xs.append(torch.randn((n, k), generator=g, dtype=dtype))  # pageable
