@@ -1100,21 +1100,36 @@ __global__ void __launch_bounds__(kR3Threads, 1) sym_spmm_k8r3_kernel(const Spmm
     const uint64_t pol_keep = policy_evict_last();
     int stage = 0;
     uint32_t phase = 0;
-    unsigned int u = 0;
     const long long n_items = p.n_units * p.n_pass;
-    if (lane == 0) u = atomicAdd(p.counter, 1u);
+    // work-item metadata software-pipelined as in the tensor-core producer:
+    // holding item i+1's unit header and item i+2's ticket at the start of
+    // item i, load item i+1's first 32 tile columns and item i+2's header,
+    // and claim item i+3 — no dependent global load between two items' copies
+    const int4 zero4 = make_int4(0, 0, 0, 0);
+    unsigned int u = 0, u1 = 0, u2 = 0;
+    if (lane == 0) {
+      u = atomicAdd(p.counter, 1u);
+      u1 = atomicAdd(p.counter, 1u);
+      u2 = atomicAdd(p.counter, 1u);
+    }
     u = __shfl_sync(0xffffffffu, u, 0);
+    u1 = __shfl_sync(0xffffffffu, u1, 0);
+    u2 = __shfl_sync(0xffffffffu, u2, 0);
+    int4 unit = (long long)u < n_items ? p.units[u / (unsigned)p.n_pass] : zero4;
+    int4 unit1 = (long long)u1 < n_items ? p.units[u1 / (unsigned)p.n_pass] : zero4;
+    int myC0 = (unit.y + lane < unit.z) ? p.tile_rc[unit.y + lane].y : 0;
     while ((long long)u < n_items) {
+      const int myC1 = (unit1.y + lane < unit1.z) ? p.tile_rc[unit1.y + lane].y : 0;
+      const int4 unit2 = (long long)u2 < n_items ? p.units[u2 / (unsigned)p.n_pass] : zero4;
+      unsigned int u3 = 0;
+      if (lane == 0) u3 = atomicAdd(p.counter, 1u);
       const unsigned int ui = u / (unsigned)p.n_pass, pass = u - ui * (unsigned)p.n_pass;
-      const int4 unit = p.units[ui];
-      unsigned int u_next = 0;
-      if (lane == 0) u_next = atomicAdd(p.counter, 1u);
       const int R = unit.x, t0 = unit.y, t1 = unit.z;
       const int orr = R / p.chunk_blocks, lr = R - orr * p.chunk_blocks;
       const unsigned char *xs = p.xch[0] + (size_t)pass * (size_t)p.xpass_bytes;  // pass slice (n_chunks = 1)
       for (int tb = t0; tb < t1; tb += 32) {
         const int t = tb + lane;
-        const int myC = (t < t1) ? p.tile_rc[t].y : 0;
+        const int myC = tb == t0 ? myC0 : ((t < t1) ? p.tile_rc[t].y : 0);
         const int cnt = min(32, t1 - tb);
         for (int q = 0; q < cnt; ++q) {
           const int C = __shfl_sync(0xffffffffu, myC, q);
@@ -1146,7 +1161,12 @@ __global__ void __launch_bounds__(kR3Threads, 1) sym_spmm_k8r3_kernel(const Spmm
           }
         }
       }
-      u = __shfl_sync(0xffffffffu, u_next, 0);
+      u = u1;
+      unit = unit1;
+      myC0 = myC1;
+      u1 = u2;
+      unit1 = unit2;
+      u2 = __shfl_sync(0xffffffffu, u3, 0);
     }
     if (lane == 0) {
       mbar_wait_backoff(&empty[stage], phase ^ 1u);
