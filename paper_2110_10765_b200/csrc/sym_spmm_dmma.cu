@@ -100,17 +100,30 @@ __global__ void __launch_bounds__(kThreads, 1) sym_spmm_dmma_kernel(const DmPara
     const unsigned xblk = p.xblk;
     int stage = 0;
     uint32_t phase = 0;
-    unsigned int u = 0;
-    if (lane == 0) u = atomicAdd(p.counter, 1u);
+    // work-unit metadata software-pipelined (see the tcgen05 kernel's producer)
+    const long long n_units = p.n_units;
+    const int4 zero4 = make_int4(0, 0, 0, 0);
+    unsigned int u = 0, u1 = 0, u2 = 0;
+    if (lane == 0) {
+      u = atomicAdd(p.counter, 1u);
+      u1 = atomicAdd(p.counter, 1u);
+      u2 = atomicAdd(p.counter, 1u);
+    }
     u = __shfl_sync(0xffffffffu, u, 0);
-    while ((long long)u < p.n_units) {
-      const int4 unit = p.units[u];
-      unsigned int u_next = 0;
-      if (lane == 0) u_next = atomicAdd(p.counter, 1u);
+    u1 = __shfl_sync(0xffffffffu, u1, 0);
+    u2 = __shfl_sync(0xffffffffu, u2, 0);
+    int4 unit = (long long)u < n_units ? p.units[u] : zero4;
+    int4 unit1 = (long long)u1 < n_units ? p.units[u1] : zero4;
+    int myC0 = (unit.y + lane < unit.z) ? p.tile_rc[unit.y + lane].y : 0;
+    while ((long long)u < n_units) {
+      const int myC1 = (unit1.y + lane < unit1.z) ? p.tile_rc[unit1.y + lane].y : 0;
+      const int4 unit2 = (long long)u2 < n_units ? p.units[u2] : zero4;
+      unsigned int u3 = 0;
+      if (lane == 0) u3 = atomicAdd(p.counter, 1u);
       const int R = unit.x, t0 = unit.y, t1 = unit.z;
       for (int tb = t0; tb < t1; tb += 32) {
         const int t = tb + lane;
-        const int myC = (t < t1) ? p.tile_rc[t].y : 0;
+        const int myC = tb == t0 ? myC0 : ((t < t1) ? p.tile_rc[t].y : 0);
         const int cnt = min(32, t1 - tb);
         for (int q = 0; q < cnt; ++q) {
           const int Cb = __shfl_sync(0xffffffffu, myC, q);
@@ -131,7 +144,12 @@ __global__ void __launch_bounds__(kThreads, 1) sym_spmm_dmma_kernel(const DmPara
           }
         }
       }
-      u = __shfl_sync(0xffffffffu, u_next, 0);
+      u = u1;
+      unit = unit1;
+      myC0 = myC1;
+      u1 = u2;
+      unit1 = unit2;
+      u2 = __shfl_sync(0xffffffffu, u3, 0);
     }
     if (lane == 0)
       for (int e = 0; e < 2; ++e) {  // one terminator per consumer group
