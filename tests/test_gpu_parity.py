@@ -847,3 +847,31 @@ def test_reference_pipeline_pins_on_device_storage(pkg, name):
         A2 = pkg.sym_spmm(H64, X2.cuda()).cpu()
         lhs, rhs = (X1 * A2).sum(0), (A1 * X2).sum(0)
         assert torch.allclose(lhs, rhs, rtol=1e-12, atol=1e-12 * float(lhs.abs().max()))
+
+
+@pytest.mark.parametrize("dtype,k", [(torch.float32, 16), (torch.float32, 8), (torch.float64, 8), (torch.float64, 16)])
+def test_tensor_core_kernels_strided_y_and_accumulate(pkg, c1_small, dtype, k):
+    """Through the C-ABI: Y a column slice of a wider buffer (ldy = 2k, so the
+    bulk-reduction flush falls back to per-row reductions), the neighbouring
+    columns untouched, and CIM_ACCUMULATE adding a second product."""
+    from paper_2110_10765_b200._lib import CIM_ACCUMULATE, check, lib
+
+    n, rc, tiles = c1_small
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=dtype, layout="tc")
+    X = torch.randn((H.n_pad, k), generator=torch.Generator().manual_seed(3), dtype=dtype)
+    X[n:] = 0
+    Xd = X.cuda()
+    Yw = torch.full((H.n_pad, 2 * k), 3.0, dtype=dtype, device="cuda")
+    Yv = Yw[:, k:]
+    s = torch.cuda.current_stream().cuda_stream
+    check(lib().cim_sym_spmm(H.descriptor(), Xd.data_ptr(), Yv.data_ptr(), k, k, 2 * k, 0, s), "cim_sym_spmm")
+    torch.cuda.synchronize()
+    Y1 = Yv.cpu().numpy()[:n]
+    check_result(n, rc, tiles.astype(np.float64), X.numpy()[:n], Y1, dtype)
+    assert torch.all(Yw[:, :k] == 3.0)
+    check(lib().cim_sym_spmm(H.descriptor(), Xd.data_ptr(), Yv.data_ptr(), k, k, 2 * k, CIM_ACCUMULATE, s),
+          "cim_sym_spmm")
+    torch.cuda.synchronize()
+    Y2 = Yv.cpu().numpy()[:n]
+    tol = 1e-5 if dtype == torch.float32 else 1e-12
+    assert np.abs(Y2 - 2 * Y1).max() <= tol * np.abs(Y1).max()
