@@ -83,7 +83,7 @@ struct TcParams {
 // issuer, 1 splitter row warp, 2 splitter column warp, 3 epilogue direct
 // warp, 4 epilogue transposed warp.
 enum : int { P_WAIT0 = 0, P_WAIT1, P_WAIT2, P_WORK0, P_WORK1, P_WORK2, P_WORK3, P_TILES = 14, P_TOTAL = 15, P_SLOTS = 16 };
-constexpr int kProfRoles = 5, kProfCtas = 160;
+constexpr int kProfRoles = 6, kProfCtas = 160;  // role 5: the producer lane
 #ifdef CIM_TC_PROF
 __device__ unsigned long long g_prof[kProfCtas][kProfRoles][P_SLOTS];
 #define TPROF_DECL long long _pa[P_SLOTS] = {0}; long long _pt = clock64(); const long long _p0 = _pt
@@ -259,6 +259,7 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
   uint64_t *full = bars, *empty = bars + S;
   uint64_t *splitf = bars + 2 * S, *ab_empty = splitf + NA;
   uint64_t *d_full = ab_empty + NA, *d_empty = d_full + ND, *meta_f = d_empty + ND;
+  uint64_t *hdr_ready = meta_f + ND;  // [S]: tile producer → X producer, the stage's header is written
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + p.off_tmem);
   int4 *hdrj = reinterpret_cast<int4 *>(smem + p.off_hdrj);
   int4 *meta = reinterpret_cast<int4 *>(smem + p.off_meta);
@@ -267,6 +268,7 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 4);
+      mbar_init(&hdr_ready[s], 1);
     }
     for (int j = 0; j < NA; ++j) {
       mbar_init(&splitf[j], 4);
@@ -295,6 +297,7 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
 
   if (warp == 0) {
     // ================================ producer ================================
+    TPROF_DECL;
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_keep = p.xpol == 1 ? policy_evict_first() : p.xpol == 2 ? policy_evict_normal() : policy_evict_last();
     const unsigned int xblk = p.xblk;
@@ -341,7 +344,9 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
         for (int q = 0; q < cnt; ++q) {
           const int Cb = __shfl_sync(0xffffffffu, myC, q);
           if (lane == 0) {
+            TPROF(P_WORK0);
             mbar_wait_backoff(&empty[stage], phase ^ 1u);
+            TPROF(P_WAIT0);
             unsigned char *st = smem + (size_t)stage * SB;
             const int tt = tb + q;
             const bool diag = Cb == R;
@@ -357,10 +362,11 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
             const int flags = (tt == t0 ? HDR_FIRST : 0) | (tt == t1 - 1 ? HDR_LAST : 0) | (diag ? HDR_DIAG : 0) |
                               (need_xr ? HDR_XR : 0);
             *reinterpret_cast<int4 *>(st + p.off_hdr) = make_int4(R, Cb, flags, 0);
+            // all of the stage's bytes are expected before the X producer
+            // (warp 2) may issue its copies: complete_tx never precedes expect_tx
             mbar_arrive_expect_tx(&full[stage], 16384u + (need_xr ? 2u * xblk : xblk));
+            mbar_arrive(&hdr_ready[stage]);
             bulk_g2s(st, p.vals + (size_t)tt * 16384u, 16384u, &full[stage], pol_stream);
-            bulk_g2s(st + p.off_xc, p.X + (size_t)Cb * xblk, xblk, &full[stage], pol_keep);
-            if (need_xr) bulk_g2s(st + p.off_xr, p.X + (size_t)R * xblk, xblk, &full[stage], pol_keep);
           }
           __syncwarp();
           ++seq;
@@ -377,13 +383,43 @@ __global__ void __launch_bounds__(512, 1) sym_spmm_tc_kernel(const TcParams p) {
       unit1 = unit2;
       u2 = __shfl_sync(0xffffffffu, u3, 0);
     }
+    TPROF_TILE();
+    TPROF_DUMP(5);
     if (lane == 0) {
       // one terminator per splitter group (they take alternate tiles); only
       // the first travels on to the MMA issuer and the epilogue
       for (int e = 0; e < 2; ++e) {
         mbar_wait_backoff(&empty[stage], phase ^ 1u);
         *reinterpret_cast<int4 *>(smem + (size_t)stage * SB + p.off_hdr) = make_int4(0, 0, e ? HDR_TERM2 : HDR_TERM, 0);
+        mbar_arrive(&hdr_ready[stage]);
         mbar_arrive(&full[stage]);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+  } else if (warp == 2) {
+    // ============================ X-block producer ============================
+    // The X_C (and, when the B buffer's row changes, X_R) copies of every
+    // stage, issued by a second warp: a bulk-copy issue blocks its warp while
+    // the copy engine's queue is full, and with one producer warp issuing all
+    // three copies per tile the producer was busy 85% of the time at k = 8
+    // (role timers) — the ring, not the DRAM, paced the kernel.
+    if (lane == 0) {
+      const uint64_t pol_keep = p.xpol == 1 ? policy_evict_first() : p.xpol == 2 ? policy_evict_normal() : policy_evict_last();
+      const unsigned int xblk = p.xblk;
+      int stage = 0;
+      uint32_t phase = 0;
+      while (true) {
+        mbar_wait(&hdr_ready[stage], phase);
+        unsigned char *st = smem + (size_t)stage * SB;
+        const int4 h = *reinterpret_cast<const int4 *>(st + p.off_hdr);
+        if (h.z & HDR_TERM2) break;
+        if (!(h.z & HDR_TERM)) {
+          bulk_g2s(st + p.off_xc, p.X + (size_t)h.y * xblk, xblk, &full[stage], pol_keep);
+          if (h.z & HDR_XR) bulk_g2s(st + p.off_xr, p.X + (size_t)h.x * xblk, xblk, &full[stage], pol_keep);
+        }
         if (++stage == S) {
           stage = 0;
           phase ^= 1u;
@@ -684,7 +720,7 @@ int launch(const cim_half_tiles *H, const void *X, void *Y, long long ldy, cudaS
   p.off_xr = p.off_xc + xblk;
   p.off_hdr = p.off_xr + xblk;
   p.stage_bytes = (p.off_hdr + 16 + 127) & ~127u;
-  const size_t fixed = (size_t)Cf::NA * Cf::BBYTES + 16 * (Cf::NA + Cf::ND) + 8 * (3 * Cf::NA + 3 * Cf::ND) + 64;
+  const size_t fixed = (size_t)Cf::NA * Cf::BBYTES + 16 * (Cf::NA + Cf::ND) + 8 * (3 * Cf::NA + 3 * Cf::ND) + 64 + 8 * 8;
   const size_t budget = 227 * 1024 - 1024;  // minus the manual 1 KB alignment slack
   // bulk Y reductions need dense Y rows and 4 staging blocks; keep them unless
   // they would cost ring stages below 4
@@ -708,7 +744,7 @@ int launch(const cim_half_tiles *H, const void *X, void *Y, long long ldy, cudaS
   p.off_meta = (unsigned int)off;
   off += 16 * Cf::ND;
   p.off_bars = (unsigned int)off;
-  off += 8 * (2 * (size_t)S + 2 * Cf::NA + 3 * Cf::ND);
+  off += 8 * (3 * (size_t)S + 2 * Cf::NA + 3 * Cf::ND);
   off = (off + 15) & ~size_t(15);
   p.off_tmem = (unsigned int)off;
   off += 16;

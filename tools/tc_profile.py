@@ -15,7 +15,7 @@ for _ in range(3):
     Y = pkg.sym_spmm(H, X)
 torch.cuda.synchronize()
 L = pkg.lib()
-buf = np.zeros((160, 5, 16), np.uint64)
+buf = np.zeros((160, 6, 16), np.uint64)
 L.cim_tc_profile_read.argtypes = [ctypes.c_void_p, ctypes.c_int]
 nct = L.cim_tc_profile_read(buf.ctypes.data, 160)
 b = buf[:nct].astype(np.float64)
@@ -23,8 +23,9 @@ slots = {0: ["wait_split", "wait_d_empty", "", "issue"],
          1: ["wait_full", "wait_ab_empty", "", "t_split", "build_b+arrive", "wait_st+fence", "loop"],
          2: ["wait_full", "wait_ab_empty", "", "t_split", "build_b+arrive", "wait_st+fence", "loop"],
          3: ["wait_meta", "wait_d_full", "", "work"],
-         4: ["wait_meta", "wait_d_full", "", "work"]}
-roles = ["mma", "splitter rows", "splitter cols", "epilogue direct", "epilogue transposed"]
+         4: ["wait_meta", "wait_d_full", "", "work"],
+         5: ["wait_empty", "", "", "work"]}
+roles = ["mma", "splitter rows", "splitter cols", "epilogue direct", "epilogue transposed", "producer"]
 for r, role in enumerate(roles):
     tot = b[:, r, 15].mean()
     tiles = b[:, r, 14].mean()
