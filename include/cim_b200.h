@@ -148,6 +148,12 @@ typedef struct cim_sparse_tiles {
   int64_t         csr_nnz;
   int64_t         csr_all;   /* 1: the CSR holds the staged tiles too (the
                                 staged kernel is skipped by the SpMM) */
+  int64_t         csr_symmetric; /* 1: the CSR rows hold both triangles of
+                                the sparse tiles (each off-diagonal-block
+                                entry also stored mirrored in its column's
+                                row): the apply is a gather per row with no
+                                transposed reductions — twice the CSR bytes
+                                for the small tiles, no L2 atomics per entry */
 } cim_sparse_tiles;
 
 typedef struct cim_half_tiles {

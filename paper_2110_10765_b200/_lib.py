@@ -90,6 +90,7 @@ class CimSparseTiles(ctypes.Structure):
         ("csr_rows", ctypes.c_int64),
         ("csr_nnz", ctypes.c_int64),
         ("csr_all", ctypes.c_int64),
+        ("csr_symmetric", ctypes.c_int64),
     ]
 
 

@@ -115,7 +115,8 @@ __device__ __forceinline__ void red_vec(T *p, const T (&s)[KV]) {
 }
 
 // LPR lanes per row (a warp holds 32 / LPR rows), KV vectors per pass.
-template <typename T, int KV, int LPR>
+// SYM: the rows hold both triangles (csr_symmetric) — gathers only.
+template <typename T, int KV, int LPR, bool SYM>
 __global__ void __launch_bounds__(256) csr_spmm_kernel(const long long *__restrict__ ptr,
                                                        const int32_t *__restrict__ col, const T *__restrict__ val,
                                                        long long rows, const T *__restrict__ X, T *__restrict__ Y,
@@ -141,6 +142,7 @@ __global__ void __launch_bounds__(256) csr_spmm_kernel(const long long *__restri
         ld_vec<T, KV>(x1, X + (long long)j1 * k + v0);
 #pragma unroll
         for (int q = 0; q < KV; ++q) acc[q] = fma(w0, x0[q], fma(w1, x1[q], acc[q]));
+        if (SYM) continue;
         if ((j0 >> 6) != bi) {
 #pragma unroll
           for (int q = 0; q < KV; ++q) t[q] = w0 * xi[q];
@@ -159,7 +161,7 @@ __global__ void __launch_bounds__(256) csr_spmm_kernel(const long long *__restri
         ld_vec<T, KV>(x, X + (long long)j * k + v0);
 #pragma unroll
         for (int q = 0; q < KV; ++q) acc[q] = fma(w, x[q], acc[q]);
-        if ((j >> 6) != bi) {
+        if (!SYM && (j >> 6) != bi) {
 #pragma unroll
           for (int q = 0; q < KV; ++q) t[q] = w * xi[q];
           red_vec<T, KV>(Y + (long long)j * ldy + v0, t);
@@ -184,10 +186,14 @@ int launch_csr_kv(const cim_sparse_tiles *S, const void *X, void *Y, int k, long
   const T *v = static_cast<const T *>(S->csr_val);
   const long long per_block = avg >= 24.0 ? 8 : 32;  // rows per 256-thread block (LPR 32 or 8)
   const unsigned grid = (unsigned)std::min<long long>((rows + per_block - 1) / per_block, (long long)sms * 16);
-  if (avg >= 24.0)
-    csr_spmm_kernel<T, KV, 32><<<grid, 256, 0, stream>>>(reinterpret_cast<const long long *>(S->csr_ptr), S->csr_col, v, rows, x, y, k, ldy);
-  else
-    csr_spmm_kernel<T, KV, 8><<<grid, 256, 0, stream>>>(reinterpret_cast<const long long *>(S->csr_ptr), S->csr_col, v, rows, x, y, k, ldy);
+  const long long *ptr = reinterpret_cast<const long long *>(S->csr_ptr);
+  if (S->csr_symmetric) {
+    if (avg >= 24.0) csr_spmm_kernel<T, KV, 32, true><<<grid, 256, 0, stream>>>(ptr, S->csr_col, v, rows, x, y, k, ldy);
+    else csr_spmm_kernel<T, KV, 8, true><<<grid, 256, 0, stream>>>(ptr, S->csr_col, v, rows, x, y, k, ldy);
+  } else {
+    if (avg >= 24.0) csr_spmm_kernel<T, KV, 32, false><<<grid, 256, 0, stream>>>(ptr, S->csr_col, v, rows, x, y, k, ldy);
+    else csr_spmm_kernel<T, KV, 8, false><<<grid, 256, 0, stream>>>(ptr, S->csr_col, v, rows, x, y, k, ldy);
+  }
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? CIM_OK : set_error(CIM_ECUDA, std::string("csr_spmm launch: ") + cudaGetErrorString(e));
 }

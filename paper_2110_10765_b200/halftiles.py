@@ -147,6 +147,30 @@ def sparse_tile_offsets(rowcnt: torch.Tensor, n_tiles: int):
     return rowptr[:T], counts[:T], off
 
 
+def _mirror_csr(ptr: torch.Tensor, col: torch.Tensor, val: torch.Tensor, n_pad: int):
+    """Both triangles of a block-upper row-CSR (device): every entry (i, j)
+    whose j lies outside i's 64-block is also stored as (j, i) in row j;
+    entries of diagonal blocks are already stored both ways.  Rows stay
+    column-sorted.  Returns (ptr, col, val, nnz)."""
+    nnz = int(ptr[-1].item())
+    if nnz == 0:
+        return ptr, col, val, 0
+    dev = ptr.device
+    counts = ptr[1:] - ptr[:-1]
+    rows = torch.repeat_interleave(torch.arange(n_pad, device=dev), counts)
+    c = col[:nnz].long()
+    v = val[:nnz]
+    mask = (c >> 6) != (rows >> 6)
+    r2 = torch.cat([rows, c[mask]])
+    c2 = torch.cat([c, rows[mask]])
+    v2 = torch.cat([v, v[mask]])
+    order = torch.argsort(r2 * n_pad + c2)
+    r2, c2, v2 = r2[order], c2[order], v2[order]
+    cnt = torch.bincount(r2, minlength=n_pad)
+    ptr2 = exclusive_scan(cnt[:n_pad].to(torch.int64))
+    return ptr2, c2.to(torch.int32).contiguous(), v2.contiguous(), int(r2.numel())
+
+
 def exclusive_scan(x: torch.Tensor) -> torch.Tensor:
     """Offsets + total of int64 device counts (scan_serial, scan.py:131-139,
     followed by the total, as CountsAndOffsets holds them): y[i] = Σ_(j<i) x[j],
@@ -277,6 +301,13 @@ class SparseTiles:
     # lazily for the row-walk apply; use_csr=False keeps the entry-parallel path
     use_csr: bool = field(default_factory=lambda: os.environ.get("CIM_SPARSE_CSR", "1") != "0")
     _csr: tuple | None = field(default=None, repr=False)
+    # csr_symmetric: the CSR rows also hold the mirrored off-diagonal-block
+    # entries (a gather per row, no transposed L2 reductions; 2x the CSR
+    # bytes).  The default: the half-stored CSR is bound by the L2's
+    # reduction rate (basis skeleton n = 262,144: 0.713 → 0.506 ms per apply);
+    # CIM_SPARSE_CSR_SYM=0 keeps one triangle.  The tiles themselves stay
+    # half-stored — the CSR is the apply's derived copy either way.
+    csr_symmetric: bool = field(default_factory=lambda: os.environ.get("CIM_SPARSE_CSR_SYM", "1") != "0")
 
     @property
     def n_tiles(self) -> int:
@@ -368,6 +399,8 @@ class SparseTiles:
             check(L.cim_sparse_csr_fill(ctypes.byref(base), CIM_F32 if self.vals.dtype == torch.float32 else CIM_F64,
                                         panel_R.data_ptr(), panel_ptr.data_ptr(), int(starts.size), ptr.data_ptr(),
                                         col.data_ptr(), val.data_ptr(), stream), "cim_sparse_csr_fill")
+        if self.csr_symmetric:
+            ptr, col, val, nnz = _mirror_csr(ptr, col, val, int(n_pad))
         self._csr = (ptr, col, val, nnz, int(n_pad))
         self._csr_list = all_dev  # keeps the merged list alive for the fill
         self._desc = None
@@ -402,6 +435,7 @@ class SparseTiles:
                 ptr, col, val, nnz, rows = self._csr
                 d.csr_ptr, d.csr_col, d.csr_val = ptr.data_ptr(), col.data_ptr(), val.data_ptr()
                 d.csr_rows, d.csr_nnz, d.csr_all = rows, nnz, 1
+                d.csr_symmetric = 1 if self.csr_symmetric else 0
             self._desc = d
         return self._desc
 
@@ -899,6 +933,22 @@ class HalfTiles:
                 check(lib().cim_unpack_tiles(self.vals.data_ptr(), self.n_tiles, _dtype_code(self.dtype),
                                              LAYOUTS[self.layout], out.data_ptr(), stream), "cim_unpack_tiles")
         return out
+
+    def use_symmetric_csr(self, flag: bool = True) -> "HalfTiles":
+        """Apply the sparse tiles' row-CSR with both triangles stored (each
+        off-diagonal-block entry mirrored into its column's row): every row a
+        gather, no per-entry transposed reduction into Y — the L2 reduction
+        rate (~95 G rows/s) bounds the half-stored CSR on basis skeletons.
+        Costs 2x the CSR entry bytes of the small tiles; the dense tiles stay
+        half-stored.  Returns self."""
+        if self.sparse is not None:
+            self.sparse.csr_symmetric = bool(flag)
+            self.sparse._csr = None
+            self.sparse._desc = None
+            if flag:
+                self.sparse.use_csr = True
+        self._desc = None
+        return self
 
     def export_dense(self) -> tuple[np.ndarray, np.ndarray]:
         """Host (tile_rc, row-major tiles) of every stored tile — dense and

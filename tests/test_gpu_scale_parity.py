@@ -389,7 +389,7 @@ def test_small_tiles_csr_path(pkg, dtype, k, fill, monkeypatch):
 
     monkeypatch.setattr(halftiles, "CSR_MIN_ROW_ENTRIES", 0)
     n = 5000
-    H = pkg.HalfTiles.synthetic_sparse(n, 0.3, fill=fill, seed=4, fill_seed=2, dtype=dtype)
+    H = pkg.HalfTiles.synthetic_sparse(n, 0.3, fill=fill, seed=4, fill_seed=2, dtype=dtype).use_symmetric_csr(False)
     sp = H.sparse
     st, sm = sp.work_split()
     assert sm.numel() > 0
@@ -417,17 +417,34 @@ def test_small_tiles_csr_path(pkg, dtype, k, fill, monkeypatch):
     H2.sparse.use_csr = False
     Y2 = pkg.sym_spmm(H2, X.cuda()).cpu().numpy()
     assert np.abs(Y2 - Y).max() <= (1e-5 if dtype == torch.float32 else 1e-12) * max(1.0, np.abs(Y).max())
+    # both triangles in the CSR rows (use_symmetric_csr): exactly the full
+    # matrix's sparse entries, applied by gathers only
+    H3 = pkg.HalfTiles.synthetic_sparse(n, 0.3, fill=fill, seed=4, fill_seed=2, dtype=dtype).use_symmetric_csr()
+    H3.descriptor()
+    p3, c3, v3, nnz3, _ = H3.sparse._csr
+    full = sorted(want + [(j, i, w) for (i, j, w) in want if i // 64 != j // 64])
+    assert nnz3 == len(full)
+    rows3 = np.repeat(np.arange(rows), np.diff(p3.cpu().numpy()))
+    got3 = sorted(zip(rows3.tolist(), c3[:nnz3].cpu().numpy().tolist(), v3[:nnz3].cpu().numpy().tolist()))
+    assert got3 == full
+    Y3 = pkg.sym_spmm(H3, X.cuda()).cpu().numpy()
+    assert np.abs(Y3 - Y).max() <= (1e-5 if dtype == torch.float32 else 1e-12) * max(1.0, np.abs(Y).max())
 
 
-def test_basis_skeleton_csr_path(pkg):
+@pytest.mark.parametrize("symmetric", [False, True])
+def test_basis_skeleton_csr_path(pkg, symmetric):
     """A reference-style basis skeleton (the golden n=1024 fixture's basis,
     device-built) through the CSR small-tile path vs the reference's scipy
     product."""
     f = load_fixture("skel_n1024.npz")
     H = pkg.HalfTiles.from_basis(f["basis_occ"], f["basis_bits_lo"], rank=int(f["rank_threshold"]) // 2)
+    if symmetric:
+        H.use_symmetric_csr()
     X = torch.from_numpy(f["X"]).cuda()
     Y = pkg.sym_spmm(H, X).cpu().numpy()
     assert H.sparse is not None
+    if symmetric and H.sparse._csr is not None:  # both triangles: nnz = 2·off-block + diagonal-block entries
+        assert H.sparse.csr_symmetric
     ptr = H.sparse._csr[0] if H.sparse._csr is not None else None
     if ptr is not None:
         assert int(ptr[-1]) > 0
