@@ -258,7 +258,12 @@ def fragment_pack_host(tiles: np.ndarray, layout: str = "frag") -> np.ndarray:
     return np.ascontiguousarray(tiles.reshape(T, 4096)[:, row * BLOCK + col])
 
 
-CSR_MIN_ROW_ENTRIES = 12  # mean entries per non-empty row below which small tiles stay entry-parallel
+# mean (one-triangle) entries per non-empty row below which small tiles stay
+# entry-parallel: 12 for the half-stored CSR; with both triangles in the rows
+# (no per-entry reductions) the row walk already wins at 4.8 (1%-fill C2
+# family: 0.511 → 0.490 ms), so 4
+CSR_MIN_ROW_ENTRIES = int(os.environ.get("CIM_CSR_MIN_ROW", "12"))
+CSR_MIN_ROW_ENTRIES_SYM = int(os.environ.get("CIM_CSR_MIN_ROW_SYM", "4"))
 SPARSE_ALIGN = 16  # entries: every sparse tile's entry range starts 16-entry aligned (vector staging)
 SPARSE_PTR_STRIDE = 72  # uint16 row / column pointers per sparse tile (65 used): 144-byte, 16-B-aligned rows
 
@@ -350,7 +355,7 @@ class SparseTiles:
         ne = np.diff(self.entry_off_host)
         _, n_st, sm, n_sm, _ = self._split
         small_entries = int(ne[sm[:n_sm].cpu().numpy()].sum()) if n_sm else 0
-        return 2 * small_entries >= int(ne.sum())
+        return 2 * small_entries >= float(os.environ.get("CIM_CSR_SMALL_SHARE", "0.5")) * 2 * int(ne.sum())
 
     def build_csr(self, n_pad: int):
         """The row-CSR of the small tiles on the device (cim_sparse_csr_count →
@@ -377,7 +382,7 @@ class SparseTiles:
         ptr = exclusive_scan(cnt[:n_pad])
         nnz = int(ptr[-1].item())
         busy = int((cnt[:n_pad] > 0).sum().item())
-        if nnz < CSR_MIN_ROW_ENTRIES * max(busy, 1):
+        if nnz < (CSR_MIN_ROW_ENTRIES_SYM if self.csr_symmetric else CSR_MIN_ROW_ENTRIES) * max(busy, 1):
             # rows this short leave most lanes of a row group idle: the
             # entry-parallel small-tile kernel is faster (1%-fill C2 family:
             # 4.8 entries per row, 0.52 vs 0.57 ms) — keep it

@@ -388,6 +388,7 @@ def test_small_tiles_csr_path(pkg, dtype, k, fill, monkeypatch):
     from paper_2110_10765_b200 import halftiles
 
     monkeypatch.setattr(halftiles, "CSR_MIN_ROW_ENTRIES", 0)
+    monkeypatch.setattr(halftiles, "CSR_MIN_ROW_ENTRIES_SYM", 0)
     n = 5000
     H = pkg.HalfTiles.synthetic_sparse(n, 0.3, fill=fill, seed=4, fill_seed=2, dtype=dtype).use_symmetric_csr(False)
     sp = H.sparse
