@@ -30,6 +30,16 @@
 #include "common.cuh"
 #include "host_util.h"
 
+#ifndef CIM_CSR_SYM_ILP
+#define CIM_CSR_SYM_ILP 4  // entries gathered per lane per step in the symmetric row walk (2 or 4)
+#endif
+#ifndef CIM_CSR_SYM_MINB
+#define CIM_CSR_SYM_MINB 4  // resident 256-thread blocks per SM (64 registers: 4 gathers of 32 B in flight, no spills)
+#endif
+#ifndef CIM_CSR_SYM_SUB
+#define CIM_CSR_SYM_SUB 8  // most lanes sharing one entry's X row in the symmetric walk (1 = one lane per entry)
+#endif
+
 namespace cim {
 namespace {
 
@@ -115,8 +125,8 @@ __device__ __forceinline__ void red_vec(T *p, const T (&s)[KV]) {
 }
 
 // LPR lanes per row (a warp holds 32 / LPR rows), KV vectors per pass.
-// SYM: the rows hold both triangles (csr_symmetric) — gathers only.
-template <typename T, int KV, int LPR, bool SYM>
+// The rows hold one triangle: the transposed product is scattered.
+template <typename T, int KV, int LPR>
 __global__ void __launch_bounds__(256) csr_spmm_kernel(const long long *__restrict__ ptr,
                                                        const int32_t *__restrict__ col, const T *__restrict__ val,
                                                        long long rows, const T *__restrict__ X, T *__restrict__ Y,
@@ -142,7 +152,6 @@ __global__ void __launch_bounds__(256) csr_spmm_kernel(const long long *__restri
         ld_vec<T, KV>(x1, X + (long long)j1 * k + v0);
 #pragma unroll
         for (int q = 0; q < KV; ++q) acc[q] = fma(w0, x0[q], fma(w1, x1[q], acc[q]));
-        if (SYM) continue;
         if ((j0 >> 6) != bi) {
 #pragma unroll
           for (int q = 0; q < KV; ++q) t[q] = w0 * xi[q];
@@ -161,7 +170,7 @@ __global__ void __launch_bounds__(256) csr_spmm_kernel(const long long *__restri
         ld_vec<T, KV>(x, X + (long long)j * k + v0);
 #pragma unroll
         for (int q = 0; q < KV; ++q) acc[q] = fma(w, x[q], acc[q]);
-        if (!SYM && (j >> 6) != bi) {
+        if ((j >> 6) != bi) {
 #pragma unroll
           for (int q = 0; q < KV; ++q) t[q] = w * xi[q];
           red_vec<T, KV>(Y + (long long)j * ldy + v0, t);
@@ -173,6 +182,82 @@ __global__ void __launch_bounds__(256) csr_spmm_kernel(const long long *__restri
         for (int q = 0; q < KV; ++q) acc[q] += __shfl_xor_sync(gmask, acc[q], off);
       if (sl == 0) red_vec<T, KV>(Y + i * ldy + v0, acc);
     }
+  }
+}
+
+// The rows hold both triangles (csr_symmetric): gathers only, one reduction
+// per row.  The walk is bound by the L1's gather wavefronts (one per X row
+// slice, every entry a different line): SUB lanes share one entry, each
+// gathering KV vectors of the same X row, so an entry whose row is 64 or 128
+// bytes (f32 k = 16 / 32) costs one line request instead of two or four;
+// LPR / SUB entries per row group per step, U of them in flight per lane.
+template <typename T, int KV, int LPR, int SUB>
+__global__ void __launch_bounds__(256, CIM_CSR_SYM_MINB) csr_sym_kernel(const long long *__restrict__ ptr,
+                                                      const int32_t *__restrict__ col, const T *__restrict__ val,
+                                                      long long rows, const T *__restrict__ X, T *__restrict__ Y,
+                                                      int k, long long ldy) {
+  constexpr int U = CIM_CSR_SYM_ILP, ES = LPR / SUB;
+  const int lane = threadIdx.x & 31, sl = lane % LPR, es = sl / SUB, part = sl % SUB;
+  const unsigned gmask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (lane - sl));
+  const long long groups = ((long long)gridDim.x * blockDim.x) / LPR;
+  for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / LPR; i < rows; i += groups) {
+    const long long p0 = ptr[i], p1 = ptr[i + 1];
+    if (p0 == p1) continue;  // uniform within the row group
+    for (int v0 = part * KV; v0 < k; v0 += SUB * KV) {
+      T acc[KV];
+#pragma unroll
+      for (int q = 0; q < KV; ++q) acc[q] = T(0);
+      long long e = p0 + es;
+      for (; e + (U - 1) * ES < p1; e += U * ES) {
+        int j[U];
+        T w[U], x[U][KV];
+#pragma unroll
+        for (int u = 0; u < U; ++u) j[u] = __ldg(col + e + u * ES), w[u] = __ldg(val + e + u * ES);
+#pragma unroll
+        for (int u = 0; u < U; ++u) ld_vec<T, KV>(x[u], X + (long long)j[u] * k + v0);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int q = 0; q < KV; ++q) acc[q] = fma(w[u], x[u][q], acc[q]);
+      }
+      if (U > 2 && e + ES < p1) {
+        const int j0 = __ldg(col + e), j1 = __ldg(col + e + ES);
+        const T w0 = __ldg(val + e), w1 = __ldg(val + e + ES);
+        T x0[KV], x1[KV];
+        ld_vec<T, KV>(x0, X + (long long)j0 * k + v0);
+        ld_vec<T, KV>(x1, X + (long long)j1 * k + v0);
+#pragma unroll
+        for (int q = 0; q < KV; ++q) acc[q] = fma(w0, x0[q], fma(w1, x1[q], acc[q]));
+        e += 2 * ES;
+      }
+      for (; e < p1; e += ES) {
+        const int j = __ldg(col + e);
+        const T w = __ldg(val + e);
+        T x[KV];
+        ld_vec<T, KV>(x, X + (long long)j * k + v0);
+#pragma unroll
+        for (int q = 0; q < KV; ++q) acc[q] = fma(w, x[q], acc[q]);
+      }
+#pragma unroll
+      for (int off = LPR / 2; off >= SUB; off >>= 1)
+#pragma unroll
+        for (int q = 0; q < KV; ++q) acc[q] += __shfl_xor_sync(gmask, acc[q], off);
+      if (es == 0) red_vec<T, KV>(Y + i * ldy + v0, acc);
+    }
+  }
+}
+
+template <typename T, int KV, int LPR>
+void launch_csr_sym(const long long *ptr, const int32_t *col, const T *v, long long rows, const T *x, T *y, int k,
+                    long long ldy, unsigned grid, cudaStream_t stream) {
+  int sub = 1;
+  if constexpr (sizeof(T) * KV == 32)  // full 32-byte slices: lanes share an entry's X row
+    while (sub < CIM_CSR_SYM_SUB && sub < LPR && k % (2 * sub * KV) == 0) sub *= 2;
+  switch (sub) {
+    case 8: csr_sym_kernel<T, KV, LPR, 8><<<grid, 256, 0, stream>>>(ptr, col, v, rows, x, y, k, ldy); break;
+    case 4: csr_sym_kernel<T, KV, LPR, 4><<<grid, 256, 0, stream>>>(ptr, col, v, rows, x, y, k, ldy); break;
+    case 2: csr_sym_kernel<T, KV, LPR, 2><<<grid, 256, 0, stream>>>(ptr, col, v, rows, x, y, k, ldy); break;
+    default: csr_sym_kernel<T, KV, LPR, 1><<<grid, 256, 0, stream>>>(ptr, col, v, rows, x, y, k, ldy); break;
   }
 }
 
@@ -188,11 +273,11 @@ int launch_csr_kv(const cim_sparse_tiles *S, const void *X, void *Y, int k, long
   const unsigned grid = (unsigned)std::min<long long>((rows + per_block - 1) / per_block, (long long)sms * 16);
   const long long *ptr = reinterpret_cast<const long long *>(S->csr_ptr);
   if (S->csr_symmetric) {
-    if (avg >= 24.0) csr_spmm_kernel<T, KV, 32, true><<<grid, 256, 0, stream>>>(ptr, S->csr_col, v, rows, x, y, k, ldy);
-    else csr_spmm_kernel<T, KV, 8, true><<<grid, 256, 0, stream>>>(ptr, S->csr_col, v, rows, x, y, k, ldy);
+    if (avg >= 24.0) launch_csr_sym<T, KV, 32>(ptr, S->csr_col, v, rows, x, y, k, ldy, grid, stream);
+    else launch_csr_sym<T, KV, 8>(ptr, S->csr_col, v, rows, x, y, k, ldy, grid, stream);
   } else {
-    if (avg >= 24.0) csr_spmm_kernel<T, KV, 32, false><<<grid, 256, 0, stream>>>(ptr, S->csr_col, v, rows, x, y, k, ldy);
-    else csr_spmm_kernel<T, KV, 8, false><<<grid, 256, 0, stream>>>(ptr, S->csr_col, v, rows, x, y, k, ldy);
+    if (avg >= 24.0) csr_spmm_kernel<T, KV, 32><<<grid, 256, 0, stream>>>(ptr, S->csr_col, v, rows, x, y, k, ldy);
+    else csr_spmm_kernel<T, KV, 8><<<grid, 256, 0, stream>>>(ptr, S->csr_col, v, rows, x, y, k, ldy);
   }
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? CIM_OK : set_error(CIM_ECUDA, std::string("csr_spmm launch: ") + cudaGetErrorString(e));

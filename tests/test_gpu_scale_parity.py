@@ -377,7 +377,9 @@ def test_c3_full_size_256_rows(pkg):
 # ----------------------------------------------------------------------------
 
 @pytest.mark.parametrize("dtype,k", [(torch.float32, 8), (torch.float32, 3), (torch.float32, 16),
-                                     (torch.float64, 4), (torch.float64, 1)])
+                                     (torch.float32, 24), (torch.float32, 32), (torch.float32, 48),
+                                     (torch.float32, 64), (torch.float64, 4), (torch.float64, 1),
+                                     (torch.float64, 8), (torch.float64, 16), (torch.float64, 32)])
 @pytest.mark.parametrize("fill", [0.004, 0.02])
 def test_small_tiles_csr_path(pkg, dtype, k, fill, monkeypatch):
     """Tiles of a few dozen entries go through the row-CSR of the small tiles
