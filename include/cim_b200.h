@@ -303,6 +303,17 @@ CIM_API int cim_tsmm_blocked_hc(const float *A, int64_t lda, int32_t a_bw, int64
 CIM_API int cim_block_residual(const float *X, const float *AX, const double *lam_host, int32_t m, float *W,
                                int64_t rows, int32_t bw, void *stream);
 
+/* Device: the LOBPCG Ritz update fused with the next residual, over bw = 8
+   block-major f32 slots.  S and AS are q/8 consecutive slots each (q ∈ {8,
+   16, 24, 32, 48}, slot stride bstride floats); C_host is the HOST q × 16
+   row-major f32 coefficient matrix [C_p | C].  Writes five consecutive slots
+   of Out (stride o_bstride): [S·C_p, S·C, AS·C − (S·C)·diag(λ), AS·C_p,
+   AS·C] = [P', X', W', AP', AX'] with λ_j from HOST f64 lam[0..m), 0 for
+   j ≥ m.  Out must not overlap S or AS. */
+CIM_API int cim_ritz_update_b8(const float *S, const float *AS, int64_t bstride, int32_t q, const float *C_host,
+                               const double *lam_host, int32_t m, float *Out, int64_t o_bstride, int64_t rows,
+                               void *stream);
+
 /*
  * Device: values on the entries of sparse tiles — vals_out[e] = value(i, j)
  * of entry e where mask[e] != 0 (mask: the pattern's own values, or NULL =

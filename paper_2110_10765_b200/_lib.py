@@ -62,6 +62,7 @@ EXPORTS = (
     "cim_sparse_tile_offsets",
     "cim_sparse_csr_count",
     "cim_sparse_csr_fill",
+    "cim_ritz_update_b8",
 )
 
 
@@ -207,6 +208,8 @@ def lib() -> ctypes.CDLL:
             getattr(L, name).restype = c.c_int
     L.cim_block_residual.argtypes = [c.c_void_p, c.c_void_p, c.c_void_p, c.c_int32, c.c_void_p, c.c_int64, c.c_int32,
                                      c.c_void_p]
+    L.cim_ritz_update_b8.argtypes = [c.c_void_p, c.c_void_p, c.c_int64, c.c_int32, c.c_void_p, c.c_void_p, c.c_int32,
+                                     c.c_void_p, c.c_int64, c.c_int64, c.c_void_p]
     L.cim_host_batch_workspace_bytes.restype = c.c_uint64
     L.cim_gram_workspace_bytes.restype = c.c_uint64
     _lib = L

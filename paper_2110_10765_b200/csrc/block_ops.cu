@@ -759,3 +759,106 @@ extern "C" int cim_block_residual(const float *X, const float *AX, const double 
   if (e != cudaSuccess) return cim::set_error(CIM_ECUDA, std::string("block_residual: ") + cudaGetErrorString(e));
   return CIM_OK;
 }
+
+namespace {
+// ---------------------------------------------------------------------------
+// LOBPCG Ritz update fused with the next residual (bw = 8 block-major f32
+// slots): per row, [P' X'] = S·C and [AP' AX'] = AS·C (C = [C_p | C], q × 16)
+// and W' = AX' − X'·diag(λ), written into five consecutive slots
+// [P' X' W' AP' AX'] of the other work buffer.  One pass reads the 2·q/8
+// input slots and writes five, where two tsmm passes and the residual pass
+// read and wrote 2·q/8 + 7.  C and λ ride in the kernel parameters.
+// ---------------------------------------------------------------------------
+struct RitzPar {
+  float c[48 * 16];
+  float lam[8];
+};
+
+template <int Q>
+__device__ __forceinline__ void ritz_load(const float *__restrict__ A, long long bstride, long long r, float (&a)[Q]) {
+#pragma unroll
+  for (int s = 0; s < Q / 8; ++s) {
+    const float4 *src = reinterpret_cast<const float4 *>(A + s * bstride + r * 8);
+    const float4 u = __ldcs(src), v = __ldcs(src + 1);  // streamed once
+    a[8 * s + 0] = u.x, a[8 * s + 1] = u.y, a[8 * s + 2] = u.z, a[8 * s + 3] = u.w;
+    a[8 * s + 4] = v.x, a[8 * s + 5] = v.y, a[8 * s + 6] = v.z, a[8 * s + 7] = v.w;
+  }
+}
+
+template <int Q>
+__device__ __forceinline__ void ritz_mul(const float (&a)[Q], const float *c, float (&o)[16]) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) o[j] = 0.f;
+#pragma unroll
+  for (int i = 0; i < Q; ++i)
+#pragma unroll
+    for (int j = 0; j < 16; ++j) o[j] = fmaf(a[i], c[i * 16 + j], o[j]);
+}
+
+__device__ __forceinline__ void st8(float *dst, const float *v) {
+  float4 *d = reinterpret_cast<float4 *>(dst);
+  d[0] = make_float4(v[0], v[1], v[2], v[3]);
+  d[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+
+// Lane pairs share a row: the even lane multiplies the S row ([P' X']),
+// the odd lane the AS row ([AP' AX']) and forms W' with X' from its partner
+// (one shuffle) — half the registers of one thread per row (whose loads
+// ptxas interleaved with the first product's FMAs), twice the resident
+// warps.
+template <int Q>
+__global__ void __launch_bounds__(256) ritz_update_b8_kernel(const float *__restrict__ S, const float *__restrict__ AS,
+                                                             long long bstride, float *__restrict__ Out,
+                                                             long long o_bstride, long long rows, const RitzPar par) {
+  const int h = threadIdx.x & 1;
+  const long long step = ((long long)gridDim.x * blockDim.x) >> 1;
+  for (long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 1; r < rows; r += step) {
+    float a[Q], o[16], x[8];
+    ritz_load<Q>(h ? AS : S, bstride, r, a);
+    ritz_mul<Q>(a, par.c, o);
+    const unsigned mask = __activemask();  // both lanes of a pair are in or out together
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = __shfl_xor_sync(mask, o[8 + j], 1);  // odd lane: X' of the row
+    float *dst = Out + (h ? 3 : 0) * o_bstride + r * 8;
+    st8(dst, o);                  // P' | AP'
+    st8(dst + o_bstride, o + 8);  // X' | AX'
+    if (h) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = fmaf(-par.lam[j], x[j], o[8 + j]);
+      st8(Out + 2 * o_bstride + r * 8, x);  // W' = AX' − X'Λ
+    }
+  }
+}
+}  // namespace
+
+extern "C" int cim_ritz_update_b8(const float *S, const float *AS, int64_t bstride, int32_t q, const float *C_host,
+                                  const double *lam_host, int32_t m, float *Out, int64_t o_bstride, int64_t rows,
+                                  void *stream_) {
+  cim::clear_error();
+  if (q != 8 && q != 16 && q != 24 && q != 32 && q != 48) return cim::set_error(CIM_EINVAL, "q must be 8, 16, 24, 32 or 48");
+  if (m < 0 || m > 8) return cim::set_error(CIM_EINVAL, "m must be in [0, 8]");
+  if (rows < 0) return cim::set_error(CIM_EINVAL, "rows must be >= 0");
+  if (rows == 0) return CIM_OK;
+  if (!S || !AS || !Out || !C_host || (m > 0 && !lam_host)) return cim::set_error(CIM_EINVAL, "NULL pointer");
+  if ((reinterpret_cast<uintptr_t>(S) | reinterpret_cast<uintptr_t>(AS) | reinterpret_cast<uintptr_t>(Out)) & 15 ||
+      (bstride & 3) || (o_bstride & 3))
+    return cim::set_error(CIM_EINVAL, "slots must be 16-byte aligned");
+  RitzPar par{};
+  std::memcpy(par.c, C_host, sizeof(float) * (size_t)q * 16);
+  for (int j = 0; j < m; ++j) par.lam[j] = (float)lam_host[j];
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned blocks = (unsigned)std::min<long long>((rows + 255) / 256, 16LL * sms);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
+  switch (q) {
+    case 8: ritz_update_b8_kernel<8><<<blocks, 256, 0, st>>>(S, AS, bstride, Out, o_bstride, rows, par); break;
+    case 16: ritz_update_b8_kernel<16><<<blocks, 256, 0, st>>>(S, AS, bstride, Out, o_bstride, rows, par); break;
+    case 24: ritz_update_b8_kernel<24><<<blocks, 256, 0, st>>>(S, AS, bstride, Out, o_bstride, rows, par); break;
+    case 32: ritz_update_b8_kernel<32><<<blocks, 256, 0, st>>>(S, AS, bstride, Out, o_bstride, rows, par); break;
+    default: ritz_update_b8_kernel<48><<<blocks, 256, 0, st>>>(S, AS, bstride, Out, o_bstride, rows, par); break;
+  }
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cim::set_error(CIM_ECUDA, std::string("ritz_update_b8: ") + cudaGetErrorString(e));
+  return CIM_OK;
+}

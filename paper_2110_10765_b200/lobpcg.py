@@ -119,22 +119,47 @@ def tsmm(A: torch.Tensor, C: torch.Tensor, out: torch.Tensor, alpha: float = 1.0
         out.mul_(beta).add_(prod, alpha=alpha)
 
 
+def _chol_inv_t(M: np.ndarray, eps: float) -> np.ndarray | None:
+    """L⁻ᵀ for M = L·Lᵀ when M is numerically positive definite (LAPACK
+    condition estimate above ``eps``), else None.  LAPACK's symmetric eigen
+    solver costs ~60–80 µs at 24 × 24 on the host — the solver's critical
+    path while the GPU waits — where Cholesky, its condition estimate and
+    the triangular inverse take ~20 µs."""
+    from scipy.linalg import lapack
+
+    L, info = lapack.dpotrf(M, lower=1, clean=1)
+    if info != 0:
+        return None
+    rc, info = lapack.dpocon(L, float(np.abs(M).sum(0).max()), uplo="L")
+    if info != 0 or not rc > eps:
+        return None
+    Li, info = lapack.dtrtri(L, lower=1)
+    return Li.T if info == 0 else None
+
+
 def _orth_factor(M: np.ndarray, eps: float = 1e-12) -> np.ndarray:
     """T with (V·T)ᵀ(V·T) = I given M = VᵀV; numerically dependent columns
     are dropped (T has ≤ M.shape[0] columns)."""
     M = 0.5 * (M + M.T)
+    T = _chol_inv_t(M, 1e-8)
+    if T is not None:
+        return T
     w, U = np.linalg.eigh(M)
     keep = w > eps * max(w.max(), 1e-300)
     return U[:, keep] / np.sqrt(w[keep])
 
 
 def _rayleigh_ritz(G: np.ndarray, M: np.ndarray, m: int, largest: bool, eps: float = 1e-10):
-    """Lowest (or largest) m solutions of G c = λ M c with M-orthonormal c."""
+    """Lowest (or largest) m solutions of G c = λ M c with M-orthonormal c.
+    Well-conditioned M (the usual case): M = L·Lᵀ, one eigen solve of
+    L⁻¹·G·L⁻ᵀ; otherwise M's eigenbasis drops the dependent directions."""
     G = 0.5 * (G + G.T)
     M = 0.5 * (M + M.T)
-    w, U = np.linalg.eigh(M)
-    keep = w > eps * w.max()
-    T = U[:, keep] / np.sqrt(w[keep])  # Tᵀ M T = I
+    T = _chol_inv_t(M, 1e-8)
+    if T is None:
+        w, U = np.linalg.eigh(M)
+        keep = w > eps * w.max()
+        T = U[:, keep] / np.sqrt(w[keep])  # Tᵀ M T = I
     lam, Z = np.linalg.eigh(T.T @ G @ T)
     order = np.argsort(lam)[::-1] if largest else np.argsort(lam)
     sel = order[:m]
@@ -243,6 +268,26 @@ class _Work:
         lam_p[: lam.size] = lam
         torch.addcmul(self.buf[self.AX], self.buf[self.X], _upload(lam_p, self.buf.dtype, self.buf.device),
                       value=-1.0, out=self.buf[self.W])
+
+    def ritz_update(self, b0: int, CC: np.ndarray, lam: np.ndarray, dst: "_Work") -> bool:
+        """dst's [P X] = S·CC, [AP AX] = AS·CC (S = slots b0..AP) and, when
+        the fused native kernel runs (bw = 8 f32), also dst's residual
+        W = AX − X·diag(λ); returns whether the residual was written."""
+        if self._native() and self.buf.dtype == torch.float32 and self.bw == 8 and dst._base != self._base:
+            from ._lib import check, lib
+
+            Ch = np.ascontiguousarray(CC, dtype=np.float32)
+            lam64 = np.ascontiguousarray(lam, dtype=np.float64)
+            with self._ctx():
+                check(lib().cim_ritz_update_b8(self._base + b0 * self._slot_bytes,
+                                               self._base + (b0 + 3) * self._slot_bytes, self.rows * self.bw,
+                                               Ch.shape[0], Ch.ctypes.data, lam64.ctypes.data, lam64.size,
+                                               dst._base + self.P * dst._slot_bytes, dst.rows * dst.bw, self.rows,
+                                               self._stream), "cim_ritz_update_b8")
+            return True
+        self.tsmm(b0, self.AP, CC, dst, self.P, self.W)
+        self.tsmm(b0 + 3, self.AW + 1, CC, dst, self.AP, self.AW)
+        return False
 
     def tsmm(self, a0: int, a1: int, C: np.ndarray, dst: "_Work", o0: int, o1: int, alpha=1.0, beta=0.0) -> None:
         """dst[slots o0..o1) ← alpha·[slots a0..a1)·C + beta·dst (virtual columns)."""
@@ -429,10 +474,12 @@ def lobpcg(apply: Callable[[torch.Tensor], torch.Tensor], X0: torch.Tensor, *, t
     rnorm = np.full(m, np.inf)
     it = 0
     converged = False
+    w_ready = False  # W already holds AX − XΛ (written by the fused Ritz update)
     for it in range(1, max_iter + 1):
         # residuals R = AX − X·Λ into the W slot
         # (full bw-wide blocks: padding columns of X / AX are zero, λ padded with 0)
-        cur.residual(lam)
+        if not w_ready:
+            cur.residual(lam)
         # one Gram pass gives both the residual norms (WᵀW) and the projection
         # coefficients ([P X]ᵀW) — soft locking only selects columns of W
         b0 = Wk.P if have_p else Wk.X
@@ -458,14 +505,18 @@ def lobpcg(apply: Callable[[torch.Tensor], torch.Tensor], X0: torch.Tensor, *, t
         bidx = cur.vidx(range(b0, Wk.W), [m] * (Wk.W - b0))
         wi = np.arange(nw)
         G_bw = G_all[np.ix_(bidx, act)]
-        cur.tsmm(b0, Wk.W, _embed(G_bw, bidx, wi, ((Wk.W - b0) * bw, bw)), cur, Wk.W, Wk.W + 1, alpha=-1.0, beta=1.0)
+        Gb = _embed(G_bw, bidx, wi, ((Wk.W - b0) * bw, bw))
         if BtB is not None and derived_w_gram and w_orth_passes == 1 and bw <= 16:
+            # projection and orthonormalisation in one pass over [P X W]:
+            # W ← (W − B·G)·T = W·T − B·(G·T), T from the derived Gram
             WtW = G_all[np.ix_(wb + act, act)]
             T = _orth_factor(WtW - 2.0 * (G_bw.T @ G_bw) + G_bw.T @ BtB @ G_bw)
             nw = T.shape[1]
             if nw > 0:
-                cur.tsmm(Wk.W, Wk.W + 1, _embed(T, wi, np.arange(nw), (bw, bw)), cur, Wk.W, Wk.W + 1)
+                Tb = _embed(T, wi, np.arange(nw), (bw, bw))
+                cur.tsmm(b0, Wk.W + 1, np.vstack([-Gb @ Tb, Tb]), cur, Wk.W, Wk.W + 1)
         else:
+            cur.tsmm(b0, Wk.W, Gb, cur, Wk.W, Wk.W + 1, alpha=-1.0, beta=1.0)
             nw = _orthonormalize_slot(cur, Wk.W, nw, nxt, group, passes=w_orth_passes)
         if nw == 0:
             converged = True
@@ -505,8 +556,7 @@ def lobpcg(apply: Callable[[torch.Tensor], torch.Tensor], X0: torch.Tensor, *, t
         CC[sidx, bw:bw + m] = C
         PX = np.hstack([Cp, C])
         BtB = PX.T @ M @ PX
-        cur.tsmm(b0, Wk.AP, CC, nxt, Wk.P, Wk.W)
-        cur.tsmm(b0 + 3, Wk.AW + 1, CC, nxt, Wk.AP, Wk.AW)
+        w_ready = cur.ritz_update(b0, CC, lam, nxt)
         have_p = True
         cur, nxt = nxt, cur
     return LobpcgResult(eigenvalues=lam, X=cur.slot(Wk.X).clone(), iterations=it, converged=converged,

@@ -590,6 +590,42 @@ def test_tsmm_host_c_and_residual(pkg, rows, qs, ps):
     assert torch.all(W[:, m:] == 0)
 
 
+@pytest.mark.parametrize("rows,q,m", [(1, 8, 8), (100_001, 24, 8), (4099, 16, 5), (70_000, 48, 3), (3, 32, 0)])
+def test_ritz_update_fused(pkg, rows, q, m):
+    """cim_ritz_update_b8 (the LOBPCG Ritz update fused with the next
+    residual) = two tsmm over S and AS plus W = AX − X·diag(λ), f64 reference;
+    padding columns (C columns ≥ m in each half are zero, λ_j = 0) stay zero."""
+    from paper_2110_10765_b200._lib import lib
+
+    L = lib()
+    g = torch.Generator().manual_seed(rows + q + m)
+    bw, qs = 8, q // 8
+    inp = torch.randn((2 * qs, rows, bw), generator=g)  # S slots then AS slots
+    C = torch.randn((q, 16), generator=g)
+    C[:, m:8] = 0
+    C[:, 8 + m:] = 0
+    lam = np.linspace(-2.0, 3.0, m)
+    out = torch.full((5, rows, bw), 7.0).cuda()
+    d = inp.cuda()
+    Ch = C.numpy().astype(np.float32)
+    bs = rows * bw
+    assert L.cim_ritz_update_b8(d[0].data_ptr(), d[qs].data_ptr(), bs, q, Ch.ctypes.data, lam.ctypes.data, m,
+                                out.data_ptr(), bs, rows, None) == 0
+    S = inp[:qs].permute(1, 0, 2).reshape(rows, q).double()
+    AS = inp[qs:].permute(1, 0, 2).reshape(rows, q).double()
+    PX, APX = S @ C.double(), AS @ C.double()
+    lam_p = torch.zeros(bw, dtype=torch.float64)
+    lam_p[:m] = torch.from_numpy(lam)
+    want = [PX[:, :8], PX[:, 8:], APX[:, 8:] - PX[:, 8:] * lam_p, APX[:, :8], APX[:, 8:]]
+    got = out.cpu().double()
+    scale = max(PX.abs().max().item(), APX.abs().max().item(), 1.0) * q
+    for s in range(5):
+        assert (got[s] - want[s]).abs().max().item() <= 2e-6 * scale, s
+        assert torch.all(got[s][:, m:] == 0), s
+    assert L.cim_ritz_update_b8(d[0].data_ptr(), d[qs].data_ptr(), bs, 40, Ch.ctypes.data, lam.ctypes.data, m,
+                                out.data_ptr(), bs, rows, None) == 1  # q not supported
+
+
 @pytest.mark.parametrize("rows,q,p,off", [(1, 1, 1, 0), (1000, 8, 8, 0), (100_001, 24, 16, 8), (5000, 7, 5, 3),
                                           (4096, 64, 64, 0)])
 def test_tsmm_matches_torch(pkg, rows, q, p, off):
