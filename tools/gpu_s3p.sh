@@ -1,5 +1,6 @@
 #!/bin/bash
 # LOBPCG per-kernel breakdown, new vs previous solver; fused-kernel parity.
+# scratch_ab/lobpcg_prev.py is the previous solver: git show 6227252:paper_2110_10765_b200/lobpcg.py > scratch_ab/lobpcg_prev.py
 set -u
 O=gpurun_out/s3p; mkdir -p $O
 timeout 900 python -m pytest tests/test_lobpcg.py tests/test_gpu_parity.py -q -m gpu -k "lobpcg or ritz" -x --timeout 300 > $O/pytest.txt 2>&1; echo "pytest exit $?" >> $O/pytest.txt
