@@ -92,18 +92,18 @@ __device__ __forceinline__ void load_operand(T *dst, const Operand &o, int mode,
     for (int b = 0; b < nb8; ++b) {
       const T *src = base + (long long)b * o.bstride + r0 * 8;
       T *d = dst + b * sbs;
-      for (int e = threadIdx.x; e < per; e += kGramThreads) cp_async16(d + e * V, src + e * V);
+      for (int e = threadIdx.x; e < per; e += blockDim.x) cp_async16(d + e * V, src + e * V);
     }
   } else if (mode == 1) {
     const int cpr = (o.cols + V - 1) / V;  // chunks per row
     const int n = nr * cpr;
-    for (int e = threadIdx.x; e < n; e += kGramThreads) {
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
       const int r = e / cpr, ch = e - r * cpr, c = ch * V;
       cp_async16(dst + (c >> 3) * sbs + r * 8 + (c & 7), base + (r0 + r) * o.ld + c);
     }
   } else {
     const int n = nr * o.cols, mask = (1 << o.bw_shift) - 1;
-    for (int e = threadIdx.x; e < n; e += kGramThreads) {
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
       const int r = __float2int_rz(((float)e + 0.5f) * inv_c);
       const int c = e - r * o.cols;
       const T *src = base + (long long)(c >> o.bw_shift) * o.bstride + (r0 + r) * o.ld + (c & mask);
@@ -150,8 +150,13 @@ __device__ __forceinline__ unsigned long long gfma2(float t, unsigned long long 
   return r;
 }
 
-template <typename T, bool FAST>
-__global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const Operand A, const Operand B, int mode_a,
+// NT threads per CTA, each owning an 8 × JW block of G.  (JW = 4 with 256
+// threads halves the per-thread accumulators and doubles the resident warps
+// of the 254-register 8 × 8 FAST version, but loads 1.5× the shared bytes
+// per FMA: 0.382 vs 0.351 ms per LOBPCG iteration's Gram passes — 8 × 8
+// stays the launch.)
+template <typename T, bool FAST, int NT = kGramThreads, int JW = 8>
+__global__ void __launch_bounds__(NT) gram_partial_kernel(const Operand A, const Operand B, int mode_a,
                                                                     int mode_b, long long rows,
                                                                     double *__restrict__ part, uint64_t block_mask,
                                                                     bool a_in_b) {
@@ -163,7 +168,8 @@ __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const Operan
   const int sbs = sblk_stride(kSlab);
   const int nbi = cap / 8, nbj = cbp / 8, nblk = nbi * nbj;
   const uint64_t live = (nblk >= 64 ? ~0ull : ((1ull << nblk) - 1)) & block_mask;
-  const int nact = max(1, __popcll(live));
+  constexpr int NH = 8 / JW;  // threads per 8×8 output block
+  const int nact = max(1, __popcll(live)) * NH;
   const int stage_elems = (nbi_st + nbj) * sbs;
   T *ring = reinterpret_cast<T *>(smem_raw);
   __shared__ uint64_t full[kGramStages];  // bulk mode: slab k landed in stage k % S
@@ -173,33 +179,34 @@ __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const Operan
     cim::fence_mbar_init();
   }
   const int red_cap = (int)((kGramStages * (size_t)stage_elems * sizeof(T)) / (sizeof(double) * cap * cbp));
-  const int split = min(kGramThreads / nact, red_cap);  // row residue classes (≥ 1)
+  const int split = min(NT / nact, red_cap);  // row residue classes (≥ 1)
   const int t = threadIdx.x;
   const int a_idx = t % nact, grp = t / nact;
   const bool active = grp < split && live != 0;
   int blk = 0;
-  {  // the a_idx-th live block
+  const int jh = a_idx % NH;  // which JW columns of the block
+  {  // the (a_idx / NH)-th live block
     uint64_t m = live;
-    for (int q = 0; q < a_idx; ++q) m &= m - 1;
+    for (int q = 0; q < a_idx / NH; ++q) m &= m - 1;
     blk = m ? __ffsll((long long)m) - 1 : 0;
   }
   const int bi = blk / nbj, bj = blk % nbj;
   const float inv_ca = 1.0f / (float)ca, inv_cb = 1.0f / (float)cb;
-  for (int e = t; e < kGramStages * stage_elems; e += kGramThreads) ring[e] = T(0);  // pads stay zero
+  for (int e = t; e < kGramStages * stage_elems; e += NT) ring[e] = T(0);  // pads stay zero
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zeros before the bulk copies' writes
   __syncthreads();
-  double acc[8][8];
+  double acc[8][JW];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
-  unsigned long long acc2[8][4];  // FAST: f32 pairs (row i, columns 2jp, 2jp+1)
+    for (int j = 0; j < JW; ++j) acc[i][j] = 0.0;
+  unsigned long long acc2[8][JW / 2];  // FAST: f32 pairs (row i, columns 2jp, 2jp+1)
   int run = 0;
   auto flush = [&]() {
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int jp = 0; jp < 4; ++jp) {
+      for (int jp = 0; jp < JW / 2; ++jp) {
         float lo, hi;
         asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc2[i][jp]));
         acc[i][2 * jp] += (double)lo;
@@ -212,7 +219,7 @@ __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const Operan
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int jp = 0; jp < 4; ++jp) acc2[i][jp] = 0ull;
+      for (int jp = 0; jp < JW / 2; ++jp) acc2[i][jp] = 0ull;
   }
 
   const long long nslabs = (rows + kSlab - 1) / kSlab;
@@ -257,31 +264,35 @@ __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const Operan
     const long long r0 = sl * kSlab;
     const int nr = (int)min((long long)kSlab, rows - r0);
     const T *sa = ring + (size_t)(k % kGramStages) * stage_elems + bi * sbs;
-    const T *sb = ring + (size_t)(k % kGramStages) * stage_elems + (nbi_st + bj) * sbs;
+    const T *sb = ring + (size_t)(k % kGramStages) * stage_elems + (nbi_st + bj) * sbs + jh * JW;
     if (active) {
       if constexpr (FAST) {
         for (int r = grp; r < nr; r += split) {
           const float4 a0 = *reinterpret_cast<const float4 *>(sa + r * 8);
           const float4 a1 = *reinterpret_cast<const float4 *>(sa + r * 8 + 4);
-          const ulonglong2 b01 = *reinterpret_cast<const ulonglong2 *>(sb + r * 8);
-          const ulonglong2 b23 = *reinterpret_cast<const ulonglong2 *>(sb + r * 8 + 4);
           const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-          const unsigned long long bv[4] = {b01.x, b01.y, b23.x, b23.y};
+          unsigned long long bv[JW / 2];
+#pragma unroll
+          for (int q = 0; q < JW / 4; ++q) {
+            const ulonglong2 b = *reinterpret_cast<const ulonglong2 *>(sb + r * 8 + 4 * q);
+            bv[2 * q] = b.x, bv[2 * q + 1] = b.y;
+          }
 #pragma unroll
           for (int i = 0; i < 8; ++i)
 #pragma unroll
-            for (int jp = 0; jp < 4; ++jp) acc2[i][jp] = gfma2(av[i], bv[jp], acc2[i][jp]);
+            for (int jp = 0; jp < JW / 2; ++jp) acc2[i][jp] = gfma2(av[i], bv[jp], acc2[i][jp]);
           if (++run == kFastRun) flush();
         }
       } else {
         for (int r = grp; r < nr; r += split) {
+          static_assert(FAST || JW == 8, "the exact path owns whole 8×8 blocks");
           double av[8], bv[8];
           load8<T>(av, sa + r * 8);
           load8<T>(bv, sb + r * 8);
 #pragma unroll
           for (int i = 0; i < 8; ++i)
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+            for (int j = 0; j < JW; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
         }
       }
     }
@@ -295,11 +306,11 @@ __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const Operan
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) red[(size_t)grp * cap * cbp + (8 * bi + i) * cbp + 8 * bj + j] = acc[i][j];
+      for (int j = 0; j < JW; ++j) red[(size_t)grp * cap * cbp + (8 * bi + i) * cbp + 8 * bj + jh * JW + j] = acc[i][j];
   }
   __syncthreads();
   double *out = part + (size_t)blockIdx.x * ca * cb;
-  for (int e = t; e < ca * cb; e += kGramThreads) {
+  for (int e = t; e < ca * cb; e += NT) {
     const int i = e / cb, j = e % cb;
     double s = 0.0;
     if ((live >> ((i >> 3) * nbj + (j >> 3))) & 1ull)
@@ -368,18 +379,17 @@ int gram_impl(const Operand &A, const Operand &B, long long rows, int32_t dtype,
   const int ma = load_mode(A, es), mb = load_mode(B, es);
   if (block_mask == 0) block_mask = ~0ull;
   cudaError_t e;
-  auto run = [&](auto kern) {
+  auto run = [&](auto kern, int nt) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
-      kern<<<grid, kGramThreads, smem, stream>>>(A, B, ma, mb, rows, static_cast<double *>(workspace), block_mask,
-                                                 a_in_b);
+      kern<<<grid, nt, smem, stream>>>(A, B, ma, mb, rows, static_cast<double *>(workspace), block_mask, a_in_b);
   };
   if (dtype == CIM_F32 && (flags & CIM_GRAM_FAST))
-    run(gram_partial_kernel<float, true>);
+    run(gram_partial_kernel<float, true>, kGramThreads);
   else if (dtype == CIM_F32)
-    run(gram_partial_kernel<float, false>);
+    run(gram_partial_kernel<float, false>, kGramThreads);
   else
-    run(gram_partial_kernel<double, false>);
+    run(gram_partial_kernel<double, false>, kGramThreads);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return cim::set_error(CIM_ECUDA, std::string("gram_partial_kernel: ") + cudaGetErrorString(e));
   const int count = ca * cb;
