@@ -453,3 +453,63 @@ def test_basis_skeleton_csr_path(pkg, symmetric):
         assert int(ptr[-1]) > 0
     rel = np.linalg.norm(Y - f["Y_ref"]) / np.linalg.norm(f["Y_ref"])
     assert rel <= 1e-5
+
+
+def _biased_basis(n: int, particles: int = 6, bias: float = 0.1, n_sp: int = 128, seed: int = 0):
+    """A reference-style many-body basis (occupations of `particles` of n_sp
+    orbitals, low orbitals favoured — tools/bench_basis_spmm.py), grouped by
+    the low bits so the basis-built matrix has the reference's block mix of a
+    few dense and many ~16-entry tiles."""
+    rng = np.random.default_rng(seed)
+    w = np.exp(-bias * np.arange(1, n_sp + 1))
+    occ = np.zeros((0, particles), np.uint16)
+    while occ.shape[0] < n:
+        keys = np.log(rng.random((2 * (n - occ.shape[0]) + 1024, n_sp))) / w
+        pick = np.sort(np.argpartition(-keys, particles, axis=1)[:, :particles] + 1, axis=1).astype(np.uint16)
+        occ = np.unique(np.concatenate([occ, pick]), axis=0)
+    occ = occ[rng.permutation(occ.shape[0])[:n]]
+    lo = np.zeros(n, np.uint64)
+    for q in range(particles):
+        sel = occ[:, q] <= 64
+        lo[sel] |= np.left_shift(np.uint64(1), (occ[sel, q] - 1).astype(np.uint64))
+    order = np.argsort(lo & np.uint64(0xFF), kind="stable")
+    return occ[order], lo[order]
+
+
+@pytest.fixture(scope="module")
+def basis_65k():
+    return _biased_basis(65536)
+
+
+@pytest.mark.parametrize("dtype,k", [(torch.float32, 8), (torch.float32, 16), (torch.float32, 32),
+                                     (torch.float32, 64), (torch.float64, 8), (torch.float64, 16)])
+def test_basis_65k_symmetric_csr_widths(pkg, basis_65k, dtype, k):
+    """A basis-built matrix at n = 65,536 (26.7 M stored entries, ~300 K
+    small sparse tiles through the CSR): the both-triangle CSR walk (lanes
+    sharing an entry's X row at k ≥ 16 f32 / k ≥ 8 f64) against the
+    half-stored CSR and the entry-parallel kernel, plus the forward/transposed
+    symmetry pin ⟨X₁, A·X₂⟩ = ⟨A·X₁, X₂⟩ (reference test_pipeline.py:278-286)."""
+    occ, lo = basis_65k
+    H = pkg.HalfTiles.from_basis(occ, lo, dtype=dtype)
+    assert H.sparse is not None and H.n_sparse_tiles > 100_000
+    n = H.n
+    g = torch.Generator(device="cuda").manual_seed(k)
+    X = torch.randn((n, k), device="cuda", dtype=dtype, generator=g)
+    X2 = torch.randn((n, k), device="cuda", dtype=dtype, generator=g)
+    Ys = pkg.sym_spmm(H, X).double()
+    assert H.sparse.csr_symmetric and H.sparse._csr is not None
+    Yh = pkg.sym_spmm(H.use_symmetric_csr(False), X).double()
+    H.sparse.use_csr = False
+    H.sparse._desc = None
+    H._desc = None
+    Ye = pkg.sym_spmm(H, X).double()
+    tol = 2e-5 if dtype == torch.float32 else 1e-12
+    scale = Ys.abs().max().item()
+    assert (Ys - Yh).abs().max().item() <= tol * scale
+    assert (Ys - Ye).abs().max().item() <= tol * scale
+    H.use_symmetric_csr(True)
+    AX2 = pkg.sym_spmm(H, X2).double()
+    lhs = (X.double() * AX2).sum(0)
+    rhs = (Ys * X2.double()).sum(0)
+    denom = (X.double().abs() * AX2.abs()).sum(0)
+    assert torch.all((lhs - rhs).abs() <= (1e-5 if dtype == torch.float32 else 1e-12) * denom)
