@@ -27,6 +27,8 @@
 // kernels (pipeline.py:461-531) over the COO of _collect_pairs (:428-458).
 #include <algorithm>
 #include <cstdlib>
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
+#include <cuda.h>  // CUtensorMap and its enums (the encoder comes through cudaGetDriverEntryPoint)
 #include <cstdio>
 #include <mutex>
 #include <string>
@@ -34,6 +36,10 @@
 #include "cim_b200.h"
 #include "common.cuh"
 #include "host_util.h"
+
+#ifndef CIM_DMMA_TMA_X
+#define CIM_DMMA_TMA_X 1  // k = 16 / 32: X blocks by TMA tensor copies with the 128-byte swizzle
+#endif
 
 namespace cim {
 namespace dmma {
@@ -52,7 +58,29 @@ struct DmParams {
   unsigned int stages, stage_bytes, xblk;
   unsigned int off_xc, off_xr, off_hdr, off_bars;
   unsigned int off_ebuf;  // 2 groups × 2 staging blocks of 64·K doubles (bulk flush), 0 = scalar reds
+  alignas(64) CUtensorMap tmx;  // k ∈ {16, 32}: X as a 2-D tensor (K × n_pad doubles), 16 × 64 boxes, 128-B swizzle
 };
+
+// X blocks through TMA with the 128-byte swizzle (k = 16, 32): the m8n8k4 B
+// fragment reads rows 4kb + q4 of X at one column, and with 128-byte (or
+// 256-byte) rows every X row starts on the same bank — 8 wavefronts per
+// 8-byte fragment load from a row-major stage.  The swizzle stores the
+// 16-byte chunk j of row r of each 16-column box at chunk j ^ (r % 8): the
+// four rows land on different banks (4 wavefronts, the two lanes of a bank
+// pair read different rows).
+template <int K>
+struct XSwz {
+  static constexpr bool on = CIM_DMMA_TMA_X && (K == 16 || K == 32);
+};
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 
 constexpr int kTileBytes = 4096 * 8;
 constexpr int kThreads = 288;  // 2 consumer groups × 4 warps + 1 producer warp
@@ -77,9 +105,12 @@ __device__ __forceinline__ void bulk_wait_read_le1() { asm volatile("cp.async.bu
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 template <int K>
-__global__ void __launch_bounds__(kThreads, 1) sym_spmm_dmma_kernel(const DmParams p) {
+__global__ void __launch_bounds__(kThreads, 1) sym_spmm_dmma_kernel(const __grid_constant__ DmParams p) {
   constexpr int NB = K / 8;  // 8-vector column blocks
-  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr bool SWZ = XSwz<K>::on;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // the 128-byte swizzle needs 1024-byte aligned boxes (1 KB of slack is allocated)
+  unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const int S = (int)p.stages;
@@ -131,11 +162,19 @@ __global__ void __launch_bounds__(kThreads, 1) sym_spmm_dmma_kernel(const DmPara
             mbar_wait_backoff(&empty[stage], phase ^ 1u);
             unsigned char *st = smem + (size_t)stage * SB;
             const bool diag = Cb == R;
-            *reinterpret_cast<int4 *>(st + p.off_hdr) = make_int4(R, Cb, diag ? HDR_DIAG : 0, 0);
+            *reinterpret_cast<int4 *>(smem + p.off_hdr + 16 * stage) = make_int4(R, Cb, diag ? HDR_DIAG : 0, 0);
             mbar_arrive_expect_tx(&full[stage], (unsigned)kTileBytes + (diag ? xblk : 2u * xblk));
             bulk_g2s(st, p.vals + (size_t)(tb + q) * kTileBytes, kTileBytes, &full[stage], pol_stream);
-            bulk_g2s(st + p.off_xc, p.X + (size_t)Cb * xblk, xblk, &full[stage], pol_keep);
-            if (!diag) bulk_g2s(st + p.off_xr, p.X + (size_t)R * xblk, xblk, &full[stage], pol_keep);
+            if constexpr (SWZ) {
+#pragma unroll
+              for (int hb = 0; hb < K / 16; ++hb) {
+                tma_load_2d(st + p.off_xc + hb * 8192, &p.tmx, 16 * hb, Cb * kBlock, &full[stage], pol_keep);
+                if (!diag) tma_load_2d(st + p.off_xr + hb * 8192, &p.tmx, 16 * hb, R * kBlock, &full[stage], pol_keep);
+              }
+            } else {
+              bulk_g2s(st + p.off_xc, p.X + (size_t)Cb * xblk, xblk, &full[stage], pol_keep);
+              if (!diag) bulk_g2s(st + p.off_xr, p.X + (size_t)R * xblk, xblk, &full[stage], pol_keep);
+            }
           }
           __syncwarp();
           if (++stage == S) {
@@ -154,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1) sym_spmm_dmma_kernel(const DmPara
     if (lane == 0)
       for (int e = 0; e < 2; ++e) {  // one terminator per consumer group
         mbar_wait_backoff(&empty[stage], phase ^ 1u);
-        *reinterpret_cast<int4 *>(smem + (size_t)stage * SB + p.off_hdr) = make_int4(0, 0, HDR_TERM, 0);
+        *reinterpret_cast<int4 *>(smem + p.off_hdr + 16 * stage) = make_int4(0, 0, HDR_TERM, 0);
         mbar_arrive(&full[stage]);
         if (++stage == S) {
           stage = 0;
@@ -180,8 +219,16 @@ __global__ void __launch_bounds__(kThreads, 1) sym_spmm_dmma_kernel(const DmPara
       const int chunk = 4 * w + 2 * cb + (g >> 2);
       a_tr[cb][par] = (unsigned)(q4 * 512 + ((chunk ^ (4 * par + q4)) << 5) + (g & 3) * 8);
     }
-  // B fragments: X[4kb + q4][8nb + g]
+  // B fragments: X[4kb + q4][8nb + g] — row-major stage, or (SWZ) box nb/2,
+  // row r = 4kb + q4 at r·128, chunk (4(nb&1) + g/2) ^ (r % 8), half g&1
   const unsigned b_off = (unsigned)(q4 * K * 8 + g * 8);
+  unsigned b_swz[2][NB];
+#pragma unroll
+  for (int par = 0; par < 2; ++par)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+      b_swz[par][nb] = (unsigned)((nb >> 1) * 8192 + q4 * 128 + (((4 * (nb & 1) + (g >> 1)) ^ (4 * par + q4)) << 4) +
+                                  (g & 1) * 8);
 
   double acc[2][NB][2];
 #pragma unroll
@@ -234,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1) sym_spmm_dmma_kernel(const DmPara
   while (true) {
     mbar_wait(&full[stage], phase);
     const unsigned char *st = smem + (size_t)stage * SB;
-    const int4 h = *reinterpret_cast<const int4 *>(st + p.off_hdr);
+    const int4 h = *reinterpret_cast<const int4 *>(smem + p.off_hdr + 16 * stage);
     if (h.z & HDR_TERM) {
       if (curR >= 0) flush_direct(curR);
       if (bulk && issuer) bulk_wait_all();
@@ -250,7 +297,9 @@ __global__ void __launch_bounds__(kThreads, 1) sym_spmm_dmma_kernel(const DmPara
     for (int kb = 0; kb < 16; ++kb) {
       double b[NB];
 #pragma unroll
-      for (int nb = 0; nb < NB; ++nb) b[nb] = *reinterpret_cast<const double *>(Xc + b_off + kb * 32 * K + nb * 64);
+      for (int nb = 0; nb < NB; ++nb)
+          b[nb] = SWZ ? *reinterpret_cast<const double *>(Xc + b_swz[kb & 1][nb] + kb * 512)
+                      : *reinterpret_cast<const double *>(Xc + b_off + kb * 32 * K + nb * 64);
 #pragma unroll
       for (int rb = 0; rb < 2; ++rb) {
         const double a = *reinterpret_cast<const double *>(st + ((a_dir + rb * 8 * 512) ^ (unsigned)(kb << 5)));
@@ -270,7 +319,9 @@ __global__ void __launch_bounds__(kThreads, 1) sym_spmm_dmma_kernel(const DmPara
       for (int kb = 0; kb < 16; ++kb) {
         double b[NB];
 #pragma unroll
-        for (int nb = 0; nb < NB; ++nb) b[nb] = *reinterpret_cast<const double *>(Xr + b_off + kb * 32 * K + nb * 64);
+        for (int nb = 0; nb < NB; ++nb)
+          b[nb] = SWZ ? *reinterpret_cast<const double *>(Xr + b_swz[kb & 1][nb] + kb * 512)
+                      : *reinterpret_cast<const double *>(Xr + b_off + kb * 32 * K + nb * 64);
 #pragma unroll
         for (int cb = 0; cb < 2; ++cb) {
           const double a = *reinterpret_cast<const double *>(st + kb * 2048 + a_tr[cb][kb & 1]);
@@ -302,9 +353,9 @@ int launch(const cim_half_tiles *H, const void *X, void *Y, long long ldy, cudaS
   DmParams p{};
   p.off_xc = kTileBytes;
   p.off_xr = p.off_xc + xblk;
-  p.off_hdr = p.off_xr + xblk;
-  p.stage_bytes = (p.off_hdr + 16 + 127) & ~127u;
-  const size_t budget = 227 * 1024 - 256;
+  p.stage_bytes = kTileBytes + 2 * xblk;  // a multiple of 1024 (swizzled TMA boxes stay aligned)
+  // stages, then the bulk-flush staging blocks, the stage headers and the barriers
+  const size_t budget = 227 * 1024 - 1024 - 32 * 8;
   // bulk flushes need dense Y rows and 2 groups × 2 staging blocks; keep them
   // unless they would cost ring stages
   const size_t ebytes = 4 * (size_t)64 * K * 8;
@@ -320,8 +371,30 @@ int launch(const cim_half_tiles *H, const void *X, void *Y, long long ldy, cudaS
   if (S < 2) return set_error(CIM_EUNSUPPORTED, "DMMA path: k too large for shared memory");
   p.stages = (unsigned)S;
   p.off_ebuf = use_bulk ? (unsigned)S * p.stage_bytes : 0u;
-  p.off_bars = (unsigned)((size_t)S * p.stage_bytes + (use_bulk ? ebytes : 0));
-  const size_t smem = p.off_bars + 16 * (size_t)S;
+  p.off_hdr = (unsigned)((size_t)S * p.stage_bytes + (use_bulk ? ebytes : 0));
+  p.off_bars = p.off_hdr + 16u * (unsigned)S;
+  const size_t smem = p.off_bars + 16 * (size_t)S + 1024;
+  if constexpr (XSwz<K>::on) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      if (!encode) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+          return set_error(CIM_ECUDA, "cuTensorMapEncodeTiled not available");
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+      }
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)((H->n + kBlock - 1) / kBlock * kBlock)};
+    const cuuint64_t strides[1] = {(cuuint64_t)K * 8};
+    const cuuint32_t box[2] = {16, (cuuint32_t)kBlock}, estr[2] = {1, 1};
+    const CUresult r = encode(&p.tmx, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void *>(X), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(CIM_EINVAL, "cuTensorMapEncodeTiled(X) failed (alignment?)");
+  }
   auto kern = sym_spmm_dmma_kernel<K>;
   int dev = 0;
   cudaGetDevice(&dev);
