@@ -189,7 +189,9 @@ CIM_API const char *cim_last_error(void);
 /*
  * Y = A·X (or Y += A·X with CIM_ACCUMULATE) on `stream` (a cudaStream_t, may
  * be NULL for the legacy stream).  X, Y are device pointers to (n_pad, k)
- * row-major arrays of the tile dtype.
+ * row-major arrays of the tile dtype, 16-byte aligned (the kernels stage
+ * 64-row X blocks with bulk / TMA tensor copies: f64 tensor-core tiles at
+ * k = 16, 32 read X through a 2-D tensor map encoded per call).
  *
  * Replaces: contract_observables(...) (pipeline.py:534-570) as the operator
  * that walks every stored pair once per call; its validation contract

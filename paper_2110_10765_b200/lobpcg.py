@@ -125,8 +125,10 @@ def _chol_inv_t(M: np.ndarray, eps: float) -> np.ndarray | None:
     solver costs ~60–80 µs at 24 × 24 on the host — the solver's critical
     path while the GPU waits — where Cholesky, its condition estimate and
     the triangular inverse take ~20 µs."""
-    from scipy.linalg import lapack
-
+    try:
+        from scipy.linalg import lapack
+    except ImportError:  # the eigenbasis path needs only numpy
+        return None
     L, info = lapack.dpotrf(M, lower=1, clean=1)
     if info != 0:
         return None
