@@ -56,7 +56,8 @@ def parse():
     ap.add_argument("--tiles-per-gpu", type=int, default=TILES_PER_GPU)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget for the cpu_baseline leg")
-    ap.add_argument("--e2e-steps", type=int, default=16)
+    ap.add_argument("--e2e-steps", type=int, default=64,
+                    help="host blocks through the e2e leg (the pipeline fill and drain amortise over them)")
     ap.add_argument("--bands", type=int, default=1, help="column bands of the tile order (0 = auto)")
     ap.add_argument("--no-overlap", action="store_true",
                     help="N > 1: serial all-gather → kernel → reduce-scatter instead of the overlapped schedule")
