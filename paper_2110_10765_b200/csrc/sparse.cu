@@ -568,7 +568,10 @@ int launch_sparse(const cim_sparse_tiles *S, const void *X, void *Y, int k, long
   int stages = ((size_t)8 * L.bytes + 128 <= 113 * 1024) ? 8 : 4;
 #endif
   const size_t smem = (size_t)stages * L.bytes + 16 * (size_t)stages;  // + full / empty mbarriers
-  if (smem > 227 * 1024) return set_error(CIM_EUNSUPPORTED, "k too large for the sparse-tile stages");
+  const bool listed0 = S->staged_tiles != nullptr || S->small_tiles != nullptr;
+  const bool csr0 = S->csr_ptr && S->csr_rows > 0;
+  const long long n_ring0 = (csr0 && S->csr_all) ? 0 : listed0 ? (S->staged_tiles ? S->n_staged : 0) : S->n_tiles;
+  if (n_ring0 > 0 && smem > 227 * 1024) return set_error(CIM_EUNSUPPORTED, "k too large for the sparse-tile stages");
   CounterLease lease;
   if (const int lrc = lease.take(*st->ring, stream, 1)) return lrc;
   unsigned int *ctr = lease.ctr;
@@ -594,16 +597,16 @@ int launch_sparse(const cim_sparse_tiles *S, const void *X, void *Y, int k, long
   p.staged = S->staged_tiles;
   p.n_staged = S->staged_tiles ? S->n_staged : 0;
   const bool listed = S->staged_tiles != nullptr || S->small_tiles != nullptr;
-  e = cudaFuncSetAttribute(sparse_spmm_kernel<T, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("sparse attr: ") + cudaGetErrorString(e));
-  int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sparse_spmm_kernel<T, KV>, kSpConsumers + 32, smem) !=
-          cudaSuccess ||
-      occ < 1)
-    occ = 1;
   const bool csr = S->csr_ptr && S->csr_rows > 0;
   const long long n_ring = (csr && S->csr_all) ? 0 : listed ? p.n_staged : S->n_tiles;
   if (n_ring > 0) {
+    e = cudaFuncSetAttribute(sparse_spmm_kernel<T, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("sparse attr: ") + cudaGetErrorString(e));
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sparse_spmm_kernel<T, KV>, kSpConsumers + 32, smem) !=
+            cudaSuccess ||
+        occ < 1)
+      occ = 1;
     const long long grid = std::min<long long>(n_ring, (long long)st->sms * occ);
     sparse_spmm_kernel<T, KV><<<(unsigned)grid, kSpConsumers + 32, smem, stream>>>(p, stages);
     e = cudaGetLastError();
@@ -628,22 +631,80 @@ int launch_sparse(const cim_sparse_tiles *S, const void *X, void *Y, int k, long
 extern "C" int32_t cim_sparse_small_max(void) { return cim::sparse_small_max(); }
 
 namespace cim {
+namespace {
+// Does the staged ring for W-wide vector blocks fit in shared memory (the
+// plan of launch_sparse)?
+template <typename T>
+bool sparse_stage_fits(const cim_sparse_tiles *S, int W) {
+  const int cap = (S->staged_max_entries > 0 && S->staged_max_entries <= kSpCapSmall) ? kSpCapSmall : kSpCap;
+  const SpLayout L = sp_layout(W, (int)sizeof(T), cap);
+  const int stages = ((size_t)8 * L.bytes + 128 <= 113 * 1024) ? 8 : 4;
+  return (size_t)stages * L.bytes + 16 * (size_t)stages <= 227 * 1024;
+}
+
+// X (n_pad × k) → pass-major slices (passes × n_pad × W), 16-byte chunks.
+__global__ void sparse_pass_major_kernel(const uint4 *__restrict__ X, uint4 *__restrict__ Xp, long long rows,
+                                         int row_chunks, int w_chunks) {
+  const long long total = rows * row_chunks;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / row_chunks;
+    const int c = (int)(e - r * row_chunks);
+    const int ps = c / w_chunks, cc = c - ps * w_chunks;
+    Xp[((long long)ps * rows + r) * w_chunks + cc] = X[e];
+  }
+}
+
+// Widths whose staged X blocks (64·k values each for X_C and X_R) exceed the
+// shared-memory ring (f64 k = 64) run as column passes of the largest W that
+// fits, each on a pass-major copy of X (stream-ordered allocation) writing
+// its W columns of Y in place.
+template <typename T, int KV>
+int sparse_dispatch(const cim_sparse_tiles *S, const void *X, void *Y, int k, long long ldx, long long ldy,
+                    long long n_pad, cudaStream_t stream) {
+  const bool listed = S->staged_tiles != nullptr || S->small_tiles != nullptr;
+  const bool csr_all = S->csr_ptr && S->csr_rows > 0 && S->csr_all;
+  const bool ring = !csr_all && (listed ? (S->staged_tiles != nullptr && S->n_staged > 0) : S->n_tiles > 0);
+  if (!ring || sparse_stage_fits<T>(S, k)) return launch_sparse<T, KV>(S, X, Y, k, ldx, ldy, stream);
+  int W = k;
+  while (W % (2 * KV) == 0 && (W / 2 * (int)sizeof(T)) % 16 == 0 && !sparse_stage_fits<T>(S, W)) W /= 2;
+  if (!sparse_stage_fits<T>(S, W) || ldx != k || n_pad <= 0)
+    return set_error(CIM_EUNSUPPORTED, "k too large for the sparse-tile stages");
+  const int passes = k / W;
+  void *Xp = nullptr;
+  cudaError_t e = cudaMallocAsync(&Xp, (size_t)n_pad * k * sizeof(T), stream);
+  if (e != cudaSuccess) return set_error(CIM_ECUDA, std::string("sparse pass scratch: ") + cudaGetErrorString(e));
+  const int row_chunks = k * (int)sizeof(T) / 16, w_chunks = W * (int)sizeof(T) / 16;
+  const long long total = n_pad * row_chunks;
+  sparse_pass_major_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 4096), 256, 0, stream>>>(
+      static_cast<const uint4 *>(X), static_cast<uint4 *>(Xp), n_pad, row_chunks, w_chunks);
+  int rc = CIM_OK;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) rc = set_error(CIM_ECUDA, std::string("sparse pass-major copy: ") + cudaGetErrorString(e));
+  for (int ps = 0; ps < passes && rc == CIM_OK; ++ps)
+    rc = launch_sparse<T, KV>(S, static_cast<const T *>(Xp) + (size_t)ps * n_pad * W, static_cast<T *>(Y) + ps * W, W,
+                              W, ldy, stream);
+  cudaFreeAsync(Xp, stream);
+  return rc;
+}
+}  // namespace
+
 // Called by cim_sym_spmm after the dense tiles (Y already zeroed or accumulating).
 int sym_spmm_sparse(const cim_sparse_tiles *S, int dtype, const void *X, void *Y, int k, long long ldx,
-                    long long ldy, cudaStream_t stream) {
+                    long long ldy, long long n_pad, cudaStream_t stream) {
   if (!S || S->n_tiles == 0) return CIM_OK;
   if (!S->tile_rc || !S->entry_off || !S->rowptr || !S->colptr ||
       (S->n_entries > 0 && (!S->col || !S->row || !S->cperm || !S->vals)))
     return set_error(CIM_EINVAL, "sparse tile arrays are NULL");
   if (dtype == CIM_F32) {
-    if (k % 8 == 0) return launch_sparse<float, 8>(S, X, Y, k, ldx, ldy, stream);
-    if (k % 4 == 0) return launch_sparse<float, 4>(S, X, Y, k, ldx, ldy, stream);
-    if (k % 2 == 0) return launch_sparse<float, 2>(S, X, Y, k, ldx, ldy, stream);
-    return launch_sparse<float, 1>(S, X, Y, k, ldx, ldy, stream);
+    if (k % 8 == 0) return sparse_dispatch<float, 8>(S, X, Y, k, ldx, ldy, n_pad, stream);
+    if (k % 4 == 0) return sparse_dispatch<float, 4>(S, X, Y, k, ldx, ldy, n_pad, stream);
+    if (k % 2 == 0) return sparse_dispatch<float, 2>(S, X, Y, k, ldx, ldy, n_pad, stream);
+    return sparse_dispatch<float, 1>(S, X, Y, k, ldx, ldy, n_pad, stream);
   }
-  if (k % 4 == 0) return launch_sparse<double, 4>(S, X, Y, k, ldx, ldy, stream);
-  if (k % 2 == 0) return launch_sparse<double, 2>(S, X, Y, k, ldx, ldy, stream);
-  return launch_sparse<double, 1>(S, X, Y, k, ldx, ldy, stream);
+  if (k % 4 == 0) return sparse_dispatch<double, 4>(S, X, Y, k, ldx, ldy, n_pad, stream);
+  if (k % 2 == 0) return sparse_dispatch<double, 2>(S, X, Y, k, ldx, ldy, n_pad, stream);
+  return sparse_dispatch<double, 1>(S, X, Y, k, ldx, ldy, n_pad, stream);
 }
 
 }  // namespace cim

@@ -1735,7 +1735,9 @@ int launch_wide(const cim_half_tiles *H, int k, const Chunks &ck, long long ldy,
 
 bool wide_supported(int dtype, int k) {
   if (dtype == CIM_F32) return k == 8 || k == 16 || k == 24 || k == 32 || k == 48 || k == 64;
-  return k == 4 || k == 8 || k == 12 || k == 16 || k == 32;
+  // f64 k > 32: column passes of the wide kernel (a generic-kernel stage with
+  // whole 64-row X blocks of k > 40 doubles does not fit shared memory)
+  return k == 4 || k == 8 || k == 12 || k == 16 || k == 32 || (k > 32 && k <= 64 && k % 4 == 0);
 }
 
 }  // namespace
@@ -1766,7 +1768,7 @@ extern "C" int cim_layout_supports(int32_t layout, int32_t dtype, int32_t k) {
 
 namespace cim {
 int sym_spmm_sparse(const cim_sparse_tiles *S, int dtype, const void *X, void *Y, int k, long long ldx,
-                    long long ldy, cudaStream_t stream);
+                    long long ldy, long long n_pad, cudaStream_t stream);
 int sym_spmm_deterministic(const cim_half_tiles *H, const void *X, void *Y, int k, long long ldy, bool accumulate,
                            cudaStream_t stream);
 }
@@ -1830,6 +1832,8 @@ static int sym_spmm_dense(const cim_half_tiles *H, const void *X, void *Y, int32
     if (H->dtype == CIM_F32 && k == 24) return launch_k8_passes<float, 1>(H, X, Y, k, ldy, stream, ds);
     if (H->dtype == CIM_F64 && (k == 16 || k == 32)) return launch_k8_passes<double, 2>(H, X, Y, k, ldy, stream, ds);
     if (H->dtype == CIM_F64 && k == 12) return launch_k8_passes<double, 1>(H, X, Y, k, ldy, stream, ds);
+    if (H->dtype == CIM_F64 && k > 32 && k % 8 == 0) return launch_k8_passes<double, 2>(H, X, Y, k, ldy, stream, ds);
+    if (H->dtype == CIM_F64 && k > 32) return launch_k8_passes<double, 1>(H, X, Y, k, ldy, stream, ds);
 #endif
     Chunks ck;
     ck.x[0] = X;
@@ -1884,7 +1888,8 @@ extern "C" int cim_sym_spmm(const cim_half_tiles *H, const void *X, void *Y, int
                             uint32_t flags, void *stream_) {
   const int rc = sym_spmm_dense(H, X, Y, k, ldx, ldy, flags, stream_);
   if (rc != CIM_OK || (flags & CIM_DETERMINISTIC) || !H->sparse || H->sparse->n_tiles == 0) return rc;
-  return sym_spmm_sparse(H->sparse, H->dtype, X, Y, k, ldx, ldy, reinterpret_cast<cudaStream_t>(stream_));
+  return sym_spmm_sparse(H->sparse, H->dtype, X, Y, k, ldx, ldy, (H->n + kBlock - 1) / kBlock * kBlock,
+                         reinterpret_cast<cudaStream_t>(stream_));
 }
 
 extern "C" int cim_sym_spmm_chunked(const cim_half_tiles *H, const void *const *X_chunks, void *const *Y_chunks,

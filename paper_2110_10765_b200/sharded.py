@@ -162,7 +162,14 @@ class ShardedSymSpmm:
                 raise ValueError("the fused peer-memory apply streams dense tiles only; use the NCCL exchange "
                                  "(fused=False) for matrices with sparse tiles")
             self._setup_fused()
-        self.overlap = bool(overlap) and self.world > 1 and local_apply == self._cuda_apply and not self.fused
+        # the own-chunk group reads X through a virtual base (only this rank's
+        # rows are backed); sparse tiles too wide for the staged ring (f64
+        # k = 64) run as column passes over a pass-major copy of every X row,
+        # so that case keeps the serial exchange
+        wide_sparse = (H_local is not None and H_local.n_sparse_tiles > 0 and dtype == torch.float64
+                       and self.k > 32)
+        self.overlap = (bool(overlap) and self.world > 1 and local_apply == self._cuda_apply and not self.fused
+                        and not wide_sparse)
         if self.overlap:
             self.g_local, self.g_cols = column_groups(H_local, self.rows_per_rank, self.world, self.rank)
         self._staged = (self.world > 1 and self.device.type == "cuda"

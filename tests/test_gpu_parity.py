@@ -238,7 +238,7 @@ def test_k_sweep_f32(pkg, c1_small, k, layout):
 
 
 @pytest.mark.parametrize("layout", ["frag", "tc"])
-@pytest.mark.parametrize("k", [1, 2, 4, 8, 12, 16, 24, 32, 40])
+@pytest.mark.parametrize("k", [1, 2, 4, 8, 12, 16, 24, 32, 40, 44, 48, 64])
 def test_k_sweep_f64(pkg, c1_small, k, layout):
     n, rc, tiles = c1_small
     H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=torch.float64, layout=layout)
@@ -678,7 +678,7 @@ def test_column_banded_storage(pkg, c1_small, bands):
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 @pytest.mark.parametrize("fill", [0.0, 0.02, 0.05, 0.3, 0.9])  # 0.05: every staged tile fits 512-entry stages
-@pytest.mark.parametrize("k", [1, 2, 3, 4, 8, 12, 16, 24])
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 8, 12, 16, 24, 32, 64])
 def test_sparse_tiles_vs_oracle(pkg, dtype, fill, k):
     """COO-in-tile storage: random symmetric matrices whose 64-tiles have a
     given fill (ragged n, empty rows, diagonal and off-diagonal tiles), stored

@@ -484,7 +484,8 @@ def basis_65k():
 
 
 @pytest.mark.parametrize("dtype,k", [(torch.float32, 8), (torch.float32, 16), (torch.float32, 32),
-                                     (torch.float32, 64), (torch.float64, 8), (torch.float64, 16)])
+                                     (torch.float32, 64), (torch.float64, 8), (torch.float64, 16),
+                                     (torch.float64, 32)])
 def test_basis_65k_symmetric_csr_widths(pkg, basis_65k, dtype, k):
     """A basis-built matrix at n = 65,536 (26.7 M stored entries, ~300 K
     small sparse tiles through the CSR): the both-triangle CSR walk (lanes
