@@ -1735,9 +1735,10 @@ int launch_wide(const cim_half_tiles *H, int k, const Chunks &ck, long long ldy,
 
 bool wide_supported(int dtype, int k) {
   if (dtype == CIM_F32) return k == 8 || k == 16 || k == 24 || k == 32 || k == 48 || k == 64;
-  // f64 k > 32: column passes of the wide kernel (a generic-kernel stage with
-  // whole 64-row X blocks of k > 40 doubles does not fit shared memory)
-  return k == 4 || k == 8 || k == 12 || k == 16 || k == 32 || (k > 32 && k <= 64 && k % 4 == 0);
+  // f64 k = 20, 28 and k > 32: column passes of the wide kernel (a
+  // generic-kernel stage with whole 64-row X blocks of that many doubles
+  // does not fit shared memory)
+  return k == 4 || k == 8 || k == 12 || k == 16 || k == 32 || (k > 16 && k <= 64 && k % 4 == 0 && k != 24);
 }
 
 }  // namespace
@@ -1833,7 +1834,7 @@ static int sym_spmm_dense(const cim_half_tiles *H, const void *X, void *Y, int32
     if (H->dtype == CIM_F64 && (k == 16 || k == 32)) return launch_k8_passes<double, 2>(H, X, Y, k, ldy, stream, ds);
     if (H->dtype == CIM_F64 && k == 12) return launch_k8_passes<double, 1>(H, X, Y, k, ldy, stream, ds);
     if (H->dtype == CIM_F64 && k > 32 && k % 8 == 0) return launch_k8_passes<double, 2>(H, X, Y, k, ldy, stream, ds);
-    if (H->dtype == CIM_F64 && k > 32) return launch_k8_passes<double, 1>(H, X, Y, k, ldy, stream, ds);
+    if (H->dtype == CIM_F64 && k > 16 && k % 8 == 4) return launch_k8_passes<double, 1>(H, X, Y, k, ldy, stream, ds);
 #endif
     Chunks ck;
     ck.x[0] = X;

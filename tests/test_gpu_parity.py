@@ -228,7 +228,7 @@ def c1_small(pkg):
 
 
 @pytest.mark.parametrize("layout", F32_LAYOUTS)
-@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 8, 16, 24, 32, 40, 48, 64])
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 7, 8, 9, 16, 24, 32, 40, 48, 56, 63, 64])
 def test_k_sweep_f32(pkg, c1_small, k, layout):
     n, rc, tiles = c1_small
     H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=torch.float32, layout=layout)
@@ -238,7 +238,7 @@ def test_k_sweep_f32(pkg, c1_small, k, layout):
 
 
 @pytest.mark.parametrize("layout", ["frag", "tc"])
-@pytest.mark.parametrize("k", [1, 2, 4, 8, 12, 16, 24, 32, 40, 44, 48, 64])
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 7, 8, 12, 16, 20, 24, 28, 32, 40, 44, 48, 60, 63, 64])
 def test_k_sweep_f64(pkg, c1_small, k, layout):
     n, rc, tiles = c1_small
     H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=torch.float64, layout=layout)
@@ -247,7 +247,8 @@ def test_k_sweep_f64(pkg, c1_small, k, layout):
     check_result(n, rc, tiles.astype(np.float64), X.numpy(), Y, torch.float64)
 
 
-@pytest.mark.parametrize("dtype,k", [(torch.float32, 32), (torch.float32, 64), (torch.float64, 16)])
+@pytest.mark.parametrize("dtype,k", [(torch.float32, 32), (torch.float32, 64), (torch.float64, 16),
+                                     (torch.float64, 64)])
 def test_multipass_widths_on_concurrent_streams(pkg, c1_small, dtype, k):
     """Widths above one pass stage a pass-major copy of X in a per-stream
     scratch buffer: applies queued on two streams at once (different X, same
@@ -765,7 +766,7 @@ def test_synthetic_sparse_device_construction(pkg, fill):
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
-@pytest.mark.parametrize("k", [1, 4, 8, 16])
+@pytest.mark.parametrize("k", [1, 4, 8, 16, 32, 64])
 def test_deterministic_mode_bitwise_reproducible(pkg, c1_small, dtype, k):
     """CIM_DETERMINISTIC: no float atomics — repeated applies are bitwise
     identical (the atomic path is not, in general), and the result passes the
