@@ -398,7 +398,9 @@ CIM_API int cim_sym_spmm_supported(int32_t dtype, int32_t k);
 
 /* 1 if (layout, dtype, k) has a compiled kernel, else 0.  CIM_LAYOUT_TC:
  * f32 with k ∈ {8, 16, …, 64} (tcgen05 kind::tf32, 3×TF32-split FP32 accuracy);
- * f64 with k ∈ {8, 16, 24, 32} (mma.sync DMMA m8n8k4). */
+ * f64 with k ∈ {8, 16, 24, 32} (mma.sync DMMA m8n8k4) and k = 64 (two
+ * column passes of 32 over a pass-major copy of X in a per-device scratch
+ * buffer, as for the fragment layout's multi-pass widths). */
 CIM_API int cim_layout_supports(int32_t layout, int32_t dtype, int32_t k);
 
 /*

@@ -1762,7 +1762,7 @@ extern "C" int cim_layout_supports(int32_t layout, int32_t dtype, int32_t k) {
   if (layout == CIM_LAYOUT_FRAG) return cim_sym_spmm_supported(dtype, k);
   if (layout == CIM_LAYOUT_TC) {
     if (dtype == CIM_F32) return (k >= 8 && k <= 64 && k % 8 == 0) ? 1 : 0;
-    return (k >= 8 && k <= 32 && k % 8 == 0) ? 1 : 0;  // f64: DMMA kernel
+    return ((k >= 8 && k <= 32 && k % 8 == 0) || k == 64) ? 1 : 0;  // f64: DMMA kernel (k = 64: two column passes)
   }
   return 0;
 }
@@ -1815,10 +1815,36 @@ static int sym_spmm_dense(const cim_half_tiles *H, const void *X, void *Y, int32
 
   if (H->layout == CIM_LAYOUT_TC) {
     if ((reinterpret_cast<uintptr_t>(Y) & 15) || (ldy % 4)) return set_error(CIM_EINVAL, "TC path needs 16-B aligned Y rows");
+    // widths above one launch (f64 k > 32: the DMMA kernel's register-resident
+    // accumulators) run as column passes of W on a pass-major copy of X, each
+    // writing its W columns of Y in place (row stride ldy)
+    const int W = (H->dtype == CIM_F64 && k > 32) ? 32 : k;
+    if (W == k) {
+      CounterLease lease;
+      if (const int lrc = lease.take(*ds->ring, stream, 1)) return lrc;
+      if (H->dtype == CIM_F64) return sym_spmm_dmma_dispatch(H, X, Y, k, ldy, stream, ds->sms, lease.ctr);
+      return sym_spmm_tc_dispatch(H, X, Y, k, ldy, stream, ds->sms, lease.ctr);
+    }
+    if (k % W != 0) return set_error(CIM_EUNSUPPORTED, "tensor-core layout: k must be a multiple of 32 above 32 (f64)");
+    const int passes = k / W;
+    void *Xp = nullptr;
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    int rc = scratch_begin(ds, stream, (size_t)n_pad * k * es, &Xp);
+    if (rc) return rc;
+    const int row_chunks = k * (int)es / 16, w_chunks = W * (int)es / 16;
+    const long long total = n_pad * row_chunks;
+    pass_major_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 16LL * ds->sms), 256, 0, stream>>>(
+        static_cast<const uint4 *>(X), static_cast<uint4 *>(Xp), n_pad, row_chunks, w_chunks);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) rc = set_error(CIM_ECUDA, std::string("pass_major_kernel: ") + cudaGetErrorString(e));
     CounterLease lease;
-    if (const int lrc = lease.take(*ds->ring, stream, 1)) return lrc;
-    if (H->dtype == CIM_F64) return sym_spmm_dmma_dispatch(H, X, Y, k, ldy, stream, ds->sms, lease.ctr);
-    return sym_spmm_tc_dispatch(H, X, Y, k, ldy, stream, ds->sms, lease.ctr);
+    if (!rc) rc = lease.take(*ds->ring, stream, passes);
+    for (int ps = 0; ps < passes && rc == CIM_OK; ++ps)
+      rc = sym_spmm_dmma_dispatch(H, static_cast<const unsigned char *>(Xp) + (size_t)ps * n_pad * W * es,
+                                  static_cast<unsigned char *>(Y) + (size_t)ps * W * es, W, ldy, stream, ds->sms,
+                                  lease.ctr + ps);
+    const int rc2 = scratch_done(ds, stream);
+    return rc ? rc : rc2;
   }
 
 #ifndef CIM_NO_K8

@@ -33,7 +33,7 @@ def supported_k(dtype: torch.dtype, k: int, layout: str = "frag") -> bool:
 
 
 TC_MAX_K = 64  # f32 vectors per tensor-core apply (N = 2k ≤ 128 TMEM columns per accumulator)
-TC_MAX_K_F64 = 32  # f64 (DMMA kernel, register-resident accumulators)
+TC_MAX_K_F64 = 64  # f64: one C-ABI call (the DMMA kernel takes ≤ 32; k = 64 runs as two column passes inside)
 
 
 def tc_max_k(dtype: torch.dtype) -> int:
@@ -42,8 +42,8 @@ def tc_max_k(dtype: torch.dtype) -> int:
 
 def padded_k(dtype: torch.dtype, k: int, layout: str = "frag") -> int:
     """Smallest compiled vector count ≥ k for the layout (extra columns are zero).
-    The tensor-core layout takes multiples of 8 up to 64 (f32) / 32 (f64);
-    wider f64 blocks run as column passes of 32."""
+    The tensor-core layout takes multiples of 8 up to 64 (f32) / 32 (f64)
+    and f64 k = 64 (two column passes of 32 inside the library)."""
     kk = int(k)
     if layout == "tc" and kk > tc_max_k(dtype):
         return -(-kk // tc_max_k(dtype)) * tc_max_k(dtype)

@@ -449,7 +449,9 @@ def test_c2_full_size_properties(pkg, layout):
 
 @pytest.mark.parametrize("dtype,k,layout", [(torch.float32, 8, "frag"), (torch.float32, 4, "frag"), (torch.float64, 8, "frag"),
                                              (torch.float32, 32, "frag"), (torch.float64, 16, "frag"),
-                                             (torch.float32, 16, "tc"), (torch.float64, 8, "tc")])
+                                             (torch.float32, 16, "tc"), (torch.float64, 8, "tc"),
+                                             (torch.float32, 64, "tc"), (torch.float64, 32, "tc"),
+                                             (torch.float64, 64, "frag"), (torch.float64, 64, "tc")])
 def test_host_batch_pipeline_matches_oracle(pkg, c1_small, dtype, k, layout):
     """cim_sym_spmm_host_batch: host (pinned and pageable, numpy and torch)
     blocks in, host blocks out; every block checked against the oracle, and
@@ -912,3 +914,49 @@ def test_tensor_core_kernels_strided_y_and_accumulate(pkg, c1_small, dtype, k):
     Y2 = Yv.cpu().numpy()[:n]
     tol = 1e-5 if dtype == torch.float32 else 1e-12
     assert np.abs(Y2 - 2 * Y1).max() <= tol * np.abs(Y1).max()
+
+
+@pytest.mark.parametrize("dtype,layout,k", [(torch.float32, "frag", 8), (torch.float32, "tc", 16),
+                                            (torch.float32, "tc", 40), (torch.float64, "tc", 8),
+                                            (torch.float64, "tc", 24), (torch.float64, "frag", 64),
+                                            (torch.float32, "frag", 5), (torch.float64, "tc", 3)])
+def test_api_layouts_and_accumulate(pkg, c1_small, dtype, layout, k):
+    """The public call in its variants on every kernel family: X as (n, k) or
+    the reference's (k, n), torch or numpy, `out=` (device / numpy) and
+    `accumulate=True`, padded widths — each against the oracle."""
+    n, rc, tiles = c1_small
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=dtype, layout=layout)
+    tl = tiles.astype(np.float64)
+    g = torch.Generator().manual_seed(11 + k)
+    X = torch.randn((n, k), generator=g, dtype=dtype)
+    Y_nk = pkg.sym_spmm(H, X.cuda()).cpu().numpy()
+    check_result(n, rc, tl, X.numpy(), Y_nk, dtype)
+    # the reference layout (k, n), numpy in → numpy out
+    Y_kn = pkg.sym_spmm(H, np.ascontiguousarray(X.numpy().T))
+    assert isinstance(Y_kn, np.ndarray) and Y_kn.shape == (k, n)
+    tol = 1e-5 if dtype == torch.float32 else 1e-12
+    scale = max(1.0, np.abs(Y_nk).max())
+    assert np.abs(Y_kn.T - Y_nk).max() <= tol * scale
+    # out= on the device, then accumulate into it
+    out = torch.empty((n, k), dtype=dtype, device="cuda")
+    assert pkg.sym_spmm(H, X.cuda(), out=out) is out
+    assert np.abs(out.cpu().numpy() - Y_nk).max() <= tol * scale
+    pkg.sym_spmm(H, X.cuda(), out=out, accumulate=True)
+    assert np.abs(out.cpu().numpy() - 2 * Y_nk).max() <= 2 * tol * scale
+    # out= numpy
+    out_np = np.zeros((n, k), dtype=np.float32 if dtype == torch.float32 else np.float64)
+    pkg.sym_spmm(H, X.numpy(), out=out_np)
+    assert np.abs(out_np - Y_nk).max() <= tol * scale
+
+
+@pytest.mark.parametrize("dtype,k,layout,kk", [(torch.float32, 3, "frag", 4), (torch.float64, 48, "tc", 64),
+                                               (torch.float32, 20, "tc", 24)])
+def test_host_batch_rejects_uncompiled_widths(pkg, c1_small, dtype, k, layout, kk):
+    """The host-buffer pipeline hands blocks straight to the C-ABI: a width
+    without a compiled kernel (which sym_spmm pads or splits into column
+    passes on the device) is refused before any copy, naming the width to pad
+    to."""
+    n, rc, _ = c1_small
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=dtype, layout=layout)
+    with pytest.raises(ValueError, match=f"pad X to k={kk}"):
+        pkg.sym_spmm_host_batch(H, [torch.zeros((n, k), dtype=dtype)])
