@@ -93,6 +93,12 @@ def kernel_label(dtype, k: int, layout: str = "frag") -> tuple[str, int]:
     """(the dense-tile kernel the library dispatches for (dtype, k, layout),
     our kernel launches per apply besides the Y memset) — the dispatch of
     sym_spmm_dense in csrc/sym_spmm.cu."""
+    if layout == "tc" and dtype == torch.float64:
+        swz = " with TMA 128-byte-swizzled X" if k in (16, 32, 64) else ""
+        if k > 32:
+            return (f"sym_spmm_dmma_kernel<32> (DMMA m8n8k4{swz}, {k // 32} column passes) + pass_major_kernel",
+                    1 + k // 32)
+        return f"sym_spmm_dmma_kernel<{k}> (DMMA m8n8k4{swz})", 1
     if layout == "tc":
         return "sym_spmm_tc_kernel<%d> (tcgen05 kind::tf32, A = [T; Tᵀ] in TMEM, 3xTF32 along K)" % k, 1
     if dtype == torch.float32 and k == 8:
@@ -101,7 +107,7 @@ def kernel_label(dtype, k: int, layout: str = "frag") -> tuple[str, int]:
         return (f"sym_spmm_k8r3_kernel<float, 8> (FFMA2, {k // 8} paired passes) + pass_major_kernel", 2)
     if dtype == torch.float64 and k in (4, 8):
         return f"sym_spmm_k8_kernel<double, G={k // 4}> (DFMA, two rings)", 1
-    if dtype == torch.float64 and k in (12, 16, 32):
+    if dtype == torch.float64 and (k in (12, 16, 32) or (k > 16 and k % 4 == 0 and k != 24)):
         g = 2 if (k // 4) % 2 == 0 else 1
         return f"sym_spmm_k8_kernel<double, G={g}> (DFMA, {k // (4 * g)} paired passes) + pass_major_kernel", 2
     return "sym_spmm_kernel (FFMA/DFMA, shared-memory column reduction)", 1

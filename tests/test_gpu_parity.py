@@ -143,7 +143,8 @@ def test_contract_observables_matches_reference(pkg, name, layout):
         assert np.all(np.abs(got - 1.0) <= 2.0 ** -20)
 
 
-@pytest.mark.parametrize("dtype,layout", [(torch.float32, "frag"), (torch.float32, "tc"), (torch.float64, "frag")])
+@pytest.mark.parametrize("dtype,layout", [(torch.float32, "frag"), (torch.float32, "tc"), (torch.float64, "frag"),
+                                          (torch.float64, "tc")])
 @pytest.mark.parametrize("n_vec,m_ops,op_kind", [(1, 1, "symmetric_hash"), (8, 3, "symmetric_hash"),
                                                  (16, 16, "symmetric_hash"), (5, 7, "identity"),
                                                  (20, 19, "symmetric_hash")])
@@ -960,3 +961,43 @@ def test_host_batch_rejects_uncompiled_widths(pkg, c1_small, dtype, k, layout, k
     H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=dtype, layout=layout)
     with pytest.raises(ValueError, match=f"pad X to k={kk}"):
         pkg.sym_spmm_host_batch(H, [torch.zeros((n, k), dtype=dtype)])
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_tensor_core_layout_around_the_operator(pkg, tmp_path, dtype):
+    """The tensor-core tile layout through the rest of the API: npz save/load
+    (values round-trip bit-exactly into the same layout), a reference basis
+    built on the device straight into tc tiles (vs the reference's scipy
+    product), the fused contraction over a tc pattern (vs the frag pattern),
+    and LOBPCG on tc tiles (vs the frag tiles' Ritz values)."""
+    from paper_2110_10765_b200.lobpcg import lobpcg_sym
+
+    tol = 1e-5 if dtype == torch.float32 else 1e-12
+    f = load_fixture("skel_n1024.npz")
+    Hb = pkg.HalfTiles.from_basis(f["basis_occ"], f["basis_bits_lo"], rank=int(f["rank_threshold"]) // 2,
+                                  dtype=dtype, layout="tc")
+    assert Hb.layout == "tc"
+    k = 16
+    X = torch.from_numpy(np.ascontiguousarray(np.tile(f["X"], (1, k // f["X"].shape[1] + 1))[:, :k])).to(dtype)
+    Yb = pkg.sym_spmm(Hb, X.cuda()).cpu().numpy()
+    Hf = pkg.HalfTiles.from_basis(f["basis_occ"], f["basis_bits_lo"], rank=int(f["rank_threshold"]) // 2,
+                                  dtype=dtype, layout="frag")
+    Yf = pkg.sym_spmm(Hf, X.cuda()).cpu().numpy()
+    assert np.abs(Yb - Yf).max() <= tol * max(1.0, np.abs(Yf).max())
+    kx = f["X"].shape[1]
+    rel = np.linalg.norm(Yb[:, :kx] - f["Y_ref"]) / np.linalg.norm(f["Y_ref"])
+    assert rel <= tol
+    # save / load keeps the layout and the values
+    Hb.save(tmp_path / "tc.npz")
+    H2 = pkg.HalfTiles.load(tmp_path / "tc.npz")
+    assert H2.layout == "tc" and torch.equal(H2.vals, Hb.vals) and H2.n_sparse_tiles == Hb.n_sparse_tiles
+    Y2 = pkg.sym_spmm(H2, X.cuda()).cpu().numpy()
+    assert np.abs(Y2 - Yb).max() <= tol * max(1.0, np.abs(Yb).max())
+    # LOBPCG on tc tiles: the same lowest Ritz values as on frag tiles
+    n = 2048
+    rc = pkg.synthetic_pattern(n // 64, 0.1, seed=2)
+    Ht = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=dtype, layout="tc")
+    Hq = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=dtype, layout="frag")
+    lt = np.sort(lobpcg_sym(Ht, 8, tol=1e-6, max_iter=800, dtype=torch.float64).eigenvalues)
+    lq = np.sort(lobpcg_sym(Hq, 8, tol=1e-6, max_iter=800, dtype=torch.float64).eigenvalues)
+    assert np.abs(lt - lq).max() <= 1e-4 * np.abs(lq).max()
