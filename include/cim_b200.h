@@ -70,9 +70,9 @@ extern "C" {
 #define CIM_ACCUMULATE    1u  /* Y += A·X instead of Y = A·X                */
 #define CIM_DETERMINISTIC 2u  /* no float atomics: every Y row block summed
                                  in a fixed order by one CTA (bitwise
-                                 reproducible; needs the det_* tile lists,
-                                 fragment-layout tiles; reads each        
-                                 tile twice — a validation mode)           */
+                                 reproducible; needs the det_* tile lists;
+                                 either tile layout; reads each tile
+                                 twice — a validation mode)                */
 
 /* cim_contract_tiles flags (with CIM_ACCUMULATE) */
 #define CIM_CONTRACT_EXACT_F64 4u  /* products and sums in f64: contract_oracle

@@ -35,6 +35,17 @@ __device__ __forceinline__ int frag_index(int r, int c) {
     return ((2 * i + (j >> 1)) * 128 + mb) * 2 + (j & 1);
 }
 
+// Storage index of tile element (r, c) in either tile layout: fragment order
+// v1 or the tensor-core layout's row-major rows with 4-element chunks
+// XOR-swizzled by row (include/cim_b200.h).
+template <typename T, bool TC>
+__device__ __forceinline__ int tile_index(int r, int c) {
+  if constexpr (TC)
+    return r * 64 + (((c >> 2) ^ (r & 7)) << 2) + (c & 3);
+  else
+    return frag_index<T>(r, c);
+}
+
 template <typename T>
 struct DetSparse {
   long long n_tiles;
@@ -54,7 +65,7 @@ __device__ __forceinline__ void det_fma(T (&acc)[VMAX], T a, const T *x, int g, 
   }
 }
 
-template <typename T>
+template <typename T, bool TC>
 __global__ void __launch_bounds__(kDetThreads) det_spmm_kernel(int n_dense, const int2 *tile_rc, const T *vals,
                                                                DetSparse<T> sp, const long long *row_ptr,
                                                                const int *row_tiles, const long long *col_ptr,
@@ -81,7 +92,7 @@ __global__ void __launch_bounds__(kDetThreads) det_spmm_kernel(int n_dense, cons
     const int C = tile_rc[t].y;
     const T *tv = vals + (size_t)t * kTileElems;
     const T *xc = X + (long long)C * 64 * k;
-    for (int c = 0; c < 64; ++c) det_fma<T, VMAX>(acc, tv[frag_index<T>(r, c)], xc + (long long)c * k, g, k);
+    for (int c = 0; c < 64; ++c) det_fma<T, VMAX>(acc, tv[tile_index<T, TC>(r, c)], xc + (long long)c * k, g, k);
   }
   // transposed: Y_b[r] += Σ_r' T[r'][r] X_R[r'] over tiles (R, b), R < b
   for (long long s = col_ptr[b]; s < col_ptr[b + 1]; ++s) {
@@ -100,7 +111,7 @@ __global__ void __launch_bounds__(kDetThreads) det_spmm_kernel(int n_dense, cons
     const int R = tile_rc[t].x;
     const T *tv = vals + (size_t)t * kTileElems;
     const T *xr = X + (long long)R * 64 * k;
-    for (int rr = 0; rr < 64; ++rr) det_fma<T, VMAX>(acc, tv[frag_index<T>(rr, r)], xr + (long long)rr * k, g, k);
+    for (int rr = 0; rr < 64; ++rr) det_fma<T, VMAX>(acc, tv[tile_index<T, TC>(rr, r)], xr + (long long)rr * k, g, k);
   }
   T *y = Y + ((long long)b * 64 + r) * ldy;
 #pragma unroll
@@ -114,7 +125,7 @@ __global__ void __launch_bounds__(kDetThreads) det_spmm_kernel(int n_dense, cons
 
 int sym_spmm_deterministic(const cim_half_tiles *H, const void *X, void *Y, int k, long long ldy, bool accumulate,
                            cudaStream_t stream) {
-  if (H->layout != CIM_LAYOUT_FRAG) return set_error(CIM_EUNSUPPORTED, "CIM_DETERMINISTIC needs fragment-layout tiles");
+  if (H->layout != CIM_LAYOUT_FRAG && H->layout != CIM_LAYOUT_TC) return set_error(CIM_EINVAL, "unknown tile layout");
   if (k > kDetMaxK) return set_error(CIM_EUNSUPPORTED, "CIM_DETERMINISTIC supports k <= 64");
   if (!H->det_row_ptr || !H->det_row_tiles || !H->det_col_ptr || !H->det_col_tiles)
     return set_error(CIM_EINVAL, "CIM_DETERMINISTIC needs the det_* tile lists");
@@ -132,7 +143,8 @@ int sym_spmm_deterministic(const cim_half_tiles *H, const void *X, void *Y, int 
     if (has_sp)
       sp = {S->n_tiles,  reinterpret_cast<const int2 *>(S->tile_rc), reinterpret_cast<const long long *>(S->entry_off),
             S->rowptr,   S->colptr, S->cperm, S->col, S->row, static_cast<const T *>(S->vals)};
-    det_spmm_kernel<T><<<(unsigned)nb, kDetThreads, 0, stream>>>(
+    auto kern = H->layout == CIM_LAYOUT_TC ? det_spmm_kernel<T, true> : det_spmm_kernel<T, false>;
+    kern<<<(unsigned)nb, kDetThreads, 0, stream>>>(
         (int)H->n_tiles, rc, static_cast<const T *>(H->vals), sp, reinterpret_cast<const long long *>(H->det_row_ptr),
         H->det_row_tiles, reinterpret_cast<const long long *>(H->det_col_ptr), H->det_col_tiles,
         static_cast<const T *>(X), static_cast<T *>(Y), k, ldy, accumulate);

@@ -770,12 +770,14 @@ def test_synthetic_sparse_device_construction(pkg, fill):
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 @pytest.mark.parametrize("k", [1, 4, 8, 16, 32, 64])
-def test_deterministic_mode_bitwise_reproducible(pkg, c1_small, dtype, k):
+@pytest.mark.parametrize("layout", ["frag", "tc"])
+def test_deterministic_mode_bitwise_reproducible(pkg, c1_small, dtype, k, layout):
     """CIM_DETERMINISTIC: no float atomics — repeated applies are bitwise
     identical (the atomic path is not, in general), and the result passes the
-    oracle gates; accumulate adds onto Y."""
+    oracle gates; accumulate adds onto Y.  Both tile layouts walk the same
+    elements in the same order: the same bits."""
     n, rc, tiles = c1_small
-    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=dtype, max_unit=3)
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=dtype, max_unit=3, layout=layout)
     X = torch.randn((n, k), generator=torch.Generator().manual_seed(k), dtype=dtype).cuda()
     Y1 = pkg.sym_spmm(H, X, deterministic=True)
     Y2 = pkg.sym_spmm(H, X, deterministic=True)
@@ -785,6 +787,9 @@ def test_deterministic_mode_bitwise_reproducible(pkg, c1_small, dtype, k):
     out = torch.ones_like(X)
     pkg.sym_spmm(H, X, out=out, accumulate=True, deterministic=True)
     assert torch.equal(out, Y1 + 1.0)
+    if layout == "tc":
+        Hf = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=dtype, max_unit=3, layout="frag")
+        assert torch.equal(Y1, pkg.sym_spmm(Hf, X, deterministic=True))
 
 
 @pytest.mark.parametrize("name", ["skel_small.npz", "skel_n1024.npz", "skel_identity.npz"])
