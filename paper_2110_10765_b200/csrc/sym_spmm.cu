@@ -1730,7 +1730,8 @@ int launch_wide(const cim_half_tiles *H, int k, const Chunks &ck, long long ldy,
       case 32: return launch_k8<double, 2, 32>(H, ck, ldy, stream, ds);
     }
   }
-  return CIM_EUNSUPPORTED;
+  return set_error(CIM_EUNSUPPORTED, "no single-launch wide kernel for (dtype, k) (multi-pass widths run through "
+                                     "cim_sym_spmm only)");
 }
 
 bool wide_supported(int dtype, int k) {
