@@ -525,9 +525,9 @@ def lobpcg(apply: Callable[[torch.Tensor], torch.Tensor], X0: torch.Tensor, *, t
             break
         if apply_out:  # W's unused columns are zero, so A·W over the full block is AW
             apply(cur.buf[Wk.W], out=cur.buf[Wk.AW])
-        else:
+        else:  # the operator takes the solver's m-column blocks; W's columns ≥ nw are zero
             cur.buf[Wk.AW].zero_()
-            cur.slot(Wk.AW, nw).copy_(apply(cur.slot(Wk.W, nw).contiguous()))
+            cur.slot(Wk.AW, m).copy_(apply(cur.slot(Wk.W, m).contiguous()))
         calls += 1
         # Rayleigh–Ritz on S = [P X W] (or [X W]): one Gram pass of S against
         # all six slots gives SᵀS and SᵀAS
