@@ -390,15 +390,22 @@ def test_save_load_roundtrip(pkg, c1_small, tmp_path):
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and M2.n_sparse_tiles == M.n_sparse_tiles
 
 
-@pytest.mark.parametrize("dtype,k,layout", [(torch.float32, 8, "frag"), (torch.float32, 16, "tc"), (torch.float64, 8, "tc")])
+@pytest.mark.parametrize("dtype,k,layout", [(torch.float32, 8, "frag"), (torch.float32, 16, "tc"), (torch.float64, 8, "tc"),
+                                             (torch.float32, 3, "frag"), (torch.float64, 12, "frag"),
+                                             (torch.float32, 40, "tc"), (torch.float64, 20, "frag"),
+                                             (torch.float64, 64, "tc")])
 def test_sharded_world1_equals_direct(pkg, dtype, k, layout):
-    n = 4096
+    n = 4000  # ragged: the last block row is partly padding
     S = pkg.ShardedSymSpmm.synthetic(n, k=k, p=0.1, seed=3, dtype=dtype, layout=layout)
-    rc = pkg.synthetic_pattern(64, 0.1, seed=3)
+    rc = pkg.synthetic_pattern((n + 63) // 64, 0.1, seed=3)
     H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=dtype, layout=layout)
-    X = torch.randn((n, k), generator=torch.Generator().manual_seed(0), dtype=dtype).cuda()
+    X = torch.zeros((S.rows_per_rank, k), dtype=dtype)  # the operator's rows: n_pad, rows ≥ n zero
+    X[:n] = torch.randn((n, k), generator=torch.Generator().manual_seed(0), dtype=dtype)
+    X = X.cuda()
     Y = S.apply(X)
-    assert torch.allclose(Y, pkg.sym_spmm(H, X), rtol=0, atol=1e-5 * pkg.sym_spmm(H, X).abs().max().item())
+    Yd = pkg.sym_spmm(H, X[:n].contiguous())
+    assert torch.allclose(Y[:n], Yd, rtol=0, atol=1e-5 * Yd.abs().max().item())
+    assert torch.all(Y[n:] == 0)
 
 
 # ----------------------------------------------------------------------------
