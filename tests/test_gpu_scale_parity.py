@@ -193,14 +193,14 @@ def _sharded_worker(rank, world, port, kind, overlap, q):
         import paper_2110_10765_b200 as pkg
 
         torch.cuda.set_device(0)
-        n, k = 3000, (16 if kind.startswith("synthetic_tc") else 8)
+        n, k = 3000, (16 if kind.startswith("synthetic_tc") or kind == "mixed_tc" else 8)
         dt = torch.float64 if kind == "synthetic_tc64" else torch.float32
         if kind.startswith("synthetic"):
             S = pkg.ShardedSymSpmm.synthetic(n, k=k, p=0.2, seed=5, device="cuda:0", max_unit=4, overlap=overlap,
                                              layout="tc" if kind.startswith("synthetic_tc") else None, dtype=dt)
         else:  # mixed dense + sparse tiles, every rank builds the global matrix and keeps its panel
             H = pkg.HalfTiles.synthetic_sparse(n, 0.2, fill=0.07, seed=5, fill_seed=3)
-            D = pkg.HalfTiles.synthetic(n, p=0.05, seed=9)
+            D = pkg.HalfTiles.synthetic(n, p=0.05, seed=9, layout="tc" if kind == "mixed_tc" else None)
             Hm = merge_dense_sparse(pkg, D, H)
             S = pkg.ShardedSymSpmm.from_halftiles(Hm, k=k, overlap=overlap)
         g = torch.Generator().manual_seed(7)
@@ -242,7 +242,8 @@ def _global_reference(pkg, kind, n):
 @pytest.mark.parametrize("world,kind,overlap", [(2, "synthetic", False), (2, "synthetic", True), (2, "mixed", False),
                                                 (2, "mixed", True), (3, "synthetic", True), (3, "mixed", True),
                                                 (3, "mixed", False), (2, "synthetic_tc", True), (3, "synthetic_tc", False),
-                                                (2, "synthetic_tc64", True), (3, "synthetic_tc64", False)])
+                                                (2, "synthetic_tc64", True), (3, "synthetic_tc64", False),
+                                                (2, "mixed_tc", True), (3, "mixed_tc", False)])
 def test_sharded_cuda_ranks_one_gpu(pkg, world, kind, overlap):
     """Two or three processes, one GPU, the product's default CUDA panel
     kernels: the balanced partition (dense and mixed dense + sparse panels),
@@ -251,7 +252,7 @@ def test_sharded_cuda_ranks_one_gpu(pkg, world, kind, overlap):
     the f64 oracle of the global matrix."""
     import torch.multiprocessing as mp
 
-    n, k = 3000, (16 if kind.startswith("synthetic_tc") else 8)
+    n, k = 3000, (16 if kind.startswith("synthetic_tc") or kind == "mixed_tc" else 8)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
