@@ -1013,3 +1013,44 @@ def test_tensor_core_layout_around_the_operator(pkg, tmp_path, dtype):
     lt = np.sort(lobpcg_sym(Ht, 8, tol=1e-6, max_iter=800, dtype=torch.float64).eigenvalues)
     lq = np.sort(lobpcg_sym(Hq, 8, tol=1e-6, max_iter=800, dtype=torch.float64).eigenvalues)
     assert np.abs(lt - lq).max() <= 1e-4 * np.abs(lq).max()
+
+
+@pytest.mark.parametrize("layout", ["frag", "tc"])
+def test_c_abi_rejects_bad_arguments(pkg, c1_small, layout):
+    """cim_sym_spmm validates before any launch: every malformed call returns
+    its documented code (EINVAL 1 / EUNSUPPORTED 3) with a message, nothing
+    is written to Y, and a good call afterwards still works."""
+    import ctypes
+
+    from paper_2110_10765_b200._lib import CIM_EINVAL, CIM_EUNSUPPORTED, lib
+
+    L = lib()
+    n, rc, tiles = c1_small
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, layout=layout)
+    d = H.descriptor()
+    k = 16
+    X = torch.randn((H.n_pad, k), device="cuda")
+    Y = torch.full((H.n_pad + 8, k), 7.0, device="cuda")
+    st = None
+    kb = 12  # no f32 kernel for k = 12 in either layout (16-byte rows, so validation passes)
+    cases = [
+        (L.cim_sym_spmm(None, X.data_ptr(), Y.data_ptr(), k, k, k, 0, st), CIM_EINVAL),
+        (L.cim_sym_spmm(d, 0, Y.data_ptr(), k, k, k, 0, st), CIM_EINVAL),
+        (L.cim_sym_spmm(d, X.data_ptr(), 0, k, k, k, 0, st), CIM_EINVAL),
+        (L.cim_sym_spmm(d, X.data_ptr() + 4, Y.data_ptr(), k, k, k, 0, st), CIM_EINVAL),  # misaligned X
+        (L.cim_sym_spmm(d, X.data_ptr(), Y.data_ptr() + 4, k, k, k, 0, st), CIM_EINVAL),  # misaligned Y
+        (L.cim_sym_spmm(d, X.data_ptr(), Y.data_ptr(), k, k, k - 1, 0, st), CIM_EINVAL),  # ldy < k
+        (L.cim_sym_spmm(d, X.data_ptr(), Y.data_ptr(), 0, k, k, 0, st), None),
+        (L.cim_sym_spmm(d, X.data_ptr(), Y.data_ptr(), 65, 65, 65, 0, st), None),
+        (L.cim_sym_spmm(d, X.data_ptr(), Y.data_ptr(), kb, kb, kb, 0, st), CIM_EUNSUPPORTED),  # no kernel
+    ]
+    for got, want in cases:
+        assert got != 0
+        if want is not None:
+            assert got == want, (got, want)
+        assert L.cim_last_error() and len(L.cim_last_error()) > 0
+    torch.cuda.synchronize()
+    assert torch.all(Y == 7.0)  # nothing written by a refused call
+    assert L.cim_sym_spmm(d, X.data_ptr(), Y.data_ptr(), k, k, k, 0, st) == 0
+    tl = tiles.astype(np.float64)
+    check_result(n, rc, tl, X[:n].cpu().numpy(), Y[:n].cpu().numpy(), torch.float32)
