@@ -248,15 +248,16 @@ def test_k_sweep_f64(pkg, c1_small, k, layout):
     check_result(n, rc, tiles.astype(np.float64), X.numpy(), Y, torch.float64)
 
 
-@pytest.mark.parametrize("dtype,k", [(torch.float32, 32), (torch.float32, 64), (torch.float64, 16),
-                                     (torch.float64, 64)])
-def test_multipass_widths_on_concurrent_streams(pkg, c1_small, dtype, k):
+@pytest.mark.parametrize("dtype,k,layout", [(torch.float32, 32, "frag"), (torch.float32, 64, "frag"),
+                                             (torch.float64, 16, "frag"), (torch.float64, 64, "frag"),
+                                             (torch.float32, 32, "tc"), (torch.float64, 64, "tc")])
+def test_multipass_widths_on_concurrent_streams(pkg, c1_small, dtype, k, layout):
     """Widths above one pass stage a pass-major copy of X in a per-stream
     scratch buffer: applies queued on two streams at once (different X, same
     H) must each match their own oracle product, and repeated calls on one
     stream (the buffer reused) stay exact."""
     n, rc, tiles = c1_small
-    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=dtype)
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=dtype, layout=layout)
     g = torch.Generator().manual_seed(k)
     Xs = [torch.randn((n, k), generator=g, dtype=dtype) for _ in range(2)]
     streams = [torch.cuda.Stream(), torch.cuda.Stream()]
