@@ -305,15 +305,18 @@ def test_c1_config_vs_c_oracle(pkg, layout):
     assert oracle.componentwise_ok(Y, Y_ref, absAX, nnz_row, U32)
 
 
-@pytest.mark.parametrize("layout", F32_LAYOUTS)
+@pytest.mark.parametrize("dtype,layout,k", [(torch.float32, "tc", 4), (torch.float32, "frag", 4),
+                                            (torch.float32, "tc", 32), (torch.float64, "frag", 4),
+                                            (torch.float64, "tc", 16), (torch.float64, "tc", 64)])
 @pytest.mark.parametrize("n", [1, 63, 64, 65, 200])
-def test_ragged_and_tiny(pkg, n, layout):
+def test_ragged_and_tiny(pkg, n, dtype, layout, k):
     nb = (n + 63) // 64
     rc = pkg.synthetic_pattern(nb, 1.0, seed=0)  # every upper tile
     tiles = oracle.synthetic_dense_tiles(n, rc, seed=5)
-    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, value_seed=5, layout=layout)
-    X = torch.randn((n, 4), generator=torch.Generator().manual_seed(n))
-    check_result(n, rc, tiles, X.numpy(), pkg.sym_spmm(H, X.cuda()).cpu().numpy(), torch.float32)
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, value_seed=5, layout=layout, dtype=dtype)
+    X = torch.randn((n, k), generator=torch.Generator().manual_seed(n), dtype=dtype)
+    check_result(n, rc, tiles.astype(np.float64) if dtype == torch.float64 else tiles, X.numpy(),
+                 pkg.sym_spmm(H, X.cuda()).cpu().numpy(), dtype)
 
 
 @pytest.mark.parametrize("layout", F32_LAYOUTS)
