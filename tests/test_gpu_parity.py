@@ -319,16 +319,19 @@ def test_ragged_and_tiny(pkg, n, dtype, layout, k):
                  pkg.sym_spmm(H, X.cuda()).cpu().numpy(), dtype)
 
 
-@pytest.mark.parametrize("layout", F32_LAYOUTS)
-def test_diagonal_only_and_long_rows(pkg, layout):
+@pytest.mark.parametrize("dtype,layout,k", [(torch.float32, "frag", 8), (torch.float32, "tc", 8),
+                                            (torch.float32, "tc", 64), (torch.float64, "tc", 32),
+                                            (torch.float64, "frag", 8)])
+def test_diagonal_only_and_long_rows(pkg, dtype, layout, k):
     # no off-diagonal tiles at all; then a dense upper triangle (long block rows → many units)
     for p in (0.0, 1.0):
         n = 40 * 64
         rc = pkg.synthetic_pattern(40, p, seed=0)
-        H = pkg.HalfTiles.synthetic(n, tile_rc=rc, max_unit=7, layout=layout)
+        H = pkg.HalfTiles.synthetic(n, tile_rc=rc, max_unit=7, layout=layout, dtype=dtype)
         tiles = oracle.synthetic_dense_tiles(n, rc, seed=0)
-        X = torch.randn((n, 8), generator=torch.Generator().manual_seed(2))
-        check_result(n, rc, tiles, X.numpy(), pkg.sym_spmm(H, X.cuda()).cpu().numpy(), torch.float32)
+        X = torch.randn((n, k), generator=torch.Generator().manual_seed(2), dtype=dtype)
+        check_result(n, rc, tiles.astype(np.float64) if dtype == torch.float64 else tiles, X.numpy(),
+                     pkg.sym_spmm(H, X.cuda()).cpu().numpy(), dtype)
 
 
 def test_layouts_numpy_out_accumulate(pkg, c1_small):
