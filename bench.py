@@ -103,7 +103,7 @@ def kernel_label(dtype, k: int, layout: str = "frag") -> tuple[str, int]:
         return "sym_spmm_tc_kernel<%d> (tcgen05 kind::tf32, A = [T; Tᵀ] in TMEM, 3xTF32 along K)" % k, 1
     if dtype == torch.float32 and k == 8:
         return "sym_spmm_k8r3_kernel<float, 8> (FFMA2, three rings per CTA)", 1
-    if dtype == torch.float32 and k in (16, 24, 32, 48, 64):
+    if dtype == torch.float32 and k > 8 and k % 8 == 0:
         return (f"sym_spmm_k8r3_kernel<float, 8> (FFMA2, {k // 8} paired passes) + pass_major_kernel", 2)
     if dtype == torch.float64 and k in (4, 8):
         return f"sym_spmm_k8_kernel<double, G={k // 4}> (DFMA, two rings)", 1

@@ -1735,7 +1735,7 @@ int launch_wide(const cim_half_tiles *H, int k, const Chunks &ck, long long ldy,
 }
 
 bool wide_supported(int dtype, int k) {
-  if (dtype == CIM_F32) return k == 8 || k == 16 || k == 24 || k == 32 || k == 48 || k == 64;
+  if (dtype == CIM_F32) return k % 8 == 0 && k >= 8 && k <= 64;  // k > 8: paired passes of 8 (or 16 / 8)
   // f64 k = 20, 28 and k > 32: column passes of the wide kernel (a
   // generic-kernel stage with whole 64-row X blocks of that many doubles
   // does not fit shared memory)
@@ -1856,8 +1856,8 @@ static int sym_spmm_dense(const cim_half_tiles *H, const void *X, void *Y, int32
       return launch_k8r3_paired<float, 8>(H, X, Y, k, ldy, stream, ds);
     if (H->dtype == CIM_F64 && k > 4 && k % 4 == 0 && use_r3() && use_paired_f64())
       return launch_k8r3_paired<double, 4>(H, X, Y, k, ldy, stream, ds);
-    if (H->dtype == CIM_F32 && (k == 32 || k == 48 || k == 64)) return launch_k8_passes<float, 2>(H, X, Y, k, ldy, stream, ds);
-    if (H->dtype == CIM_F32 && k == 24) return launch_k8_passes<float, 1>(H, X, Y, k, ldy, stream, ds);
+    if (H->dtype == CIM_F32 && k > 16 && k % 16 == 0) return launch_k8_passes<float, 2>(H, X, Y, k, ldy, stream, ds);
+    if (H->dtype == CIM_F32 && k > 16) return launch_k8_passes<float, 1>(H, X, Y, k, ldy, stream, ds);
     if (H->dtype == CIM_F64 && (k == 16 || k == 32)) return launch_k8_passes<double, 2>(H, X, Y, k, ldy, stream, ds);
     if (H->dtype == CIM_F64 && k == 12) return launch_k8_passes<double, 1>(H, X, Y, k, ldy, stream, ds);
     if (H->dtype == CIM_F64 && k > 32 && k % 8 == 0) return launch_k8_passes<double, 2>(H, X, Y, k, ldy, stream, ds);
