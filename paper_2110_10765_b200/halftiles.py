@@ -624,14 +624,18 @@ class HalfTiles:
         return 2 * k * ((2 * self.n_off_tiles + self.n_diag_tiles) * BLOCK * BLOCK + 2 * s_off + s_diag)
 
     def algorithmic_bytes(self, k: int) -> int:
-        """s·nnz_stored + index bytes + 8·tiles + 2·n·k·s:
-        sparse entries carry a column, a row and a column-permutation index
-        (4 B), sparse tiles two 130-byte pointer arrays and an 8-byte offset."""
+        """SURVEY.md §8(d) literally: s·nnz_stored + 2·nnz_COO + 8·n_tiles +
+        2·n·k·s — a COO-in-tile entry is credited its value and a 2-byte
+        (row, column) index, every stored tile (dense or sparse) its 8-byte
+        (R, C) header, X read once and Y written once.  The storage's other
+        index bytes (column permutation, per-tile pointer arrays, the
+        small-tile CSR) and any extra X gathers or Y updates are overhead,
+        not credit."""
         s = self.vals.element_size()
-        idx = 0
+        n_coo, n_sp_tiles = 0, 0
         if self.sparse is not None:
-            idx = 4 * self.sparse.n_real_entries + (260 + 8 + 8) * self.sparse.n_tiles
-        return s * self.nnz_stored + idx + 8 * self.n_tiles + 2 * self.n * k * s
+            n_coo, n_sp_tiles = self.sparse.n_real_entries, self.sparse.n_tiles
+        return s * self.nnz_stored + 2 * n_coo + 8 * (self.n_tiles + n_sp_tiles) + 2 * self.n * k * s
 
     def descriptor(self) -> CimHalfTiles:
         if self._desc is None:
