@@ -189,6 +189,9 @@ def candidate_tiles(and_: np.ndarray, or_: np.ndarray, threshold: int) -> np.nda
     return np.concatenate(out).astype(np.int32)
 
 
+COUNT_CHUNK_TILES = 1 << 25  # candidate tiles counted per pass (8 GB of per-row counts)
+
+
 def from_basis(basis_or_occ, bits_lo=None, *, rank: int = 2, value_seed: int = 0, dtype=torch.float32,
                device="cuda", dense_fill: float | None = None, max_unit: int | None = None,
                layout: str | None = None) -> HalfTiles:
@@ -210,15 +213,34 @@ def from_basis(basis_or_occ, bits_lo=None, *, rank: int = 2, value_seed: int = 0
     stream = torch.cuda.current_stream(dev).cuda_stream
     d_lo = torch.from_numpy(lo.view(np.int64)).to(dev)
     d_occ = torch.from_numpy(occ.view(np.int16)).to(dev)
+    T_cand = cand.shape[0]
+    # count in chunks of candidate tiles and keep only the non-empty ones:
+    # the block-pair bound can leave most block pairs as candidates (weakly
+    # grouped bases), and per-row counts of every candidate would not fit
+    kept_rc, kept_cnt = [], []
+    for c0 in range(0, max(T_cand, 1), COUNT_CHUNK_TILES):
+        chunk = cand[c0:c0 + COUNT_CHUNK_TILES]
+        Tc = chunk.shape[0]
+        if Tc == 0:
+            break
+        d_cand = torch.from_numpy(np.ascontiguousarray(chunk)).to(dev)
+        rc_cnt = torch.zeros((Tc, BLOCK), dtype=torch.int32, device=dev)
+        with torch.cuda.device(dev):
+            check(L.cim_basis_count_tiles(d_lo.data_ptr(), d_occ.data_ptr(), n, npart, thr, d_cand.data_ptr(), Tc,
+                                          rc_cnt.data_ptr(), stream), "cim_basis_count_tiles")
+        nzc = (rc_cnt.sum(dim=1, dtype=torch.int32) > 0).cpu().numpy()
+        if Tc == T_cand and nzc.all():  # one chunk, nothing to drop: keep the buffers as they are
+            kept_rc.append(chunk)
+            kept_cnt.append(rc_cnt)
+        else:
+            idx = np.flatnonzero(nzc)
+            kept_rc.append(chunk[idx])
+            kept_cnt.append(rc_cnt[torch.from_numpy(idx).to(dev)])
+        del d_cand, rc_cnt
+    cand = np.concatenate(kept_rc) if kept_rc else np.zeros((0, 2), np.int32)
     T = cand.shape[0]
-    d_cand = torch.from_numpy(cand).to(dev)
-    rowcnt = torch.zeros((max(T, 1), BLOCK), dtype=torch.int32, device=dev)
-    with torch.cuda.device(dev):
-        check(L.cim_basis_count_tiles(d_lo.data_ptr(), d_occ.data_ptr(), n, npart, thr,
-                                      d_cand.data_ptr() if T else None, T, rowcnt.data_ptr(), stream),
-              "cim_basis_count_tiles")
-    rowcnt = rowcnt[:T]
-    counts = rowcnt.sum(dim=1).cpu().numpy()
+    rowcnt = torch.cat(kept_cnt) if kept_cnt else torch.zeros((0, BLOCK), dtype=torch.int32, device=dev)
+    counts = rowcnt.sum(dim=1, dtype=torch.int64).cpu().numpy()
     thr_fill = DEFAULT_DENSE_FILL if dense_fill is None else float(dense_fill)
     nz = counts > 0
     dense_sel = nz & (counts >= thr_fill * BLOCK * BLOCK)
@@ -254,5 +276,5 @@ def from_basis(basis_or_occ, bits_lo=None, *, rank: int = 2, value_seed: int = 0
         H.sparse = sp
         H._desc = None
     H.meta.update(kind="basis", rank=int(d), threshold=thr, value_seed=value_seed, n_particles=npart,
-                  candidate_tiles=int(T), stored_entries=int(counts.sum()), dense_fill=thr_fill)
+                  candidate_tiles=int(T_cand), stored_entries=int(counts.sum()), dense_fill=thr_fill)
     return H

@@ -1061,3 +1061,21 @@ def test_c_abi_rejects_bad_arguments(pkg, c1_small, layout):
     assert L.cim_sym_spmm(d, X.data_ptr(), Y.data_ptr(), k, k, k, 0, st) == 0
     tl = tiles.astype(np.float64)
     check_result(n, rc, tl, X[:n].cpu().numpy(), Y[:n].cpu().numpy(), torch.float32)
+
+
+def test_from_basis_chunked_count_identical(pkg, monkeypatch):
+    """The candidate tiles are counted in chunks (memory-bounded for bases
+    whose block-pair bound keeps most pairs): any chunk size gives the same
+    tiles, entry order and value bits."""
+    from paper_2110_10765_b200 import construct
+
+    f = load_fixture("skel_n1024.npz")
+    args = (f["basis_occ"], f["basis_bits_lo"])
+    kw = dict(rank=int(f["rank_threshold"]) // 2, value_seed=int(f["value_seed"]))
+    H1 = pkg.HalfTiles.from_basis(*args, **kw)
+    monkeypatch.setattr(construct, "COUNT_CHUNK_TILES", 7)
+    H2 = pkg.HalfTiles.from_basis(*args, **kw)
+    assert np.array_equal(H1.tile_rc_host, H2.tile_rc_host) and torch.equal(H1.vals, H2.vals)
+    a, b = H1.export_dense(), H2.export_dense()
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1].view(np.uint32), b[1].view(np.uint32))
+    assert H1.meta["candidate_tiles"] == H2.meta["candidate_tiles"]
