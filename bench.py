@@ -132,6 +132,16 @@ def box_copy_gbs(dev, nbytes: int = 1 << 31, reps: int = 5) -> float:
     return gbs
 
 
+def host_threads() -> int:
+    """Every host thread this process may run on.  Not omp_get_max_threads():
+    torchrun exports OMP_NUM_THREADS=1 to each rank, which would run the CPU
+    reference single-threaded at N > 1."""
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except (AttributeError, OSError):
+        return max(1, os.cpu_count() or 1)
+
+
 def measured_peaks():
     try:
         return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -246,7 +256,7 @@ def cpu_sample(n, nb, p, k, sample_tiles):
     rc = pkg.synthetic_pattern(nb, p, seed=0)
     rows_end = np.searchsorted(rc[:, 0], rc[min(sample_tiles, rc.shape[0]) - 1, 0], side="right")
     rc = rc[:rows_end]
-    tiles = cpu.fill_h(rc, n, 0)
+    tiles = cpu.fill_h(rc, n, 0, threads=host_threads())
     X = np.random.default_rng(0).standard_normal((nb * 64, k)).astype(np.float32)
     return cpu.F32Problem(rc, tiles, X), rc.shape[0]
 
@@ -272,7 +282,7 @@ def run_cpu(n, nb, p, k, budget_s, sample_tiles=24576, min_reps=3):
     from oracle import cpu
 
     prob, ntiles = cpu_sample(n, nb, p, k, sample_tiles)
-    threads = cpu.max_threads()
+    threads = host_threads()
     prob.run(threads)  # warmup (reference protocol: one warmup, bench.py:170-178)
     times = []
     t_start = time.perf_counter()
@@ -364,7 +374,7 @@ def scipy_csr_rate(n, nb, p, k, budget_s=3.0):
     from oracle import cpu
 
     rc = pkg.synthetic_pattern(nb, p, seed=0)[:2048]
-    tiles = cpu.fill_h(rc, n, 0)
+    tiles = cpu.fill_h(rc, n, 0, threads=host_threads())
     a = np.arange(64, dtype=np.int64)
     I = (rc[:, 0, None, None].astype(np.int64) * 64 + a[None, :, None]).repeat(64, 2)
     J = (rc[:, 1, None, None].astype(np.int64) * 64 + a[None, None, :]).repeat(64, 1)
@@ -401,7 +411,7 @@ def impl_reference(args):
     n, nb, n_off, p = workload(args, world)
     from oracle import cpu
 
-    threads = cpu.max_threads()
+    threads = host_threads()
     rc_all = __import__("paper_2110_10765_b200").synthetic_pattern(nb, p, seed=0)
     need = rc_all.shape[0] * 4096 * 4 + (threads + 3) * nb * 64 * args.k * 4
     full = mem_available_bytes() > need * 1.25 and args.k == K_DEFAULT
