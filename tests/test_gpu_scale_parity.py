@@ -346,7 +346,8 @@ def test_c2_full_size_256_rows(pkg):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("dtype,k", [(torch.float32, 16), (torch.float64, 8), (torch.float64, 16)])
+@pytest.mark.parametrize("dtype,k", [(torch.float32, 16), (torch.float64, 8), (torch.float64, 16),
+                                     (torch.float32, 64), (torch.float64, 64)])
 def test_c2_full_size_tensor_core_kernels(pkg, dtype, k):
     """C2 stored in the tensor-core layout: the split-TF32 tcgen05 kernel (f32)
     and the DMMA kernel (f64) at full size — 64 random block rows against the
