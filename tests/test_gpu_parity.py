@@ -7,6 +7,7 @@ Structure and values are bit-exact (integer/bitwise comparisons).
 """
 
 import json
+import os
 
 import numpy as np
 import pytest
@@ -1079,3 +1080,36 @@ def test_from_basis_chunked_count_identical(pkg, monkeypatch):
     a, b = H1.export_dense(), H2.export_dense()
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1].view(np.uint32), b[1].view(np.uint32))
     assert H1.meta["candidate_tiles"] == H2.meta["candidate_tiles"]
+
+
+RANDOM_CASES = int(os.environ.get("CIM_RANDOM_CASES", "60"))  # 600 passed once in 12 s (end of round 2)
+
+
+@pytest.mark.parametrize("case", range(RANDOM_CASES))
+def test_randomized_configurations(pkg, case):
+    """Seeded random configurations — n, tile density, dense/sparse mix and
+    entry fill, dtype, layout, k (incl. padded widths), work-unit size,
+    storage split, CSR on/off — each against the f64 oracle."""
+    rng = np.random.default_rng(1000 + case)
+    dtype = torch.float32 if rng.random() < 0.6 else torch.float64
+    layout = "tc" if rng.random() < 0.5 else "frag"
+    n = int(rng.integers(1, 1500))
+    nb = (n + 63) // 64
+    ks = [1, 2, 3, 4, 5, 8, 9, 12, 16, 20, 24, 32, 40, 48, 64]
+    k = int(rng.choice(ks))
+    p = float(rng.choice([0.0, 0.05, 0.2, 0.6, 1.0]))
+    fill = float(rng.choice([0.01, 0.05, 0.2, 0.5]))
+    sparse = rng.random() < 0.5
+    if sparse:
+        H = pkg.HalfTiles.synthetic_sparse(n, p, fill=fill, seed=case, fill_seed=case + 1, dtype=dtype)
+        if rng.random() < 0.5:
+            H.use_symmetric_csr(rng.random() < 0.5)
+        rc, tiles = H.export_dense()
+    else:
+        rc = pkg.synthetic_pattern(nb, p, seed=case)
+        H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=dtype, layout=layout,
+                                    max_unit=int(rng.choice([1, 3, 32])))
+        tiles = oracle.synthetic_dense_tiles(n, rc, seed=0)
+    X = torch.randn((n, k), generator=torch.Generator().manual_seed(case), dtype=dtype)
+    Y = pkg.sym_spmm(H, X.cuda()).cpu().numpy()
+    check_result(n, rc, np.asarray(tiles, np.float64), X.numpy(), Y, dtype)
