@@ -146,3 +146,34 @@ def test_lobpcg_gpu_f32_blocks_vs_eigsh(derived, m):
     assert res.converged
     got = np.sort(res.eigenvalues)
     assert np.abs(got - want).max() <= 2e-5 * np.abs(want).max(), (got, want, res.iterations)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", range(8))
+def test_lobpcg_gpu_randomized(case):
+    """Seeded random small problems on the GPU operator (dtype, layout, m,
+    largest / lowest, density) against numpy's eigvalsh of the assembled
+    matrix."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2110_10765_b200 as pkg
+    from paper_2110_10765_b200.lobpcg import lobpcg_sym
+
+    rng = np.random.default_rng(500 + case)
+    dtype = torch.float64 if rng.random() < 0.5 else torch.float32
+    layout = "tc" if rng.random() < 0.5 else "frag"
+    m = int(rng.integers(1, 11))
+    largest = bool(rng.random() < 0.3)
+    n = int(rng.integers(300, 1200))
+    rc = pkg.synthetic_pattern((n + 63) // 64, float(rng.choice([0.1, 0.3, 1.0])), seed=case)
+    H = pkg.HalfTiles.synthetic(n, tile_rc=rc, dtype=dtype, layout=layout)
+    tiles = oracle.synthetic_dense_tiles(n, rc, seed=0).astype(np.float64)
+    i, j, v = oracle.half_tiles_to_coo(n, rc, tiles)
+    A = np.zeros((n, n))
+    np.add.at(A, (i, j), v)
+    w = np.linalg.eigvalsh(A)
+    want = np.sort(w[-m:] if largest else w[:m])
+    res = lobpcg_sym(H, m, tol=1e-7, max_iter=3000, largest=largest, dtype=torch.float64)
+    got = np.sort(res.eigenvalues)
+    tol = (5e-5 if dtype == torch.float32 else 1e-8) * np.abs(w).max()
+    assert np.abs(got - want).max() <= tol, (dtype, layout, m, largest, n, got, want)
