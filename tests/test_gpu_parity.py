@@ -187,9 +187,8 @@ def test_contract_fused_vs_oracle(pkg, dtype, layout, n_vec, m_ops, op_kind):
     tol = oracle.contraction_tolerance(c, I.size)
     assert np.abs(got - want).max() <= tol
     from paper_2110_10765_b200.observables import contract_materialized
-    if dtype == torch.float32 or n_vec <= 16:  # the f64 sparse SpMM stops at k = 16
-        mat = contract_materialized(pattern, inp)
-        assert np.abs(got - mat).max() <= tol
+    mat = contract_materialized(pattern, inp)  # every width: sparse tiles too wide for the ring run as passes
+    assert np.abs(got - mat).max() <= tol
     # accumulate flag through the C ABI: a second walk doubles the result
     dev_c = torch.from_numpy(c).cuda().t().contiguous()
     acc = torch.zeros((n_vec, m_ops), dtype=torch.float64, device="cuda")
