@@ -183,7 +183,7 @@ def _free_port():
     return p
 
 
-def _sharded_worker(rank, world, port, kind, overlap, q):
+def _sharded_worker(rank, world, port, kind, overlap, q, n=3000):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -193,7 +193,7 @@ def _sharded_worker(rank, world, port, kind, overlap, q):
         import paper_2110_10765_b200 as pkg
 
         torch.cuda.set_device(0)
-        n, k = 3000, (16 if kind.startswith("synthetic_tc") or kind == "mixed_tc" else 8)
+        k = 16 if kind.startswith("synthetic_tc") or kind == "mixed_tc" else 8
         dt = torch.float64 if kind == "synthetic_tc64" else torch.float32
         if kind.startswith("synthetic"):
             S = pkg.ShardedSymSpmm.synthetic(n, k=k, p=0.2, seed=5, device="cuda:0", max_unit=4, overlap=overlap,
@@ -212,6 +212,15 @@ def _sharded_worker(rank, world, port, kind, overlap, q):
         q.put((rank, lo, Y, Y2, S.local_tiles()))
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,kind,overlap,n", [(3, "synthetic", True, 100), (3, "mixed", True, 130),
+                                                  (2, "synthetic_tc", False, 64 * 3 + 1), (3, "synthetic", False, 1)])
+def test_sharded_cuda_ranks_tiny_matrices(pkg, world, kind, overlap, n):
+    """Fewer block rows than ranks (some ranks own no rows / tiles), a one-row
+    matrix, a block row cut after one row: the partition, the exchanges and
+    the panel kernels stay exact."""
+    test_sharded_cuda_ranks_one_gpu(pkg, world, kind, overlap, n=n)
 
 
 def merge_dense_sparse(pkg, D, Sp):
@@ -244,7 +253,7 @@ def _global_reference(pkg, kind, n):
                                                 (3, "mixed", False), (2, "synthetic_tc", True), (3, "synthetic_tc", False),
                                                 (2, "synthetic_tc64", True), (3, "synthetic_tc64", False),
                                                 (2, "mixed_tc", True), (3, "mixed_tc", False)])
-def test_sharded_cuda_ranks_one_gpu(pkg, world, kind, overlap):
+def test_sharded_cuda_ranks_one_gpu(pkg, world, kind, overlap, n=3000):
     """Two or three processes, one GPU, the product's default CUDA panel
     kernels: the balanced partition (dense and mixed dense + sparse panels),
     the exchange (host-staged under gloo) and — with ``overlap`` — the
@@ -252,11 +261,11 @@ def test_sharded_cuda_ranks_one_gpu(pkg, world, kind, overlap):
     the f64 oracle of the global matrix."""
     import torch.multiprocessing as mp
 
-    n, k = 3000, (16 if kind.startswith("synthetic_tc") or kind == "mixed_tc" else 8)
+    k = 16 if kind.startswith("synthetic_tc") or kind == "mixed_tc" else 8
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_sharded_worker, args=(r, world, port, kind, overlap, q)) for r in range(world)]
+    procs = [ctx.Process(target=_sharded_worker, args=(r, world, port, kind, overlap, q, n)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
