@@ -1112,3 +1112,41 @@ def test_randomized_configurations(pkg, case):
     X = torch.randn((n, k), generator=torch.Generator().manual_seed(case), dtype=dtype)
     Y = pkg.sym_spmm(H, X.cuda()).cpu().numpy()
     check_result(n, rc, np.asarray(tiles, np.float64), X.numpy(), Y, dtype)
+
+
+@pytest.mark.parametrize("case", range(6))
+def test_from_basis_randomized_vs_bruteforce(pkg, case):
+    """Seeded random bases (orbital count, particle number, size, order,
+    rank): the device build's pair set equals the brute-force set of the
+    reference predicate (oracle.occ_diff ≤ 2·rank over all pairs) and every
+    stored value is h(i XOR j; seed) bit for bit."""
+    rng = np.random.default_rng(77 + case)
+    n_sp = int(rng.choice([16, 40, 64, 100, 128]))
+    npart = int(rng.integers(1, 6))
+    n_want = int(rng.integers(50, 400))
+    rank = int(rng.integers(1, 3))
+    occ = np.unique(np.sort(np.stack([rng.choice(n_sp, npart, replace=False) + 1 for _ in range(n_want)]), axis=1),
+                    axis=0).astype(np.uint16)
+    occ = occ[rng.permutation(occ.shape[0])]
+    if rng.random() < 0.5:  # grouped-like order by the low bits
+        lo0 = np.array([sum(1 << (o - 1) for o in row if o <= 64) for row in occ.tolist()], dtype=np.uint64)
+        occ = occ[np.argsort(lo0 & np.uint64(0xFF), kind="stable")]
+    n = occ.shape[0]
+    lo = np.array([sum(1 << (o - 1) for o in row if o <= 64) for row in occ.tolist()], dtype=np.uint64)
+    H = pkg.HalfTiles.from_basis(occ, lo, rank=rank, value_seed=case)
+    rc, tiles = H.export_dense()
+    i, j, v = oracle.half_tiles_to_coo(n, rc, tiles)
+    rows = occ.tolist()
+    bi, bj = [], []
+    for a in range(n):
+        for b in range(a, n):
+            if oracle.occ_diff(rows[a], rows[b]) <= 2 * rank:
+                bi.append(a)
+                bj.append(b)
+    bi, bj = np.array(bi), np.array(bj)
+    off = bi != bj
+    I = np.concatenate([bi, bj[off]])
+    J = np.concatenate([bj, bi[off]])
+    assert oracle.pair_set_digest(i, j) == oracle.pair_set_digest(I, J)
+    want = oracle.h_values(i, j, case)
+    assert np.array_equal(np.asarray(v, np.float32).view(np.uint32), np.asarray(want, np.float32).view(np.uint32))
