@@ -1150,3 +1150,45 @@ def test_from_basis_randomized_vs_bruteforce(pkg, case):
     assert oracle.pair_set_digest(i, j) == oracle.pair_set_digest(I, J)
     want = oracle.h_values(i, j, case)
     assert np.array_equal(np.asarray(v, np.float32).view(np.uint32), np.asarray(want, np.float32).view(np.uint32))
+
+
+@pytest.mark.parametrize("case", range(10))
+def test_contract_pattern_randomized(pkg, case):
+    """Seeded random stored patterns (n, tile density, per-tile fill, dense /
+    sparse split), vector and operator counts, operator kind, dtype and tile
+    layout: the fused contraction matches the f64 oracle within the
+    reference's tolerance, forward and transposed."""
+    rng = np.random.default_rng(300 + case)
+    dtype = torch.float64 if rng.random() < 0.4 else torch.float32
+    layout = "tc" if rng.random() < 0.5 else "frag"
+    n = int(rng.integers(10, 900))
+    nb = (n + 63) // 64
+    rc = pkg.synthetic_pattern(nb, float(rng.choice([0.1, 0.4, 1.0])), seed=case)
+    ii, jj = [], []
+    for R, C in rc:
+        m = rng.random((64, 64)) < float(rng.choice([0.02, 0.2, 0.95]))
+        if R == C:
+            m = m | m.T
+        a, b = np.nonzero(m)
+        ii.append(R * 64 + a)
+        jj.append(C * 64 + b)
+    i, j = np.concatenate(ii), np.concatenate(jj)
+    ok = (i < n) & (j < n)
+    key = np.unique(np.minimum(i[ok], j[ok]) * n + np.maximum(i[ok], j[ok]))
+    lo, hi = key // n, key % n
+    I = np.concatenate([lo, hi[lo != hi]])
+    J = np.concatenate([hi, lo[lo != hi]])
+    if I.size == 0:
+        I, J = np.array([0]), np.array([0])
+    pattern = pkg.HalfTiles.from_coo(n, I, J, np.ones(I.size), dtype=dtype, layout=layout)
+    n_vec, m_ops = int(rng.integers(1, 21)), int(rng.integers(1, 20))
+    op_kind = "identity" if rng.random() < 0.2 else "symmetric_hash"
+    c = pkg.random_coefficients(n_vec, n, seed=case, kind="gauss")
+    inp = pkg.ObservablesInput(c=c, m_ops=m_ops, op_kind=op_kind, seed=case + 5)
+    got = pkg.contract_pattern(pattern, inp).astype(np.float64)
+    want = oracle.contract_vmv(c, I, J, m_ops, {"symmetric_hash": 1, "identity": 0}[op_kind], case + 5)
+    tol = oracle.contraction_tolerance(c, I.size)
+    assert np.abs(got - want).max() <= tol
+    got_t = pkg.contract_pattern(pattern, pkg.ObservablesInput(c=c, m_ops=m_ops, op_kind=op_kind, seed=case + 5),
+                                 transpose=True)
+    assert np.abs(got_t - got).max() <= tol
