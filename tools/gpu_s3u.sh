@@ -1,5 +1,6 @@
 #!/bin/bash
 # tc kernel at k = 32: three A/B stages (ND = 2 accumulators, scalar Y reductions) vs two (ND = 4, bulk).
+# (A/B of a variant that was measured and reverted — see profiles/r02; the variant code is no longer in the tree)
 set -u
 O=gpurun_out/s3u; mkdir -p $O
 for rep in 1 2; do for v in base na3; do

@@ -1,5 +1,6 @@
 #!/bin/bash
 # DMMA kernel: paired column blocks with interleaved vectors (16-byte B loads, conflict-free) vs the previous build.
+# (A/B of a variant that was measured and reverted — see profiles/r02; the variant code is no longer in the tree)
 set -u
 O=gpurun_out/s3w; mkdir -p $O
 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_scale_parity.py -q -m gpu -k "float64 or f64" -x --timeout 300 > $O/pytest.txt 2>&1; echo "pytest exit $?" >> $O/pytest.txt

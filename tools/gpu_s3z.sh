@@ -1,5 +1,6 @@
 #!/bin/bash
 # Gram on DMMA (exact f64 products) vs the FFMA2 FAST kernel: parity, LOBPCG per-kernel times.
+# (A/B of a variant that was measured and reverted — see profiles/r02; the variant code is no longer in the tree)
 set -u
 O=gpurun_out/s3z; mkdir -p $O
 timeout 900 python -m pytest tests/test_lobpcg.py tests/test_gpu_parity.py -q -m gpu -k "lobpcg or gram or ritz or tsmm" -x --timeout 300 > $O/pytest.txt 2>&1; echo "pytest exit $?" >> $O/pytest.txt

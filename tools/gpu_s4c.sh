@@ -1,5 +1,6 @@
 #!/bin/bash
 # Staged sparse kernel: lane-dependent half order of the 32-byte X gathers vs the previous build.
+# (A/B of a variant that was measured and reverted — see profiles/r02; the variant code is no longer in the tree)
 set -u
 O=gpurun_out/s4c; mkdir -p $O
 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_scale_parity.py -q -m gpu -k "sparse or csr or basis or fill" -x --timeout 300 > $O/pytest.txt 2>&1; echo "pytest exit $?" >> $O/pytest.txt

@@ -1,5 +1,6 @@
 #!/bin/bash
 # DMMA permuted k-slots (PERM=1: k = 32; PERM=2: k = 16 and 32; PERM=0: off), parity and kernel ms.
+# (A/B of a variant that was measured and reverted — see profiles/r02; the variant code is no longer in the tree)
 set -u
 O=gpurun_out/s4h; mkdir -p $O
 for v in perm1 dperm2; do
