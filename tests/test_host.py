@@ -222,3 +222,33 @@ def test_integration_doc_struct_matches_header():
     block = block[:block.index("\n\n")]  # the class body ends at the first blank line
     names = re.findall(r'\("([a-z_]+)", ctypes\.', block)
     assert names == [f for f, _ in pkg._lib.CimHalfTiles._fields_]
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_plan_and_partition_randomized(case):
+    """Seeded random tile lists (size, density, unit cap, part count, incl.
+    more parts than block rows): units cover every tile once inside one block
+    row and respect the cap; partitions are monotone, cover every unit,
+    never split a block row across parts and stay balanced (native planner,
+    no GPU)."""
+    rng = np.random.default_rng(case)
+    nb = int(rng.integers(1, 3000))
+    p = float(rng.choice([0.0, 0.001, 0.01, 0.2, 1.0 if nb < 200 else 0.05]))
+    rc = pkg.synthetic_pattern(nb, p, seed=case)
+    mu = int(rng.choice([1, 2, 7, 32]))
+    u = pkg.plan_units(rc, nb, max_unit=mu)
+    assert u[0, 1] == 0 and u[-1, 2] == rc.shape[0]
+    assert np.all(u[1:, 1] == u[:-1, 2]) and np.all(u[:, 2] - u[:, 1] <= mu) and np.all(u[:, 2] > u[:, 1])
+    for R, t0, t1, _ in u[:: max(1, u.shape[0] // 200)]:
+        assert np.all(rc[t0:t1, 0] == R)
+    parts = int(rng.integers(1, 9))
+    b = pkg.partition_units(u, parts)
+    assert b[0] == 0 and b[-1] == u.shape[0] and np.all(np.diff(b) >= 0)
+    for q in range(1, parts):
+        if 0 < b[q] < u.shape[0]:
+            assert u[b[q], 0] != u[b[q] - 1, 0]
+    tiles = [int(u[b[q + 1] - 1, 2] - u[b[q], 1]) if b[q + 1] > b[q] else 0 for q in range(parts)]
+    assert sum(tiles) == rc.shape[0]
+    # balance: no part exceeds the ideal share by more than the largest block row (rows are indivisible)
+    row_tiles = np.bincount(rc[:, 0], minlength=nb).max()
+    assert max(tiles) <= rc.shape[0] / parts + row_tiles + 1
