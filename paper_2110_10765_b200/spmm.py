@@ -93,12 +93,13 @@ def sym_spmm(H: HalfTiles, X, out=None, *, layout: str = "auto", accumulate: boo
     X : torch.Tensor (CUDA or CPU) or numpy array, (n, k) or (k, n), dtype of H
     out : optional tensor/array of X's shape to write into (``accumulate``
         adds to it instead of overwriting)
-    layout : "auto" | "nk" | "kn"
+    layout : "auto" | "nk" | "kn" ("auto" reads the shape; a square X with
+        n = k > 1 is ambiguous and raises ValueError)
     stream : torch.cuda.Stream or raw cudaStream_t handle (default: current);
         staging, the kernel and the copy-back all run on it
     deterministic : no float atomics — bitwise reproducible Y (CIM_DETERMINISTIC;
-        fragment-layout dense and sparse tiles; a validation mode, ~2× the
-        traffic)
+        dense tiles in either layout and sparse tiles; a validation mode, ~2×
+        the traffic)
     """
     if not isinstance(H, HalfTiles):
         raise ValueError(f"H must be a HalfTiles, got {type(H).__name__}")
@@ -121,6 +122,8 @@ def sym_spmm(H: HalfTiles, X, out=None, *, layout: str = "auto", accumulate: boo
         raise ValueError(f"X dtype {Xt.dtype} does not match the matrix dtype {H.dtype}")
     n = H.n
     if layout == "auto":
+        if Xt.shape[0] == n and Xt.shape[1] == n and n > 1:
+            raise ValueError(f"X is {n} × {n}: (n, k) and (k, n) are indistinguishable; pass layout='nk' or 'kn'")
         if Xt.shape[0] == n:
             layout = "nk"
         elif Xt.shape[1] == n:

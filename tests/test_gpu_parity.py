@@ -316,7 +316,7 @@ def test_ragged_and_tiny(pkg, n, dtype, layout, k):
     H = pkg.HalfTiles.synthetic(n, tile_rc=rc, value_seed=5, layout=layout, dtype=dtype)
     X = torch.randn((n, k), generator=torch.Generator().manual_seed(n), dtype=dtype)
     check_result(n, rc, tiles.astype(np.float64) if dtype == torch.float64 else tiles, X.numpy(),
-                 pkg.sym_spmm(H, X.cuda()).cpu().numpy(), dtype)
+                 pkg.sym_spmm(H, X.cuda(), layout="nk").cpu().numpy(), dtype)
 
 
 @pytest.mark.parametrize("dtype,layout,k", [(torch.float32, "frag", 8), (torch.float32, "tc", 8),
@@ -1110,7 +1110,7 @@ def test_randomized_configurations(pkg, case):
                                     max_unit=int(rng.choice([1, 3, 32])))
         tiles = oracle.synthetic_dense_tiles(n, rc, seed=0)
     X = torch.randn((n, k), generator=torch.Generator().manual_seed(case), dtype=dtype)
-    Y = pkg.sym_spmm(H, X.cuda()).cpu().numpy()
+    Y = pkg.sym_spmm(H, X.cuda(), layout="nk").cpu().numpy()
     check_result(n, rc, np.asarray(tiles, np.float64), X.numpy(), Y, dtype)
 
 
@@ -1192,3 +1192,16 @@ def test_contract_pattern_randomized(pkg, case):
     got_t = pkg.contract_pattern(pattern, pkg.ObservablesInput(c=c, m_ops=m_ops, op_kind=op_kind, seed=case + 5),
                                  transpose=True)
     assert np.abs(got_t - got).max() <= tol
+
+
+def test_square_input_needs_an_explicit_layout(pkg):
+    """X of shape (n, n) reads the same as (n, k) and the reference's (k, n):
+    "auto" refuses it; an explicit layout applies it either way."""
+    n = 40
+    H = pkg.HalfTiles.synthetic(n, p=1.0, seed=1)
+    X = torch.randn((n, n), generator=torch.Generator().manual_seed(1))
+    with pytest.raises(ValueError, match="indistinguishable"):
+        pkg.sym_spmm(H, X.cuda())
+    Y_nk = pkg.sym_spmm(H, X.cuda(), layout="nk")
+    Y_kn = pkg.sym_spmm(H, X.t().contiguous().cuda(), layout="kn")
+    assert torch.allclose(Y_nk, Y_kn.t(), rtol=0, atol=1e-5 * Y_nk.abs().max().item())

@@ -57,7 +57,7 @@ def one(seed):
     det = bool(rng.random() < 0.15)
     kn = bool(rng.random() < 0.3)
     Xin = np.ascontiguousarray(X.numpy().T) if kn else X.cuda()
-    Y = pkg.sym_spmm(H, Xin, deterministic=det)
+    Y = pkg.sym_spmm(H, Xin, deterministic=det, layout="kn" if kn else "nk")
     Y = Y.T if kn else Y.cpu().numpy()
     Y_ref = oracle.sym_spmm(n, rcd, tiles.astype(np.float64), X.numpy().astype(np.float64))
     err = oracle.normwise_error(Y, Y_ref, max(oracle.frobenius_full(rcd, tiles.astype(np.float64)), 1e-300), X.numpy())
