@@ -1,7 +1,8 @@
 """Robustness sweep (not part of the suite): N seeded random configurations
 through the public API — dtype, layout, n, density, dense / sparse mix via
 from_coo, k (padded widths too), unit size, CSR forms, deterministic mode,
-accumulate, (k, n) input — each against the f64 oracle.  Prints a summary
+accumulate, (k, n) input, the host-buffer pipeline and the sharded
+operator at world 1 — each against the f64 oracle.  Prints a summary
 line; exits 1 on the first failure with its seed.
 
     python tools/fuzz_spmm.py [N] [first_seed]
@@ -64,9 +65,25 @@ def one(seed):
     gate = 1e-5 if dtype == torch.float32 else 1e-12
     if not err <= gate:
         raise AssertionError(f"seed {seed}: err {err:.3e} dtype={dtype} layout={layout} n={n} k={k} p={p} det={det} kn={kn}")
+    if not det and rng.random() < 0.25 and pkg.padded_k(dtype, k, layout) == k:  # host-buffer pipeline
+        Yb = pkg.sym_spmm_host_batch(H, [X.pin_memory(), X])
+        for yb in Yb:
+            e = oracle.normwise_error(yb.numpy(), Y_ref, max(oracle.frobenius_full(rcd, tiles.astype(np.float64)),
+                                                             1e-300), X.numpy())
+            if not e <= gate:
+                raise AssertionError(f"seed {seed}: host batch err {e:.3e}")
+    if not det and rng.random() < 0.25:  # the sharded operator at world 1 (rows padded to n_pad)
+        S = pkg.ShardedSymSpmm(n, k, dtype, torch.device("cuda"), H_local=H)
+        Xs = torch.zeros((S.rows_per_rank, k), dtype=dtype)
+        Xs[:n] = X
+        Ys = S.apply(Xs.cuda()).cpu().numpy()
+        e = oracle.normwise_error(Ys[:n], Y_ref, max(oracle.frobenius_full(rcd, tiles.astype(np.float64)), 1e-300),
+                                  X.numpy())
+        if not e <= gate or np.any(Ys[n:] != 0):
+            raise AssertionError(f"seed {seed}: sharded world-1 err {e:.3e}")
     if rng.random() < 0.2:  # accumulate on top
         out = torch.from_numpy(np.ascontiguousarray(Y)).to(dtype).cuda()
-        pkg.sym_spmm(H, X.cuda(), out=out, accumulate=True)
+        pkg.sym_spmm(H, X.cuda(), out=out, accumulate=True, layout="nk")
         err2 = np.abs(out.cpu().numpy() - 2 * Y_ref).max() / max(np.abs(Y_ref).max(), 1e-300)
         if not err2 <= 10 * gate * max(1, np.sqrt(k)):
             raise AssertionError(f"seed {seed}: accumulate err {err2:.3e}")
