@@ -1114,7 +1114,7 @@ def test_randomized_configurations(pkg, case):
     check_result(n, rc, np.asarray(tiles, np.float64), X.numpy(), Y, dtype)
 
 
-@pytest.mark.parametrize("case", range(6))
+@pytest.mark.parametrize("case", range(int(os.environ.get("CIM_BASIS_CASES", "6"))))
 def test_from_basis_randomized_vs_bruteforce(pkg, case):
     """Seeded random bases (orbital count, particle number, size, order,
     rank): the device build's pair set equals the brute-force set of the
@@ -1152,7 +1152,7 @@ def test_from_basis_randomized_vs_bruteforce(pkg, case):
     assert np.array_equal(np.asarray(v, np.float32).view(np.uint32), np.asarray(want, np.float32).view(np.uint32))
 
 
-@pytest.mark.parametrize("case", range(10))
+@pytest.mark.parametrize("case", range(int(os.environ.get("CIM_CONTRACT_CASES", "10"))))
 def test_contract_pattern_randomized(pkg, case):
     """Seeded random stored patterns (n, tile density, per-tile fill, dense /
     sparse split), vector and operator counts, operator kind, dtype and tile

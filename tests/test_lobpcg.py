@@ -149,7 +149,7 @@ def test_lobpcg_gpu_f32_blocks_vs_eigsh(derived, m):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", range(8))
+@pytest.mark.parametrize("case", range(int(os.environ.get("CIM_LOBPCG_CASES", "8"))))
 def test_lobpcg_gpu_randomized(case):
     """Seeded random small problems on the GPU operator (dtype, layout, m,
     largest / lowest, density) against numpy's eigvalsh of the assembled
