@@ -223,6 +223,19 @@ def test_sharded_cuda_ranks_tiny_matrices(pkg, world, kind, overlap, n):
     test_sharded_cuda_ranks_one_gpu(pkg, world, kind, overlap, n=n)
 
 
+@pytest.mark.parametrize("case", range(int(os.environ.get("CIM_SHARD_CASES", "4"))))
+def test_sharded_cuda_ranks_randomized(pkg, case):
+    """Seeded random sharded runs (2–4 ranks on one GPU): matrix kind (dense,
+    dense + sparse, tensor-core f32 / f64), serial or overlapped exchange, n
+    from one row to a few thousand."""
+    rng = np.random.default_rng(900 + case)
+    world = int(rng.integers(2, 5))
+    kind = str(rng.choice(["synthetic", "mixed", "synthetic_tc", "mixed_tc", "synthetic_tc64"]))
+    overlap = bool(rng.random() < 0.5)
+    n = int(rng.choice([1, 65, int(rng.integers(100, 4000))]))
+    test_sharded_cuda_ranks_one_gpu(pkg, world, kind, overlap, n=n)
+
+
 def merge_dense_sparse(pkg, D, Sp):
     """A matrix holding D's dense tiles and Sp's sparse tiles where the two
     patterns do not overlap (test helper)."""
