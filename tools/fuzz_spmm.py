@@ -5,7 +5,7 @@ accumulate, (k, n) input, the host-buffer pipeline and the sharded
 operator at world 1 — each against the f64 oracle.  Prints a summary
 line; exits 1 on the first failure with its seed.
 
-    python tools/fuzz_spmm.py [N] [first_seed]
+    python tools/fuzz_spmm.py [N] [first_seed] [max_n]
 """
 import os, sys, traceback
 import numpy as np
@@ -18,16 +18,17 @@ from oracle import oracle
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 500
 S0 = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+N_MAX = int(sys.argv[3]) if len(sys.argv) > 3 else 5000  # larger n: sparser patterns (the oracle is numpy)
 
 
 def one(seed):
     rng = np.random.default_rng(seed)
     dtype = torch.float32 if rng.random() < 0.6 else torch.float64
     layout = "tc" if rng.random() < 0.5 else "frag"
-    n = int(rng.integers(1, 5000))
+    n = int(rng.integers(1, N_MAX))
     nb = (n + 63) // 64
     k = int(rng.choice([1, 2, 3, 4, 5, 7, 8, 12, 16, 20, 24, 32, 40, 48, 56, 64]))
-    p = float(rng.choice([0.0, 0.02, 0.1, 0.4, 1.0]))
+    p = float(rng.choice([0.0, 0.02, 0.1, 0.4, 1.0] if n <= 5000 else [0.0, 0.002, 0.01]))
     rc = pkg.synthetic_pattern(nb, p, seed=seed)
     # per-tile fill → from_coo decides dense / sparse per tile
     ii, jj = [], []
