@@ -821,10 +821,31 @@ def write_reference_csv(path, line: dict, variant: str) -> None:
     Path(path).write_text("\n".join(lines) + "\n")
 
 
+def cuda_ready_or_reexec():
+    """A fresh box once refused cuInit for a single process ("CUDA driver
+    initialization failed"; the runs before and after were fine).  The
+    driver does not retry cuInit inside a process, so on that error the bench
+    re-executes itself (at most twice, a few seconds apart)."""
+    try:
+        torch.cuda.init()
+        return
+    except RuntimeError as ex:
+        if "driver initialization failed" not in str(ex):
+            raise
+        tries = int(os.environ.get("CIM_BENCH_CUDA_RETRY", "0"))
+        if tries >= 2:
+            raise
+        print(f"warning: {ex}; re-executing the bench ({tries + 1}/2)", file=sys.stderr)
+        time.sleep(3.0)
+        os.environ["CIM_BENCH_CUDA_RETRY"] = str(tries + 1)
+        os.execv(sys.executable, [sys.executable] + sys.argv)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return impl_reference(args)
+    cuda_ready_or_reexec()
     return impl_ours(args)
 
 
